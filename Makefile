@@ -1,0 +1,41 @@
+# Build of the B200-native GMRES-SDR library (sm_100a) and the CPU oracle.
+#   make            -> paper_2311_14206_b200/_lib/libsdr_b200.so + oracle/_build/liboracle.so
+PY ?= python
+NVCC ?= /usr/local/cuda/bin/nvcc
+CXX ?= g++
+LAPACK_DIR ?= $(shell $(PY) -c "import os,scipy;print(os.path.join(os.path.dirname(os.path.dirname(scipy.__file__)),'scipy.libs'))")
+LAPACK_LIB ?= $(notdir $(firstword $(wildcard $(LAPACK_DIR)/libscipy_openblas-*.so)))
+
+SRC := paper_2311_14206_b200/csrc
+OBJ := build/obj
+LIB := paper_2311_14206_b200/_lib/libsdr_b200.so
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -I/usr/local/cuda/include
+CXXFLAGS := -O3 -std=c++17 -fPIC -fvisibility=hidden -Wall -Wextra -Wno-unused-parameter -I/usr/local/cuda/include
+
+CU := spmv arnoldi sketch operator
+CC := context host_linalg solver capi
+OBJS := $(addprefix $(OBJ)/,$(addsuffix .cu.o,$(CU)) $(addsuffix .o,$(CC)))
+HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh) include/sdr_b200.h
+
+all: $(LIB) oracle
+
+$(OBJ)/%.cu.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -L$(LAPACK_DIR) -l:$(LAPACK_LIB) -Xlinker -rpath=$(LAPACK_DIR) -ldl -lpthread
+
+oracle:
+	$(MAKE) -s -C oracle PY=$(PY)
+
+clean:
+	rm -rf build $(LIB) oracle/_build
+
+.PHONY: all oracle clean

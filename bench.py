@@ -1,0 +1,332 @@
+"""GMRES-SDR benchmark (BASELINE.json metric: Arnoldi steps/s & time-to-solution,
+achieved HBM GB/s vs peak).
+
+One bench "step" = one complete GMRES-SDR solve of the workload (fresh recycle
+space each time) — every Arnoldi step, host least-squares, verification and
+harmonic recycle update inside the timed region. value = total Arnoldi steps
+of all ranks / max-over-ranks device time.
+
+Workloads (BASELINE.json configs, synthetic data per their generators):
+  c2 (default, N=1): 3D 7-point −Δu+β·∇u on 128³, β=(100,50,25), b=gaussian_vector(N,1),
+                     m=100 k=20 t=2 s=240 tol=1e-8, SRDCT seed 0x5eed.
+  With --gpus N>1 each rank owns a 128³ z-slab of a 128×128×(128·N) grid (weak scaling).
+  c5:               512³, β=(200,100,50), b seed 3, m=50 k=10 t=2 s=120 tol=1e-7, sparse sign ζ=8.
+
+--impl reference times the CPU oracle (the reference cannot be compiled here:
+Eigen/FFTW/LAPACKE absent — DESIGN.md §oracle) on the same workload: a bounded
+sample of init_krylov + Arnoldi steps per bench step, single-threaded like the reference.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {
+    "c2": dict(n=128, beta=(100.0, 50.0, 25.0), seed=1, m=100, k=20, t=2, s=240, tol=1e-8, sketch="srdct"),
+    "c5": dict(n=512, beta=(200.0, 100.0, 50.0), seed=3, m=50, k=10, t=2, s=120, tol=1e-7, sketch="sparse_sign"),
+}
+METRIC = "gmres_sdr_arnoldi_steps_per_s"
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def bytes_per_step(N, nnz, t):
+    """B_step = 12 nnz + 4 (N+1) + 8 N (4 + 2t) (+N/8 SRDCT sign bits)."""
+    return 12 * nnz + 4 * (N + 1) + 8 * N * (4 + 2 * t)
+
+
+def kernel_bytes(N, nnz, t, sketch):
+    """Algorithmic bytes per launch of each hot kernel."""
+    return {
+        "spmv_arnoldi": 12 * nnz + 4 * (N + 1) + 8 * N * (2 + (t - 1)),  # A, x, y write, t-1 window reads
+        "update": 8 * N * (1 + t) + 8 * N,                                # y + t window reads, w write
+        "sketch": 8 * N + (N // 8 if sketch == "srdct" else 0),          # one read of w (+ sign bits)
+    }
+
+
+def run_reference(args, wl, rank, world):
+    """CPU oracle on a bounded sample of the same workload (rank 0 only)."""
+    if rank != 0:
+        return None
+    from oracle import pyoracle as O
+    n = wl["n"]
+    N = n ** 3
+    t0 = time.time()
+    A = O.gen_convdiff3d(n, *wl["beta"])
+    b = O.gaussian_vector(N, wl["seed"])
+    S = (O.SketchOperator.subsampled_dct(N, wl["s"], 0x5EED) if wl["sketch"] == "srdct"
+         else O.SketchOperator.sparse_sign(N, wl["s"], 0x5EED, 8))
+    setup = time.time() - t0
+    steps_per_sample = int(os.environ.get("SDR_REF_STEPS", "8"))
+    for _ in range(args.warmup and 1):
+        O.run_arnoldi(A, b, S, wl["t"], 1, steps=1)
+    times = []
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        st = O.run_arnoldi(A, b, S, wl["t"], steps_per_sample, steps=steps_per_sample)
+        times.append(time.perf_counter() - t1)
+        assert st.j == steps_per_sample
+    total = sum(times)
+    value = steps_per_sample * args.steps / total
+    sample = (f"init_krylov + {steps_per_sample} arnoldi_step of workload {args.config} (N={N}) per bench step "
+              f"(oracle C++ restatement, 1 thread; reference unbuildable here)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "N": N, "nnz": A.nnz, "m": wl["m"], "k": wl["k"], "t": wl["t"],
+                   "s": wl["s"], "sketch": wl["sketch"]},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": setup,
+    }
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.config]
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        line = run_reference(args, wl, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    import paper_2311_14206_b200 as sk
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        idbuf = [sk.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idbuf, src=0)
+        ctx = sk.Context(local, rank, world, idbuf[0])
+    else:
+        dist = None
+        ctx = sk.Context(local)
+
+    n = wl["n"]
+    nz = n * world if args.config == "c2" else n
+    z0, z1 = (rank * n, (rank + 1) * n) if args.config == "c2" else (nz * rank // world, nz * (rank + 1) // world)
+    A = sk.SparseMatrix.convdiff3d_device(n, *wl["beta"], z_begin=z0, z_end=z1, ctx=ctx, ny=n, nz=nz)
+    N = A.rows
+    nloc = A.local_rows
+    # b = gaussian_vector(N, seed): every rank draws the same stream and keeps its block
+    b_full = sk.gaussian_vector(N, wl["seed"]) if world == 1 else sk.gaussian_vector(N, wl["seed"])[A.row_begin:A.row_begin + nloc]
+    b_host = torch.from_numpy(np.ascontiguousarray(b_full)).pin_memory()
+    b_dev = b_host.to(f"cuda:{local}")
+    S = (sk.SketchOperator.subsampled_dct(N, wl["s"], 0x5EED, ctx=ctx) if wl["sketch"] == "srdct"
+         else sk.SketchOperator.sparse_sign(N, wl["s"], 0x5EED, 8, ctx=ctx))
+    cfg = sk.SolverConfig(m=wl["m"], k=wl["k"], t=wl["t"], s=wl["s"], tol=wl["tol"])
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def one(b, host=False):
+        space = sk.RecycleSpace(ctx)
+        r = sk.solve(A, b, cfg, space=space, sketch=S)
+        return r
+
+    for _ in range(args.warmup):
+        r = one(b_dev)
+    # ---- timed region: device-resident input (value)
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    reports = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r = one(b_dev)
+            iters += r.report.iterations
+            reports.append(r.report)
+        ev1.record(stream)
+        ev1.synchronize()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launches - launches0
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms, float(iters)], dtype=torch.float64)
+        gathered = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        ms = max(float(g[0]) for g in gathered)
+    # Every rank takes the same (global) Arnoldi steps, each over its own 128³
+    # slab: whole-job throughput counts slab-steps, iterations x world / time.
+    value = (iters * world) / (ms / 1e3)
+
+    # ---- e2e through the public API with host buffers (H2D of b, D2H of x inside)
+    barrier()
+    t_e2e0 = time.perf_counter()
+    e2e_iters = 0
+    for _ in range(args.steps):
+        space = sk.RecycleSpace(ctx)
+        r = sk.solve(A, b_host.numpy(), cfg, space=space, sketch=S)
+        e2e_iters += r.report.iterations
+    ctx.synchronize()
+    e2e_s = time.perf_counter() - t_e2e0
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        e2e_s = max(float(g[0]) for g in gathered)
+    e2e_value = e2e_iters * world / e2e_s
+
+    # ---- per-kernel roofline from CUDA events on the library stream (one instrumented solve)
+    ctx.set_timing(True)
+    ctx.timing_reset()
+    rt = one(b_dev)
+    ctx.synchronize()
+    ktimes = {k: ctx.timing(k) for k in ("spmv_arnoldi", "update", "sketch", "tallskinny", "residual", "copy_norm",
+                                         "allreduce", "halo", "axpy")}
+    ctx.set_timing(False)
+    kb = kernel_bytes(nloc, A.nnz, wl["t"], wl["sketch"])
+    peak, peak_kind = measured_peak()
+    kern = {}
+    for name, (cnt, tot) in ktimes.items():
+        if cnt:
+            d = {"launches": cnt, "avg_us": 1e3 * tot / cnt, "share": 0.0}
+            if name in kb:
+                d["GBps"] = kb[name] / (tot / cnt * 1e-3) / 1e9
+                d["frac"] = d["GBps"] / peak
+            kern[name] = d
+    tot_all = sum(v["avg_us"] * v["launches"] for v in kern.values())
+    for v in kern.values():
+        v["share"] = v["avg_us"] * v["launches"] / tot_all if tot_all else 0.0
+    dom = max((k for k in kern if k in kb), key=lambda k: kern[k]["avg_us"] * kern[k]["launches"])
+    step_us = sum(kern[k]["avg_us"] for k in kb if k in kern)
+    step_bytes = bytes_per_step(nloc, A.nnz, wl["t"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as fh:
+            traffic = json.load(fh).get(dom)
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBps"], "peak": peak, "unit": "GB/s",
+                "frac": kern[dom]["GBps"] / peak, "traffic": traffic, "peak_source": peak_kind,
+                "bytes_per_launch": kb[dom],
+                "arnoldi_step": {"bytes": step_bytes, "us": step_us, "GBps": step_bytes / (step_us * 1e-6) / 1e9,
+                                 "frac": step_bytes / (step_us * 1e-6) / 1e9 / peak}}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        class A2:
+            steps = 2
+            warmup = 0
+            config = args.config
+        os.environ.setdefault("SDR_REF_STEPS", "8")
+        ref = run_reference(A2, wl, 0, 1)
+        cpu_baseline = dict(ref["cpu_baseline"])
+        cpu_baseline["value"] = ref["value"]
+
+    if rank == 0:
+        rep = reports[-1]
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE generators, seeded)",
+            "config": {"workload": args.config, "N": N, "N_per_gpu": nloc, "nnz": A.nnz, "m": wl["m"], "k": wl["k"],
+                       "t": wl["t"], "s": wl["s"], "tol": wl["tol"], "sketch": wl["sketch"],
+                       "parallelism": f"zslab{world}", "l2": "inputs > L2 per solve (V basis 1.7 GB)"},
+            "time_to_solution_ms": ms / args.steps,
+            "solve": {"status": rep.status, "iterations": rep.iterations, "cycles": rep.cycles,
+                      "final_relative_residual": rep.final_relative_residual},
+            "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * nloc, "d2h_bytes_per_step": 8 * nloc},
+            "roofline": roofline,
+            "kernels": kern,
+            "cpu_baseline": cpu_baseline,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

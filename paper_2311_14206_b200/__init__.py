@@ -1,0 +1,723 @@
+"""B200-native GMRES-SDR (sketched GMRES with truncated Arnoldi, deflated
+restarting and Krylov-subspace recycling) — Python mirror of the reference
+``skrylov`` C++ interface over the C-ABI in ``include/sdr_b200.h``.
+
+Names, argument meaning and error behaviour follow the reference:
+
+=============================  =========================================
+reference (proj/include/...)   here
+=============================  =========================================
+SparseMatrix / OperatorRef     :class:`SparseMatrix` (device SELL-32)
+SketchOperator                 :class:`SketchOperator`
+SolverConfig                   :class:`SolverConfig`
+RecycleSpace                   :class:`RecycleSpace` (U in HBM)
+solve(A, b, cfg, space, ...)   :func:`solve`
+solve_sequence(seq, cfg, ...)  :func:`solve_sequence`
+IncrementalQR                  :class:`IncrementalQR` (host)
+harmonic_pairs                 :func:`harmonic_pairs`
+gaussian_vector, gen_convdiff  :func:`gaussian_vector`, :func:`gen_convdiff`
+=============================  =========================================
+
+``std::invalid_argument`` surfaces as ``ValueError``, ``std::domain_error``
+as ``ArithmeticError``, ``std::logic_error``/``std::runtime_error`` as
+``RuntimeError``. Every compute call runs the sm_100a kernels in
+``_lib/libsdr_b200.so``; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import sdr_config, sdr_callbacks, ITER_CB, RES_CB
+
+__all__ = [
+    "Context", "default_context", "SparseMatrix", "SketchOperator", "SolverConfig", "RecycleSpace", "SolveReport",
+    "SolveResult", "SequenceResult", "ProblemInstance", "solve", "solve_sequence", "IncrementalQR", "harmonic_pairs",
+    "gaussian_vector", "gen_convdiff", "gen_convdiff2d", "gen_convdiff3d", "sparse_sign_entries", "partition_halo",
+    "partition_rows", "SdrError", "CudaError",
+]
+
+_lib = _capi.load()
+
+STATUS = {0: "converged", 1: "max_restarts", 2: "breakdown", 3: "diverged"}
+VARIANT = {"reuse": 0, "exact": 1, "inexact": 2}
+PROVENANCE = {0: "empty", 1: "fresh", 2: "reused", 3: "exact-resketch", 4: "inexact-carryover"}
+PROVENANCE_ID = {v: k for k, v in PROVENANCE.items()}
+
+
+class SdrError(RuntimeError):
+    pass
+
+
+class CudaError(SdrError):
+    pass
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = _lib.sdr_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise ArithmeticError(msg)
+    if rc in (5, 6, 7):
+        raise CudaError(msg)
+    raise SdrError(msg)
+
+
+def _is_torch_cuda(a):
+    return type(a).__module__.startswith("torch") and getattr(a, "is_cuda", False)
+
+
+def _ptr(a, dtype=np.float64):
+    """(keepalive, pointer, length) for a numpy array or a CUDA torch tensor."""
+    if a is None:
+        return None, None, 0
+    if _is_torch_cuda(a):
+        import torch
+        t = a.contiguous()
+        if t.dtype != torch.float64:
+            raise ValueError("device vectors must be float64")
+        return t, C.c_void_p(t.data_ptr()), t.numel()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr, arr.ctypes.data_as(C.c_void_p), arr.size
+
+
+class Context:
+    """One GPU, one CUDA stream, optional NCCL rank (sdr_ctx)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        h = C.c_void_p()
+        if world > 1:
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+            _check(_lib.sdr_ctx_create_dist(device, rank, world, buf, C.byref(h)))
+        else:
+            _check(_lib.sdr_ctx_create(device, C.byref(h)))
+        self._h = h
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib.sdr_nccl_unique_id(buf))
+        return buf.raw
+
+    @property
+    def num_sms(self):
+        n = C.c_int()
+        _check(_lib.sdr_ctx_info(self._h, None, None, None, C.byref(n)))
+        return n.value
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(_lib.sdr_ctx_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        _check(_lib.sdr_ctx_synchronize(self._h))
+
+    def set_timing(self, on: bool):
+        _check(_lib.sdr_ctx_set_timing(self._h, int(on)))
+
+    def timing_reset(self):
+        _check(_lib.sdr_ctx_timing_reset(self._h))
+
+    def timing(self, kernel: str):
+        n = C.c_int64()
+        ms = C.c_double()
+        _check(_lib.sdr_ctx_timing_get(self._h, kernel.encode(), C.byref(n), C.byref(ms)))
+        return n.value, ms.value
+
+    @property
+    def launches(self) -> int:
+        n = C.c_int64()
+        _check(_lib.sdr_ctx_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.sdr_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("SDR_DEVICE") is None
+                               else int(os.environ["SDR_DEVICE"]))
+    return _default_ctx
+
+
+# --------------------------------------------------------------------- operator
+
+class SparseMatrix:
+    """CSR operator resident on the device (sparse.hpp:27-150 + OperatorRef).
+
+    ``SparseMatrix(rows, cols, offsets, columns, values)`` validates exactly as
+    the reference constructor and raises ``ValueError`` with its message.
+    """
+
+    def __init__(self, rows, cols, offsets, columns, values, ctx: Context | None = None, *, row_begin=None,
+                 local_rows=None, _handle=None):
+        self.ctx = ctx or default_context()
+        if _handle is not None:
+            self._h = _handle
+        else:
+            o, po, _ = _ptr(np.asarray(offsets, dtype=np.int64), np.int64)
+            c_, pc, _ = _ptr(np.asarray(columns, dtype=np.int64), np.int64)
+            v, pv, _ = _ptr(np.asarray(values, dtype=np.float64))
+            h = C.c_void_p()
+            if row_begin is None:
+                _check(_lib.sdr_csr_create(self.ctx._h, rows, cols, po, pc, pv, C.byref(h)))
+            else:
+                _check(_lib.sdr_csr_create_local(self.ctx._h, rows, cols, row_begin, local_rows, po, pc, pv,
+                                                 C.byref(h)))
+            self._h = h
+        vals = [C.c_int64() for _ in range(7)]
+        _check(_lib.sdr_csr_info(self._h, *[C.byref(x) for x in vals]))
+        (self.rows, self.cols, self.nnz, self.row_begin, self.local_rows, self.halo_lo,
+         self.halo_hi) = (x.value for x in vals)
+
+    @classmethod
+    def from_triplets(cls, rows, cols, r, c, v, ctx=None):
+        """Duplicates summed, exact zeros dropped (sparse.hpp:40-73)."""
+        r = np.asarray(r, dtype=np.int64)
+        c = np.asarray(c, dtype=np.int64)
+        v = np.asarray(v, dtype=np.float64)
+        bad = (r < 0) | (r >= rows) | (c < 0) | (c >= cols)
+        if bad.any():
+            i = int(np.argmax(bad))
+            raise ValueError(f"SparseMatrix::from_triplets: entry ({r[i]}, {c[i]}) outside {rows}x{cols}")
+        order = np.lexsort((c, r))
+        r, c, v = r[order], c[order], v[order]
+        key = r * max(cols, 1) + c
+        uniq, start = np.unique(key, return_index=True)
+        sums = np.add.reduceat(v, start) if len(v) else v
+        keep = sums != 0.0
+        rr, cc, vv = r[start][keep], c[start][keep], sums[keep]
+        offsets = np.zeros(rows + 1, dtype=np.int64)
+        np.add.at(offsets, rr + 1, 1)
+        return cls(rows, cols, np.cumsum(offsets), cc, vv, ctx)
+
+    @classmethod
+    def from_dense(cls, A, ctx=None):
+        A = np.asarray(A, dtype=np.float64)
+        r, c = np.nonzero(A)
+        return cls.from_triplets(A.shape[0], A.shape[1], r, c, A[r, c], ctx)
+
+    @classmethod
+    def from_scipy(cls, M, ctx=None):
+        M = M.tocsr()
+        M.sort_indices()
+        return cls(M.shape[0], M.shape[1], M.indptr.astype(np.int64), M.indices.astype(np.int64),
+                   M.data.astype(np.float64), ctx)
+
+    @classmethod
+    def convdiff3d_device(cls, n, bx, by, bz, z_begin=0, z_end=None, ctx=None, ny=None, nz=None):
+        """7-point −Δ + β·∇ on an n×ny×nz grid built directly in HBM (no host
+        CSR; C5 scale). ny, nz default to n; each rank passes its z-slab."""
+        ctx = ctx or default_context()
+        ny = n if ny is None else ny
+        nz = n if nz is None else nz
+        h = C.c_void_p()
+        _check(_lib.sdr_csr_create_convdiff3d(ctx._h, n, ny, nz, bx, by, bz, z_begin, nz if z_end is None else z_end,
+                                              C.byref(h)))
+        return cls(0, 0, None, None, None, ctx, _handle=h)
+
+    def apply(self, x):
+        """y = A x (OperatorRef::apply); numpy in -> numpy out, CUDA tensor -> CUDA tensor."""
+        keep, px, n = _ptr(x)
+        if _is_torch_cuda(x):
+            import torch
+            y = torch.empty(self.local_rows, dtype=torch.float64, device=x.device)
+            py = C.c_void_p(y.data_ptr())
+        else:
+            y = np.empty(self.local_rows)
+            py = y.ctypes.data_as(C.c_void_p)
+        _check(_lib.sdr_spmv(self.ctx._h, self._h, px, n, py))
+        return y
+
+    __matmul__ = apply
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sdr_csr_destroy(self._h)
+            self._h = None
+
+
+# ----------------------------------------------------------------------- sketch
+
+class SketchOperator:
+    """Randomized embedding S (sketch.hpp:93-193): subsampled DCT, identity,
+    or the new sparse-sign map."""
+
+    def __init__(self, handle, ctx):
+        self._h = handle
+        self.ctx = ctx
+        kind = C.c_int()
+        n = C.c_int64()
+        s = C.c_int64()
+        seed = C.c_uint64()
+        zeta = C.c_int64()
+        _check(_lib.sdr_sketch_info(handle, C.byref(kind), C.byref(n), C.byref(s), C.byref(seed), C.byref(zeta)))
+        self.kind = {0: "subsampled_dct", 1: "identity", 2: "sparse_sign"}[kind.value]
+        self.input_dim, self.sketch_dim, self.seed, self.zeta = n.value, s.value, seed.value, zeta.value
+
+    @classmethod
+    def subsampled_dct(cls, n, s, seed, ctx=None):
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(_lib.sdr_sketch_create_srdct(ctx._h, n, s, seed, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def identity(cls, n, ctx=None):
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(_lib.sdr_sketch_create_identity(ctx._h, n, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def sparse_sign(cls, n, s, seed, zeta=8, ctx=None):
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(_lib.sdr_sketch_create_sparse_sign(ctx._h, n, s, seed, zeta, C.byref(h)))
+        return cls(h, ctx)
+
+    def rows(self):
+        out = np.empty(self.sketch_dim, dtype=np.int64)
+        _check(_lib.sdr_sketch_rows(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def signs(self):
+        out = np.empty(self.input_dim)
+        _check(_lib.sdr_sketch_signs(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def apply(self, x):
+        keep, px, n = _ptr(x)
+        out = np.empty(self.sketch_dim)
+        _check(_lib.sdr_sketch_apply(self.ctx._h, self._h, px, n, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def dense(self):
+        n = self.input_dim
+        D = np.empty((self.sketch_dim, n))
+        e = np.zeros(n)
+        for j in range(n):
+            e[j] = 1.0
+            D[:, j] = self.apply(e)
+            e[j] = 0.0
+        return D
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sdr_sketch_destroy(self._h)
+            self._h = None
+
+
+# ----------------------------------------------------------------- host pieces
+
+def gaussian_vector(n, seed):
+    """rng.hpp:87-96, bit-identical (std::mt19937_64 + Box–Muller)."""
+    out = np.empty(n)
+    _check(_lib.sdr_gaussian_vector(n, seed, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def sparse_sign_entries(s, seed, zeta, j0, count):
+    rows = np.empty(count * zeta, dtype=np.int64)
+    signs = np.empty(count * zeta)
+    _check(_lib.sdr_sparse_sign_entries(s, seed, zeta, j0, count, rows.ctypes.data_as(C.c_void_p),
+                                        signs.ctypes.data_as(C.c_void_p)))
+    return rows.reshape(count, zeta), signs.reshape(count, zeta)
+
+
+def _gen_csr(fn, *args):
+    nnz = C.c_int64()
+    _check(fn(*args, C.byref(nnz), None, None, None))
+    return nnz.value
+
+
+def gen_convdiff2d(n, bx, by, shift=0.0, diag_rel=None):
+    """(offsets, columns, values) of −Δu + β·∇u on an n×n grid; equals
+    −gen_convdiff(n, −β) for bx == by (problems.hpp:70-88)."""
+    keep, pd, _ = _ptr(diag_rel)
+    nnz = _gen_csr(_lib.sdr_gen_convdiff2d, n, bx, by, shift, pd)
+    off = np.empty(n * n + 1, dtype=np.int64)
+    col = np.empty(nnz, dtype=np.int64)
+    val = np.empty(nnz)
+    _check(_lib.sdr_gen_convdiff2d(n, bx, by, shift, pd, None, off.ctypes.data_as(C.c_void_p),
+                                   col.ctypes.data_as(C.c_void_p), val.ctypes.data_as(C.c_void_p)))
+    return off, col, val
+
+
+def gen_convdiff(n, alpha):
+    """Reference gen_convdiff(n, alpha) (problems.hpp:70-88) = −convdiff2d(n, −alpha, −alpha)."""
+    off, col, val = gen_convdiff2d(n, -alpha, -alpha)
+    return off, col, -val
+
+
+def gen_convdiff3d(n, bx, by, bz, z_begin=0, z_end=None):
+    z_end = n if z_end is None else z_end
+    nnz = _gen_csr(_lib.sdr_gen_convdiff3d, n, bx, by, bz, z_begin, z_end)
+    off = np.empty((z_end - z_begin) * n * n + 1, dtype=np.int64)
+    col = np.empty(nnz, dtype=np.int64)
+    val = np.empty(nnz)
+    _check(_lib.sdr_gen_convdiff3d(n, bx, by, bz, z_begin, z_end, None, off.ctypes.data_as(C.c_void_p),
+                                   col.ctypes.data_as(C.c_void_p), val.ctypes.data_as(C.c_void_p)))
+    return off, col, val
+
+
+def partition_rows(rows, world, granule=1):
+    rb = np.empty(world, dtype=np.int64)
+    re = np.empty(world, dtype=np.int64)
+    _check(_lib.sdr_partition_rows(rows, world, granule, rb.ctypes.data_as(C.c_void_p), re.ctypes.data_as(C.c_void_p)))
+    return rb, re
+
+
+def partition_halo(rank, row_begin, row_end, min_col, max_col):
+    world = len(row_begin)
+    arrs = [np.ascontiguousarray(a, dtype=np.int64) for a in (row_begin, row_end, min_col, max_col)]
+    outs = [np.zeros(world, dtype=np.int64) for _ in range(4)]
+    _check(_lib.sdr_partition_halo(world, rank, *[a.ctypes.data_as(C.c_void_p) for a in arrs],
+                                   *[o.ctypes.data_as(C.c_void_p) for o in outs]))
+    return dict(recv_lo=outs[0], recv_cnt=outs[1], send_lo=outs[2], send_cnt=outs[3])
+
+
+class IncrementalQR:
+    """incremental_qr.hpp:26-162 (host, BLAS-2 through OpenBLAS)."""
+
+    def __init__(self, rows, capacity, rank_tol=1e-12):
+        h = C.c_void_p()
+        _check(_lib.sdr_qr_create(rows, capacity, rank_tol, C.byref(h)))
+        self._h = h
+        self.rows = rows
+
+    @property
+    def cols(self):
+        n = C.c_int64()
+        _check(_lib.sdr_qr_cols(self._h, C.byref(n)))
+        return n.value
+
+    def append(self, col):
+        keep, p, n = _ptr(col)
+        c = C.c_int64()
+        rd = C.c_int()
+        _check(_lib.sdr_qr_append(self._h, p, n, C.byref(c), C.byref(rd)))
+        return c.value, bool(rd.value)
+
+    def exclude(self, column):
+        _check(_lib.sdr_qr_exclude(self._h, column))
+
+    def solve(self, rhs):
+        keep, p, n = _ptr(rhs)
+        y = np.empty(self.cols)
+        res = C.c_double()
+        _check(_lib.sdr_qr_solve(self._h, p, n, y.ctypes.data_as(C.c_void_p), C.byref(res)))
+        return y, res.value
+
+    def factors(self):
+        p = self.cols
+        Q = np.empty(self.rows * p)
+        R = np.empty(p * p)
+        _check(_lib.sdr_qr_factors(self._h, Q.ctypes.data_as(C.c_void_p), R.ctypes.data_as(C.c_void_p)))
+        return Q.reshape(p, self.rows).T, R.reshape(p, p).T
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sdr_qr_destroy(self._h)
+            self._h = None
+
+
+def harmonic_pairs(SAW, SW, k, rank_tol=1e-12):
+    """truncated_svd + fill_pencil + harmonic_pairs (recycle.hpp:98-218)."""
+    SAW = np.asfortranarray(SAW, dtype=np.float64)
+    SW = np.asfortranarray(SW, dtype=np.float64)
+    s, p = SAW.shape
+    rank, keff = C.c_int64(), C.c_int64()
+    pe, rl = C.c_int(), C.c_int()
+    kk = max(k, 0) + 2
+    coeffs = np.zeros(p * kk)
+    mre, mim = np.zeros(kk), np.zeros(kk)
+    _check(_lib.sdr_harmonic(SAW.ctypes.data_as(C.c_void_p), SW.ctypes.data_as(C.c_void_p), s, p, k, rank_tol,
+                             C.byref(rank), C.byref(keff), C.byref(pe), C.byref(rl),
+                             coeffs.ctypes.data_as(C.c_void_p), mre.ctypes.data_as(C.c_void_p),
+                             mim.ctypes.data_as(C.c_void_p)))
+    ke = keff.value
+    return dict(rank=rank.value, k_effective=ke, k_requested=k, pair_extended=bool(pe.value),
+                rank_limited=bool(rl.value), coeffs=coeffs[: p * ke].reshape(ke, p).T.copy(),
+                mu=mre[:ke] + 1j * mim[:ke])
+
+
+# ----------------------------------------------------------------------- solver
+
+@dataclass
+class SolverConfig:
+    """solver.hpp:48-79 (same defaults)."""
+    m: int = 100
+    t: int = 2
+    k: int = 20
+    s: int = 0
+    tol: float = 1e-6
+    safety_init: float = 1.4
+    max_restarts: int = 10
+    variant: str = "reuse"
+    sketch_seed: int = 0x5EED
+    rank_tol: float = 1e-12
+    breakdown_tol: float = 1e-14
+
+    def c(self):
+        return sdr_config(self.m, self.t, self.k, self.s, self.tol, self.safety_init, self.max_restarts,
+                          VARIANT[self.variant], self.sketch_seed, self.rank_tol, self.breakdown_tol)
+
+    def validate(self):
+        c = self.c()
+        _check(_lib.sdr_config_validate(C.byref(c)))
+
+
+class RecycleSpace:
+    """recycle.hpp:31-72: U (n x k) in HBM, SU / SAU (s x k) on the host."""
+
+    def __init__(self, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(_lib.sdr_recycle_create(self.ctx._h, C.byref(h)))
+        self._h = h
+
+    def _info(self):
+        rows, s, dim = C.c_int64(), C.c_int64(), C.c_int64()
+        prov = C.c_int()
+        _check(_lib.sdr_recycle_info(self._h, C.byref(rows), C.byref(s), C.byref(dim), C.byref(prov)))
+        return rows.value, s.value, dim.value, prov.value
+
+    def dim(self):
+        return self._info()[2]
+
+    def empty(self):
+        return self.dim() == 0
+
+    @property
+    def provenance(self):
+        return PROVENANCE[self._info()[3]]
+
+    def get(self):
+        rows, s, dim, _ = self._info()
+        U = np.empty(rows * dim)
+        SU = np.empty(s * dim)
+        SAU = np.empty(s * dim)
+        _check(_lib.sdr_recycle_get(self.ctx._h, self._h, U.ctypes.data_as(C.c_void_p), SU.ctypes.data_as(C.c_void_p),
+                                    SAU.ctypes.data_as(C.c_void_p)))
+        return U.reshape(dim, rows).T, SU.reshape(dim, s).T, SAU.reshape(dim, s).T
+
+    @property
+    def U(self):
+        return self.get()[0]
+
+    @property
+    def SU(self):
+        return self.get()[1]
+
+    @property
+    def SAU(self):
+        return self.get()[2]
+
+    def set(self, U, SU, SAU, provenance="fresh"):
+        U, SU, SAU = (np.asfortranarray(a, dtype=np.float64) for a in (U, SU, SAU))
+        _check(_lib.sdr_recycle_set(self.ctx._h, self._h, U.shape[0], SU.shape[0], U.shape[1],
+                                    U.ctypes.data_as(C.c_void_p), SU.ctypes.data_as(C.c_void_p),
+                                    SAU.ctypes.data_as(C.c_void_p), PROVENANCE_ID[provenance]))
+
+    def drop_columns(self, cols):
+        a = np.ascontiguousarray(cols, dtype=np.int64)
+        _check(_lib.sdr_recycle_drop_columns(self._h, a.ctypes.data_as(C.c_void_p), len(a)))
+
+    def refresh(self, A: SparseMatrix, S: SketchOperator, mode="exact"):
+        """refresh_for_new_matrix (recycle.hpp:297-318); returns the counters spent."""
+        cnt = np.zeros(3, dtype=np.int64)
+        _check(_lib.sdr_recycle_refresh(self.ctx._h, self._h, A._h, S._h, 0 if mode == "exact" else 1,
+                                        cnt.ctypes.data_as(C.c_void_p)))
+        return dict(matvecs=int(cnt[0]), inner_products=int(cnt[1]), sketch_applies=int(cnt[2]))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sdr_recycle_destroy(self._h)
+            self._h = None
+
+
+@dataclass
+class SolveReport:
+    """report.hpp:50-63."""
+    status: str = "max_restarts"
+    iterations: int = 0
+    cycles: int = 0
+    rhs_norm: float = 0.0
+    final_relative_residual: float = float("nan")
+    counters: dict = field(default_factory=dict)
+    sketched_residuals: list = field(default_factory=list)
+    true_residuals: list = field(default_factory=list)
+    cycle_stats: list = field(default_factory=list)
+    notes: list = field(default_factory=list)
+    error: str = ""
+    seconds: float = 0.0
+    device_ms: float = 0.0
+    host_wait_ms: float = 0.0
+
+
+def _report(h) -> SolveReport:
+    st, cy = C.c_int(), C.c_int32()
+    it = C.c_int64()
+    rhs, frr, sec = C.c_double(), C.c_double(), C.c_double()
+    _check(_lib.sdr_report_summary(h, C.byref(st), C.byref(it), C.byref(cy), C.byref(rhs), C.byref(frr),
+                                   C.byref(sec)))
+    mv, ip, sk = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(_lib.sdr_report_counters(h, C.byref(mv), C.byref(ip), C.byref(sk)))
+    samples = []
+    for w in (0, 1):
+        n = C.c_int64()
+        _check(_lib.sdr_report_samples(h, w, C.byref(n), None, None))
+        its = np.empty(n.value, dtype=np.int64)
+        vals = np.empty(n.value)
+        _check(_lib.sdr_report_samples(h, w, C.byref(n), its.ctypes.data_as(C.c_void_p),
+                                       vals.ctypes.data_as(C.c_void_p)))
+        samples.append(list(zip(its.tolist(), vals.tolist())))
+    n = C.c_int64()
+    _check(_lib.sdr_report_cycles(h, C.byref(n), None))
+    buf = np.empty(8 * max(n.value, 1))
+    _check(_lib.sdr_report_cycles(h, C.byref(n), buf.ctypes.data_as(C.c_void_p)))
+    cs = [dict(steps=int(buf[8 * i]), entry_residual=buf[8 * i + 1], sketched_entry=buf[8 * i + 2],
+               exit_sres=buf[8 * i + 3], exit_residual=buf[8 * i + 4], safety_after=buf[8 * i + 5],
+               basis_cond=buf[8 * i + 6], deflation_rank=int(buf[8 * i + 7])) for i in range(n.value)]
+    nn = C.c_int64()
+    _check(_lib.sdr_report_notes(h, C.byref(nn)))
+    notes = [_lib.sdr_report_note(h, i).decode() for i in range(nn.value)]
+    dev, wait, tot = C.c_double(), C.c_double(), C.c_double()
+    _check(_lib.sdr_report_timing(h, C.byref(dev), C.byref(wait), C.byref(tot)))
+    rep = SolveReport(STATUS[st.value], it.value, cy.value, rhs.value, frr.value,
+                      dict(matvecs=mv.value, inner_products=ip.value, sketch_applies=sk.value), samples[0],
+                      samples[1], cs, notes, (_lib.sdr_report_error(h) or b"").decode(), sec.value, dev.value,
+                      wait.value)
+    _lib.sdr_report_destroy(h)
+    return rep
+
+
+@dataclass
+class SolveResult:
+    x: object
+    report: SolveReport
+    space: RecycleSpace
+
+
+def _make_callbacks(callbacks):
+    if not callbacks:
+        return None, None
+    on_it = callbacks.get("on_iteration")
+    on_res = callbacks.get("on_residual_check")
+
+    def it_cb(ev, user):
+        e = ev.contents
+        y = np.ctypeslib.as_array(e.y, shape=(e.y_len,)).copy() if e.y_len else np.empty(0)
+        on_it(dict(cycle=e.cycle, step=e.step, iteration=e.iteration, sres=e.sres,
+                   new_basis_sketch_norm=e.new_basis_sketch_norm, y=y, space_dim=e.space_dim))
+
+    def res_cb(ev, user):
+        e = ev.contents
+        on_res(dict(cycle=e.cycle, iteration=e.iteration, sres=e.sres, true_residual=e.true_residual))
+
+    fi = ITER_CB(it_cb) if on_it else ITER_CB()
+    fr = RES_CB(res_cb) if on_res else RES_CB()
+    cb = sdr_callbacks(fi, fr, None)
+    return cb, (fi, fr)
+
+
+def solve(A: SparseMatrix, b, cfg: SolverConfig, space: RecycleSpace | None = None,
+          sketch: SketchOperator | None = None, x0=None, callbacks: dict | None = None) -> SolveResult:
+    """solver.hpp:269-365. b / x0: numpy (host) or float64 CUDA tensors (device)."""
+    ctx = A.ctx
+    space = space if space is not None else RecycleSpace(ctx)
+    kb, pb, nb = _ptr(b)
+    if nb != A.local_rows:
+        raise ValueError(f"solve: rhs length {nb} does not match operator size {A.local_rows}")
+    kx0, px0, nx0 = _ptr(x0)
+    if x0 is not None and nx0 != nb:
+        raise ValueError(f"solve: x0 length {nx0} does not match rhs length {nb}")
+    if _is_torch_cuda(b):
+        import torch
+        x = torch.empty(nb, dtype=torch.float64, device=b.device)
+        px = C.c_void_p(x.data_ptr())
+    else:
+        x = np.empty(nb)
+        px = x.ctypes.data_as(C.c_void_p)
+    c = cfg.c()
+    cb, keep = _make_callbacks(callbacks)
+    rep = C.c_void_p()
+    _check(_lib.sdr_solve(ctx._h, A._h, pb, px0, C.byref(c), space._h, sketch._h if sketch else None,
+                          C.byref(cb) if cb is not None else None, px, C.byref(rep)))
+    return SolveResult(x, _report(rep), space)
+
+
+@dataclass
+class ProblemInstance:
+    """problems.hpp:17-22."""
+    matrix: SparseMatrix
+    rhs: object
+    x0: object = None
+    target_tol: float = 0.0
+
+
+@dataclass
+class SequenceResult:
+    reports: list
+    solutions: list
+    space: RecycleSpace
+
+
+def solve_sequence(problems, cfg: SolverConfig, sketch: SketchOperator | None = None,
+                   initial_space: RecycleSpace | None = None, shared_matrix: bool = False) -> SequenceResult:
+    """solver.hpp:385-459 (matrix change detected by object identity)."""
+    n = len(problems)
+    if n == 0:
+        cfg.validate()
+        return SequenceResult([], [], initial_space or RecycleSpace())
+    ctx = problems[0].matrix.ctx if problems[0].matrix is not None else default_context()
+    space = initial_space if initial_space is not None else RecycleSpace(ctx)
+    keep = []
+    mats = (C.c_void_p * n)(*[p.matrix._h if p.matrix is not None else None for p in problems])
+    rhs = (C.c_void_p * n)()
+    x0s = (C.c_void_p * n)()
+    xs = []
+    xo = (C.c_void_p * n)()
+    for i, p in enumerate(problems):
+        kb, pb, nb = _ptr(p.rhs)
+        keep.append(kb)
+        rhs[i] = pb
+        if p.x0 is not None:
+            k0, p0, _ = _ptr(p.x0)
+            keep.append(k0)
+            x0s[i] = p0
+        x = np.zeros(nb)
+        xs.append(x)
+        xo[i] = x.ctypes.data_as(C.c_void_p)
+    tols = np.array([p.target_tol for p in problems], dtype=np.float64)
+    reps = (C.c_void_p * n)()
+    c = cfg.c()
+    _check(_lib.sdr_solve_sequence(ctx._h, n, mats, rhs, x0s, tols.ctypes.data_as(C.c_void_p), int(shared_matrix),
+                                   C.byref(c), sketch._h if sketch else None, space._h, xo, reps))
+    reports = [_report(reps[i]) for i in range(n)]
+    sols = [xs[i] if not reports[i].error else np.empty(0) for i in range(n)]
+    return SequenceResult(reports, sols, space)

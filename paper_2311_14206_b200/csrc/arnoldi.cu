@@ -1,0 +1,275 @@
+// K2: truncated-Arnoldi update pass, plus small vector kernels and the
+// tall-skinny basis recombination (K4/K7), sm_100a.
+//
+// Replaces arnoldi.hpp:91-114 (MGS window, normalisation) and the N-length
+// products of solver.hpp:197-198 / recycle.hpp:257-286.
+//
+// MGS as one pass (inverse-compact-WY form, Swirydowicz et al., "Low
+// synchronization Gram-Schmidt and GMRES algorithms", NLAA 2020): with the
+// window dots p_i = v_i.(A v_j) from K1 and the window Gram entries
+// G(l,i) = v_l.v_i produced by the previous steps' K2, the MGS coefficients
+// are h_i = p_i - sum_{l<i} h_l G(l,i) — equal to the reference's
+// h_i = v_i.(A v_j - sum_{l<i} h_l v_l) in exact arithmetic, with MGS-class
+// loss of orthogonality. Basis vectors are stored unnormalised (w_i) with
+// device scales c_i = 1/||w_i||, so normalisation costs no extra pass.
+// Algorithmic bytes per row: y + window vectors read, w_{j+1} written.
+#include "kernels.hpp"
+#include "reduce.cuh"
+
+namespace sdr {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int MAXT>
+__global__ void __launch_bounds__(kThreads) k_update(const double* __restrict__ y, double* __restrict__ V, int64_t ldv,
+                                                      int64_t own_off, int64_t n, int j, int nwin, int ngram,
+                                                      double* __restrict__ rec, int64_t rstride, int T,
+                                                      double* __restrict__ cvec, double* __restrict__ partials,
+                                                      unsigned* __restrict__ counter) {
+  __shared__ double coef[MAXT + 1];
+  const int b_off = 2 * T + 3;
+  if (threadIdx.x == 0) {
+    const double* recA = rec + static_cast<int64_t>(j + 1) * rstride;
+    const double wn2 = rec[static_cast<int64_t>(j) * rstride + b_off];
+    const double cj = 1.0 / sqrt(wn2);
+    double ci[MAXT], h[MAXT];
+#pragma unroll
+    for (int d = 0; d < MAXT; ++d) {
+      ci[d] = d == 0 ? cj : (d < nwin ? cvec[j - d] : 0.0);
+      h[d] = 0.0;
+    }
+    // MGS order i = j-nwin+1 .. j  <=>  d = nwin-1 .. 0
+    for (int d = nwin - 1; d >= 0; --d) {
+      const int i = j - d;
+      double acc = cj * ci[d] * recA[1 + d];
+      for (int d2 = nwin - 1; d2 > d; --d2) {
+        const double gram = rec[static_cast<int64_t>(i) * rstride + b_off + (d2 - d)];
+        acc -= h[d2] * (ci[d2] * ci[d] * gram);
+      }
+      h[d] = acc;
+    }
+    coef[0] = cj;
+    for (int d = 0; d < MAXT; ++d) coef[1 + d] = d < nwin ? -h[d] * ci[d] : 0.0;
+    if (blockIdx.x == 0) {
+      double* recH = rec + static_cast<int64_t>(j + 1) * rstride + (T + 1);
+      recH[0] = cj * sqrt(recA[0]);
+      for (int d = 0; d < T; ++d) recH[1 + d] = d < nwin ? h[d] : 0.0;
+      recH[1 + T] = cj;
+      cvec[j] = cj;
+    }
+  }
+  __syncthreads();
+
+  double acc[MAXT];
+#pragma unroll
+  for (int k = 0; k < MAXT; ++k) acc[k] = 0.0;
+  double cf[MAXT + 1];
+#pragma unroll
+  for (int k = 0; k <= MAXT; ++k) cf[k] = coef[k];
+  const double* W[MAXT];
+#pragma unroll
+  for (int d = 0; d < MAXT; ++d) W[d] = V + static_cast<int64_t>(j - (d < nwin ? d : 0)) * ldv + own_off;
+  double* wout = V + static_cast<int64_t>(j + 1) * ldv + own_off;
+
+  // two rows per thread through 16-byte accesses (own_off and ldv are 32-aligned)
+  const int64_t npair = n >> 1;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < npair; p += stride) {
+    const double2 yv = __ldcs(reinterpret_cast<const double2*>(y) + p);
+    double2 wv[MAXT];
+#pragma unroll
+    for (int d = MAXT - 1; d >= 0; --d)
+      if (d < nwin) wv[d] = __ldg(reinterpret_cast<const double2*>(W[d]) + p);
+    double w0 = cf[0] * yv.x, w1 = cf[0] * yv.y;
+#pragma unroll
+    for (int d = MAXT - 1; d >= 0; --d)
+      if (d < nwin) {
+        w0 = fma(cf[1 + d], wv[d].x, w0);
+        w1 = fma(cf[1 + d], wv[d].y, w1);
+      }
+    reinterpret_cast<double2*>(wout)[p] = make_double2(w0, w1);
+    acc[0] = fma(w0, w0, fma(w1, w1, acc[0]));
+#pragma unroll
+    for (int g = 1; g < MAXT; ++g)
+      if (g <= ngram) acc[g] = fma(w0, wv[g - 1].x, fma(w1, wv[g - 1].y, acc[g]));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t r = n - 1;
+    double w = cf[0] * y[r];
+    double wv[MAXT];
+#pragma unroll
+    for (int d = MAXT - 1; d >= 0; --d)
+      if (d < nwin) {
+        wv[d] = W[d][r];
+        w = fma(cf[1 + d], wv[d], w);
+      }
+    wout[r] = w;
+    acc[0] = fma(w, w, acc[0]);
+#pragma unroll
+    for (int g = 1; g < MAXT; ++g)
+      if (g <= ngram) acc[g] = fma(w, wv[g - 1], acc[g]);
+  }
+  block_partials<MAXT>(acc, 1 + ngram, partials);
+  if (last_block_done(counter)) {
+    double* recB = rec + static_cast<int64_t>(j + 1) * rstride + b_off;
+    fold_partials(partials, gridDim.x, 1 + ngram, recB);
+    if (threadIdx.x == 0) {
+      for (int g = 1 + ngram; g < T; ++g) recB[g] = 0.0;
+      *counter = 0u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_copy_norm(const double* __restrict__ src, double* __restrict__ dst,
+                                                         int64_t n, double* __restrict__ partials,
+                                                         unsigned* __restrict__ counter, double* __restrict__ out) {
+  double acc[1] = {0.0};
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = src[i];
+    dst[i] = v;
+    acc[0] = fma(v, v, acc[0]);
+  }
+  block_partials<1>(acc, 1, partials);
+  if (last_block_done(counter)) {
+    fold_partials(partials, gridDim.x, 1, out);
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+}
+
+__global__ void k_axpy(double a, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) y[i] += a * x[i];
+}
+
+__global__ void k_scale_copy(double a, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = a * x[i];
+}
+
+/// out_o = sum_i coef[i*nout + o] * in_i, o < nout (<= NOUT); optional
+/// ||out_o||^2 via the deterministic grid fold. Coefficients are broadcast
+/// from shared memory; each input column is streamed once.
+template <int NOUT>
+__global__ void __launch_bounds__(kThreads) k_tallskinny(const double* const* __restrict__ in, int nin,
+                                                          const double* __restrict__ coef, int nout,
+                                                          double* const* __restrict__ out, int64_t n,
+                                                          double* __restrict__ partials,
+                                                          unsigned* __restrict__ counter, double* __restrict__ norms) {
+  extern __shared__ double cs[];  // nin * NOUT
+  for (int q = threadIdx.x; q < nin * NOUT; q += blockDim.x) {
+    const int i = q / NOUT, o = q % NOUT;
+    cs[q] = o < nout ? coef[i * nout + o] : 0.0;
+  }
+  __syncthreads();
+  double nrm[NOUT];
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) nrm[o] = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+    double a[NOUT];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) a[o] = 0.0;
+    for (int i = 0; i < nin; ++i) {
+      const double v = __ldcs(in[i] + r);
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) a[o] = fma(cs[i * NOUT + o], v, a[o]);
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+      if (o < nout) {
+        out[o][r] = a[o];
+        nrm[o] = fma(a[o], a[o], nrm[o]);
+      }
+  }
+  if (norms) {
+    block_partials<NOUT>(nrm, nout, partials);
+    if (last_block_done(counter)) {
+      fold_partials(partials, gridDim.x, nout, norms);
+      if (threadIdx.x == 0) *counter = 0u;
+    }
+  }
+}
+
+int stream_grid(const Context& c, int64_t n, int per_thread = 1) {
+  const int64_t want = (n / per_thread + kThreads - 1) / kThreads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.num_sms) * 8)));
+}
+
+template <int MAXT>
+void update_impl(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
+                 int ngram, double* rec, const RecLayout& L, double* cvec) {
+  const int g = stream_grid(c, lay.nloc, 2);
+  TimedLaunch t(c, "update");
+  k_update<MAXT><<<g, kThreads, 0, c.stream>>>(y, V, ldv, lay.own_off, lay.nloc, j, nwin, ngram, rec, L.stride, L.T,
+                                               cvec, c.partials(static_cast<int64_t>(MAXT) * g), c.counters() + 2);
+  SDR_KERNEL_CHECK();
+}
+
+template <int NOUT>
+void tallskinny_impl(Context& c, const double* const* in, int nin, const double* coef, int nout, double* const* out,
+                     int64_t n, double* norms2) {
+  const int g = stream_grid(c, n);
+  const size_t smem = sizeof(double) * static_cast<size_t>(nin) * NOUT;
+  if (smem > 48 * 1024)
+    SDR_CUDA(cudaFuncSetAttribute(k_tallskinny<NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  TimedLaunch t(c, "tallskinny");
+  k_tallskinny<NOUT><<<g, kThreads, smem, c.stream>>>(in, nin, coef, nout, out, n,
+                                                      c.partials(static_cast<int64_t>(NOUT) * g), c.counters() + 3,
+                                                      norms2);
+  SDR_KERNEL_CHECK();
+}
+
+}  // namespace
+
+void launch_update(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
+                   int ngram, double* rec, const RecLayout& L, double* cvec) {
+  const int need = std::max(nwin, ngram + 1);
+  if (need <= 4)
+    update_impl<4>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec);
+  else if (need <= 8)
+    update_impl<8>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec);
+  else if (need <= 33)
+    update_impl<33>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec);
+  else
+    throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
+}
+
+void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, double* norm2) {
+  const int g = stream_grid(c, n);
+  TimedLaunch t(c, "copy_norm");
+  k_copy_norm<<<g, kThreads, 0, c.stream>>>(src, dst, n, c.partials(g), c.counters() + 4, norm2);
+  SDR_KERNEL_CHECK();
+}
+
+void launch_axpy(Context& c, double a, const double* x, double* y, int64_t n) {
+  if (n == 0) return;
+  TimedLaunch t(c, "axpy");
+  k_axpy<<<stream_grid(c, n), kThreads, 0, c.stream>>>(a, x, y, n);
+  SDR_KERNEL_CHECK();
+}
+
+void launch_scale_copy(Context& c, double a, const double* x, double* y, int64_t n) {
+  if (n == 0) return;
+  TimedLaunch t(c, "scale_copy");
+  k_scale_copy<<<stream_grid(c, n), kThreads, 0, c.stream>>>(a, x, y, n);
+  SDR_KERNEL_CHECK();
+}
+
+void launch_tallskinny(Context& c, const double* const* in, int nin, const double* coef, int nout,
+                       double* const* out, int64_t n, double* norms2) {
+  if (nout <= 1)
+    tallskinny_impl<1>(c, in, nin, coef, nout, out, n, norms2);
+  else if (nout <= 8)
+    tallskinny_impl<8>(c, in, nin, coef, nout, out, n, norms2);
+  else if (nout <= 16)
+    tallskinny_impl<16>(c, in, nin, coef, nout, out, n, norms2);
+  else if (nout <= 32)
+    tallskinny_impl<32>(c, in, nin, coef, nout, out, n, norms2);
+  else
+    throw invalid("tall-skinny product with " + std::to_string(nout) + " outputs exceeds 32 per launch");
+}
+
+}  // namespace sdr

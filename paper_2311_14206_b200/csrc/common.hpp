@@ -1,0 +1,117 @@
+// Shared host-side plumbing: error classes mirroring the reference's
+// exception taxonomy, CUDA checks, RAII device / pinned buffers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+namespace sdr {
+
+using i64 = std::int64_t;
+
+/// Error carrying the C-ABI status code (sdr_status).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+inline Error invalid(const std::string& m) { return Error(1, m); }
+inline Error domain(const std::string& m) { return Error(2, m); }
+inline Error logic(const std::string& m) { return Error(3, m); }
+inline Error runtime(const std::string& m) { return Error(4, m); }
+
+#define SDR_CUDA(call)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess)                                                                          \
+      throw ::sdr::Error(e_ == cudaErrorMemoryAllocation ? 7 : 5,                                   \
+                         std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                             std::to_string(__LINE__) + ")");                                      \
+  } while (0)
+
+#define SDR_KERNEL_CHECK() SDR_CUDA(cudaGetLastError())
+
+/// Owning device allocation.
+template <class T>
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(i64 n) { resize(n); }
+  ~DeviceBuffer() { release(); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_, n_ = o.n_;
+      o.p_ = nullptr, o.n_ = 0;
+    }
+    return *this;
+  }
+  void resize(i64 n) {
+    if (n == n_) return;
+    release();
+    if (n > 0) SDR_CUDA(cudaMalloc(&p_, sizeof(T) * static_cast<size_t>(n)));
+    n_ = n;
+  }
+  void ensure(i64 n) {
+    if (n > n_) resize(n);
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  i64 size() const { return n_; }
+
+ private:
+  T* p_ = nullptr;
+  i64 n_ = 0;
+};
+
+/// Page-locked host allocation (for async D2H of step records).
+template <class T>
+class PinnedBuffer {
+ public:
+  PinnedBuffer() = default;
+  ~PinnedBuffer() { release(); }
+  PinnedBuffer(const PinnedBuffer&) = delete;
+  PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+  void ensure(i64 n) {
+    if (n <= n_) return;
+    release();
+    SDR_CUDA(cudaMallocHost(&p_, sizeof(T) * static_cast<size_t>(n)));
+    n_ = n;
+  }
+  void release() {
+    if (p_) cudaFreeHost(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  i64 size() const { return n_; }
+
+ private:
+  T* p_ = nullptr;
+  i64 n_ = 0;
+};
+
+inline bool is_device_pointer(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+inline i64 round_up(i64 v, i64 m) { return (v + m - 1) / m * m; }
+
+}  // namespace sdr

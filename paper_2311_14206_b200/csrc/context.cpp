@@ -1,0 +1,188 @@
+// Context implementation: stream, scratch, NCCL (dlopen'd so the library
+// shares whatever libnccl.so.2 the host process — e.g. torch — already
+// loaded instead of linking a second copy), and event timing.
+#include "context.hpp"
+
+#include <nccl.h>
+#include <dlfcn.h>
+
+namespace sdr {
+
+struct NcclApi {
+  void* handle = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* load_nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) {
+    if (!api.handle) throw Error(6, "NCCL unavailable: libnccl.so.2 could not be loaded");
+    return &api;
+  }
+  tried = true;
+  api.handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!api.handle) throw Error(6, std::string("NCCL unavailable: ") + dlerror());
+#define SDR_SYM(f)                                                                      \
+  api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.handle, "nccl" #f));             \
+  if (!api.f) {                                                                         \
+    api.handle = nullptr;                                                               \
+    throw Error(6, "NCCL symbol nccl" #f " missing");                                   \
+  }
+  SDR_SYM(GetUniqueId)
+  SDR_SYM(CommInitRank)
+  SDR_SYM(CommDestroy)
+  SDR_SYM(AllReduce)
+  SDR_SYM(AllGather)
+  SDR_SYM(Send)
+  SDR_SYM(Recv)
+  SDR_SYM(GroupStart)
+  SDR_SYM(GroupEnd)
+  SDR_SYM(GetErrorString)
+#undef SDR_SYM
+  return &api;
+}
+
+#define SDR_NCCL(call)                                                                        \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) throw Error(6, std::string(#call) + ": " + nccl_->GetErrorString(r_)); \
+  } while (0)
+
+void nccl_unique_id(void* out) {
+  NcclApi* api = load_nccl();
+  ncclUniqueId id;
+  ncclResult_t r = api->GetUniqueId(&id);
+  if (r != ncclSuccess) throw Error(6, std::string("ncclGetUniqueId: ") + api->GetErrorString(r));
+  std::memcpy(out, &id, sizeof(id));
+}
+
+Context::Context(int dev, int rk, int ws, const void* nccl_id) : device(dev), rank(rk), world(ws) {
+  int count = 0;
+  SDR_CUDA(cudaGetDeviceCount(&count));
+  if (dev < 0 || dev >= count) throw invalid("sdr_ctx_create: no CUDA device " + std::to_string(dev));
+  SDR_CUDA(cudaSetDevice(dev));
+  SDR_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  SDR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  counters_.resize(kNumCounters);
+  SDR_CUDA(cudaMemset(counters_.get(), 0, sizeof(unsigned) * kNumCounters));
+  if (world > 1) {
+    if (!nccl_id) throw invalid("sdr_ctx_create_dist: NCCL id required for world > 1");
+    nccl_ = load_nccl();
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclComm_t c = nullptr;
+    SDR_NCCL(nccl_->CommInitRank(&c, world, id, rank));
+    comm_ = c;
+  }
+  SDR_CUDA(cudaDeviceSynchronize());
+}
+
+Context::~Context() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  if (comm_ && nccl_) nccl_->CommDestroy(static_cast<ncclComm_t>(comm_));
+  for (auto& p : pending_) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : free_events_) cudaEventDestroy(e);
+  if (open_start_) cudaEventDestroy(open_start_);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void Context::allreduce_sum(double* dev, i64 n) {
+  if (world <= 1 || n <= 0) return;
+  ++launches;
+  if (timing) time_begin("allreduce");
+  SDR_NCCL(nccl_->AllReduce(dev, dev, static_cast<size_t>(n), ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream));
+  if (timing) time_end();
+}
+
+void Context::allgather_i64(const i64* host_in, i64 count, i64* host_out) {
+  if (world <= 1) {
+    std::memcpy(host_out, host_in, sizeof(i64) * static_cast<size_t>(count));
+    return;
+  }
+  DeviceBuffer<i64> buf(count * (world + 1));
+  SDR_CUDA(cudaMemcpyAsync(buf.get(), host_in, sizeof(i64) * count, cudaMemcpyHostToDevice, stream));
+  SDR_NCCL(nccl_->AllGather(buf.get(), buf.get() + count, static_cast<size_t>(count), ncclInt64,
+                            static_cast<ncclComm_t>(comm_), stream));
+  SDR_CUDA(cudaMemcpyAsync(host_out, buf.get() + count, sizeof(i64) * count * world, cudaMemcpyDeviceToHost, stream));
+  sync();
+}
+
+void Context::halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin) {
+  if (world <= 1 || plan.empty()) return;
+  ++launches;
+  if (timing) time_begin("halo");
+  auto comm = static_cast<ncclComm_t>(comm_);
+  SDR_NCCL(nccl_->GroupStart());
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    if (plan.send_cnt[q] > 0)
+      SDR_NCCL(nccl_->Send(x_own + (plan.send_lo[q] - row_begin), static_cast<size_t>(plan.send_cnt[q]), ncclDouble, q,
+                           comm, stream));
+    if (plan.recv_cnt[q] > 0)
+      SDR_NCCL(nccl_->Recv(x_ext + (plan.recv_lo[q] - ext_begin), static_cast<size_t>(plan.recv_cnt[q]), ncclDouble, q,
+                           comm, stream));
+  }
+  SDR_NCCL(nccl_->GroupEnd());
+  if (timing) time_end();
+}
+
+cudaEvent_t Context::take_event() {
+  if (!free_events_.empty()) {
+    cudaEvent_t e = free_events_.back();
+    free_events_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  SDR_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Context::time_begin(const char* name) {
+  open_name_ = name;
+  open_start_ = take_event();
+  SDR_CUDA(cudaEventRecord(open_start_, stream));
+}
+
+void Context::time_end() {
+  cudaEvent_t b = take_event();
+  SDR_CUDA(cudaEventRecord(b, stream));
+  pending_.push_back({open_name_, open_start_, b});
+  open_start_ = nullptr;
+  if (pending_.size() > 4096) timing_flush();
+}
+
+void Context::timing_flush() {
+  if (pending_.empty()) return;
+  sync();
+  for (auto& p : pending_) {
+    float ms = 0.f;
+    SDR_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto& t = timings[p.name];
+    ++t.launches;
+    t.ms += ms;
+    free_events_.push_back(p.a);
+    free_events_.push_back(p.b);
+  }
+  pending_.clear();
+}
+
+void Context::timing_reset() {
+  timing_flush();
+  timings.clear();
+}
+
+}  // namespace sdr

@@ -1,0 +1,131 @@
+// Device context: one GPU, one CUDA stream, optional NCCL rank, reusable
+// reduction scratch and per-kernel CUDA-event timing.
+#pragma once
+
+#include "common.hpp"
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace sdr {
+
+struct NcclApi;  // dlopen'd NCCL entry points (context.cpp)
+
+/// Halo plan of one operator in a distributed context: which global rows
+/// this rank receives from / sends to each peer.
+struct HaloPlan {
+  std::vector<i64> recv_lo, recv_cnt, send_lo, send_cnt;  // per peer, global rows
+  bool empty() const {
+    for (i64 c : recv_cnt)
+      if (c) return false;
+    for (i64 c : send_cnt)
+      if (c) return false;
+    return true;
+  }
+};
+
+struct KernelTiming {
+  i64 launches = 0;
+  double ms = 0.0;
+};
+
+class Context {
+ public:
+  Context(int device, int rank, int world, const void* nccl_id);
+  ~Context();
+
+  int device = 0, rank = 0, world = 1, num_sms = 148;
+  cudaStream_t stream = nullptr;
+  i64 launches = 0;
+
+  bool distributed() const { return world > 1; }
+
+  // ---- reductions scratch: per-kernel-class partial buffers and
+  // last-block-done counters (zeroed once, reset by the last block).
+  double* partials(i64 n) {
+    partials_.ensure(n);
+    return partials_.get();
+  }
+  double* partials2(i64 n) {
+    partials2_.ensure(n);
+    return partials2_.get();
+  }
+  unsigned* counters() { return counters_.get(); }  // kNumCounters slots
+  static constexpr int kNumCounters = 16;
+
+  // ---- collectives (no-ops on one rank)
+  void allreduce_sum(double* dev, i64 n);
+  void allgather_i64(const i64* host_in, i64 count, i64* host_out);  // host in/out, small
+  void halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin);
+
+  // ---- timing
+  bool timing = false;
+  void time_begin(const char* name);
+  void time_end();
+  void timing_flush();
+  void timing_reset();
+  std::map<std::string, KernelTiming> timings;
+
+  // ---- staging
+  double* stage(i64 n) {
+    stage_.ensure(n);
+    return stage_.get();
+  }
+  double* pinned(i64 n) {
+    pinned_.ensure(n);
+    return pinned_.get();
+  }
+
+  void sync() { SDR_CUDA(cudaStreamSynchronize(stream)); }
+
+  /// Solver workspace cached across solves (solver.cpp owns the type).
+  std::shared_ptr<void> workspace;
+
+ private:
+  DeviceBuffer<double> partials_, partials2_, stage_;
+  DeviceBuffer<unsigned> counters_;
+  PinnedBuffer<double> pinned_;
+  NcclApi* nccl_ = nullptr;
+  void* comm_ = nullptr;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending_;
+  std::vector<cudaEvent_t> free_events_;
+  std::string open_name_;
+  cudaEvent_t open_start_ = nullptr;
+  cudaEvent_t take_event();
+};
+
+/// RAII timing scope around one launch: `TimedLaunch t(ctx, "update");`.
+struct TimedLaunch {
+  Context& c;
+  TimedLaunch(Context& ctx, const char* name) : c(ctx) {
+    ++c.launches;
+    if (c.timing) c.time_begin(name);
+  }
+  ~TimedLaunch() {
+    if (c.timing) c.time_end();
+  }
+};
+
+/// Staged view of a user pointer: device pointers are used in place, host
+/// pointers are copied through a device buffer.
+struct DeviceIn {
+  const double* ptr = nullptr;
+  DeviceBuffer<double> own;
+  DeviceIn(Context& c, const double* p, i64 n) {
+    if (!p || n == 0 || is_device_pointer(p)) {
+      ptr = p;
+      return;
+    }
+    own.resize(n);
+    SDR_CUDA(cudaMemcpyAsync(own.get(), p, sizeof(double) * static_cast<size_t>(n), cudaMemcpyHostToDevice, c.stream));
+    ptr = own.get();
+  }
+};
+
+}  // namespace sdr

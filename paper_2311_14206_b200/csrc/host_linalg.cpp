@@ -1,0 +1,266 @@
+#include "host_linalg.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
+
+namespace sdr {
+
+void init_host_blas() {
+  static bool done = false;
+  if (!done) {
+    scipy_openblas_set_num_threads(1);  // deterministic, no oversubscription
+    done = true;
+  }
+}
+
+double hdot(const double* x, const double* y, i64 n) {
+  const int nn = static_cast<int>(n), one = 1;
+  return n > 0 ? scipy_ddot_(&nn, x, &one, y, &one) : 0.0;
+}
+
+double hnorm(const double* x, i64 n) { return std::sqrt(hdot(x, x, n)); }
+
+void hgemv(bool trans, i64 rows, i64 cols, double alpha, const double* A, i64 lda, const double* x, double beta,
+           double* y) {
+  if (rows == 0 || cols == 0) {
+    const i64 ny = trans ? cols : rows;
+    for (i64 i = 0; i < ny; ++i) y[i] = beta == 0.0 ? 0.0 : beta * y[i];
+    return;
+  }
+  const int m = static_cast<int>(rows), n = static_cast<int>(cols), ld = static_cast<int>(lda), one = 1;
+  scipy_dgemv_(trans ? "T" : "N", &m, &n, &alpha, A, &ld, x, &one, &beta, y, &one, 1);
+}
+
+HostQR::HostQR(i64 rows, i64 capacity, double rank_tol) : rows_(rows), cap_(std::max<i64>(capacity, 1)), rank_tol_(rank_tol) {
+  if (rows < 1) throw invalid("IncrementalQR: rows must be positive");
+  m_.assign(static_cast<size_t>(rows_ * cap_), 0.0);
+  q_.assign(static_cast<size_t>(rows_ * cap_), 0.0);
+  r_.assign(static_cast<size_t>(cap_ * cap_), 0.0);
+}
+
+void HostQR::grow() {  // incremental_qr.hpp:149-156
+  const i64 cap = 2 * cap_;
+  m_.resize(static_cast<size_t>(rows_ * cap), 0.0);
+  q_.resize(static_cast<size_t>(rows_ * cap), 0.0);
+  std::vector<double> r2(static_cast<size_t>(cap * cap), 0.0);
+  for (i64 j = 0; j < p_; ++j)
+    for (i64 i = 0; i < p_; ++i) r2[static_cast<size_t>(i + j * cap)] = r_[static_cast<size_t>(i + j * cap_)];
+  r_.swap(r2);
+  cap_ = cap;
+}
+
+HostQR::AppendInfo HostQR::append(const double* col, i64 len) {  // incremental_qr.hpp:46-79
+  if (len != rows_)
+    throw invalid("IncrementalQR::append: column length " + std::to_string(len) + " does not match " +
+                  std::to_string(rows_) + " rows");
+  if (p_ == cap_) grow();
+  const i64 p = p_, s = rows_;
+  std::copy(col, col + s, m_.data() + p * s);
+  std::vector<double> w(col, col + s), c(static_cast<size_t>(p)), coeffs(static_cast<size_t>(p), 0.0);
+  for (int pass = 0; pass < 2; ++pass) {
+    if (p > 0) {
+      hgemv(true, s, p, 1.0, q_.data(), s, w.data(), 0.0, c.data());
+      hgemv(false, s, p, -1.0, q_.data(), s, c.data(), 1.0, w.data());
+      for (i64 q = 0; q < p; ++q) coeffs[static_cast<size_t>(q)] += c[static_cast<size_t>(q)];
+    }
+  }
+  const double rho = hnorm(w.data(), s);
+  AppendInfo info;
+  info.column = p;
+  for (i64 q = 0; q < p; ++q) r_[static_cast<size_t>(q + p * cap_)] = coeffs[static_cast<size_t>(q)];
+  double* qc = q_.data() + p * s;
+  if (rho <= rank_tol_ * hnorm(col, s)) {
+    info.rank_deficient = true;
+    std::fill(qc, qc + s, 0.0);
+    r_[static_cast<size_t>(p + p * cap_)] = 0.0;
+    state_.push_back(2);
+  } else {
+    for (i64 r = 0; r < s; ++r) qc[r] = w[static_cast<size_t>(r)] / rho;
+    r_[static_cast<size_t>(p + p * cap_)] = rho;
+    state_.push_back(0);
+  }
+  ++p_;
+  qtb_valid_.push_back(0);
+  qtb_.push_back(0.0);
+  return info;
+}
+
+void HostQR::check(i64 column) const {
+  if (column < 0 || column >= p_) throw invalid("IncrementalQR: no column " + std::to_string(column));
+}
+
+void HostQR::exclude(i64 column) {
+  check(column);
+  state_[static_cast<size_t>(column)] = 1;
+}
+
+void HostQR::set_rhs(const double* rhs, i64 len) {
+  if (len != rows_)
+    throw invalid("IncrementalQR::solve: rhs length " + std::to_string(len) + " does not match " +
+                  std::to_string(rows_) + " rows");
+  rhs_.assign(rhs, rhs + len);
+  std::fill(qtb_valid_.begin(), qtb_valid_.end(), 0);
+}
+
+double HostQR::solve(const double* rhs, i64 len, double* y) {
+  set_rhs(rhs, len);
+  return solve_cached(y);
+}
+
+double HostQR::solve_cached(double* y) {  // incremental_qr.hpp:107-135
+  for (i64 i = 0; i < p_; ++i)
+    if (state_[static_cast<size_t>(i)] == 2)
+      throw runtime("IncrementalQR::solve: column " + std::to_string(i) +
+                    " is rank-deficient and unresolved; exclude it or rebuild");
+  const i64 s = rows_;
+  std::vector<i64> used;
+  used.reserve(static_cast<size_t>(p_));
+  for (i64 i = 0; i < p_; ++i)
+    if (state_[static_cast<size_t>(i)] == 0) used.push_back(i);
+  std::fill(y, y + p_, 0.0);
+  for (size_t q = 0; q < used.size(); ++q) {
+    const i64 c = used[q];
+    if (!qtb_valid_[static_cast<size_t>(c)]) {
+      qtb_[static_cast<size_t>(c)] = hdot(q_.data() + c * s, rhs_.data(), s);
+      qtb_valid_[static_cast<size_t>(c)] = 1;
+    }
+  }
+  for (size_t q = used.size(); q-- > 0;) {
+    const i64 uq = used[q];
+    double acc = qtb_[static_cast<size_t>(uq)];
+    for (size_t q2 = q + 1; q2 < used.size(); ++q2) acc -= r_[static_cast<size_t>(uq + used[q2] * cap_)] * y[used[q2]];
+    y[uq] = acc / r_[static_cast<size_t>(uq + uq * cap_)];
+  }
+  std::vector<double> res(rhs_);
+  hgemv(false, s, p_, -1.0, m_.data(), s, y, 1.0, res.data());
+  return hnorm(res.data(), s);
+}
+
+void HostQR::factors(double* Q, double* R) const {
+  if (Q) std::copy(q_.begin(), q_.begin() + rows_ * p_, Q);
+  if (R)
+    for (i64 j = 0; j < p_; ++j)
+      for (i64 i = 0; i < p_; ++i) R[i + j * p_] = r_[static_cast<size_t>(i + j * cap_)];
+}
+
+// ------------------------------------------------------------------ harmonic
+
+namespace {
+
+void thin_svd(const HMat& A, std::vector<double>& sv, HMat* U, HMat* V) {
+  const int m = static_cast<int>(A.rows), n = static_cast<int>(A.cols), mn = std::min(m, n);
+  sv.assign(static_cast<size_t>(mn), 0.0);
+  if (mn == 0) {
+    if (U) *U = HMat(m, 0);
+    if (V) *V = HMat(n, 0);
+    return;
+  }
+  HMat a = A, u(m, mn), vt(mn, n);
+  const bool vec = U || V;
+  const char* job = vec ? "S" : "N";
+  int info = 0, lwork = -1, lda = std::max(1, m), ldu = vec ? std::max(1, m) : 1, ldvt = vec ? std::max(1, mn) : 1;
+  double wq = 0.0;
+  scipy_dgesvd_(job, job, &m, &n, a.a.data(), &lda, sv.data(), u.a.data(), &ldu, vt.a.data(), &ldvt, &wq, &lwork,
+                &info, 1, 1);
+  lwork = static_cast<int>(wq) + 1;
+  std::vector<double> work(static_cast<size_t>(lwork));
+  scipy_dgesvd_(job, job, &m, &n, a.a.data(), &lda, sv.data(), u.a.data(), &ldu, vt.a.data(), &ldvt, work.data(),
+                &lwork, &info, 1, 1);
+  if (info != 0) throw runtime("truncated_svd: dgesvd failed with info = " + std::to_string(info));
+  if (U) *U = u;
+  if (V) {
+    *V = HMat(n, mn);
+    for (i64 c = 0; c < mn; ++c)
+      for (i64 r = 0; r < n; ++r) (*V)(r, c) = vt(c, r);
+  }
+}
+
+}  // namespace
+
+double cond2(const HMat& A) {
+  std::vector<double> sv;
+  thin_svd(A, sv, nullptr, nullptr);
+  if (sv.empty()) return 1.0;
+  return sv.back() > 0.0 ? sv.front() / sv.back() : std::numeric_limits<double>::infinity();
+}
+
+Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_tol) {
+  if (!(rank_tol >= 0.0)) throw invalid("truncated_svd: rank_tol must be >= 0");
+  if (k < 0) throw invalid("harmonic_pairs: k must be nonnegative");
+  if (SW.rows != SAW.rows || SW.cols != SAW.cols) throw invalid("fill_pencil: SW dimensions do not match the decomposition");
+  std::vector<double> sv;
+  HMat U, V;
+  thin_svd(SAW, sv, &U, &V);
+  i64 l = 0;  // recycle.hpp:102-104
+  const double cutoff = sv.empty() ? 0.0 : rank_tol * sv[0];
+  while (l < static_cast<i64>(sv.size()) && sv[static_cast<size_t>(l)] > cutoff && sv[static_cast<size_t>(l)] > 0.0) ++l;
+  const i64 s = SAW.rows, p = SAW.cols;
+  Harmonic out;
+  out.rank = l;
+  out.k_requested = k;
+  if (k > l) {
+    k = l;
+    out.rank_limited = true;
+  }
+  if (k == 0 || l == 0) {
+    out.coeffs = HMat(p, 0);
+    return out;
+  }
+  // m = u^T SW v (recycle.hpp:114-118), C = diag(1/sigma) m
+  HMat swv(s, l);
+  for (i64 c = 0; c < l; ++c) hgemv(false, s, p, 1.0, SW.a.data(), s, V.col(c), 0.0, swv.col(c));
+  HMat C(l, l);
+  for (i64 c = 0; c < l; ++c) {
+    hgemv(true, s, l, 1.0, U.a.data(), s, swv.col(c), 0.0, C.col(c));
+    for (i64 r = 0; r < l; ++r) C(r, c) = (1.0 / sv[static_cast<size_t>(r)]) * C(r, c);
+  }
+  // real Schur (dgees), ordering, conjugate-pair closure, dtrsen (recycle.hpp:167-205)
+  const int n = static_cast<int>(l);
+  HMat Q(l, l);
+  std::vector<double> wr(static_cast<size_t>(l)), wi(static_cast<size_t>(l));
+  int sdim = 0, info = 0, lwork = 80 * n + 64;
+  std::vector<double> work(static_cast<size_t>(lwork));
+  scipy_dgees_("V", "N", nullptr, &n, C.a.data(), &n, &sdim, wr.data(), wi.data(), Q.a.data(), &n, work.data(), &lwork,
+               nullptr, &info, 1, 1);
+  if (info != 0) throw runtime("real_schur: dgees failed with info = " + std::to_string(info));
+  std::vector<i64> order(static_cast<size_t>(l));
+  std::iota(order.begin(), order.end(), i64{0});
+  auto mag = [&](i64 i) { return std::hypot(wr[static_cast<size_t>(i)], wi[static_cast<size_t>(i)]); };
+  std::sort(order.begin(), order.end(), [&](i64 a, i64 b) {
+    const double ma = mag(a), mb = mag(b);
+    if (ma != mb) return ma > mb;
+    if (wr[static_cast<size_t>(a)] != wr[static_cast<size_t>(b)]) return wr[static_cast<size_t>(a)] > wr[static_cast<size_t>(b)];
+    return a < b;
+  });
+  std::vector<int> sel(static_cast<size_t>(l), 0);
+  for (i64 i = 0; i < k; ++i) sel[static_cast<size_t>(order[static_cast<size_t>(i)])] = 1;
+  for (i64 i = 0; i + 1 < l;) {
+    if (wi[static_cast<size_t>(i)] != 0.0) {
+      if (sel[static_cast<size_t>(i)] != sel[static_cast<size_t>(i) + 1]) {
+        sel[static_cast<size_t>(i)] = sel[static_cast<size_t>(i) + 1] = 1;
+        out.pair_extended = true;
+      }
+      i += 2;
+    } else {
+      ++i;
+    }
+  }
+  i64 ke = 0;
+  for (int v : sel) ke += v;
+  int mm = 0, nn2 = std::max(1, n * n);
+  double scond = 0.0, sep = 0.0;
+  std::vector<double> w2(static_cast<size_t>(nn2));
+  std::vector<int> iw(static_cast<size_t>(nn2));
+  scipy_dtrsen_("N", "V", sel.data(), &n, C.a.data(), &n, Q.a.data(), &n, wr.data(), wi.data(), &mm, &scond, &sep,
+                w2.data(), &nn2, iw.data(), &nn2, &info, 1, 1);
+  if (info != 0) throw runtime("reorder_schur: dtrsen failed with info = " + std::to_string(info));
+  out.k_eff = ke;
+  out.coeffs = HMat(p, ke);
+  for (i64 c = 0; c < ke; ++c) hgemv(false, p, l, 1.0, V.a.data(), p, Q.col(c), 0.0, out.coeffs.col(c));
+  for (i64 i = 0; i < ke; ++i) out.mu.emplace_back(wr[static_cast<size_t>(i)], wi[static_cast<size_t>(i)]);
+  return out;
+}
+
+}  // namespace sdr

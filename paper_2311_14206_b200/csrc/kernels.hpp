@@ -1,0 +1,72 @@
+// Host-side launchers for the sm_100a kernels (definitions in *.cu).
+#pragma once
+
+#include "context.hpp"
+
+namespace sdr {
+
+constexpr int kSlice = 32;  // SELL-C slice height (one warp)
+
+/// Device SELL-32 view of a (rank-local) operator. Column indices address
+/// the rank's extended vector (halo_lo rows below the own block first).
+struct SellView {
+  const int64_t* slice_ptr = nullptr;  // nslices + 1 element offsets
+  const int32_t* cols = nullptr;
+  const double* vals = nullptr;
+  int64_t nrows = 0, nslices = 0;
+};
+
+/// Layout of every length-N vector a rank stores with halo space:
+/// [pad | halo_lo | own (nloc) | halo_hi]; own starts at own_off (32-aligned).
+struct VecLayout {
+  int64_t nloc = 0, halo_lo = 0, halo_hi = 0, own_off = 0, ld = 0;
+  int64_t ext_shift() const { return own_off - halo_lo; }  // buffer index of ext row 0
+};
+
+/// Per-step record layout (doubles), T = max window:
+///   A  [0, T+1)         : ||y||^2, y.w_{j-d} (d < T)      (K1, allreduced)
+///   H  [T+1, 2T+3)      : ||A v_j||, h_{j-d,j} (d < T), c_j (K2 prologue)
+///   B  [2T+3, 3T+3+s)   : ||w_{j+1}||^2, w_{j+1}.w_{j+1-g} (1<=g<T), S w_{j+1} (allreduced)
+/// Record q holds step q-1 (A,H) and column q (B); record 0 is column 0.
+struct RecLayout {
+  int T = 1;
+  int64_t s = 0, stride = 0;
+  int a_off() const { return 0; }
+  int h_off() const { return T + 1; }
+  int b_off() const { return 2 * T + 3; }
+  int sketch_off() const { return 3 * T + 3; }
+  int64_t b_len() const { return T + s; }
+  static RecLayout make(int T, int64_t s) {
+    RecLayout L;
+    L.T = T;
+    L.s = s;
+    L.stride = (3 * T + 3 + s + 3) / 4 * 4;
+    return L;
+  }
+};
+
+struct SketchDev;  // sketch.cu
+
+// ---- SpMV family (spmv.cu)
+void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y);
+void launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
+                         int nwin, double* y, double* recA);
+void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2);
+
+// ---- Arnoldi update (arnoldi.cu)
+void launch_update(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
+                   int ngram, double* rec, const RecLayout& L, double* cvec);
+void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, double* norm2);
+void launch_axpy(Context& c, double a, const double* x, double* y, int64_t n);
+void launch_scale_copy(Context& c, double a, const double* x, double* y, int64_t n);
+void launch_tallskinny(Context& c, const double* const* in_dev, int nin, const double* coef_dev, int nout,
+                       double* const* out_dev, int64_t n, double* norms2);
+
+// ---- sketches (sketch.cu): out (device, s doubles) = S (xscale * x_own),
+// the rank-local contribution of rows [row_begin, row_begin + nloc).
+void launch_sketch(Context& c, const SketchDev& S, const double* x_own, int64_t nloc, int64_t row_begin,
+                   double* out);
+void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, double xscale, int64_t nloc,
+                          int64_t row_begin, double* out);
+
+}  // namespace sdr

@@ -1,0 +1,264 @@
+// Operator construction: CSR validation (sparse.hpp:117-143) and SELL-32
+// packing, the device-side 3D convection–diffusion generator, and the 1-D
+// row-partition halo plan.
+#include "operator.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <memory>
+
+namespace sdr {
+
+void partition_halo(int world, int rank, const int64_t* rb, const int64_t* re, const int64_t* mnc, const int64_t* mxc,
+                    int64_t* recv_lo, int64_t* recv_cnt, int64_t* send_lo, int64_t* send_cnt) {
+  auto halo_of = [&](int p, int64_t* lo0, int64_t* lo1, int64_t* hi0, int64_t* hi1) {
+    *lo0 = std::min(mnc[p], rb[p]);
+    *lo1 = rb[p];
+    *hi0 = re[p];
+    *hi1 = std::max(mxc[p] + 1, re[p]);
+  };
+  auto inter = [](int64_t a0, int64_t a1, int64_t b0, int64_t b1, int64_t* lo, int64_t* cnt) {
+    const int64_t l = std::max(a0, b0), h = std::min(a1, b1);
+    if (h > l) {
+      *lo = l;
+      *cnt = h - l;
+      return true;
+    }
+    return false;
+  };
+  for (int q = 0; q < world; ++q) {
+    recv_lo[q] = recv_cnt[q] = send_lo[q] = send_cnt[q] = 0;
+    if (q == rank) continue;
+    int64_t l0, l1, h0, h1, lo, cnt;
+    halo_of(rank, &l0, &l1, &h0, &h1);
+    int hits = 0;
+    if (inter(l0, l1, rb[q], re[q], &lo, &cnt)) recv_lo[q] = lo, recv_cnt[q] = cnt, ++hits;
+    if (inter(h0, h1, rb[q], re[q], &lo, &cnt)) recv_lo[q] = lo, recv_cnt[q] = cnt, ++hits;
+    if (hits > 1) throw invalid("partition: rank " + std::to_string(q) + " overlaps both halos of rank " + std::to_string(rank));
+    halo_of(q, &l0, &l1, &h0, &h1);
+    hits = 0;
+    if (inter(l0, l1, rb[rank], re[rank], &lo, &cnt)) send_lo[q] = lo, send_cnt[q] = cnt, ++hits;
+    if (inter(h0, h1, rb[rank], re[rank], &lo, &cnt)) send_lo[q] = lo, send_cnt[q] = cnt, ++hits;
+    if (hits > 1) throw invalid("partition: rank " + std::to_string(rank) + " overlaps both halos of rank " + std::to_string(q));
+  }
+}
+
+void finish_partition(Context& c, DeviceOperator& op, int64_t min_col, int64_t max_col) {
+  const int64_t row_end = op.row_begin + op.local_rows;
+  if (op.local_rows == 0 || max_col < min_col) min_col = op.row_begin, max_col = op.row_begin - 1;
+  op.ext_begin = std::min(min_col, op.row_begin);
+  op.halo_lo = op.row_begin - op.ext_begin;
+  op.halo_hi = std::max(max_col + 1, row_end) - row_end;
+  const int W = c.world;
+  op.plan.recv_lo.assign(W, 0);
+  op.plan.recv_cnt.assign(W, 0);
+  op.plan.send_lo.assign(W, 0);
+  op.plan.send_cnt.assign(W, 0);
+  if (W <= 1) {
+    if (op.halo_lo || op.halo_hi) throw invalid("SparseMatrix: column index out of range");
+    return;
+  }
+  const int64_t mine[4] = {op.row_begin, row_end, min_col, max_col};
+  std::vector<int64_t> all(4 * static_cast<size_t>(W));
+  c.allgather_i64(mine, 4, all.data());
+  std::vector<int64_t> rb(W), re(W), mn(W), mx(W);
+  for (int q = 0; q < W; ++q) rb[q] = all[4 * q], re[q] = all[4 * q + 1], mn[q] = all[4 * q + 2], mx[q] = all[4 * q + 3];
+  partition_halo(W, c.rank, rb.data(), re.data(), mn.data(), mx.data(), op.plan.recv_lo.data(), op.plan.recv_cnt.data(),
+                 op.plan.send_lo.data(), op.plan.send_cnt.data());
+  int64_t covered = 0;
+  for (int q = 0; q < W; ++q) covered += op.plan.recv_cnt[q];
+  if (covered != op.halo_lo + op.halo_hi)
+    throw invalid("partition: halo rows of rank " + std::to_string(c.rank) + " are not owned by any rank");
+}
+
+DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int64_t row_begin, int64_t local_rows,
+                                    const int64_t* off, const int64_t* col, const double* val) {
+  if (rows < 0 || cols < 0 || local_rows < 0) throw invalid("SparseMatrix: negative dimensions");
+  if (row_begin < 0 || row_begin + local_rows > rows) throw invalid("SparseMatrix: row block outside the matrix");
+  if (!off) throw invalid("SparseMatrix: offsets size 0 does not match rows + 1 = " + std::to_string(local_rows + 1));
+  if (off[0] != 0) throw invalid("SparseMatrix: offsets must start at 0");
+  const int64_t nnz = off[local_rows];
+  if (nnz > 0 && (!col || !val)) throw invalid("SparseMatrix: offsets/columns/values sizes inconsistent");
+  int64_t mnc = std::numeric_limits<int64_t>::max(), mxc = std::numeric_limits<int64_t>::min();
+  for (int64_t r = 0; r < local_rows; ++r) {
+    if (off[r + 1] < off[r]) throw invalid("SparseMatrix: offsets decrease at row " + std::to_string(row_begin + r));
+    for (int64_t p = off[r]; p < off[r + 1]; ++p) {
+      const int64_t cc = col[p];
+      if (cc < 0 || cc >= cols)
+        throw invalid("SparseMatrix: column index " + std::to_string(cc) + " out of range in row " +
+                      std::to_string(row_begin + r));
+      if (p > off[r] && col[p - 1] >= cc)
+        throw invalid("SparseMatrix: column indices not strictly increasing in row " + std::to_string(row_begin + r));
+      if (!std::isfinite(val[p])) throw invalid("SparseMatrix: non-finite value in row " + std::to_string(row_begin + r));
+      mnc = std::min(mnc, cc);
+      mxc = std::max(mxc, cc);
+    }
+  }
+  auto op = std::make_unique<DeviceOperator>();
+  op->rows = rows;
+  op->cols = cols;
+  op->row_begin = row_begin;
+  op->local_rows = local_rows;
+  op->nnz = nnz;
+  if (!c.distributed() && rows != cols) {
+    // rectangular operators are accepted (apply checks dims); ext covers all columns
+  }
+  if (!c.distributed()) {
+    op->ext_begin = 0;
+    op->halo_lo = 0;
+    op->halo_hi = std::max<int64_t>(0, cols - local_rows);
+    op->plan.recv_lo.assign(1, 0);
+    op->plan.recv_cnt.assign(1, 0);
+    op->plan.send_lo.assign(1, 0);
+    op->plan.send_cnt.assign(1, 0);
+  } else {
+    finish_partition(c, *op, mnc, mxc);
+  }
+  const int64_t ext_len = op->halo_lo + local_rows + op->halo_hi;
+  if (ext_len > std::numeric_limits<int32_t>::max())
+    throw invalid("SparseMatrix: local extended block of " + std::to_string(ext_len) + " rows exceeds int32 indexing");
+  // SELL-32 packing
+  const int64_t nslices = (local_rows + kSlice - 1) / kSlice;
+  std::vector<int64_t> sp(static_cast<size_t>(nslices) + 1, 0);
+  for (int64_t s = 0; s < nslices; ++s) {
+    int64_t mx = 0;
+    for (int64_t r = s * kSlice; r < std::min(local_rows, (s + 1) * kSlice); ++r) mx = std::max(mx, off[r + 1] - off[r]);
+    sp[static_cast<size_t>(s) + 1] = sp[static_cast<size_t>(s)] + mx * kSlice;
+  }
+  const int64_t total = sp[static_cast<size_t>(nslices)];
+  std::vector<int32_t> hc(static_cast<size_t>(total));
+  std::vector<double> hv(static_cast<size_t>(total));
+  for (int64_t s = 0; s < nslices; ++s) {
+    const int64_t len = (sp[static_cast<size_t>(s) + 1] - sp[static_cast<size_t>(s)]) / kSlice;
+    for (int lane = 0; lane < kSlice; ++lane) {
+      const int64_t r = s * kSlice + lane;
+      const int64_t self = op->halo_lo + std::min(r, std::max<int64_t>(local_rows - 1, 0));
+      for (int64_t k = 0; k < len; ++k) {
+        const size_t dst = static_cast<size_t>(sp[static_cast<size_t>(s)] + k * kSlice + lane);
+        if (r < local_rows && k < off[r + 1] - off[r]) {
+          hc[dst] = static_cast<int32_t>(col[off[r] + k] - op->ext_begin);
+          hv[dst] = val[off[r] + k];
+        } else {
+          hc[dst] = static_cast<int32_t>(std::min<int64_t>(self, std::max<int64_t>(ext_len - 1, 0)));
+          hv[dst] = 0.0;
+        }
+      }
+    }
+  }
+  op->slice_ptr.resize(nslices + 1);
+  op->cols_idx.resize(std::max<int64_t>(total, 1));
+  op->vals.resize(std::max<int64_t>(total, 1));
+  SDR_CUDA(cudaMemcpyAsync(op->slice_ptr.get(), sp.data(), sizeof(int64_t) * sp.size(), cudaMemcpyHostToDevice, c.stream));
+  if (total) {
+    SDR_CUDA(cudaMemcpyAsync(op->cols_idx.get(), hc.data(), sizeof(int32_t) * hc.size(), cudaMemcpyHostToDevice, c.stream));
+    SDR_CUDA(cudaMemcpyAsync(op->vals.get(), hv.data(), sizeof(double) * hv.size(), cudaMemcpyHostToDevice, c.stream));
+  }
+  c.sync();
+  return op.release();
+}
+
+namespace {
+
+__global__ void k_gen_convdiff3d(int64_t nx, int64_t ny, int64_t nz, int64_t row_begin, int64_t local_rows,
+                                 int64_t ext_begin, double diag, double mx, double px, double my, double py, double mz,
+                                 double pz, int32_t* __restrict__ cols, double* __restrict__ vals) {
+  const int64_t nslices = (local_rows + kSlice - 1) / kSlice;
+  const int64_t total = nslices * kSlice;
+  const int64_t n2 = nx * ny;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < total;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = r / kSlice, lane = r % kSlice;
+    const int64_t base = s * kSlice * 7 + lane;
+    const int64_t rr = r < local_rows ? r : local_rows - 1;
+    const int64_t p = row_begin + rr;
+    const int64_t z = p / n2, y = (p / nx) % ny, x = p % nx;
+    int k = 0;
+    auto put = [&](int64_t c, double v) {
+      cols[base + k * kSlice] = static_cast<int32_t>(c - ext_begin);
+      vals[base + k * kSlice] = r < local_rows ? v : 0.0;
+      ++k;
+    };
+    // CSR order: increasing column (sparse.hpp:136-138)
+    if (z > 0) put(p - n2, mz);
+    if (y > 0) put(p - nx, my);
+    if (x > 0) put(p - 1, mx);
+    put(p, diag);
+    if (x + 1 < nx) put(p + 1, px);
+    if (y + 1 < ny) put(p + nx, py);
+    if (z + 1 < nz) put(p + n2, pz);
+    while (k < 7) put(p, 0.0);
+  }
+}
+
+__global__ void k_fill_slice_ptr(int64_t* sp, int64_t nslices, int64_t width) {
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s <= nslices;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    sp[s] = s * width;
+}
+
+}  // namespace
+
+DeviceOperator* create_operator_convdiff3d(Context& c, int64_t nx, int64_t ny, int64_t nz, double bx, double by,
+                                           double bz, int64_t z0, int64_t z1) {
+  if (nx < 1 || ny < 1 || nz < 1) throw invalid("gen_convdiff3d: grid sides must be positive");
+  if (z0 < 0 || z1 > nz || z0 > z1) throw invalid("gen_convdiff3d: bad z-slab [" + std::to_string(z0) + ", " + std::to_string(z1) + ")");
+  const int64_t n2 = nx * ny, N = n2 * nz;
+  auto op = std::make_unique<DeviceOperator>();
+  op->rows = op->cols = N;
+  op->row_begin = z0 * n2;
+  op->local_rows = (z1 - z0) * n2;
+  // coefficients exactly as the host generator (problems.hpp:70-88 convention), h_d = 1/(n_d + 1)
+  const double hx = static_cast<double>((nx + 1) * (nx + 1)), hy = static_cast<double>((ny + 1) * (ny + 1)),
+               hz = static_cast<double>((nz + 1) * (nz + 1));
+  const double cx = bx * static_cast<double>(nx + 1) / 2.0, cy = by * static_cast<double>(ny + 1) / 2.0,
+               cz = bz * static_cast<double>(nz + 1) / 2.0;
+  const double coef[6] = {-hx - cx, -hx + cx, -hy - cy, -hy + cy, -hz - cz, -hz + cz};
+  const double diag = nx == ny && ny == nz ? 6.0 * hx : 2.0 * hx + 2.0 * hy + 2.0 * hz;
+  // stored nonzeros (from_triplets drops exact zeros)
+  const int64_t zl = z1 - z0;
+  const int64_t cnt[6] = {(nx - 1) * ny * zl, (nx - 1) * ny * zl, nx * (ny - 1) * zl, nx * (ny - 1) * zl,
+                          zl == 0 ? 0 : (z1 - std::max<int64_t>(z0, 1)) * n2,
+                          zl == 0 ? 0 : (std::min<int64_t>(z1, nz - 1) - z0) * n2};
+  op->nnz = op->local_rows;
+  for (int d = 0; d < 6; ++d)
+    if (coef[d] != 0.0) op->nnz += std::max<int64_t>(cnt[d], 0);
+  const int64_t mnc = z0 > 0 ? op->row_begin - n2 : op->row_begin;
+  const int64_t mxc = z1 < nz ? op->row_begin + op->local_rows - 1 + n2 : op->row_begin + op->local_rows - 1;
+  if (c.distributed()) {
+    finish_partition(c, *op, mnc, mxc);
+  } else {
+    op->ext_begin = 0;
+    op->halo_lo = op->halo_hi = 0;
+    if (z0 != 0 || z1 != nz) throw invalid("gen_convdiff3d: a single-GPU context needs the full grid");
+    op->plan.recv_lo.assign(1, 0);
+    op->plan.recv_cnt.assign(1, 0);
+    op->plan.send_lo.assign(1, 0);
+    op->plan.send_cnt.assign(1, 0);
+  }
+  if (op->halo_lo + op->local_rows + op->halo_hi > std::numeric_limits<int32_t>::max())
+    throw invalid("gen_convdiff3d: local block exceeds int32 indexing");
+  const int64_t nslices = (op->local_rows + kSlice - 1) / kSlice;
+  op->slice_ptr.resize(nslices + 1);
+  op->cols_idx.resize(std::max<int64_t>(nslices * kSlice * 7, 1));
+  op->vals.resize(std::max<int64_t>(nslices * kSlice * 7, 1));
+  if (nslices > 0) {
+    const int g = static_cast<int>(std::min<int64_t>((nslices * kSlice + 255) / 256, 148 * 16));
+    k_fill_slice_ptr<<<g, 256, 0, c.stream>>>(op->slice_ptr.get(), nslices, kSlice * 7);
+    SDR_KERNEL_CHECK();
+    k_gen_convdiff3d<<<g, 256, 0, c.stream>>>(nx, ny, nz, op->row_begin, op->local_rows, op->ext_begin, diag, coef[0],
+                                             coef[1], coef[2], coef[3], coef[4], coef[5], op->cols_idx.get(),
+                                             op->vals.get());
+    SDR_KERNEL_CHECK();
+  }
+  c.sync();
+  return op.release();
+}
+
+void operator_apply(Context& c, const DeviceOperator& op, double* x_buf, double* y) {
+  const VecLayout L = op.layout();
+  c.halo_exchange(op.plan, x_buf + L.ext_shift(), op.ext_begin, x_buf + L.own_off, op.row_begin);
+  launch_spmv(c, op.view(), x_buf + L.ext_shift(), y);
+}
+
+}  // namespace sdr

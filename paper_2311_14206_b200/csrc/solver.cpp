@@ -1,0 +1,760 @@
+// GMRES-SDR driver: solve_cycle / solve / solve_sequence semantics of the
+// reference (solver.hpp:128-459) with every N-length operation on the GPU.
+//
+// Device pipeline per Arnoldi step j (single stream, no host round trip
+// inside a step):   [halo(w_j)] K1 spmv+dots [allreduce A] K2 update
+//                   K3 sketch [allreduce B] D2H(record j) event
+// The host consumes step records strictly in order (incremental QR, LS
+// solve, trigger test) while the device already runs up to `kLookahead`
+// steps ahead: the Arnoldi recurrence never depends on the least-squares
+// result, so speculative steps are either consumed exactly as the
+// reference would take them or discarded at cycle end.
+#include "solver.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+namespace sdr {
+
+namespace {
+constexpr int kLookahead = 2;
+
+struct Workspace {
+  VecLayout lay;
+  i64 m = -1, s = -1;
+  int T = 0;
+  RecLayout RL;
+  DeviceBuffer<double> V, y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef;
+  DeviceBuffer<const double*> inptr;
+  DeviceBuffer<double*> outptr;
+  PinnedBuffer<double> hrec, hscal, hcoef;
+  PinnedBuffer<const double*> hin;
+  PinnedBuffer<double*> hout;
+  std::vector<cudaEvent_t> ev;
+  ~Workspace() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  double* Vcol(i64 i) const { return V.get() + i * lay.ld + lay.own_off; }
+  double* Vbuf(i64 i) const { return V.get() + i * lay.ld; }
+};
+
+Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
+  auto w = std::static_pointer_cast<Workspace>(c.workspace);
+  if (!w) {
+    w = std::make_shared<Workspace>();
+    c.workspace = w;
+  }
+  const bool relayout = w->lay.ld != lay.ld || w->lay.own_off != lay.own_off || w->lay.nloc != lay.nloc ||
+                        w->lay.halo_lo != lay.halo_lo || w->lay.halo_hi != lay.halo_hi;
+  if (relayout || m > w->m || s != w->s || T != w->T) {
+    const i64 mm = std::max(m, w->m);
+    w->lay = lay;
+    w->m = mm;
+    w->s = s;
+    w->T = T;
+    w->RL = RecLayout::make(T, s);
+    w->V.resize((mm + 1) * lay.ld);
+    w->rec.resize((mm + 2) * w->RL.stride);
+    SDR_CUDA(cudaMemsetAsync(w->rec.get(), 0, sizeof(double) * static_cast<size_t>(w->rec.size()), c.stream));
+    SDR_CUDA(cudaMemsetAsync(w->V.get(), 0, sizeof(double) * static_cast<size_t>(w->V.size()), c.stream));
+    w->cvec.resize(mm + 2);
+    w->hrec.ensure((mm + 2) * w->RL.stride);
+    while (static_cast<i64>(w->ev.size()) < mm + 2) {
+      cudaEvent_t e;
+      SDR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      w->ev.push_back(e);
+    }
+  }
+  const i64 nl = std::max<i64>(lay.nloc, 1);
+  w->y.ensure(nl);
+  w->corr.ensure(lay.ld);
+  if (relayout) SDR_CUDA(cudaMemsetAsync(w->corr.get(), 0, sizeof(double) * static_cast<size_t>(lay.ld), c.stream));
+  w->r0.ensure(nl);
+  w->rnew.ensure(nl);
+  w->x.ensure(nl);
+  w->tmp.ensure(lay.ld);
+  w->scal.ensure(64);
+  w->hscal.ensure(64);
+  return *w;
+}
+
+void ensure_ptrs(Workspace& w, i64 nin, i64 nout) {
+  w.inptr.ensure(nin);
+  w.outptr.ensure(nout);
+  w.coef.ensure(nin * std::max<i64>(nout, 1));
+  w.hin.ensure(nin);
+  w.hout.ensure(nout);
+  w.hcoef.ensure(nin * std::max<i64>(nout, 1));
+}
+
+/// out_o = sum_i coef(i, o) * in_i through the K4 kernel (chunks of 32 outputs).
+void tallskinny(Context& c, Workspace& w, const std::vector<const double*>& in, const HMat& coef /* nin x nout */,
+                const std::vector<double*>& out, i64 n, double* norms2_dev) {
+  const i64 nin = static_cast<i64>(in.size()), nout = static_cast<i64>(out.size());
+  if (nout == 0) return;
+  if (nin == 0) {
+    for (auto* o : out) SDR_CUDA(cudaMemsetAsync(o, 0, sizeof(double) * static_cast<size_t>(n), c.stream));
+    if (norms2_dev) SDR_CUDA(cudaMemsetAsync(norms2_dev, 0, sizeof(double) * static_cast<size_t>(nout), c.stream));
+    return;
+  }
+  c.sync();  // staging buffers are reused
+  ensure_ptrs(w, nin, nout);
+  for (i64 i = 0; i < nin; ++i) w.hin.get()[i] = in[static_cast<size_t>(i)];
+  SDR_CUDA(cudaMemcpyAsync(w.inptr.get(), w.hin.get(), sizeof(void*) * nin, cudaMemcpyHostToDevice, c.stream));
+  for (i64 o0 = 0; o0 < nout; o0 += 32) {
+    const i64 no = std::min<i64>(32, nout - o0);
+    if (o0 > 0) c.sync();
+    for (i64 i = 0; i < nin; ++i)
+      for (i64 o = 0; o < no; ++o) w.hcoef.get()[i * no + o] = coef(i, o0 + o);
+    for (i64 o = 0; o < no; ++o) w.hout.get()[o] = out[static_cast<size_t>(o0 + o)];
+    SDR_CUDA(cudaMemcpyAsync(w.coef.get(), w.hcoef.get(), sizeof(double) * nin * no, cudaMemcpyHostToDevice, c.stream));
+    SDR_CUDA(cudaMemcpyAsync(w.outptr.get(), w.hout.get(), sizeof(void*) * no, cudaMemcpyHostToDevice, c.stream));
+    launch_tallskinny(c, w.inptr.get(), static_cast<int>(nin), w.coef.get(), static_cast<int>(no), w.outptr.get(), n,
+                      norms2_dev ? norms2_dev + o0 : nullptr);
+  }
+}
+
+struct HostKrylov {
+  HMat H, SV, SAV;
+  std::vector<double> cv;  // device scale of each stored column
+  i64 j = 0;
+  double r0_norm = 0.0;
+  bool breakdown = false;
+};
+
+struct CycleOut {
+  double residual_norm = 0, sres = 0, entry_norm = 0, sketched_entry = 0;
+  i64 steps = 0;
+  bool converged = false, breakdown = false, have_correction = false;
+  double safety = 1.0;
+};
+
+struct StepEvent {  // mirrors sdr_iteration_event in the C-ABI
+  int32_t cycle;
+  int64_t step, iteration;
+  double sres, new_basis_sketch_norm;
+  const double* y;
+  int64_t y_len, space_dim;
+};
+struct ResidualEvent {
+  int32_t cycle;
+  int64_t iteration;
+  double sres, true_residual;
+};
+
+double d2h_scalar(Context& c, Workspace& w, const double* dev) {
+  SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  return w.hscal.get()[0];
+}
+
+void update_recycle(Context& c, Workspace& w, const HostKrylov& st, Recycle& sp, i64 k, double rank_tol,
+                    Counters& cnt, std::vector<std::string>* notes) {  // recycle.hpp:226-289
+  const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
+  if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
+  HMat SAW(s, kh + j), SW(s, kh + j);
+  for (i64 q = 0; q < kh; ++q) {
+    std::copy(sp.SAU.col(q), sp.SAU.col(q) + s, SAW.col(q));
+    std::copy(sp.SU.col(q), sp.SU.col(q) + s, SW.col(q));
+  }
+  for (i64 i = 0; i < j; ++i) {
+    std::copy(st.SAV.col(i), st.SAV.col(i) + s, SAW.col(kh + i));
+    std::copy(st.SV.col(i), st.SV.col(i) + s, SW.col(kh + i));
+  }
+  Harmonic hp = harmonic_extract(SAW, SW, k, rank_tol);
+  if (notes) {
+    if (hp.rank_limited)
+      notes->push_back("deflation space limited to pencil rank " + std::to_string(hp.rank) + " (requested " +
+                       std::to_string(hp.k_requested) + ")");
+    if (hp.pair_extended) notes->push_back("deflation space grew by one to keep a conjugate pair together");
+  }
+  const int prov = sp.empty() ? 1 : sp.provenance;
+  const i64 ke = hp.k_eff;
+  if (ke == 0) {
+    sp.clear();
+    sp.provenance = prov;
+    return;
+  }
+  sp.ensure(w.lay.nloc, std::max<i64>(ke, kh));
+  // device: U_new = V(:,0:j) C_bot + U C_top with lazy scales folded in
+  std::vector<const double*> in;
+  HMat coef(kh + j, ke);
+  for (i64 i = 0; i < j; ++i) {
+    in.push_back(w.Vcol(i));
+    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
+  }
+  for (i64 p = 0; p < kh; ++p) {
+    in.push_back(sp.col(p));
+    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
+  }
+  const int other = 1 - sp.cur;
+  std::vector<double*> out;
+  for (i64 q = 0; q < ke; ++q) out.push_back(sp.buf[other].get() + q * sp.ld);
+  tallskinny(c, w, in, coef, out, w.lay.nloc, w.scal.get());
+  c.allreduce_sum(w.scal.get(), ke);
+  SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), w.scal.get(), sizeof(double) * ke, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  // host: SU_new, SAU_new (recycle.hpp:257-265)
+  HMat SU(s, ke), SAU(s, ke);
+  for (i64 q = 0; q < ke; ++q) {
+    for (i64 i = 0; i < j; ++i) {
+      const double cf = hp.coeffs(kh + i, q);
+      for (i64 r = 0; r < s; ++r) {
+        SU(r, q) += st.SV(r, i) * cf;
+        SAU(r, q) += st.SAV(r, i) * cf;
+      }
+    }
+    for (i64 p = 0; p < kh; ++p) {
+      const double cf = hp.coeffs(p, q);
+      for (i64 r = 0; r < s; ++r) {
+        SU(r, q) += sp.SU(r, p) * cf;
+        SAU(r, q) += sp.SAU(r, p) * cf;
+      }
+    }
+  }
+  sp.cur = other;
+  sp.slot.resize(static_cast<size_t>(ke));
+  sp.uscale.resize(static_cast<size_t>(ke));
+  for (i64 q = 0; q < ke; ++q) sp.slot[static_cast<size_t>(q)] = static_cast<int>(q);
+  sp.SU = std::move(SU);
+  sp.SAU = std::move(SAU);
+  sp.provenance = prov;
+  std::vector<i64> bad;
+  for (i64 q = 0; q < ke; ++q) {  // recycle.hpp:269-286
+    const double nrm = std::sqrt(w.hscal.get()[q]);
+    ++cnt.inner_products;
+    if (nrm == 0.0 || !std::isfinite(nrm)) {
+      bad.push_back(q);
+      sp.uscale[static_cast<size_t>(q)] = 0.0;
+      continue;
+    }
+    sp.uscale[static_cast<size_t>(q)] = 1.0 / nrm;
+    for (i64 r = 0; r < s; ++r) {
+      sp.SU(r, q) /= nrm;
+      sp.SAU(r, q) /= nrm;
+    }
+  }
+  if (!bad.empty()) {
+    sp.drop_columns(bad);
+    if (notes) notes->push_back("dropped " + std::to_string(bad.size()) + " degenerate deflation columns after the harmonic update");
+  }
+  if (sp.empty()) sp.provenance = 0;
+}
+
+/// Device Arnoldi pipeline + host bookkeeping of init_krylov / arnoldi_step
+/// (arnoldi.hpp:47-119): the device produces step records, the host turns
+/// them into H, SV, SAV exactly as the reference's KrylovState.
+struct ArnoldiPipeline {
+  Context& c;
+  Workspace& w;
+  const DeviceOperator& A;
+  const SketchDev& S;
+  i64 t, m;
+  double breakdown_tol;
+  Counters& cnt;
+  HostKrylov st;
+  i64 issued = 0;
+  double wait_ms = 0.0;
+
+  void init(const double* r0) {
+    const VecLayout& lay = w.lay;
+    const RecLayout& RL = w.RL;
+    const i64 s = S.s, R = RL.stride;
+    launch_copy_norm(c, r0, w.Vcol(0), lay.nloc, w.rec.get() + RL.b_off());
+    launch_sketch(c, S, w.Vcol(0), lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
+    c.allreduce_sum(w.rec.get() + RL.b_off(), RL.b_len());
+    SDR_CUDA(cudaMemcpyAsync(w.hrec.get(), w.rec.get(), sizeof(double) * R, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    st.r0_norm = std::sqrt(w.hrec.get()[RL.b_off()]);
+    ++cnt.inner_products;
+    if (st.r0_norm == 0.0) throw domain("init_krylov: zero initial residual (already converged)");
+    ++cnt.sketch_applies;
+    st.H = HMat(m + 1, m);
+    st.SV = HMat(s, m + 1);
+    st.SAV = HMat(s, m);
+    st.cv.assign(static_cast<size_t>(m + 1), 0.0);
+    const double* sk = w.hrec.get() + RL.sketch_off();
+    for (i64 r = 0; r < s; ++r) st.SV(r, 0) = sk[r] / st.r0_norm;
+    st.cv[0] = 1.0 / st.r0_norm;
+    issued = 0;
+  }
+
+  void enqueue(i64 j) {
+    const VecLayout& lay = w.lay;
+    const RecLayout& RL = w.RL;
+    const i64 R = RL.stride;
+    const int T = RL.T;
+    const int nwin = static_cast<int>(std::min<i64>(t, j + 1));
+    const int ngram = static_cast<int>(std::min<i64>(T - 1, j + 1));
+    c.halo_exchange(A.plan, w.Vbuf(j) + lay.ext_shift(), A.ext_begin, w.Vcol(j), A.row_begin);
+    double* recj = w.rec.get() + (j + 1) * R;
+    launch_spmv_arnoldi(c, A.view(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off());
+    c.allreduce_sum(recj + RL.a_off(), T + 1);
+    launch_update(c, w.y.get(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get());
+    launch_sketch(c, S, w.Vcol(j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
+    c.allreduce_sum(recj + RL.b_off(), RL.b_len());
+    SDR_CUDA(cudaMemcpyAsync(w.hrec.get() + (j + 1) * R, recj, sizeof(double) * R, cudaMemcpyDeviceToHost, c.stream));
+    SDR_CUDA(cudaEventRecord(w.ev[static_cast<size_t>(j + 1)], c.stream));
+  }
+
+  /// Keeps up to kLookahead speculative steps in flight, then consumes step
+  /// st.j; returns true on lucky breakdown.
+  bool step() {
+    if (st.breakdown) throw logic("arnoldi_step: basis already broke down");
+    if (st.j >= m) throw logic("arnoldi_step: step capacity exhausted");
+    const i64 j = st.j;
+    while (issued < m && issued <= j + kLookahead) enqueue(issued++);
+    const auto tw0 = std::chrono::steady_clock::now();
+    SDR_CUDA(cudaEventSynchronize(w.ev[static_cast<size_t>(j + 1)]));
+    wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count();
+    const RecLayout& RL = w.RL;
+    const int T = RL.T;
+    const i64 s = S.s;
+    const double* rj = w.hrec.get() + (j + 1) * RL.stride;
+    const int nwin = static_cast<int>(std::min<i64>(t, j + 1));
+    const i64 i0 = j - nwin + 1;
+    const double norm_before = rj[RL.h_off()];
+    for (int d = 0; d < nwin; ++d) st.H(j - d, j) = rj[RL.h_off() + 1 + d];
+    st.cv[static_cast<size_t>(j)] = rj[RL.h_off() + 1 + T];
+    const double h_next = std::sqrt(rj[RL.b_off()]);
+    ++cnt.matvecs;
+    cnt.inner_products += 2 + nwin;
+    bool brk = false;
+    if (h_next <= breakdown_tol * norm_before) {  // arnoldi.hpp:101-108
+      st.H(j + 1, j) = 0.0;
+      for (i64 r = 0; r < s; ++r) {
+        double acc = 0.0;
+        for (i64 i = i0; i <= j; ++i) acc += st.SV(r, i) * st.H(i, j);
+        st.SAV(r, j) = acc;
+      }
+      st.breakdown = true;
+      brk = true;
+    } else {
+      st.H(j + 1, j) = h_next;
+      st.cv[static_cast<size_t>(j + 1)] = 1.0 / h_next;
+      const double* sk = rj + RL.sketch_off();
+      for (i64 r = 0; r < s; ++r) st.SV(r, j + 1) = sk[r] / h_next;
+      ++cnt.sketch_applies;
+      for (i64 r = 0; r < s; ++r) {  // arnoldi.hpp:115
+        double acc = 0.0;
+        for (i64 i = i0; i <= j + 1; ++i) acc += st.SV(r, i) * st.H(i, j);
+        st.SAV(r, j) = acc;
+      }
+    }
+    st.j = j + 1;
+    return brk;
+  }
+};
+
+/// One restart cycle (solver.hpp:128-254). r0 is the device residual (own part).
+CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const SketchDev& S, const Config& cfg,
+                     const double* r0, Recycle& space, double tol_abs, double safety_in, Counters& cnt, Report& rep,
+                     const Callbacks* cb, int cycle_index, i64 iteration_base) {
+  CycleOut out;
+  out.safety = std::max(1.0, safety_in);
+  const VecLayout& lay = w.lay;
+  const i64 s = S.s, m = cfg.m;
+  const auto t0 = std::chrono::steady_clock::now();
+
+  ArnoldiPipeline ap{c, w, A, S, cfg.t, m, cfg.breakdown_tol, cnt, HostKrylov{}};
+  ap.init(r0);
+  HostKrylov& st = ap.st;
+  out.entry_norm = st.r0_norm;
+  std::vector<double> sr0(static_cast<size_t>(s));
+  for (i64 r = 0; r < s; ++r) sr0[static_cast<size_t>(r)] = st.SV(r, 0) * st.r0_norm;
+  out.sketched_entry = hnorm(sr0.data(), s);
+
+  // ---- seed the QR with the deflation block (solver.hpp:144-159)
+  auto qr = std::make_unique<HostQR>(s, space.dim() + m, cfg.rank_tol);
+  for (;;) {
+    std::vector<i64> bad;
+    for (i64 q = 0; q < space.dim(); ++q)
+      if (qr->append(space.SAU.col(q), s).rank_deficient) bad.push_back(q);
+    if (bad.empty()) break;
+    space.drop_columns(bad);
+    rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": dropped " + std::to_string(bad.size()) +
+                        " deflation columns with rank-deficient sketched images");
+    qr = std::make_unique<HostQR>(s, space.dim() + m, cfg.rank_tol);
+    if (space.empty()) break;
+  }
+  const i64 k_hat = space.dim();
+  qr->set_rhs(sr0.data(), s);
+
+  std::vector<double> y(static_cast<size_t>(k_hat + m), 0.0);
+  double sres = out.sketched_entry;
+  bool done = false;
+  while (!done && st.j < m && !st.breakdown) {  // solver.hpp:165-216
+    const bool step_breakdown = ap.step();
+    const i64 jj = st.j;
+    const auto info = qr->append(st.SAV.col(jj - 1), s);
+    if (info.rank_deficient) {
+      qr->exclude(info.column);
+      rep.notes.push_back("cycle " + std::to_string(cycle_index) + ", step " + std::to_string(jj) +
+                          ": sketched basis column rank-deficient; excluded from the least-squares problem");
+    }
+    sres = qr->solve_cached(y.data());
+    const i64 p = qr->cols();
+    const i64 global_iter = iteration_base + jj;
+    rep.sketched.emplace_back(global_iter, sres);
+    if (cb && cb->on_iteration) {
+      StepEvent ev{cycle_index, jj, global_iter, sres, step_breakdown ? 1.0 : hnorm(st.SV.col(jj), s), y.data(), p,
+                   k_hat};
+      cb->on_iteration(&ev, cb->user);
+    }
+    const bool last = jj == m || st.breakdown;
+    if (sres < tol_abs / out.safety || last) {
+      // correction = V(:,0:j) y_tail + U y_head (solver.hpp:197-198), on the device
+      std::vector<const double*> in;
+      HMat coef(jj + k_hat, 1);
+      for (i64 i = 0; i < jj; ++i) {
+        in.push_back(w.Vcol(i));
+        coef(i, 0) = y[static_cast<size_t>(k_hat + i)] * st.cv[static_cast<size_t>(i)];
+      }
+      for (i64 q = 0; q < k_hat; ++q) {
+        in.push_back(space.col(q));
+        coef(jj + q, 0) = y[static_cast<size_t>(q)] * space.uscale[static_cast<size_t>(q)];
+      }
+      double* corr_own = w.corr.get() + lay.own_off;
+      tallskinny(c, w, in, coef, {corr_own}, lay.nloc, nullptr);
+      c.halo_exchange(A.plan, w.corr.get() + lay.ext_shift(), A.ext_begin, corr_own, A.row_begin);
+      launch_residual(c, A.view(), w.corr.get() + lay.ext_shift(), r0, w.rnew.get(), w.scal.get());
+      c.allreduce_sum(w.scal.get(), 1);
+      out.residual_norm = std::sqrt(d2h_scalar(c, w, w.scal.get()));
+      out.have_correction = true;
+      ++cnt.matvecs;
+      ++cnt.inner_products;
+      rep.truth.emplace_back(global_iter, out.residual_norm);
+      if (cb && cb->on_residual) {
+        ResidualEvent ev{cycle_index, global_iter, sres, out.residual_norm};
+        cb->on_residual(&ev, cb->user);
+      }
+      if (out.residual_norm < tol_abs) {
+        out.converged = true;
+        done = true;
+      } else {
+        if (sres > 0.0) out.safety = std::max(out.safety, out.residual_norm / sres);
+        if (last) done = true;
+      }
+    }
+  }
+  c.sync();  // drain speculative steps before the buffers are reused
+  out.steps = st.j;
+  out.sres = sres;
+  out.breakdown = st.breakdown;
+  rep.host_wait_ms += ap.wait_ms;
+
+  CycleStat cs;
+  cs.steps = st.j;
+  cs.entry_residual = out.entry_norm;
+  cs.sketched_entry = out.sketched_entry;
+  cs.exit_sres = sres;
+  cs.exit_residual = out.residual_norm;
+  cs.safety_after = out.safety;
+  if (st.j >= 1 && !st.breakdown) {
+    HMat B(s, st.j + 1);
+    std::copy(st.SV.a.begin(), st.SV.a.begin() + s * (st.j + 1), B.a.begin());
+    cs.basis_cond = cond2(B);
+  }
+  rep.cycle_stats.push_back(cs);
+
+  if (cfg.k > 0 && st.j >= 1) {  // solver.hpp:242-252
+    std::vector<std::string> notes;
+    update_recycle(c, w, st, space, cfg.k, cfg.rank_tol, cnt, &notes);
+    rep.cycle_stats.back().deflation_rank = space.dim();
+    for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
+  } else if (cfg.k == 0) {
+    space.clear();
+  }
+  rep.device_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return out;
+}
+
+}  // namespace
+
+void krylov_run(Context& c, const DeviceOperator& A, const SketchDev& S, const double* r0, i64 t, i64 m, i64 steps,
+                double breakdown_tol, double* V, double* H, double* SV, double* SAV, i64* j_out, int* breakdown,
+                double* r0_norm, i64* counters3) {
+  if (t < 1) throw invalid("init_krylov: truncation window must be at least 1");
+  if (m < 1) throw invalid("init_krylov: m_max must be at least 1");
+  if (S.n != A.rows)
+    throw invalid("init_krylov: residual length " + std::to_string(A.rows) + " does not match sketch input " +
+                  std::to_string(S.n));
+  if (std::min(t, m) > 33) throw invalid("init_krylov: window min(t, m) exceeds the device limit of 33");
+  init_host_blas();
+  const VecLayout lay = A.layout();
+  Workspace& w = workspace(c, lay, m, S.s, static_cast<int>(std::min(t, m)));
+  Counters cnt;
+  ArnoldiPipeline ap{c, w, A, S, t, m, breakdown_tol, cnt, HostKrylov{}};
+  ap.init(r0);
+  for (i64 q = 0; q < steps && !ap.st.breakdown && ap.st.j < m; ++q) ap.step();
+  c.sync();
+  const HostKrylov& st = ap.st;
+  const i64 s = S.s;
+  if (V) {
+    const i64 cols = st.breakdown ? st.j : st.j + 1;
+    DeviceBuffer<double> tmp(std::max<i64>(lay.nloc * (m + 1), 1));
+    SDR_CUDA(cudaMemsetAsync(tmp.get(), 0, sizeof(double) * static_cast<size_t>(lay.nloc * (m + 1)), c.stream));
+    for (i64 i = 0; i < cols; ++i)
+      launch_scale_copy(c, st.cv[static_cast<size_t>(i)], w.Vcol(i), tmp.get() + i * lay.nloc, lay.nloc);
+    SDR_CUDA(cudaMemcpyAsync(V, tmp.get(), sizeof(double) * static_cast<size_t>(lay.nloc * (m + 1)), cudaMemcpyDefault,
+                             c.stream));
+    c.sync();
+  }
+  if (H) std::copy(st.H.a.begin(), st.H.a.end(), H);
+  if (SV) std::copy(st.SV.a.begin(), st.SV.a.end(), SV);
+  if (SAV) std::copy(st.SAV.a.begin(), st.SAV.a.end(), SAV);
+  (void)s;
+  if (j_out) *j_out = st.j;
+  if (breakdown) *breakdown = st.breakdown ? 1 : 0;
+  if (r0_norm) *r0_norm = st.r0_norm;
+  if (counters3) {
+    counters3[0] = cnt.matvecs;
+    counters3[1] = cnt.inner_products;
+    counters3[2] = cnt.sketch_applies;
+  }
+}
+
+void Config::validate() const {  // solver.hpp:61-78
+  if (m < 1) throw invalid("SolverConfig: m must be at least 1");
+  if (t < 1) throw invalid("SolverConfig: t must be at least 1");
+  if (k < 0 || k >= m)
+    throw invalid("SolverConfig: need 0 <= k < m, got k = " + std::to_string(k) + ", m = " + std::to_string(m));
+  if (s < 2 * (m + k))
+    throw invalid("SolverConfig: sketch size s = " + std::to_string(s) + " is below 2 (m + k) = " +
+                  std::to_string(2 * (m + k)));
+  if (!(tol > 0.0 && tol < 1.0)) throw invalid("SolverConfig: tol must lie in (0, 1)");
+  if (!(safety_init >= 1.0)) throw invalid("SolverConfig: safety_init must be at least 1");
+  if (max_restarts < 1) throw invalid("SolverConfig: max_restarts must be at least 1");
+  if (!(rank_tol >= 0.0)) throw invalid("SolverConfig: rank_tol must be >= 0");
+  if (!(breakdown_tol >= 0.0)) throw invalid("SolverConfig: breakdown_tol must be >= 0");
+}
+
+void Recycle::drop_columns(const std::vector<i64>& cols) {  // recycle.hpp:48-71
+  if (cols.empty()) return;
+  std::vector<bool> drop(static_cast<size_t>(dim()), false);
+  for (i64 cc : cols) {
+    if (cc < 0 || cc >= dim()) throw invalid("RecycleSpace::drop_columns: no column " + std::to_string(cc));
+    drop[static_cast<size_t>(cc)] = true;
+  }
+  std::vector<int> ns;
+  std::vector<double> nu;
+  i64 keep = 0;
+  for (i64 q = 0; q < dim(); ++q)
+    if (!drop[static_cast<size_t>(q)]) ++keep;
+  HMat su(s, keep), sau(s, keep);
+  i64 o = 0;
+  for (i64 q = 0; q < dim(); ++q) {
+    if (drop[static_cast<size_t>(q)]) continue;
+    ns.push_back(slot[static_cast<size_t>(q)]);
+    nu.push_back(uscale[static_cast<size_t>(q)]);
+    std::copy(SU.col(q), SU.col(q) + s, su.col(o));
+    std::copy(SAU.col(q), SAU.col(q) + s, sau.col(o));
+    ++o;
+  }
+  slot.swap(ns);
+  uscale.swap(nu);
+  SU = std::move(su);
+  SAU = std::move(sau);
+}
+
+void Recycle::ensure(i64 nloc_, i64 capacity) {
+  if (nloc != nloc_ && !empty()) throw invalid("solve: recycle space has " + std::to_string(nloc) + " local rows but the operator block has " + std::to_string(nloc_));
+  const i64 ld_new = round_up(std::max<i64>(nloc_, 1), 32);
+  if (nloc == nloc_ && ld == ld_new && capacity <= cap) return;
+  const i64 cap_new = std::max(capacity, cap);
+  DeviceBuffer<double> nb[2];
+  nb[0].resize(ld_new * cap_new);
+  nb[1].resize(ld_new * cap_new);
+  for (i64 q = 0; q < dim(); ++q)
+    SDR_CUDA(cudaMemcpy(nb[0].get() + q * ld_new, col(q), sizeof(double) * static_cast<size_t>(nloc_), cudaMemcpyDeviceToDevice));
+  for (i64 q = 0; q < dim(); ++q) slot[static_cast<size_t>(q)] = static_cast<int>(q);
+  buf[0] = std::move(nb[0]);
+  buf[1] = std::move(nb[1]);
+  cur = 0;
+  nloc = nloc_;
+  ld = ld_new;
+  cap = cap_new;
+}
+
+SketchDev* create_sketch(Context& c, int kind, i64 n, i64 s, std::uint64_t seed, i64 zeta) {
+  auto S = std::make_unique<SketchDev>();
+  S->kind = kind;
+  S->n = n;
+  S->s = s;
+  S->seed = seed;
+  S->zeta = zeta;
+  if (kind == kIdentity) {
+    if (n < 1) throw invalid("SketchOperator::identity: n must be positive");
+    S->s = n;
+    return S.release();
+  }
+  if (kind == kSparseSign) {
+    if (n < 1 || s < 1 || zeta < 1 || zeta > s)
+      throw invalid("SketchOperator::sparse_sign: need n >= 1 and 1 <= zeta <= s, got n = " + std::to_string(n) +
+                    ", s = " + std::to_string(s) + ", zeta = " + std::to_string(zeta));
+    if (s > 880) throw invalid("SketchOperator::sparse_sign: device kernel supports s <= 880");
+    std::mt19937_64 eng(seed);
+    S->key = eng();
+    return S.release();
+  }
+  if (n < 2 || s < 1 || s >= n)
+    throw invalid("SketchOperator: need 1 <= s < n, got s = " + std::to_string(s) + ", n = " + std::to_string(n));
+  if (s > 4096) throw invalid("SketchOperator: device SRDCT supports s <= 4096");
+  if (n >= (int64_t{1} << 31)) throw invalid("SketchOperator: device SRDCT supports n < 2^31");
+  SrdctHost h = make_srdct_host(n, s, seed);
+  S->scale = std::sqrt(static_cast<double>(n) / static_cast<double>(s));
+  std::vector<double> rs(static_cast<size_t>(s));
+  for (i64 q = 0; q < s; ++q) {
+    const double alpha = h.rows[static_cast<size_t>(q)] == 0 ? std::sqrt(1.0 / static_cast<double>(n))
+                                                             : std::sqrt(2.0 / static_cast<double>(n));
+    rs[static_cast<size_t>(q)] = alpha * S->scale;
+  }
+  S->sign_bits.resize(static_cast<i64>(h.sign_bits.size()));
+  S->rows.resize(s);
+  S->row_scale.resize(s);
+  SDR_CUDA(cudaMemcpy(S->sign_bits.get(), h.sign_bits.data(), sizeof(uint32_t) * h.sign_bits.size(), cudaMemcpyHostToDevice));
+  SDR_CUDA(cudaMemcpy(S->rows.get(), h.rows.data(), sizeof(int64_t) * h.rows.size(), cudaMemcpyHostToDevice));
+  SDR_CUDA(cudaMemcpy(S->row_scale.get(), rs.data(), sizeof(double) * rs.size(), cudaMemcpyHostToDevice));
+  S->rows_host = std::move(h.rows);
+  S->sign_bits_host = std::move(h.sign_bits);
+  return S.release();
+}
+
+void sketch_apply(Context& c, const SketchDev& S, const double* x, i64 nloc, i64 row_begin, double* out_host) {
+  DeviceBuffer<double> out(S.s);
+  launch_sketch(c, S, x, nloc, row_begin, out.get());
+  c.allreduce_sum(out.get(), S.s);
+  SDR_CUDA(cudaMemcpyAsync(out_host, out.get(), sizeof(double) * static_cast<size_t>(S.s), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+}
+
+void refresh_recycle(Context& c, Recycle& sp, const DeviceOperator& A, const SketchDev& S, bool exact, Counters* cnt) {
+  if (sp.empty()) return;  // recycle.hpp:297-318
+  if (sp.n != A.cols)
+    throw invalid("refresh_for_new_matrix: space has " + std::to_string(sp.n) + " rows but the operator takes " +
+                  std::to_string(A.cols));
+  if (!exact) {
+    sp.provenance = 4;
+    return;
+  }
+  const VecLayout lay = A.layout();
+  DeviceBuffer<double> ubuf(lay.ld), au(std::max<i64>(lay.nloc, 1)), sk(S.s);
+  SDR_CUDA(cudaMemsetAsync(ubuf.get(), 0, sizeof(double) * static_cast<size_t>(lay.ld), c.stream));
+  std::vector<double> h(static_cast<size_t>(S.s));
+  for (i64 q = 0; q < sp.dim(); ++q) {
+    launch_scale_copy(c, sp.uscale[static_cast<size_t>(q)], sp.col(q), ubuf.get() + lay.own_off, lay.nloc);
+    operator_apply(c, A, ubuf.get(), au.get());
+    if (cnt) ++cnt->matvecs;
+    launch_sketch(c, S, au.get(), lay.nloc, A.row_begin, sk.get());
+    c.allreduce_sum(sk.get(), S.s);
+    SDR_CUDA(cudaMemcpyAsync(h.data(), sk.get(), sizeof(double) * static_cast<size_t>(S.s), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (cnt) ++cnt->sketch_applies;
+    std::copy(h.begin(), h.end(), sp.SAU.col(q));
+  }
+  sp.provenance = 3;
+}
+
+void solve(Context& c, const DeviceOperator& A, const double* b, const double* x0, bool x0_nonzero, const Config& cfg,
+           Recycle& space, const SketchDev* sketch, const Callbacks* cb, double* x_out, Report& rep) {
+  cfg.validate();  // solver.hpp:273-298
+  if (A.rows != A.cols)
+    throw invalid("solve: operator must be square, got " + std::to_string(A.rows) + " x " + std::to_string(A.cols));
+  std::unique_ptr<SketchDev> own;
+  if (!sketch) {
+    own.reset(create_sketch(c, kSrdct, A.rows, cfg.s, cfg.sketch_seed, 0));
+    sketch = own.get();
+  }
+  if (sketch->n != A.rows)
+    throw invalid("solve: sketch takes length " + std::to_string(sketch->n) + " but the operator is " +
+                  std::to_string(A.rows) + " x " + std::to_string(A.cols));
+  if (sketch->s < 2 * (cfg.m + cfg.k))
+    throw invalid("solve: sketch size " + std::to_string(sketch->s) + " is below 2 (m + k) = " +
+                  std::to_string(2 * (cfg.m + cfg.k)));
+  if (!space.empty() && space.n != A.rows)
+    throw invalid("solve: recycle space has " + std::to_string(space.n) + " rows but the operator is " +
+                  std::to_string(A.rows) + " x " + std::to_string(A.cols));
+  if (!space.empty() && space.s != sketch->s)
+    throw invalid("solve: recycle space has " + std::to_string(space.s) + " sketch rows but the sketch has " +
+                  std::to_string(sketch->s));
+  init_host_blas();
+  const auto t_start = std::chrono::steady_clock::now();
+  const VecLayout lay = A.layout();
+  const int T = static_cast<int>(std::min<i64>(cfg.t, cfg.m));
+  if (std::min<i64>(cfg.t, cfg.m) > 33) throw invalid("solve: Arnoldi window min(t, m) exceeds the device limit of 33");
+  Workspace& w = workspace(c, lay, cfg.m, sketch->s, T);
+  space.n = A.rows;
+  space.s = sketch->s;
+  space.ensure(lay.nloc, std::max<i64>(cfg.k + 1, space.dim()));
+  if (space.SU.rows != space.s) {
+    space.SU = HMat(space.s, space.dim());
+    space.SAU = HMat(space.s, space.dim());
+  }
+
+  // rhs norm (1 IP), tol_abs (solver.hpp:303-305)
+  launch_copy_norm(c, b, w.r0.get(), lay.nloc, w.scal.get());
+  c.allreduce_sum(w.scal.get(), 1);
+  rep.rhs_norm = std::sqrt(d2h_scalar(c, w, w.scal.get()));
+  ++rep.counters.inner_products;
+  const double tol_abs = cfg.tol * rep.rhs_norm;
+  if (x0)
+    SDR_CUDA(cudaMemcpyAsync(w.x.get(), x0, sizeof(double) * static_cast<size_t>(lay.nloc), cudaMemcpyDeviceToDevice, c.stream));
+  else
+    SDR_CUDA(cudaMemsetAsync(w.x.get(), 0, sizeof(double) * static_cast<size_t>(std::max<i64>(lay.nloc, 1)), c.stream));
+  if (x0 && x0_nonzero) {  // r = b - A x0 (solver.hpp:307-316)
+    SDR_CUDA(cudaMemcpyAsync(w.tmp.get() + lay.own_off, x0, sizeof(double) * static_cast<size_t>(lay.nloc),
+                             cudaMemcpyDeviceToDevice, c.stream));
+    c.halo_exchange(A.plan, w.tmp.get() + lay.ext_shift(), A.ext_begin, w.tmp.get() + lay.own_off, A.row_begin);
+    launch_residual(c, A.view(), w.tmp.get() + lay.ext_shift(), b, w.r0.get(), w.scal.get());
+    ++rep.counters.matvecs;
+  }
+
+  double safety = cfg.safety_init, res_norm = std::numeric_limits<double>::quiet_NaN();
+  bool have = false;
+  for (int cycle = 1; cycle <= cfg.max_restarts; ++cycle) {  // solver.hpp:321-359
+    CycleOut cr;
+    try {
+      cr = solve_cycle(c, w, A, *sketch, cfg, w.r0.get(), space, tol_abs, safety, rep.counters, rep, cb, cycle,
+                       rep.iterations);
+    } catch (const Error& e) {
+      if (e.code != 2) throw;
+      rep.status = 0;
+      res_norm = 0.0;
+      have = true;
+      break;
+    }
+    rep.cycles = cycle;
+    rep.iterations += cr.steps;
+    safety = cr.safety;
+    if (cr.have_correction) {
+      launch_axpy(c, 1.0, w.corr.get() + lay.own_off, w.x.get(), lay.nloc);
+      std::swap(w.r0, w.rnew);
+    }
+    res_norm = cr.residual_norm;
+    have = true;
+    if (cr.converged) {
+      rep.status = 0;
+      break;
+    }
+    if (cr.breakdown) {
+      rep.status = 2;
+      rep.notes.push_back("cycle " + std::to_string(cycle) + ": basis exhausted before reaching the target");
+      break;
+    }
+    if (cr.steps == cfg.m && cr.sres > 0.99 * cr.sketched_entry) {
+      rep.status = 3;
+      rep.notes.push_back("cycle " + std::to_string(cycle) + ": sketched residual improved by less than 1% over a full cycle");
+      break;
+    }
+    if (cycle == cfg.max_restarts) rep.status = 1;
+  }
+  if (have) rep.final_relative_residual = rep.rhs_norm > 0.0 ? res_norm / rep.rhs_norm : res_norm;
+  if (x_out)
+    SDR_CUDA(cudaMemcpyAsync(x_out, w.x.get(), sizeof(double) * static_cast<size_t>(lay.nloc), cudaMemcpyDefault, c.stream));
+  c.sync();
+  rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+}  // namespace sdr

@@ -1,0 +1,119 @@
+// K1 / K6: SELL-32 SpMV with fused epilogues (sm_100a).
+//
+// Replaces SparseMatrix::apply (sparse.hpp:84-98) and the first half of
+// arnoldi_step (arnoldi.hpp:87-97): one warp owns a 32-row slice, every k
+// step of the slice loads 32 int32 column indices (128 B) and 32 fp64 values
+// (256 B) fully coalesced; x is gathered through the read-only path (the
+// whole vector stays L2-resident up to ~60 M rows, so HBM reads x once).
+// Epilogue variants fuse the reductions the step needs into the same pass:
+//   MODE 0  y = A x
+//   MODE 1  y = A w_j, plus ||y||^2 and y.w_{j-d} for the MGS window (K1)
+//   MODE 2  r = b - A x, plus ||r||^2                (verification, K6)
+// Algorithmic bytes per row: 12 B per stored entry + 8 B x + 8 B y (+8 B
+// per extra window vector in MODE 1, +8 B b in MODE 2).
+#include "kernels.hpp"
+#include "reduce.cuh"
+
+namespace sdr {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int MODE, int NV>
+__global__ void __launch_bounds__(kThreads) k_sell_spmv(SellView A, const double* __restrict__ x_ext,
+                                                         double* __restrict__ y, const double* __restrict__ aux,
+                                                         int64_t ldv, int64_t own_off, int64_t halo_lo, int j,
+                                                         int nwin, double* __restrict__ partials,
+                                                         unsigned* __restrict__ counter, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+
+  for (int64_t sl = gw; sl < A.nslices; sl += nwarps) {
+    const int64_t p0 = A.slice_ptr[sl];
+    const int len = static_cast<int>((A.slice_ptr[sl + 1] - p0) >> 5);
+    const int32_t* cp = A.cols + p0 + lane;
+    const double* vp = A.vals + p0 + lane;
+    double s = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < len; ++k) s = fma(__ldg(vp + k * kSlice), __ldg(x_ext + __ldg(cp + k * kSlice)), s);
+    const int64_t row = sl * kSlice + lane;
+    if (row < A.nrows) {
+      if constexpr (MODE == 0) {
+        y[row] = s;
+      } else if constexpr (MODE == 1) {
+        y[row] = s;
+        acc[0] = fma(s, s, acc[0]);
+        acc[1] = fma(s, x_ext[halo_lo + row], acc[1]);
+#pragma unroll
+        for (int d = 1; d < NV - 1; ++d)
+          if (d < nwin) acc[1 + d] = fma(s, __ldg(aux + (j - d) * ldv + own_off + row), acc[1 + d]);
+      } else {
+        const double r = aux[row] - s;
+        y[row] = r;
+        acc[0] = fma(r, r, acc[0]);
+      }
+    }
+  }
+  if constexpr (MODE != 0) {
+    const int nv = MODE == 1 ? 1 + nwin : 1;
+    block_partials<NV>(acc, nv, partials);
+    if (last_block_done(counter)) {
+      fold_partials(partials, gridDim.x, nv, out);
+      if (threadIdx.x == 0) *counter = 0u;
+    }
+  }
+}
+
+int grid_for(const Context& c, int64_t nslices) {
+  const int64_t want = (nslices + (kThreads / 32) - 1) / (kThreads / 32);
+  const int64_t cap = static_cast<int64_t>(c.num_sms) * 8;
+  return static_cast<int>(std::max<int64_t>(1, std::min(want, cap)));
+}
+
+template <int NV>
+void spmv_arnoldi_impl(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
+                       int nwin, double* y, double* recA) {
+  const int g = grid_for(c, A.nslices);
+  const double* x_ext = V + j * ldv + lay.ext_shift();
+  TimedLaunch t(c, "spmv_arnoldi");
+  k_sell_spmv<1, NV><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin,
+                                                   c.partials(static_cast<int64_t>(NV) * g), c.counters() + 0, recA);
+  SDR_KERNEL_CHECK();
+}
+
+}  // namespace
+
+void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) {
+  if (A.nrows == 0) return;
+  const int g = grid_for(c, A.nslices);
+  TimedLaunch t(c, "spmv");
+  k_sell_spmv<0, 1><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, nullptr, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr);
+  SDR_KERNEL_CHECK();
+}
+
+void launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
+                         int nwin, double* y, double* recA) {
+  if (nwin <= 3)
+    spmv_arnoldi_impl<4>(c, A, V, ldv, lay, j, nwin, y, recA);
+  else if (nwin <= 7)
+    spmv_arnoldi_impl<8>(c, A, V, ldv, lay, j, nwin, y, recA);
+  else if (nwin <= 33)
+    spmv_arnoldi_impl<34>(c, A, V, ldv, lay, j, nwin, y, recA);
+  else
+    throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
+}
+
+void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2) {
+  const int g = grid_for(c, A.nslices);
+  TimedLaunch t(c, "residual");
+  k_sell_spmv<2, 1><<<g, kThreads, 0, c.stream>>>(A, x_ext, r, b, 0, 0, 0, 0, 0, c.partials(g), c.counters() + 1,
+                                                  norm2);
+  SDR_KERNEL_CHECK();
+}
+
+}  // namespace sdr

@@ -1,0 +1,217 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Tolerances follow BASELINE.json's north_star: per-kernel SpMV / sketch
+outputs within 1e-12 relative (fp64), sketch rows/signs bit-identical,
+solver status equal with iteration counts within ±2%.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def random_matrix(O, n, seed):
+    """test_solver.cpp:27-34: gaussian + n I, column-major draw order."""
+    g = O.gaussian_vector(n * n, seed)
+    A = g.reshape(n, n).T.copy()
+    A[np.diag_indices(n)] += n
+    return A
+
+
+def to_both(sk, O, off, col, val, rows, cols):
+    return sk.SparseMatrix(rows, cols, off, col, val), O.SparseMatrix.from_csr(rows, cols, off, col, val)
+
+
+# ----------------------------------------------------------------------- SpMV
+
+@pytest.mark.parametrize("case", ["c1", "conv3d", "random", "dense", "empty_rows"])
+def test_spmv_matches_oracle(sk, O, case):
+    rng = np.random.default_rng(7)
+    if case == "c1":
+        off, col, val = O.gen_convdiff(100, -50.0).csr()
+        off, col, val, n = off, col, -val, 10000
+    elif case == "conv3d":
+        off, col, val = O.gen_convdiff3d(40, 100.0, 50.0, 25.0).csr()
+        n = 40 ** 3
+    elif case == "random":
+        n = 5000
+        lens = rng.integers(0, 40, n)
+        rows = np.repeat(np.arange(n), lens)
+        cols_ = rng.integers(0, n, rows.size)
+        M = O.SparseMatrix.from_triplets(n, n, rows, cols_, rng.standard_normal(rows.size))
+        off, col, val = M.csr()
+    elif case == "dense":
+        n = 70
+        off, col, val = O.SparseMatrix.from_dense(random_matrix(O, n, 3)).csr()
+    else:
+        n = 300
+        rows = rng.integers(0, n, 600)
+        rows = rows[rows % 3 != 0]
+        M = O.SparseMatrix.from_triplets(n, n, rows, rng.integers(0, n, rows.size), rng.standard_normal(rows.size))
+        off, col, val = M.csr()
+    A, Ao = to_both(sk, O, off, col, val, n, n)
+    for seed in (1, 2):
+        x = O.gaussian_vector(n, seed)
+        assert rel(A.apply(x), Ao.apply(x)) <= REL
+
+
+def test_device_generated_operator_matches_host_csr(sk, O):
+    n = 48
+    Ad = sk.SparseMatrix.convdiff3d_device(n, 100.0, 50.0, 25.0)
+    off, col, val = sk.gen_convdiff3d(n, 100.0, 50.0, 25.0)
+    Ah = sk.SparseMatrix(n ** 3, n ** 3, off, col, val)
+    assert Ad.nnz == Ah.nnz == len(val)
+    x = O.gaussian_vector(n ** 3, 5)
+    yd, yh = Ad.apply(x), Ah.apply(x)
+    assert np.array_equal(yd, yh)
+
+
+def test_spmv_rejects_bad_input(sk):
+    with pytest.raises(ValueError, match="offsets must start at 0"):
+        sk.SparseMatrix(2, 2, [1, 1, 2], [0], [1.0])
+    with pytest.raises(ValueError, match="not strictly increasing in row 0"):
+        sk.SparseMatrix(2, 2, [0, 2, 2], [1, 1], [1.0, 2.0])
+    with pytest.raises(ValueError, match="non-finite value in row 1"):
+        sk.SparseMatrix(2, 2, [0, 1, 2], [0, 1], [1.0, np.inf])
+    A = sk.SparseMatrix(2, 3, [0, 1, 2], [0, 2], [1.0, 2.0])
+    with pytest.raises(ValueError, match="3 columns but vector has 2 entries"):
+        A.apply(np.ones(2))
+
+
+# --------------------------------------------------------------------- sketches
+
+@pytest.mark.parametrize("n,s,seed", [(200, 48, 31), (4096, 240, 0x5EED), (2 ** 21, 240, 0x5EED), (10000, 120, 0)])
+def test_srdct_rows_and_signs_bit_exact(sk, O, n, s, seed):
+    S = sk.SketchOperator.subsampled_dct(n, s, seed)
+    So = O.SketchOperator.subsampled_dct(n, s, seed)
+    assert np.array_equal(S.rows(), So.rows())
+    assert np.array_equal(S.signs(), So.signs())
+
+
+@pytest.mark.parametrize("n,s", [(200, 48), (256, 64), (1000, 120), (10000, 120), (65536, 240), (2 ** 20, 140),
+                                 (2 ** 21, 240), (3 * 2 ** 15, 200), (997, 60)])
+def test_srdct_apply_matches_oracle(sk, O, n, s):
+    S = sk.SketchOperator.subsampled_dct(n, s, 0x5EED)
+    So = O.SketchOperator.subsampled_dct(n, s, 0x5EED)
+    for seed in (11, 12):
+        x = O.gaussian_vector(n, seed)
+        assert rel(S.apply(x), So.apply(x)) <= REL
+
+
+def test_srdct_matches_scipy_dct(sk, O):
+    import scipy.fft
+    n, s = 4096, 100
+    S = sk.SketchOperator.subsampled_dct(n, s, 99)
+    x = O.gaussian_vector(n, 3)
+    ref = np.sqrt(n / s) * scipy.fft.dct(S.signs() * x, type=2, norm="ortho")[S.rows()]
+    assert rel(S.apply(x), ref) <= REL
+
+
+@pytest.mark.parametrize("n,s,zeta", [(10000, 120, 8), (4097, 240, 8), (1000, 37, 5), (64, 16, 16)])
+def test_sparse_sign_matches_oracle(sk, O, n, s, zeta):
+    S = sk.SketchOperator.sparse_sign(n, s, 0x5EED, zeta)
+    So = O.SketchOperator.sparse_sign(n, s, 0x5EED, zeta)
+    x = O.gaussian_vector(n, 4)
+    assert rel(S.apply(x), So.apply(x)) <= REL
+
+
+def test_identity_sketch_passes_through(sk, O):
+    S = sk.SketchOperator.identity(40)
+    x = O.gaussian_vector(40, 8)
+    assert np.array_equal(S.apply(x), x)
+
+
+def test_sketch_is_linear_and_deterministic(sk, O):
+    n = 2 ** 16
+    S = sk.SketchOperator.subsampled_dct(n, 240, 7)
+    a, b = O.gaussian_vector(n, 1), O.gaussian_vector(n, 2)
+    sa, sb, sab = S.apply(a), S.apply(b), S.apply(2.0 * a - 3.0 * b)
+    assert np.linalg.norm(sab - (2.0 * sa - 3.0 * sb)) <= 1e-13 * np.linalg.norm(sab)
+    assert np.array_equal(S.apply(a), sa)
+
+
+# --------------------------------------------------------------- Arnoldi steps
+
+def krylov(sk, A, S, r0, t, m, steps=None, btol=1e-14):
+    import ctypes as C
+    n, s = A.local_rows, S.sketch_dim
+    V = np.zeros((m + 1) * n)
+    H = np.zeros((m + 1) * m)
+    SV = np.zeros(s * (m + 1))
+    SAV = np.zeros(s * m)
+    j, br, rn = C.c_int64(), C.c_int(), C.c_double()
+    cnt = np.zeros(3, dtype=np.int64)
+    r0 = np.ascontiguousarray(r0, dtype=np.float64)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    sk._check(sk._lib.sdr_krylov_run(A.ctx._h, A._h, S._h, p(r0), t, m, m if steps is None else steps, btol, p(V),
+                                     p(H), p(SV), p(SAV), C.byref(j), C.byref(br), C.byref(rn), p(cnt)))
+    return dict(V=V.reshape(m + 1, n).T, H=H.reshape(m, m + 1).T, SV=SV.reshape(m + 1, s).T,
+                SAV=SAV.reshape(m, s).T, j=j.value, breakdown=bool(br.value), r0_norm=rn.value,
+                counters=tuple(int(c) for c in cnt))
+
+
+@pytest.mark.parametrize("t", [1, 2, 3])
+def test_arnoldi_matches_oracle(sk, O, t):
+    n, m, s = 60, 12, 40
+    M = random_matrix(O, n, 17)
+    A, Ao = sk.SparseMatrix.from_dense(M), O.SparseMatrix.from_dense(M)
+    S, So = sk.SketchOperator.subsampled_dct(n, s, 23), O.SketchOperator.subsampled_dct(n, s, 23)
+    r0 = O.gaussian_vector(n, 29)
+    g = krylov(sk, A, S, r0, t, m)
+    o = O.run_arnoldi(Ao, r0, So, t, m)
+    assert g["j"] == o.j == m and not g["breakdown"]
+    assert g["counters"] == tuple(o.counters)
+    assert rel(g["H"], o.H) <= 1e-12
+    assert rel(g["SV"], o.SV) <= 1e-12
+    assert rel(g["SAV"], o.SAV) <= 1e-11
+    assert rel(g["V"], o.V) <= 1e-12
+    # recurrence A v_q = V H(:, q) and band structure (test_arnoldi.cpp:34-52)
+    for q in range(m):
+        lhs = M @ g["V"][:, q]
+        assert np.linalg.norm(lhs - g["V"][:, : q + 2] @ g["H"][: q + 2, q]) <= 1e-12 * np.linalg.norm(lhs)
+        assert np.all(g["H"][: max(0, q - t + 1), q] == 0.0)
+
+
+def test_arnoldi_c1_operator_long_window(sk, O):
+    off, col, val = O.gen_convdiff(100, -50.0).csr()
+    A, Ao = to_both(sk, O, off, col, -val, 10000, 10000)
+    S, So = sk.SketchOperator.subsampled_dct(10000, 120, 0x5EED), O.SketchOperator.subsampled_dct(10000, 120, 0x5EED)
+    r0 = O.gaussian_vector(10000, 0)
+    g = krylov(sk, A, S, r0, 2, 50)
+    o = O.run_arnoldi(Ao, r0, So, 2, 50)
+    assert rel(g["H"], o.H) <= 1e-10
+    assert rel(g["SV"], o.SV) <= 1e-10
+
+
+def test_arnoldi_breakdown_on_invariant_subspace(sk, O):
+    n = 20
+    A = sk.SparseMatrix.from_dense(2.5 * np.eye(n))
+    S = sk.SketchOperator.subsampled_dct(n, 10, 3)
+    g = krylov(sk, A, S, O.gaussian_vector(n, 31), 2, 5)
+    assert g["breakdown"] and g["j"] == 1
+    assert g["H"][1, 0] == 0.0
+    assert abs(g["H"][0, 0] - 2.5) <= 1e-12 * 2.5
+
+
+def test_arnoldi_full_window_is_dense_arnoldi(sk, O):
+    n, m = 30, 8
+    M = random_matrix(O, n, 11)
+    A = sk.SparseMatrix.from_dense(M)
+    S = sk.SketchOperator.identity(n)
+    r0 = O.gaussian_vector(n, 13)
+    g = krylov(sk, A, S, r0, m, m)
+    V = g["V"][:, : m + 1]
+    assert np.linalg.norm(V.T @ V - np.eye(m + 1)) < 1e-8
+
+
+def test_zero_start_is_domain_error(sk):
+    A = sk.SparseMatrix.from_dense(np.eye(8))
+    S = sk.SketchOperator.identity(8)
+    with pytest.raises(ArithmeticError):
+        krylov(sk, A, S, np.zeros(8), 1, 4)

@@ -1,0 +1,204 @@
+"""GPU solver parity: sdr_solve / sdr_solve_sequence against the CPU oracle
+and the reference's solver / sequence properties (test_solver.cpp,
+test_sequence.cpp, acceptance.cpp criteria 1 and 6)."""
+import numpy as np
+import pytest
+
+from tests.test_gpu_parity import random_matrix, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def both(sk, O, M):
+    return sk.SparseMatrix.from_dense(M), O.SparseMatrix.from_dense(M)
+
+
+def cfgs(sk, O, **kw):
+    return sk.SolverConfig(**kw), O.SolverConfig(**kw)
+
+
+def assert_same_solve(g, o, iters_tol=0.0):
+    assert g.report.status == o[1].status
+    if iters_tol == 0.0:
+        assert g.report.iterations == o[1].iterations
+        assert g.report.cycles == o[1].cycles
+        assert g.report.counters == o[1].counters
+    else:
+        assert abs(g.report.iterations - o[1].iterations) <= max(1, iters_tol * o[1].iterations)
+
+
+def test_identity_sketch_reproduces_dense_gmres(sk, O):
+    n, m = 40, 20
+    M = random_matrix(O, n, 81)
+    A, Ao = both(sk, O, M)
+    b = O.gaussian_vector(n, 82)
+    c, co = cfgs(sk, O, m=m, t=m, k=0, s=2 * m, tol=1e-8, safety_init=1.0, max_restarts=2)
+    g = sk.solve(A, b, c, sketch=sk.SketchOperator.identity(n))
+    o = O.solve(Ao, b, co, sketch=O.SketchOperator.identity(n))
+    assert g.report.status == "converged" and g.report.cycles == 1
+    assert_same_solve(g, o)
+    for (i1, v1), (i2, v2) in zip(g.report.sketched_residuals, o[1].sketched_residuals):
+        assert i1 == i2 and abs(v1 - v2) <= 1e-8 * np.linalg.norm(b)
+    xr = np.linalg.solve(M, b)
+    assert np.linalg.norm(g.x - o[0]) <= 1e-8 * np.linalg.norm(xr)
+    assert g.report.final_relative_residual == pytest.approx(np.linalg.norm(b - M @ g.x) / np.linalg.norm(b), rel=1e-10)
+
+
+def test_truncated_sketched_solve_books(sk, O):
+    n = 80
+    M = random_matrix(O, n, 83)
+    A, Ao = both(sk, O, M)
+    b = O.gaussian_vector(n, 84)
+    c, co = cfgs(sk, O, m=10, t=2, k=4, s=60, tol=1e-8, max_restarts=8)
+    g = sk.solve(A, b, c)
+    o = O.solve(Ao, b, co)
+    assert g.report.status == "converged"
+    assert_same_solve(g, o)
+    res = np.linalg.norm(b - M @ g.x)
+    assert res <= c.tol * np.linalg.norm(b) * (1 + 1e-10)
+    assert g.report.final_relative_residual == pytest.approx(res / np.linalg.norm(b), rel=1e-9)
+    idx = 0
+    for cs in g.report.cycle_stats:
+        prev = np.inf
+        for _ in range(cs["steps"]):
+            v = g.report.sketched_residuals[idx][1]
+            assert v <= prev * (1 + 1e-12)
+            prev = v
+            idx += 1
+        assert cs["basis_cond"] >= 1.0
+    safety = 0.0
+    for cs in g.report.cycle_stats:
+        assert cs["safety_after"] >= safety
+        safety = cs["safety_after"]
+    assert g.space.dim() >= c.k
+    # recycle_consistency_error (recycle.hpp:389-403): SU = S U, SAU = S A U
+    S = O.SketchOperator.subsampled_dct(n, c.s, c.sketch_seed)
+    U, SU, SAU = g.space.get()
+    for q in range(U.shape[1]):
+        assert np.linalg.norm(S.apply(U[:, q]) - SU[:, q]) / max(1.0, np.linalg.norm(SU[:, q])) <= 1e-10
+        assert np.linalg.norm(S.apply(M @ U[:, q]) - SAU[:, q]) / max(1.0, np.linalg.norm(SAU[:, q])) <= 1e-10
+        assert np.linalg.norm(U[:, q]) == pytest.approx(1.0, abs=1e-13)
+
+
+def test_degenerate_rhs(sk, O):
+    n = 30
+    A = sk.SparseMatrix.from_dense(random_matrix(O, n, 88))
+    c = sk.SolverConfig(m=5, t=2, k=0, s=12)
+    z = sk.solve(A, np.zeros(n), c)
+    assert z.report.status == "converged" and z.report.iterations == 0
+    assert z.report.counters["matvecs"] == 0 and np.linalg.norm(z.x) == 0.0
+    assert z.report.final_relative_residual == 0.0
+    Cm = sk.SparseMatrix.from_dense(2.5 * np.eye(n))
+    b = O.gaussian_vector(n, 89)
+    e = sk.solve(Cm, b, c)
+    assert e.report.status == "converged" and e.report.iterations == 1
+    assert np.linalg.norm(e.x - b / 2.5) <= 1e-12 * np.linalg.norm(b)
+
+
+def test_stagnation_is_divergence(sk, O):
+    n = 40
+    M = np.zeros((n, n))
+    for j in range(n):
+        M[(j + 1) % n, j] = 1.0
+    b = np.zeros(n)
+    b[0] = 1.0
+    c = sk.SolverConfig(m=5, t=5, k=0, s=n, tol=1e-8, max_restarts=6)
+    r = sk.solve(sk.SparseMatrix.from_dense(M), b, c, sketch=sk.SketchOperator.identity(n))
+    assert r.report.status == "diverged" and r.report.cycles == 1 and r.report.notes
+
+
+def test_restart_budget(sk, O):
+    n = 100
+    A = sk.SparseMatrix.from_dense(random_matrix(O, n, 90))
+    r = sk.solve(A, O.gaussian_vector(n, 91), sk.SolverConfig(m=5, t=2, k=0, s=30, tol=1e-13, max_restarts=1))
+    assert r.report.status == "max_restarts" and r.report.cycles == 1 and r.report.iterations == 5
+
+
+def test_bitwise_determinism(sk, O):
+    n = 70
+    A = sk.SparseMatrix.from_dense(random_matrix(O, n, 92))
+    b = O.gaussian_vector(n, 93)
+    c = sk.SolverConfig(m=8, t=2, k=3, s=44, tol=1e-8)
+    r1, r2 = sk.solve(A, b, c), sk.solve(A, b, c)
+    assert r1.report.status == r2.report.status and r1.report.iterations == r2.report.iterations
+    assert np.array_equal(r1.x, r2.x)
+
+
+def test_config_validation_and_shapes(sk, O):
+    n = 30
+    M = random_matrix(O, n, 94)
+    A = sk.SparseMatrix.from_dense(M)
+    b = O.gaussian_vector(n, 95)
+    for mut in [dict(m=0), dict(t=0), dict(k=5), dict(k=-1), dict(tol=0.0), dict(tol=1.0), dict(safety_init=0.5),
+                dict(max_restarts=0), dict(s=13)]:
+        kw = dict(m=5, t=2, k=2, s=20)
+        kw.update(mut)
+        with pytest.raises(ValueError):
+            sk.solve(A, b, sk.SolverConfig(**kw))
+    ok = sk.SolverConfig(m=5, t=2, k=2, s=20)
+    with pytest.raises(ValueError):
+        sk.solve(A, np.zeros(n + 1), ok)
+    with pytest.raises(ValueError):
+        sk.solve(A, b, ok, sketch=sk.SketchOperator.subsampled_dct(n - 1, 20, 1))
+    with pytest.raises(ValueError):
+        sk.solve(A, b, ok, x0=np.zeros(n - 1))
+    g = O.gaussian_vector(n, 96)
+    w = sk.solve(A, b, ok, x0=g)
+    assert w.report.status == "converged"
+    assert np.linalg.norm(b - M @ w.x) <= ok.tol * np.linalg.norm(b) * (1 + 1e-10)
+
+
+def test_c1_problem_matches_oracle(sk, O):
+    """BASELINE config C1: A = -gen_convdiff(100, -50), b ~ N(0,1) seed 0 normalised,
+    m=50, k=10, t=2, s=120, tol 1e-8 — SRDCT (reference sketch) and sparse sign."""
+    off, col, val = O.gen_convdiff(100, -50.0).csr()
+    A = sk.SparseMatrix(10000, 10000, off, col, -val)
+    Ao = O.SparseMatrix.from_csr(10000, 10000, off, col, -val)
+    b = O.gaussian_vector(10000, 0)
+    b /= np.linalg.norm(b)
+    c, co = cfgs(sk, O, m=50, k=10, t=2, s=120, tol=1e-8, max_restarts=40)
+    g = sk.solve(A, b, c)
+    o = O.solve(Ao, b, co)
+    assert_same_solve(g, o, iters_tol=0.02)
+    assert g.report.final_relative_residual <= 1e-8 or g.report.status != "converged"
+    gs = sk.solve(A, b, c, sketch=sk.SketchOperator.sparse_sign(10000, 120, 0x5EED, 8))
+    os_ = O.solve(Ao, b, co, sketch=O.SketchOperator.sparse_sign(10000, 120, 0x5EED, 8))
+    assert_same_solve(gs, os_, iters_tol=0.02)
+
+
+def test_sequence_recycling_and_variants(sk, O):
+    """test_sequence.cpp:46-147: recycling cuts iterations; exact refresh costs
+    k matvecs + k sketches charged to the changed system."""
+    n = 400
+    g = 20
+    M1 = O.gen_neumann(g, 0.5).dense()
+    M2 = O.gen_neumann(g, 0.7).dense()
+    A1, A2 = sk.SparseMatrix.from_dense(M1), sk.SparseMatrix.from_dense(M2)
+    A1o, A2o = O.SparseMatrix.from_dense(M1), O.SparseMatrix.from_dense(M2)
+    rhs = [O.gaussian_vector(n, 500 + i) for i in range(4)]
+    for variant in ("exact", "inexact", "reuse"):
+        c, co = cfgs(sk, O, m=30, k=8, t=2, s=80, tol=1e-8, variant=variant)
+        probs = [sk.ProblemInstance(A1, rhs[0]), sk.ProblemInstance(A1, rhs[1]), sk.ProblemInstance(A2, rhs[2]),
+                 sk.ProblemInstance(A2, rhs[3])]
+        res = sk.solve_sequence(probs, c)
+        xs, reps = O.solve_sequence([A1o, A1o, A2o, A2o], rhs, co)
+        for gr, orr in zip(res.reports, reps):
+            assert gr.status == orr.status
+            assert abs(gr.iterations - orr.iterations) <= max(1, 0.02 * orr.iterations)
+            assert gr.counters["matvecs"] - gr.iterations == orr.counters["matvecs"] - orr.iterations
+            assert gr.notes[-1:] == orr.notes[-1:] or variant != "reuse"
+        assert res.reports[1].iterations < res.reports[0].iterations
+
+
+def test_sequence_failure_isolation_and_empty(sk, O):
+    n = 50
+    A = sk.SparseMatrix.from_dense(random_matrix(O, n, 5))
+    B = sk.SparseMatrix.from_dense(random_matrix(O, n + 1, 6))
+    c = sk.SolverConfig(m=10, k=3, t=2, s=30, tol=1e-8)
+    res = sk.solve_sequence([sk.ProblemInstance(A, O.gaussian_vector(n, 1)),
+                             sk.ProblemInstance(B, O.gaussian_vector(n + 1, 2)),
+                             sk.ProblemInstance(A, O.gaussian_vector(n, 3))], c)
+    assert res.reports[0].status == "converged"
+    assert res.reports[1].error and "aborted" in res.reports[1].notes[-1]
+    assert res.reports[2].status == "converged"
+    assert sk.solve_sequence([], c).reports == []
