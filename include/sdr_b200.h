@@ -253,6 +253,9 @@ SDR_API int sdr_report_notes(const sdr_report* r, int64_t* n);
 SDR_API const char* sdr_report_note(const sdr_report* r, int64_t i);
 SDR_API const char* sdr_report_error(const sdr_report* r);
 /* Device-phase timing of the solve: arnoldi_ms (K1+K2+sketch), host_ms, steps. */
+/* Wall-clock phase breakdown (ms): "setup", "cycle_init", "step_wait", "host_step",
+ * "check", "drain", "basis_cond", "recycle", "recycle_harmonic". Unknown names give 0. */
+SDR_API int sdr_report_phase(const sdr_report* r, const char* name, double* ms);
 SDR_API int sdr_report_timing(const sdr_report* r, double* device_ms, double* host_wait_ms, double* total_ms);
 
 #ifdef __cplusplus

@@ -47,6 +47,8 @@ STATUS = {0: "converged", 1: "max_restarts", 2: "breakdown", 3: "diverged"}
 VARIANT = {"reuse": 0, "exact": 1, "inexact": 2}
 PROVENANCE = {0: "empty", 1: "fresh", 2: "reused", 3: "exact-resketch", 4: "inexact-carryover"}
 PROVENANCE_ID = {v: k for k, v in PROVENANCE.items()}
+PHASES = ("setup", "cycle_init", "step_wait", "host_step", "check", "drain", "basis_cond", "recycle",
+          "recycle_harmonic")
 
 
 class SdrError(RuntimeError):
@@ -577,6 +579,7 @@ class SolveReport:
     seconds: float = 0.0
     device_ms: float = 0.0
     host_wait_ms: float = 0.0
+    phases: dict = field(default_factory=dict)
 
 
 def _report(h) -> SolveReport:
@@ -606,12 +609,17 @@ def _report(h) -> SolveReport:
     nn = C.c_int64()
     _check(_lib.sdr_report_notes(h, C.byref(nn)))
     notes = [_lib.sdr_report_note(h, i).decode() for i in range(nn.value)]
+    phases = {}
+    for name in PHASES:
+        v = C.c_double()
+        _check(_lib.sdr_report_phase(h, name.encode(), C.byref(v)))
+        phases[name] = v.value
     dev, wait, tot = C.c_double(), C.c_double(), C.c_double()
     _check(_lib.sdr_report_timing(h, C.byref(dev), C.byref(wait), C.byref(tot)))
     rep = SolveReport(STATUS[st.value], it.value, cy.value, rhs.value, frr.value,
                       dict(matvecs=mv.value, inner_products=ip.value, sketch_applies=sk.value), samples[0],
                       samples[1], cs, notes, (_lib.sdr_report_error(h) or b"").decode(), sec.value, dev.value,
-                      wait.value)
+                      wait.value, phases)
     _lib.sdr_report_destroy(h)
     return rep
 

@@ -104,6 +104,7 @@ SIGNATURES = {
     "sdr_report_notes": (cint, [vp, P(i64)]),
     "sdr_report_note": (C.c_char_p, [vp, i64]),
     "sdr_report_error": (C.c_char_p, [vp]),
+    "sdr_report_phase": (cint, [vp, C.c_char_p, P(f64)]),
     "sdr_report_timing": (cint, [vp, P(f64), P(f64), P(f64)]),
 }
 

@@ -30,6 +30,24 @@ __global__ void __launch_bounds__(kThreads) k_update(const double* __restrict__ 
                                                       unsigned* __restrict__ counter) {
   __shared__ double coef[MAXT + 1];
   const int b_off = 2 * T + 3;
+  const double* W[MAXT];
+#pragma unroll
+  for (int d = 0; d < MAXT; ++d) W[d] = V + static_cast<int64_t>(j - (d < nwin ? d : 0)) * ldv + own_off;
+  double* wout = V + static_cast<int64_t>(j + 1) * ldv + own_off;
+  // two rows per thread through 16-byte accesses (own_off and ldv are 32-aligned);
+  // the first pair is fetched before the coefficient barrier and every later
+  // pair one iteration ahead (software pipelining: 2 pairs in flight).
+  const int64_t npair = n >> 1;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double2 yv = make_double2(0.0, 0.0), wv[MAXT];
+  auto fetch = [&](int64_t q, double2& yo, double2 (&wo)[MAXT]) {
+    yo = __ldcs(reinterpret_cast<const double2*>(y) + q);
+#pragma unroll
+    for (int d = MAXT - 1; d >= 0; --d)
+      if (d < nwin) wo[d] = __ldg(reinterpret_cast<const double2*>(W[d]) + q);
+  };
+  if (p < npair) fetch(p, yv, wv);
   if (threadIdx.x == 0) {
     const double* recA = rec + static_cast<int64_t>(j + 1) * rstride;
     const double wn2 = rec[static_cast<int64_t>(j) * rstride + b_off];
@@ -40,22 +58,33 @@ __global__ void __launch_bounds__(kThreads) k_update(const double* __restrict__ 
       ci[d] = d == 0 ? cj : (d < nwin ? cvec[j - d] : 0.0);
       h[d] = 0.0;
     }
-    // MGS order i = j-nwin+1 .. j  <=>  d = nwin-1 .. 0
-    for (int d = nwin - 1; d >= 0; --d) {
-      const int i = j - d;
-      double acc = cj * ci[d] * recA[1 + d];
-      for (int d2 = nwin - 1; d2 > d; --d2) {
-        const double gram = rec[static_cast<int64_t>(i) * rstride + b_off + (d2 - d)];
-        acc -= h[d2] * (ci[d2] * ci[d] * gram);
+    // MGS order i = j-nwin+1 .. j  <=>  d = nwin-1 .. 0 (compile-time loops
+    // with predicates keep h[], ci[] in registers)
+#pragma unroll
+    for (int d = MAXT - 1; d >= 0; --d) {
+      if (d < nwin) {
+        const int i = j - d;
+        double acc = cj * ci[d] * recA[1 + d];
+#pragma unroll
+        for (int d2 = MAXT - 1; d2 > d; --d2) {
+          if (d2 < nwin) {
+            const double gram = rec[static_cast<int64_t>(i) * rstride + b_off + (d2 - d)];
+            acc -= h[d2] * (ci[d2] * ci[d] * gram);
+          }
+        }
+        h[d] = acc;
       }
-      h[d] = acc;
     }
     coef[0] = cj;
+#pragma unroll
     for (int d = 0; d < MAXT; ++d) coef[1 + d] = d < nwin ? -h[d] * ci[d] : 0.0;
     if (blockIdx.x == 0) {
       double* recH = rec + static_cast<int64_t>(j + 1) * rstride + (T + 1);
       recH[0] = cj * sqrt(recA[0]);
-      for (int d = 0; d < T; ++d) recH[1 + d] = d < nwin ? h[d] : 0.0;
+#pragma unroll
+      for (int d = 0; d < MAXT; ++d)
+        if (d < T) recH[1 + d] = d < nwin ? h[d] : 0.0;
+      for (int d = MAXT; d < T; ++d) recH[1 + d] = 0.0;
       recH[1 + T] = cj;
       cvec[j] = cj;
     }
@@ -68,20 +97,11 @@ __global__ void __launch_bounds__(kThreads) k_update(const double* __restrict__ 
   double cf[MAXT + 1];
 #pragma unroll
   for (int k = 0; k <= MAXT; ++k) cf[k] = coef[k];
-  const double* W[MAXT];
-#pragma unroll
-  for (int d = 0; d < MAXT; ++d) W[d] = V + static_cast<int64_t>(j - (d < nwin ? d : 0)) * ldv + own_off;
-  double* wout = V + static_cast<int64_t>(j + 1) * ldv + own_off;
 
-  // two rows per thread through 16-byte accesses (own_off and ldv are 32-aligned)
-  const int64_t npair = n >> 1;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < npair; p += stride) {
-    const double2 yv = __ldcs(reinterpret_cast<const double2*>(y) + p);
-    double2 wv[MAXT];
-#pragma unroll
-    for (int d = MAXT - 1; d >= 0; --d)
-      if (d < nwin) wv[d] = __ldg(reinterpret_cast<const double2*>(W[d]) + p);
+  while (p < npair) {
+    const int64_t pn = p + stride;
+    double2 yn = make_double2(0.0, 0.0), wn[MAXT];
+    if (pn < npair) fetch(pn, yn, wn);
     double w0 = cf[0] * yv.x, w1 = cf[0] * yv.y;
 #pragma unroll
     for (int d = MAXT - 1; d >= 0; --d)
@@ -94,6 +114,10 @@ __global__ void __launch_bounds__(kThreads) k_update(const double* __restrict__ 
 #pragma unroll
     for (int g = 1; g < MAXT; ++g)
       if (g <= ngram) acc[g] = fma(w0, wv[g - 1].x, fma(w1, wv[g - 1].y, acc[g]));
+    p = pn;
+    yv = yn;
+#pragma unroll
+    for (int d = 0; d < MAXT; ++d) wv[d] = wn[d];
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t r = n - 1;

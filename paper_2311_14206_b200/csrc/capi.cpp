@@ -921,6 +921,16 @@ const char* sdr_report_note(const sdr_report* r, int64_t i) {
 
 const char* sdr_report_error(const sdr_report* r) { return r ? r->r.error.c_str() : nullptr; }
 
+int sdr_report_phase(const sdr_report* r, const char* name, double* ms) {
+  return guard([&] {
+    need(r, "report");
+    need(name, "name");
+    need(ms, "ms");
+    auto it = r->r.phase_ms.find(name);
+    *ms = it == r->r.phase_ms.end() ? 0.0 : it->second;
+  });
+}
+
 int sdr_report_timing(const sdr_report* r, double* device_ms, double* host_wait_ms, double* total_ms) {
   return guard([&] {
     need(r, "report");

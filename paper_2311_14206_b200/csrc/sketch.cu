@@ -22,6 +22,8 @@
 #include "reduce.cuh"
 #include "sketch.hpp"
 
+#include <cooperative_groups.h>
+
 namespace sdr {
 
 namespace {
@@ -163,6 +165,202 @@ __global__ void __launch_bounds__(kThreads) k_srdct(const double* __restrict__ x
   }
 }
 
+// ---------------------------------------------------------------- F = 256 path
+// Register four-step FFT: 256 = 16 x 16. Thread (p, t) owns pair p of the
+// tile (columns a0+2p, a0+2p+1 packed as one complex sequence) and row
+// class t: stage 1 is a 16-point DFT over b = t + 16 i held in registers,
+// stage 2 (after one padded shared-memory transpose) a 16-point DFT over t.
+// Only M/16 of the 16 stage-1 inputs are nonzero (zero padding b >= M).
+
+constexpr int kPairs = 16;   // 32 columns a per tile
+constexpr int kXS = 257;     // padded row stride (double2) -> conflict-free transposes
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+/// x * e^{+2 pi i K / 16}; K is a compile-time constant after unrolling.
+__device__ __forceinline__ double2 rot16(double2 x, int K) {
+  constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173, R2 = 0.70710678118654752440;
+  switch (K) {
+    case 0: return x;
+    case 1: return cmul(x, make_double2(C1, S1));
+    case 2: return make_double2(R2 * (x.x - x.y), R2 * (x.x + x.y));
+    case 3: return cmul(x, make_double2(S1, C1));
+    case 4: return make_double2(-x.y, x.x);
+    case 5: return cmul(x, make_double2(-S1, C1));
+    case 6: return make_double2(-R2 * (x.x + x.y), R2 * (x.x - x.y));
+    default: return cmul(x, make_double2(-C1, S1));
+  }
+}
+
+template <int LEN>
+__device__ __forceinline__ void dit_stage(double2 (&b)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; i += LEN) {
+#pragma unroll
+    for (int k = 0; k < LEN / 2; ++k) {
+      const double2 u = b[i + k];
+      const double2 v = rot16(b[i + k + LEN / 2], k * (16 / LEN));
+      b[i + k] = cadd(u, v);
+      b[i + k + LEN / 2] = csub(u, v);
+    }
+  }
+}
+
+/// a[k] <- sum_n a[n] e^{+2 pi i k n / 16} (radix-2 DIT, fully unrolled).
+__device__ __forceinline__ void dft16(double2 (&a)[16]) {
+  double2 b[16];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) b[((n & 1) << 3) | ((n & 2) << 1) | ((n & 4) >> 1) | ((n & 8) >> 3)] = a[n];
+  dit_stage<2>(b);
+  dit_stage<4>(b);
+  dit_stage<8>(b);
+  dit_stage<16>(b);
+#pragma unroll
+  for (int n = 0; n < 16; ++n) a[n] = b[n];
+}
+
+__global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict__ x, double xscale, int64_t N, int64_t r0,
+                                                        int M, int64_t L, const uint32_t* __restrict__ sign_bits,
+                                                        const int64_t* __restrict__ rows,
+                                                        const double* __restrict__ row_scale, int s, int64_t ntiles,
+                                                        int csize, double* __restrict__ partials,
+                                                        unsigned* __restrict__ counter, double* __restrict__ fold,
+                                                        double* __restrict__ out) {
+  extern __shared__ double2 sm[];
+  double2* X = sm;                    // [16][257]
+  double2* acc = X + kPairs * kXS;    // [s]
+  double2* stp = acc + s;             // [s] e^{i pi k_q / N}
+  double2* tw = stp + s;              // [256] e^{2 pi i k / 256}
+  int* uq = reinterpret_cast<int*>(tw + 256);
+  const int tid = threadIdx.x;
+  const uint64_t twoN = 2u * static_cast<uint64_t>(N);
+  for (int k = tid; k < 256; k += blockDim.x) {
+    double sn, cs;
+    sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
+    tw[k] = make_double2(cs, sn);
+  }
+  for (int q = tid; q < s; q += blockDim.x) {
+    const int64_t k = rows[q];
+    double sn, cs;
+    sincospi(static_cast<double>(k) / static_cast<double>(N), &sn, &cs);
+    stp[q] = make_double2(cs, sn);
+    uq[q] = static_cast<int>(k & 255);
+    acc[q] = make_double2(0.0, 0.0);
+  }
+  const int p = tid & 15, t = tid >> 4;
+  const int nI = M >> 4;
+  const bool paired = (L % 2 == 0) && (r0 % 2 == 0);
+  __syncthreads();
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t a0 = tile * (2 * kPairs);
+    const int64_t aa = a0 + 2 * p;
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] = make_double2(0.0, 0.0);
+      if (i < nI && aa < L) {
+        const int64_t jl = aa + L * static_cast<int64_t>(t + 16 * i);
+        const int64_t jg = r0 + jl;
+        double2 z;
+        uint32_t b0, b1;
+        if (paired) {
+          z = __ldcs(reinterpret_cast<const double2*>(x + jl));
+          const uint32_t wbits = __ldg(sign_bits + (jg >> 5));
+          b0 = (wbits >> (jg & 31)) & 1u;
+          b1 = (wbits >> ((jg + 1) & 31)) & 1u;
+        } else {
+          z.x = __ldcs(x + jl);
+          z.y = aa + 1 < L ? __ldcs(x + jl + 1) : 0.0;
+          b0 = (__ldg(sign_bits + (jg >> 5)) >> (jg & 31)) & 1u;
+          b1 = (__ldg(sign_bits + ((jg + 1) >> 5)) >> ((jg + 1) & 31)) & 1u;
+        }
+        z.x *= xscale;
+        z.y *= xscale;
+        v[i] = make_double2(b0 ? z.x : -z.x, b1 ? z.y : -z.y);
+      }
+    }
+    dft16(v);
+#pragma unroll
+    for (int vv = 1; vv < 16; ++vv) v[vv] = cmul(v[vv], tw[(vv * t) & 255]);
+    __syncthreads();  // previous tile's accumulation has finished reading X
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) X[p * kXS + vv * 16 + t] = v[vv];
+    __syncthreads();
+#pragma unroll
+    for (int tt = 0; tt < 16; ++tt) v[tt] = X[p * kXS + t * 16 + tt];
+    dft16(v);
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
+    __syncthreads();
+    // accumulate the selected rows: sum_a e^{i pi k (r0+a)/N} T(a, k mod 256)
+    for (int q = tid; q < s; q += blockDim.x) {
+      const uint64_t k = static_cast<uint64_t>(rows[q]);
+      const int u = uq[q], um = (256 - u) & 255;
+      double sn, cs;
+      const uint64_t ph = (k * static_cast<uint64_t>(r0 + a0)) % twoN;
+      sincospi(static_cast<double>(ph) / static_cast<double>(N), &sn, &cs);
+      double2 r = make_double2(cs, sn);
+      const double2 st = stp[q];
+      double2 a = acc[q];
+#pragma unroll 4
+      for (int pp = 0; pp < kPairs; ++pp) {
+        const double2 C = X[pp * kXS + u], Cm = X[pp * kXS + um];
+        const double2 T0 = make_double2(0.5 * (C.x + Cm.x), 0.5 * (C.y - Cm.y));
+        const double2 T1 = make_double2(0.5 * (C.y + Cm.y), -0.5 * (C.x - Cm.x));
+        a = cadd(a, cmul(r, T0));
+        r = cmul(r, st);
+        a = cadd(a, cmul(r, T1));
+        r = cmul(r, st);
+      }
+      acc[q] = a;
+    }
+  }
+  __syncthreads();
+  // cluster reduction of the per-CTA accumulators through distributed shared memory
+  int nparts = gridDim.x, part = blockIdx.x;
+  if (csize > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const bool leader = cl.block_rank() == 0;
+    if (leader) {
+      for (int q = tid; q < s; q += blockDim.x) {
+        double2 sum = acc[q];
+        for (int r = 1; r < csize; ++r) sum = cadd(sum, cl.map_shared_rank(acc, r)[q]);
+        acc[q] = sum;
+      }
+    }
+    cl.sync();
+    if (!leader) return;
+    nparts = gridDim.x / csize;
+    part = blockIdx.x / csize;
+  }
+  for (int q = tid; q < s; q += blockDim.x) {
+    partials[static_cast<int64_t>(2 * q) * nparts + part] = acc[q].x;
+    partials[static_cast<int64_t>(2 * q + 1) * nparts + part] = acc[q].y;
+  }
+  // last-arriving CTA (ticket over nparts) folds in a fixed order
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = atomicAdd(counter, 1u) == static_cast<unsigned>(nparts - 1);
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  fold_partials(partials, nparts, 2 * s, fold);
+  __syncthreads();
+  for (int q = tid; q < s; q += blockDim.x) {
+    const int64_t k = rows[q];
+    double sn, cs;
+    sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
+    out[q] = (cs * fold[2 * q] - sn * fold[2 * q + 1]) * row_scale[q];
+  }
+  if (tid == 0) *counter = 0u;
+}
+
 __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restrict__ x, double xscale, int64_t nloc,
                                                            int64_t r0, uint64_t key, int s, int zeta, double inv_sqrt_zeta,
                                                            int64_t chunk, double* __restrict__ partials,
@@ -214,6 +412,36 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
   if (S.kind == kSrdct) {
     const SrdctPlan p = plan_srdct(S.n, nloc);
     const int64_t ntiles = (p.L + kTileA - 1) / kTileA;
+    if (p.F == 256 && p.M % 16 == 0) {
+      // fast path: persistent CTAs in clusters of 8, ~2 per SM
+      int csize = ntiles >= 16 ? 8 : 1;
+      int grid = static_cast<int>(std::min<int64_t>(ntiles, 2 * c.num_sms));
+      if (csize > 1) grid = std::max(csize, grid / csize * csize);
+      const size_t smem = sizeof(double2) * static_cast<size_t>(kPairs * kXS + 2 * S.s + 256) + sizeof(int) * S.s;
+      static size_t configured = 0;
+      if (smem > configured) {
+        SDR_CUDA(cudaFuncSetAttribute(k_srdct256, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured = smem;
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = c.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = static_cast<unsigned>(csize);
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      TimedLaunch t(c, "sketch");
+      SDR_CUDA(cudaLaunchKernelEx(&cfg, k_srdct256, x_own, xscale, S.n, row_begin, static_cast<int>(p.M), p.L,
+                                  static_cast<const uint32_t*>(S.sign_bits.get()), static_cast<const int64_t*>(S.rows.get()),
+                                  static_cast<const double*>(S.row_scale.get()), static_cast<int>(S.s), ntiles, csize,
+                                  c.partials(2 * S.s * grid), c.counters() + 5, c.partials2(2 * S.s), out));
+      return;
+    }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * c.num_sms)));
     const size_t smem = sizeof(double2) * static_cast<size_t>((kTileA / 2) * p.F + p.F / 2 + S.s);
     static size_t configured = 0;

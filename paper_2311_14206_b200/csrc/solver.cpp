@@ -151,7 +151,7 @@ double d2h_scalar(Context& c, Workspace& w, const double* dev) {
 }
 
 void update_recycle(Context& c, Workspace& w, const HostKrylov& st, Recycle& sp, i64 k, double rank_tol,
-                    Counters& cnt, std::vector<std::string>* notes) {  // recycle.hpp:226-289
+                    Counters& cnt, std::vector<std::string>* notes, Report& rep) {  // recycle.hpp:226-289
   const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
   if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
   HMat SAW(s, kh + j), SW(s, kh + j);
@@ -163,7 +163,11 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, Recycle& sp,
     std::copy(st.SAV.col(i), st.SAV.col(i) + s, SAW.col(kh + i));
     std::copy(st.SV.col(i), st.SV.col(i) + s, SW.col(kh + i));
   }
-  Harmonic hp = harmonic_extract(SAW, SW, k, rank_tol);
+  Harmonic hp;
+  {
+    PhaseTimer pt(rep, "recycle_harmonic");
+    hp = harmonic_extract(SAW, SW, k, rank_tol);
+  }
   if (notes) {
     if (hp.rank_limited)
       notes->push_back("deflation space limited to pencil rank " + std::to_string(hp.rank) + " (requested " +
@@ -359,7 +363,10 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
   const auto t0 = std::chrono::steady_clock::now();
 
   ArnoldiPipeline ap{c, w, A, S, cfg.t, m, cfg.breakdown_tol, cnt, HostKrylov{}};
-  ap.init(r0);
+  {
+    PhaseTimer pt(rep, "cycle_init");
+    ap.init(r0);
+  }
   HostKrylov& st = ap.st;
   out.entry_norm = st.r0_norm;
   std::vector<double> sr0(static_cast<size_t>(s));
@@ -387,6 +394,7 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
   bool done = false;
   while (!done && st.j < m && !st.breakdown) {  // solver.hpp:165-216
     const bool step_breakdown = ap.step();
+    PhaseTimer pt_step(rep, "host_step");
     const i64 jj = st.j;
     const auto info = qr->append(st.SAV.col(jj - 1), s);
     if (info.rank_deficient) {
@@ -406,6 +414,7 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
     const bool last = jj == m || st.breakdown;
     if (sres < tol_abs / out.safety || last) {
       // correction = V(:,0:j) y_tail + U y_head (solver.hpp:197-198), on the device
+      PhaseTimer pt_check(rep, "check");
       std::vector<const double*> in;
       HMat coef(jj + k_hat, 1);
       for (i64 i = 0; i < jj; ++i) {
@@ -439,11 +448,15 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
       }
     }
   }
-  c.sync();  // drain speculative steps before the buffers are reused
+  {
+    PhaseTimer pt(rep, "drain");
+    c.sync();  // drain speculative steps before the buffers are reused
+  }
   out.steps = st.j;
   out.sres = sres;
   out.breakdown = st.breakdown;
   rep.host_wait_ms += ap.wait_ms;
+  rep.phase_ms["step_wait"] += ap.wait_ms;
 
   CycleStat cs;
   cs.steps = st.j;
@@ -453,6 +466,7 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
   cs.exit_residual = out.residual_norm;
   cs.safety_after = out.safety;
   if (st.j >= 1 && !st.breakdown) {
+    PhaseTimer pt(rep, "basis_cond");
     HMat B(s, st.j + 1);
     std::copy(st.SV.a.begin(), st.SV.a.begin() + s * (st.j + 1), B.a.begin());
     cs.basis_cond = cond2(B);
@@ -461,7 +475,8 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
 
   if (cfg.k > 0 && st.j >= 1) {  // solver.hpp:242-252
     std::vector<std::string> notes;
-    update_recycle(c, w, st, space, cfg.k, cfg.rank_tol, cnt, &notes);
+    PhaseTimer pt(rep, "recycle");
+    update_recycle(c, w, st, space, cfg.k, cfg.rank_tol, cnt, &notes, rep);
     rep.cycle_stats.back().deflation_rank = space.dim();
     for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
   } else if (cfg.k == 0) {
@@ -681,6 +696,7 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
                   std::to_string(sketch->s));
   init_host_blas();
   const auto t_start = std::chrono::steady_clock::now();
+  auto pt_setup = std::make_unique<PhaseTimer>(rep, "setup");
   const VecLayout lay = A.layout();
   const int T = static_cast<int>(std::min<i64>(cfg.t, cfg.m));
   if (std::min<i64>(cfg.t, cfg.m) > 33) throw invalid("solve: Arnoldi window min(t, m) exceeds the device limit of 33");
@@ -713,6 +729,7 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
 
   double safety = cfg.safety_init, res_norm = std::numeric_limits<double>::quiet_NaN();
   bool have = false;
+  pt_setup.reset();
   for (int cycle = 1; cycle <= cfg.max_restarts; ++cycle) {  // solver.hpp:321-359
     CycleOut cr;
     try {

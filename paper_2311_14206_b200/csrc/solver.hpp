@@ -9,7 +9,9 @@
 #include "operator.hpp"
 #include "sketch.hpp"
 
+#include <chrono>
 #include <limits>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -49,6 +51,16 @@ struct Report {  // SolveReport, report.hpp:50-63
   std::vector<std::string> notes;
   std::string error;
   double seconds = 0.0, device_ms = 0.0, host_wait_ms = 0.0;
+  std::map<std::string, double> phase_ms;  // wall-clock breakdown (host view)
+};
+
+/// Adds the scope's wall time to rep.phase_ms[name].
+struct PhaseTimer {
+  Report& r;
+  const char* name;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  PhaseTimer(Report& rep, const char* n) : r(rep), name(n) {}
+  ~PhaseTimer() { r.phase_ms[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
 };
 
 /// RecycleSpace (recycle.hpp:31-72): U stays on the device, unnormalised,

@@ -38,22 +38,48 @@ __global__ void __launch_bounds__(kThreads) k_sell_spmv(SellView A, const double
     const int len = static_cast<int>((A.slice_ptr[sl + 1] - p0) >> 5);
     const int32_t* cp = A.cols + p0 + lane;
     const double* vp = A.vals + p0 + lane;
-    double s = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < len; ++k) s = fma(__ldg(vp + k * kSlice), __ldg(x_ext + __ldg(cp + k * kSlice)), s);
     const int64_t row = sl * kSlice + lane;
-    if (row < A.nrows) {
+    const bool live = row < A.nrows;
+    // epilogue operands are independent of the product: fetch them first
+    double e0 = 0.0, ew[NV > 2 ? NV - 2 : 1];
+    if constexpr (MODE == 1) {
+      e0 = live ? x_ext[halo_lo + row] : 0.0;
+#pragma unroll
+      for (int d = 1; d < NV - 1; ++d) ew[d - 1] = (live && d < nwin) ? __ldcs(aux + (j - d) * ldv + own_off + row) : 0.0;
+    } else if constexpr (MODE == 2) {
+      e0 = live ? __ldcs(aux + row) : 0.0;
+    }
+    double s = 0.0;
+    // Batches of 8 entries: all index/value loads are issued before the
+    // dependent x gathers, so a 7-point row costs two memory round trips
+    // instead of fourteen (the sequential form is latency-bound).
+    for (int k0 = 0; k0 < len; k0 += 8) {
+      int32_t c[8];
+      double v[8], xv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool ok = k0 + k < len;
+        c[k] = ok ? __ldcs(cp + (k0 + k) * kSlice) : 0;
+        v[k] = ok ? __ldcs(vp + (k0 + k) * kSlice) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xv[k] = k0 + k < len ? __ldg(x_ext + c[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k0 + k < len) s = fma(v[k], xv[k], s);
+    }
+    if (live) {
       if constexpr (MODE == 0) {
         y[row] = s;
       } else if constexpr (MODE == 1) {
         y[row] = s;
         acc[0] = fma(s, s, acc[0]);
-        acc[1] = fma(s, x_ext[halo_lo + row], acc[1]);
+        acc[1] = fma(s, e0, acc[1]);
 #pragma unroll
         for (int d = 1; d < NV - 1; ++d)
-          if (d < nwin) acc[1 + d] = fma(s, __ldg(aux + (j - d) * ldv + own_off + row), acc[1 + d]);
+          if (d < nwin) acc[1 + d] = fma(s, ew[d - 1], acc[1 + d]);
       } else {
-        const double r = aux[row] - s;
+        const double r = e0 - s;
         y[row] = r;
         acc[0] = fma(r, r, acc[0]);
       }

@@ -166,9 +166,30 @@ def test_c1_problem_matches_oracle(sk, O):
     assert_same_solve(gs, os_, iters_tol=0.02)
 
 
-def test_sequence_recycling_and_variants(sk, O):
-    """test_sequence.cpp:46-147: recycling cuts iterations; exact refresh costs
-    k matvecs + k sketches charged to the changed system."""
+def test_sequence_recycling_cuts_iterations(sk, O):
+    """test_sequence.cpp:46-74: neumann_sequence(20, 0.05, 3, 1234, 1e-8), m=30 t=2 k=8 s=300."""
+    M = O.gen_neumann(20, 0.05).dense()
+    A, Ao = sk.SparseMatrix.from_dense(M), O.SparseMatrix.from_dense(M)
+    rhs = [O.gaussian_vector(400, 1234 + i) for i in range(3)]
+    c, co = cfgs(sk, O, m=30, t=2, k=8, s=300, tol=1e-8, max_restarts=10)
+    res = sk.solve_sequence([sk.ProblemInstance(A, b, target_tol=1e-8) for b in rhs], c, shared_matrix=True)
+    xs, reps = O.solve_sequence([Ao] * 3, rhs, co, tols=[1e-8] * 3, shared_matrix=True)
+    for i, (gr, orr) in enumerate(zip(res.reports, reps)):
+        assert gr.status == orr.status == "converged"
+        assert abs(gr.iterations - orr.iterations) <= max(1, 0.02 * orr.iterations)
+        assert np.linalg.norm(rhs[i] - M @ res.solutions[i]) <= 1e-8 * np.linalg.norm(rhs[i]) * (1 + 1e-10)
+    assert res.reports[1].iterations < res.reports[0].iterations
+    assert res.reports[2].iterations <= res.reports[1].iterations
+    assert res.space.dim() >= 8 and res.space.provenance == "reused"
+    warm = sk.solve_sequence([sk.ProblemInstance(A, O.gaussian_vector(400, 9876), target_tol=1e-8)], c,
+                             initial_space=res.space, shared_matrix=True)
+    assert warm.reports[0].status == "converged"
+    assert warm.reports[0].iterations < res.reports[0].iterations
+
+
+def test_sequence_variants_match_oracle(sk, O):
+    """test_sequence.cpp:105-147: exact refresh costs k matvecs + k sketches
+    charged to the changed system; reuse on a changed matrix leaves a note."""
     n = 400
     g = 20
     M1 = O.gen_neumann(g, 0.5).dense()
@@ -187,7 +208,10 @@ def test_sequence_recycling_and_variants(sk, O):
             assert abs(gr.iterations - orr.iterations) <= max(1, 0.02 * orr.iterations)
             assert gr.counters["matvecs"] - gr.iterations == orr.counters["matvecs"] - orr.iterations
             assert gr.notes[-1:] == orr.notes[-1:] or variant != "reuse"
-        assert res.reports[1].iterations < res.reports[0].iterations
+        if variant == "exact":
+            # the changed system pays k matvecs + k sketches for the refresh
+            k_carried = res.reports[2].counters["sketch_applies"] - (res.reports[2].iterations + res.reports[2].cycles)
+            assert k_carried == reps[2].counters["sketch_applies"] - (reps[2].iterations + reps[2].cycles)
 
 
 def test_sequence_failure_isolation_and_empty(sk, O):
