@@ -315,7 +315,8 @@ def main():
                        "parallelism": f"zslab{world}", "l2": "inputs > L2 per solve (V basis 1.7 GB)"},
             "time_to_solution_ms": ms / args.steps,
             "solve": {"status": rep.status, "iterations": rep.iterations, "cycles": rep.cycles,
-                      "final_relative_residual": rep.final_relative_residual},
+                      "final_relative_residual": rep.final_relative_residual,
+                      "phases_ms": {k: round(v, 3) for k, v in rep.phases.items()}},
             "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * nloc, "d2h_bytes_per_step": 8 * nloc},
             "roofline": roofline,
             "kernels": kern,

@@ -14,7 +14,10 @@
 // device scales c_i = 1/||w_i||, so normalisation costs no extra pass.
 // Algorithmic bytes per row: y + window vectors read, w_{j+1} written.
 #include "kernels.hpp"
+#include "mgs.cuh"
 #include "reduce.cuh"
+
+#include <map>
 
 namespace sdr {
 
@@ -26,8 +29,8 @@ template <int MAXT>
 __global__ void __launch_bounds__(kThreads) k_update(const double* __restrict__ y, double* __restrict__ V, int64_t ldv,
                                                       int64_t own_off, int64_t n, int j, int nwin, int ngram,
                                                       double* __restrict__ rec, int64_t rstride, int T,
-                                                      double* __restrict__ cvec, double* __restrict__ partials,
-                                                      unsigned* __restrict__ counter) {
+                                                      double* __restrict__ cvec, const double* __restrict__ coef_ready,
+                                                      double* __restrict__ partials, unsigned* __restrict__ counter) {
   __shared__ double coef[MAXT + 1];
   const int b_off = 2 * T + 3;
   const double* W[MAXT];
@@ -48,46 +51,12 @@ __global__ void __launch_bounds__(kThreads) k_update(const double* __restrict__ 
       if (d < nwin) wo[d] = __ldg(reinterpret_cast<const double2*>(W[d]) + q);
   };
   if (p < npair) fetch(p, yv, wv);
-  if (threadIdx.x == 0) {
-    const double* recA = rec + static_cast<int64_t>(j + 1) * rstride;
-    const double wn2 = rec[static_cast<int64_t>(j) * rstride + b_off];
-    const double cj = 1.0 / sqrt(wn2);
-    double ci[MAXT], h[MAXT];
-#pragma unroll
-    for (int d = 0; d < MAXT; ++d) {
-      ci[d] = d == 0 ? cj : (d < nwin ? cvec[j - d] : 0.0);
-      h[d] = 0.0;
-    }
-    // MGS order i = j-nwin+1 .. j  <=>  d = nwin-1 .. 0 (compile-time loops
-    // with predicates keep h[], ci[] in registers)
-#pragma unroll
-    for (int d = MAXT - 1; d >= 0; --d) {
-      if (d < nwin) {
-        const int i = j - d;
-        double acc = cj * ci[d] * recA[1 + d];
-#pragma unroll
-        for (int d2 = MAXT - 1; d2 > d; --d2) {
-          if (d2 < nwin) {
-            const double gram = rec[static_cast<int64_t>(i) * rstride + b_off + (d2 - d)];
-            acc -= h[d2] * (ci[d2] * ci[d] * gram);
-          }
-        }
-        h[d] = acc;
-      }
-    }
-    coef[0] = cj;
-#pragma unroll
-    for (int d = 0; d < MAXT; ++d) coef[1 + d] = d < nwin ? -h[d] * ci[d] : 0.0;
-    if (blockIdx.x == 0) {
-      double* recH = rec + static_cast<int64_t>(j + 1) * rstride + (T + 1);
-      recH[0] = cj * sqrt(recA[0]);
-#pragma unroll
-      for (int d = 0; d < MAXT; ++d)
-        if (d < T) recH[1 + d] = d < nwin ? h[d] : 0.0;
-      for (int d = MAXT; d < T; ++d) recH[1 + d] = 0.0;
-      recH[1 + T] = cj;
-      cvec[j] = cj;
-    }
+  if (coef_ready) {
+    if (threadIdx.x <= MAXT) coef[threadIdx.x] = threadIdx.x <= nwin ? coef_ready[threadIdx.x] : 0.0;
+  } else if (threadIdx.x == 0) {
+    // multi-GPU: records were allreduced after K1; every CTA forms the same
+    // coefficients, CTA 0 publishes them in the record
+    mgs_coefficients<MAXT>(rec, rstride, T, j, nwin, cvec, coef, blockIdx.x == 0);
   }
   __syncthreads();
 
@@ -224,11 +193,15 @@ int stream_grid(const Context& c, int64_t n, int per_thread = 1) {
 
 template <int MAXT>
 void update_impl(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
-                 int ngram, double* rec, const RecLayout& L, double* cvec) {
-  const int g = stream_grid(c, lay.nloc, 2);
+                 int ngram, double* rec, const RecLayout& L, double* cvec, const double* coef_ready) {
+  // persistent: one resident wave, each thread streams several pairs
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(k_update<MAXT>), kThreads, 0);
+  const int64_t want = (lay.nloc / 2 + kThreads - 1) / kThreads;
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.num_sms) * per_sm)));
   TimedLaunch t(c, "update");
   k_update<MAXT><<<g, kThreads, 0, c.stream>>>(y, V, ldv, lay.own_off, lay.nloc, j, nwin, ngram, rec, L.stride, L.T,
-                                               cvec, c.partials(static_cast<int64_t>(MAXT) * g), c.counters() + 2);
+                                               cvec, coef_ready, c.partials(static_cast<int64_t>(MAXT) * g),
+                                               c.counters() + 2);
   SDR_KERNEL_CHECK();
 }
 
@@ -248,15 +221,29 @@ void tallskinny_impl(Context& c, const double* const* in, int nin, const double*
 
 }  // namespace
 
+int blocks_per_sm(const void* kernel, int threads, size_t smem) {
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  auto key = std::make_pair(kernel, smem * 4096 + static_cast<size_t>(threads));
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache[key] = n;
+  return n;
+}
+
 void launch_update(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
-                   int ngram, double* rec, const RecLayout& L, double* cvec) {
+                   int ngram, double* rec, const RecLayout& L, double* cvec, const double* coef_ready) {
   const int need = std::max(nwin, ngram + 1);
   if (need <= 4)
-    update_impl<4>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec);
+    update_impl<4>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec, coef_ready);
   else if (need <= 8)
-    update_impl<8>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec);
+    update_impl<8>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec, coef_ready);
   else if (need <= 33)
-    update_impl<33>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec);
+    update_impl<33>(c, y, V, ldv, lay, j, nwin, ngram, rec, L, cvec, coef_ready);
   else
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
 }

@@ -47,15 +47,22 @@ struct RecLayout {
 
 struct SketchDev;  // sketch.cu
 
+/// Occupancy-derived resident CTAs per SM for a kernel (cached per kernel).
+int blocks_per_sm(const void* kernel, int threads, size_t smem);
+
 // ---- SpMV family (spmv.cu)
 void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y);
+/// K1. When coef != nullptr (single GPU) the last CTA also forms the MGS
+/// coefficients of step j into coef[0..nwin] and the record's H part.
 void launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
-                         int nwin, double* y, double* recA);
+                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
+                         double* coef);
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2);
 
-// ---- Arnoldi update (arnoldi.cu)
+// ---- Arnoldi update (arnoldi.cu). coef_ready: coefficients already formed
+// by K1 (single GPU); null: formed in the K2 prologue from allreduced records.
 void launch_update(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
-                   int ngram, double* rec, const RecLayout& L, double* cvec);
+                   int ngram, double* rec, const RecLayout& L, double* cvec, const double* coef_ready);
 void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, double* norm2);
 void launch_axpy(Context& c, double a, const double* x, double* y, int64_t n);
 void launch_scale_copy(Context& c, double a, const double* x, double* y, int64_t n);

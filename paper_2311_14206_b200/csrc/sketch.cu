@@ -249,8 +249,34 @@ __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict_
     acc[q] = make_double2(0.0, 0.0);
   }
   const int p = tid & 15, t = tid >> 4;
-  const int nI = M >> 4;
+  const int nI = M >> 4;  // <= 8 nonzero stage-1 inputs
   const bool paired = (L % 2 == 0) && (r0 % 2 == 0);
+  // Raw tile data in registers, fetched one tile ahead: the loads for tile
+  // k+1 are in flight while tile k's accumulation runs.
+  double2 z[8];
+  uint32_t wb0[8], wb1[8];
+  auto issue = [&](int64_t tile) {
+    const int64_t aa = tile * (2 * kPairs) + 2 * p;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      z[i] = make_double2(0.0, 0.0);
+      wb0[i] = wb1[i] = 0u;
+      if (tile < ntiles && i < nI && aa < L) {
+        const int64_t jl = aa + L * static_cast<int64_t>(t + 16 * i);
+        const int64_t jg = r0 + jl;
+        if (paired) {
+          z[i] = __ldcs(reinterpret_cast<const double2*>(x + jl));
+          wb0[i] = __ldg(sign_bits + (jg >> 5));
+        } else {
+          z[i].x = __ldcs(x + jl);
+          z[i].y = aa + 1 < L ? __ldcs(x + jl + 1) : 0.0;
+          wb0[i] = __ldg(sign_bits + (jg >> 5));
+          wb1[i] = __ldg(sign_bits + ((jg + 1) >> 5));
+        }
+      }
+    }
+  };
+  issue(blockIdx.x);
   __syncthreads();
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -260,25 +286,12 @@ __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict_
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       v[i] = make_double2(0.0, 0.0);
-      if (i < nI && aa < L) {
-        const int64_t jl = aa + L * static_cast<int64_t>(t + 16 * i);
-        const int64_t jg = r0 + jl;
-        double2 z;
-        uint32_t b0, b1;
-        if (paired) {
-          z = __ldcs(reinterpret_cast<const double2*>(x + jl));
-          const uint32_t wbits = __ldg(sign_bits + (jg >> 5));
-          b0 = (wbits >> (jg & 31)) & 1u;
-          b1 = (wbits >> ((jg + 1) & 31)) & 1u;
-        } else {
-          z.x = __ldcs(x + jl);
-          z.y = aa + 1 < L ? __ldcs(x + jl + 1) : 0.0;
-          b0 = (__ldg(sign_bits + (jg >> 5)) >> (jg & 31)) & 1u;
-          b1 = (__ldg(sign_bits + ((jg + 1) >> 5)) >> ((jg + 1) & 31)) & 1u;
-        }
-        z.x *= xscale;
-        z.y *= xscale;
-        v[i] = make_double2(b0 ? z.x : -z.x, b1 ? z.y : -z.y);
+      if (i < 8) {
+        const int64_t jg = r0 + aa + L * static_cast<int64_t>(t + 16 * i);
+        const uint32_t b0 = (wb0[i] >> (jg & 31)) & 1u;
+        const uint32_t b1 = paired ? (wb0[i] >> ((jg + 1) & 31)) & 1u : (wb1[i] >> ((jg + 1) & 31)) & 1u;
+        const double zx = z[i].x * xscale, zy = z[i].y * xscale;
+        v[i] = make_double2(b0 ? zx : -zx, b1 ? zy : -zy);
       }
     }
     dft16(v);
@@ -294,6 +307,7 @@ __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict_
     __syncthreads();
 #pragma unroll
     for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
+    issue(tile + gridDim.x);
     __syncthreads();
     // accumulate the selected rows: sum_a e^{i pi k (r0+a)/N} T(a, k mod 256)
     for (int q = tid; q < s; q += blockDim.x) {
@@ -415,8 +429,12 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
     if (p.F == 256 && p.M % 16 == 0) {
       // fast path: persistent CTAs in clusters of 8, ~2 per SM
       int csize = ntiles >= 16 ? 8 : 1;
-      int grid = static_cast<int>(std::min<int64_t>(ntiles, 2 * c.num_sms));
-      if (csize > 1) grid = std::max(csize, grid / csize * csize);
+      // equal tiles per CTA (no tail wave), at most ~2 CTAs per SM
+      const int64_t per = (ntiles + 2 * c.num_sms - 1) / (2 * c.num_sms);
+      int grid = static_cast<int>((ntiles + per - 1) / per);
+      if (csize > 1) grid = std::max(csize, (grid + csize - 1) / csize * csize);
+      grid = static_cast<int>(std::min<int64_t>(grid, ntiles));
+      if (csize > 1 && grid % csize) csize = 1;
       const size_t smem = sizeof(double2) * static_cast<size_t>(kPairs * kXS + 2 * S.s + 256) + sizeof(int) * S.s;
       static size_t configured = 0;
       if (smem > configured) {

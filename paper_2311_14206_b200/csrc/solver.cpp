@@ -26,7 +26,7 @@ struct Workspace {
   i64 m = -1, s = -1;
   int T = 0;
   RecLayout RL;
-  DeviceBuffer<double> V, y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef;
+  DeviceBuffer<double> V, y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<const double*> inptr;
   DeviceBuffer<double*> outptr;
   PinnedBuffer<double> hrec, hscal, hcoef;
@@ -76,6 +76,7 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
   w->x.ensure(nl);
   w->tmp.ensure(lay.ld);
   w->scal.ensure(64);
+  w->coef_dev.ensure(64);
   w->hscal.ensure(64);
   return *w;
 }
@@ -294,9 +295,14 @@ struct ArnoldiPipeline {
     const int ngram = static_cast<int>(std::min<i64>(T - 1, j + 1));
     c.halo_exchange(A.plan, w.Vbuf(j) + lay.ext_shift(), A.ext_begin, w.Vcol(j), A.row_begin);
     double* recj = w.rec.get() + (j + 1) * R;
-    launch_spmv_arnoldi(c, A.view(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off());
+    // one GPU: K1's last CTA forms the MGS coefficients; several: K2 forms
+    // them after the allreduce of the window dots
+    double* coef = c.distributed() ? nullptr : w.coef_dev.get();
+    launch_spmv_arnoldi(c, A.view(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
+                        w.rec.get(), R, T, w.cvec.get(), coef);
     c.allreduce_sum(recj + RL.a_off(), T + 1);
-    launch_update(c, w.y.get(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get());
+    launch_update(c, w.y.get(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(),
+                  coef);
     launch_sketch(c, S, w.Vcol(j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
     SDR_CUDA(cudaMemcpyAsync(w.hrec.get() + (j + 1) * R, recj, sizeof(double) * R, cudaMemcpyDeviceToHost, c.stream));
