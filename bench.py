@@ -46,50 +46,64 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed
+    region through NVML (the library nvidia-smi queries; polling in-process
+    avoids a competing nvidia-smi client contending for the driver)."""
 
-    def __init__(self, device):
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
+    def __init__(self, device, period=0.1):
         self.device = device
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
-        self._proc = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                           "--format=csv,noheader,nounits", "-lms", "100"],
-                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         except Exception:
-            self._proc = None
+            self._nv = None
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
+    def _sample(self):
+        nv = self._nv
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.samples.append((sm, rs))
+
+    def _run(self):
+        while not self._stop.wait(self.period):
+            try:
+                self._sample()
+            except Exception:
+                break
 
     def __exit__(self, *a):
-        if self._proc:
-            self._proc.terminate()
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join(timeout=2)
             try:
-                self._proc.wait(timeout=2)
+                self._sample()
             except Exception:
-                self._proc.kill()
+                pass
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for _, rs in self.samples for name, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 def dist_env():

@@ -56,23 +56,47 @@ __device__ __forceinline__ bool last_block_done(unsigned* counter) {
 }
 
 /// In the last CTA: out[k * out_stride] = sum_b partials[k * nblocks + b] for
-/// k < nv, in a fixed lane/tree order. One warp per value.
-__device__ __forceinline__ void fold_partials(const double* partials, int nblocks, int nv, double* out,
-                                              int out_stride = 1) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = warp; k < nv; k += nw) {
-    const double* p = partials + static_cast<int64_t>(k) * nblocks;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int b = lane;
-    for (; b + 96 < nblocks; b += 128) {
-      a0 += __ldcg(p + b);
-      a1 += __ldcg(p + b + 32);
-      a2 += __ldcg(p + b + 64);
-      a3 += __ldcg(p + b + 96);
+/// k < nv, in a fixed order. Wide two-level fold: the CTA's threads split
+/// (value, block-group) pairs so every thread issues a handful of
+/// independent loads (one or two L2 round trips in total instead of one per
+/// value), then each value's group sums are combined in group order.
+/// Requires blockDim.x <= 1024 and a multiple of 32.
+static __device__ __noinline__ void fold_partials(const double* partials, int nblocks, int nv, double* out,
+                                           int out_stride = 1) {
+  __shared__ double red[1024];
+  const int T = blockDim.x, t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5, nw = T >> 5;
+  for (int k0 = 0; k0 < nv; k0 += T) {
+    const int nk = min(T, nv - k0);
+    const int G = T / nk;  // block groups per value
+    const int k = t % nk, g = t / nk;
+    if (g < G) {
+      const double* p = partials + static_cast<int64_t>(k0 + k) * nblocks;
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = 0.0;
+      int b = g;
+      for (; b + 7 * G < nblocks; b += 8 * G) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += __ldcg(p + b + u * G);
+      }
+      for (; b < nblocks; b += G) a[0] += __ldcg(p + b);
+      red[g * nk + k] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
-    for (; b < nblocks; b += 32) a0 += __ldcg(p + b);
-    double s = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) out[static_cast<int64_t>(k) * out_stride] = s;
+    __syncthreads();
+    if (nk <= nw) {
+      if (warp < nk) {
+        double v = 0.0;
+        for (int gg = lane; gg < G; gg += 32) v += red[gg * nk + warp];
+        v = warp_sum(v);
+        if (lane == 0) out[static_cast<int64_t>(k0 + warp) * out_stride] = v;
+      }
+    } else if (t < nk) {
+      double v = 0.0;
+      for (int gg = 0; gg < G; ++gg) v += red[gg * nk + t];
+      out[static_cast<int64_t>(k0 + t) * out_stride] = v;
+    }
+    __syncthreads();
   }
 }
 

@@ -220,6 +220,24 @@ __device__ __forceinline__ void dft16(double2 (&a)[16]) {
   for (int n = 0; n < 16; ++n) a[n] = b[n];
 }
 
+/// dft16 for inputs a[8..15] == 0 (zero-padded stage 1 when M = 128): after
+/// the bit-reversal every first-stage butterfly pairs a value with a zero.
+__device__ __forceinline__ void dft16_half(double2 (&a)[16]) {
+  double2 b[16];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int n = ((2 * m) & 1) << 3 | ((2 * m) & 2) << 1 | ((2 * m) & 4) >> 1 | ((2 * m) & 8) >> 3;
+    b[2 * m] = a[n];
+    b[2 * m + 1] = a[n];
+  }
+  dit_stage<4>(b);
+  dit_stage<8>(b);
+  dit_stage<16>(b);
+#pragma unroll
+  for (int n = 0; n < 16; ++n) a[n] = b[n];
+}
+
+template <int NI, bool PAIRED>
 __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict__ x, double xscale, int64_t N, int64_t r0,
                                                         int M, int64_t L, const uint32_t* __restrict__ sign_bits,
                                                         const int64_t* __restrict__ rows,
@@ -230,8 +248,10 @@ __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict_
   extern __shared__ double2 sm[];
   double2* X = sm;                    // [16][257]
   double2* acc = X + kPairs * kXS;    // [s]
-  double2* stp = acc + s;             // [s] e^{i pi k_q / N}
-  double2* tw = stp + s;              // [256] e^{2 pi i k / 256}
+  double2* zq = acc + s;              // [s] e^{2 i pi k_q / N}  (two columns per pair)
+  double2* ga = zq + s;               // [s] (1 - i e^{i pi k/N}) / 2
+  double2* gb = ga + s;               // [s] (1 + i e^{i pi k/N}) / 2
+  double2* tw = gb + s;               // [256] e^{2 pi i k / 256}
   int* uq = reinterpret_cast<int*>(tw + 256);
   const int tid = threadIdx.x;
   const uint64_t twoN = 2u * static_cast<uint64_t>(N);
@@ -244,27 +264,30 @@ __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict_
     const int64_t k = rows[q];
     double sn, cs;
     sincospi(static_cast<double>(k) / static_cast<double>(N), &sn, &cs);
-    stp[q] = make_double2(cs, sn);
+    ga[q] = make_double2(0.5 * (1.0 + sn), -0.5 * cs);
+    gb[q] = make_double2(0.5 * (1.0 - sn), 0.5 * cs);
+    sincospi(static_cast<double>((2 * static_cast<uint64_t>(k)) % twoN) / static_cast<double>(N), &sn, &cs);
+    zq[q] = make_double2(cs, sn);
     uq[q] = static_cast<int>(k & 255);
     acc[q] = make_double2(0.0, 0.0);
   }
   const int p = tid & 15, t = tid >> 4;
-  const int nI = M >> 4;  // <= 8 nonzero stage-1 inputs
-  const bool paired = (L % 2 == 0) && (r0 % 2 == 0);
+  const int nI = NI ? NI : (M >> 4);  // <= 8 nonzero stage-1 inputs
   // Raw tile data in registers, fetched one tile ahead: the loads for tile
   // k+1 are in flight while tile k's accumulation runs.
   double2 z[8];
-  uint32_t wb0[8], wb1[8];
+  uint32_t wb0[8], wb1[PAIRED ? 1 : 8];
   auto issue = [&](int64_t tile) {
     const int64_t aa = tile * (2 * kPairs) + 2 * p;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       z[i] = make_double2(0.0, 0.0);
-      wb0[i] = wb1[i] = 0u;
+      wb0[i] = 0u;
+      if constexpr (!PAIRED) wb1[i] = 0u;
       if (tile < ntiles && i < nI && aa < L) {
         const int64_t jl = aa + L * static_cast<int64_t>(t + 16 * i);
         const int64_t jg = r0 + jl;
-        if (paired) {
+        if constexpr (PAIRED) {
           z[i] = __ldcs(reinterpret_cast<const double2*>(x + jl));
           wb0[i] = __ldg(sign_bits + (jg >> 5));
         } else {
@@ -289,12 +312,15 @@ __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict_
       if (i < 8) {
         const int64_t jg = r0 + aa + L * static_cast<int64_t>(t + 16 * i);
         const uint32_t b0 = (wb0[i] >> (jg & 31)) & 1u;
-        const uint32_t b1 = paired ? (wb0[i] >> ((jg + 1) & 31)) & 1u : (wb1[i] >> ((jg + 1) & 31)) & 1u;
+        uint32_t b1;
+        if constexpr (PAIRED) b1 = (wb0[i] >> ((jg + 1) & 31)) & 1u;
+        else b1 = (wb1[i] >> ((jg + 1) & 31)) & 1u;
         const double zx = z[i].x * xscale, zy = z[i].y * xscale;
         v[i] = make_double2(b0 ? zx : -zx, b1 ? zy : -zy);
       }
     }
-    dft16(v);
+    if constexpr (NI == 8) dft16_half(v);
+    else dft16(v);
 #pragma unroll
     for (int vv = 1; vv < 16; ++vv) v[vv] = cmul(v[vv], tw[(vv * t) & 255]);
     __syncthreads();  // previous tile's accumulation has finished reading X
@@ -309,27 +335,29 @@ __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict_
     for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
     issue(tile + gridDim.x);
     __syncthreads();
-    // accumulate the selected rows: sum_a e^{i pi k (r0+a)/N} T(a, k mod 256)
+    // accumulate the selected rows: sum_a e^{i pi k (r0+a)/N} T(a, k mod 256).
+    // With the pair unpacking folded into g_alpha / g_beta, a tile contributes
+    //   r0 (g_alpha sum_p z^p C_p[u] + g_beta sum_p z^p conj(C_p[-u])),
+    // z = e^{2 i pi k / N}: two Horner recurrences over the 16 pairs.
     for (int q = tid; q < s; q += blockDim.x) {
       const uint64_t k = static_cast<uint64_t>(rows[q]);
       const int u = uq[q], um = (256 - u) & 255;
+      const double2 zz = zq[q];
+      double2 S1 = X[(kPairs - 1) * kXS + u];
+      double2 Cm = X[(kPairs - 1) * kXS + um];
+      double2 S2 = make_double2(Cm.x, -Cm.y);
+#pragma unroll
+      for (int pp = kPairs - 2; pp >= 0; --pp) {
+        const double2 C = X[pp * kXS + u];
+        Cm = X[pp * kXS + um];
+        S1 = make_double2(fma(S1.x, zz.x, fma(-S1.y, zz.y, C.x)), fma(S1.x, zz.y, fma(S1.y, zz.x, C.y)));
+        S2 = make_double2(fma(S2.x, zz.x, fma(-S2.y, zz.y, Cm.x)), fma(S2.x, zz.y, fma(S2.y, zz.x, -Cm.y)));
+      }
       double sn, cs;
       const uint64_t ph = (k * static_cast<uint64_t>(r0 + a0)) % twoN;
       sincospi(static_cast<double>(ph) / static_cast<double>(N), &sn, &cs);
-      double2 r = make_double2(cs, sn);
-      const double2 st = stp[q];
-      double2 a = acc[q];
-#pragma unroll 4
-      for (int pp = 0; pp < kPairs; ++pp) {
-        const double2 C = X[pp * kXS + u], Cm = X[pp * kXS + um];
-        const double2 T0 = make_double2(0.5 * (C.x + Cm.x), 0.5 * (C.y - Cm.y));
-        const double2 T1 = make_double2(0.5 * (C.y + Cm.y), -0.5 * (C.x - Cm.x));
-        a = cadd(a, cmul(r, T0));
-        r = cmul(r, st);
-        a = cadd(a, cmul(r, T1));
-        r = cmul(r, st);
-      }
-      acc[q] = a;
+      const double2 tsum = cadd(cmul(ga[q], S1), cmul(gb[q], S2));
+      acc[q] = cadd(acc[q], cmul(make_double2(cs, sn), tsum));
     }
   }
   __syncthreads();
@@ -435,11 +463,13 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
       if (csize > 1) grid = std::max(csize, (grid + csize - 1) / csize * csize);
       grid = static_cast<int>(std::min<int64_t>(grid, ntiles));
       if (csize > 1 && grid % csize) csize = 1;
-      const size_t smem = sizeof(double2) * static_cast<size_t>(kPairs * kXS + 2 * S.s + 256) + sizeof(int) * S.s;
-      static size_t configured = 0;
-      if (smem > configured) {
-        SDR_CUDA(cudaFuncSetAttribute(k_srdct256, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = smem;
+      const size_t smem = sizeof(double2) * static_cast<size_t>(kPairs * kXS + 4 * S.s + 256) + sizeof(int) * S.s;
+      const bool fast = p.M == 128 && p.L % 2 == 0 && row_begin % 2 == 0;
+      auto kern = fast ? k_srdct256<8, true> : k_srdct256<0, false>;
+      static size_t configured[2] = {0, 0};
+      if (smem > configured[fast]) {
+        SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured[fast] = smem;
       }
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(grid);
@@ -454,7 +484,7 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       TimedLaunch t(c, "sketch");
-      SDR_CUDA(cudaLaunchKernelEx(&cfg, k_srdct256, x_own, xscale, S.n, row_begin, static_cast<int>(p.M), p.L,
+      SDR_CUDA(cudaLaunchKernelEx(&cfg, kern, x_own, xscale, S.n, row_begin, static_cast<int>(p.M), p.L,
                                   static_cast<const uint32_t*>(S.sign_bits.get()), static_cast<const int64_t*>(S.rows.get()),
                                   static_cast<const double*>(S.row_scale.get()), static_cast<int>(S.s), ntiles, csize,
                                   c.partials(2 * S.s * grid), c.counters() + 5, c.partials2(2 * S.s), out));

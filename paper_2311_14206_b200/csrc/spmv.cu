@@ -18,6 +18,8 @@
 #include "mgs.cuh"
 #include "reduce.cuh"
 
+#include <cstdlib>
+
 namespace sdr {
 
 namespace {
@@ -33,8 +35,8 @@ struct MgsArgs {
   double* coef = nullptr;  // null: coefficients are formed later (after an allreduce)
 };
 
-template <int MODE, int NV>
-__global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 2) k_sell_spmv(SellView A, const double* __restrict__ x_ext,
+template <int MODE, int NV, bool PIPE>
+__global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : (PIPE ? 2 : 3)) k_sell_spmv(SellView A, const double* __restrict__ x_ext,
                                                          double* __restrict__ y, const double* __restrict__ aux,
                                                          int64_t ldv, int64_t own_off, int64_t halo_lo, int j,
                                                          int nwin, double* __restrict__ partials,
@@ -62,8 +64,9 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 2) k_sell_spmv(SellView
   int32_t c[kBatch];
   int len;
   int64_t p0;
-  fetch_idx(sl, c, len, p0);
+  if constexpr (PIPE) fetch_idx(sl, c, len, p0);
   while (sl < A.nslices) {
+    if constexpr (!PIPE) fetch_idx(sl, c, len, p0);
     const int64_t row = sl * kSlice + lane;
     const bool live = row < A.nrows;
     // epilogue operands are independent of the product: fetch them first
@@ -83,9 +86,9 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 2) k_sell_spmv(SellView
     }
     const int64_t sn = sl + nwarps;
     int32_t cn[kBatch];
-    int lenn;
-    int64_t p0n;
-    fetch_idx(sn, cn, lenn, p0n);
+    int lenn = 0;
+    int64_t p0n = 0;
+    if constexpr (PIPE) fetch_idx(sn, cn, lenn, p0n);
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < kBatch; ++k)
@@ -122,10 +125,12 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 2) k_sell_spmv(SellView
       }
     }
     sl = sn;
-    len = lenn;
-    p0 = p0n;
+    if constexpr (PIPE) {
+      len = lenn;
+      p0 = p0n;
 #pragma unroll
-    for (int k = 0; k < kBatch; ++k) c[k] = cn[k];
+      for (int k = 0; k < kBatch; ++k) c[k] = cn[k];
+    }
   }
   if constexpr (MODE != 0) {
     const int nv = MODE == 1 ? 1 + nwin : 1;
@@ -151,14 +156,25 @@ int resident_grid(const Context& c, K kernel, int64_t want_blocks) {
 
 int64_t blocks_for(int64_t nslices) { return (nslices + (kThreads / 32) - 1) / (kThreads / 32); }
 
-template <int NV>
+/// SDR_K1_PIPE=1 selects the software-pipelined slice loop (fewer resident
+/// warps, more bytes in flight per warp); default is the 4-CTA/SM variant.
+bool use_pipe() {
+  static const int v = [] {
+    const char* e = std::getenv("SDR_K1_PIPE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+template <int NV, bool PIPE>
 void spmv_arnoldi_impl(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                        int nwin, double* y, double* recA, const MgsArgs& mg) {
-  const int g = resident_grid(c, k_sell_spmv<1, NV>, blocks_for(A.nslices));
+  const int g = resident_grid(c, k_sell_spmv<1, NV, PIPE>, blocks_for(A.nslices));
   const double* x_ext = V + j * ldv + lay.ext_shift();
   TimedLaunch t(c, "spmv_arnoldi");
-  k_sell_spmv<1, NV><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin,
-                                                   c.partials(static_cast<int64_t>(NV) * g), c.counters() + 0, recA, mg);
+  k_sell_spmv<1, NV, PIPE><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin,
+                                                         c.partials(static_cast<int64_t>(NV) * g), c.counters() + 0,
+                                                         recA, mg);
   SDR_KERNEL_CHECK();
 }
 
@@ -166,10 +182,10 @@ void spmv_arnoldi_impl(Context& c, const SellView& A, const double* V, int64_t l
 
 void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) {
   if (A.nrows == 0) return;
-  const int g = resident_grid(c, k_sell_spmv<0, 1>, blocks_for(A.nslices));
+  const int g = resident_grid(c, k_sell_spmv<0, 1, false>, blocks_for(A.nslices));
   TimedLaunch t(c, "spmv");
-  k_sell_spmv<0, 1><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, nullptr, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr,
-                                                  MgsArgs{});
+  k_sell_spmv<0, 1, false><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, nullptr, 0, 0, 0, 0, 0, nullptr, nullptr,
+                                                         nullptr, MgsArgs{});
   SDR_KERNEL_CHECK();
 }
 
@@ -177,21 +193,25 @@ void launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t
                          int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
                          double* coef) {
   const MgsArgs mg{rec, rstride, T, cvec, coef};
-  if (nwin <= 3)
-    spmv_arnoldi_impl<4>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
-  else if (nwin <= 7)
-    spmv_arnoldi_impl<8>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
-  else if (nwin <= 33)
-    spmv_arnoldi_impl<34>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
-  else
+  if (nwin <= 3) {
+    if (use_pipe())
+      spmv_arnoldi_impl<4, true>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
+    else
+      spmv_arnoldi_impl<4, false>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
+  } else if (nwin <= 7) {
+    spmv_arnoldi_impl<8, false>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
+  } else if (nwin <= 33) {
+    spmv_arnoldi_impl<34, false>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
+  } else {
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
+  }
 }
 
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2) {
-  const int g = resident_grid(c, k_sell_spmv<2, 1>, blocks_for(A.nslices));
+  const int g = resident_grid(c, k_sell_spmv<2, 1, false>, blocks_for(A.nslices));
   TimedLaunch t(c, "residual");
-  k_sell_spmv<2, 1><<<g, kThreads, 0, c.stream>>>(A, x_ext, r, b, 0, 0, 0, 0, 0, c.partials(g), c.counters() + 1,
-                                                  norm2, MgsArgs{});
+  k_sell_spmv<2, 1, false><<<g, kThreads, 0, c.stream>>>(A, x_ext, r, b, 0, 0, 0, 0, 0, c.partials(g),
+                                                         c.counters() + 1, norm2, MgsArgs{});
   SDR_KERNEL_CHECK();
 }
 
