@@ -232,10 +232,13 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = 0
     reports = []
+    walls = []
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
+            tw = time.perf_counter()
             r = one(b_dev)
+            walls.append(1e3 * (time.perf_counter() - tw))
             iters += r.report.iterations
             reports.append(r.report)
         ev1.record(stream)
@@ -258,10 +261,13 @@ def main():
     barrier()
     t_e2e0 = time.perf_counter()
     e2e_iters = 0
+    e2e_walls = []
     for _ in range(args.steps):
+        tw = time.perf_counter()
         space = sk.RecycleSpace(ctx)
         r = sk.solve(A, b_host.numpy(), cfg, space=space, sketch=S)
         e2e_iters += r.report.iterations
+        e2e_walls.append(1e3 * (time.perf_counter() - tw))
     ctx.synchronize()
     e2e_s = time.perf_counter() - t_e2e0
     if dist is not None:
@@ -330,6 +336,8 @@ def main():
             "time_to_solution_ms": ms / args.steps,
             "solve": {"status": rep.status, "iterations": rep.iterations, "cycles": rep.cycles,
                       "final_relative_residual": rep.final_relative_residual,
+                      "wall_ms": [round(v, 2) for v in walls], "e2e_wall_ms": [round(v, 2) for v in e2e_walls],
+                      "internal_ms": [round(1e3 * rr.seconds, 2) for rr in reports],
                       "phases_ms": {k: round(v, 3) for k, v in rep.phases.items()}},
             "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * nloc, "d2h_bytes_per_step": 8 * nloc},
             "roofline": roofline,

@@ -6,6 +6,8 @@
 
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -35,6 +37,43 @@ inline Error runtime(const std::string& m) { return Error(4, m); }
 
 #define SDR_KERNEL_CHECK() SDR_CUDA(cudaGetLastError())
 
+/// Process-wide cache of large freed device allocations (keyed by device and
+/// exact byte size), so per-solve buffers — the recycle space's U blocks,
+/// staging vectors — are recycled instead of going through cudaMalloc /
+/// cudaFree (both synchronise the device) on every solve.
+struct DeviceCache {
+  static constexpr size_t kMinBytes = size_t{8} << 20;
+  static constexpr int kPerSize = 4;
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::multimap<std::pair<int, size_t>, void*>& pool() {
+    static std::multimap<std::pair<int, size_t>, void*> p;
+    return p;
+  }
+  static void* take(size_t bytes) {
+    if (bytes < kMinBytes) return nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu());
+    auto it = pool().find({dev, bytes});
+    if (it == pool().end()) return nullptr;
+    void* p = it->second;
+    pool().erase(it);
+    return p;
+  }
+  static bool give(void* p, size_t bytes) {
+    if (bytes < kMinBytes) return false;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu());
+    if (static_cast<int>(pool().count({dev, bytes})) >= kPerSize) return false;
+    pool().insert({{dev, bytes}, p});
+    return true;
+  }
+};
+
 /// Owning device allocation.
 template <class T>
 class DeviceBuffer {
@@ -56,14 +95,18 @@ class DeviceBuffer {
   void resize(i64 n) {
     if (n == n_) return;
     release();
-    if (n > 0) SDR_CUDA(cudaMalloc(&p_, sizeof(T) * static_cast<size_t>(n)));
+    if (n > 0) {
+      const size_t bytes = sizeof(T) * static_cast<size_t>(n);
+      p_ = static_cast<T*>(DeviceCache::take(bytes));
+      if (!p_) SDR_CUDA(cudaMalloc(&p_, bytes));
+    }
     n_ = n;
   }
   void ensure(i64 n) {
     if (n > n_) resize(n);
   }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_ && !DeviceCache::give(p_, sizeof(T) * static_cast<size_t>(n_))) cudaFree(p_);
     p_ = nullptr;
     n_ = 0;
   }

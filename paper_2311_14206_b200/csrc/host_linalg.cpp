@@ -159,16 +159,20 @@ void thin_svd(const HMat& A, std::vector<double>& sv, HMat* U, HMat* V) {
   }
   HMat a = A, u(m, mn), vt(mn, n);
   const bool vec = U || V;
+  // divide-and-conquer SVD (the reference uses Eigen::JacobiSVD; singular
+  // values and subspaces agree to rounding, singular-vector signs cancel in
+  // the pencil C = diag(1/sigma) u^T SW v)
   const char* job = vec ? "S" : "N";
   int info = 0, lwork = -1, lda = std::max(1, m), ldu = vec ? std::max(1, m) : 1, ldvt = vec ? std::max(1, mn) : 1;
+  std::vector<int> iwork(static_cast<size_t>(8 * mn));
   double wq = 0.0;
-  scipy_dgesvd_(job, job, &m, &n, a.a.data(), &lda, sv.data(), u.a.data(), &ldu, vt.a.data(), &ldvt, &wq, &lwork,
-                &info, 1, 1);
+  scipy_dgesdd_(job, &m, &n, a.a.data(), &lda, sv.data(), u.a.data(), &ldu, vt.a.data(), &ldvt, &wq, &lwork,
+                iwork.data(), &info, 1);
   lwork = static_cast<int>(wq) + 1;
   std::vector<double> work(static_cast<size_t>(lwork));
-  scipy_dgesvd_(job, job, &m, &n, a.a.data(), &lda, sv.data(), u.a.data(), &ldu, vt.a.data(), &ldvt, work.data(),
-                &lwork, &info, 1, 1);
-  if (info != 0) throw runtime("truncated_svd: dgesvd failed with info = " + std::to_string(info));
+  scipy_dgesdd_(job, &m, &n, a.a.data(), &lda, sv.data(), u.a.data(), &ldu, vt.a.data(), &ldvt, work.data(), &lwork,
+                iwork.data(), &info, 1);
+  if (info != 0) throw runtime("truncated_svd: dgesdd failed with info = " + std::to_string(info));
   if (U) *U = u;
   if (V) {
     *V = HMat(n, mn);

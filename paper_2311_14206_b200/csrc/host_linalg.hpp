@@ -25,6 +25,9 @@ void scipy_dtrsen_(const char* job, const char* compq, const int* select, const 
 void scipy_dgesvd_(const char* jobu, const char* jobvt, const int* m, const int* n, double* a, const int* lda, double* s,
                    double* u, const int* ldu, double* vt, const int* ldvt, double* work, const int* lwork, int* info,
                    size_t, size_t);
+void scipy_dgesdd_(const char* jobz, const int* m, const int* n, double* a, const int* lda, double* s, double* u,
+                   const int* ldu, double* vt, const int* ldvt, double* work, const int* lwork, int* iwork, int* info,
+                   size_t);
 void scipy_openblas_set_num_threads(int);
 }
 

@@ -1,20 +1,29 @@
-// GMRES-SDR driver: solve_cycle / solve / solve_sequence semantics of the
-// reference (solver.hpp:128-459) with every N-length operation on the GPU.
+// GMRES-SDR driver: solve_cycle / solve semantics of the reference
+// (solver.hpp:128-365) with every N-length operation on the GPU.
 //
 // Device pipeline per Arnoldi step j (single stream, no host round trip
-// inside a step):   [halo(w_j)] K1 spmv+dots [allreduce A] K2 update
-//                   K3 sketch [allreduce B] D2H(record j) event
+// inside a step):   [halo(w_j)] K1 spmv+dots(+MGS coefficients) [allreduce A]
+//                   K2 update  K3 sketch [allreduce B]  D2H(record j) event
 // The host consumes step records strictly in order (incremental QR, LS
-// solve, trigger test) while the device already runs up to `kLookahead`
-// steps ahead: the Arnoldi recurrence never depends on the least-squares
-// result, so speculative steps are either consumed exactly as the
-// reference would take them or discarded at cycle end.
+// solve, trigger test) while the device runs up to `kLookahead` steps ahead:
+// the Arnoldi recurrence never depends on the least-squares result, so
+// speculative steps are either consumed exactly as the reference would take
+// them or discarded at cycle end.
+//
+// Cycle overlap: the Krylov basis V is double-buffered. When a cycle ends
+// and another follows, the next cycle's init_krylov and first speculative
+// steps are enqueued on the other buffer *before* the host runs the
+// harmonic-Ritz SVD/Schur of the finished cycle, so the LAPACK work hides
+// under device work (the recycle product U_new = [V U] P reads the finished
+// buffer, which the new cycle does not touch).
 #include "solver.hpp"
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
+#include <optional>
 
 namespace sdr {
 
@@ -26,18 +35,22 @@ struct Workspace {
   i64 m = -1, s = -1;
   int T = 0;
   RecLayout RL;
-  DeviceBuffer<double> V, y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
+  DeviceBuffer<double> V[2];
+  int nV = 0;
+  DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<const double*> inptr;
   DeviceBuffer<double*> outptr;
   PinnedBuffer<double> hrec, hscal, hcoef;
   PinnedBuffer<const double*> hin;
   PinnedBuffer<double*> hout;
   std::vector<cudaEvent_t> ev;
+  cudaEvent_t ev_init = nullptr;
   ~Workspace() {
     for (auto e : ev) cudaEventDestroy(e);
+    if (ev_init) cudaEventDestroy(ev_init);
   }
-  double* Vcol(i64 i) const { return V.get() + i * lay.ld + lay.own_off; }
-  double* Vbuf(i64 i) const { return V.get() + i * lay.ld; }
+  double* Vcol(int b, i64 i) const { return V[b].get() + i * lay.ld + lay.own_off; }
+  double* Vbuf(int b, i64 i) const { return V[b].get() + i * lay.ld; }
 };
 
 Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
@@ -55,10 +68,21 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
     w->s = s;
     w->T = T;
     w->RL = RecLayout::make(T, s);
-    w->V.resize((mm + 1) * lay.ld);
+    w->V[1].release();
+    w->V[0].resize((mm + 1) * lay.ld);
+    SDR_CUDA(cudaMemsetAsync(w->V[0].get(), 0, sizeof(double) * static_cast<size_t>(w->V[0].size()), c.stream));
+    w->nV = 1;
+    // second basis buffer for cycle overlap, only when it leaves ample headroom
+    size_t free_b = 0, total_b = 0;
+    SDR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t need = sizeof(double) * static_cast<size_t>((mm + 1) * lay.ld);
+    if (free_b > need + (size_t{4} << 30) + total_b / 16) {
+      w->V[1].resize((mm + 1) * lay.ld);
+      SDR_CUDA(cudaMemsetAsync(w->V[1].get(), 0, need, c.stream));
+      w->nV = 2;
+    }
     w->rec.resize((mm + 2) * w->RL.stride);
     SDR_CUDA(cudaMemsetAsync(w->rec.get(), 0, sizeof(double) * static_cast<size_t>(w->rec.size()), c.stream));
-    SDR_CUDA(cudaMemsetAsync(w->V.get(), 0, sizeof(double) * static_cast<size_t>(w->V.size()), c.stream));
     w->cvec.resize(mm + 2);
     w->hrec.ensure((mm + 2) * w->RL.stride);
     while (static_cast<i64>(w->ev.size()) < mm + 2) {
@@ -66,6 +90,7 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
       SDR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       w->ev.push_back(e);
     }
+    if (!w->ev_init) SDR_CUDA(cudaEventCreateWithFlags(&w->ev_init, cudaEventDisableTiming));
   }
   const i64 nl = std::max<i64>(lay.nloc, 1);
   w->y.ensure(nl);
@@ -151,106 +176,10 @@ double d2h_scalar(Context& c, Workspace& w, const double* dev) {
   return w.hscal.get()[0];
 }
 
-void update_recycle(Context& c, Workspace& w, const HostKrylov& st, Recycle& sp, i64 k, double rank_tol,
-                    Counters& cnt, std::vector<std::string>* notes, Report& rep) {  // recycle.hpp:226-289
-  const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
-  if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
-  HMat SAW(s, kh + j), SW(s, kh + j);
-  for (i64 q = 0; q < kh; ++q) {
-    std::copy(sp.SAU.col(q), sp.SAU.col(q) + s, SAW.col(q));
-    std::copy(sp.SU.col(q), sp.SU.col(q) + s, SW.col(q));
-  }
-  for (i64 i = 0; i < j; ++i) {
-    std::copy(st.SAV.col(i), st.SAV.col(i) + s, SAW.col(kh + i));
-    std::copy(st.SV.col(i), st.SV.col(i) + s, SW.col(kh + i));
-  }
-  Harmonic hp;
-  {
-    PhaseTimer pt(rep, "recycle_harmonic");
-    hp = harmonic_extract(SAW, SW, k, rank_tol);
-  }
-  if (notes) {
-    if (hp.rank_limited)
-      notes->push_back("deflation space limited to pencil rank " + std::to_string(hp.rank) + " (requested " +
-                       std::to_string(hp.k_requested) + ")");
-    if (hp.pair_extended) notes->push_back("deflation space grew by one to keep a conjugate pair together");
-  }
-  const int prov = sp.empty() ? 1 : sp.provenance;
-  const i64 ke = hp.k_eff;
-  if (ke == 0) {
-    sp.clear();
-    sp.provenance = prov;
-    return;
-  }
-  sp.ensure(w.lay.nloc, std::max<i64>(ke, kh));
-  // device: U_new = V(:,0:j) C_bot + U C_top with lazy scales folded in
-  std::vector<const double*> in;
-  HMat coef(kh + j, ke);
-  for (i64 i = 0; i < j; ++i) {
-    in.push_back(w.Vcol(i));
-    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
-  }
-  for (i64 p = 0; p < kh; ++p) {
-    in.push_back(sp.col(p));
-    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
-  }
-  const int other = 1 - sp.cur;
-  std::vector<double*> out;
-  for (i64 q = 0; q < ke; ++q) out.push_back(sp.buf[other].get() + q * sp.ld);
-  tallskinny(c, w, in, coef, out, w.lay.nloc, w.scal.get());
-  c.allreduce_sum(w.scal.get(), ke);
-  SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), w.scal.get(), sizeof(double) * ke, cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
-  // host: SU_new, SAU_new (recycle.hpp:257-265)
-  HMat SU(s, ke), SAU(s, ke);
-  for (i64 q = 0; q < ke; ++q) {
-    for (i64 i = 0; i < j; ++i) {
-      const double cf = hp.coeffs(kh + i, q);
-      for (i64 r = 0; r < s; ++r) {
-        SU(r, q) += st.SV(r, i) * cf;
-        SAU(r, q) += st.SAV(r, i) * cf;
-      }
-    }
-    for (i64 p = 0; p < kh; ++p) {
-      const double cf = hp.coeffs(p, q);
-      for (i64 r = 0; r < s; ++r) {
-        SU(r, q) += sp.SU(r, p) * cf;
-        SAU(r, q) += sp.SAU(r, p) * cf;
-      }
-    }
-  }
-  sp.cur = other;
-  sp.slot.resize(static_cast<size_t>(ke));
-  sp.uscale.resize(static_cast<size_t>(ke));
-  for (i64 q = 0; q < ke; ++q) sp.slot[static_cast<size_t>(q)] = static_cast<int>(q);
-  sp.SU = std::move(SU);
-  sp.SAU = std::move(SAU);
-  sp.provenance = prov;
-  std::vector<i64> bad;
-  for (i64 q = 0; q < ke; ++q) {  // recycle.hpp:269-286
-    const double nrm = std::sqrt(w.hscal.get()[q]);
-    ++cnt.inner_products;
-    if (nrm == 0.0 || !std::isfinite(nrm)) {
-      bad.push_back(q);
-      sp.uscale[static_cast<size_t>(q)] = 0.0;
-      continue;
-    }
-    sp.uscale[static_cast<size_t>(q)] = 1.0 / nrm;
-    for (i64 r = 0; r < s; ++r) {
-      sp.SU(r, q) /= nrm;
-      sp.SAU(r, q) /= nrm;
-    }
-  }
-  if (!bad.empty()) {
-    sp.drop_columns(bad);
-    if (notes) notes->push_back("dropped " + std::to_string(bad.size()) + " degenerate deflation columns after the harmonic update");
-  }
-  if (sp.empty()) sp.provenance = 0;
-}
-
 /// Device Arnoldi pipeline + host bookkeeping of init_krylov / arnoldi_step
-/// (arnoldi.hpp:47-119): the device produces step records, the host turns
-/// them into H, SV, SAV exactly as the reference's KrylovState.
+/// (arnoldi.hpp:47-119) on basis buffer `vb`: the device produces step
+/// records, the host turns them into H, SV, SAV exactly as the reference's
+/// KrylovState.
 struct ArnoldiPipeline {
   Context& c;
   Workspace& w;
@@ -258,20 +187,32 @@ struct ArnoldiPipeline {
   const SketchDev& S;
   i64 t, m;
   double breakdown_tol;
-  Counters& cnt;
+  int vb;
   HostKrylov st;
   i64 issued = 0;
   double wait_ms = 0.0;
 
-  void init(const double* r0) {
-    const VecLayout& lay = w.lay;
+  ArnoldiPipeline(Context& c_, Workspace& w_, const DeviceOperator& A_, const SketchDev& S_, i64 t_, i64 m_,
+                  double btol, int vb_)
+      : c(c_), w(w_), A(A_), S(S_), t(t_), m(m_), breakdown_tol(btol), vb(vb_) {}
+
+  /// w_0 = r0, ||r0||^2 and S r0 on the device; the host reads them in init_finish.
+  void init_enqueue(const double* r0) {
     const RecLayout& RL = w.RL;
-    const i64 s = S.s, R = RL.stride;
-    launch_copy_norm(c, r0, w.Vcol(0), lay.nloc, w.rec.get() + RL.b_off());
-    launch_sketch(c, S, w.Vcol(0), lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
+    launch_copy_norm(c, r0, w.Vcol(vb, 0), w.lay.nloc, w.rec.get() + RL.b_off());
+    launch_sketch(c, S, w.Vcol(vb, 0), w.lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
     c.allreduce_sum(w.rec.get() + RL.b_off(), RL.b_len());
-    SDR_CUDA(cudaMemcpyAsync(w.hrec.get(), w.rec.get(), sizeof(double) * R, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    SDR_CUDA(cudaMemcpyAsync(w.hrec.get(), w.rec.get(), sizeof(double) * RL.stride, cudaMemcpyDeviceToHost, c.stream));
+    SDR_CUDA(cudaEventRecord(w.ev_init, c.stream));
+    issued = 0;
+  }
+
+  /// init_krylov bookkeeping (arnoldi.hpp:47-72); throws domain on a zero residual.
+  void init_finish(Counters& cnt) {
+    SDR_CUDA(cudaEventSynchronize(w.ev_init));
+    const RecLayout& RL = w.RL;
+    const i64 s = S.s;
+    st = HostKrylov{};
     st.r0_norm = std::sqrt(w.hrec.get()[RL.b_off()]);
     ++cnt.inner_products;
     if (st.r0_norm == 0.0) throw domain("init_krylov: zero initial residual (already converged)");
@@ -283,7 +224,6 @@ struct ArnoldiPipeline {
     const double* sk = w.hrec.get() + RL.sketch_off();
     for (i64 r = 0; r < s; ++r) st.SV(r, 0) = sk[r] / st.r0_norm;
     st.cv[0] = 1.0 / st.r0_norm;
-    issued = 0;
   }
 
   void enqueue(i64 j) {
@@ -293,29 +233,34 @@ struct ArnoldiPipeline {
     const int T = RL.T;
     const int nwin = static_cast<int>(std::min<i64>(t, j + 1));
     const int ngram = static_cast<int>(std::min<i64>(T - 1, j + 1));
-    c.halo_exchange(A.plan, w.Vbuf(j) + lay.ext_shift(), A.ext_begin, w.Vcol(j), A.row_begin);
+    double* Vb = w.V[vb].get();
+    c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
     double* recj = w.rec.get() + (j + 1) * R;
     // one GPU: K1's last CTA forms the MGS coefficients; several: K2 forms
     // them after the allreduce of the window dots
     double* coef = c.distributed() ? nullptr : w.coef_dev.get();
-    launch_spmv_arnoldi(c, A.view(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
+    launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
                         w.rec.get(), R, T, w.cvec.get(), coef);
     c.allreduce_sum(recj + RL.a_off(), T + 1);
-    launch_update(c, w.y.get(), w.V.get(), lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(),
-                  coef);
-    launch_sketch(c, S, w.Vcol(j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
+    launch_update(c, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(), coef);
+    launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
     SDR_CUDA(cudaMemcpyAsync(w.hrec.get() + (j + 1) * R, recj, sizeof(double) * R, cudaMemcpyDeviceToHost, c.stream));
     SDR_CUDA(cudaEventRecord(w.ev[static_cast<size_t>(j + 1)], c.stream));
   }
 
-  /// Keeps up to kLookahead speculative steps in flight, then consumes step
-  /// st.j; returns true on lucky breakdown.
-  bool step() {
+  /// Keep up to kLookahead speculative steps ahead of step j in flight.
+  void issue_ahead(i64 j) {
+    while (issued < m && issued <= j + kLookahead) enqueue(issued++);
+  }
+
+  /// Consumes step st.j (arnoldi.hpp:87-118 bookkeeping); returns true on
+  /// lucky breakdown.
+  bool step(Counters& cnt) {
     if (st.breakdown) throw logic("arnoldi_step: basis already broke down");
     if (st.j >= m) throw logic("arnoldi_step: step capacity exhausted");
     const i64 j = st.j;
-    while (issued < m && issued <= j + kLookahead) enqueue(issued++);
+    issue_ahead(j);
     const auto tw0 = std::chrono::steady_clock::now();
     SDR_CUDA(cudaEventSynchronize(w.ev[static_cast<size_t>(j + 1)]));
     wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count();
@@ -358,20 +303,116 @@ struct ArnoldiPipeline {
   }
 };
 
-/// One restart cycle (solver.hpp:128-254). r0 is the device residual (own part).
-CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const SketchDev& S, const Config& cfg,
-                     const double* r0, Recycle& space, double tol_abs, double safety_in, Counters& cnt, Report& rep,
-                     const Callbacks* cb, int cycle_index, i64 iteration_base) {
+void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recycle& sp, i64 k, double rank_tol,
+                    Counters& cnt, std::vector<std::string>* notes, Report& rep) {  // recycle.hpp:226-289
+  const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
+  if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
+  HMat SAW(s, kh + j), SW(s, kh + j);
+  for (i64 q = 0; q < kh; ++q) {
+    std::copy(sp.SAU.col(q), sp.SAU.col(q) + s, SAW.col(q));
+    std::copy(sp.SU.col(q), sp.SU.col(q) + s, SW.col(q));
+  }
+  for (i64 i = 0; i < j; ++i) {
+    std::copy(st.SAV.col(i), st.SAV.col(i) + s, SAW.col(kh + i));
+    std::copy(st.SV.col(i), st.SV.col(i) + s, SW.col(kh + i));
+  }
+  Harmonic hp;
+  {
+    PhaseTimer pt(rep, "recycle_harmonic");
+    hp = harmonic_extract(SAW, SW, k, rank_tol);
+  }
+  if (notes) {
+    if (hp.rank_limited)
+      notes->push_back("deflation space limited to pencil rank " + std::to_string(hp.rank) + " (requested " +
+                       std::to_string(hp.k_requested) + ")");
+    if (hp.pair_extended) notes->push_back("deflation space grew by one to keep a conjugate pair together");
+  }
+  const int prov = sp.empty() ? 1 : sp.provenance;
+  const i64 ke = hp.k_eff;
+  if (ke == 0) {
+    sp.clear();
+    sp.provenance = prov;
+    return;
+  }
+  sp.ensure(w.lay.nloc, std::max<i64>(ke, kh));
+  // device: U_new = V(:,0:j) C_bot + U C_top with lazy scales folded in
+  std::vector<const double*> in;
+  HMat coef(kh + j, ke);
+  for (i64 i = 0; i < j; ++i) {
+    in.push_back(w.Vcol(vb, i));
+    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
+  }
+  for (i64 p = 0; p < kh; ++p) {
+    in.push_back(sp.col(p));
+    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
+  }
+  const int other = 1 - sp.cur;
+  std::vector<double*> out;
+  for (i64 q = 0; q < ke; ++q) out.push_back(sp.buf[other].get() + q * sp.ld);
+  tallskinny(c, w, in, coef, out, w.lay.nloc, w.scal.get());
+  c.allreduce_sum(w.scal.get(), ke);
+  SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), w.scal.get(), sizeof(double) * ke, cudaMemcpyDeviceToHost, c.stream));
+  // host: SU_new, SAU_new (recycle.hpp:257-265) while the product runs
+  HMat SU(s, ke), SAU(s, ke);
+  for (i64 q = 0; q < ke; ++q) {
+    for (i64 i = 0; i < j; ++i) {
+      const double cf = hp.coeffs(kh + i, q);
+      for (i64 r = 0; r < s; ++r) {
+        SU(r, q) += st.SV(r, i) * cf;
+        SAU(r, q) += st.SAV(r, i) * cf;
+      }
+    }
+    for (i64 p = 0; p < kh; ++p) {
+      const double cf = hp.coeffs(p, q);
+      for (i64 r = 0; r < s; ++r) {
+        SU(r, q) += sp.SU(r, p) * cf;
+        SAU(r, q) += sp.SAU(r, p) * cf;
+      }
+    }
+  }
+  c.sync();
+  sp.cur = other;
+  sp.slot.resize(static_cast<size_t>(ke));
+  sp.uscale.resize(static_cast<size_t>(ke));
+  for (i64 q = 0; q < ke; ++q) sp.slot[static_cast<size_t>(q)] = static_cast<int>(q);
+  sp.SU = std::move(SU);
+  sp.SAU = std::move(SAU);
+  sp.provenance = prov;
+  std::vector<i64> bad;
+  for (i64 q = 0; q < ke; ++q) {  // recycle.hpp:269-286
+    const double nrm = std::sqrt(w.hscal.get()[q]);
+    ++cnt.inner_products;
+    if (nrm == 0.0 || !std::isfinite(nrm)) {
+      bad.push_back(q);
+      sp.uscale[static_cast<size_t>(q)] = 0.0;
+      continue;
+    }
+    sp.uscale[static_cast<size_t>(q)] = 1.0 / nrm;
+    for (i64 r = 0; r < s; ++r) {
+      sp.SU(r, q) /= nrm;
+      sp.SAU(r, q) /= nrm;
+    }
+  }
+  if (!bad.empty()) {
+    sp.drop_columns(bad);
+    if (notes) notes->push_back("dropped " + std::to_string(bad.size()) + " degenerate deflation columns after the harmonic update");
+  }
+  if (sp.empty()) sp.provenance = 0;
+}
+
+/// Steps, least squares and verification of one restart cycle
+/// (solver.hpp:128-216). `ap` has its init enqueued (and possibly
+/// speculative steps in flight); r0 is the device residual (own part).
+CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOperator& A, const Config& cfg,
+                   const double* r0, Recycle& space, double tol_abs, double safety_in, Counters& cnt, Report& rep,
+                   const Callbacks* cb, int cycle_index, i64 iteration_base) {
   CycleOut out;
   out.safety = std::max(1.0, safety_in);
   const VecLayout& lay = w.lay;
-  const i64 s = S.s, m = cfg.m;
-  const auto t0 = std::chrono::steady_clock::now();
-
-  ArnoldiPipeline ap{c, w, A, S, cfg.t, m, cfg.breakdown_tol, cnt, HostKrylov{}};
+  const i64 s = ap.S.s, m = cfg.m;
   {
     PhaseTimer pt(rep, "cycle_init");
-    ap.init(r0);
+    ap.init_finish(cnt);
   }
   HostKrylov& st = ap.st;
   out.entry_norm = st.r0_norm;
@@ -399,7 +440,7 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
   double sres = out.sketched_entry;
   bool done = false;
   while (!done && st.j < m && !st.breakdown) {  // solver.hpp:165-216
-    const bool step_breakdown = ap.step();
+    const bool step_breakdown = ap.step(cnt);
     PhaseTimer pt_step(rep, "host_step");
     const i64 jj = st.j;
     const auto info = qr->append(st.SAV.col(jj - 1), s);
@@ -424,7 +465,7 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
       std::vector<const double*> in;
       HMat coef(jj + k_hat, 1);
       for (i64 i = 0; i < jj; ++i) {
-        in.push_back(w.Vcol(i));
+        in.push_back(w.Vcol(ap.vb, i));
         coef(i, 0) = y[static_cast<size_t>(k_hat + i)] * st.cv[static_cast<size_t>(i)];
       }
       for (i64 q = 0; q < k_hat; ++q) {
@@ -454,21 +495,24 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
       }
     }
   }
-  {
-    PhaseTimer pt(rep, "drain");
-    c.sync();  // drain speculative steps before the buffers are reused
-  }
   out.steps = st.j;
   out.sres = sres;
   out.breakdown = st.breakdown;
   rep.host_wait_ms += ap.wait_ms;
   rep.phase_ms["step_wait"] += ap.wait_ms;
+  return out;
+}
 
+/// Cycle statistics and the harmonic recycle update (solver.hpp:218-253).
+void finish_cycle(Context& c, Workspace& w, const ArnoldiPipeline& ap, const CycleOut& out, const Config& cfg,
+                  Recycle& space, Counters& cnt, Report& rep, int cycle_index) {
+  const HostKrylov& st = ap.st;
+  const i64 s = ap.S.s;
   CycleStat cs;
   cs.steps = st.j;
   cs.entry_residual = out.entry_norm;
   cs.sketched_entry = out.sketched_entry;
-  cs.exit_sres = sres;
+  cs.exit_sres = out.sres;
   cs.exit_residual = out.residual_norm;
   cs.safety_after = out.safety;
   if (st.j >= 1 && !st.breakdown) {
@@ -478,18 +522,15 @@ CycleOut solve_cycle(Context& c, Workspace& w, const DeviceOperator& A, const Sk
     cs.basis_cond = cond2(B);
   }
   rep.cycle_stats.push_back(cs);
-
-  if (cfg.k > 0 && st.j >= 1) {  // solver.hpp:242-252
+  if (cfg.k > 0 && st.j >= 1) {
     std::vector<std::string> notes;
     PhaseTimer pt(rep, "recycle");
-    update_recycle(c, w, st, space, cfg.k, cfg.rank_tol, cnt, &notes, rep);
+    update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep);
     rep.cycle_stats.back().deflation_rank = space.dim();
     for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
   } else if (cfg.k == 0) {
     space.clear();
   }
-  rep.device_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  return out;
 }
 
 }  // namespace
@@ -507,18 +548,18 @@ void krylov_run(Context& c, const DeviceOperator& A, const SketchDev& S, const d
   const VecLayout lay = A.layout();
   Workspace& w = workspace(c, lay, m, S.s, static_cast<int>(std::min(t, m)));
   Counters cnt;
-  ArnoldiPipeline ap{c, w, A, S, t, m, breakdown_tol, cnt, HostKrylov{}};
-  ap.init(r0);
-  for (i64 q = 0; q < steps && !ap.st.breakdown && ap.st.j < m; ++q) ap.step();
+  ArnoldiPipeline ap(c, w, A, S, t, m, breakdown_tol, 0);
+  ap.init_enqueue(r0);
+  ap.init_finish(cnt);
+  for (i64 q = 0; q < steps && !ap.st.breakdown && ap.st.j < m; ++q) ap.step(cnt);
   c.sync();
   const HostKrylov& st = ap.st;
-  const i64 s = S.s;
   if (V) {
     const i64 cols = st.breakdown ? st.j : st.j + 1;
     DeviceBuffer<double> tmp(std::max<i64>(lay.nloc * (m + 1), 1));
     SDR_CUDA(cudaMemsetAsync(tmp.get(), 0, sizeof(double) * static_cast<size_t>(lay.nloc * (m + 1)), c.stream));
     for (i64 i = 0; i < cols; ++i)
-      launch_scale_copy(c, st.cv[static_cast<size_t>(i)], w.Vcol(i), tmp.get() + i * lay.nloc, lay.nloc);
+      launch_scale_copy(c, st.cv[static_cast<size_t>(i)], w.Vcol(0, i), tmp.get() + i * lay.nloc, lay.nloc);
     SDR_CUDA(cudaMemcpyAsync(V, tmp.get(), sizeof(double) * static_cast<size_t>(lay.nloc * (m + 1)), cudaMemcpyDefault,
                              c.stream));
     c.sync();
@@ -526,7 +567,6 @@ void krylov_run(Context& c, const DeviceOperator& A, const SketchDev& S, const d
   if (H) std::copy(st.H.a.begin(), st.H.a.end(), H);
   if (SV) std::copy(st.SV.a.begin(), st.SV.a.end(), SV);
   if (SAV) std::copy(st.SAV.a.begin(), st.SAV.a.end(), SAV);
-  (void)s;
   if (j_out) *j_out = st.j;
   if (breakdown) *breakdown = st.breakdown ? 1 : 0;
   if (r0_norm) *r0_norm = st.r0_norm;
@@ -535,147 +575,6 @@ void krylov_run(Context& c, const DeviceOperator& A, const SketchDev& S, const d
     counters3[1] = cnt.inner_products;
     counters3[2] = cnt.sketch_applies;
   }
-}
-
-void Config::validate() const {  // solver.hpp:61-78
-  if (m < 1) throw invalid("SolverConfig: m must be at least 1");
-  if (t < 1) throw invalid("SolverConfig: t must be at least 1");
-  if (k < 0 || k >= m)
-    throw invalid("SolverConfig: need 0 <= k < m, got k = " + std::to_string(k) + ", m = " + std::to_string(m));
-  if (s < 2 * (m + k))
-    throw invalid("SolverConfig: sketch size s = " + std::to_string(s) + " is below 2 (m + k) = " +
-                  std::to_string(2 * (m + k)));
-  if (!(tol > 0.0 && tol < 1.0)) throw invalid("SolverConfig: tol must lie in (0, 1)");
-  if (!(safety_init >= 1.0)) throw invalid("SolverConfig: safety_init must be at least 1");
-  if (max_restarts < 1) throw invalid("SolverConfig: max_restarts must be at least 1");
-  if (!(rank_tol >= 0.0)) throw invalid("SolverConfig: rank_tol must be >= 0");
-  if (!(breakdown_tol >= 0.0)) throw invalid("SolverConfig: breakdown_tol must be >= 0");
-}
-
-void Recycle::drop_columns(const std::vector<i64>& cols) {  // recycle.hpp:48-71
-  if (cols.empty()) return;
-  std::vector<bool> drop(static_cast<size_t>(dim()), false);
-  for (i64 cc : cols) {
-    if (cc < 0 || cc >= dim()) throw invalid("RecycleSpace::drop_columns: no column " + std::to_string(cc));
-    drop[static_cast<size_t>(cc)] = true;
-  }
-  std::vector<int> ns;
-  std::vector<double> nu;
-  i64 keep = 0;
-  for (i64 q = 0; q < dim(); ++q)
-    if (!drop[static_cast<size_t>(q)]) ++keep;
-  HMat su(s, keep), sau(s, keep);
-  i64 o = 0;
-  for (i64 q = 0; q < dim(); ++q) {
-    if (drop[static_cast<size_t>(q)]) continue;
-    ns.push_back(slot[static_cast<size_t>(q)]);
-    nu.push_back(uscale[static_cast<size_t>(q)]);
-    std::copy(SU.col(q), SU.col(q) + s, su.col(o));
-    std::copy(SAU.col(q), SAU.col(q) + s, sau.col(o));
-    ++o;
-  }
-  slot.swap(ns);
-  uscale.swap(nu);
-  SU = std::move(su);
-  SAU = std::move(sau);
-}
-
-void Recycle::ensure(i64 nloc_, i64 capacity) {
-  if (nloc != nloc_ && !empty()) throw invalid("solve: recycle space has " + std::to_string(nloc) + " local rows but the operator block has " + std::to_string(nloc_));
-  const i64 ld_new = round_up(std::max<i64>(nloc_, 1), 32);
-  if (nloc == nloc_ && ld == ld_new && capacity <= cap) return;
-  const i64 cap_new = std::max(capacity, cap);
-  DeviceBuffer<double> nb[2];
-  nb[0].resize(ld_new * cap_new);
-  nb[1].resize(ld_new * cap_new);
-  for (i64 q = 0; q < dim(); ++q)
-    SDR_CUDA(cudaMemcpy(nb[0].get() + q * ld_new, col(q), sizeof(double) * static_cast<size_t>(nloc_), cudaMemcpyDeviceToDevice));
-  for (i64 q = 0; q < dim(); ++q) slot[static_cast<size_t>(q)] = static_cast<int>(q);
-  buf[0] = std::move(nb[0]);
-  buf[1] = std::move(nb[1]);
-  cur = 0;
-  nloc = nloc_;
-  ld = ld_new;
-  cap = cap_new;
-}
-
-SketchDev* create_sketch(Context& c, int kind, i64 n, i64 s, std::uint64_t seed, i64 zeta) {
-  auto S = std::make_unique<SketchDev>();
-  S->kind = kind;
-  S->n = n;
-  S->s = s;
-  S->seed = seed;
-  S->zeta = zeta;
-  if (kind == kIdentity) {
-    if (n < 1) throw invalid("SketchOperator::identity: n must be positive");
-    S->s = n;
-    return S.release();
-  }
-  if (kind == kSparseSign) {
-    if (n < 1 || s < 1 || zeta < 1 || zeta > s)
-      throw invalid("SketchOperator::sparse_sign: need n >= 1 and 1 <= zeta <= s, got n = " + std::to_string(n) +
-                    ", s = " + std::to_string(s) + ", zeta = " + std::to_string(zeta));
-    if (s > 880) throw invalid("SketchOperator::sparse_sign: device kernel supports s <= 880");
-    std::mt19937_64 eng(seed);
-    S->key = eng();
-    return S.release();
-  }
-  if (n < 2 || s < 1 || s >= n)
-    throw invalid("SketchOperator: need 1 <= s < n, got s = " + std::to_string(s) + ", n = " + std::to_string(n));
-  if (s > 4096) throw invalid("SketchOperator: device SRDCT supports s <= 4096");
-  if (n >= (int64_t{1} << 31)) throw invalid("SketchOperator: device SRDCT supports n < 2^31");
-  SrdctHost h = make_srdct_host(n, s, seed);
-  S->scale = std::sqrt(static_cast<double>(n) / static_cast<double>(s));
-  std::vector<double> rs(static_cast<size_t>(s));
-  for (i64 q = 0; q < s; ++q) {
-    const double alpha = h.rows[static_cast<size_t>(q)] == 0 ? std::sqrt(1.0 / static_cast<double>(n))
-                                                             : std::sqrt(2.0 / static_cast<double>(n));
-    rs[static_cast<size_t>(q)] = alpha * S->scale;
-  }
-  S->sign_bits.resize(static_cast<i64>(h.sign_bits.size()));
-  S->rows.resize(s);
-  S->row_scale.resize(s);
-  SDR_CUDA(cudaMemcpy(S->sign_bits.get(), h.sign_bits.data(), sizeof(uint32_t) * h.sign_bits.size(), cudaMemcpyHostToDevice));
-  SDR_CUDA(cudaMemcpy(S->rows.get(), h.rows.data(), sizeof(int64_t) * h.rows.size(), cudaMemcpyHostToDevice));
-  SDR_CUDA(cudaMemcpy(S->row_scale.get(), rs.data(), sizeof(double) * rs.size(), cudaMemcpyHostToDevice));
-  S->rows_host = std::move(h.rows);
-  S->sign_bits_host = std::move(h.sign_bits);
-  return S.release();
-}
-
-void sketch_apply(Context& c, const SketchDev& S, const double* x, i64 nloc, i64 row_begin, double* out_host) {
-  DeviceBuffer<double> out(S.s);
-  launch_sketch(c, S, x, nloc, row_begin, out.get());
-  c.allreduce_sum(out.get(), S.s);
-  SDR_CUDA(cudaMemcpyAsync(out_host, out.get(), sizeof(double) * static_cast<size_t>(S.s), cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
-}
-
-void refresh_recycle(Context& c, Recycle& sp, const DeviceOperator& A, const SketchDev& S, bool exact, Counters* cnt) {
-  if (sp.empty()) return;  // recycle.hpp:297-318
-  if (sp.n != A.cols)
-    throw invalid("refresh_for_new_matrix: space has " + std::to_string(sp.n) + " rows but the operator takes " +
-                  std::to_string(A.cols));
-  if (!exact) {
-    sp.provenance = 4;
-    return;
-  }
-  const VecLayout lay = A.layout();
-  DeviceBuffer<double> ubuf(lay.ld), au(std::max<i64>(lay.nloc, 1)), sk(S.s);
-  SDR_CUDA(cudaMemsetAsync(ubuf.get(), 0, sizeof(double) * static_cast<size_t>(lay.ld), c.stream));
-  std::vector<double> h(static_cast<size_t>(S.s));
-  for (i64 q = 0; q < sp.dim(); ++q) {
-    launch_scale_copy(c, sp.uscale[static_cast<size_t>(q)], sp.col(q), ubuf.get() + lay.own_off, lay.nloc);
-    operator_apply(c, A, ubuf.get(), au.get());
-    if (cnt) ++cnt->matvecs;
-    launch_sketch(c, S, au.get(), lay.nloc, A.row_begin, sk.get());
-    c.allreduce_sum(sk.get(), S.s);
-    SDR_CUDA(cudaMemcpyAsync(h.data(), sk.get(), sizeof(double) * static_cast<size_t>(S.s), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    if (cnt) ++cnt->sketch_applies;
-    std::copy(h.begin(), h.end(), sp.SAU.col(q));
-  }
-  sp.provenance = 3;
 }
 
 void solve(Context& c, const DeviceOperator& A, const double* b, const double* x0, bool x0_nonzero, const Config& cfg,
@@ -736,14 +635,16 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
   double safety = cfg.safety_init, res_norm = std::numeric_limits<double>::quiet_NaN();
   bool have = false;
   pt_setup.reset();
+  auto cur = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, 0);
+  cur->init_enqueue(w.r0.get());
   for (int cycle = 1; cycle <= cfg.max_restarts; ++cycle) {  // solver.hpp:321-359
     CycleOut cr;
     try {
-      cr = solve_cycle(c, w, A, *sketch, cfg, w.r0.get(), space, tol_abs, safety, rep.counters, rep, cb, cycle,
-                       rep.iterations);
+      cr = run_cycle(c, w, *cur, A, cfg, w.r0.get(), space, tol_abs, safety, rep.counters, rep, cb, cycle,
+                     rep.iterations);
     } catch (const Error& e) {
       if (e.code != 2) throw;
-      rep.status = 0;
+      rep.status = 0;  // zero residual at cycle entry: converged exactly
       res_norm = 0.0;
       have = true;
       break;
@@ -757,21 +658,38 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
     }
     res_norm = cr.residual_norm;
     have = true;
+    // the outcome is known before the recycle update; notes keep the reference order
+    int status = -1;
+    std::string note;
     if (cr.converged) {
-      rep.status = 0;
+      status = 0;
+    } else if (cr.breakdown) {
+      status = 2;
+      note = "cycle " + std::to_string(cycle) + ": basis exhausted before reaching the target";
+    } else if (cr.steps == cfg.m && cr.sres > 0.99 * cr.sketched_entry) {
+      status = 3;
+      note = "cycle " + std::to_string(cycle) + ": sketched residual improved by less than 1% over a full cycle";
+    } else if (cycle == cfg.max_restarts) {
+      status = 1;
+    }
+    std::unique_ptr<ArnoldiPipeline> next;
+    if (status < 0 && w.nV == 2) {
+      // overlap: next cycle's init + speculative steps on the other basis buffer
+      next = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, 1 - cur->vb);
+      next->init_enqueue(w.r0.get());
+      next->issue_ahead(0);
+    }
+    finish_cycle(c, w, *cur, cr, cfg, space, rep.counters, rep, cycle);
+    if (status >= 0) {
+      rep.status = status;
+      if (!note.empty()) rep.notes.push_back(note);
       break;
     }
-    if (cr.breakdown) {
-      rep.status = 2;
-      rep.notes.push_back("cycle " + std::to_string(cycle) + ": basis exhausted before reaching the target");
-      break;
+    if (!next) {
+      next = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, cur->vb);
+      next->init_enqueue(w.r0.get());
     }
-    if (cr.steps == cfg.m && cr.sres > 0.99 * cr.sketched_entry) {
-      rep.status = 3;
-      rep.notes.push_back("cycle " + std::to_string(cycle) + ": sketched residual improved by less than 1% over a full cycle");
-      break;
-    }
-    if (cycle == cfg.max_restarts) rep.status = 1;
+    cur = std::move(next);
   }
   if (have) rep.final_relative_residual = rep.rhs_norm > 0.0 ? res_norm / rep.rhs_norm : res_norm;
   if (x_out)
