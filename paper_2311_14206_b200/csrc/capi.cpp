@@ -921,6 +921,19 @@ const char* sdr_report_note(const sdr_report* r, int64_t i) {
 
 const char* sdr_report_error(const sdr_report* r) { return r ? r->r.error.c_str() : nullptr; }
 
+/* internal diagnostics (not part of the public header): ||x||^2 through the
+   copy_norm kernel and sum of y = A x through the plain SpMV. */
+SDR_API int sdr_debug_norm2(sdr_ctx* ctx, const double* x, int64_t n, double* out) {
+  return guard([&] {
+    Context& c = *ctx->c;
+    DeviceIn xin(c, x, n);
+    DeviceBuffer<double> dst(std::max<int64_t>(n, 1)), nrm(1);
+    launch_copy_norm(c, xin.ptr, dst.get(), n, nrm.get());
+    SDR_CUDA(cudaMemcpyAsync(out, nrm.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
 int sdr_report_phase(const sdr_report* r, const char* name, double* ms) {
   return guard([&] {
     need(r, "report");

@@ -61,7 +61,7 @@ __device__ __forceinline__ bool last_block_done(unsigned* counter) {
 /// independent loads (one or two L2 round trips in total instead of one per
 /// value), then each value's group sums are combined in group order.
 /// Requires blockDim.x <= 1024 and a multiple of 32.
-static __device__ __noinline__ void fold_partials(const double* partials, int nblocks, int nv, double* out,
+__device__ __forceinline__ void fold_partials(const double* partials, int nblocks, int nv, double* out,
                                            int out_stride = 1) {
   __shared__ double red[1024];
   const int T = blockDim.x, t = threadIdx.x;
