@@ -75,5 +75,11 @@ void launch_sketch(Context& c, const SketchDev& S, const double* x_own, int64_t 
                    double* out);
 void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, double xscale, int64_t nloc,
                           int64_t row_begin, double* out);
+/// Fused K2 + K3a (update pass and SRDCT of w_{j+1} in one sweep), writing
+/// the record's B part (norm, Gram, sketch). Returns false when the
+/// configuration is not eligible (caller runs K2 and K3 separately).
+bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
+                          int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec,
+                          const double* coef_ready, int64_t row_begin);
 
 }  // namespace sdr

@@ -19,6 +19,7 @@
 // owns one (lane, row-block) pair and accumulates into private shared-memory
 // bins, so the result is deterministic without atomics.
 #include "kernels.hpp"
+#include "mgs.cuh"
 #include "reduce.cuh"
 #include "sketch.hpp"
 
@@ -237,6 +238,193 @@ __device__ __forceinline__ void dft16_half(double2 (&a)[16]) {
   for (int n = 0; n < 16; ++n) a[n] = b[n];
 }
 
+// ------------------------------------------------ fused K2 + K3a (F = 256)
+// One pass over the step's vectors: the Arnoldi update
+//   w_{j+1} = c_j y - sum_d h_{j-d} c_{j-d} w_{j-d}          (arnoldi.hpp:91-114)
+// is evaluated in the SRDCT tile order (it is elementwise, so any order is
+// valid), w_{j+1} is stored once, its norm / Gram partials are accumulated,
+// and the sign-flipped values go straight from registers into the stage-1
+// FFT. HBM traffic is the update's alone (y + window reads, one write); the
+// sketch's FFT and row accumulation overlap with it instead of re-reading
+// w_{j+1} in a second kernel. Requires M = 128 (F = 256) and an even block.
+template <int MAXT>
+__global__ void __launch_bounds__(kThreads, 2) k_update_srdct256(
+    const double* __restrict__ y, double* __restrict__ V, int64_t ldv, int64_t own_off, int j, int nwin, int ngram,
+    double* __restrict__ rec, int64_t rstride, int T, double* __restrict__ cvec, const double* __restrict__ coef_ready,
+    int64_t N, int64_t r0, int64_t L, const uint32_t* __restrict__ sign_bits, const int64_t* __restrict__ rows,
+    const double* __restrict__ row_scale, int s, int64_t ntiles, int csize, double* __restrict__ partials,
+    unsigned* __restrict__ counter, double* __restrict__ fold) {
+  extern __shared__ double2 sm[];
+  double2* X = sm;                    // [16][257]
+  double2* acc = X + kPairs * kXS;    // [s] sketch rows, then [MAXT] norm/Gram (as .x)
+  double2* zq = acc + s + MAXT;
+  double2* ga = zq + s;
+  double2* gb = ga + s;
+  double2* tw = gb + s;
+  int* uq = reinterpret_cast<int*>(tw + 256);
+  __shared__ double coef[MAXT + 1];
+  __shared__ double nred[MAXT][kThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t twoN = 2u * static_cast<uint64_t>(N);
+  const int b_off = 2 * T + 3;
+  for (int k = tid; k < 256; k += blockDim.x) {
+    double sn, cs;
+    sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
+    tw[k] = make_double2(cs, sn);
+  }
+  for (int q = tid; q < s; q += blockDim.x) {
+    const int64_t k = rows[q];
+    double sn, cs;
+    sincospi(static_cast<double>(k) / static_cast<double>(N), &sn, &cs);
+    ga[q] = make_double2(0.5 * (1.0 + sn), -0.5 * cs);
+    gb[q] = make_double2(0.5 * (1.0 - sn), 0.5 * cs);
+    sincospi(static_cast<double>((2 * static_cast<uint64_t>(k)) % twoN) / static_cast<double>(N), &sn, &cs);
+    zq[q] = make_double2(cs, sn);
+    uq[q] = static_cast<int>(k & 255);
+    acc[q] = make_double2(0.0, 0.0);
+  }
+  if (coef_ready) {
+    if (tid <= MAXT) coef[tid] = tid <= nwin ? coef_ready[tid] : 0.0;
+  } else if (tid == 0) {
+    mgs_coefficients<MAXT>(rec, rstride, T, j, nwin, cvec, coef, blockIdx.x == 0);
+  }
+  __syncthreads();
+  double cf[MAXT + 1];
+#pragma unroll
+  for (int k = 0; k <= MAXT; ++k) cf[k] = coef[k];
+  const double* W[MAXT];
+#pragma unroll
+  for (int d = 0; d < MAXT; ++d) W[d] = V + static_cast<int64_t>(j - (d < nwin ? d : 0)) * ldv + own_off;
+  double* wout = V + static_cast<int64_t>(j + 1) * ldv + own_off;
+  double nacc[MAXT];
+#pragma unroll
+  for (int g = 0; g < MAXT; ++g) nacc[g] = 0.0;
+  const int p = tid & 15, t = tid >> 4;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t a0 = tile * (2 * kPairs);
+    const int64_t aa = a0 + 2 * p;
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = make_double2(0.0, 0.0);
+    if (aa < L) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t jl = aa + L * static_cast<int64_t>(t + 16 * i);
+        const double2 yv = __ldcs(reinterpret_cast<const double2*>(y + jl));
+        double2 wv[MAXT];
+#pragma unroll
+        for (int d = MAXT - 1; d >= 0; --d)
+          if (d < nwin) wv[d] = __ldg(reinterpret_cast<const double2*>(W[d] + jl));
+        double w0 = cf[0] * yv.x, w1 = cf[0] * yv.y;
+#pragma unroll
+        for (int d = MAXT - 1; d >= 0; --d)
+          if (d < nwin) {
+            w0 = fma(cf[1 + d], wv[d].x, w0);
+            w1 = fma(cf[1 + d], wv[d].y, w1);
+          }
+        *reinterpret_cast<double2*>(wout + jl) = make_double2(w0, w1);
+        nacc[0] = fma(w0, w0, fma(w1, w1, nacc[0]));
+#pragma unroll
+        for (int g = 1; g < MAXT; ++g)
+          if (g <= ngram) nacc[g] = fma(w0, wv[g - 1].x, fma(w1, wv[g - 1].y, nacc[g]));
+        const int64_t jg = r0 + jl;
+        const uint32_t bits = __ldg(sign_bits + (jg >> 5));
+        v[i] = make_double2((bits >> (jg & 31)) & 1u ? w0 : -w0, (bits >> ((jg + 1) & 31)) & 1u ? w1 : -w1);
+      }
+    }
+    dft16_half(v);
+#pragma unroll
+    for (int vv = 1; vv < 16; ++vv) v[vv] = cmul(v[vv], tw[(vv * t) & 255]);
+    __syncthreads();
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) X[p * kXS + vv * 16 + t] = v[vv];
+    __syncthreads();
+#pragma unroll
+    for (int tt = 0; tt < 16; ++tt) v[tt] = X[p * kXS + t * 16 + tt];
+    dft16(v);
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
+    __syncthreads();
+    for (int q = tid; q < s; q += blockDim.x) {
+      const uint64_t k = static_cast<uint64_t>(rows[q]);
+      const int u = uq[q], um = (256 - u) & 255;
+      const double2 zz = zq[q];
+      double2 S1 = X[(kPairs - 1) * kXS + u];
+      double2 Cm = X[(kPairs - 1) * kXS + um];
+      double2 S2 = make_double2(Cm.x, -Cm.y);
+#pragma unroll
+      for (int pp = kPairs - 2; pp >= 0; --pp) {
+        const double2 C = X[pp * kXS + u];
+        Cm = X[pp * kXS + um];
+        S1 = make_double2(fma(S1.x, zz.x, fma(-S1.y, zz.y, C.x)), fma(S1.x, zz.y, fma(S1.y, zz.x, C.y)));
+        S2 = make_double2(fma(S2.x, zz.x, fma(-S2.y, zz.y, Cm.x)), fma(S2.x, zz.y, fma(S2.y, zz.x, -Cm.y)));
+      }
+      double sn, cs;
+      const uint64_t ph = (k * static_cast<uint64_t>(r0 + a0)) % twoN;
+      sincospi(static_cast<double>(ph) / static_cast<double>(N), &sn, &cs);
+      const double2 tsum = cadd(cmul(ga[q], S1), cmul(gb[q], S2));
+      acc[q] = cadd(acc[q], cmul(make_double2(cs, sn), tsum));
+    }
+  }
+  // norm / Gram partials of this CTA into acc[s + g].x
+#pragma unroll
+  for (int g = 0; g < MAXT; ++g) {
+    const double v = warp_sum(nacc[g]);
+    if (lane == 0) nred[g][warp] = v;
+  }
+  __syncthreads();
+  if (tid < MAXT) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += nred[tid][w];
+    acc[s + tid] = make_double2(v, 0.0);
+  }
+  __syncthreads();
+  const int nacc_tot = s + MAXT;
+  int nparts = gridDim.x, part = blockIdx.x;
+  if (csize > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const bool leader = cl.block_rank() == 0;
+    if (leader) {
+      for (int q = tid; q < nacc_tot; q += blockDim.x) {
+        double2 sum = acc[q];
+        for (int r = 1; r < csize; ++r) sum = cadd(sum, cl.map_shared_rank(acc, r)[q]);
+        acc[q] = sum;
+      }
+    }
+    cl.sync();
+    if (!leader) return;
+    nparts = gridDim.x / csize;
+    part = blockIdx.x / csize;
+  }
+  for (int q = tid; q < s; q += blockDim.x) {
+    partials[static_cast<int64_t>(2 * q) * nparts + part] = acc[q].x;
+    partials[static_cast<int64_t>(2 * q + 1) * nparts + part] = acc[q].y;
+  }
+  for (int g = tid; g < MAXT; g += blockDim.x) partials[static_cast<int64_t>(2 * s + g) * nparts + part] = acc[s + g].x;
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = atomicAdd(counter, 1u) == static_cast<unsigned>(nparts - 1);
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  fold_partials(partials, nparts, 2 * s + MAXT, fold);
+  __syncthreads();
+  double* recB = rec + static_cast<int64_t>(j + 1) * rstride + b_off;
+  for (int q = tid; q < s; q += blockDim.x) {
+    const int64_t k = rows[q];
+    double sn, cs;
+    sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
+    recB[T + q] = (cs * fold[2 * q] - sn * fold[2 * q + 1]) * row_scale[q];
+  }
+  for (int g = tid; g < T; g += blockDim.x) recB[g] = (g <= ngram && g < MAXT) ? fold[2 * s + g] : 0.0;
+  if (tid == 0) *counter = 0u;
+}
+
 template <int NI, bool PAIRED>
 __global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict__ x, double xscale, int64_t N, int64_t r0,
                                                         int M, int64_t L, const uint32_t* __restrict__ sign_bits,
@@ -439,6 +627,48 @@ __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restri
 }
 
 }  // namespace
+
+bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
+                          int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec,
+                          const double* coef_ready, int64_t row_begin) {
+  constexpr int MAXT = 4;
+  if (S.kind != kSrdct || std::max(nwin, ngram + 1) > MAXT) return false;
+  const SrdctPlan p = plan_srdct(S.n, lay.nloc);
+  if (p.F != 256 || p.M != 128 || p.L % 2 || row_begin % 2 || lay.own_off % 2 || ldv % 2) return false;
+  const int64_t ntiles = (p.L + kTileA - 1) / kTileA;
+  int csize = ntiles >= 16 ? 8 : 1;
+  const int64_t per = (ntiles + 2 * c.num_sms - 1) / (2 * c.num_sms);
+  int grid = static_cast<int>((ntiles + per - 1) / per);
+  if (csize > 1) grid = std::max(csize, (grid + csize - 1) / csize * csize);
+  grid = static_cast<int>(std::min<int64_t>(grid, ntiles));
+  if (csize > 1 && grid % csize) csize = 1;
+  const size_t smem = sizeof(double2) * static_cast<size_t>(kPairs * kXS + 4 * S.s + MAXT + 256) + sizeof(int) * S.s;
+  static size_t configured = 0;
+  if (smem > configured) {
+    SDR_CUDA(cudaFuncSetAttribute(k_update_srdct256<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(csize);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TimedLaunch t(c, "update_sketch");
+  SDR_CUDA(cudaLaunchKernelEx(&cfg, k_update_srdct256<MAXT>, y, V, ldv, lay.own_off, j, nwin, ngram, rec, RL.stride,
+                              RL.T, cvec, coef_ready, S.n, row_begin, p.L, static_cast<const uint32_t*>(S.sign_bits.get()),
+                              static_cast<const int64_t*>(S.rows.get()), static_cast<const double*>(S.row_scale.get()),
+                              static_cast<int>(S.s), ntiles, csize, c.partials((2 * S.s + MAXT) * grid),
+                              c.counters() + 7, c.partials2(2 * S.s + MAXT)));
+  return true;
+}
 
 void launch_sketch(Context& c, const SketchDev& S, const double* x_own, int64_t nloc, int64_t row_begin, double* out) {
   launch_sketch_scaled(c, S, x_own, 1.0, nloc, row_begin, out);

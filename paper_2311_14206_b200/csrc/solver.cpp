@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <optional>
@@ -29,6 +30,15 @@ namespace sdr {
 
 namespace {
 constexpr int kLookahead = 2;
+
+/// SDR_FUSE=0 disables the fused update+sketch kernel (A/B and parity checks).
+bool fuse_update_sketch() {
+  static const bool on = [] {
+    const char* e = std::getenv("SDR_FUSE");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 
 struct Workspace {
   VecLayout lay;
@@ -242,8 +252,12 @@ struct ArnoldiPipeline {
     launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
                         w.rec.get(), R, T, w.cvec.get(), coef);
     c.allreduce_sum(recj + RL.a_off(), T + 1);
-    launch_update(c, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(), coef);
-    launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
+    if (!fuse_update_sketch() || !launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin,
+                                                       ngram, w.rec.get(), RL, w.cvec.get(), coef, A.row_begin)) {
+      launch_update(c, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(),
+                    coef);
+      launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
+    }
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
     SDR_CUDA(cudaMemcpyAsync(w.hrec.get() + (j + 1) * R, recj, sizeof(double) * R, cudaMemcpyDeviceToHost, c.stream));
     SDR_CUDA(cudaEventRecord(w.ev[static_cast<size_t>(j + 1)], c.stream));
@@ -637,11 +651,15 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
   pt_setup.reset();
   auto cur = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, 0);
   cur->init_enqueue(w.r0.get());
+  double step_ms = 0.0, finish_ms = 0.0;  // measured per-step and per-cycle-end wall times
   for (int cycle = 1; cycle <= cfg.max_restarts; ++cycle) {  // solver.hpp:321-359
     CycleOut cr;
+    double cycle_ms = 0.0;
     try {
+      const auto tc0 = std::chrono::steady_clock::now();
       cr = run_cycle(c, w, *cur, A, cfg, w.r0.get(), space, tol_abs, safety, rep.counters, rep, cb, cycle,
                      rep.iterations);
+      cycle_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count();
     } catch (const Error& e) {
       if (e.code != 2) throw;
       rep.status = 0;  // zero residual at cycle entry: converged exactly
@@ -674,12 +692,19 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
     }
     std::unique_ptr<ArnoldiPipeline> next;
     if (status < 0 && w.nV == 2) {
-      // overlap: next cycle's init + speculative steps on the other basis buffer
+      // overlap: next cycle's init + enough speculative steps on the other
+      // basis buffer to cover the host SVD/Schur of the finished cycle
       next = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, 1 - cur->vb);
       next->init_enqueue(w.r0.get());
-      next->issue_ahead(0);
+      i64 ahead = kLookahead;
+      if (step_ms > 0.0) ahead = static_cast<i64>(std::ceil(1.25 * finish_ms / step_ms)) + kLookahead;
+      else ahead = 32;
+      next->issue_ahead(std::min<i64>(ahead, cfg.m - 1));
     }
+    const auto tf0 = std::chrono::steady_clock::now();
     finish_cycle(c, w, *cur, cr, cfg, space, rep.counters, rep, cycle);
+    finish_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tf0).count();
+    if (cr.steps > 0) step_ms = cycle_ms / static_cast<double>(cr.steps);
     if (status >= 0) {
       rep.status = status;
       if (!note.empty()) rep.notes.push_back(note);

@@ -40,7 +40,7 @@ run(args.steps)
 wall = time.perf_counter() - t0
 out = {"N": N, "nnz": A.nnz, "steps": args.steps, "wall_ms_per_step": 1e3 * wall / args.steps,
        "K1_PIPE": os.environ.get("SDR_K1_PIPE", "0")}
-for k in ("spmv_arnoldi", "update", "sketch", "copy_norm"):
+for k in ("spmv_arnoldi", "update", "sketch", "update_sketch", "copy_norm"):
     n, ms = ctx.timing(k)
     if n:
         out[k] = round(1e3 * ms / n, 2)
