@@ -282,7 +282,7 @@ def main():
     ctx.timing_reset()
     rt = one(b_dev)
     ctx.synchronize()
-    ktimes = {k: ctx.timing(k) for k in ("spmv_arnoldi", "update", "sketch", "update_sketch", "tallskinny", "residual", "copy_norm",
+    ktimes = {k: ctx.timing(k) for k in ("spmv_arnoldi", "update", "sketch", "update_sketch", "tallskinny", "correction", "residual", "copy_norm",
                                          "allreduce", "halo", "axpy")}
     ctx.set_timing(False)
     kb = kernel_bytes(nloc, A.nnz, wl["t"], wl["sketch"])

@@ -143,39 +143,93 @@ __global__ void k_scale_copy(double a, const double* __restrict__ x, double* __r
 }
 
 /// out_o = sum_i coef[i*nout + o] * in_i, o < nout (<= NOUT); optional
-/// ||out_o||^2 via the deterministic grid fold. Coefficients are broadcast
-/// from shared memory; each input column is streamed once.
-template <int NOUT>
+/// ||out_o||^2 via the deterministic grid fold. Each thread owns RPT
+/// consecutive rows (RPT-wide vector loads) and keeps U input columns in
+/// flight; input pointers and coefficients are broadcast from shared memory,
+/// so every input column is streamed from HBM exactly once.
+template <int NOUT, int RPT, int U>
 __global__ void __launch_bounds__(kThreads) k_tallskinny(const double* const* __restrict__ in, int nin,
                                                           const double* __restrict__ coef, int nout,
                                                           double* const* __restrict__ out, int64_t n,
                                                           double* __restrict__ partials,
                                                           unsigned* __restrict__ counter, double* __restrict__ norms) {
-  extern __shared__ double cs[];  // nin * NOUT
+  extern __shared__ double cs[];  // nin * NOUT coefficients, then nin pointers
+  const double** ptr = reinterpret_cast<const double**>(cs + nin * NOUT);
   for (int q = threadIdx.x; q < nin * NOUT; q += blockDim.x) {
     const int i = q / NOUT, o = q % NOUT;
     cs[q] = o < nout ? coef[i * nout + o] : 0.0;
   }
+  for (int i = threadIdx.x; i < nin; i += blockDim.x) ptr[i] = in[i];
   __syncthreads();
   double nrm[NOUT];
 #pragma unroll
   for (int o = 0; o < NOUT; ++o) nrm[o] = 0.0;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
-    double a[NOUT];
-#pragma unroll
-    for (int o = 0; o < NOUT; ++o) a[o] = 0.0;
-    for (int i = 0; i < nin; ++i) {
-      const double v = __ldcs(in[i] + r);
-#pragma unroll
-      for (int o = 0; o < NOUT; ++o) a[o] = fma(cs[i * NOUT + o], v, a[o]);
-    }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * RPT;
+  const int64_t nfull = n / RPT * RPT;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * RPT; r < n; r += stride) {
+    double a[NOUT][RPT];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o)
-      if (o < nout) {
-        out[o][r] = a[o];
-        nrm[o] = fma(a[o], a[o], nrm[o]);
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) a[o][q] = 0.0;
+    const bool full = r < nfull;
+    for (int i0 = 0; i0 < nin; i0 += U) {
+      double v[U][RPT];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u < nin) {
+          const double* src = ptr[i0 + u] + r;
+          if (full && RPT == 2) {
+            const double2 t = __ldcs(reinterpret_cast<const double2*>(src));
+            v[u][0] = t.x;
+            v[u][RPT - 1] = t.y;
+          } else if (full && RPT == 4) {
+            const double2 t0 = __ldcs(reinterpret_cast<const double2*>(src));
+            const double2 t1 = __ldcs(reinterpret_cast<const double2*>(src) + 1);
+            v[u][0] = t0.x;
+            v[u][1 % RPT] = t0.y;
+            v[u][2 % RPT] = t1.x;
+            v[u][3 % RPT] = t1.y;
+          } else {
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) v[u][q] = r + q < n ? __ldcs(src + q) : 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) v[u][q] = 0.0;
+        }
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u < nin) {
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o) {
+            const double cf = cs[(i0 + u) * NOUT + o];
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) a[o][q] = fma(cf, v[u][q], a[o][q]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+      if (o < nout) {
+        double* dst = out[o] + r;
+        if (full && RPT == 2) {
+          *reinterpret_cast<double2*>(dst) = make_double2(a[o][0], a[o][RPT - 1]);
+        } else if (full && RPT == 4) {
+          reinterpret_cast<double2*>(dst)[0] = make_double2(a[o][0], a[o][1 % RPT]);
+          reinterpret_cast<double2*>(dst)[1] = make_double2(a[o][2 % RPT], a[o][3 % RPT]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < RPT; ++q)
+            if (r + q < n) dst[q] = a[o][q];
+        }
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+          if (r + q < n) nrm[o] = fma(a[o][q], a[o][q], nrm[o]);
+      }
+    }
   }
   if (norms) {
     block_partials<NOUT>(nrm, nout, partials);
@@ -205,17 +259,19 @@ void update_impl(Context& c, const double* y, double* V, int64_t ldv, const VecL
   SDR_KERNEL_CHECK();
 }
 
-template <int NOUT>
+template <int NOUT, int RPT, int U>
 void tallskinny_impl(Context& c, const double* const* in, int nin, const double* coef, int nout, double* const* out,
                      int64_t n, double* norms2) {
-  const int g = stream_grid(c, n);
-  const size_t smem = sizeof(double) * static_cast<size_t>(nin) * NOUT;
+  auto kern = k_tallskinny<NOUT, RPT, U>;
+  const size_t smem = sizeof(double) * static_cast<size_t>(nin) * NOUT + sizeof(void*) * static_cast<size_t>(nin);
   if (smem > 48 * 1024)
-    SDR_CUDA(cudaFuncSetAttribute(k_tallskinny<NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  TimedLaunch t(c, "tallskinny");
-  k_tallskinny<NOUT><<<g, kThreads, smem, c.stream>>>(in, nin, coef, nout, out, n,
-                                                      c.partials(static_cast<int64_t>(NOUT) * g), c.counters() + 3,
-                                                      norms2);
+    SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kThreads, smem);
+  const int64_t want = (n / RPT + kThreads - 1) / kThreads;
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.num_sms) * per_sm)));
+  TimedLaunch t(c, NOUT == 1 ? "correction" : "tallskinny");
+  kern<<<g, kThreads, smem, c.stream>>>(in, nin, coef, nout, out, n, c.partials(static_cast<int64_t>(NOUT) * g),
+                                        c.counters() + 3, norms2);
   SDR_KERNEL_CHECK();
 }
 
@@ -272,13 +328,15 @@ void launch_scale_copy(Context& c, double a, const double* x, double* y, int64_t
 void launch_tallskinny(Context& c, const double* const* in, int nin, const double* coef, int nout,
                        double* const* out, int64_t n, double* norms2) {
   if (nout <= 1)
-    tallskinny_impl<1>(c, in, nin, coef, nout, out, n, norms2);
+    tallskinny_impl<1, 4, 8>(c, in, nin, coef, nout, out, n, norms2);
   else if (nout <= 8)
-    tallskinny_impl<8>(c, in, nin, coef, nout, out, n, norms2);
+    tallskinny_impl<8, 2, 8>(c, in, nin, coef, nout, out, n, norms2);
   else if (nout <= 16)
-    tallskinny_impl<16>(c, in, nin, coef, nout, out, n, norms2);
+    tallskinny_impl<16, 2, 4>(c, in, nin, coef, nout, out, n, norms2);
+  else if (nout <= 24)
+    tallskinny_impl<24, 2, 4>(c, in, nin, coef, nout, out, n, norms2);
   else if (nout <= 32)
-    tallskinny_impl<32>(c, in, nin, coef, nout, out, n, norms2);
+    tallskinny_impl<32, 1, 8>(c, in, nin, coef, nout, out, n, norms2);
   else
     throw invalid("tall-skinny product with " + std::to_string(nout) + " outputs exceeds 32 per launch");
 }
