@@ -123,6 +123,10 @@ SDR_API int sdr_sketch_apply(sdr_ctx* ctx, const sdr_sketch* S, const double* x,
 
 /* -------------------------------------------------------- host pieces -- */
 SDR_API int sdr_gaussian_vector(int64_t n, uint64_t seed, double* out);
+/* Host generator behind sdr_sketch_create_srdct: rows (s, sorted) and signs
+ * (+1/-1, n; may be NULL) drawn from std::mt19937_64(seed) in the reference
+ * order (sketch.hpp:116-119). Needs no GPU. */
+SDR_API int sdr_srdct_indices(int64_t n, int64_t s, uint64_t seed, int64_t* rows, double* signs);
 /* Sparse-sign (row, sign) entries of columns [j0, j0+count): rows/signs hold count*zeta. */
 SDR_API int sdr_sparse_sign_entries(int64_t s, uint64_t seed, int64_t zeta, int64_t j0, int64_t count,
                                     int64_t* rows, double* signs);

@@ -342,6 +342,15 @@ def gaussian_vector(n, seed):
     return out
 
 
+def srdct_indices(n, s, seed, with_signs=True):
+    """(rows, signs) of SketchOperator::subsampled_dct(n, s, seed), host-side (sketch.hpp:105-122)."""
+    rows = np.empty(s, dtype=np.int64)
+    signs = np.empty(n) if with_signs else None
+    _check(_lib.sdr_srdct_indices(n, s, seed, rows.ctypes.data_as(C.c_void_p),
+                                  signs.ctypes.data_as(C.c_void_p) if with_signs else None))
+    return rows, signs
+
+
 def sparse_sign_entries(s, seed, zeta, j0, count):
     rows = np.empty(count * zeta, dtype=np.int64)
     signs = np.empty(count * zeta)

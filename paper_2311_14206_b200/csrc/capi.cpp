@@ -415,6 +415,18 @@ int sdr_gaussian_vector(int64_t n, uint64_t seed, double* out) {  // rng.hpp:45-
   });
 }
 
+int sdr_srdct_indices(int64_t n, int64_t s, uint64_t seed, int64_t* rows, double* signs) {
+  return guard([&] {
+    if (n < 2 || s < 1 || s >= n)
+      throw invalid("SketchOperator: need 1 <= s < n, got s = " + std::to_string(s) + ", n = " + std::to_string(n));
+    need(rows, "rows");
+    const SrdctHost h = make_srdct_host(n, s, seed);
+    std::memcpy(rows, h.rows.data(), sizeof(int64_t) * h.rows.size());
+    if (signs)
+      for (int64_t i = 0; i < n; ++i) signs[i] = (h.sign_bits[static_cast<size_t>(i >> 5)] >> (i & 31)) & 1u ? 1.0 : -1.0;
+  });
+}
+
 int sdr_sparse_sign_entries(int64_t s, uint64_t seed, int64_t zeta, int64_t j0, int64_t count, int64_t* rows,
                             double* signs) {
   return guard([&] {

@@ -1,0 +1,79 @@
+"""Generates tests/golden/*.json from the CPU oracle (oracle/, the C++
+restatement of the reference). The GPU tests compare the sm_100a path with
+these fixtures at BASELINE sizes where rerunning the oracle would take
+minutes. Run: python tests/golden/make_golden.py [c1 c2 c3 small]"""
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+import numpy as np  # noqa: E402
+
+from oracle import pyoracle as O  # noqa: E402
+
+
+def summary(x, rep, extra=None):
+    d = dict(status=rep.status, iterations=rep.iterations, cycles=rep.cycles, rhs_norm=rep.rhs_norm,
+             final_relative_residual=rep.final_relative_residual, counters=rep.counters,
+             sketched_residuals=rep.sketched_residuals, true_residuals=rep.true_residuals,
+             cycle_stats=rep.cycle_stats, notes=rep.notes, seconds=rep.seconds,
+             x_head=x[:16].tolist(), x_norm=float(np.linalg.norm(x)))
+    d.update(extra or {})
+    return d
+
+
+def c1():
+    """BASELINE C1: A = -gen_convdiff(100, -50), b = N(0,1) seed 0 normalised, m=50 k=10 t=2 s=120, tol 1e-8."""
+    off, col, val = O.gen_convdiff(100, -50.0).csr()
+    A = O.SparseMatrix.from_csr(10000, 10000, off, col, -val)
+    b = O.gaussian_vector(10000, 0)
+    b /= np.linalg.norm(b)
+    out = {}
+    for name, S in (("srdct", None), ("sparse_sign", O.SketchOperator.sparse_sign(10000, 120, 0x5EED, 8))):
+        cfg = O.SolverConfig(m=50, k=10, t=2, s=120, tol=1e-8, max_restarts=40)
+        x, rep = O.solve(A, b, cfg, sketch=S)
+        out[name] = summary(x, rep, dict(config=dict(m=50, k=10, t=2, s=120, tol=1e-8, max_restarts=40)))
+    return out
+
+
+def c2():
+    """BASELINE C2: 3D 128^3, beta=(100,50,25), b = gaussian_vector(N, 1), m=100 k=20 t=2 s=240 tol 1e-8."""
+    n = 128
+    A = O.gen_convdiff3d(n, 100.0, 50.0, 25.0)
+    b = O.gaussian_vector(n ** 3, 1)
+    cfg = O.SolverConfig(m=100, k=20, t=2, s=240, tol=1e-8)
+    t0 = time.time()
+    x, rep = O.solve(A, b, cfg)
+    return summary(x, rep, dict(config=dict(n=n, m=100, k=20, t=2, s=240, tol=1e-8), wall_s=time.time() - t0))
+
+
+def c3_small():
+    """C3-shaped sequence at a CPU-friendly size (64^2 grid, 5 systems)."""
+    n, count = 64, 5
+    rng = O
+    b0 = O.gaussian_vector(n * n, 0x3000)
+    mats, rhss = [], []
+    for i in range(count):
+        rel = 1e-3 * (2.0 * O.uniform_stream(0x3100 + i, n * n) - 1.0)
+        mats.append(O.gen_convdiff2d(n, 100.0 + 2 * i, 100.0 - 2 * i, 0.01 * i, rel))
+        rhss.append(b0 + 0.05 * O.gaussian_vector(n * n, 0x3000 + i) if i else b0.copy())
+    cfg = O.SolverConfig(m=50, k=20, t=2, s=140, tol=1e-8, variant="exact", max_restarts=20)
+    xs, reps = O.solve_sequence(mats, rhss, cfg)
+    return [summary(x, r) for x, r in zip(xs, reps)]
+
+
+def main(which):
+    jobs = {"c1": c1, "c2": c2, "c3_small": c3_small}
+    for name in which:
+        t0 = time.time()
+        data = jobs[name]()
+        path = os.path.join(HERE, f"{name}_oracle.json")
+        with open(path, "w") as fh:
+            json.dump(data, fh, indent=1)
+        print(f"{name}: wrote {path} in {time.time() - t0:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["c1", "c3_small", "c2"])
