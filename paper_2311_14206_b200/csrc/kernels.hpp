@@ -14,6 +14,7 @@ struct SellView {
   const int32_t* cols = nullptr;
   const double* vals = nullptr;
   int64_t nrows = 0, nslices = 0;
+  int64_t max_group = 0;  // max stored entries of any 8-slice group (bulk-staged K1)
 };
 
 /// Layout of every length-N vector a rank stores with halo space:

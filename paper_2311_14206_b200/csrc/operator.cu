@@ -127,6 +127,8 @@ DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int6
     sp[static_cast<size_t>(s) + 1] = sp[static_cast<size_t>(s)] + mx * kSlice;
   }
   const int64_t total = sp[static_cast<size_t>(nslices)];
+  for (int64_t s = 0; s < nslices; s += 8)
+    op->max_group = std::max(op->max_group, sp[static_cast<size_t>(std::min(nslices, s + 8))] - sp[static_cast<size_t>(s)]);
   std::vector<int32_t> hc(static_cast<size_t>(total));
   std::vector<double> hv(static_cast<size_t>(total));
   for (int64_t s = 0; s < nslices; ++s) {
@@ -239,6 +241,7 @@ DeviceOperator* create_operator_convdiff3d(Context& c, int64_t nx, int64_t ny, i
   if (op->halo_lo + op->local_rows + op->halo_hi > std::numeric_limits<int32_t>::max())
     throw invalid("gen_convdiff3d: local block exceeds int32 indexing");
   const int64_t nslices = (op->local_rows + kSlice - 1) / kSlice;
+  op->max_group = std::min<int64_t>(nslices, 8) * kSlice * 7;
   op->slice_ptr.resize(nslices + 1);
   op->cols_idx.resize(std::max<int64_t>(nslices * kSlice * 7, 1));
   op->vals.resize(std::max<int64_t>(nslices * kSlice * 7, 1));

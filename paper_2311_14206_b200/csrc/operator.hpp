@@ -20,6 +20,7 @@ struct DeviceOperator {
   DeviceBuffer<int32_t> cols_idx;
   DeviceBuffer<double> vals;
   HaloPlan plan;
+  int64_t max_group = 0;  // max stored entries over groups of 8 consecutive slices
 
   SellView view() const {
     SellView v;
@@ -28,6 +29,7 @@ struct DeviceOperator {
     v.vals = vals.get();
     v.nrows = local_rows;
     v.nslices = (local_rows + kSlice - 1) / kSlice;
+    v.max_group = max_group;
     return v;
   }
   /// Layout for vectors used as SpMV inputs of this operator.
