@@ -113,17 +113,19 @@ def dist_env():
     return rank, world, local
 
 
-def bytes_per_step(N, nnz, t):
-    """B_step = 12 nnz + 4 (N+1) + 8 N (4 + 2t) (+N/8 SRDCT sign bits)."""
-    return 12 * nnz + 4 * (N + 1) + 8 * N * (4 + 2 * t)
+def bytes_per_step(N, a_bytes, t):
+    """B_step = bytes(A) + 8 N (4 + 2t), with bytes(A) the
+    operator storage one SpMV streams (CSR in the reference: 12 nnz + 4 (N+1);
+    here SELL-DIA 8 B per stored entry, or SELL-32 12 B; A.storage["bytes"])."""
+    return a_bytes + 8 * N * (4 + 2 * t)
 
 
-def kernel_bytes(N, nnz, t, sketch):
+def kernel_bytes(N, a_bytes, t, sketch):
     """Algorithmic bytes per launch of each hot kernel."""
     return {
-        "spmv_arnoldi": 12 * nnz + 4 * (N + 1) + 8 * N * (2 + (t - 1)),  # A, x, y write, t-1 window reads
-        "update": 8 * N * (1 + t) + 8 * N,                                # y + t window reads, w write
-        "sketch": 8 * N + (N // 8 if sketch == "srdct" else 0),          # one read of w (+ sign bits)
+        "spmv_arnoldi": a_bytes + 8 * N * (2 + (t - 1)),          # A, x, y write, t-1 window reads
+        "update": 8 * N * (1 + t) + 8 * N,                        # y + t window reads, w write
+        "sketch": 8 * N + (N // 8 if sketch == "srdct" else 0),  # one read of w (+ sign bits)
     }
 
 
@@ -285,7 +287,7 @@ def main():
     ktimes = {k: ctx.timing(k) for k in ("spmv_arnoldi", "update", "sketch", "update_sketch", "tallskinny", "correction", "residual", "copy_norm",
                                          "allreduce", "halo", "axpy")}
     ctx.set_timing(False)
-    kb = kernel_bytes(nloc, A.nnz, wl["t"], wl["sketch"])
+    kb = kernel_bytes(nloc, A.storage["bytes"], wl["t"], wl["sketch"])
     peak, peak_kind = measured_peak()
     kern = {}
     for name, (cnt, tot) in ktimes.items():
@@ -300,7 +302,7 @@ def main():
         v["share"] = v["avg_us"] * v["launches"] / tot_all if tot_all else 0.0
     dom = max((k for k in kern if k in kb), key=lambda k: kern[k]["avg_us"] * kern[k]["launches"])
     step_us = sum(kern[k]["avg_us"] for k in kb if k in kern)
-    step_bytes = bytes_per_step(nloc, A.nnz, wl["t"])
+    step_bytes = bytes_per_step(nloc, A.storage["bytes"], wl["t"])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as fh:
@@ -330,7 +332,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE generators, seeded)",
-            "config": {"workload": args.config, "N": N, "N_per_gpu": nloc, "nnz": A.nnz, "m": wl["m"], "k": wl["k"],
+            "config": {"workload": args.config, "N": N, "N_per_gpu": nloc, "nnz": A.nnz, "storage": A.storage, "m": wl["m"], "k": wl["k"],
                        "t": wl["t"], "s": wl["s"], "tol": wl["tol"], "sketch": wl["sketch"],
                        "parallelism": f"zslab{world}", "l2": "inputs > L2 per solve (V basis 1.7 GB)"},
             "time_to_solution_ms": ms / args.steps,

@@ -98,6 +98,11 @@ SDR_API int sdr_csr_destroy(sdr_csr* A);
 /* rows/cols global; nnz local (stored, before SELL padding); row_begin/local_rows this rank. */
 SDR_API int sdr_csr_info(const sdr_csr* A, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* row_begin,
                          int64_t* local_rows, int64_t* halo_lo, int64_t* halo_hi);
+/* NEW: device storage chosen for the block. format 0 = SELL-32 (12 B per stored
+ * entry), 1 = SELL-DIA (8 B per stored entry + one int32 offset per slice
+ * diagonal); diagonals = DIA diagonals per slice (0 for SELL); stored =
+ * entries incl. padding; bytes = storage bytes one SpMV streams. */
+SDR_API int sdr_csr_storage(const sdr_csr* A, int32_t* format, int32_t* diagonals, int64_t* stored, int64_t* bytes);
 /* y = A x (OperatorRef::apply, operator_ref.hpp:38-44). x: local_rows entries of this
  * rank's block (halos are exchanged internally); y: local_rows entries. Host or device. */
 SDR_API int sdr_spmv(sdr_ctx* ctx, const sdr_csr* A, const double* x, int64_t xlen, double* y);

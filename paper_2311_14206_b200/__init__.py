@@ -194,6 +194,11 @@ class SparseMatrix:
         _check(_lib.sdr_csr_info(self._h, *[C.byref(x) for x in vals]))
         (self.rows, self.cols, self.nnz, self.row_begin, self.local_rows, self.halo_lo,
          self.halo_hi) = (x.value for x in vals)
+        fmt, dg, st, nb = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+        _check(_lib.sdr_csr_storage(self._h, C.byref(fmt), C.byref(dg), C.byref(st), C.byref(nb)))
+        # device storage: "sell" or "dia", diagonals per slice, stored entries, bytes per SpMV
+        self.storage = dict(format=("sell", "dia")[fmt.value], diagonals=dg.value, stored=st.value,
+                            bytes=nb.value)
 
     @classmethod
     def from_triplets(cls, rows, cols, r, c, v, ctx=None):

@@ -9,6 +9,7 @@
 #include "solver.hpp"
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -258,6 +259,19 @@ int sdr_csr_create_convdiff3d(sdr_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, 
 
 int sdr_csr_destroy(sdr_csr* A) {
   return guard([&] { delete A; });
+}
+
+int sdr_csr_storage(const sdr_csr* A, int32_t* format, int32_t* diagonals, int64_t* stored, int64_t* bytes) {
+  return guard([&] {
+    need(A, "A");
+    const auto& o = *A->op;
+    const int64_t nslices = (o.local_rows + sdr::kSlice - 1) / sdr::kSlice;
+    if (format) *format = o.dia ? 1 : 0;
+    if (diagonals) *diagonals = o.dia ? o.dia_d : 0;
+    if (stored) *stored = o.stored;
+    if (bytes)
+      *bytes = o.dia ? 8 * o.stored + 4 * nslices * o.dia_d : 12 * o.stored + 8 * (nslices + 1);
+  });
 }
 
 int sdr_csr_info(const sdr_csr* A, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* row_begin, int64_t* local_rows,
@@ -943,6 +957,28 @@ SDR_API int sdr_debug_norm2(sdr_ctx* ctx, const double* x, int64_t n, double* ou
     launch_copy_norm(c, xin.ptr, dst.get(), n, nrm.get());
     SDR_CUDA(cudaMemcpyAsync(out, nrm.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+  });
+}
+
+/* internal: kernel phase trace (SDR_TRACE=1); copies min(cap, size) entries, *n = size */
+SDR_API int sdr_debug_trace(sdr_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n) {
+  return guard([&] {
+    const auto v = ctx->c->trace_read();
+    if (n) *n = static_cast<int64_t>(v.size());
+    for (int64_t i = 0; i < std::min<int64_t>(cap, static_cast<int64_t>(v.size())); ++i) out[i] = v[static_cast<size_t>(i)];
+  });
+}
+
+/* internal: writes the timed-launch timeline (name,start_us,end_us) as CSV */
+SDR_API int sdr_debug_timeline(sdr_ctx* ctx, const char* path) {
+  return guard([&] {
+    Context& c = *ctx->c;
+    c.timing_flush();
+    FILE* f = std::fopen(path, "w");
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path);
+    std::fprintf(f, "name,start_us,end_us\n");
+    for (const auto& sp : c.timeline) std::fprintf(f, "%s,%.3f,%.3f\n", sp.name.c_str(), sp.start_us, sp.end_us);
+    std::fclose(f);
   });
 }
 

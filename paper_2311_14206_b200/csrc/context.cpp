@@ -3,6 +3,8 @@
 // loaded instead of linking a second copy), and event timing.
 #include "context.hpp"
 
+#include <cstdlib>
+
 #include <nccl.h>
 #include <dlfcn.h>
 
@@ -155,6 +157,10 @@ void Context::time_begin(const char* name) {
   open_name_ = name;
   open_start_ = take_event();
   SDR_CUDA(cudaEventRecord(open_start_, stream));
+  if (!origin_) {
+    SDR_CUDA(cudaEventCreate(&origin_));
+    SDR_CUDA(cudaEventRecord(origin_, stream));
+  }
 }
 
 void Context::time_end() {
@@ -174,6 +180,12 @@ void Context::timing_flush() {
     auto& t = timings[p.name];
     ++t.launches;
     t.ms += ms;
+    if (origin_ && timeline.size() < 100000) {
+      float s0 = 0.f, s1 = 0.f;
+      SDR_CUDA(cudaEventElapsedTime(&s0, origin_, p.a));
+      SDR_CUDA(cudaEventElapsedTime(&s1, origin_, p.b));
+      timeline.push_back({p.name, 1e3 * s0, 1e3 * s1});
+    }
     free_events_.push_back(p.a);
     free_events_.push_back(p.b);
   }
@@ -183,6 +195,33 @@ void Context::timing_flush() {
 void Context::timing_reset() {
   timing_flush();
   timings.clear();
+  timeline.clear();
+  if (origin_) {
+    SDR_CUDA(cudaEventDestroy(origin_));
+    origin_ = nullptr;
+  }
+}
+
+unsigned long long* Context::trace(i64 n) {
+  static const bool on = [] {
+    const char* e = std::getenv("SDR_TRACE");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!on) return nullptr;
+  if (trace_.size() < n) {
+    trace_.resize(n);
+    SDR_CUDA(cudaMemsetAsync(trace_.get(), 0, sizeof(unsigned long long) * static_cast<size_t>(n), stream));
+  }
+  return trace_.get();
+}
+
+std::vector<unsigned long long> Context::trace_read() {
+  std::vector<unsigned long long> out(static_cast<size_t>(trace_.size()));
+  if (!out.empty())
+    SDR_CUDA(cudaMemcpyAsync(out.data(), trace_.get(), sizeof(unsigned long long) * out.size(), cudaMemcpyDeviceToHost,
+                             stream));
+  sync();
+  return out;
 }
 
 }  // namespace sdr

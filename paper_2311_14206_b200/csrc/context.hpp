@@ -53,7 +53,10 @@ class Context {
     return partials2_.get();
   }
   unsigned* counters() { return counters_.get(); }  // kNumCounters slots
-  static constexpr int kNumCounters = 16;
+  /// Kernel phase trace buffer (SDR_TRACE=1, debugging only): null when off.
+  unsigned long long* trace(i64 n);
+  std::vector<unsigned long long> trace_read();
+  static constexpr int kNumCounters = 64;
 
   // ---- collectives (no-ops on one rank)
   void allreduce_sum(double* dev, i64 n);
@@ -67,6 +70,11 @@ class Context {
   void timing_flush();
   void timing_reset();
   std::map<std::string, KernelTiming> timings;
+  struct Span {
+    std::string name;
+    double start_us, end_us;  // from the first timed launch since timing_reset
+  };
+  std::vector<Span> timeline;  // debugging (sdr_debug_timeline)
 
   // ---- staging
   double* stage(i64 n) {
@@ -86,6 +94,7 @@ class Context {
  private:
   DeviceBuffer<double> partials_, partials2_, stage_;
   DeviceBuffer<unsigned> counters_;
+  DeviceBuffer<unsigned long long> trace_;
   PinnedBuffer<double> pinned_;
   NcclApi* nccl_ = nullptr;
   void* comm_ = nullptr;
@@ -97,6 +106,7 @@ class Context {
   std::vector<cudaEvent_t> free_events_;
   std::string open_name_;
   cudaEvent_t open_start_ = nullptr;
+  cudaEvent_t origin_ = nullptr;  // first event since timing_reset (kept)
   cudaEvent_t take_event();
 };
 

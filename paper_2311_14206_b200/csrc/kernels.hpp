@@ -13,8 +13,10 @@ struct SellView {
   const int64_t* slice_ptr = nullptr;  // nslices + 1 element offsets
   const int32_t* cols = nullptr;
   const double* vals = nullptr;
+  const int32_t* doff = nullptr;  // SELL-DIA: [nslices][dia_d] diagonal offsets; null for plain SELL
+  int dia_d = 0;                   // SELL-DIA diagonals per slice (slice_ptr unused)
   int64_t nrows = 0, nslices = 0;
-  int64_t max_group = 0;  // max stored entries of any 8-slice group (bulk-staged K1)
+  int64_t halo_lo = 0, ext_len = 0;  // own row r is extended index halo_lo + r
 };
 
 /// Layout of every length-N vector a rank stores with halo space:
@@ -76,6 +78,8 @@ void launch_sketch(Context& c, const SketchDev& S, const double* x_own, int64_t 
                    double* out);
 void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, double xscale, int64_t nloc,
                           int64_t row_begin, double* out);
+/// Builds SketchDev::tab / uq (per-row SRDCT constants) once per sketch.
+void prepare_srdct_tables(Context& c, SketchDev& S);
 /// Fused K2 + K3a (update pass and SRDCT of w_{j+1} in one sweep), writing
 /// the record's B part (norm, Gram, sketch). Returns false when the
 /// configuration is not eligible (caller runs K2 and K3 separately).

@@ -4,11 +4,21 @@
 #include "operator.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <memory>
 
 namespace sdr {
+
+/// SDR_DIA=0 forces plain SELL storage (A/B and parity checks).
+bool dia_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SDR_DIA");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 
 void partition_halo(int world, int rank, const int64_t* rb, const int64_t* re, const int64_t* mnc, const int64_t* mxc,
                     int64_t* recv_lo, int64_t* recv_cnt, int64_t* send_lo, int64_t* send_cnt) {
@@ -118,17 +128,74 @@ DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int6
   const int64_t ext_len = op->halo_lo + local_rows + op->halo_hi;
   if (ext_len > std::numeric_limits<int32_t>::max())
     throw invalid("SparseMatrix: local extended block of " + std::to_string(ext_len) + " rows exceeds int32 indexing");
-  // SELL-32 packing
   const int64_t nslices = (local_rows + kSlice - 1) / kSlice;
   std::vector<int64_t> sp(static_cast<size_t>(nslices) + 1, 0);
+  // SELL-DIA when every slice's entries lie on at most kMaxDiag diagonals
+  // (offset = column - row); gaps become explicit zeros.
+  constexpr size_t kMaxDiag = 16;
+  std::vector<std::vector<int64_t>> diag(static_cast<size_t>(nslices));
+  bool use_dia = local_rows > 0 && dia_enabled();
+  for (int64_t s = 0; s < nslices && use_dia; ++s) {
+    auto& d = diag[static_cast<size_t>(s)];
+    for (int64_t r = s * kSlice; r < std::min(local_rows, (s + 1) * kSlice) && use_dia; ++r)
+      for (int64_t p = off[r]; p < off[r + 1]; ++p) {
+        const int64_t o = col[p] - (row_begin + r);
+        if (std::find(d.begin(), d.end(), o) == d.end()) {
+          d.push_back(o);
+          if (d.size() > kMaxDiag) {
+            use_dia = false;
+            break;
+          }
+        }
+      }
+    std::sort(d.begin(), d.end());
+  }
+  size_t D = 0;
+  int64_t used = 0;
+  for (const auto& d : diag) {
+    D = std::max(D, d.size());
+    used += static_cast<int64_t>(d.size());
+  }
+  // uniform D per slice (no slice_ptr indirection); padding is offset 0 /
+  // value 0 and must stay below 1/8 of the stored diagonals
+  if (use_dia && static_cast<int64_t>(D) * nslices * 8 > used * 9) use_dia = false;
+  if (use_dia) {
+    const int64_t total = static_cast<int64_t>(D) * nslices * kSlice;
+    for (int64_t s = 0; s <= nslices; ++s) sp[static_cast<size_t>(s)] = s * static_cast<int64_t>(D) * kSlice;
+    std::vector<int32_t> hd(static_cast<size_t>(total / kSlice), 0);
+    std::vector<double> hv(static_cast<size_t>(total), 0.0);
+    for (int64_t s = 0; s < nslices; ++s) {
+      const auto& d = diag[static_cast<size_t>(s)];
+      const int64_t base = sp[static_cast<size_t>(s)];
+      for (size_t k = 0; k < d.size(); ++k) hd[static_cast<size_t>(base / kSlice) + k] = static_cast<int32_t>(d[k]);
+      for (int64_t r = s * kSlice; r < std::min(local_rows, (s + 1) * kSlice); ++r)
+        for (int64_t p = off[r]; p < off[r + 1]; ++p) {
+          const int64_t k = std::lower_bound(d.begin(), d.end(), col[p] - (row_begin + r)) - d.begin();
+          hv[static_cast<size_t>(base + k * kSlice + (r - s * kSlice))] = val[p];
+        }
+    }
+    op->dia = true;
+    op->dia_d = static_cast<int>(D);
+    op->stored = total;
+    op->slice_ptr.resize(nslices + 1);
+    op->doff.resize(std::max<int64_t>(total / kSlice, 1));
+    op->vals.resize(std::max<int64_t>(total, 1));
+    SDR_CUDA(cudaMemcpyAsync(op->slice_ptr.get(), sp.data(), sizeof(int64_t) * sp.size(), cudaMemcpyHostToDevice, c.stream));
+    if (total) {
+      SDR_CUDA(cudaMemcpyAsync(op->doff.get(), hd.data(), sizeof(int32_t) * hd.size(), cudaMemcpyHostToDevice, c.stream));
+      SDR_CUDA(cudaMemcpyAsync(op->vals.get(), hv.data(), sizeof(double) * hv.size(), cudaMemcpyHostToDevice, c.stream));
+    }
+    c.sync();
+    return op.release();
+  }
+  // SELL-32 packing
   for (int64_t s = 0; s < nslices; ++s) {
     int64_t mx = 0;
     for (int64_t r = s * kSlice; r < std::min(local_rows, (s + 1) * kSlice); ++r) mx = std::max(mx, off[r + 1] - off[r]);
     sp[static_cast<size_t>(s) + 1] = sp[static_cast<size_t>(s)] + mx * kSlice;
   }
   const int64_t total = sp[static_cast<size_t>(nslices)];
-  for (int64_t s = 0; s < nslices; s += 8)
-    op->max_group = std::max(op->max_group, sp[static_cast<size_t>(std::min(nslices, s + 8))] - sp[static_cast<size_t>(s)]);
+  op->stored = total;
   std::vector<int32_t> hc(static_cast<size_t>(total));
   std::vector<double> hv(static_cast<size_t>(total));
   for (int64_t s = 0; s < nslices; ++s) {
@@ -193,6 +260,41 @@ __global__ void k_gen_convdiff3d(int64_t nx, int64_t ny, int64_t nz, int64_t row
   }
 }
 
+// SELL-DIA form of the same operator: every slice uses the seven offsets
+// {-nx*ny, -nx, -1, 0, 1, nx, nx*ny} (increasing column = CSR order); entries
+// whose neighbour is outside the grid hold 0 (the column is clamped in K1).
+__global__ void k_gen_convdiff3d_dia(int64_t nx, int64_t ny, int64_t nz, int64_t row_begin, int64_t local_rows,
+                                     double diag, double mx, double px, double my, double py, double mz, double pz,
+                                     double* __restrict__ vals) {
+  const int64_t nslices = (local_rows + kSlice - 1) / kSlice;
+  const int64_t total = nslices * kSlice;
+  const int64_t n2 = nx * ny;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < total;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = r / kSlice, lane = r % kSlice;
+    double* v = vals + s * kSlice * 7 + lane;
+    const bool live = r < local_rows;
+    const int64_t p = row_begin + (live ? r : 0);
+    const int64_t z = p / n2, y = (p / nx) % ny, x = p % nx;
+    v[0 * kSlice] = live && z > 0 ? mz : 0.0;
+    v[1 * kSlice] = live && y > 0 ? my : 0.0;
+    v[2 * kSlice] = live && x > 0 ? mx : 0.0;
+    v[3 * kSlice] = live ? diag : 0.0;
+    v[4 * kSlice] = live && x + 1 < nx ? px : 0.0;
+    v[5 * kSlice] = live && y + 1 < ny ? py : 0.0;
+    v[6 * kSlice] = live && z + 1 < nz ? pz : 0.0;
+  }
+}
+
+__global__ void k_fill_doff(int32_t* doff, int64_t nslices, int32_t nx, int32_t n2) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nslices * 7;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % 7);
+    const int32_t o[7] = {-n2, -nx, -1, 0, 1, nx, n2};
+    doff[i] = o[k];
+  }
+}
+
 __global__ void k_fill_slice_ptr(int64_t* sp, int64_t nslices, int64_t width) {
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s <= nslices;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -241,17 +343,29 @@ DeviceOperator* create_operator_convdiff3d(Context& c, int64_t nx, int64_t ny, i
   if (op->halo_lo + op->local_rows + op->halo_hi > std::numeric_limits<int32_t>::max())
     throw invalid("gen_convdiff3d: local block exceeds int32 indexing");
   const int64_t nslices = (op->local_rows + kSlice - 1) / kSlice;
-  op->max_group = std::min<int64_t>(nslices, 8) * kSlice * 7;
+  op->dia = dia_enabled() && n2 <= std::numeric_limits<int32_t>::max();
+  op->dia_d = op->dia ? 7 : 0;
+  op->stored = nslices * kSlice * 7;
   op->slice_ptr.resize(nslices + 1);
-  op->cols_idx.resize(std::max<int64_t>(nslices * kSlice * 7, 1));
   op->vals.resize(std::max<int64_t>(nslices * kSlice * 7, 1));
+  if (op->dia)
+    op->doff.resize(std::max<int64_t>(nslices * 7, 1));
+  else
+    op->cols_idx.resize(std::max<int64_t>(nslices * kSlice * 7, 1));
   if (nslices > 0) {
     const int g = static_cast<int>(std::min<int64_t>((nslices * kSlice + 255) / 256, 148 * 16));
     k_fill_slice_ptr<<<g, 256, 0, c.stream>>>(op->slice_ptr.get(), nslices, kSlice * 7);
     SDR_KERNEL_CHECK();
-    k_gen_convdiff3d<<<g, 256, 0, c.stream>>>(nx, ny, nz, op->row_begin, op->local_rows, op->ext_begin, diag, coef[0],
-                                             coef[1], coef[2], coef[3], coef[4], coef[5], op->cols_idx.get(),
-                                             op->vals.get());
+    if (op->dia) {
+      k_fill_doff<<<g, 256, 0, c.stream>>>(op->doff.get(), nslices, static_cast<int32_t>(nx), static_cast<int32_t>(n2));
+      SDR_KERNEL_CHECK();
+      k_gen_convdiff3d_dia<<<g, 256, 0, c.stream>>>(nx, ny, nz, op->row_begin, op->local_rows, diag, coef[0], coef[1],
+                                                    coef[2], coef[3], coef[4], coef[5], op->vals.get());
+    } else {
+      k_gen_convdiff3d<<<g, 256, 0, c.stream>>>(nx, ny, nz, op->row_begin, op->local_rows, op->ext_begin, diag,
+                                               coef[0], coef[1], coef[2], coef[3], coef[4], coef[5],
+                                               op->cols_idx.get(), op->vals.get());
+    }
     SDR_KERNEL_CHECK();
   }
   c.sync();

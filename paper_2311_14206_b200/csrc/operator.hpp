@@ -17,19 +17,25 @@ struct DeviceOperator {
   int64_t ext_begin = 0;                  // global row of extended-vector index 0
   int64_t halo_lo = 0, halo_hi = 0;
   DeviceBuffer<int64_t> slice_ptr;
-  DeviceBuffer<int32_t> cols_idx;
+  DeviceBuffer<int32_t> cols_idx;  // SELL
+  DeviceBuffer<int32_t> doff;      // SELL-DIA
   DeviceBuffer<double> vals;
   HaloPlan plan;
-  int64_t max_group = 0;  // max stored entries over groups of 8 consecutive slices
+  bool dia = false;
+  int dia_d = 0;  // SELL-DIA diagonals per slice
+  int64_t stored = 0;  // stored entries (incl. padding) — bytes = stored * (dia ? 8 : 12)
 
   SellView view() const {
     SellView v;
     v.slice_ptr = slice_ptr.get();
-    v.cols = cols_idx.get();
+    v.cols = dia ? nullptr : cols_idx.get();
+    v.doff = dia ? doff.get() : nullptr;
+    v.dia_d = dia ? dia_d : 0;
     v.vals = vals.get();
     v.nrows = local_rows;
     v.nslices = (local_rows + kSlice - 1) / kSlice;
-    v.max_group = max_group;
+    v.halo_lo = halo_lo;
+    v.ext_len = halo_lo + local_rows + halo_hi;
     return v;
   }
   /// Layout for vectors used as SpMV inputs of this operator.

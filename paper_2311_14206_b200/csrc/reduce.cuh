@@ -40,20 +40,27 @@ __device__ __forceinline__ void block_partials(const double (&v)[NV], int nv, do
   }
 }
 
-/// Atomic ticket: true in exactly one CTA, after every CTA's partials are
-/// globally visible. The ticket counter is reset by the caller's last CTA.
-__device__ __forceinline__ bool last_block_done(unsigned* counter) {
-  __shared__ bool am_last;
-  __threadfence();
+/// Ticket over `expected` arriving CTAs: true in exactly one CTA, after every
+/// arriving CTA's global writes have reached L2. Thread 0's release atomic
+/// publishes the CTA's writes (cumulative through the preceding bar.sync);
+/// the last CTA reads them with L1-bypassing loads (ld.cg) only after its
+/// atomic returned — the threadFenceReduction pattern. No acquire fence on
+/// the reader side: an acquire invalidates L1 (CCTL.IVALL), after which
+/// every spilled-register reload of the folding CTA misses to L2/HBM, which
+/// showed up as a multi-µs kernel tail. The caller resets *ctr.
+__device__ __forceinline__ bool ticket(unsigned* ctr, unsigned expected) {
+  __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned ticket = atomicAdd(counter, 1u);
-    am_last = (ticket == gridDim.x - 1);
+    unsigned prev;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
+    last = prev == expected - 1u;
   }
   __syncthreads();
-  if (am_last) __threadfence();
-  return am_last;
+  return last;
 }
+
+__device__ __forceinline__ bool last_block_done(unsigned* counter) { return ticket(counter, gridDim.x); }
 
 /// In the last CTA: out[k * out_stride] = sum_b partials[k * nblocks + b] for
 /// k < nv, in a fixed order. Wide two-level fold: the CTA's threads split

@@ -173,7 +173,6 @@ __global__ void __launch_bounds__(kThreads) k_srdct(const double* __restrict__ x
 // stage 2 (after one padded shared-memory transpose) a 16-point DFT over t.
 // Only M/16 of the 16 stage-1 inputs are nonzero (zero padding b >= M).
 
-constexpr int kPairs = 16;   // 32 columns a per tile
 constexpr int kXS = 257;     // padded row stride (double2) -> conflict-free transposes
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -238,357 +237,345 @@ __device__ __forceinline__ void dft16_half(double2 (&a)[16]) {
   for (int n = 0; n < 16; ++n) a[n] = b[n];
 }
 
-// ------------------------------------------------ fused K2 + K3a (F = 256)
-// One pass over the step's vectors: the Arnoldi update
+// ------------------------------------------------ F = 256 tile kernels
+// One kernel template serves the plain sketch (SRC = kSrcSketch, input z =
+// sign ⊙ xscale·x) and the fused Arnoldi update (SRC = kSrcUpdate):
 //   w_{j+1} = c_j y - sum_d h_{j-d} c_{j-d} w_{j-d}          (arnoldi.hpp:91-114)
-// is evaluated in the SRDCT tile order (it is elementwise, so any order is
-// valid), w_{j+1} is stored once, its norm / Gram partials are accumulated,
-// and the sign-flipped values go straight from registers into the stage-1
-// FFT. HBM traffic is the update's alone (y + window reads, one write); the
-// sketch's FFT and row accumulation overlap with it instead of re-reading
-// w_{j+1} in a second kernel. Requires M = 128 (F = 256) and an even block.
-template <int MAXT>
-__global__ void __launch_bounds__(kThreads, 2) k_update_srdct256(
-    const double* __restrict__ y, double* __restrict__ V, int64_t ldv, int64_t own_off, int j, int nwin, int ngram,
-    double* __restrict__ rec, int64_t rstride, int T, double* __restrict__ cvec, const double* __restrict__ coef_ready,
-    int64_t N, int64_t r0, int64_t L, const uint32_t* __restrict__ sign_bits, const int64_t* __restrict__ rows,
-    const double* __restrict__ row_scale, int s, int64_t ntiles, int csize, double* __restrict__ partials,
-    unsigned* __restrict__ counter, double* __restrict__ fold) {
+// evaluated in the SRDCT tile order (elementwise, so any order is valid);
+// w_{j+1} is stored once, its norm / Gram partials are accumulated, and the
+// sign-flipped values go from registers straight into the stage-1 FFT. HBM
+// traffic is the update's alone (y + window reads, one write).
+//
+// Work split: one CTA per SM owns the contiguous tile range [tb, te); each of
+// its kGroups tile groups walks its share downwards, so the two Horner
+// recurrences over column pairs (z = e^{2 i pi k / N} per pair) continue from
+// tile to tile (jumping over the other groups' tiles with a precomputed
+// z^{8 (kGroups-1)}); the phase of a group's lowest tile,
+// e^{i pi k (r0 + 16 t_low) / N}, is applied once at the end with an exact
+// integer reduction. Per-row constants come precomputed with the sketch
+// (SketchDev::tab). CTA partials go out CTA-major and a separate small
+// kernel (k_srdct_fold) folds them in a fixed order — deterministic, no
+// floating-point atomics, and no serial last-CTA tail.
+enum { kSrcSketch = 0, kSrcUpdate = 1 };
+
+struct TileArgs {
+  int64_t N = 0, r0 = 0, L = 0, ntiles = 0;
+  int M = 0, s = 0;
+  const uint32_t* sign_bits = nullptr;
+  const int64_t* rows = nullptr;
+  const double* row_scale = nullptr;
+  const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][twiddle 256]
+  const int* uq = nullptr;       // k mod 256
+  double* partials = nullptr;    // [G][nvp] CTA partials
+  unsigned long long* trace = nullptr;  // SDR_TRACE: per-CTA phase timestamps [G][16]
+};
+
+__device__ __forceinline__ void trace_mark(unsigned long long* tr, int slot) {
+  if (tr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * 16 + slot] = t;
+  }
+}
+
+struct UpdateArgs {
+  const double* y = nullptr;
+  double* V = nullptr;
+  int64_t ldv = 0, own_off = 0, rstride = 0;
+  int j = 0, nwin = 0, ngram = 0, T = 0;
+  double* rec = nullptr;
+  double* cvec = nullptr;
+  const double* coef_ready = nullptr;
+};
+
+// Tile-group layout: a CTA of kGroups x 128 threads per SM. Each group of
+// four warps owns its own tiles (8 column pairs x 128 rows), transpose
+// buffer and Horner state and synchronises on its own named barrier, so the
+// groups' load, FFT and accumulation phases interleave on the SM.
+constexpr int kGPairs = 8;                       // column pairs per tile (16 columns)
+constexpr int kGThreads = kGPairs * 16;          // threads per group
+constexpr int kGroups = 4;
+constexpr int kCtaThreads = kGroups * kGThreads; // 512
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGThreads) : "memory");
+}
+
+template <int SRC, int NI, bool PAIRED, int MAXT>
+__global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, const double* __restrict__ x,
+                                                                 double xscale, double* __restrict__ out,
+                                                                 UpdateArgs ua) {
   extern __shared__ double2 sm[];
-  double2* X = sm;                    // [16][257]
-  double2* acc = X + kPairs * kXS;    // [s] sketch rows, then [MAXT] norm/Gram (as .x)
-  double2* zq = acc + s + MAXT;
-  double2* ga = zq + s;
-  double2* gb = ga + s;
-  double2* tw = gb + s;
-  int* uq = reinterpret_cast<int*>(tw + 256);
-  __shared__ double coef[MAXT + 1];
-  __shared__ double nred[MAXT][kThreads / 32];
+  const int s = ta.s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t twoN = 2u * static_cast<uint64_t>(N);
-  const int b_off = 2 * T + 3;
-  for (int k = tid; k < 256; k += blockDim.x) {
-    double sn, cs;
-    sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
-    tw[k] = make_double2(cs, sn);
+  const int g = tid / kGThreads, lt = tid % kGThreads;
+  double2* X = sm + g * (kGPairs * kXS);                  // [8][257] per group
+  double2* S1s = sm + kGroups * (kGPairs * kXS) + g * 2 * s;  // [s] per group
+  double2* S2s = S1s + s;                                  // [s] per group
+  double2* zq = sm + kGroups * (kGPairs * kXS + 2 * s);   // [s]  z = e^{2 i pi k/N}
+  double2* zj = zq + s;                                    // [s]  z^{8 (kGroups - 1)}: jump over the other groups' tiles
+  double2* tw = zj + s;                                    // [256]
+  int* uq = reinterpret_cast<int*>(tw + 256);              // [s]
+  __shared__ double coef[MAXT + 1];
+  __shared__ double nred[MAXT][kCtaThreads / 32];
+  const int G = gridDim.x, b = blockIdx.x;
+  const uint64_t twoN = 2u * static_cast<uint64_t>(ta.N);
+  trace_mark(ta.trace, 0);
+  for (int k = tid; k < 256; k += kCtaThreads) tw[k] = ta.tab[5 * s + k];
+  for (int q = tid; q < s; q += kCtaThreads) {
+    zq[q] = ta.tab[2 * s + q];
+    zj[q] = ta.tab[4 * s + q];
+    uq[q] = ta.uq[q];
   }
-  for (int q = tid; q < s; q += blockDim.x) {
-    const int64_t k = rows[q];
-    double sn, cs;
-    sincospi(static_cast<double>(k) / static_cast<double>(N), &sn, &cs);
-    ga[q] = make_double2(0.5 * (1.0 + sn), -0.5 * cs);
-    gb[q] = make_double2(0.5 * (1.0 - sn), 0.5 * cs);
-    sincospi(static_cast<double>((2 * static_cast<uint64_t>(k)) % twoN) / static_cast<double>(N), &sn, &cs);
-    zq[q] = make_double2(cs, sn);
-    uq[q] = static_cast<int>(k & 255);
-    acc[q] = make_double2(0.0, 0.0);
-  }
-  if (coef_ready) {
-    if (tid <= MAXT) coef[tid] = tid <= nwin ? coef_ready[tid] : 0.0;
-  } else if (tid == 0) {
-    mgs_coefficients<MAXT>(rec, rstride, T, j, nwin, cvec, coef, blockIdx.x == 0);
+  for (int q = tid; q < kGroups * 2 * s; q += kCtaThreads) S1s[q - g * 2 * s] = make_double2(0.0, 0.0);
+  if constexpr (SRC == kSrcUpdate) {
+    if (ua.coef_ready) {
+      if (tid <= MAXT) coef[tid] = tid <= ua.nwin ? ua.coef_ready[tid] : 0.0;
+    } else if (tid == 0) {
+      mgs_coefficients<MAXT>(ua.rec, ua.rstride, ua.T, ua.j, ua.nwin, ua.cvec, coef, b == 0);
+    }
   }
   __syncthreads();
+  trace_mark(ta.trace, 1);
   double cf[MAXT + 1];
-#pragma unroll
-  for (int k = 0; k <= MAXT; ++k) cf[k] = coef[k];
   const double* W[MAXT];
-#pragma unroll
-  for (int d = 0; d < MAXT; ++d) W[d] = V + static_cast<int64_t>(j - (d < nwin ? d : 0)) * ldv + own_off;
-  double* wout = V + static_cast<int64_t>(j + 1) * ldv + own_off;
+  double* wout = nullptr;
   double nacc[MAXT];
 #pragma unroll
-  for (int g = 0; g < MAXT; ++g) nacc[g] = 0.0;
-  const int p = tid & 15, t = tid >> 4;
+  for (int k = 0; k < MAXT; ++k) nacc[k] = 0.0;
+  if constexpr (SRC == kSrcUpdate) {
+#pragma unroll
+    for (int k = 0; k <= MAXT; ++k) cf[k] = coef[k];
+#pragma unroll
+    for (int d = 0; d < MAXT; ++d)
+      W[d] = ua.V + static_cast<int64_t>(ua.j - (d < ua.nwin ? d : 0)) * ua.ldv + ua.own_off;
+    wout = ua.V + static_cast<int64_t>(ua.j + 1) * ua.ldv + ua.own_off;
+  }
+  const int p = lt & (kGPairs - 1), t = lt / kGPairs;
+  const int nI = NI ? NI : (ta.M >> 4);  // <= 8 nonzero stage-1 inputs
+  // CTA b owns tiles [tb, te); group g takes te-1-g, te-1-g-kGroups, ... (descending)
+  const int64_t tb = static_cast<int64_t>(b) * ta.ntiles / G, te = static_cast<int64_t>(b + 1) * ta.ntiles / G;
+  int64_t tlow = -1;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t a0 = tile * (2 * kPairs);
-    const int64_t aa = a0 + 2 * p;
+  for (int64_t tile = te - 1 - g; tile >= tb; tile -= kGroups) {
+    const int64_t aa = tile * (2 * kGPairs) + 2 * p;
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = make_double2(0.0, 0.0);
-    if (aa < L) {
+    if (aa < ta.L) {
+      if constexpr (SRC == kSrcUpdate) {
+        // loads in chunks of CH rows, all issued before the chunk's math
+        constexpr int CH = MAXT <= 2 ? 2 : 1;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t jl = aa + L * static_cast<int64_t>(t + 16 * i);
-        const double2 yv = __ldcs(reinterpret_cast<const double2*>(y + jl));
-        double2 wv[MAXT];
+        for (int i0 = 0; i0 < 8; i0 += CH) {
+          double2 yv[CH], wv[CH][MAXT];
+          uint32_t bits[CH];
 #pragma unroll
-        for (int d = MAXT - 1; d >= 0; --d)
-          if (d < nwin) wv[d] = __ldg(reinterpret_cast<const double2*>(W[d] + jl));
-        double w0 = cf[0] * yv.x, w1 = cf[0] * yv.y;
+          for (int c = 0; c < CH; ++c) {
+            const int64_t jl = aa + ta.L * static_cast<int64_t>(t + 16 * (i0 + c));
+            yv[c] = __ldcs(reinterpret_cast<const double2*>(ua.y + jl));
 #pragma unroll
-        for (int d = MAXT - 1; d >= 0; --d)
-          if (d < nwin) {
-            w0 = fma(cf[1 + d], wv[d].x, w0);
-            w1 = fma(cf[1 + d], wv[d].y, w1);
+            for (int d = 0; d < MAXT; ++d)
+              if (d < ua.nwin) wv[c][d] = __ldg(reinterpret_cast<const double2*>(W[d] + jl));
+            bits[c] = __ldg(ta.sign_bits + ((ta.r0 + jl) >> 5));
           }
-        *reinterpret_cast<double2*>(wout + jl) = make_double2(w0, w1);
-        nacc[0] = fma(w0, w0, fma(w1, w1, nacc[0]));
 #pragma unroll
-        for (int g = 1; g < MAXT; ++g)
-          if (g <= ngram) nacc[g] = fma(w0, wv[g - 1].x, fma(w1, wv[g - 1].y, nacc[g]));
-        const int64_t jg = r0 + jl;
-        const uint32_t bits = __ldg(sign_bits + (jg >> 5));
-        v[i] = make_double2((bits >> (jg & 31)) & 1u ? w0 : -w0, (bits >> ((jg + 1) & 31)) & 1u ? w1 : -w1);
-      }
-    }
-    dft16_half(v);
+          for (int c = 0; c < CH; ++c) {
+            const int64_t jl = aa + ta.L * static_cast<int64_t>(t + 16 * (i0 + c));
+            double w0 = cf[0] * yv[c].x, w1 = cf[0] * yv[c].y;
 #pragma unroll
-    for (int vv = 1; vv < 16; ++vv) v[vv] = cmul(v[vv], tw[(vv * t) & 255]);
-    __syncthreads();
+            for (int d = MAXT - 1; d >= 0; --d)
+              if (d < ua.nwin) {
+                w0 = fma(cf[1 + d], wv[c][d].x, w0);
+                w1 = fma(cf[1 + d], wv[c][d].y, w1);
+              }
+            *reinterpret_cast<double2*>(wout + jl) = make_double2(w0, w1);
+            nacc[0] = fma(w0, w0, fma(w1, w1, nacc[0]));
 #pragma unroll
-    for (int vv = 0; vv < 16; ++vv) X[p * kXS + vv * 16 + t] = v[vv];
-    __syncthreads();
-#pragma unroll
-    for (int tt = 0; tt < 16; ++tt) v[tt] = X[p * kXS + t * 16 + tt];
-    dft16(v);
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
-    __syncthreads();
-    for (int q = tid; q < s; q += blockDim.x) {
-      const uint64_t k = static_cast<uint64_t>(rows[q]);
-      const int u = uq[q], um = (256 - u) & 255;
-      const double2 zz = zq[q];
-      double2 S1 = X[(kPairs - 1) * kXS + u];
-      double2 Cm = X[(kPairs - 1) * kXS + um];
-      double2 S2 = make_double2(Cm.x, -Cm.y);
-#pragma unroll
-      for (int pp = kPairs - 2; pp >= 0; --pp) {
-        const double2 C = X[pp * kXS + u];
-        Cm = X[pp * kXS + um];
-        S1 = make_double2(fma(S1.x, zz.x, fma(-S1.y, zz.y, C.x)), fma(S1.x, zz.y, fma(S1.y, zz.x, C.y)));
-        S2 = make_double2(fma(S2.x, zz.x, fma(-S2.y, zz.y, Cm.x)), fma(S2.x, zz.y, fma(S2.y, zz.x, -Cm.y)));
-      }
-      double sn, cs;
-      const uint64_t ph = (k * static_cast<uint64_t>(r0 + a0)) % twoN;
-      sincospi(static_cast<double>(ph) / static_cast<double>(N), &sn, &cs);
-      const double2 tsum = cadd(cmul(ga[q], S1), cmul(gb[q], S2));
-      acc[q] = cadd(acc[q], cmul(make_double2(cs, sn), tsum));
-    }
-  }
-  // norm / Gram partials of this CTA into acc[s + g].x
-#pragma unroll
-  for (int g = 0; g < MAXT; ++g) {
-    const double v = warp_sum(nacc[g]);
-    if (lane == 0) nred[g][warp] = v;
-  }
-  __syncthreads();
-  if (tid < MAXT) {
-    double v = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) v += nred[tid][w];
-    acc[s + tid] = make_double2(v, 0.0);
-  }
-  __syncthreads();
-  const int nacc_tot = s + MAXT;
-  int nparts = gridDim.x, part = blockIdx.x;
-  if (csize > 1) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    cl.sync();
-    const bool leader = cl.block_rank() == 0;
-    if (leader) {
-      for (int q = tid; q < nacc_tot; q += blockDim.x) {
-        double2 sum = acc[q];
-        for (int r = 1; r < csize; ++r) sum = cadd(sum, cl.map_shared_rank(acc, r)[q]);
-        acc[q] = sum;
-      }
-    }
-    cl.sync();
-    if (!leader) return;
-    nparts = gridDim.x / csize;
-    part = blockIdx.x / csize;
-  }
-  for (int q = tid; q < s; q += blockDim.x) {
-    partials[static_cast<int64_t>(2 * q) * nparts + part] = acc[q].x;
-    partials[static_cast<int64_t>(2 * q + 1) * nparts + part] = acc[q].y;
-  }
-  for (int g = tid; g < MAXT; g += blockDim.x) partials[static_cast<int64_t>(2 * s + g) * nparts + part] = acc[s + g].x;
-  __shared__ bool am_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) am_last = atomicAdd(counter, 1u) == static_cast<unsigned>(nparts - 1);
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  fold_partials(partials, nparts, 2 * s + MAXT, fold);
-  __syncthreads();
-  double* recB = rec + static_cast<int64_t>(j + 1) * rstride + b_off;
-  for (int q = tid; q < s; q += blockDim.x) {
-    const int64_t k = rows[q];
-    double sn, cs;
-    sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
-    recB[T + q] = (cs * fold[2 * q] - sn * fold[2 * q + 1]) * row_scale[q];
-  }
-  for (int g = tid; g < T; g += blockDim.x) recB[g] = (g <= ngram && g < MAXT) ? fold[2 * s + g] : 0.0;
-  if (tid == 0) *counter = 0u;
-}
-
-template <int NI, bool PAIRED>
-__global__ void __launch_bounds__(kThreads) k_srdct256(const double* __restrict__ x, double xscale, int64_t N, int64_t r0,
-                                                        int M, int64_t L, const uint32_t* __restrict__ sign_bits,
-                                                        const int64_t* __restrict__ rows,
-                                                        const double* __restrict__ row_scale, int s, int64_t ntiles,
-                                                        int csize, double* __restrict__ partials,
-                                                        unsigned* __restrict__ counter, double* __restrict__ fold,
-                                                        double* __restrict__ out) {
-  extern __shared__ double2 sm[];
-  double2* X = sm;                    // [16][257]
-  double2* acc = X + kPairs * kXS;    // [s]
-  double2* zq = acc + s;              // [s] e^{2 i pi k_q / N}  (two columns per pair)
-  double2* ga = zq + s;               // [s] (1 - i e^{i pi k/N}) / 2
-  double2* gb = ga + s;               // [s] (1 + i e^{i pi k/N}) / 2
-  double2* tw = gb + s;               // [256] e^{2 pi i k / 256}
-  int* uq = reinterpret_cast<int*>(tw + 256);
-  const int tid = threadIdx.x;
-  const uint64_t twoN = 2u * static_cast<uint64_t>(N);
-  for (int k = tid; k < 256; k += blockDim.x) {
-    double sn, cs;
-    sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
-    tw[k] = make_double2(cs, sn);
-  }
-  for (int q = tid; q < s; q += blockDim.x) {
-    const int64_t k = rows[q];
-    double sn, cs;
-    sincospi(static_cast<double>(k) / static_cast<double>(N), &sn, &cs);
-    ga[q] = make_double2(0.5 * (1.0 + sn), -0.5 * cs);
-    gb[q] = make_double2(0.5 * (1.0 - sn), 0.5 * cs);
-    sincospi(static_cast<double>((2 * static_cast<uint64_t>(k)) % twoN) / static_cast<double>(N), &sn, &cs);
-    zq[q] = make_double2(cs, sn);
-    uq[q] = static_cast<int>(k & 255);
-    acc[q] = make_double2(0.0, 0.0);
-  }
-  const int p = tid & 15, t = tid >> 4;
-  const int nI = NI ? NI : (M >> 4);  // <= 8 nonzero stage-1 inputs
-  // Raw tile data in registers, fetched one tile ahead: the loads for tile
-  // k+1 are in flight while tile k's accumulation runs.
-  double2 z[8];
-  uint32_t wb0[8], wb1[PAIRED ? 1 : 8];
-  auto issue = [&](int64_t tile) {
-    const int64_t aa = tile * (2 * kPairs) + 2 * p;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      z[i] = make_double2(0.0, 0.0);
-      wb0[i] = 0u;
-      if constexpr (!PAIRED) wb1[i] = 0u;
-      if (tile < ntiles && i < nI && aa < L) {
-        const int64_t jl = aa + L * static_cast<int64_t>(t + 16 * i);
-        const int64_t jg = r0 + jl;
-        if constexpr (PAIRED) {
-          z[i] = __ldcs(reinterpret_cast<const double2*>(x + jl));
-          wb0[i] = __ldg(sign_bits + (jg >> 5));
-        } else {
-          z[i].x = __ldcs(x + jl);
-          z[i].y = aa + 1 < L ? __ldcs(x + jl + 1) : 0.0;
-          wb0[i] = __ldg(sign_bits + (jg >> 5));
-          wb1[i] = __ldg(sign_bits + ((jg + 1) >> 5));
+            for (int k = 1; k < MAXT; ++k)
+              if (k <= ua.ngram) nacc[k] = fma(w0, wv[c][k - 1].x, fma(w1, wv[c][k - 1].y, nacc[k]));
+            const int64_t jg = ta.r0 + jl;
+            v[i0 + c] = make_double2((bits[c] >> (jg & 31)) & 1u ? w0 : -w0, (bits[c] >> ((jg + 1) & 31)) & 1u ? w1 : -w1);
+          }
         }
-      }
-    }
-  };
-  issue(blockIdx.x);
-  __syncthreads();
-
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t a0 = tile * (2 * kPairs);
-    const int64_t aa = a0 + 2 * p;
-    double2 v[16];
+      } else {
+        double2 zv[8];
+        uint32_t b0[8], b1[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      v[i] = make_double2(0.0, 0.0);
-      if (i < 8) {
-        const int64_t jg = r0 + aa + L * static_cast<int64_t>(t + 16 * i);
-        const uint32_t b0 = (wb0[i] >> (jg & 31)) & 1u;
-        uint32_t b1;
-        if constexpr (PAIRED) b1 = (wb0[i] >> ((jg + 1) & 31)) & 1u;
-        else b1 = (wb1[i] >> ((jg + 1) & 31)) & 1u;
-        const double zx = z[i].x * xscale, zy = z[i].y * xscale;
-        v[i] = make_double2(b0 ? zx : -zx, b1 ? zy : -zy);
+        for (int i = 0; i < 8; ++i) {
+          zv[i] = make_double2(0.0, 0.0);
+          b0[i] = b1[i] = 0u;
+          if (i < nI) {
+            const int64_t jl = aa + ta.L * static_cast<int64_t>(t + 16 * i);
+            const int64_t jg = ta.r0 + jl;
+            if constexpr (PAIRED) {
+              zv[i] = __ldcs(reinterpret_cast<const double2*>(x + jl));
+              b0[i] = __ldg(ta.sign_bits + (jg >> 5));
+              b1[i] = b0[i];
+            } else {
+              zv[i].x = __ldcs(x + jl);
+              zv[i].y = aa + 1 < ta.L ? __ldcs(x + jl + 1) : 0.0;
+              b0[i] = __ldg(ta.sign_bits + (jg >> 5));
+              b1[i] = __ldg(ta.sign_bits + ((jg + 1) >> 5));
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int64_t jg = ta.r0 + aa + ta.L * static_cast<int64_t>(t + 16 * i);
+          const double zx = zv[i].x * xscale, zy = zv[i].y * xscale;
+          v[i] = make_double2((b0[i] >> (jg & 31)) & 1u ? zx : -zx, (b1[i] >> ((jg + 1) & 31)) & 1u ? zy : -zy);
+        }
       }
     }
     if constexpr (NI == 8) dft16_half(v);
     else dft16(v);
 #pragma unroll
     for (int vv = 1; vv < 16; ++vv) v[vv] = cmul(v[vv], tw[(vv * t) & 255]);
-    __syncthreads();  // previous tile's accumulation has finished reading X
+    group_sync(g);  // the group's previous Horner pass has finished reading X
 #pragma unroll
     for (int vv = 0; vv < 16; ++vv) X[p * kXS + vv * 16 + t] = v[vv];
-    __syncthreads();
+    group_sync(g);
 #pragma unroll
     for (int tt = 0; tt < 16; ++tt) v[tt] = X[p * kXS + t * 16 + tt];
     dft16(v);
-    __syncthreads();
+    group_sync(g);
 #pragma unroll
     for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
-    issue(tile + gridDim.x);
-    __syncthreads();
-    // accumulate the selected rows: sum_a e^{i pi k (r0+a)/N} T(a, k mod 256).
-    // With the pair unpacking folded into g_alpha / g_beta, a tile contributes
-    //   r0 (g_alpha sum_p z^p C_p[u] + g_beta sum_p z^p conj(C_p[-u])),
-    // z = e^{2 i pi k / N}: two Horner recurrences over the 16 pairs.
-    for (int q = tid; q < s; q += blockDim.x) {
-      const uint64_t k = static_cast<uint64_t>(rows[q]);
+    group_sync(g);
+    // Horner over the tile's 8 pairs, continuing the group's recurrence;
+    // the first step also jumps over the kGroups - 1 tiles in between
+    const bool first = tlow < 0;
+    for (int q = lt; q < s; q += kGThreads) {
       const int u = uq[q], um = (256 - u) & 255;
       const double2 zz = zq[q];
-      double2 S1 = X[(kPairs - 1) * kXS + u];
-      double2 Cm = X[(kPairs - 1) * kXS + um];
-      double2 S2 = make_double2(Cm.x, -Cm.y);
+      double2 S1 = S1s[q], S2 = S2s[q];
+      if (!first) {
+        const double2 jz = zj[q];
+        S1 = cmul(S1, jz);
+        S2 = cmul(S2, jz);
+      }
 #pragma unroll
-      for (int pp = kPairs - 2; pp >= 0; --pp) {
+      for (int pp = kGPairs - 1; pp >= 0; --pp) {
         const double2 C = X[pp * kXS + u];
-        Cm = X[pp * kXS + um];
+        const double2 Cm = X[pp * kXS + um];
         S1 = make_double2(fma(S1.x, zz.x, fma(-S1.y, zz.y, C.x)), fma(S1.x, zz.y, fma(S1.y, zz.x, C.y)));
         S2 = make_double2(fma(S2.x, zz.x, fma(-S2.y, zz.y, Cm.x)), fma(S2.x, zz.y, fma(S2.y, zz.x, -Cm.y)));
       }
+      S1s[q] = S1;
+      S2s[q] = S2;
+    }
+    tlow = tile;
+  }
+  // publish each group's lowest tile, then combine the groups per row:
+  // sum_g e^{i pi k (r0 + 16 tlow_g)/N} (g_alpha S1_g + g_beta S2_g)
+  __shared__ int64_t glow[kGroups];
+  if (lt == 0) glow[g] = tlow;
+  if constexpr (SRC == kSrcUpdate) {
+#pragma unroll
+    for (int k = 0; k < MAXT; ++k) {
+      const double v = warp_sum(nacc[k]);
+      if (lane == 0) nred[k][warp] = v;
+    }
+  }
+  __syncthreads();
+  trace_mark(ta.trace, 2);
+  // CTA-major partials [b][nvp] so that both the writes here and the folds'
+  // reads are coalesced (a value-major layout made every fold load its own
+  // L2 request: a multi-µs tail)
+  const int nv = 2 * s + (SRC == kSrcUpdate ? MAXT : 0);
+  const int nvp = (nv + 1) & ~1;
+  for (int q = tid; q < s; q += kCtaThreads) {
+    const uint64_t k = static_cast<uint64_t>(ta.rows[q]);
+    const double2 ga = ta.tab[q], gb = ta.tab[s + q];
+    double2 acc = make_double2(0.0, 0.0);
+    for (int gg = 0; gg < kGroups; ++gg) {
+      if (glow[gg] < 0) continue;
+      const double2* S = sm + kGroups * (kGPairs * kXS) + gg * 2 * s;
       double sn, cs;
-      const uint64_t ph = (k * static_cast<uint64_t>(r0 + a0)) % twoN;
-      sincospi(static_cast<double>(ph) / static_cast<double>(N), &sn, &cs);
-      const double2 tsum = cadd(cmul(ga[q], S1), cmul(gb[q], S2));
-      acc[q] = cadd(acc[q], cmul(make_double2(cs, sn), tsum));
+      const uint64_t ph = (k * static_cast<uint64_t>(ta.r0 + glow[gg] * 2 * kGPairs)) % twoN;
+      sincospi(static_cast<double>(ph) / static_cast<double>(ta.N), &sn, &cs);
+      acc = cadd(acc, cmul(make_double2(cs, sn), cadd(cmul(ga, S[q]), cmul(gb, S[s + q]))));
+    }
+    *reinterpret_cast<double2*>(ta.partials + static_cast<int64_t>(b) * nvp + 2 * q) = acc;
+  }
+  if constexpr (SRC == kSrcUpdate) {
+    if (tid < MAXT) {
+      double v = 0.0;
+      for (int w = 0; w < kCtaThreads / 32; ++w) v += nred[tid][w];
+      ta.partials[static_cast<int64_t>(b) * nvp + 2 * s + tid] = v;
     }
   }
-  __syncthreads();
-  // cluster reduction of the per-CTA accumulators through distributed shared memory
-  int nparts = gridDim.x, part = blockIdx.x;
-  if (csize > 1) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    cl.sync();
-    const bool leader = cl.block_rank() == 0;
-    if (leader) {
-      for (int q = tid; q < s; q += blockDim.x) {
-        double2 sum = acc[q];
-        for (int r = 1; r < csize; ++r) sum = cadd(sum, cl.map_shared_rank(acc, r)[q]);
-        acc[q] = sum;
-      }
+  trace_mark(ta.trace, 3);
+}
+
+/// Fold of the tile kernels' CTA partials ([G][nvp], CTA-major), one warp per
+/// sketch row (plus one per norm / Gram entry for the update source): lane
+/// sums over CTAs lane, lane+32, ... then a fixed xor-tree — deterministic.
+/// A separate small kernel instead of a last-CTA fold: the in-kernel version
+/// ran serially on one SM with cold code and cost ~10 µs per launch.
+template <int SRC>
+__global__ void __launch_bounds__(256) k_srdct_fold(const double* __restrict__ partials, int G, int nvp, int s,
+                                                     const double2* __restrict__ tab,
+                                                     const double* __restrict__ row_scale, double* __restrict__ out,
+                                                     UpdateArgs ua, int maxt) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q < s) {
+    double re = 0.0, im = 0.0;
+    for (int b = lane; b < G; b += 32) {
+      const double2 v = *reinterpret_cast<const double2*>(partials + static_cast<int64_t>(b) * nvp + 2 * q);
+      re += v.x;
+      im += v.y;
     }
-    cl.sync();
-    if (!leader) return;
-    nparts = gridDim.x / csize;
-    part = blockIdx.x / csize;
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) {
+      const double2 hp = tab[3 * s + q];
+      const double r = (hp.x * re - hp.y * im) * row_scale[q];
+      if constexpr (SRC == kSrcUpdate)
+        ua.rec[static_cast<int64_t>(ua.j + 1) * ua.rstride + (2 * ua.T + 3) + ua.T + q] = r;
+      else
+        out[q] = r;
+    }
+  } else if (SRC == kSrcUpdate && q < s + ua.T) {
+    const int g = q - s;
+    double a = 0.0;
+    if (g <= ua.ngram && g < maxt)
+      for (int b = lane; b < G; b += 32) a += partials[static_cast<int64_t>(b) * nvp + 2 * s + g];
+    a = warp_sum(a);
+    if (lane == 0) ua.rec[static_cast<int64_t>(ua.j + 1) * ua.rstride + (2 * ua.T + 3) + g] = a;
   }
-  for (int q = tid; q < s; q += blockDim.x) {
-    partials[static_cast<int64_t>(2 * q) * nparts + part] = acc[q].x;
-    partials[static_cast<int64_t>(2 * q + 1) * nparts + part] = acc[q].y;
-  }
-  // last-arriving CTA (ticket over nparts) folds in a fixed order
-  __shared__ bool am_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) am_last = atomicAdd(counter, 1u) == static_cast<unsigned>(nparts - 1);
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  fold_partials(partials, nparts, 2 * s, fold);
-  __syncthreads();
-  for (int q = tid; q < s; q += blockDim.x) {
-    const int64_t k = rows[q];
+}
+
+/// Per-row constants of an SRDCT: g_alpha, g_beta, z = e^{2 i pi k/N},
+/// half-phase e^{i pi k/2N}, the group jump z^{8 (kGroups-1)}, k mod 256, and
+/// the 256 stage twiddles.
+__global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int s, double2* __restrict__ tab,
+                               int* __restrict__ uq) {
+  const uint64_t twoN = 2u * static_cast<uint64_t>(N);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < s + 256; q += gridDim.x * blockDim.x) {
     double sn, cs;
-    sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
-    out[q] = (cs * fold[2 * q] - sn * fold[2 * q + 1]) * row_scale[q];
+    if (q < s) {
+      const uint64_t k = static_cast<uint64_t>(rows[q]);
+      sincospi(static_cast<double>(k) / static_cast<double>(N), &sn, &cs);
+      tab[q] = make_double2(0.5 * (1.0 + sn), -0.5 * cs);
+      tab[s + q] = make_double2(0.5 * (1.0 - sn), 0.5 * cs);
+      sincospi(static_cast<double>((2 * k) % twoN) / static_cast<double>(N), &sn, &cs);
+      tab[2 * s + q] = make_double2(cs, sn);
+      sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
+      tab[3 * s + q] = make_double2(cs, sn);
+      // z^{8 (kGroups - 1)} = e^{2 i pi k 8 (kGroups-1) / N}, exact reduction
+      const uint64_t e = (2 * k * static_cast<uint64_t>(kGPairs * (kGroups - 1))) % twoN;
+      sincospi(static_cast<double>(e) / static_cast<double>(N), &sn, &cs);
+      tab[4 * s + q] = make_double2(cs, sn);
+      uq[q] = static_cast<int>(k & 255);
+    } else {
+      const int k = q - s;
+      sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
+      tab[5 * s + k] = make_double2(cs, sn);
+    }
   }
-  if (tid == 0) *counter = 0u;
 }
 
 __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restrict__ x, double xscale, int64_t nloc,
@@ -628,45 +615,92 @@ __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restri
 
 }  // namespace
 
+namespace {
+
+
+size_t tiles_smem(int64_t s) {
+  return sizeof(double2) * static_cast<size_t>(kGroups * (kGPairs * kXS + 2 * s) + 2 * s + 256) +
+         sizeof(int) * static_cast<size_t>(s);
+}
+
+bool tiles_eligible(const SketchDev& S, const SrdctPlan& p) {
+  return p.F == 256 && p.M % 16 == 0 && S.tab.size() > 0 && tiles_smem(S.s) <= 227 * 1024;
+}
+
+template <int SRC, int NI, bool PAIRED, int MAXT>
+void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctPlan& p, int64_t row_begin,
+                  const double* x, double xscale, double* out, const UpdateArgs& ua) {
+  const int64_t ntiles = (p.L + 2 * kGPairs - 1) / (2 * kGPairs);
+  const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((ntiles + kGroups - 1) / kGroups, c.num_sms)));
+  const int64_t nv = (2 * S.s + (SRC == kSrcUpdate ? MAXT : 0) + 1) & ~int64_t{1};
+  TileArgs ta;
+  ta.N = S.n;
+  ta.r0 = row_begin;
+  ta.L = p.L;
+  ta.ntiles = ntiles;
+  ta.M = static_cast<int>(p.M);
+  ta.s = static_cast<int>(S.s);
+  ta.sign_bits = S.sign_bits.get();
+  ta.rows = S.rows.get();
+  ta.row_scale = S.row_scale.get();
+  ta.tab = S.tab.get();
+  ta.uq = S.uq.get();
+  ta.partials = c.partials(nv * G);
+  ta.trace = c.trace(16 * static_cast<int64_t>(G));
+  const size_t smem = tiles_smem(S.s);
+  auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT>;
+  static size_t configured = 0;
+  if (smem > configured) {
+    SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    configured = smem;
+  }
+  {
+    TimedLaunch t(c, name);
+    kern<<<G, kCtaThreads, smem, c.stream>>>(ta, x, xscale, out, ua);
+    SDR_KERNEL_CHECK();
+  }
+  const int nwarps = static_cast<int>(S.s) + (SRC == kSrcUpdate ? ua.T : 0);
+  TimedLaunch t(c, "sketch_fold");
+  k_srdct_fold<SRC><<<(nwarps + 7) / 8, 256, 0, c.stream>>>(ta.partials, G, static_cast<int>(nv), static_cast<int>(S.s),
+                                                           S.tab.get(), S.row_scale.get(), out, ua, MAXT);
+  SDR_KERNEL_CHECK();
+}
+
+}  // namespace
+
+void prepare_srdct_tables(Context& c, SketchDev& S) {
+  S.tab.resize(5 * S.s + 256);
+  S.uq.resize(S.s);
+  k_srdct_tables<<<static_cast<int>((S.s + 256 + 255) / 256), 256, 0, c.stream>>>(S.n, S.rows.get(), static_cast<int>(S.s),
+                                                                                 S.tab.get(), S.uq.get());
+  SDR_KERNEL_CHECK();
+  c.sync();
+}
+
 bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
                           int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec,
                           const double* coef_ready, int64_t row_begin) {
-  constexpr int MAXT = 4;
-  if (S.kind != kSrdct || std::max(nwin, ngram + 1) > MAXT) return false;
+  const int need = std::max(nwin, ngram + 1);
+  if (S.kind != kSrdct || need > 4) return false;
   const SrdctPlan p = plan_srdct(S.n, lay.nloc);
-  if (p.F != 256 || p.M != 128 || p.L % 2 || row_begin % 2 || lay.own_off % 2 || ldv % 2) return false;
-  const int64_t ntiles = (p.L + kTileA - 1) / kTileA;
-  int csize = ntiles >= 16 ? 8 : 1;
-  const int64_t per = (ntiles + 2 * c.num_sms - 1) / (2 * c.num_sms);
-  int grid = static_cast<int>((ntiles + per - 1) / per);
-  if (csize > 1) grid = std::max(csize, (grid + csize - 1) / csize * csize);
-  grid = static_cast<int>(std::min<int64_t>(grid, ntiles));
-  if (csize > 1 && grid % csize) csize = 1;
-  const size_t smem = sizeof(double2) * static_cast<size_t>(kPairs * kXS + 4 * S.s + MAXT + 256) + sizeof(int) * S.s;
-  static size_t configured = 0;
-  if (smem > configured) {
-    SDR_CUDA(cudaFuncSetAttribute(k_update_srdct256<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = smem;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = c.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(csize);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  TimedLaunch t(c, "update_sketch");
-  SDR_CUDA(cudaLaunchKernelEx(&cfg, k_update_srdct256<MAXT>, y, V, ldv, lay.own_off, j, nwin, ngram, rec, RL.stride,
-                              RL.T, cvec, coef_ready, S.n, row_begin, p.L, static_cast<const uint32_t*>(S.sign_bits.get()),
-                              static_cast<const int64_t*>(S.rows.get()), static_cast<const double*>(S.row_scale.get()),
-                              static_cast<int>(S.s), ntiles, csize, c.partials((2 * S.s + MAXT) * grid),
-                              c.counters() + 7, c.partials2(2 * S.s + MAXT)));
+  if (!tiles_eligible(S, p) || p.M != 128 || p.L % 2 || row_begin % 2 || lay.own_off % 2 || ldv % 2) return false;
+  UpdateArgs ua;
+  ua.y = y;
+  ua.V = V;
+  ua.ldv = ldv;
+  ua.own_off = lay.own_off;
+  ua.rstride = RL.stride;
+  ua.j = j;
+  ua.nwin = nwin;
+  ua.ngram = ngram;
+  ua.T = RL.T;
+  ua.rec = rec;
+  ua.cvec = cvec;
+  ua.coef_ready = coef_ready;
+  if (need <= 2)
+    launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua);
+  else
+    launch_tiles<kSrcUpdate, 8, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua);
   return true;
 }
 
@@ -684,40 +718,11 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
   if (S.kind == kSrdct) {
     const SrdctPlan p = plan_srdct(S.n, nloc);
     const int64_t ntiles = (p.L + kTileA - 1) / kTileA;
-    if (p.F == 256 && p.M % 16 == 0) {
-      // fast path: persistent CTAs in clusters of 8, ~2 per SM
-      int csize = ntiles >= 16 ? 8 : 1;
-      // equal tiles per CTA (no tail wave), at most ~2 CTAs per SM
-      const int64_t per = (ntiles + 2 * c.num_sms - 1) / (2 * c.num_sms);
-      int grid = static_cast<int>((ntiles + per - 1) / per);
-      if (csize > 1) grid = std::max(csize, (grid + csize - 1) / csize * csize);
-      grid = static_cast<int>(std::min<int64_t>(grid, ntiles));
-      if (csize > 1 && grid % csize) csize = 1;
-      const size_t smem = sizeof(double2) * static_cast<size_t>(kPairs * kXS + 4 * S.s + 256) + sizeof(int) * S.s;
-      const bool fast = p.M == 128 && p.L % 2 == 0 && row_begin % 2 == 0;
-      auto kern = fast ? k_srdct256<8, true> : k_srdct256<0, false>;
-      static size_t configured[2] = {0, 0};
-      if (smem > configured[fast]) {
-        SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured[fast] = smem;
-      }
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(kThreads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = c.stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = static_cast<unsigned>(csize);
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      TimedLaunch t(c, "sketch");
-      SDR_CUDA(cudaLaunchKernelEx(&cfg, kern, x_own, xscale, S.n, row_begin, static_cast<int>(p.M), p.L,
-                                  static_cast<const uint32_t*>(S.sign_bits.get()), static_cast<const int64_t*>(S.rows.get()),
-                                  static_cast<const double*>(S.row_scale.get()), static_cast<int>(S.s), ntiles, csize,
-                                  c.partials(2 * S.s * grid), c.counters() + 5, c.partials2(2 * S.s), out));
+    if (tiles_eligible(S, p)) {
+      if (p.M == 128 && p.L % 2 == 0 && row_begin % 2 == 0)
+        launch_tiles<kSrcSketch, 8, true, 1>(c, "sketch", S, p, row_begin, x_own, xscale, out, UpdateArgs{});
+      else
+        launch_tiles<kSrcSketch, 0, false, 1>(c, "sketch", S, p, row_begin, x_own, xscale, out, UpdateArgs{});
       return;
     }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * c.num_sms)));

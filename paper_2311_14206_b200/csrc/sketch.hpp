@@ -85,6 +85,8 @@ struct SketchDev {
   DeviceBuffer<std::uint32_t> sign_bits;   // SRDCT
   DeviceBuffer<std::int64_t> rows;         // SRDCT, sorted
   DeviceBuffer<double> row_scale;          // SRDCT: alpha_k * sqrt(n/s)
+  DeviceBuffer<double2> tab;               // SRDCT per-row constants (sketch.cu k_srdct_tables)
+  DeviceBuffer<int> uq;                    // SRDCT k mod 256
   std::vector<std::int64_t> rows_host;
   std::vector<std::uint32_t> sign_bits_host;
 };

@@ -53,11 +53,33 @@ struct Workspace {
   PinnedBuffer<double> hrec, hscal, hcoef;
   PinnedBuffer<const double*> hin;
   PinnedBuffer<double*> hout;
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t ev_init = nullptr;
+  std::vector<cudaEvent_t> ev;   // record j copied to the host (copy stream)
+  std::vector<cudaEvent_t> evk;  // record j complete on the device (compute stream)
+  cudaEvent_t ev_init = nullptr, ev_init_k = nullptr, ev_copies = nullptr;
+  // Record read-back runs on its own stream so the compute stream never waits
+  // for a device-to-host copy between steps (it did: ~9 µs per step).
+  cudaStream_t copy_stream = nullptr;
   ~Workspace() {
     for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : evk) cudaEventDestroy(e);
     if (ev_init) cudaEventDestroy(ev_init);
+    if (ev_init_k) cudaEventDestroy(ev_init_k);
+    if (ev_copies) cudaEventDestroy(ev_copies);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+  }
+  /// D2H copy of n doubles once the compute stream reaches this point; done
+  /// is recorded on the copy stream.
+  void copy_back(Context& c, double* host, const double* dev, i64 n, cudaEvent_t ready, cudaEvent_t done) {
+    SDR_CUDA(cudaEventRecord(ready, c.stream));
+    SDR_CUDA(cudaStreamWaitEvent(copy_stream, ready, 0));
+    SDR_CUDA(cudaMemcpyAsync(host, dev, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, copy_stream));
+    SDR_CUDA(cudaEventRecord(done, copy_stream));
+  }
+  /// The compute stream waits for every copy issued so far (before rec rows
+  /// that a pending copy may still read are rewritten by a new cycle).
+  void fence_copies(Context& c) {
+    SDR_CUDA(cudaEventRecord(ev_copies, copy_stream));
+    SDR_CUDA(cudaStreamWaitEvent(c.stream, ev_copies, 0));
   }
   double* Vcol(int b, i64 i) const { return V[b].get() + i * lay.ld + lay.own_off; }
   double* Vbuf(int b, i64 i) const { return V[b].get() + i * lay.ld; }
@@ -96,11 +118,18 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
     w->cvec.resize(mm + 2);
     w->hrec.ensure((mm + 2) * w->RL.stride);
     while (static_cast<i64>(w->ev.size()) < mm + 2) {
-      cudaEvent_t e;
+      cudaEvent_t e, k;
       SDR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      SDR_CUDA(cudaEventCreateWithFlags(&k, cudaEventDisableTiming));
       w->ev.push_back(e);
+      w->evk.push_back(k);
     }
-    if (!w->ev_init) SDR_CUDA(cudaEventCreateWithFlags(&w->ev_init, cudaEventDisableTiming));
+    if (!w->ev_init) {
+      SDR_CUDA(cudaEventCreateWithFlags(&w->ev_init, cudaEventDisableTiming));
+      SDR_CUDA(cudaEventCreateWithFlags(&w->ev_init_k, cudaEventDisableTiming));
+      SDR_CUDA(cudaEventCreateWithFlags(&w->ev_copies, cudaEventDisableTiming));
+      SDR_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+    }
   }
   const i64 nl = std::max<i64>(lay.nloc, 1);
   w->y.ensure(nl);
@@ -209,11 +238,11 @@ struct ArnoldiPipeline {
   /// w_0 = r0, ||r0||^2 and S r0 on the device; the host reads them in init_finish.
   void init_enqueue(const double* r0) {
     const RecLayout& RL = w.RL;
+    w.fence_copies(c);
     launch_copy_norm(c, r0, w.Vcol(vb, 0), w.lay.nloc, w.rec.get() + RL.b_off());
     launch_sketch(c, S, w.Vcol(vb, 0), w.lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
     c.allreduce_sum(w.rec.get() + RL.b_off(), RL.b_len());
-    SDR_CUDA(cudaMemcpyAsync(w.hrec.get(), w.rec.get(), sizeof(double) * RL.stride, cudaMemcpyDeviceToHost, c.stream));
-    SDR_CUDA(cudaEventRecord(w.ev_init, c.stream));
+    w.copy_back(c, w.hrec.get(), w.rec.get(), RL.stride, w.ev_init_k, w.ev_init);
     issued = 0;
   }
 
@@ -259,8 +288,8 @@ struct ArnoldiPipeline {
       launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
     }
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
-    SDR_CUDA(cudaMemcpyAsync(w.hrec.get() + (j + 1) * R, recj, sizeof(double) * R, cudaMemcpyDeviceToHost, c.stream));
-    SDR_CUDA(cudaEventRecord(w.ev[static_cast<size_t>(j + 1)], c.stream));
+    w.copy_back(c, w.hrec.get() + (j + 1) * R, recj, R, w.evk[static_cast<size_t>(j + 1)],
+                w.ev[static_cast<size_t>(j + 1)]);
   }
 
   /// Keep up to kLookahead speculative steps ahead of step j in flight.

@@ -111,6 +111,7 @@ SketchDev* create_sketch(Context& c, int kind, i64 n, i64 s, std::uint64_t seed,
   SDR_CUDA(cudaMemcpy(S->row_scale.get(), rs.data(), sizeof(double) * rs.size(), cudaMemcpyHostToDevice));
   S->rows_host = std::move(h.rows);
   S->sign_bits_host = std::move(h.sign_bits);
+  prepare_srdct_tables(c, *S);
   return S.release();
 }
 

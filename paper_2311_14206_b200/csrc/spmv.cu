@@ -1,19 +1,23 @@
 // K1 / K6: SELL-32 SpMV with fused epilogues (sm_100a).
 //
 // Replaces SparseMatrix::apply (sparse.hpp:84-98) and the first half of
-// arnoldi_step (arnoldi.hpp:87-97): one warp owns a 32-row slice, every k
-// step of the slice loads 32 int32 column indices (128 B) and 32 fp64 values
-// (256 B) fully coalesced; x is gathered through the read-only path (the
-// whole vector stays L2-resident up to ~60 M rows, so HBM reads x once).
-// The slice loop is software-pipelined: the next slice's column indices are
-// in flight while the current slice's values and x gathers are consumed.
+// arnoldi_step (arnoldi.hpp:87-97). One warp owns a 32-row slice; every k
+// step of the slice loads 32 fp64 values (256 B) fully coalesced.
+// Two storage forms (operator.cu chooses per matrix):
+//   SELL      32 int32 column indices per k step; x gathered through them.
+//   SELL-DIA  when every slice's entries lie on <= 16 distinct diagonals
+//             (banded / stencil operators; gaps stored as explicit zeros),
+//             D diagonals per slice (padded to the operator's maximum), one
+//             int32 offset per (slice, k): 8 instead of 12 bytes per entry,
+//             and x[row + off] is a coalesced load that does not wait on an
+//             index load (offsets are fetched a slice ahead, one per lane,
+//             and broadcast with shuffles).
+// Row sums run in CSR (increasing column) order like the reference.
 // Epilogue variants fuse the reductions the step needs into the same pass:
 //   MODE 0  y = A x
 //   MODE 1  y = A w_j, plus ||y||^2 and y.w_{j-d} for the MGS window (K1);
 //           on one GPU the last CTA also forms the MGS coefficients (mgs.cuh)
 //   MODE 2  r = b - A x, plus ||r||^2                (verification, K6)
-// Algorithmic bytes per row: 12 B per stored entry + 8 B x + 8 B y (+8 B
-// per extra window vector in MODE 1, +8 B b in MODE 2).
 #include "kernels.hpp"
 #include "mgs.cuh"
 #include "reduce.cuh"
@@ -35,13 +39,80 @@ struct MgsArgs {
   double* coef = nullptr;  // null: coefficients are formed later (after an allreduce)
 };
 
-template <int MODE, int NV, bool PIPE>
-__global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : (PIPE ? 2 : 3)) k_sell_spmv(SellView A, const double* __restrict__ x_ext,
-                                                         double* __restrict__ y, const double* __restrict__ aux,
-                                                         int64_t ldv, int64_t own_off, int64_t halo_lo, int j,
-                                                         int nwin, double* __restrict__ partials,
-                                                         unsigned* __restrict__ counter, double* __restrict__ out,
-                                                         MgsArgs mg) {
+/// Row sums of one 32-row slice (lane = row), CSR order.
+/// FMT 0: SELL (column index per entry); FMT > 0: SELL-DIA with FMT
+/// diagonals (compile-time, loop fully unrolled so every load of the slice
+/// is in flight at once); FMT < 0: SELL-DIA with A.dia_d diagonals.
+template <int FMT>
+__device__ __forceinline__ double slice_row_sum(const SellView& A, const double* __restrict__ x_ext, int64_t sl,
+                                                int64_t row, int64_t halo_lo, int lane, int cur_off) {
+  double s = 0.0;
+  if constexpr (FMT > 0) {
+    const double* vp = A.vals + sl * kSlice * FMT + lane;
+    const int64_t rx = halo_lo + row;
+    double v[FMT], xv[FMT];
+#pragma unroll
+    for (int k = 0; k < FMT; ++k) {
+      const int o = __shfl_sync(0xffffffffu, cur_off, k);
+      int64_t cidx = rx + o;
+      cidx = cidx < 0 ? 0 : (cidx >= A.ext_len ? A.ext_len - 1 : cidx);
+      v[k] = __ldcs(vp + k * kSlice);
+      xv[k] = __ldg(x_ext + cidx);
+    }
+#pragma unroll
+    for (int k = 0; k < FMT; ++k) s = fma(v[k], xv[k], s);
+  } else if constexpr (FMT < 0) {
+    const int len = A.dia_d;
+    const double* vp = A.vals + sl * kSlice * len + lane;
+    const int64_t rx = halo_lo + row;
+    for (int k0 = 0; k0 < len; k0 += kBatch) {
+      double v[kBatch], xv[kBatch];
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        const bool ok = k0 + k < len;
+        const int o = __shfl_sync(0xffffffffu, cur_off, (k0 + k) & 31);
+        int64_t cidx = rx + o;
+        cidx = cidx < 0 ? 0 : (cidx >= A.ext_len ? A.ext_len - 1 : cidx);
+        v[k] = ok ? __ldcs(vp + (k0 + k) * kSlice) : 0.0;
+        xv[k] = ok ? __ldg(x_ext + cidx) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k)
+        if (k0 + k < len) s = fma(v[k], xv[k], s);
+    }
+  } else {
+    const int64_t p0 = A.slice_ptr[sl];
+    const int len = static_cast<int>((A.slice_ptr[sl + 1] - p0) >> 5);
+    const double* vp = A.vals + p0 + lane;
+    const int32_t* cp = A.cols + p0 + lane;
+    // all index/value loads of a batch are issued before the dependent gathers
+    for (int k0 = 0; k0 < len; k0 += kBatch) {
+      int32_t c[kBatch];
+      double v[kBatch], xv[kBatch];
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        const bool ok = k0 + k < len;
+        c[k] = ok ? __ldcs(cp + (k0 + k) * kSlice) : 0;
+        v[k] = ok ? __ldcs(vp + (k0 + k) * kSlice) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) xv[k] = k0 + k < len ? __ldg(x_ext + c[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k)
+        if (k0 + k < len) s = fma(v[k], xv[k], s);
+    }
+  }
+  return s;
+}
+
+template <int MODE, int NV, int FMT>
+__global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView A, const double* __restrict__ x_ext,
+                                                                         double* __restrict__ y,
+                                                                         const double* __restrict__ aux, int64_t ldv,
+                                                                         int64_t own_off, int64_t halo_lo, int j,
+                                                                         int nwin, double* __restrict__ partials,
+                                                                         unsigned* __restrict__ counter,
+                                                                         double* __restrict__ out, MgsArgs mg) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -49,24 +120,14 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : (PIPE ? 2 : 3)) k_sell_
 #pragma unroll
   for (int k = 0; k < NV; ++k) acc[k] = 0.0;
 
-  auto fetch_idx = [&](int64_t sl, int32_t (&cc)[kBatch], int& ll, int64_t& pp) {
-    ll = 0;
-    pp = 0;
-    if (sl < A.nslices) {
-      pp = A.slice_ptr[sl];
-      ll = static_cast<int>((A.slice_ptr[sl + 1] - pp) >> 5);
-    }
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k) cc[k] = k < ll ? __ldcs(A.cols + pp + k * kSlice + lane) : 0;
-  };
-
-  int64_t sl = gw;
-  int32_t c[kBatch];
-  int len;
-  int64_t p0;
-  if constexpr (PIPE) fetch_idx(sl, c, len, p0);
-  while (sl < A.nslices) {
-    if constexpr (!PIPE) fetch_idx(sl, c, len, p0);
+  // DIA: the next slice's diagonal offsets (one per lane) are fetched an
+  // iteration ahead, so no load of the current slice waits on an index load
+  const int D = FMT > 0 ? FMT : (FMT < 0 ? A.dia_d : 0);
+  int nx_off = 0;
+  if (FMT != 0 && gw < A.nslices && lane < D) nx_off = __ldg(A.doff + gw * D + lane);
+  for (int64_t sl = gw; sl < A.nslices; sl += nwarps) {
+    const int cur_off = nx_off;
+    if (FMT != 0 && sl + nwarps < A.nslices && lane < D) nx_off = __ldg(A.doff + (sl + nwarps) * D + lane);
     const int64_t row = sl * kSlice + lane;
     const bool live = row < A.nrows;
     // epilogue operands are independent of the product: fetch them first
@@ -78,36 +139,7 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : (PIPE ? 2 : 3)) k_sell_
     } else if constexpr (MODE == 2) {
       e0 = live ? __ldcs(aux + row) : 0.0;
     }
-    double v[kBatch], xv[kBatch];
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k) {
-      v[k] = k < len ? __ldcs(A.vals + p0 + k * kSlice + lane) : 0.0;
-      xv[k] = k < len ? __ldg(x_ext + c[k]) : 0.0;
-    }
-    const int64_t sn = sl + nwarps;
-    int32_t cn[kBatch];
-    int lenn = 0;
-    int64_t p0n = 0;
-    if constexpr (PIPE) fetch_idx(sn, cn, lenn, p0n);
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k)
-      if (k < len) s = fma(v[k], xv[k], s);
-    for (int k0 = kBatch; k0 < len; k0 += kBatch) {  // rows longer than one batch
-      int32_t c2[kBatch];
-      double v2[kBatch], x2[kBatch];
-#pragma unroll
-      for (int k = 0; k < kBatch; ++k) {
-        const bool ok = k0 + k < len;
-        c2[k] = ok ? __ldcs(A.cols + p0 + (k0 + k) * kSlice + lane) : 0;
-        v2[k] = ok ? __ldcs(A.vals + p0 + (k0 + k) * kSlice + lane) : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < kBatch; ++k) x2[k] = k0 + k < len ? __ldg(x_ext + c2[k]) : 0.0;
-#pragma unroll
-      for (int k = 0; k < kBatch; ++k)
-        if (k0 + k < len) s = fma(v2[k], x2[k], s);
-    }
+    const double s = slice_row_sum<FMT>(A, x_ext, sl, row, halo_lo, lane, cur_off);
     if (live) {
       if constexpr (MODE == 0) {
         y[row] = s;
@@ -123,13 +155,6 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : (PIPE ? 2 : 3)) k_sell_
         y[row] = r;
         acc[0] = fma(r, r, acc[0]);
       }
-    }
-    sl = sn;
-    if constexpr (PIPE) {
-      len = lenn;
-      p0 = p0n;
-#pragma unroll
-      for (int k = 0; k < kBatch; ++k) c[k] = cn[k];
     }
   }
   if constexpr (MODE != 0) {
@@ -148,133 +173,6 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : (PIPE ? 2 : 3)) k_sell_
   }
 }
 
-// ------------------------------------------------- K1 with bulk-copy staging
-// Groups of kGroup slices (kGroup warps, one slice each). A single thread
-// streams each group's SELL values and column indices into a kStages-deep
-// shared-memory ring with cp.async.bulk (SASS UBLKCP, the TMA engine's 1-D
-// path) completing on an mbarrier; warps wait on the stage's barrier, gather
-// x through L1/L2, and release the stage at a CTA barrier. Matrix bytes — 85%
-// of K1's traffic — thereby stream with no register cost and a deep queue.
-constexpr int kGroup = kThreads / 32;
-constexpr int kStages = 3;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-template <int NV>
-__global__ void __launch_bounds__(kThreads) k_sell_spmv_bulk(SellView A, const double* __restrict__ x_ext,
-                                                              double* __restrict__ y, const double* __restrict__ V,
-                                                              int64_t ldv, int64_t own_off, int64_t halo_lo, int j,
-                                                              int nwin, int64_t stage_entries,
-                                                              double* __restrict__ partials,
-                                                              unsigned* __restrict__ counter, double* __restrict__ out,
-                                                              MgsArgs mg) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sval = reinterpret_cast<double*>(smem_raw);                       // [kStages][stage_entries]
-  int32_t* scol = reinterpret_cast<int32_t*>(sval + kStages * stage_entries);  // [kStages][stage_entries]
-  __shared__ __align__(8) uint64_t full[kStages];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t ngroups = (A.nslices + kGroup - 1) / kGroup;
-  const int64_t per = (ngroups + gridDim.x - 1) / gridDim.x;
-  const int64_t g0 = blockIdx.x * per, g1 = min(ngroups, g0 + per);
-  auto issue = [&](int64_t g) {
-    const int st = static_cast<int>((g - g0) % kStages);
-    const int64_t s0 = g * kGroup, s1 = min(A.nslices, s0 + kGroup);
-    const int64_t e0 = A.slice_ptr[s0], e1 = A.slice_ptr[s1];
-    const unsigned ne = static_cast<unsigned>(e1 - e0);
-    mbar_arrive_tx(&full[st], ne * 12u);
-    bulk_g2s(sval + st * stage_entries, A.vals + e0, ne * 8u, &full[st]);
-    bulk_g2s(scol + st * stage_entries, A.cols + e0, ne * 4u, &full[st]);
-  };
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int64_t g = g0; g < min(g1, g0 + kStages); ++g) issue(g);
-  double acc[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (int64_t g = g0; g < g1; ++g) {
-    const int st = static_cast<int>((g - g0) % kStages);
-    const unsigned parity = static_cast<unsigned>(((g - g0) / kStages) & 1);
-    const int64_t sl = g * kGroup + warp;
-    const int64_t row = sl * kSlice + lane;
-    const bool live = sl < A.nslices && row < A.nrows;
-    // operands independent of the staged matrix data first
-    double e0 = 0.0, ew[NV > 2 ? NV - 2 : 1];
-    if (live) {
-      e0 = x_ext[halo_lo + row];
-#pragma unroll
-      for (int d = 1; d < NV - 1; ++d) ew[d - 1] = d < nwin ? __ldcs(V + (j - d) * ldv + own_off + row) : 0.0;
-    }
-    int64_t base = 0;
-    int len = 0;
-    if (sl < A.nslices) {
-      const int64_t gbase = A.slice_ptr[g * kGroup];
-      const int64_t p0 = A.slice_ptr[sl];
-      base = p0 - gbase;
-      len = static_cast<int>((A.slice_ptr[sl + 1] - p0) >> 5);
-    }
-    mbar_wait(&full[st], parity);
-    const double* sv = sval + st * stage_entries + base + lane;
-    const int32_t* sc = scol + st * stage_entries + base + lane;
-    double s = 0.0;
-    for (int k0 = 0; k0 < len; k0 += kBatch) {
-      double xv[kBatch], vv[kBatch];
-#pragma unroll
-      for (int k = 0; k < kBatch; ++k) {
-        const bool ok = k0 + k < len;
-        xv[k] = ok ? __ldg(x_ext + sc[(k0 + k) * kSlice]) : 0.0;
-        vv[k] = ok ? sv[(k0 + k) * kSlice] : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < kBatch; ++k)
-        if (k0 + k < len) s = fma(vv[k], xv[k], s);
-    }
-    if (live) {
-      y[row] = s;
-      acc[0] = fma(s, s, acc[0]);
-      acc[1] = fma(s, e0, acc[1]);
-#pragma unroll
-      for (int d = 1; d < NV - 1; ++d)
-        if (d < nwin) acc[1 + d] = fma(s, ew[d - 1], acc[1 + d]);
-    }
-    __syncthreads();  // stage st fully consumed
-    if (threadIdx.x == 0 && g + kStages < g1) issue(g + kStages);
-  }
-  block_partials<NV>(acc, 1 + nwin, partials);
-  if (last_block_done(counter)) {
-    fold_partials(partials, gridDim.x, 1 + nwin, out);
-    if (mg.coef) {
-      __syncthreads();
-      if (threadIdx.x == 0) mgs_coefficients<NV - 1>(mg.rec, mg.rstride, mg.T, j, nwin, mg.cvec, mg.coef, true);
-    }
-    if (threadIdx.x == 0) *counter = 0u;
-  }
-}
-
 template <class K>
 int resident_grid(const Context& c, K kernel, int64_t want_blocks) {
   const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), kThreads, 0);
@@ -283,93 +181,59 @@ int resident_grid(const Context& c, K kernel, int64_t want_blocks) {
 
 int64_t blocks_for(int64_t nslices) { return (nslices + (kThreads / 32) - 1) / (kThreads / 32); }
 
-/// SDR_K1_PIPE=1 selects the software-pipelined slice loop (fewer resident
-/// warps, more bytes in flight per warp); default is the 4-CTA/SM variant.
-bool use_pipe() {
-  static const int v = [] {
-    const char* e = std::getenv("SDR_K1_PIPE");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v != 0;
+template <int MODE, int NV, int FMT>
+void launch_impl(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
+                 int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
+                 const MgsArgs& mg) {
+  auto kern = k_sell_spmv<MODE, NV, FMT>;
+  const int g = resident_grid(c, kern, blocks_for(A.nslices));
+  TimedLaunch t(c, name);
+  kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin,
+                                     MODE ? c.partials(static_cast<int64_t>(NV) * g) : nullptr, counter, out, mg);
+  SDR_KERNEL_CHECK();
 }
 
-template <int NV, bool PIPE>
-void spmv_arnoldi_impl(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
-                       int nwin, double* y, double* recA, const MgsArgs& mg) {
-  const int g = resident_grid(c, k_sell_spmv<1, NV, PIPE>, blocks_for(A.nslices));
-  const double* x_ext = V + j * ldv + lay.ext_shift();
-  TimedLaunch t(c, "spmv_arnoldi");
-  k_sell_spmv<1, NV, PIPE><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin,
-                                                         c.partials(static_cast<int64_t>(NV) * g), c.counters() + 0,
-                                                         recA, mg);
-  SDR_KERNEL_CHECK();
+template <int MODE, int NV>
+void launch_fmt(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
+                int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
+                const MgsArgs& mg) {
+#define SDR_SPMV_FMT(F) launch_impl<MODE, NV, F>(c, name, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, counter, out, mg)
+  if (!A.doff)
+    SDR_SPMV_FMT(0);
+  else if (A.dia_d == 7)  // 3-D 7-point stencils
+    SDR_SPMV_FMT(7);
+  else if (A.dia_d == 5)  // 2-D 5-point stencils
+    SDR_SPMV_FMT(5);
+  else
+    SDR_SPMV_FMT(-1);
+#undef SDR_SPMV_FMT
 }
 
 }  // namespace
 
 void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) {
   if (A.nrows == 0) return;
-  const int g = resident_grid(c, k_sell_spmv<0, 1, false>, blocks_for(A.nslices));
-  TimedLaunch t(c, "spmv");
-  k_sell_spmv<0, 1, false><<<g, kThreads, 0, c.stream>>>(A, x_ext, y, nullptr, 0, 0, 0, 0, 0, nullptr, nullptr,
-                                                         nullptr, MgsArgs{});
-  SDR_KERNEL_CHECK();
+  launch_fmt<0, 1>(c, "spmv", A, x_ext, y, nullptr, 0, 0, A.halo_lo, 0, 0, nullptr, nullptr, MgsArgs{});
 }
 
 void launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                          int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
                          double* coef) {
   const MgsArgs mg{rec, rstride, T, cvec, coef};
-  // bulk-staged variant when a group's stage fits comfortably in shared memory
-  static const bool bulk_on = [] {
-    const char* e = std::getenv("SDR_K1_BULK");
-    return !e || std::atoi(e) != 0;
-  }();
-  const int64_t stage = round_up(std::max<int64_t>(A.max_group, 32), 32);
-  const size_t smem = static_cast<size_t>(kStages) * static_cast<size_t>(stage) * 12;
-  if (bulk_on && nwin <= 7 && A.nslices > 0 && smem <= 150 * 1024) {
-    auto launch = [&](auto kern, int nv) {
-      static size_t configured[2] = {0, 0};
-      size_t& cfgd = configured[nv > 4];
-      if (smem > cfgd) {
-        SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        cfgd = smem;
-      }
-      const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kThreads, smem);
-      const int64_t ngroups = (A.nslices + kGroup - 1) / kGroup;
-      const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ngroups, static_cast<int64_t>(c.num_sms) * per_sm)));
-      const double* x_ext = V + j * ldv + lay.ext_shift();
-      TimedLaunch t(c, "spmv_arnoldi");
-      kern<<<g, kThreads, smem, c.stream>>>(A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, stage,
-                                            c.partials(static_cast<int64_t>(nv) * g), c.counters() + 0, recA, mg);
-      SDR_KERNEL_CHECK();
-    };
-    if (nwin <= 3)
-      launch(k_sell_spmv_bulk<4>, 4);
-    else
-      launch(k_sell_spmv_bulk<8>, 8);
-    return;
-  }
-  if (nwin <= 3) {
-    if (use_pipe())
-      spmv_arnoldi_impl<4, true>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
-    else
-      spmv_arnoldi_impl<4, false>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
-  } else if (nwin <= 7) {
-    spmv_arnoldi_impl<8, false>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
-  } else if (nwin <= 33) {
-    spmv_arnoldi_impl<34, false>(c, A, V, ldv, lay, j, nwin, y, recA, mg);
-  } else {
+  const double* x_ext = V + j * ldv + lay.ext_shift();
+  if (nwin <= 3)
+    launch_fmt<1, 4>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0, recA, mg);
+  else if (nwin <= 7)
+    launch_fmt<1, 8>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0, recA, mg);
+  else if (nwin <= 33)
+    launch_fmt<1, 34>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0, recA,
+                      mg);
+  else
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
-  }
 }
 
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2) {
-  const int g = resident_grid(c, k_sell_spmv<2, 1, false>, blocks_for(A.nslices));
-  TimedLaunch t(c, "residual");
-  k_sell_spmv<2, 1, false><<<g, kThreads, 0, c.stream>>>(A, x_ext, r, b, 0, 0, 0, 0, 0, c.partials(g),
-                                                         c.counters() + 1, norm2, MgsArgs{});
-  SDR_KERNEL_CHECK();
+  launch_fmt<2, 1>(c, "residual", A, x_ext, r, b, 0, 0, A.halo_lo, 0, 0, c.counters() + 1, norm2, MgsArgs{});
 }
 
 }  // namespace sdr
