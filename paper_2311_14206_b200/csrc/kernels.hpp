@@ -56,10 +56,13 @@ int blocks_per_sm(const void* kernel, int threads, size_t smem);
 // ---- SpMV family (spmv.cu)
 void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y);
 /// K1. When coef != nullptr (single GPU) the last CTA also forms the MGS
-/// coefficients of step j into coef[0..nwin] and the record's H part.
-void launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
-                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
-                         double* coef);
+/// coefficients of step j into coef[0..nwin] and the record's H part. With
+/// partials_out (deferred step pipeline) the CTAs only leave their window
+/// dots there, value-major [1 + nwin][grid], and nothing is folded; the
+/// return value is the grid size.
+int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
+                        int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
+                        double* coef, double* partials_out = nullptr);
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2);
 
 // ---- Arnoldi update (arnoldi.cu). coef_ready: coefficients already formed
@@ -80,11 +83,30 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
                           int64_t row_begin, double* out);
 /// Builds SketchDev::tab / uq (per-row SRDCT constants) once per sketch.
 void prepare_srdct_tables(Context& c, SketchDev& S);
+/// Deferred folds of the one-GPU step pipeline: K1(j) leaves its window dots
+/// as CTA partials; the fused update K2(j) folds them, together with
+/// K2(j-1)'s norm / Gram / sketch partials (record row j), in its prologue,
+/// forms the MGS coefficients there and leaves its own partials for K2(j+1).
+/// No kernel of a step ends in a serial last-CTA fold.
+struct StepFold {
+  const double* k1_partials = nullptr;
+  int k1_G = 0;
+  const double* prev_partials = nullptr;  // null at j = 0 (row 0 comes from the cycle init)
+  int prev_G = 0, prev_nvp = 0, prev_ngram = 0;
+  double* out_partials = nullptr;  // this update's partials (update_sketch_partials_size doubles)
+  int out_G = 0, out_nvp = 0;      // set by the launch
+};
+bool update_sketch_eligible(const SketchDev& S, const VecLayout& lay, int need, int64_t row_begin, int64_t ldv);
+int64_t update_sketch_partials_size(const SketchDev& S, int num_sms);
 /// Fused K2 + K3a (update pass and SRDCT of w_{j+1} in one sweep), writing
-/// the record's B part (norm, Gram, sketch). Returns false when the
-/// configuration is not eligible (caller runs K2 and K3 separately).
+/// the record's B part (norm, Gram, sketch) — through a fold kernel, or, with
+/// sf (deferred pipeline), left as partials for the next step. Returns false
+/// when the configuration is not eligible (caller runs K2 and K3 separately).
 bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
                           int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec,
-                          const double* coef_ready, int64_t row_begin);
+                          const double* coef_ready, int64_t row_begin, StepFold* sf = nullptr);
+/// Folds the partials a deferred K2(j) left (sf.out_*) into record row j+1.
+void launch_update_sketch_flush(Context& c, const SketchDev& S, const StepFold& sf, double* rec, const RecLayout& RL,
+                                int j, int ngram);
 
 }  // namespace sdr

@@ -16,12 +16,20 @@
 
 namespace sdr {
 
+/// recA_in: the step's A values (||y||^2, y.w_{j-d}); null = record row j+1.
+/// curB_in: column j's B values (||w_j||^2, w_j.w_{j-g}); null = record row j.
+/// Both are given when the caller folded them itself (the deferred path, in
+/// which the rows are written by CTA 0 of the same launch).
 template <int MAXT>
 __device__ __forceinline__ void mgs_coefficients(double* __restrict__ rec, int64_t rstride, int T, int j, int nwin,
-                                                 double* __restrict__ cvec, double* __restrict__ coef, bool write_rec) {
+                                                 double* __restrict__ cvec, double* __restrict__ coef, bool write_rec,
+                                                 const double* recA_in = nullptr, const double* curB_in = nullptr) {
   const int b_off = 2 * T + 3;
-  const double* recA = rec + static_cast<int64_t>(j + 1) * rstride;
-  const double wn2 = rec[static_cast<int64_t>(j) * rstride + b_off];
+  const double* recA = recA_in ? recA_in : rec + static_cast<int64_t>(j + 1) * rstride;
+  auto colB = [&](int i, int g) {  // B entry g of column i (g = 0: norm, g >= 1: Gram with column i - g)
+    return (i == j && curB_in) ? curB_in[g] : rec[static_cast<int64_t>(i) * rstride + b_off + g];
+  };
+  const double wn2 = colB(j, 0);
   const double cj = 1.0 / sqrt(wn2);
   double ci[MAXT], h[MAXT];
 #pragma unroll
@@ -38,7 +46,7 @@ __device__ __forceinline__ void mgs_coefficients(double* __restrict__ rec, int64
 #pragma unroll
       for (int d2 = MAXT - 1; d2 > d; --d2) {
         if (d2 < nwin) {
-          const double gram = rec[static_cast<int64_t>(i) * rstride + b_off + (d2 - d)];
+          const double gram = colB(i, d2 - d);
           acc -= h[d2] * (ci[d2] * ci[d] * gram);
         }
       }

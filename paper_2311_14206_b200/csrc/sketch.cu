@@ -286,7 +286,32 @@ struct UpdateArgs {
   double* rec = nullptr;
   double* cvec = nullptr;
   const double* coef_ready = nullptr;
+  // deferred folds (one GPU): K1's value-major
+  // partials [1 + nwin][k1_G] and the previous update's CTA-major partials
+  // [prev_G][prev_nvp] are folded in this kernel's prologue
+  const double* k1_partials = nullptr;
+  const double* prev_partials = nullptr;
+  int k1_G = 0, prev_G = 0, prev_nvp = 0, prev_ngram = 0;
 };
+
+/// Sketch row q from CTA-major tile partials [G][nvp]: lane-strided sums over
+/// CTAs, a fixed xor tree, then Re(e^{i pi k/2N} Z) scaled — deterministic.
+__device__ __forceinline__ void sketch_row_fold(const double* __restrict__ partials, int G, int nvp, int q, int lane,
+                                                int s, const double2* __restrict__ tab,
+                                                const double* __restrict__ row_scale, double* __restrict__ dst) {
+  double re = 0.0, im = 0.0;
+  for (int b = lane; b < G; b += 32) {
+    const double2 v = *reinterpret_cast<const double2*>(partials + static_cast<int64_t>(b) * nvp + 2 * q);
+    re += v.x;
+    im += v.y;
+  }
+  re = warp_sum(re);
+  im = warp_sum(im);
+  if (lane == 0) {
+    const double2 hp = tab[3 * s + q];
+    dst[q] = (hp.x * re - hp.y * im) * row_scale[q];
+  }
+}
 
 // Tile-group layout: a CTA of kGroups x 128 threads per SM. Each group of
 // four warps owns its own tiles (8 column pairs x 128 rows), transpose
@@ -329,7 +354,60 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
   }
   for (int q = tid; q < kGroups * 2 * s; q += kCtaThreads) S1s[q - g * 2 * s] = make_double2(0.0, 0.0);
   if constexpr (SRC == kSrcUpdate) {
-    if (ua.coef_ready) {
+    if (ua.k1_partials) {
+      // deferred: fold K1's window dots and the previous update's norm / Gram
+      // here (every CTA, same fixed order), the previous sketch rows once
+      // (one warp per row), then the MGS coefficients
+      __shared__ double red[2 * MAXT + 1][kCtaThreads / 32];
+      __shared__ double sA[MAXT + 1], sB[MAXT];
+      const int nA = 1 + ua.nwin;
+      const bool prev = ua.prev_partials != nullptr;
+      double a[MAXT + 1], bs[MAXT];
+#pragma unroll
+      for (int v = 0; v <= MAXT; ++v) a[v] = 0.0;
+#pragma unroll
+      for (int v = 0; v < MAXT; ++v) bs[v] = 0.0;
+      for (int bb = tid; bb < ua.k1_G; bb += kCtaThreads)
+#pragma unroll
+        for (int v = 0; v <= MAXT; ++v)
+          if (v < nA) a[v] += __ldcg(ua.k1_partials + static_cast<int64_t>(v) * ua.k1_G + bb);
+      if (prev)
+        for (int bb = tid; bb < ua.prev_G; bb += kCtaThreads)
+#pragma unroll
+          for (int v = 0; v < MAXT; ++v) bs[v] += __ldcg(ua.prev_partials + static_cast<int64_t>(bb) * ua.prev_nvp + 2 * s + v);
+#pragma unroll
+      for (int v = 0; v <= MAXT; ++v) {
+        const double r = warp_sum(a[v]);
+        if (lane == 0) red[v][warp] = r;
+      }
+#pragma unroll
+      for (int v = 0; v < MAXT; ++v) {
+        const double r = warp_sum(bs[v]);
+        if (lane == 0) red[MAXT + 1 + v][warp] = r;
+      }
+      const int64_t R = ua.rstride;
+      double* recj = ua.rec + static_cast<int64_t>(ua.j) * R + (2 * ua.T + 3);  // column j's B part
+      if (prev)
+        for (int q = b * (kCtaThreads / 32) + warp; q < s; q += G * (kCtaThreads / 32))
+          sketch_row_fold(ua.prev_partials, ua.prev_G, ua.prev_nvp, q, lane, s, ta.tab, ta.row_scale, recj + ua.T);
+      __syncthreads();
+      if (tid < 2 * MAXT + 1) {
+        double r = 0.0;
+        for (int w = 0; w < kCtaThreads / 32; ++w) r += red[tid][w];
+        if (tid <= MAXT) sA[tid] = r;
+        else sB[tid - MAXT - 1] = (tid - MAXT - 1 <= ua.prev_ngram) ? r : 0.0;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        mgs_coefficients<MAXT>(ua.rec, R, ua.T, ua.j, ua.nwin, ua.cvec, coef, b == 0, sA, prev ? sB : nullptr);
+        if (b == 0) {
+          double* recA = ua.rec + static_cast<int64_t>(ua.j + 1) * R;
+          for (int v = 0; v < nA; ++v) recA[v] = sA[v];
+          if (prev)
+            for (int g2 = 0; g2 < ua.T; ++g2) recj[g2] = g2 < MAXT ? sB[g2] : 0.0;
+        }
+      }
+    } else if (ua.coef_ready) {
       if (tid <= MAXT) coef[tid] = tid <= ua.nwin ? ua.coef_ready[tid] : 0.0;
     } else if (tid == 0) {
       mgs_coefficients<MAXT>(ua.rec, ua.rstride, ua.T, ua.j, ua.nwin, ua.cvec, coef, b == 0);
@@ -522,22 +600,9 @@ __global__ void __launch_bounds__(256) k_srdct_fold(const double* __restrict__ p
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q < s) {
-    double re = 0.0, im = 0.0;
-    for (int b = lane; b < G; b += 32) {
-      const double2 v = *reinterpret_cast<const double2*>(partials + static_cast<int64_t>(b) * nvp + 2 * q);
-      re += v.x;
-      im += v.y;
-    }
-    re = warp_sum(re);
-    im = warp_sum(im);
-    if (lane == 0) {
-      const double2 hp = tab[3 * s + q];
-      const double r = (hp.x * re - hp.y * im) * row_scale[q];
-      if constexpr (SRC == kSrcUpdate)
-        ua.rec[static_cast<int64_t>(ua.j + 1) * ua.rstride + (2 * ua.T + 3) + ua.T + q] = r;
-      else
-        out[q] = r;
-    }
+    double* dst = out;
+    if constexpr (SRC == kSrcUpdate) dst = ua.rec + static_cast<int64_t>(ua.j + 1) * ua.rstride + (2 * ua.T + 3) + ua.T;
+    sketch_row_fold(partials, G, nvp, q, lane, s, tab, row_scale, dst);
   } else if (SRC == kSrcUpdate && q < s + ua.T) {
     const int g = q - s;
     double a = 0.0;
@@ -629,7 +694,7 @@ bool tiles_eligible(const SketchDev& S, const SrdctPlan& p) {
 
 template <int SRC, int NI, bool PAIRED, int MAXT>
 void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctPlan& p, int64_t row_begin,
-                  const double* x, double xscale, double* out, const UpdateArgs& ua) {
+                  const double* x, double xscale, double* out, const UpdateArgs& ua, StepFold* sf = nullptr) {
   const int64_t ntiles = (p.L + 2 * kGPairs - 1) / (2 * kGPairs);
   const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((ntiles + kGroups - 1) / kGroups, c.num_sms)));
   const int64_t nv = (2 * S.s + (SRC == kSrcUpdate ? MAXT : 0) + 1) & ~int64_t{1};
@@ -645,7 +710,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   ta.row_scale = S.row_scale.get();
   ta.tab = S.tab.get();
   ta.uq = S.uq.get();
-  ta.partials = c.partials(nv * G);
+  ta.partials = sf ? sf->out_partials : c.partials(nv * G);
   ta.trace = c.trace(16 * static_cast<int64_t>(G));
   const size_t smem = tiles_smem(S.s);
   auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT>;
@@ -658,6 +723,11 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
     TimedLaunch t(c, name);
     kern<<<G, kCtaThreads, smem, c.stream>>>(ta, x, xscale, out, ua);
     SDR_KERNEL_CHECK();
+  }
+  if (sf) {  // the next step's update (or the pipeline flush) folds these
+    sf->out_G = G;
+    sf->out_nvp = static_cast<int>(nv);
+    return;
   }
   const int nwarps = static_cast<int>(S.s) + (SRC == kSrcUpdate ? ua.T : 0);
   TimedLaunch t(c, "sketch_fold");
@@ -677,13 +747,21 @@ void prepare_srdct_tables(Context& c, SketchDev& S) {
   c.sync();
 }
 
-bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
-                          int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec,
-                          const double* coef_ready, int64_t row_begin) {
-  const int need = std::max(nwin, ngram + 1);
+bool update_sketch_eligible(const SketchDev& S, const VecLayout& lay, int need, int64_t row_begin, int64_t ldv) {
   if (S.kind != kSrdct || need > 4) return false;
   const SrdctPlan p = plan_srdct(S.n, lay.nloc);
-  if (!tiles_eligible(S, p) || p.M != 128 || p.L % 2 || row_begin % 2 || lay.own_off % 2 || ldv % 2) return false;
+  return tiles_eligible(S, p) && p.M == 128 && p.L % 2 == 0 && row_begin % 2 == 0 && lay.own_off % 2 == 0 &&
+         ldv % 2 == 0;
+}
+
+int64_t update_sketch_partials_size(const SketchDev& S, int num_sms) { return (2 * S.s + 8) * num_sms; }
+
+bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
+                          int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec,
+                          const double* coef_ready, int64_t row_begin, StepFold* sf) {
+  const int need = std::max(nwin, ngram + 1);
+  if (!update_sketch_eligible(S, lay, need, row_begin, ldv)) return false;
+  const SrdctPlan p = plan_srdct(S.n, lay.nloc);
   UpdateArgs ua;
   ua.y = y;
   ua.V = V;
@@ -697,11 +775,35 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
   ua.rec = rec;
   ua.cvec = cvec;
   ua.coef_ready = coef_ready;
+  if (sf) {
+    ua.k1_partials = sf->k1_partials;
+    ua.k1_G = sf->k1_G;
+    ua.prev_partials = sf->prev_partials;
+    ua.prev_G = sf->prev_G;
+    ua.prev_nvp = sf->prev_nvp;
+    ua.prev_ngram = sf->prev_ngram;
+  }
   if (need <= 2)
-    launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua);
+    launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
   else
-    launch_tiles<kSrcUpdate, 8, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua);
+    launch_tiles<kSrcUpdate, 8, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
   return true;
+}
+
+void launch_update_sketch_flush(Context& c, const SketchDev& S, const StepFold& sf, double* rec, const RecLayout& RL,
+                                int j, int ngram) {
+  UpdateArgs ua;
+  ua.rstride = RL.stride;
+  ua.j = j;
+  ua.ngram = ngram;
+  ua.T = RL.T;
+  ua.rec = rec;
+  const int nwarps = static_cast<int>(S.s) + RL.T;
+  TimedLaunch t(c, "sketch_fold");
+  k_srdct_fold<kSrcUpdate><<<(nwarps + 7) / 8, 256, 0, c.stream>>>(sf.out_partials, sf.out_G, sf.out_nvp,
+                                                                   static_cast<int>(S.s), S.tab.get(), S.row_scale.get(),
+                                                                   nullptr, ua, (sf.out_nvp - 2 * static_cast<int>(S.s)));
+  SDR_KERNEL_CHECK();
 }
 
 void launch_sketch(Context& c, const SketchDev& S, const double* x_own, int64_t nloc, int64_t row_begin, double* out) {

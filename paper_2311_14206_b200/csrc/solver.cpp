@@ -48,6 +48,7 @@ struct Workspace {
   DeviceBuffer<double> V[2];
   int nV = 0;
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
+  DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
   DeviceBuffer<const double*> inptr;
   DeviceBuffer<double*> outptr;
   PinnedBuffer<double> hrec, hscal, hcoef;
@@ -238,6 +239,7 @@ struct ArnoldiPipeline {
   /// w_0 = r0, ||r0||^2 and S r0 on the device; the host reads them in init_finish.
   void init_enqueue(const double* r0) {
     const RecLayout& RL = w.RL;
+    setup_deferred();
     w.fence_copies(c);
     launch_copy_norm(c, r0, w.Vcol(vb, 0), w.lay.nloc, w.rec.get() + RL.b_off());
     launch_sketch(c, S, w.Vcol(vb, 0), w.lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
@@ -265,6 +267,21 @@ struct ArnoldiPipeline {
     st.cv[0] = 1.0 / st.r0_norm;
   }
 
+  // deferred-fold pipeline (one GPU, fused update eligible): record row j is
+  // completed by K2(j)'s prologue, so its copy follows K2(j); see StepFold
+  bool deferred = false;
+  StepFold last;  // partials K2(issued - 1) left
+  i64 last_ngram = 0;
+
+  void setup_deferred() {
+    const int need = static_cast<int>(std::max<i64>(std::min(t, m), std::min<i64>(w.RL.T - 1, m) + 1));
+    deferred = !c.distributed() && fuse_update_sketch() &&
+               update_sketch_eligible(S, w.lay, need, A.row_begin, w.lay.ld);
+    if (!deferred) return;
+    w.p1.ensure(34 * static_cast<i64>(c.num_sms) * 8);
+    for (auto& b : w.p2) b.ensure(update_sketch_partials_size(S, c.num_sms));
+  }
+
   void enqueue(i64 j) {
     const VecLayout& lay = w.lay;
     const RecLayout& RL = w.RL;
@@ -273,8 +290,31 @@ struct ArnoldiPipeline {
     const int nwin = static_cast<int>(std::min<i64>(t, j + 1));
     const int ngram = static_cast<int>(std::min<i64>(T - 1, j + 1));
     double* Vb = w.V[vb].get();
-    c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
     double* recj = w.rec.get() + (j + 1) * R;
+    if (deferred) {
+      StepFold sf;
+      sf.k1_partials = w.p1.get();
+      sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
+                                    w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get());
+      if (j > 0) {
+        sf.prev_partials = last.out_partials;
+        sf.prev_G = last.out_G;
+        sf.prev_nvp = last.out_nvp;
+        sf.prev_ngram = static_cast<int>(last_ngram);
+      }
+      sf.out_partials = w.p2[j & 1].get();
+      if (!launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
+                                w.cvec.get(), nullptr, A.row_begin, &sf))
+        throw logic("deferred step pipeline: fused update became ineligible");
+      last = sf;
+      last_ngram = ngram;
+      if (j > 0)  // row j is complete now
+        w.copy_back(c, w.hrec.get() + j * R, w.rec.get() + j * R, R, w.evk[static_cast<size_t>(j)],
+                    w.ev[static_cast<size_t>(j)]);
+      if (j + 1 == m) flush(j);
+      return;
+    }
+    c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
     // one GPU: K1's last CTA forms the MGS coefficients; several: K2 forms
     // them after the allreduce of the window dots
     double* coef = c.distributed() ? nullptr : w.coef_dev.get();
@@ -289,6 +329,14 @@ struct ArnoldiPipeline {
     }
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
     w.copy_back(c, w.hrec.get() + (j + 1) * R, recj, R, w.evk[static_cast<size_t>(j + 1)],
+                w.ev[static_cast<size_t>(j + 1)]);
+  }
+
+  /// Deferred pipeline: completes row j + 1 when no K2(j + 1) will follow.
+  void flush(i64 j) {
+    const i64 R = w.RL.stride;
+    launch_update_sketch_flush(c, S, last, w.rec.get(), w.RL, static_cast<int>(j), static_cast<int>(last_ngram));
+    w.copy_back(c, w.hrec.get() + (j + 1) * R, w.rec.get() + (j + 1) * R, R, w.evk[static_cast<size_t>(j + 1)],
                 w.ev[static_cast<size_t>(j + 1)]);
   }
 

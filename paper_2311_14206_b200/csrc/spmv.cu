@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
   if constexpr (MODE != 0) {
     const int nv = MODE == 1 ? 1 + nwin : 1;
     block_partials<NV>(acc, nv, partials);
+    if (counter == nullptr) return;  // deferred: the consumer folds the partials
     if (last_block_done(counter)) {
       fold_partials(partials, gridDim.x, nv, out);
       if constexpr (MODE == 1) {
@@ -182,22 +183,24 @@ int resident_grid(const Context& c, K kernel, int64_t want_blocks) {
 int64_t blocks_for(int64_t nslices) { return (nslices + (kThreads / 32) - 1) / (kThreads / 32); }
 
 template <int MODE, int NV, int FMT>
-void launch_impl(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
-                 int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
-                 const MgsArgs& mg) {
+int launch_impl(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
+                int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
+                const MgsArgs& mg, double* partials_out) {
   auto kern = k_sell_spmv<MODE, NV, FMT>;
   const int g = resident_grid(c, kern, blocks_for(A.nslices));
+  double* part = partials_out ? partials_out : (MODE ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
   TimedLaunch t(c, name);
-  kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin,
-                                     MODE ? c.partials(static_cast<int64_t>(NV) * g) : nullptr, counter, out, mg);
+  kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part,
+                                     partials_out ? nullptr : counter, out, mg);
   SDR_KERNEL_CHECK();
+  return g;
 }
 
 template <int MODE, int NV>
-void launch_fmt(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
-                int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
-                const MgsArgs& mg) {
-#define SDR_SPMV_FMT(F) launch_impl<MODE, NV, F>(c, name, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, counter, out, mg)
+int launch_fmt(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
+               int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
+               const MgsArgs& mg, double* partials_out = nullptr) {
+#define SDR_SPMV_FMT(F) return launch_impl<MODE, NV, F>(c, name, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, counter, out, mg, partials_out)
   if (!A.doff)
     SDR_SPMV_FMT(0);
   else if (A.dia_d == 7)  // 3-D 7-point stencils
@@ -216,18 +219,20 @@ void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) 
   launch_fmt<0, 1>(c, "spmv", A, x_ext, y, nullptr, 0, 0, A.halo_lo, 0, 0, nullptr, nullptr, MgsArgs{});
 }
 
-void launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
-                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
-                         double* coef) {
+int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
+                        int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
+                        double* coef, double* partials_out) {
   const MgsArgs mg{rec, rstride, T, cvec, coef};
   const double* x_ext = V + j * ldv + lay.ext_shift();
   if (nwin <= 3)
-    launch_fmt<1, 4>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0, recA, mg);
+    return launch_fmt<1, 4>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0,
+                            recA, mg, partials_out);
   else if (nwin <= 7)
-    launch_fmt<1, 8>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0, recA, mg);
+    return launch_fmt<1, 8>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0,
+                            recA, mg, partials_out);
   else if (nwin <= 33)
-    launch_fmt<1, 34>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0, recA,
-                      mg);
+    return launch_fmt<1, 34>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin,
+                             c.counters() + 0, recA, mg, partials_out);
   else
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
 }
