@@ -132,6 +132,35 @@ __global__ void __launch_bounds__(kThreads) k_copy_norm(const double* __restrict
   }
 }
 
+/// Column sums of squares of C (n x ncol, ldc): grid (chunks, ncol), CTA
+/// partials then a per-column ordered fold (second kernel) — deterministic.
+__global__ void __launch_bounds__(kThreads) k_col_sumsq(const double* __restrict__ C, int64_t ldc, int64_t n,
+                                                         int64_t chunk, double* __restrict__ partials) {
+  const int col = blockIdx.y;
+  const double* x = C + static_cast<int64_t>(col) * ldc;
+  const int64_t beg = static_cast<int64_t>(blockIdx.x) * chunk, end = min(n, beg + chunk);
+  double acc[1] = {0.0};
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) acc[0] = fma(x[i], x[i], acc[0]);
+  __shared__ double red[kThreads / 32];
+  const double w = warp_sum(acc[0]);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int k = 0; k < kThreads / 32; ++k) v += red[k];
+    partials[static_cast<int64_t>(col) * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+__global__ void k_col_fold(const double* __restrict__ partials, int nchunks, int ncol, double* __restrict__ out) {
+  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (col >= ncol) return;
+  double v = 0.0;
+  for (int k = lane; k < nchunks; k += 32) v += partials[static_cast<int64_t>(col) * nchunks + k];
+  v = warp_sum(v);
+  if (lane == 0) out[col] = v;
+}
+
 __global__ void k_axpy(double a, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) y[i] += a * x[i];
@@ -308,6 +337,21 @@ void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, dou
   const int g = stream_grid(c, n);
   TimedLaunch t(c, "copy_norm");
   k_copy_norm<<<g, kThreads, 0, c.stream>>>(src, dst, n, c.partials(g), c.counters() + 4, norm2);
+  SDR_KERNEL_CHECK();
+}
+
+void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2) {
+  if (ncol == 0) return;
+  const int chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 4 * c.num_sms / std::max(1, ncol) + 1)));
+  const int64_t chunk = (n + chunks - 1) / chunks;
+  double* part = c.partials(static_cast<int64_t>(chunks) * ncol);
+  {
+    TimedLaunch t(c, "col_norms");
+    k_col_sumsq<<<dim3(chunks, ncol), kThreads, 0, c.stream>>>(C, ldc, n, chunk, part);
+    SDR_KERNEL_CHECK();
+  }
+  TimedLaunch t(c, "col_norms");
+  k_col_fold<<<(ncol + 7) / 8, 256, 0, c.stream>>>(part, chunks, ncol, norms2);
   SDR_KERNEL_CHECK();
 }
 

@@ -3,6 +3,8 @@
 // loaded instead of linking a second copy), and event timing.
 #include "context.hpp"
 
+#include <cublas_v2.h>
+
 #include <cstdlib>
 
 #include <nccl.h>
@@ -92,6 +94,7 @@ Context::Context(int dev, int rk, int ws, const void* nccl_id) : device(dev), ra
 Context::~Context() {
   cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  if (blas_) cublasDestroy(static_cast<cublasHandle_t>(blas_));
   if (comm_ && nccl_) nccl_->CommDestroy(static_cast<ncclComm_t>(comm_));
   for (auto& p : pending_) {
     cudaEventDestroy(p.a);
@@ -200,6 +203,26 @@ void Context::timing_reset() {
     SDR_CUDA(cudaEventDestroy(origin_));
     origin_ = nullptr;
   }
+}
+
+void Context::dgemm_tall(i64 n, i64 nout, i64 k, const double* A, i64 lda, const double* B, i64 ldb, double beta,
+                         double* C, i64 ldc) {
+  if (n == 0 || nout == 0) return;
+  if (!blas_) {
+    cublasHandle_t h = nullptr;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw runtime("cublasCreate failed");
+    blas_ = h;
+  }
+  auto h = static_cast<cublasHandle_t>(blas_);
+  if (cublasSetStream(h, stream) != CUBLAS_STATUS_SUCCESS) throw runtime("cublasSetStream failed");
+  const double one = 1.0;
+  ++launches;
+  if (timing) time_begin("recycle_gemm");
+  const cublasStatus_t st = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(nout),
+                                        static_cast<int>(k), &one, A, static_cast<int>(lda), B, static_cast<int>(ldb),
+                                        &beta, C, static_cast<int>(ldc));
+  if (timing) time_end();
+  if (st != CUBLAS_STATUS_SUCCESS) throw runtime("cublasDgemm failed with status " + std::to_string(static_cast<int>(st)));
 }
 
 unsigned long long* Context::trace(i64 n) {

@@ -88,6 +88,12 @@ class Context {
 
   void sync() { SDR_CUDA(cudaStreamSynchronize(stream)); }
 
+  /// C (n x nout, ldc) = beta C + A (n x k, lda) B (k x nout, ldb), column-major
+  /// fp64 on the context stream through cuBLAS (plain tall-skinny GEMM of the
+  /// recycle update; deterministic for a fixed GPU).
+  void dgemm_tall(i64 n, i64 nout, i64 k, const double* A, i64 lda, const double* B, i64 ldb, double beta, double* C,
+                  i64 ldc);
+
   /// Solver workspace cached across solves (solver.cpp owns the type).
   std::shared_ptr<void> workspace;
 
@@ -97,6 +103,7 @@ class Context {
   DeviceBuffer<unsigned long long> trace_;
   PinnedBuffer<double> pinned_;
   NcclApi* nccl_ = nullptr;
+  void* blas_ = nullptr;  // cublasHandle_t, created on first use
   void* comm_ = nullptr;
   struct Pending {
     std::string name;

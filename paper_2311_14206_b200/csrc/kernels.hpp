@@ -71,6 +71,8 @@ void launch_update(Context& c, const double* y, double* V, int64_t ldv, const Ve
                    int ngram, double* rec, const RecLayout& L, double* cvec, const double* coef_ready);
 void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, double* norm2);
 void launch_axpy(Context& c, double a, const double* x, double* y, int64_t n);
+/// norms2[q] = ||C(:, q)||^2 for q < ncol (column-major, ldc), deterministic.
+void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2);
 void launch_scale_copy(Context& c, double a, const double* x, double* y, int64_t n);
 void launch_tallskinny(Context& c, const double* const* in_dev, int nin, const double* coef_dev, int nout,
                        double* const* out_dev, int64_t n, double* norms2);

@@ -18,6 +18,11 @@
 // buffer, which the new cycle does not touch).
 #include "solver.hpp"
 
+#include <atomic>
+#include <exception>
+#include <functional>
+#include <thread>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -30,6 +35,7 @@ namespace sdr {
 
 namespace {
 constexpr int kLookahead = 2;
+constexpr int kPumpDepth = 3;  // steps kept in flight while the host runs restart bookkeeping
 
 /// SDR_FUSE=0 disables the fused update+sketch kernel (A/B and parity checks).
 bool fuse_update_sketch() {
@@ -49,6 +55,8 @@ struct Workspace {
   int nV = 0;
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
+  DeviceBuffer<double> gcoef;      // recycle-update GEMM coefficients
+  PinnedBuffer<double> hgcoef;
   DeviceBuffer<const double*> inptr;
   DeviceBuffer<double*> outptr;
   PinnedBuffer<double> hrec, hscal, hcoef;
@@ -60,7 +68,15 @@ struct Workspace {
   // Record read-back runs on its own stream so the compute stream never waits
   // for a device-to-host copy between steps (it did: ~9 µs per step).
   cudaStream_t copy_stream = nullptr;
+  // recycle-update product off the compute stream (one GPU, deferred pipeline)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_side_in = nullptr, ev_side_out = nullptr;
+  std::vector<cudaEvent_t> evd;  // K2(j) finished (speculation pump)
   ~Workspace() {
+    for (auto e : evd) cudaEventDestroy(e);
+    if (ev_side_in) cudaEventDestroy(ev_side_in);
+    if (ev_side_out) cudaEventDestroy(ev_side_out);
+    if (side_stream) cudaStreamDestroy(side_stream);
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : evk) cudaEventDestroy(e);
     if (ev_init) cudaEventDestroy(ev_init);
@@ -119,17 +135,22 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
     w->cvec.resize(mm + 2);
     w->hrec.ensure((mm + 2) * w->RL.stride);
     while (static_cast<i64>(w->ev.size()) < mm + 2) {
-      cudaEvent_t e, k;
+      cudaEvent_t e, k, d;
       SDR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       SDR_CUDA(cudaEventCreateWithFlags(&k, cudaEventDisableTiming));
+      SDR_CUDA(cudaEventCreateWithFlags(&d, cudaEventDisableTiming));
       w->ev.push_back(e);
       w->evk.push_back(k);
+      w->evd.push_back(d);
     }
     if (!w->ev_init) {
       SDR_CUDA(cudaEventCreateWithFlags(&w->ev_init, cudaEventDisableTiming));
       SDR_CUDA(cudaEventCreateWithFlags(&w->ev_init_k, cudaEventDisableTiming));
       SDR_CUDA(cudaEventCreateWithFlags(&w->ev_copies, cudaEventDisableTiming));
       SDR_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+      SDR_CUDA(cudaStreamCreateWithFlags(&w->side_stream, cudaStreamNonBlocking));
+      SDR_CUDA(cudaEventCreateWithFlags(&w->ev_side_in, cudaEventDisableTiming));
+      SDR_CUDA(cudaEventCreateWithFlags(&w->ev_side_out, cudaEventDisableTiming));
     }
   }
   const i64 nl = std::max<i64>(lay.nloc, 1);
@@ -246,6 +267,7 @@ struct ArnoldiPipeline {
     c.allreduce_sum(w.rec.get() + RL.b_off(), RL.b_len());
     w.copy_back(c, w.hrec.get(), w.rec.get(), RL.stride, w.ev_init_k, w.ev_init);
     issued = 0;
+    done_upto = 0;
   }
 
   /// init_krylov bookkeeping (arnoldi.hpp:47-72); throws domain on a zero residual.
@@ -308,6 +330,7 @@ struct ArnoldiPipeline {
         throw logic("deferred step pipeline: fused update became ineligible");
       last = sf;
       last_ngram = ngram;
+      SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
       if (j > 0)  // row j is complete now
         w.copy_back(c, w.hrec.get() + j * R, w.rec.get() + j * R, R, w.evk[static_cast<size_t>(j)],
                     w.ev[static_cast<size_t>(j)]);
@@ -328,6 +351,7 @@ struct ArnoldiPipeline {
       launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
     }
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
+    SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
     w.copy_back(c, w.hrec.get() + (j + 1) * R, recj, R, w.evk[static_cast<size_t>(j + 1)],
                 w.ev[static_cast<size_t>(j + 1)]);
   }
@@ -340,9 +364,24 @@ struct ArnoldiPipeline {
                 w.ev[static_cast<size_t>(j + 1)]);
   }
 
-  /// Keep up to kLookahead speculative steps ahead of step j in flight.
+  i64 done_upto = 0;  // steps [0, done_upto) have finished on the GPU
+  void poll_done() {
+    while (done_upto < issued && cudaEventQuery(w.evd[static_cast<size_t>(done_upto)]) == cudaSuccess) ++done_upto;
+  }
+
+  /// Keep up to kLookahead speculative steps ahead of step j in flight, and
+  /// at least two in flight while the host catches up with finished steps.
   void issue_ahead(i64 j) {
     while (issued < m && issued <= j + kLookahead) enqueue(issued++);
+    poll_done();
+    while (issued < m && issued - done_upto < 2) enqueue(issued++);
+  }
+
+  /// Speculation while the host is busy elsewhere (restart bookkeeping):
+  /// keeps kPumpDepth steps in flight without queueing the whole cycle.
+  void pump() {
+    poll_done();
+    while (issued < m && issued - done_upto < kPumpDepth) enqueue(issued++);
   }
 
   /// Consumes step st.j (arnoldi.hpp:87-118 bookkeeping); returns true on
@@ -394,8 +433,37 @@ struct ArnoldiPipeline {
   }
 };
 
+/// Runs `job` on a host thread while the calling thread keeps the GPU fed
+/// through `pump` (no CUDA call leaves the calling thread).
+template <class F>
+void host_job_while_pumping(F&& job, const std::function<void()>* pump) {
+  if (!pump) {
+    job();
+    return;
+  }
+  std::atomic<bool> done{false};
+  std::exception_ptr err;
+  std::thread th([&] {
+    try {
+      job();
+    } catch (...) {
+      err = std::current_exception();
+    }
+    done.store(true, std::memory_order_release);
+  });
+  while (!done.load(std::memory_order_acquire)) {
+    (*pump)();
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  th.join();
+  if (err) std::rethrow_exception(err);
+}
+
+/// pump: keeps the next cycle's speculative steps flowing while the host
+/// computes the harmonic pencil (the GPU otherwise idles at every restart).
 void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recycle& sp, i64 k, double rank_tol,
-                    Counters& cnt, std::vector<std::string>* notes, Report& rep) {  // recycle.hpp:226-289
+                    Counters& cnt, std::vector<std::string>* notes, Report& rep,
+                    const std::function<void()>* pump = nullptr, bool side_stream = false) {  // recycle.hpp:226-289
   const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
   if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
   HMat SAW(s, kh + j), SW(s, kh + j);
@@ -409,8 +477,15 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
   }
   Harmonic hp;
   {
-    PhaseTimer pt(rep, "recycle_harmonic");
-    hp = harmonic_extract(SAW, SW, k, rank_tol);
+    double ms = 0.0;
+    host_job_while_pumping(
+        [&] {
+          const auto t0 = std::chrono::steady_clock::now();
+          hp = harmonic_extract(SAW, SW, k, rank_tol);
+          ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        },
+        pump);
+    rep.phase_ms["recycle_harmonic"] += ms;
   }
   if (notes) {
     if (hp.rank_limited)
@@ -426,42 +501,97 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     return;
   }
   sp.ensure(w.lay.nloc, std::max<i64>(ke, kh));
-  // device: U_new = V(:,0:j) C_bot + U C_top with lazy scales folded in
-  std::vector<const double*> in;
-  HMat coef(kh + j, ke);
-  for (i64 i = 0; i < j; ++i) {
-    in.push_back(w.Vcol(vb, i));
-    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
-  }
-  for (i64 p = 0; p < kh; ++p) {
-    in.push_back(sp.col(p));
-    for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
+  // device: U_new = V(:,0:j) C_bot + U C_top with the lazy scales folded into
+  // the coefficients — two plain tall-skinny GEMMs (cuBLAS) and a column-norm
+  // pass. The U part needs its live columns to be exactly slots [0, kc)
+  // (a dead column could hold non-finite data that a zero coefficient would
+  // not cancel); otherwise the pointer-list K4 kernel runs instead.
+  const i64 nloc = w.lay.nloc;
+  i64 kc = 0;
+  bool dense_u = true;
+  {
+    std::vector<char> used(static_cast<size_t>(std::max<i64>(sp.cap, 1)), 0);
+    for (i64 p = 0; p < kh; ++p) {
+      used[static_cast<size_t>(sp.slot[static_cast<size_t>(p)])] = 1;
+      kc = std::max<i64>(kc, sp.slot[static_cast<size_t>(p)] + 1);
+    }
+    for (i64 q = 0; q < kc; ++q) dense_u = dense_u && used[static_cast<size_t>(q)];
   }
   const int other = 1 - sp.cur;
-  std::vector<double*> out;
-  for (i64 q = 0; q < ke; ++q) out.push_back(sp.buf[other].get() + q * sp.ld);
-  tallskinny(c, w, in, coef, out, w.lay.nloc, w.scal.get());
-  c.allreduce_sum(w.scal.get(), ke);
-  SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), w.scal.get(), sizeof(double) * ke, cudaMemcpyDeviceToHost, c.stream));
-  // host: SU_new, SAU_new (recycle.hpp:257-265) while the product runs
-  HMat SU(s, ke), SAU(s, ke);
-  for (i64 q = 0; q < ke; ++q) {
+  // with a side stream the product does not queue behind the speculative
+  // steps pumped onto the compute stream (it reads the finished cycle's basis
+  // and the old U only; the next cycle's correction waits for it below)
+  const bool side = side_stream && dense_u && !c.distributed();
+  if (side) {  // ev_side_in: recorded by solve() when the finished cycle's device work was enqueued
+    SDR_CUDA(cudaStreamWaitEvent(w.side_stream, w.ev_side_in, 0));
+    std::swap(c.stream, w.side_stream);
+  }
+  if (dense_u) {
+    const i64 ncoef = j * ke + kc * ke;
+    w.gcoef.ensure(std::max<i64>(ncoef, 1));
+    w.hgcoef.ensure(std::max<i64>(ncoef, 1));
+    double* hv = w.hgcoef.get();
+    for (i64 q = 0; q < ke; ++q)
+      for (i64 i = 0; i < j; ++i) hv[q * j + i] = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
+    double* hu = hv + j * ke;
+    for (i64 p = 0; p < kh; ++p)
+      for (i64 q = 0; q < ke; ++q)
+        hu[q * kc + sp.slot[static_cast<size_t>(p)]] = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
+    SDR_CUDA(cudaMemcpyAsync(w.gcoef.get(), hv, sizeof(double) * static_cast<size_t>(ncoef), cudaMemcpyHostToDevice,
+                             c.stream));
+    double* unew = sp.buf[other].get();
+    c.dgemm_tall(nloc, ke, j, w.Vcol(vb, 0), w.lay.ld, w.gcoef.get(), j, 0.0, unew, sp.ld);
+    if (kc > 0) c.dgemm_tall(nloc, ke, kc, sp.buf[sp.cur].get(), sp.ld, w.gcoef.get() + j * ke, kc, 1.0, unew, sp.ld);
+    launch_col_norms2(c, unew, sp.ld, nloc, static_cast<int>(ke), w.scal.get());
+  } else {
+    std::vector<const double*> in;
+    HMat coef(kh + j, ke);
     for (i64 i = 0; i < j; ++i) {
-      const double cf = hp.coeffs(kh + i, q);
-      for (i64 r = 0; r < s; ++r) {
-        SU(r, q) += st.SV(r, i) * cf;
-        SAU(r, q) += st.SAV(r, i) * cf;
-      }
+      in.push_back(w.Vcol(vb, i));
+      for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
     }
     for (i64 p = 0; p < kh; ++p) {
-      const double cf = hp.coeffs(p, q);
-      for (i64 r = 0; r < s; ++r) {
-        SU(r, q) += sp.SU(r, p) * cf;
-        SAU(r, q) += sp.SAU(r, p) * cf;
-      }
+      in.push_back(sp.col(p));
+      for (i64 q = 0; q < ke; ++q) coef(static_cast<i64>(in.size()) - 1, q) = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
     }
+    std::vector<double*> out;
+    for (i64 q = 0; q < ke; ++q) out.push_back(sp.buf[other].get() + q * sp.ld);
+    tallskinny(c, w, in, coef, out, nloc, w.scal.get());
   }
-  c.sync();
+  c.allreduce_sum(w.scal.get(), ke);
+  SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), w.scal.get(), sizeof(double) * ke, cudaMemcpyDeviceToHost, c.stream));
+  SDR_CUDA(cudaEventRecord(w.ev_side_out, c.stream));
+  if (side) {
+    std::swap(c.stream, w.side_stream);
+    SDR_CUDA(cudaStreamWaitEvent(c.stream, w.ev_side_out, 0));  // later work on the compute stream sees U_new
+  }
+  // host: SU_new, SAU_new (recycle.hpp:257-265) while the product runs
+  HMat SU(s, ke), SAU(s, ke);
+  host_job_while_pumping(
+      [&] {
+        for (i64 q = 0; q < ke; ++q) {
+          for (i64 i = 0; i < j; ++i) {
+            const double cf = hp.coeffs(kh + i, q);
+            for (i64 r = 0; r < s; ++r) {
+              SU(r, q) += st.SV(r, i) * cf;
+              SAU(r, q) += st.SAV(r, i) * cf;
+            }
+          }
+          for (i64 p = 0; p < kh; ++p) {
+            const double cf = hp.coeffs(p, q);
+            for (i64 r = 0; r < s; ++r) {
+              SU(r, q) += sp.SU(r, p) * cf;
+              SAU(r, q) += sp.SAU(r, p) * cf;
+            }
+          }
+        }
+      },
+      pump);
+  while (cudaEventQuery(w.ev_side_out) == cudaErrorNotReady) {
+    if (pump) (*pump)();
+    std::this_thread::sleep_for(std::chrono::microseconds(10));
+  }
+  SDR_CUDA(cudaEventSynchronize(w.ev_side_out));
   sp.cur = other;
   sp.slot.resize(static_cast<size_t>(ke));
   sp.uscale.resize(static_cast<size_t>(ke));
@@ -596,7 +726,8 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
 
 /// Cycle statistics and the harmonic recycle update (solver.hpp:218-253).
 void finish_cycle(Context& c, Workspace& w, const ArnoldiPipeline& ap, const CycleOut& out, const Config& cfg,
-                  Recycle& space, Counters& cnt, Report& rep, int cycle_index) {
+                  Recycle& space, Counters& cnt, Report& rep, int cycle_index,
+                  const std::function<void()>* pump = nullptr, bool side_stream = false) {
   const HostKrylov& st = ap.st;
   const i64 s = ap.S.s;
   CycleStat cs;
@@ -610,13 +741,13 @@ void finish_cycle(Context& c, Workspace& w, const ArnoldiPipeline& ap, const Cyc
     PhaseTimer pt(rep, "basis_cond");
     HMat B(s, st.j + 1);
     std::copy(st.SV.a.begin(), st.SV.a.begin() + s * (st.j + 1), B.a.begin());
-    cs.basis_cond = cond2(B);
+    host_job_while_pumping([&] { cs.basis_cond = cond2(B); }, pump);
   }
   rep.cycle_stats.push_back(cs);
   if (cfg.k > 0 && st.j >= 1) {
     std::vector<std::string> notes;
     PhaseTimer pt(rep, "recycle");
-    update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep);
+    update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep, pump, side_stream);
     rep.cycle_stats.back().deflation_rank = space.dim();
     for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
   } else if (cfg.k == 0) {
@@ -728,15 +859,11 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
   pt_setup.reset();
   auto cur = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, 0);
   cur->init_enqueue(w.r0.get());
-  double step_ms = 0.0, finish_ms = 0.0;  // measured per-step and per-cycle-end wall times
   for (int cycle = 1; cycle <= cfg.max_restarts; ++cycle) {  // solver.hpp:321-359
     CycleOut cr;
-    double cycle_ms = 0.0;
     try {
-      const auto tc0 = std::chrono::steady_clock::now();
       cr = run_cycle(c, w, *cur, A, cfg, w.r0.get(), space, tol_abs, safety, rep.counters, rep, cb, cycle,
                      rep.iterations);
-      cycle_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count();
     } catch (const Error& e) {
       if (e.code != 2) throw;
       rep.status = 0;  // zero residual at cycle entry: converged exactly
@@ -767,21 +894,21 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
     } else if (cycle == cfg.max_restarts) {
       status = 1;
     }
+    // the finished cycle's device work is all enqueued: the recycle product
+    // may start as soon as it completes (side stream, see update_recycle)
+    SDR_CUDA(cudaEventRecord(w.ev_side_in, c.stream));
     std::unique_ptr<ArnoldiPipeline> next;
+    std::function<void()> pump;
     if (status < 0 && w.nV == 2) {
-      // overlap: next cycle's init + enough speculative steps on the other
-      // basis buffer to cover the host SVD/Schur of the finished cycle
+      // overlap: the next cycle's init and steps on the other basis buffer,
+      // pumped while the host computes the harmonic pencil of this cycle
       next = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, 1 - cur->vb);
       next->init_enqueue(w.r0.get());
-      i64 ahead = kLookahead;
-      if (step_ms > 0.0) ahead = static_cast<i64>(std::ceil(1.25 * finish_ms / step_ms)) + kLookahead;
-      else ahead = 32;
-      next->issue_ahead(std::min<i64>(ahead, cfg.m - 1));
+      next->issue_ahead(0);
+      pump = [&next] { next->pump(); };
     }
-    const auto tf0 = std::chrono::steady_clock::now();
-    finish_cycle(c, w, *cur, cr, cfg, space, rep.counters, rep, cycle);
-    finish_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tf0).count();
-    if (cr.steps > 0) step_ms = cycle_ms / static_cast<double>(cr.steps);
+    finish_cycle(c, w, *cur, cr, cfg, space, rep.counters, rep, cycle, next ? &pump : nullptr,
+                 next && next->deferred);
     if (status >= 0) {
       rep.status = status;
       if (!note.empty()) rep.notes.push_back(note);
