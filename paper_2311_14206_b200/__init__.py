@@ -668,8 +668,10 @@ def _make_callbacks(callbacks):
 
 
 def solve(A: SparseMatrix, b, cfg: SolverConfig, space: RecycleSpace | None = None,
-          sketch: SketchOperator | None = None, x0=None, callbacks: dict | None = None) -> SolveResult:
-    """solver.hpp:269-365. b / x0: numpy (host) or float64 CUDA tensors (device)."""
+          sketch: SketchOperator | None = None, x0=None, callbacks: dict | None = None, out=None) -> SolveResult:
+    """solver.hpp:269-365. b / x0: numpy (host) or float64 CUDA tensors (device).
+    out: optional destination for x (numpy, e.g. a view of pinned memory, or a
+    CUDA tensor) of the rhs length."""
     ctx = A.ctx
     space = space if space is not None else RecycleSpace(ctx)
     kb, pb, nb = _ptr(b)
@@ -678,7 +680,14 @@ def solve(A: SparseMatrix, b, cfg: SolverConfig, space: RecycleSpace | None = No
     kx0, px0, nx0 = _ptr(x0)
     if x0 is not None and nx0 != nb:
         raise ValueError(f"solve: x0 length {nx0} does not match rhs length {nb}")
-    if _is_torch_cuda(b):
+    if out is not None:
+        kx, px, nx = _ptr(out)
+        if kx is not out:
+            raise ValueError("solve: out must be a contiguous float64 array or CUDA tensor")
+        if nx != nb:
+            raise ValueError(f"solve: out length {nx} does not match rhs length {nb}")
+        x = out
+    elif _is_torch_cuda(b):
         import torch
         x = torch.empty(nb, dtype=torch.float64, device=b.device)
         px = C.c_void_p(x.data_ptr())

@@ -157,4 +157,20 @@ inline bool is_device_pointer(const void* p) {
 
 inline i64 round_up(i64 v, i64 m) { return (v + m - 1) / m * m; }
 
+#ifdef __CUDACC__
+/// Programmatic dependent launch: a kernel launched with programmatic stream
+/// serialization may start while its predecessor drains; it must call
+/// pdl_wait() before touching the predecessor's output (no-op otherwise).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+#endif
+
+/// Launch attribute set for programmatic stream serialization (PDL).
+inline cudaLaunchAttribute pdl_attribute() {
+  cudaLaunchAttribute a{};
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+  return a;
+}
+
 }  // namespace sdr

@@ -50,6 +50,9 @@ struct RecLayout {
 
 struct SketchDev;  // sketch.cu
 
+/// SDR_PDL=0 disables programmatic dependent launch in the step pipeline.
+bool pdl_enabled();
+
 /// Occupancy-derived resident CTAs per SM for a kernel (cached per kernel).
 int blocks_per_sm(const void* kernel, int threads, size_t smem);
 

@@ -11,6 +11,14 @@
 
 namespace sdr {
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SDR_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 /// SDR_DIA=0 forces plain SELL storage (A/B and parity checks).
 bool dia_enabled() {
   static const bool on = [] {

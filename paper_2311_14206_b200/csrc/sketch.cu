@@ -353,6 +353,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
     uq[q] = ta.uq[q];
   }
   for (int q = tid; q < kGroups * 2 * s; q += kCtaThreads) S1s[q - g * 2 * s] = make_double2(0.0, 0.0);
+  pdl_trigger();
+  pdl_wait();  // everything below reads the previous kernels' output
   if constexpr (SRC == kSrcUpdate) {
     if (ua.k1_partials) {
       // deferred: fold K1's window dots and the previous update's norm / Gram
@@ -721,8 +723,15 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   }
   {
     TimedLaunch t(c, name);
-    kern<<<G, kCtaThreads, smem, c.stream>>>(ta, x, xscale, out, ua);
-    SDR_KERNEL_CHECK();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kCtaThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1] = {pdl_attribute()};
+    cfg.attrs = at;
+    cfg.numAttrs = (sf && pdl_enabled()) ? 1 : 0;  // deferred step pipeline: programmatic dependent launch
+    SDR_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, x, xscale, out, ua));
   }
   if (sf) {  // the next step's update (or the pipeline flush) folds these
     sf->out_G = G;

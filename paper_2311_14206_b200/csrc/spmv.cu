@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
   const int D = FMT > 0 ? FMT : (FMT < 0 ? A.dia_d : 0);
   int nx_off = 0;
   if (FMT != 0 && gw < A.nslices && lane < D) nx_off = __ldg(A.doff + gw * D + lane);
+  pdl_trigger();  // the next kernel may start its constant-data prologue
+  pdl_wait();     // x / the window vectors come from the previous kernel
   for (int64_t sl = gw; sl < A.nslices; sl += nwarps) {
     const int cur_off = nx_off;
     if (FMT != 0 && sl + nwarps < A.nslices && lane < D) nx_off = __ldg(A.doff + (sl + nwarps) * D + lane);
@@ -190,9 +192,20 @@ int launch_impl(Context& c, const char* name, const SellView& A, const double* x
   const int g = resident_grid(c, kern, blocks_for(A.nslices));
   double* part = partials_out ? partials_out : (MODE ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
   TimedLaunch t(c, name);
-  kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part,
-                                     partials_out ? nullptr : counter, out, mg);
-  SDR_KERNEL_CHECK();
+  if (partials_out) {  // deferred step pipeline: programmatic dependent launch
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1] = {pdl_attribute()};
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    SDR_CUDA(cudaLaunchKernelEx(&cfg, kern, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part,
+                                static_cast<unsigned*>(nullptr), out, mg));
+  } else {
+    kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part, counter, out, mg);
+    SDR_KERNEL_CHECK();
+  }
   return g;
 }
 
