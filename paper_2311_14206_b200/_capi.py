@@ -63,6 +63,7 @@ SIGNATURES = {
     "sdr_csr_storage": (cint, [vp, P(i32), P(i32), P(i64), P(i64)]),
     "sdr_debug_trace": (cint, [vp, vp, i64, P(i64)]),
     "sdr_debug_timeline": (cint, [vp, C.c_char_p]),
+    "sdr_debug_stamps": (cint, [vp, C.c_char_p]),
     "sdr_spmv": (cint, [vp, vp, vp, i64, vp]),
     "sdr_sketch_create_srdct": (cint, [vp, i64, i64, u64, P(vp)]),
     "sdr_sketch_create_identity": (cint, [vp, i64, P(vp)]),

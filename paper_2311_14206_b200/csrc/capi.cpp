@@ -982,6 +982,18 @@ SDR_API int sdr_debug_timeline(sdr_ctx* ctx, const char* path) {
   });
 }
 
+/* internal: device-clock launch timeline (SDR_TRACE=2) as CSV name,start_ns,end_ns */
+SDR_API int sdr_debug_stamps(sdr_ctx* ctx, const char* path) {
+  return guard([&] {
+    const auto v = ctx->c->launch_stamps_read();
+    FILE* f = std::fopen(path, "w");
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path);
+    std::fprintf(f, "name,start_ns,end_ns\n");
+    for (const auto& e : v) std::fprintf(f, "%s,%llu,%llu\n", e.first.c_str(), e.second.first, e.second.second);
+    std::fclose(f);
+  });
+}
+
 int sdr_report_phase(const sdr_report* r, const char* name, double* ms) {
   return guard([&] {
     need(r, "report");

@@ -163,6 +163,23 @@ inline i64 round_up(i64 v, i64 m) { return (v + m - 1) / m * m; }
 /// pdl_wait() before touching the predecessor's output (no-op otherwise).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+/// SDR_TRACE=2 launch timeline: first CTA start / last CTA end (%globaltimer).
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp_begin(unsigned long long* st) {
+  if (st && threadIdx.x == 0) atomicMin(st, global_ns());
+}
+/// Call with the whole CTA (contains a barrier).
+__device__ __forceinline__ void stamp_end(unsigned long long* st) {
+  if (st) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(st + (1 << 16), global_ns());
+  }
+}
 #endif
 
 /// Launch attribute set for programmatic stream serialization (PDL).

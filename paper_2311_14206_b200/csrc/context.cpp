@@ -225,17 +225,49 @@ void Context::dgemm_tall(i64 n, i64 nout, i64 k, const double* A, i64 lda, const
   if (st != CUBLAS_STATUS_SUCCESS) throw runtime("cublasDgemm failed with status " + std::to_string(static_cast<int>(st)));
 }
 
-unsigned long long* Context::trace(i64 n) {
-  static const bool on = [] {
+static int trace_mode() {
+  static const int m = [] {
     const char* e = std::getenv("SDR_TRACE");
-    return e && std::atoi(e) != 0;
+    return e ? std::atoi(e) : 0;
   }();
-  if (!on) return nullptr;
+  return m;
+}
+
+unsigned long long* Context::trace(i64 n) {
+  if (trace_mode() != 1) return nullptr;
   if (trace_.size() < n) {
     trace_.resize(n);
     SDR_CUDA(cudaMemsetAsync(trace_.get(), 0, sizeof(unsigned long long) * static_cast<size_t>(n), stream));
   }
   return trace_.get();
+}
+
+unsigned long long* Context::launch_stamp(const char* name) {
+  constexpr i64 kCap = 1 << 16;
+  if (trace_mode() != 2) return nullptr;
+  if (stamps_.size() == 0) {
+    stamps_.resize(2 * kCap);
+    SDR_CUDA(cudaMemsetAsync(stamps_.get(), 0xFF, sizeof(unsigned long long) * kCap, stream));
+    SDR_CUDA(cudaMemsetAsync(stamps_.get() + kCap, 0, sizeof(unsigned long long) * kCap, stream));
+  }
+  const i64 i = static_cast<i64>(stamp_names_.size());
+  if (i >= kCap) return nullptr;
+  stamp_names_.push_back(name);
+  return stamps_.get() + i;  // start at [i], end at [i + kCap]
+}
+
+std::vector<std::pair<std::string, std::pair<unsigned long long, unsigned long long>>> Context::launch_stamps_read() {
+  constexpr i64 kCap = 1 << 16;
+  std::vector<std::pair<std::string, std::pair<unsigned long long, unsigned long long>>> out;
+  if (stamps_.size() == 0) return out;
+  std::vector<unsigned long long> h(static_cast<size_t>(2 * kCap));
+  SDR_CUDA(cudaMemcpyAsync(h.data(), stamps_.get(), sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream));
+  sync();
+  for (size_t i = 0; i < stamp_names_.size(); ++i) out.push_back({stamp_names_[i], {h[i], h[i + kCap]}});
+  stamp_names_.clear();
+  SDR_CUDA(cudaMemsetAsync(stamps_.get(), 0xFF, sizeof(unsigned long long) * kCap, stream));
+  SDR_CUDA(cudaMemsetAsync(stamps_.get() + kCap, 0, sizeof(unsigned long long) * kCap, stream));
+  return out;
 }
 
 std::vector<unsigned long long> Context::trace_read() {

@@ -55,6 +55,10 @@ class Context {
   unsigned* counters() { return counters_.get(); }  // kNumCounters slots
   /// Kernel phase trace buffer (SDR_TRACE=1, debugging only): null when off.
   unsigned long long* trace(i64 n);
+  /// Device-clock launch timeline (SDR_TRACE=2, debugging only): a (first CTA
+  /// start, last CTA end) %globaltimer pair for this launch, or null.
+  unsigned long long* launch_stamp(const char* name);
+  std::vector<std::pair<std::string, std::pair<unsigned long long, unsigned long long>>> launch_stamps_read();
   std::vector<unsigned long long> trace_read();
   static constexpr int kNumCounters = 64;
 
@@ -100,7 +104,8 @@ class Context {
  private:
   DeviceBuffer<double> partials_, partials2_, stage_;
   DeviceBuffer<unsigned> counters_;
-  DeviceBuffer<unsigned long long> trace_;
+  DeviceBuffer<unsigned long long> trace_, stamps_;
+  std::vector<std::string> stamp_names_;
   PinnedBuffer<double> pinned_;
   NcclApi* nccl_ = nullptr;
   void* blas_ = nullptr;  // cublasHandle_t, created on first use

@@ -267,7 +267,8 @@ struct TileArgs {
   const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][twiddle 256]
   const int* uq = nullptr;       // k mod 256
   double* partials = nullptr;    // [G][nvp] CTA partials
-  unsigned long long* trace = nullptr;  // SDR_TRACE: per-CTA phase timestamps [G][16]
+  unsigned long long* trace = nullptr;  // SDR_TRACE=1: per-CTA phase timestamps [G][16]
+  unsigned long long* stamp = nullptr;  // SDR_TRACE=2: launch timeline
 };
 
 __device__ __forceinline__ void trace_mark(unsigned long long* tr, int slot) {
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
   __shared__ double nred[MAXT][kCtaThreads / 32];
   const int G = gridDim.x, b = blockIdx.x;
   const uint64_t twoN = 2u * static_cast<uint64_t>(ta.N);
+  stamp_begin(ta.stamp);
   trace_mark(ta.trace, 0);
   for (int k = tid; k < 256; k += kCtaThreads) tw[k] = ta.tab[5 * s + k];
   for (int q = tid; q < s; q += kCtaThreads) {
@@ -587,6 +589,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
     }
   }
   trace_mark(ta.trace, 3);
+  stamp_end(ta.stamp);
 }
 
 /// Fold of the tile kernels' CTA partials ([G][nvp], CTA-major), one warp per
@@ -714,6 +717,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   ta.uq = S.uq.get();
   ta.partials = sf ? sf->out_partials : c.partials(nv * G);
   ta.trace = c.trace(16 * static_cast<int64_t>(G));
+  ta.stamp = c.launch_stamp(name);
   const size_t smem = tiles_smem(S.s);
   auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT>;
   static size_t configured = 0;

@@ -737,22 +737,47 @@ void finish_cycle(Context& c, Workspace& w, const ArnoldiPipeline& ap, const Cyc
   cs.exit_sres = out.sres;
   cs.exit_residual = out.residual_norm;
   cs.safety_after = out.safety;
-  if (st.j >= 1 && !st.breakdown) {
-    PhaseTimer pt(rep, "basis_cond");
-    HMat B(s, st.j + 1);
+  // the basis condition number (an SVD of SV) runs on its own host thread,
+  // concurrently with the harmonic update below
+  HMat B;
+  double bc_ms = 0.0;
+  std::exception_ptr bc_err;
+  std::thread bc_thread;
+  const bool want_bc = st.j >= 1 && !st.breakdown;
+  if (want_bc) {
+    B = HMat(s, st.j + 1);
     std::copy(st.SV.a.begin(), st.SV.a.begin() + s * (st.j + 1), B.a.begin());
-    host_job_while_pumping([&] { cs.basis_cond = cond2(B); }, pump);
+    bc_thread = std::thread([&] {
+      try {
+        const auto t0 = std::chrono::steady_clock::now();
+        cs.basis_cond = cond2(B);
+        bc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      } catch (...) {
+        bc_err = std::current_exception();
+      }
+    });
   }
+  auto join_bc = [&] {
+    if (bc_thread.joinable()) bc_thread.join();
+  };
+  try {
+    if (cfg.k > 0 && st.j >= 1) {
+      std::vector<std::string> notes;
+      PhaseTimer pt(rep, "recycle");
+      update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep, pump, side_stream);
+      cs.deflation_rank = space.dim();
+      for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
+    } else if (cfg.k == 0) {
+      space.clear();
+    }
+  } catch (...) {
+    join_bc();
+    throw;
+  }
+  join_bc();
+  if (bc_err) std::rethrow_exception(bc_err);
+  if (want_bc) rep.phase_ms["basis_cond"] += bc_ms;
   rep.cycle_stats.push_back(cs);
-  if (cfg.k > 0 && st.j >= 1) {
-    std::vector<std::string> notes;
-    PhaseTimer pt(rep, "recycle");
-    update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep, pump, side_stream);
-    rep.cycle_stats.back().deflation_rank = space.dim();
-    for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
-  } else if (cfg.k == 0) {
-    space.clear();
-  }
 }
 
 }  // namespace

@@ -112,7 +112,9 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
                                                                          int64_t own_off, int64_t halo_lo, int j,
                                                                          int nwin, double* __restrict__ partials,
                                                                          unsigned* __restrict__ counter,
-                                                                         double* __restrict__ out, MgsArgs mg) {
+                                                                         double* __restrict__ out, MgsArgs mg,
+                                                                         unsigned long long* stamp) {
+  stamp_begin(stamp);
   const int lane = threadIdx.x & 31;
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -162,7 +164,10 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
   if constexpr (MODE != 0) {
     const int nv = MODE == 1 ? 1 + nwin : 1;
     block_partials<NV>(acc, nv, partials);
-    if (counter == nullptr) return;  // deferred: the consumer folds the partials
+    if (counter == nullptr) {  // deferred: the consumer folds the partials
+      stamp_end(stamp);
+      return;
+    }
     if (last_block_done(counter)) {
       fold_partials(partials, gridDim.x, nv, out);
       if constexpr (MODE == 1) {
@@ -201,9 +206,10 @@ int launch_impl(Context& c, const char* name, const SellView& A, const double* x
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     SDR_CUDA(cudaLaunchKernelEx(&cfg, kern, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part,
-                                static_cast<unsigned*>(nullptr), out, mg));
+                                static_cast<unsigned*>(nullptr), out, mg, c.launch_stamp(name)));
   } else {
-    kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part, counter, out, mg);
+    kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part, counter, out, mg,
+                                       static_cast<unsigned long long*>(nullptr));
     SDR_KERNEL_CHECK();
   }
   return g;
