@@ -65,7 +65,7 @@ void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y);
 /// return value is the grid size.
 int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
-                        double* coef, double* partials_out = nullptr);
+                        double* coef, double* partials_out = nullptr, int max_blocks_per_sm = 0);
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2);
 
 // ---- Arnoldi update (arnoldi.cu). coef_ready: coefficients already formed
@@ -110,6 +110,31 @@ int64_t update_sketch_partials_size(const SketchDev& S, int num_sms);
 bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
                           int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec,
                           const double* coef_ready, int64_t row_begin, StepFold* sf = nullptr);
+/// Split step pipeline (one GPU): K2'(j) = update alone, the SRDCT of w_{j+1}
+/// on a side stream overlapping K1(j+1) / K2'(j+1); K2'(j) folds K1(j)'s
+/// dots, K2'(j-1)'s norm / Gram (row j) and SRDCT(j-2)'s partials (row j-1).
+struct SplitFold {
+  const double* k1_partials = nullptr;
+  int k1_G = 0;
+  const double* prev_ng = nullptr;  // K2'(j-1) norm / Gram partials, null at j = 0
+  int prev_ng_G = 0, prev_ngram = 0;
+  const double* prev_sk = nullptr;  // SRDCT(j-2) partials, null for j < 2
+  int prev_sk_G = 0, prev_sk_ld = 0, sk_row = 0;
+  double* out_ng = nullptr;  // this update's norm / Gram partials (update_split_partials_size doubles)
+};
+bool sketch_partials_eligible(const SketchDev& S, int64_t nloc, int64_t row_begin);
+int64_t sketch_partials_size(const SketchDev& S, int num_sms);
+int64_t update_split_partials_size(int num_sms);
+/// SRDCT CTA partials of x (two tile groups per CTA, no fold); G / ld out.
+void launch_sketch_partials(Context& c, const SketchDev& S, const double* x_own, int64_t nloc, int64_t row_begin,
+                            double* partials, int* G, int* ld);
+/// K2' (update alone) with the deferred prologue; returns its grid size.
+int launch_update_split(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
+                        int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec, const SplitFold& sf);
+/// Completes rows j (sketch, from ska; may be null) and j+1 (sketch from skb,
+/// norm / Gram from ng) at the end of a split cycle.
+void launch_split_flush(Context& c, const SketchDev& S, const double* ska, int Ga, int lda, const double* skb, int Gb,
+                        int ldb, const double* ng, int Gn, double* rec, const RecLayout& RL, int j, int ngram, int maxt);
 /// Folds the partials a deferred K2(j) left (sf.out_*) into record row j+1.
 void launch_update_sketch_flush(Context& c, const SketchDev& S, const StepFold& sf, double* rec, const RecLayout& RL,
                                 int j, int ngram);

@@ -264,7 +264,7 @@ struct TileArgs {
   const uint32_t* sign_bits = nullptr;
   const int64_t* rows = nullptr;
   const double* row_scale = nullptr;
-  const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][twiddle 256]
+  const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][jump4 s][jump2 s][twiddle 256]
   const int* uq = nullptr;       // k mod 256
   double* partials = nullptr;    // [G][nvp] CTA partials
   unsigned long long* trace = nullptr;  // SDR_TRACE=1: per-CTA phase timestamps [G][16]
@@ -287,12 +287,18 @@ struct UpdateArgs {
   double* rec = nullptr;
   double* cvec = nullptr;
   const double* coef_ready = nullptr;
-  // deferred folds (one GPU): K1's value-major
-  // partials [1 + nwin][k1_G] and the previous update's CTA-major partials
-  // [prev_G][prev_nvp] are folded in this kernel's prologue
+  // deferred folds (one GPU), all in the prologue:
+  //   K1's value-major window-dot partials [1 + nwin][k1_G];
+  //   column j's norm / Gram partials (CTA-major rows of ng_ld, entry g at
+  //   ng_off + g), null at j = 0;
+  //   sketch partials (CTA-major rows of sk_ld, row q at 2q, 2q+1) of column
+  //   sk_row, folded once (one warp per sketch row), or null.
   const double* k1_partials = nullptr;
-  const double* prev_partials = nullptr;
-  int k1_G = 0, prev_G = 0, prev_nvp = 0, prev_ngram = 0;
+  int k1_G = 0;
+  const double* prev_ng = nullptr;
+  int prev_ng_G = 0, prev_ng_ld = 0, prev_ng_off = 0, prev_ngram = 0;
+  const double* prev_sk = nullptr;
+  int prev_sk_G = 0, prev_sk_ld = 0, sk_row = 0;
 };
 
 /// Sketch row q from CTA-major tile partials [G][nvp]: lane-strided sums over
@@ -314,103 +320,120 @@ __device__ __forceinline__ void sketch_row_fold(const double* __restrict__ parti
   }
 }
 
+
+/// Deferred-pipeline prologue of an update kernel (NT threads per CTA, every
+/// CTA): folds K1's window dots and column j's norm / Gram in the same fixed
+/// order in every CTA, folds a pending set of sketch rows (spread over all
+/// warps of the grid), forms the MGS coefficients into coef[0..MAXT]; CTA 0
+/// writes record rows j+1 (A, H), j (norm / Gram) and cvec[j].
+template <int MAXT, int NT>
+__device__ __forceinline__ void deferred_prologue(const UpdateArgs& ua, int s, const double2* __restrict__ tab,
+                                                  const double* __restrict__ row_scale, double* coef) {
+  __shared__ double red[2 * MAXT + 1][NT / 32];
+  __shared__ double sA[MAXT + 1], sB[MAXT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x, G = gridDim.x;
+  const int nA = 1 + ua.nwin;
+  const bool prev = ua.prev_ng != nullptr;
+  double a[MAXT + 1], bs[MAXT];
+#pragma unroll
+  for (int v = 0; v <= MAXT; ++v) a[v] = 0.0;
+#pragma unroll
+  for (int v = 0; v < MAXT; ++v) bs[v] = 0.0;
+  for (int bb = tid; bb < ua.k1_G; bb += NT)
+#pragma unroll
+    for (int v = 0; v <= MAXT; ++v)
+      if (v < nA) a[v] += __ldcg(ua.k1_partials + static_cast<int64_t>(v) * ua.k1_G + bb);
+  if (prev)
+    for (int bb = tid; bb < ua.prev_ng_G; bb += NT)
+#pragma unroll
+      for (int v = 0; v < MAXT; ++v)
+        bs[v] += __ldcg(ua.prev_ng + static_cast<int64_t>(bb) * ua.prev_ng_ld + ua.prev_ng_off + v);
+#pragma unroll
+  for (int v = 0; v <= MAXT; ++v) {
+    const double r = warp_sum(a[v]);
+    if (lane == 0) red[v][warp] = r;
+  }
+#pragma unroll
+  for (int v = 0; v < MAXT; ++v) {
+    const double r = warp_sum(bs[v]);
+    if (lane == 0) red[MAXT + 1 + v][warp] = r;
+  }
+  const int64_t R = ua.rstride;
+  const int b_off = 2 * ua.T + 3;
+  if (ua.prev_sk) {
+    double* dst = ua.rec + static_cast<int64_t>(ua.sk_row) * R + b_off + ua.T;
+    for (int q = b * (NT / 32) + warp; q < s; q += G * (NT / 32))
+      sketch_row_fold(ua.prev_sk, ua.prev_sk_G, ua.prev_sk_ld, q, lane, s, tab, row_scale, dst);
+  }
+  __syncthreads();
+  if (tid < 2 * MAXT + 1) {
+    double r = 0.0;
+    for (int w = 0; w < NT / 32; ++w) r += red[tid][w];
+    if (tid <= MAXT) sA[tid] = r;
+    else sB[tid - MAXT - 1] = (tid - MAXT - 1 <= ua.prev_ngram) ? r : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mgs_coefficients<MAXT>(ua.rec, R, ua.T, ua.j, ua.nwin, ua.cvec, coef, b == 0, sA, prev ? sB : nullptr);
+    if (b == 0) {
+      double* recA = ua.rec + static_cast<int64_t>(ua.j + 1) * R;
+      for (int v = 0; v < nA; ++v) recA[v] = sA[v];
+      if (prev) {
+        double* recj = ua.rec + static_cast<int64_t>(ua.j) * R + b_off;
+        for (int g2 = 0; g2 < ua.T; ++g2) recj[g2] = g2 < MAXT ? sB[g2] : 0.0;
+      }
+    }
+  }
+}
+
 // Tile-group layout: a CTA of kGroups x 128 threads per SM. Each group of
 // four warps owns its own tiles (8 column pairs x 128 rows), transpose
 // buffer and Horner state and synchronises on its own named barrier, so the
 // groups' load, FFT and accumulation phases interleave on the SM.
 constexpr int kGPairs = 8;                       // column pairs per tile (16 columns)
 constexpr int kGThreads = kGPairs * 16;          // threads per group
-constexpr int kGroups = 4;
-constexpr int kCtaThreads = kGroups * kGThreads; // 512
+constexpr int kGroupsMax = 4;                    // tile groups per CTA (GRP template: 4, or 2 to co-reside)
 
 __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGThreads) : "memory");
 }
 
-template <int SRC, int NI, bool PAIRED, int MAXT>
-__global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, const double* __restrict__ x,
+template <int SRC, int NI, bool PAIRED, int MAXT, int GRP>
+// GRP = 2 runs beside K1 / K2' on the same SMs (split pipeline): <= 85 registers.
+__global__ void __launch_bounds__(GRP * kGThreads, GRP == 2 ? 3 : 1) k_srdct_tiles(TileArgs ta, const double* __restrict__ x,
                                                                  double xscale, double* __restrict__ out,
                                                                  UpdateArgs ua) {
+  constexpr int kCta = GRP * kGThreads;
   extern __shared__ double2 sm[];
   const int s = ta.s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = tid / kGThreads, lt = tid % kGThreads;
   double2* X = sm + g * (kGPairs * kXS);                  // [8][257] per group
-  double2* S1s = sm + kGroups * (kGPairs * kXS) + g * 2 * s;  // [s] per group
+  double2* S1s = sm + GRP * (kGPairs * kXS) + g * 2 * s;  // [s] per group
   double2* S2s = S1s + s;                                  // [s] per group
-  double2* zq = sm + kGroups * (kGPairs * kXS + 2 * s);   // [s]  z = e^{2 i pi k/N}
-  double2* zj = zq + s;                                    // [s]  z^{8 (kGroups - 1)}: jump over the other groups' tiles
+  double2* zq = sm + GRP * (kGPairs * kXS + 2 * s);   // [s]  z = e^{2 i pi k/N}
+  double2* zj = zq + s;                                    // [s]  z^{8 (GRP - 1)}: jump over the other groups' tiles
   double2* tw = zj + s;                                    // [256]
   int* uq = reinterpret_cast<int*>(tw + 256);              // [s]
   __shared__ double coef[MAXT + 1];
-  __shared__ double nred[MAXT][kCtaThreads / 32];
+  __shared__ double nred[MAXT][kCta / 32];
   const int G = gridDim.x, b = blockIdx.x;
   const uint64_t twoN = 2u * static_cast<uint64_t>(ta.N);
   stamp_begin(ta.stamp);
   trace_mark(ta.trace, 0);
-  for (int k = tid; k < 256; k += kCtaThreads) tw[k] = ta.tab[5 * s + k];
-  for (int q = tid; q < s; q += kCtaThreads) {
+  for (int k = tid; k < 256; k += kCta) tw[k] = ta.tab[6 * s + k];
+  for (int q = tid; q < s; q += kCta) {
     zq[q] = ta.tab[2 * s + q];
-    zj[q] = ta.tab[4 * s + q];
+    zj[q] = ta.tab[(GRP == 4 ? 4 : 5) * s + q];
     uq[q] = ta.uq[q];
   }
-  for (int q = tid; q < kGroups * 2 * s; q += kCtaThreads) S1s[q - g * 2 * s] = make_double2(0.0, 0.0);
+  for (int q = tid; q < GRP * 2 * s; q += kCta) S1s[q - g * 2 * s] = make_double2(0.0, 0.0);
   pdl_trigger();
   pdl_wait();  // everything below reads the previous kernels' output
   if constexpr (SRC == kSrcUpdate) {
     if (ua.k1_partials) {
-      // deferred: fold K1's window dots and the previous update's norm / Gram
-      // here (every CTA, same fixed order), the previous sketch rows once
-      // (one warp per row), then the MGS coefficients
-      __shared__ double red[2 * MAXT + 1][kCtaThreads / 32];
-      __shared__ double sA[MAXT + 1], sB[MAXT];
-      const int nA = 1 + ua.nwin;
-      const bool prev = ua.prev_partials != nullptr;
-      double a[MAXT + 1], bs[MAXT];
-#pragma unroll
-      for (int v = 0; v <= MAXT; ++v) a[v] = 0.0;
-#pragma unroll
-      for (int v = 0; v < MAXT; ++v) bs[v] = 0.0;
-      for (int bb = tid; bb < ua.k1_G; bb += kCtaThreads)
-#pragma unroll
-        for (int v = 0; v <= MAXT; ++v)
-          if (v < nA) a[v] += __ldcg(ua.k1_partials + static_cast<int64_t>(v) * ua.k1_G + bb);
-      if (prev)
-        for (int bb = tid; bb < ua.prev_G; bb += kCtaThreads)
-#pragma unroll
-          for (int v = 0; v < MAXT; ++v) bs[v] += __ldcg(ua.prev_partials + static_cast<int64_t>(bb) * ua.prev_nvp + 2 * s + v);
-#pragma unroll
-      for (int v = 0; v <= MAXT; ++v) {
-        const double r = warp_sum(a[v]);
-        if (lane == 0) red[v][warp] = r;
-      }
-#pragma unroll
-      for (int v = 0; v < MAXT; ++v) {
-        const double r = warp_sum(bs[v]);
-        if (lane == 0) red[MAXT + 1 + v][warp] = r;
-      }
-      const int64_t R = ua.rstride;
-      double* recj = ua.rec + static_cast<int64_t>(ua.j) * R + (2 * ua.T + 3);  // column j's B part
-      if (prev)
-        for (int q = b * (kCtaThreads / 32) + warp; q < s; q += G * (kCtaThreads / 32))
-          sketch_row_fold(ua.prev_partials, ua.prev_G, ua.prev_nvp, q, lane, s, ta.tab, ta.row_scale, recj + ua.T);
-      __syncthreads();
-      if (tid < 2 * MAXT + 1) {
-        double r = 0.0;
-        for (int w = 0; w < kCtaThreads / 32; ++w) r += red[tid][w];
-        if (tid <= MAXT) sA[tid] = r;
-        else sB[tid - MAXT - 1] = (tid - MAXT - 1 <= ua.prev_ngram) ? r : 0.0;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        mgs_coefficients<MAXT>(ua.rec, R, ua.T, ua.j, ua.nwin, ua.cvec, coef, b == 0, sA, prev ? sB : nullptr);
-        if (b == 0) {
-          double* recA = ua.rec + static_cast<int64_t>(ua.j + 1) * R;
-          for (int v = 0; v < nA; ++v) recA[v] = sA[v];
-          if (prev)
-            for (int g2 = 0; g2 < ua.T; ++g2) recj[g2] = g2 < MAXT ? sB[g2] : 0.0;
-        }
-      }
+      deferred_prologue<MAXT, kCta>(ua, s, ta.tab, ta.row_scale, coef);
     } else if (ua.coef_ready) {
       if (tid <= MAXT) coef[tid] = tid <= ua.nwin ? ua.coef_ready[tid] : 0.0;
     } else if (tid == 0) {
@@ -435,11 +458,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
   }
   const int p = lt & (kGPairs - 1), t = lt / kGPairs;
   const int nI = NI ? NI : (ta.M >> 4);  // <= 8 nonzero stage-1 inputs
-  // CTA b owns tiles [tb, te); group g takes te-1-g, te-1-g-kGroups, ... (descending)
+  // CTA b owns tiles [tb, te); group g takes te-1-g, te-1-g-GRP, ... (descending)
   const int64_t tb = static_cast<int64_t>(b) * ta.ntiles / G, te = static_cast<int64_t>(b + 1) * ta.ntiles / G;
   int64_t tlow = -1;
 
-  for (int64_t tile = te - 1 - g; tile >= tb; tile -= kGroups) {
+  for (int64_t tile = te - 1 - g; tile >= tb; tile -= GRP) {
     const int64_t aa = tile * (2 * kGPairs) + 2 * p;
     double2 v[16];
 #pragma unroll
@@ -526,7 +549,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
     for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
     group_sync(g);
     // Horner over the tile's 8 pairs, continuing the group's recurrence;
-    // the first step also jumps over the kGroups - 1 tiles in between
+    // the first step also jumps over the GRP - 1 tiles in between
     const bool first = tlow < 0;
     for (int q = lt; q < s; q += kGThreads) {
       const int u = uq[q], um = (256 - u) & 255;
@@ -551,7 +574,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
   }
   // publish each group's lowest tile, then combine the groups per row:
   // sum_g e^{i pi k (r0 + 16 tlow_g)/N} (g_alpha S1_g + g_beta S2_g)
-  __shared__ int64_t glow[kGroups];
+  __shared__ int64_t glow[GRP];
   if (lt == 0) glow[g] = tlow;
   if constexpr (SRC == kSrcUpdate) {
 #pragma unroll
@@ -567,13 +590,13 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
   // L2 request: a multi-µs tail)
   const int nv = 2 * s + (SRC == kSrcUpdate ? MAXT : 0);
   const int nvp = (nv + 1) & ~1;
-  for (int q = tid; q < s; q += kCtaThreads) {
+  for (int q = tid; q < s; q += kCta) {
     const uint64_t k = static_cast<uint64_t>(ta.rows[q]);
     const double2 ga = ta.tab[q], gb = ta.tab[s + q];
     double2 acc = make_double2(0.0, 0.0);
-    for (int gg = 0; gg < kGroups; ++gg) {
+    for (int gg = 0; gg < GRP; ++gg) {
       if (glow[gg] < 0) continue;
-      const double2* S = sm + kGroups * (kGPairs * kXS) + gg * 2 * s;
+      const double2* S = sm + GRP * (kGPairs * kXS) + gg * 2 * s;
       double sn, cs;
       const uint64_t ph = (k * static_cast<uint64_t>(ta.r0 + glow[gg] * 2 * kGPairs)) % twoN;
       sincospi(static_cast<double>(ph) / static_cast<double>(ta.N), &sn, &cs);
@@ -584,7 +607,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_srdct_tiles(TileArgs ta, con
   if constexpr (SRC == kSrcUpdate) {
     if (tid < MAXT) {
       double v = 0.0;
-      for (int w = 0; w < kCtaThreads / 32; ++w) v += nred[tid][w];
+      for (int w = 0; w < kCta / 32; ++w) v += nred[tid][w];
       ta.partials[static_cast<int64_t>(b) * nvp + 2 * s + tid] = v;
     }
   }
@@ -618,8 +641,111 @@ __global__ void __launch_bounds__(256) k_srdct_fold(const double* __restrict__ p
   }
 }
 
+// ----------------------------------------- split step pipeline (one GPU)
+// K2' = the Arnoldi update alone (HBM streaming, deferred prologue); the
+// SRDCT of w_{j+1} runs on a side stream concurrently with K1(j+1) / K2'(j+1)
+// and its partials are folded two steps later (kernels.hpp SplitFold).
+constexpr int kUpdThreads = 256;
+constexpr int kNgLd = 4;  // norm / Gram partial row length (MAXT <= 4)
+
+template <int MAXT>
+__global__ void __launch_bounds__(kUpdThreads) k_update_split(UpdateArgs ua, int s, const double2* __restrict__ tab,
+                                                              const double* __restrict__ row_scale, int64_t npairs,
+                                                              double* __restrict__ partials,
+                                                              unsigned long long* stamp) {
+  stamp_begin(stamp);
+  __shared__ double coef[MAXT + 1];
+  __shared__ double nred[MAXT][kUpdThreads / 32];
+  pdl_trigger();
+  pdl_wait();
+  deferred_prologue<MAXT, kUpdThreads>(ua, s, tab, row_scale, coef);
+  __syncthreads();
+  double cf[MAXT + 1];
+#pragma unroll
+  for (int k = 0; k <= MAXT; ++k) cf[k] = coef[k];
+  const double2* W[MAXT];
+#pragma unroll
+  for (int d = 0; d < MAXT; ++d)
+    W[d] = reinterpret_cast<const double2*>(ua.V + static_cast<int64_t>(ua.j - (d < ua.nwin ? d : 0)) * ua.ldv + ua.own_off);
+  double2* wout = reinterpret_cast<double2*>(ua.V + static_cast<int64_t>(ua.j + 1) * ua.ldv + ua.own_off);
+  const double2* y2 = reinterpret_cast<const double2*>(ua.y);
+  double nacc[MAXT];
+#pragma unroll
+  for (int g = 0; g < MAXT; ++g) nacc[g] = 0.0;
+  constexpr int U = 4;  // pairs in flight per thread
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kUpdThreads;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kUpdThreads + threadIdx.x; i0 < npairs; i0 += U * stride) {
+    double2 yv[U], wv[U][MAXT];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      const bool ok = i < npairs;
+      yv[u] = ok ? __ldcs(y2 + i) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int d = 0; d < MAXT; ++d) wv[u][d] = (ok && d < ua.nwin) ? __ldg(W[d] + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < npairs) {
+        double w0 = cf[0] * yv[u].x, w1 = cf[0] * yv[u].y;
+#pragma unroll
+        for (int d = MAXT - 1; d >= 0; --d)
+          if (d < ua.nwin) {
+            w0 = fma(cf[1 + d], wv[u][d].x, w0);
+            w1 = fma(cf[1 + d], wv[u][d].y, w1);
+          }
+        wout[i] = make_double2(w0, w1);
+        nacc[0] = fma(w0, w0, fma(w1, w1, nacc[0]));
+#pragma unroll
+        for (int g = 1; g < MAXT; ++g)
+          if (g <= ua.ngram) nacc[g] = fma(w0, wv[u][g - 1].x, fma(w1, wv[u][g - 1].y, nacc[g]));
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int g = 0; g < MAXT; ++g) {
+    const double v = warp_sum(nacc[g]);
+    if (lane == 0) nred[g][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kNgLd) {
+    double v = 0.0;
+    if (threadIdx.x < MAXT)
+      for (int w = 0; w < kUpdThreads / 32; ++w) v += nred[threadIdx.x][w];
+    partials[static_cast<int64_t>(blockIdx.x) * kNgLd + threadIdx.x] = v;
+  }
+  stamp_end(stamp);
+}
+
+/// End of a split cycle (no K2' follows step j): folds the pending sketch
+/// partials of columns j (a) and j+1 (b) and K2'(j)'s norm / Gram (row j+1).
+__global__ void __launch_bounds__(256) k_split_flush(const double* __restrict__ ska, int Ga, int lda,
+                                                     const double* __restrict__ skb, int Gb, int ldb,
+                                                     const double* __restrict__ ng, int Gn, int s,
+                                                     const double2* __restrict__ tab,
+                                                     const double* __restrict__ row_scale, double* __restrict__ rec,
+                                                     int64_t rstride, int T, int j, int ngram, int maxt) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int b_off = 2 * T + 3;
+  if (q < s) {
+    if (ska) sketch_row_fold(ska, Ga, lda, q, lane, s, tab, row_scale, rec + static_cast<int64_t>(j) * rstride + b_off + T);
+  } else if (q < 2 * s) {
+    sketch_row_fold(skb, Gb, ldb, q - s, lane, s, tab, row_scale, rec + static_cast<int64_t>(j + 1) * rstride + b_off + T);
+  } else if (q < 2 * s + T) {
+    const int g = q - 2 * s;
+    double a = 0.0;
+    if (g <= ngram && g < maxt)
+      for (int bb = lane; bb < Gn; bb += 32) a += ng[static_cast<int64_t>(bb) * kNgLd + g];
+    a = warp_sum(a);
+    if (lane == 0) rec[static_cast<int64_t>(j + 1) * rstride + b_off + g] = a;
+  }
+}
+
 /// Per-row constants of an SRDCT: g_alpha, g_beta, z = e^{2 i pi k/N},
-/// half-phase e^{i pi k/2N}, the group jump z^{8 (kGroups-1)}, k mod 256, and
+/// half-phase e^{i pi k/2N}, the group jumps z^{8 (GRP-1)}, k mod 256, and
 /// the 256 stage twiddles.
 __global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int s, double2* __restrict__ tab,
                                int* __restrict__ uq) {
@@ -635,15 +761,18 @@ __global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int 
       tab[2 * s + q] = make_double2(cs, sn);
       sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
       tab[3 * s + q] = make_double2(cs, sn);
-      // z^{8 (kGroups - 1)} = e^{2 i pi k 8 (kGroups-1) / N}, exact reduction
-      const uint64_t e = (2 * k * static_cast<uint64_t>(kGPairs * (kGroups - 1))) % twoN;
-      sincospi(static_cast<double>(e) / static_cast<double>(N), &sn, &cs);
-      tab[4 * s + q] = make_double2(cs, sn);
+      // group jumps z^{8 (GRP - 1)} = e^{2 i pi k 8 (GRP-1) / N} for GRP = 4, 2, exact reduction
+      for (int gi = 0; gi < 2; ++gi) {
+        const uint64_t grp = gi == 0 ? 4 : 2;
+        const uint64_t e = (2 * k * static_cast<uint64_t>(kGPairs) * (grp - 1)) % twoN;
+        sincospi(static_cast<double>(e) / static_cast<double>(N), &sn, &cs);
+        tab[(4 + gi) * s + q] = make_double2(cs, sn);
+      }
       uq[q] = static_cast<int>(k & 255);
     } else {
       const int k = q - s;
       sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
-      tab[5 * s + k] = make_double2(cs, sn);
+      tab[6 * s + k] = make_double2(cs, sn);
     }
   }
 }
@@ -688,8 +817,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restri
 namespace {
 
 
-size_t tiles_smem(int64_t s) {
-  return sizeof(double2) * static_cast<size_t>(kGroups * (kGPairs * kXS + 2 * s) + 2 * s + 256) +
+size_t tiles_smem(int64_t s, int grp = kGroupsMax) {
+  return sizeof(double2) * static_cast<size_t>(grp * (kGPairs * kXS + 2 * s) + 2 * s + 256) +
          sizeof(int) * static_cast<size_t>(s);
 }
 
@@ -697,11 +826,11 @@ bool tiles_eligible(const SketchDev& S, const SrdctPlan& p) {
   return p.F == 256 && p.M % 16 == 0 && S.tab.size() > 0 && tiles_smem(S.s) <= 227 * 1024;
 }
 
-template <int SRC, int NI, bool PAIRED, int MAXT>
+template <int SRC, int NI, bool PAIRED, int MAXT, int GRP = kGroupsMax>
 void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctPlan& p, int64_t row_begin,
                   const double* x, double xscale, double* out, const UpdateArgs& ua, StepFold* sf = nullptr) {
   const int64_t ntiles = (p.L + 2 * kGPairs - 1) / (2 * kGPairs);
-  const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((ntiles + kGroups - 1) / kGroups, c.num_sms)));
+  const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((ntiles + GRP - 1) / GRP, c.num_sms)));
   const int64_t nv = (2 * S.s + (SRC == kSrcUpdate ? MAXT : 0) + 1) & ~int64_t{1};
   TileArgs ta;
   ta.N = S.n;
@@ -718,8 +847,8 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   ta.partials = sf ? sf->out_partials : c.partials(nv * G);
   ta.trace = c.trace(16 * static_cast<int64_t>(G));
   ta.stamp = c.launch_stamp(name);
-  const size_t smem = tiles_smem(S.s);
-  auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT>;
+  const size_t smem = tiles_smem(S.s, GRP);
+  auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT, GRP>;
   static size_t configured = 0;
   if (smem > configured) {
     SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -729,7 +858,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
     TimedLaunch t(c, name);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(kCtaThreads);
+    cfg.blockDim = dim3(GRP * kGThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute at[1] = {pdl_attribute()};
@@ -752,7 +881,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
 }  // namespace
 
 void prepare_srdct_tables(Context& c, SketchDev& S) {
-  S.tab.resize(5 * S.s + 256);
+  S.tab.resize(6 * S.s + 256);
   S.uq.resize(S.s);
   k_srdct_tables<<<static_cast<int>((S.s + 256 + 255) / 256), 256, 0, c.stream>>>(S.n, S.rows.get(), static_cast<int>(S.s),
                                                                                  S.tab.get(), S.uq.get());
@@ -791,10 +920,14 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
   if (sf) {
     ua.k1_partials = sf->k1_partials;
     ua.k1_G = sf->k1_G;
-    ua.prev_partials = sf->prev_partials;
-    ua.prev_G = sf->prev_G;
-    ua.prev_nvp = sf->prev_nvp;
-    ua.prev_ngram = sf->prev_ngram;
+    if (sf->prev_partials) {  // the previous fused update's partials hold both norm / Gram and sketch rows
+      ua.prev_ng = ua.prev_sk = sf->prev_partials;
+      ua.prev_ng_G = ua.prev_sk_G = sf->prev_G;
+      ua.prev_ng_ld = ua.prev_sk_ld = sf->prev_nvp;
+      ua.prev_ng_off = 2 * static_cast<int>(S.s);
+      ua.prev_ngram = sf->prev_ngram;
+      ua.sk_row = j;
+    }
   }
   if (need <= 2)
     launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
@@ -816,6 +949,89 @@ void launch_update_sketch_flush(Context& c, const SketchDev& S, const StepFold& 
   k_srdct_fold<kSrcUpdate><<<(nwarps + 7) / 8, 256, 0, c.stream>>>(sf.out_partials, sf.out_G, sf.out_nvp,
                                                                    static_cast<int>(S.s), S.tab.get(), S.row_scale.get(),
                                                                    nullptr, ua, (sf.out_nvp - 2 * static_cast<int>(S.s)));
+  SDR_KERNEL_CHECK();
+}
+
+bool sketch_partials_eligible(const SketchDev& S, int64_t nloc, int64_t row_begin) {
+  if (S.kind != kSrdct) return false;
+  const SrdctPlan p = plan_srdct(S.n, nloc);
+  return tiles_eligible(S, p) && tiles_smem(S.s, 2) <= 100 * 1024 && p.M == 128 && p.L % 2 == 0 && row_begin % 2 == 0;
+}
+
+int64_t sketch_partials_size(const SketchDev& S, int num_sms) { return (2 * S.s + 2) * num_sms; }
+
+void launch_sketch_partials(Context& c, const SketchDev& S, const double* x_own, int64_t nloc, int64_t row_begin,
+                            double* partials, int* G, int* ld) {
+  const SrdctPlan p = plan_srdct(S.n, nloc);
+  StepFold sf;
+  sf.out_partials = partials;
+  // two tile groups (256 threads, ~90 KB shared memory): co-resides with K1 / K2'
+  launch_tiles<kSrcSketch, 8, true, 1, 2>(c, "sketch_side", S, p, row_begin, x_own, 1.0, nullptr, UpdateArgs{}, &sf);
+  *G = sf.out_G;
+  *ld = sf.out_nvp;
+}
+
+int64_t update_split_partials_size(int num_sms) { return static_cast<int64_t>(kNgLd) * num_sms * 8; }
+
+int launch_update_split(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
+                        int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec, const SplitFold& sf) {
+  const int need = std::max(nwin, ngram + 1);
+  if (need > 4 || lay.nloc % 2 || lay.own_off % 2 || ldv % 2)
+    throw invalid("split step pipeline: update needs an even block and a window of at most 4");
+  UpdateArgs ua;
+  ua.y = y;
+  ua.V = V;
+  ua.ldv = ldv;
+  ua.own_off = lay.own_off;
+  ua.rstride = RL.stride;
+  ua.j = j;
+  ua.nwin = nwin;
+  ua.ngram = ngram;
+  ua.T = RL.T;
+  ua.rec = rec;
+  ua.cvec = cvec;
+  ua.k1_partials = sf.k1_partials;
+  ua.k1_G = sf.k1_G;
+  if (sf.prev_ng) {
+    ua.prev_ng = sf.prev_ng;
+    ua.prev_ng_G = sf.prev_ng_G;
+    ua.prev_ng_ld = kNgLd;
+    ua.prev_ng_off = 0;
+    ua.prev_ngram = sf.prev_ngram;
+  }
+  if (sf.prev_sk) {
+    ua.prev_sk = sf.prev_sk;
+    ua.prev_sk_G = sf.prev_sk_G;
+    ua.prev_sk_ld = sf.prev_sk_ld;
+    ua.sk_row = sf.sk_row;
+  }
+  const int64_t npairs = lay.nloc / 2;
+  const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((npairs + kUpdThreads - 1) / kUpdThreads,
+                                                                        static_cast<int64_t>(c.num_sms) * 2)));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kUpdThreads);
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1] = {pdl_attribute()};
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TimedLaunch t(c, "update");
+  if (need <= 2)
+    SDR_CUDA(cudaLaunchKernelEx(&cfg, k_update_split<2>, ua, static_cast<int>(S.s), static_cast<const double2*>(S.tab.get()),
+                                static_cast<const double*>(S.row_scale.get()), npairs, sf.out_ng, c.launch_stamp("update")));
+  else
+    SDR_CUDA(cudaLaunchKernelEx(&cfg, k_update_split<4>, ua, static_cast<int>(S.s), static_cast<const double2*>(S.tab.get()),
+                                static_cast<const double*>(S.row_scale.get()), npairs, sf.out_ng, c.launch_stamp("update")));
+  return G;
+}
+
+void launch_split_flush(Context& c, const SketchDev& S, const double* ska, int Ga, int lda, const double* skb, int Gb,
+                        int ldb, const double* ng, int Gn, double* rec, const RecLayout& RL, int j, int ngram, int maxt) {
+  const int nwarps = 2 * static_cast<int>(S.s) + RL.T;
+  TimedLaunch t(c, "sketch_fold");
+  k_split_flush<<<(nwarps + 7) / 8, 256, 0, c.stream>>>(ska, Ga, lda, skb, Gb, ldb, ng, Gn, static_cast<int>(S.s),
+                                                       S.tab.get(), S.row_scale.get(), rec, RL.stride, RL.T, j, ngram,
+                                                       maxt);
   SDR_KERNEL_CHECK();
 }
 

@@ -38,6 +38,17 @@ constexpr int kLookahead = 2;
 constexpr int kPumpDepth = 3;  // steps kept in flight while the host runs restart bookkeeping
 
 /// SDR_FUSE=0 disables the fused update+sketch kernel (A/B and parity checks).
+/// SDR_SPLIT=1 runs the SRDCT on a side stream beside K1 / K2' (SplitFold).
+/// Off by default: measured on B200 at C2, the co-resident SRDCT CTAs slowed
+/// K1 from 27.5 to 50 us and the step period rose from 52.7 to 55.5 us.
+bool split_pipeline() {
+  static const bool on = [] {
+    const char* e = std::getenv("SDR_SPLIT");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool fuse_update_sketch() {
   static const bool on = [] {
     const char* e = std::getenv("SDR_FUSE");
@@ -56,6 +67,9 @@ struct Workspace {
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
   DeviceBuffer<double> gcoef;      // recycle-update GEMM coefficients
+  DeviceBuffer<double> ps[2], pu[2];  // split pipeline: SRDCT / update partials by step parity
+  cudaStream_t sk_stream = nullptr;   // split pipeline: SRDCT beside K1 / K2'
+  cudaEvent_t ev_sk[2] = {nullptr, nullptr}, ev_u = nullptr, ev_skq = nullptr;
   PinnedBuffer<double> hgcoef;
   DeviceBuffer<const double*> inptr;
   DeviceBuffer<double*> outptr;
@@ -73,6 +87,11 @@ struct Workspace {
   cudaEvent_t ev_side_in = nullptr, ev_side_out = nullptr;
   std::vector<cudaEvent_t> evd;  // K2(j) finished (speculation pump)
   ~Workspace() {
+    for (auto e : ev_sk)
+      if (e) cudaEventDestroy(e);
+    if (ev_u) cudaEventDestroy(ev_u);
+    if (ev_skq) cudaEventDestroy(ev_skq);
+    if (sk_stream) cudaStreamDestroy(sk_stream);
     for (auto e : evd) cudaEventDestroy(e);
     if (ev_side_in) cudaEventDestroy(ev_side_in);
     if (ev_side_out) cudaEventDestroy(ev_side_out);
@@ -149,6 +168,10 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
       SDR_CUDA(cudaEventCreateWithFlags(&w->ev_copies, cudaEventDisableTiming));
       SDR_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
       SDR_CUDA(cudaStreamCreateWithFlags(&w->side_stream, cudaStreamNonBlocking));
+      SDR_CUDA(cudaStreamCreateWithFlags(&w->sk_stream, cudaStreamNonBlocking));
+      for (auto& e : w->ev_sk) SDR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      SDR_CUDA(cudaEventCreateWithFlags(&w->ev_u, cudaEventDisableTiming));
+      SDR_CUDA(cudaEventCreateWithFlags(&w->ev_skq, cudaEventDisableTiming));
       SDR_CUDA(cudaEventCreateWithFlags(&w->ev_side_in, cudaEventDisableTiming));
       SDR_CUDA(cudaEventCreateWithFlags(&w->ev_side_out, cudaEventDisableTiming));
     }
@@ -262,6 +285,8 @@ struct ArnoldiPipeline {
     const RecLayout& RL = w.RL;
     setup_deferred();
     w.fence_copies(c);
+    SDR_CUDA(cudaEventRecord(w.ev_skq, w.sk_stream));  // earlier side-stream sketches are done before reuse
+    SDR_CUDA(cudaStreamWaitEvent(c.stream, w.ev_skq, 0));
     launch_copy_norm(c, r0, w.Vcol(vb, 0), w.lay.nloc, w.rec.get() + RL.b_off());
     launch_sketch(c, S, w.Vcol(vb, 0), w.lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
     c.allreduce_sum(w.rec.get() + RL.b_off(), RL.b_len());
@@ -292,16 +317,23 @@ struct ArnoldiPipeline {
   // deferred-fold pipeline (one GPU, fused update eligible): record row j is
   // completed by K2(j)'s prologue, so its copy follows K2(j); see StepFold
   bool deferred = false;
+  bool split = false;  // deferred + SRDCT on the side stream (SplitFold)
   StepFold last;  // partials K2(issued - 1) left
   i64 last_ngram = 0;
+  int pu_G[2] = {0, 0}, ps_G[2] = {0, 0}, ps_ld[2] = {0, 0};
 
   void setup_deferred() {
     const int need = static_cast<int>(std::max<i64>(std::min(t, m), std::min<i64>(w.RL.T - 1, m) + 1));
     deferred = !c.distributed() && fuse_update_sketch() &&
                update_sketch_eligible(S, w.lay, need, A.row_begin, w.lay.ld);
+    split = deferred && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
     if (!deferred) return;
     w.p1.ensure(34 * static_cast<i64>(c.num_sms) * 8);
     for (auto& b : w.p2) b.ensure(update_sketch_partials_size(S, c.num_sms));
+    if (split) {
+      for (auto& b : w.ps) b.ensure(sketch_partials_size(S, c.num_sms));
+      for (auto& b : w.pu) b.ensure(update_split_partials_size(c.num_sms));
+    }
   }
 
   void enqueue(i64 j) {
@@ -313,6 +345,10 @@ struct ArnoldiPipeline {
     const int ngram = static_cast<int>(std::min<i64>(T - 1, j + 1));
     double* Vb = w.V[vb].get();
     double* recj = w.rec.get() + (j + 1) * R;
+    if (split) {
+      enqueue_split(j, nwin, ngram);
+      return;
+    }
     if (deferred) {
       StepFold sf;
       sf.k1_partials = w.p1.get();
@@ -356,6 +392,65 @@ struct ArnoldiPipeline {
                 w.ev[static_cast<size_t>(j + 1)]);
   }
 
+  /// Split pipeline step (SplitFold): K1(j) and K2'(j) on the compute
+  /// stream, SRDCT(j) of w_{j+1} on the side stream; row j-1 completes here.
+  void enqueue_split(i64 j, int nwin, int ngram) {
+    const VecLayout& lay = w.lay;
+    const RecLayout& RL = w.RL;
+    const i64 R = RL.stride;
+    const int T = RL.T;
+    double* Vb = w.V[vb].get();
+    const int par = static_cast<int>(j & 1);
+    SplitFold sf;
+    sf.k1_partials = w.p1.get();
+    sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
+                                  w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), 2);
+    if (j >= 1) {
+      sf.prev_ng = w.pu[1 - par].get();
+      sf.prev_ng_G = pu_G[1 - par];
+      sf.prev_ngram = static_cast<int>(last_ngram);
+    }
+    if (j >= 2) {  // SRDCT(j-2) -> sketch rows of column j-1
+      SDR_CUDA(cudaStreamWaitEvent(c.stream, w.ev_sk[par], 0));
+      sf.prev_sk = w.ps[par].get();
+      sf.prev_sk_G = ps_G[par];
+      sf.prev_sk_ld = ps_ld[par];
+      sf.sk_row = static_cast<int>(j - 1);
+    }
+    sf.out_ng = w.pu[par].get();
+    pu_G[par] = launch_update_split(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
+                                    w.cvec.get(), sf);
+    last_ngram = ngram;
+    SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
+    // SRDCT(j) of w_{j+1} beside the next steps
+    SDR_CUDA(cudaEventRecord(w.ev_u, c.stream));
+    SDR_CUDA(cudaStreamWaitEvent(w.sk_stream, w.ev_u, 0));
+    std::swap(c.stream, w.sk_stream);
+    launch_sketch_partials(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, w.ps[par].get(), &ps_G[par], &ps_ld[par]);
+    std::swap(c.stream, w.sk_stream);
+    SDR_CUDA(cudaEventRecord(w.ev_sk[par], w.sk_stream));
+    if (j >= 2)  // row j-1 is complete now
+      w.copy_back(c, w.hrec.get() + (j - 1) * R, w.rec.get() + (j - 1) * R, R, w.evk[static_cast<size_t>(j - 1)],
+                  w.ev[static_cast<size_t>(j - 1)]);
+    if (j + 1 == m) flush_split(j);
+  }
+
+  /// Split pipeline: completes rows j and j + 1 when no K2'(j + 1) follows.
+  void flush_split(i64 j) {
+    const i64 R = w.RL.stride;
+    const int par = static_cast<int>(j & 1);
+    SDR_CUDA(cudaStreamWaitEvent(c.stream, w.ev_sk[par], 0));  // SRDCT(j) (and SRDCT(j-1) before it)
+    const bool have_a = j >= 1;
+    launch_split_flush(c, S, have_a ? w.ps[1 - par].get() : nullptr, ps_G[1 - par], ps_ld[1 - par], w.ps[par].get(),
+                       ps_G[par], ps_ld[par], w.pu[par].get(), pu_G[par], w.rec.get(), w.RL, static_cast<int>(j),
+                       static_cast<int>(last_ngram), 4);
+    if (have_a)
+      w.copy_back(c, w.hrec.get() + j * R, w.rec.get() + j * R, R, w.evk[static_cast<size_t>(j)],
+                  w.ev[static_cast<size_t>(j)]);
+    w.copy_back(c, w.hrec.get() + (j + 1) * R, w.rec.get() + (j + 1) * R, R, w.evk[static_cast<size_t>(j + 1)],
+                w.ev[static_cast<size_t>(j + 1)]);
+  }
+
   /// Deferred pipeline: completes row j + 1 when no K2(j + 1) will follow.
   void flush(i64 j) {
     const i64 R = w.RL.stride;
@@ -372,7 +467,7 @@ struct ArnoldiPipeline {
   /// Keep up to kLookahead speculative steps ahead of step j in flight, and
   /// at least two in flight while the host catches up with finished steps.
   void issue_ahead(i64 j) {
-    while (issued < m && issued <= j + kLookahead) enqueue(issued++);
+    while (issued < m && issued <= j + kLookahead + (split ? 1 : 0)) enqueue(issued++);
     poll_done();
     while (issued < m && issued - done_upto < 2) enqueue(issued++);
   }

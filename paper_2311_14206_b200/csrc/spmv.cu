@@ -182,8 +182,9 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
 }
 
 template <class K>
-int resident_grid(const Context& c, K kernel, int64_t want_blocks) {
-  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), kThreads, 0);
+int resident_grid(const Context& c, K kernel, int64_t want_blocks, int max_per_sm = 0) {
+  int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), kThreads, 0);
+  if (max_per_sm > 0) per_sm = std::min(per_sm, max_per_sm);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_blocks, static_cast<int64_t>(c.num_sms) * per_sm)));
 }
 
@@ -192,9 +193,9 @@ int64_t blocks_for(int64_t nslices) { return (nslices + (kThreads / 32) - 1) / (
 template <int MODE, int NV, int FMT>
 int launch_impl(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
                 int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
-                const MgsArgs& mg, double* partials_out) {
+                const MgsArgs& mg, double* partials_out, int max_per_sm) {
   auto kern = k_sell_spmv<MODE, NV, FMT>;
-  const int g = resident_grid(c, kern, blocks_for(A.nslices));
+  const int g = resident_grid(c, kern, blocks_for(A.nslices), max_per_sm);
   double* part = partials_out ? partials_out : (MODE ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
   TimedLaunch t(c, name);
   if (partials_out) {  // deferred step pipeline: programmatic dependent launch
@@ -218,8 +219,8 @@ int launch_impl(Context& c, const char* name, const SellView& A, const double* x
 template <int MODE, int NV>
 int launch_fmt(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
                int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
-               const MgsArgs& mg, double* partials_out = nullptr) {
-#define SDR_SPMV_FMT(F) return launch_impl<MODE, NV, F>(c, name, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, counter, out, mg, partials_out)
+               const MgsArgs& mg, double* partials_out = nullptr, int max_per_sm = 0) {
+#define SDR_SPMV_FMT(F) return launch_impl<MODE, NV, F>(c, name, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, counter, out, mg, partials_out, max_per_sm)
   if (!A.doff)
     SDR_SPMV_FMT(0);
   else if (A.dia_d == 7)  // 3-D 7-point stencils
@@ -240,18 +241,18 @@ void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) 
 
 int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
-                        double* coef, double* partials_out) {
+                        double* coef, double* partials_out, int max_per_sm) {
   const MgsArgs mg{rec, rstride, T, cvec, coef};
   const double* x_ext = V + j * ldv + lay.ext_shift();
   if (nwin <= 3)
     return launch_fmt<1, 4>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0,
-                            recA, mg, partials_out);
+                            recA, mg, partials_out, max_per_sm);
   else if (nwin <= 7)
     return launch_fmt<1, 8>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0,
-                            recA, mg, partials_out);
+                            recA, mg, partials_out, max_per_sm);
   else if (nwin <= 33)
     return launch_fmt<1, 34>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin,
-                             c.counters() + 0, recA, mg, partials_out);
+                             c.counters() + 0, recA, mg, partials_out, max_per_sm);
   else
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
 }
