@@ -125,6 +125,7 @@ def kernel_bytes(N, a_bytes, t, sketch):
     return {
         "spmv_arnoldi": a_bytes + 8 * N * (2 + (t - 1)),          # A, x, y write, t-1 window reads
         "update": 8 * N * (1 + t) + 8 * N,                        # y + t window reads, w write
+        "update_sketch": 8 * N * (1 + t) + 8 * N + N // 8,        # fused update + SRDCT: the update's bytes (+ sign bits)
         "sketch": 8 * N + (N // 8 if sketch == "srdct" else 0),  # one read of w (+ sign bits)
     }
 
@@ -288,8 +289,9 @@ def main():
     ctx.timing_reset()
     rt = one(b_dev)
     ctx.synchronize()
-    ktimes = {k: ctx.timing(k) for k in ("spmv_arnoldi", "update", "sketch", "update_sketch", "tallskinny", "correction", "residual", "copy_norm",
-                                         "allreduce", "halo", "axpy")}
+    ktimes = {k: ctx.timing(k) for k in ("spmv_arnoldi", "update", "sketch", "update_sketch", "sketch_fold", "sketch_side",
+                                         "tallskinny", "recycle_gemm", "col_norms", "correction", "residual",
+                                         "copy_norm", "allreduce", "halo", "axpy")}
     ctx.set_timing(False)
     kb = kernel_bytes(nloc, A.storage["bytes"], wl["t"], wl["sketch"])
     peak, peak_kind = measured_peak()
