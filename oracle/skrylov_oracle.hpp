@@ -478,8 +478,10 @@ class SketchOperator {
   /// NEW — sparse sign embedding, block (Kane–Nelson) construction. Rows are
   /// split into ζ contiguous blocks [⌊l·s/ζ⌋, ⌊(l+1)·s/ζ⌋); column j holds
   /// exactly one nonzero ±1/√ζ in each block (so ζ distinct rows). With
-  /// key = Rng(seed).next_u64() and h = mix64(key + (j·ζ + l + 1)·φ64):
-  ///   row = block_begin + ((h >> 32) · block_size) >> 32,  sign = h & 1 ? +1 : −1.
+  /// key = Rng(seed).next_u64(), nc = ⌈ζ/4⌉ and, for the chunk c = ⌊l/4⌋,
+  /// h = mix64(key + (j·nc + c + 1)·φ64), entry l takes the 16-bit field
+  /// f = h >> 16·(l mod 4):
+  ///   row = block_begin + (((f >> 1) & 0x7FFF) · block_size) >> 15,  sign = f & 1 ? +1 : −1.
   static SketchOperator sparse_sign(Index n, Index s, std::uint64_t seed, Index zeta) {
     if (n < 1 || s < 1 || zeta < 1 || zeta > s)
       throw std::invalid_argument("SketchOperator::sparse_sign: need n >= 1 and 1 <= zeta <= s, got n = " +
@@ -507,13 +509,14 @@ class SketchOperator {
 
   /// (row, sign) of entry l of column j of the sparse-sign map.
   void sparse_entry(Index j, Index l, Index* row, double* sign) const {
+    const std::uint64_t nc = static_cast<std::uint64_t>((zeta_ + 3) / 4);
     const std::uint64_t h = detail::mix64(
-        key_ + (static_cast<std::uint64_t>(j) * static_cast<std::uint64_t>(zeta_) +
-                static_cast<std::uint64_t>(l) + 1u) * 0x9E3779B97F4A7C15ull);
+        key_ + (static_cast<std::uint64_t>(j) * nc + static_cast<std::uint64_t>(l / 4) + 1u) * 0x9E3779B97F4A7C15ull);
+    const std::uint32_t f = static_cast<std::uint32_t>(h >> (16 * (l % 4))) & 0xFFFFu;
     const Index b0 = (l * s_) / zeta_, b1 = ((l + 1) * s_) / zeta_;
     const std::uint64_t bs = static_cast<std::uint64_t>(b1 - b0);
-    *row = b0 + static_cast<Index>(((h >> 32) * bs) >> 32);
-    *sign = (h & 1u) ? 1.0 : -1.0;
+    *row = b0 + static_cast<Index>((static_cast<std::uint64_t>((f >> 1) & 0x7FFFu) * bs) >> 15);
+    *sign = (f & 1u) ? 1.0 : -1.0;
   }
 
   void apply(const double* x, Index xlen, double* out) const {  // sketch.hpp:139-162

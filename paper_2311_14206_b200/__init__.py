@@ -47,7 +47,7 @@ STATUS = {0: "converged", 1: "max_restarts", 2: "breakdown", 3: "diverged"}
 VARIANT = {"reuse": 0, "exact": 1, "inexact": 2}
 PROVENANCE = {0: "empty", 1: "fresh", 2: "reused", 3: "exact-resketch", 4: "inexact-carryover"}
 PROVENANCE_ID = {v: k for k, v in PROVENANCE.items()}
-PHASES = ("setup", "cycle_init", "step_wait", "host_step", "check", "drain", "basis_cond", "recycle",
+PHASES = ("setup", "cycle_init", "step_wait", "host_step", "check", "drain", "basis_cond", "recycle", "qr_append", "ls_solve",
           "recycle_harmonic")
 
 

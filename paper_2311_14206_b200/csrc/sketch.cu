@@ -24,6 +24,7 @@
 #include "sketch.hpp"
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace sdr {
 
@@ -399,9 +400,9 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGThreads) : "memory");
 }
 
-template <int SRC, int NI, bool PAIRED, int MAXT, int GRP>
-// GRP = 2 runs beside K1 / K2' on the same SMs (split pipeline): <= 85 registers.
-__global__ void __launch_bounds__(GRP * kGThreads, GRP == 2 ? 3 : 1) k_srdct_tiles(TileArgs ta, const double* __restrict__ x,
+template <int SRC, int NI, bool PAIRED, int MAXT, int GRP, int CHK = 0>
+// GRP = 2 sketches run beside K1 / K2' on the same SMs (split pipeline): <= 85 registers.
+__global__ void __launch_bounds__(GRP * kGThreads, (GRP == 2 && SRC == kSrcSketch) ? 3 : 1) k_srdct_tiles(TileArgs ta, const double* __restrict__ x,
                                                                  double xscale, double* __restrict__ out,
                                                                  UpdateArgs ua) {
   constexpr int kCta = GRP * kGThreads;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(GRP * kGThreads, GRP == 2 ? 3 : 1) k_srdct_til
     if (aa < ta.L) {
       if constexpr (SRC == kSrcUpdate) {
         // loads in chunks of CH rows, all issued before the chunk's math
-        constexpr int CH = MAXT <= 2 ? 2 : 1;
+        constexpr int CH = CHK > 0 ? CHK : (MAXT <= 2 ? 2 : 1);
 #pragma unroll
         for (int i0 = 0; i0 < 8; i0 += CH) {
           double2 yv[CH], wv[CH][MAXT];
@@ -777,6 +778,121 @@ __global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int 
   }
 }
 
+// Sparse sign, one warp per CTA: each lane owns a private column of the
+// warp's [s][32] shared bins, so the ζ scatter-adds per element need neither
+// atomics nor ordering; one hash serves four entries. CTA partials (row
+// sums over lanes, CTA-major) are folded by k_sparse_fold in a fixed order.
+template <int ZETA>  // 0: runtime zeta (<= 64)
+__global__ void __launch_bounds__(32) k_sparse_sign_lanes(const double* __restrict__ x, double xscale, int64_t nloc,
+                                                          int64_t r0, uint64_t key, int s, int zeta_rt,
+                                                          double* __restrict__ partials) {
+  extern __shared__ double bins[];  // [s][32]
+  __shared__ int b0s[64], bss[64];
+  const int zeta = ZETA ? ZETA : zeta_rt;
+  const int lane = threadIdx.x;
+  for (int i = lane; i < s * 32; i += 32) bins[i] = 0.0;
+  for (int l = lane; l < zeta; l += 32) {
+    b0s[l] = static_cast<int>((static_cast<int64_t>(l) * s) / zeta);
+    bss[l] = static_cast<int>((static_cast<int64_t>(l + 1) * s) / zeta) - b0s[l];
+  }
+  __syncwarp();
+  constexpr int NCH = ZETA ? (ZETA + 3) / 4 : 16;
+  int b0r[ZETA ? ZETA : 1], bsr[ZETA ? ZETA : 1];
+  if constexpr (ZETA > 0) {
+#pragma unroll
+    for (int l = 0; l < ZETA; ++l) {
+      b0r[l] = b0s[l];
+      bsr[l] = bss[l];
+    }
+  }
+  const uint64_t nc = static_cast<uint64_t>(sparse_sign_chunks(zeta));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * 32;
+  if constexpr (ZETA > 0) {
+    // UE elements per lane per iteration, loaded one iteration ahead: the
+    // hash chains of the UE elements overlap each other and the loads
+    constexpr int UE = 4;
+    const int64_t step = UE * stride;
+    int64_t j0 = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+    double vn[UE];
+#pragma unroll
+    for (int u = 0; u < UE; ++u) vn[u] = j0 + u * stride < nloc ? __ldcs(x + j0 + u * stride) : 0.0;
+    for (; j0 < nloc; j0 += step) {
+      double v[UE];
+#pragma unroll
+      for (int u = 0; u < UE; ++u) {
+        v[u] = vn[u] * xscale;
+        const int64_t jn = j0 + step + u * stride;
+        vn[u] = jn < nloc ? __ldcs(x + jn) : 0.0;
+      }
+      int row[UE][ZETA];
+      double sv[UE][ZETA];
+#pragma unroll
+      for (int u = 0; u < UE; ++u) {
+        const uint64_t jg = static_cast<uint64_t>(r0 + j0 + u * stride);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const uint64_t h = mix64(key + (jg * nc + static_cast<uint64_t>(c) + 1u) * kPhi64);
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const int l = 4 * c + e4;
+            if (l < ZETA) {
+              const uint32_t f = static_cast<uint32_t>(h >> (16 * e4)) & 0xFFFFu;
+              row[u][l] = (b0r[l] + static_cast<int>(((f >> 1) & 0x7FFFu) * static_cast<uint32_t>(bsr[l]) >> 15)) * 32 + lane;
+              sv[u][l] = (f & 1u) ? v[u] : -v[u];  // elements past the end carry v = 0
+            }
+          }
+        }
+      }
+      // a column's ZETA rows lie in distinct blocks: its read-modify-writes
+      // touch distinct bins; consecutive elements go one after the other
+#pragma unroll
+      for (int u = 0; u < UE; ++u) {
+        double t[ZETA];
+#pragma unroll
+        for (int l = 0; l < ZETA; ++l) t[l] = bins[row[u][l]];
+#pragma unroll
+        for (int l = 0; l < ZETA; ++l) bins[row[u][l]] = t[l] + sv[u][l];
+      }
+    }
+  } else {
+    for (int64_t jl = static_cast<int64_t>(blockIdx.x) * 32 + lane; jl < nloc; jl += stride) {
+      const double v = __ldcs(x + jl) * xscale;
+      const uint64_t jg = static_cast<uint64_t>(r0 + jl);
+      for (int c = 0; c < static_cast<int>(nc); ++c) {
+        const uint64_t h = mix64(key + (jg * nc + static_cast<uint64_t>(c) + 1u) * kPhi64);
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const int l = 4 * c + e4;
+          if (l < zeta) {
+            const uint32_t f = static_cast<uint32_t>(h >> (16 * e4)) & 0xFFFFu;
+            const int row = b0s[l] + static_cast<int>(((f >> 1) & 0x7FFFu) * static_cast<uint32_t>(bss[l]) >> 15);
+            bins[row * 32 + lane] += (f & 1u) ? v : -v;
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  for (int r = lane; r < s; r += 32) {
+    double acc = 0.0;
+    for (int e = 0; e < 32; ++e) acc += bins[r * 32 + e];
+    partials[static_cast<int64_t>(blockIdx.x) * s + r] = acc;
+  }
+}
+
+/// out[r] = inv_sqrt_zeta * sum_b partials[b][r]: one warp per row, lane-
+/// strided sums then a fixed xor tree.
+__global__ void __launch_bounds__(256) k_sparse_fold(const double* __restrict__ partials, int G, int s,
+                                                     double inv_sqrt_zeta, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= s) return;
+  double a = 0.0;
+  for (int b = lane; b < G; b += 32) a += partials[static_cast<int64_t>(b) * s + r];
+  a = warp_sum(a);
+  if (lane == 0) out[r] = a * inv_sqrt_zeta;
+}
+
 __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restrict__ x, double xscale, int64_t nloc,
                                                            int64_t r0, uint64_t key, int s, int zeta, double inv_sqrt_zeta,
                                                            int64_t chunk, double* __restrict__ partials,
@@ -826,7 +942,7 @@ bool tiles_eligible(const SketchDev& S, const SrdctPlan& p) {
   return p.F == 256 && p.M % 16 == 0 && S.tab.size() > 0 && tiles_smem(S.s) <= 227 * 1024;
 }
 
-template <int SRC, int NI, bool PAIRED, int MAXT, int GRP = kGroupsMax>
+template <int SRC, int NI, bool PAIRED, int MAXT, int GRP = kGroupsMax, int CHK = 0>
 void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctPlan& p, int64_t row_begin,
                   const double* x, double xscale, double* out, const UpdateArgs& ua, StepFold* sf = nullptr) {
   const int64_t ntiles = (p.L + 2 * kGPairs - 1) / (2 * kGPairs);
@@ -848,7 +964,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   ta.trace = c.trace(16 * static_cast<int64_t>(G));
   ta.stamp = c.launch_stamp(name);
   const size_t smem = tiles_smem(S.s, GRP);
-  auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT, GRP>;
+  auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT, GRP, CHK>;
   static size_t configured = 0;
   if (smem > configured) {
     SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -929,7 +1045,17 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
       ua.sk_row = j;
     }
   }
-  if (need <= 2)
+  static const int variant = [] {
+    const char* e = std::getenv("SDR_K2_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (need <= 2 && variant == 1)
+    launch_tiles<kSrcUpdate, 8, true, 2, 4, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  else if (need <= 2 && variant == 2)
+    launch_tiles<kSrcUpdate, 8, true, 2, 2, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  else if (need <= 2 && variant == 3)
+    launch_tiles<kSrcUpdate, 8, true, 2, 2, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  else if (need <= 2)
     launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
   else
     launch_tiles<kSrcUpdate, 8, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
@@ -1072,6 +1198,28 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
     return;
   }
   // sparse sign
+  const size_t lane_smem = sizeof(double) * 32 * static_cast<size_t>(S.s);
+  if (lane_smem <= 48 * 1024 && S.zeta <= 64) {
+    const int per_sm = static_cast<int>(std::max<size_t>(1, (200 * 1024) / (lane_smem + 1024)));
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>((nloc + 255) / 256, static_cast<int64_t>(c.num_sms) * std::min(per_sm, 16))));
+    double* part = c.partials(static_cast<int64_t>(grid) * S.s);
+    {
+      TimedLaunch t(c, "sketch");
+      if (S.zeta == 8)
+        k_sparse_sign_lanes<8><<<grid, 32, lane_smem, c.stream>>>(x_own, xscale, nloc, row_begin, S.key,
+                                                                  static_cast<int>(S.s), 8, part);
+      else
+        k_sparse_sign_lanes<0><<<grid, 32, lane_smem, c.stream>>>(x_own, xscale, nloc, row_begin, S.key,
+                                                                  static_cast<int>(S.s), static_cast<int>(S.zeta), part);
+      SDR_KERNEL_CHECK();
+    }
+    TimedLaunch t(c, "sketch_fold");
+    k_sparse_fold<<<static_cast<int>((S.s + 7) / 8), 256, 0, c.stream>>>(
+        part, grid, static_cast<int>(S.s), 1.0 / std::sqrt(static_cast<double>(S.zeta)), out);
+    SDR_KERNEL_CHECK();
+    return;
+  }
   const int64_t want = (nloc + 1023) / 1024;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4 * c.num_sms)));
   const int64_t chunk = round_up((nloc + grid - 1) / grid, 32);

@@ -23,16 +23,23 @@ __host__ __device__ inline std::uint64_t mix64(std::uint64_t z) {
 }
 constexpr std::uint64_t kPhi64 = 0x9E3779B97F4A7C15ull;
 
+/// Hashes per column of the sparse-sign map: four 16-bit entry fields each.
+__host__ __device__ inline std::int64_t sparse_sign_chunks(std::int64_t zeta) { return (zeta + 3) / 4; }
+
 /// (row, sign) of nonzero l of column j of the sparse-sign map (block
 /// construction: one nonzero per row block [l*s/zeta, (l+1)*s/zeta)).
+/// Entries 4c..4c+3 of column j share h_c = mix64(key + (j*nc + c + 1)*phi),
+/// nc = ceil(zeta/4); entry l uses the 16-bit field f = h_c >> 16*(l mod 4):
+/// sign = f & 1 ? +1 : -1, row = b0 + (((f >> 1) & 0x7FFF) * bsize) >> 15.
+/// Must stay identical to oracle/skrylov_oracle.hpp SketchOperator::sparse_entry.
 __host__ __device__ inline void sparse_sign_entry(std::uint64_t key, std::int64_t s, std::int64_t zeta, std::int64_t j,
                                                   std::int64_t l, std::int64_t* row, bool* positive) {
-  const std::uint64_t h =
-      mix64(key + (static_cast<std::uint64_t>(j) * static_cast<std::uint64_t>(zeta) + static_cast<std::uint64_t>(l) + 1u) *
-                      kPhi64);
+  const std::uint64_t nc = static_cast<std::uint64_t>(sparse_sign_chunks(zeta));
+  const std::uint64_t h = mix64(key + (static_cast<std::uint64_t>(j) * nc + static_cast<std::uint64_t>(l / 4) + 1u) * kPhi64);
+  const std::uint32_t f = static_cast<std::uint32_t>(h >> (16 * (l % 4))) & 0xFFFFu;
   const std::int64_t b0 = (l * s) / zeta, b1 = ((l + 1) * s) / zeta;
-  *row = b0 + static_cast<std::int64_t>(((h >> 32) * static_cast<std::uint64_t>(b1 - b0)) >> 32);
-  *positive = (h & 1u) != 0;
+  *row = b0 + static_cast<std::int64_t>((static_cast<std::uint64_t>((f >> 1) & 0x7FFFu) * static_cast<std::uint64_t>(b1 - b0)) >> 15);
+  *positive = (f & 1u) != 0;
 }
 
 /// Host-side generator state, reproducing SketchOperator::subsampled_dct

@@ -759,13 +759,18 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
     const bool step_breakdown = ap.step(cnt);
     PhaseTimer pt_step(rep, "host_step");
     const i64 jj = st.j;
+    std::optional<PhaseTimer> pt_qr(std::in_place, rep, "qr_append");
     const auto info = qr->append(st.SAV.col(jj - 1), s);
+    pt_qr.reset();
     if (info.rank_deficient) {
       qr->exclude(info.column);
       rep.notes.push_back("cycle " + std::to_string(cycle_index) + ", step " + std::to_string(jj) +
                           ": sketched basis column rank-deficient; excluded from the least-squares problem");
     }
-    sres = qr->solve_cached(y.data());
+    {
+      PhaseTimer pt_ls(rep, "ls_solve");
+      sres = qr->solve_cached(y.data());
+    }
     const i64 p = qr->cols();
     const i64 global_iter = iteration_base + jj;
     rep.sketched.emplace_back(global_iter, sres);

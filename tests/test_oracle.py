@@ -179,6 +179,12 @@ def test_sparse_sign_properties(O):
     assert np.linalg.norm(S.apply(2 * x - y) - (2 * S.apply(x) - S.apply(y))) <= 1e-13 * np.linalg.norm(S.apply(x))
     r = np.mean([np.sum(O.SketchOperator.sparse_sign(n, s, 100 + i, z).apply(x) ** 2) for i in range(40)])
     assert abs(r / np.sum(x ** 2) - 1.0) < 0.1
+    # rows within a block and signs are uniform (15-bit fields: bias <= 15/32768)
+    big = O.SketchOperator.sparse_sign(60000, s, 11, z)
+    rows, signs = big.sparse_entries(0, 60000, z)
+    counts = np.bincount((rows[:, 3] - (3 * s) // z).ravel(), minlength=s // z)
+    assert counts.min() > 0.9 * counts.mean() and counts.max() < 1.1 * counts.mean()
+    assert abs(np.mean(signs)) < 0.02
 
 
 # ----------------------------------------------------------------- arnoldi

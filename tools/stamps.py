@@ -43,3 +43,8 @@ st = np.array([a for n, a, e in rows if n == "spmv_arnoldi"])
 d = np.diff(st) / 1e3
 print(f"  step period (K1 start to next K1 start): median {np.median(d):.2f} us  (n={len(d)}, cycle restarts excluded: "
       f"{np.median(d[d < 200]):.2f})")
+# GPU idle between consecutive stamped launches (K1/K2/sketch only; boundaries also run unstamped kernels)
+idle = sum(max(0, a1 - e0) for (n0, a0, e0), (n1, a1, e1) in zip(rows, rows[1:])) / 1e6
+print(f"  idle between stamped launches: {idle:.2f} ms of a {(rows[-1][2]-rows[0][1])/1e6:.2f} ms span")
+big = sorted(((a1 - e0) / 1e3, n0, n1, (a1 - t0) / 1e3) for (n0, a0, e0), (n1, a1, e1) in zip(rows, rows[1:]))[-8:]
+print("  largest gaps (us, after, before, at us):", [(round(g), x, y, round(t)) for g, x, y, t in big])
