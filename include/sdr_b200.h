@@ -128,6 +128,9 @@ SDR_API int sdr_sketch_apply(sdr_ctx* ctx, const sdr_sketch* S, const double* x,
 
 /* -------------------------------------------------------- host pieces -- */
 SDR_API int sdr_gaussian_vector(int64_t n, uint64_t seed, double* out);
+/* Rng(seed).uniform() stream (rng.hpp:32): (engine() >> 11) * 2^-53, n draws
+ * (the C3 diagonal perturbation of the BASELINE sequence). */
+SDR_API int sdr_uniform_stream(int64_t n, uint64_t seed, double* out);
 /* Host generator behind sdr_sketch_create_srdct: rows (s, sorted) and signs
  * (+1/-1, n; may be NULL) drawn from std::mt19937_64(seed) in the reference
  * order (sketch.hpp:116-119). Needs no GPU. */

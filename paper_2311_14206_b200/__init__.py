@@ -347,6 +347,13 @@ def gaussian_vector(n, seed):
     return out
 
 
+def uniform_stream(seed, n):
+    """Rng(seed).uniform() draws (rng.hpp:32), bit-identical."""
+    out = np.empty(n)
+    _check(_lib.sdr_uniform_stream(n, seed, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
 def srdct_indices(n, s, seed, with_signs=True):
     """(rows, signs) of SketchOperator::subsampled_dct(n, s, seed), host-side (sketch.hpp:105-122)."""
     rows = np.empty(s, dtype=np.int64)

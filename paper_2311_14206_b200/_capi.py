@@ -74,6 +74,7 @@ SIGNATURES = {
     "sdr_sketch_signs": (cint, [vp, vp]),
     "sdr_sketch_apply": (cint, [vp, vp, vp, i64, vp]),
     "sdr_gaussian_vector": (cint, [i64, u64, vp]),
+    "sdr_uniform_stream": (cint, [i64, u64, vp]),
     "sdr_srdct_indices": (cint, [i64, i64, u64, vp, vp]),
     "sdr_sparse_sign_entries": (cint, [i64, u64, i64, i64, i64, vp, vp]),
     "sdr_qr_create": (cint, [i64, i64, f64, P(vp)]),

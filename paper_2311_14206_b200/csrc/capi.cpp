@@ -401,6 +401,15 @@ int sdr_sketch_apply(sdr_ctx* ctx, const sdr_sketch* S, const double* x, int64_t
 }
 
 // -------------------------------------------------------------- host pieces
+int sdr_uniform_stream(int64_t n, uint64_t seed, double* out) {  // rng.hpp:32
+  return guard([&] {
+    if (n < 0) throw invalid("uniform_stream: n must be nonnegative");
+    if (n > 0) need(out, "out");
+    std::mt19937_64 eng(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+  });
+}
+
 int sdr_gaussian_vector(int64_t n, uint64_t seed, double* out) {  // rng.hpp:45-60,87-96
   return guard([&] {
     if (n < 0) throw invalid("gaussian_vector: n must be nonnegative");

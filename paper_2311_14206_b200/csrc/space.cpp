@@ -132,21 +132,33 @@ void refresh_recycle(Context& c, Recycle& sp, const DeviceOperator& A, const Ske
     sp.provenance = 4;
     return;
   }
+  // SAU(:, q) = S (A u_q) for every column: the k products and sketches are
+  // queued back to back (no host round trip per column) and the k sketched
+  // images come back in one copy. u_q = uscale_q * buf[slot_q]: the scale is
+  // applied to the image (A and S are linear), so U is read in place when the
+  // operator needs no halo (one GPU); otherwise through a halo'd staging vector.
   const VecLayout lay = A.layout();
-  DeviceBuffer<double> ubuf(lay.ld), au(std::max<i64>(lay.nloc, 1)), sk(S.s);
-  SDR_CUDA(cudaMemsetAsync(ubuf.get(), 0, sizeof(double) * static_cast<size_t>(lay.ld), c.stream));
-  std::vector<double> h(static_cast<size_t>(S.s));
-  for (i64 q = 0; q < sp.dim(); ++q) {
-    launch_scale_copy(c, sp.uscale[static_cast<size_t>(q)], sp.col(q), ubuf.get() + lay.own_off, lay.nloc);
-    operator_apply(c, A, ubuf.get(), au.get());
+  const i64 k = sp.dim();
+  const bool in_place = lay.halo_lo == 0 && lay.halo_hi == 0 && lay.own_off == 0;
+  DeviceBuffer<double> ubuf(in_place ? 1 : lay.ld), au(std::max<i64>(lay.nloc, 1) * k), sk(S.s * k);
+  if (!in_place) SDR_CUDA(cudaMemsetAsync(ubuf.get(), 0, sizeof(double) * static_cast<size_t>(lay.ld), c.stream));
+  for (i64 q = 0; q < k; ++q) {
+    double* aq = au.get() + q * std::max<i64>(lay.nloc, 1);
+    if (in_place) {
+      launch_spmv(c, A.view(), sp.col(q), aq);
+    } else {
+      launch_scale_copy(c, 1.0, sp.col(q), ubuf.get() + lay.own_off, lay.nloc);
+      operator_apply(c, A, ubuf.get(), aq);
+    }
     if (cnt) ++cnt->matvecs;
-    launch_sketch(c, S, au.get(), lay.nloc, A.row_begin, sk.get());
-    c.allreduce_sum(sk.get(), S.s);
-    SDR_CUDA(cudaMemcpyAsync(h.data(), sk.get(), sizeof(double) * static_cast<size_t>(S.s), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    launch_sketch_scaled(c, S, aq, sp.uscale[static_cast<size_t>(q)], lay.nloc, A.row_begin, sk.get() + q * S.s);
     if (cnt) ++cnt->sketch_applies;
-    std::copy(h.begin(), h.end(), sp.SAU.col(q));
   }
+  c.allreduce_sum(sk.get(), S.s * k);
+  std::vector<double> h(static_cast<size_t>(S.s * k));
+  SDR_CUDA(cudaMemcpyAsync(h.data(), sk.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  for (i64 q = 0; q < k; ++q) std::copy(h.begin() + q * S.s, h.begin() + (q + 1) * S.s, sp.SAU.col(q));
   sp.provenance = 3;
 }
 

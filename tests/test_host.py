@@ -73,6 +73,10 @@ def test_srdct_indices_bit_exact(sk, O, n, s, seed):
     assert np.array_equal(signs, So.signs())
 
 
+def test_uniform_stream_bit_exact(sk, O):
+    assert np.array_equal(sk.uniform_stream(0x3100, 1000), O.uniform_stream(0x3100, 1000))
+
+
 def test_sparse_sign_entries_bit_exact(sk, O):
     So = O.SketchOperator.sparse_sign(10 ** 6, 120, 0x5EED, 8)
     for j0 in (0, 12345, 10 ** 6 - 64):
