@@ -48,7 +48,7 @@ VARIANT = {"reuse": 0, "exact": 1, "inexact": 2}
 PROVENANCE = {0: "empty", 1: "fresh", 2: "reused", 3: "exact-resketch", 4: "inexact-carryover"}
 PROVENANCE_ID = {v: k for k, v in PROVENANCE.items()}
 PHASES = ("setup", "cycle_init", "step_wait", "host_step", "check", "drain", "basis_cond", "recycle", "qr_append", "ls_solve",
-          "recycle_harmonic")
+          "recycle_harmonic", "harmonic_svd", "harmonic_schur", "harmonic_rest")
 
 
 class SdrError(RuntimeError):

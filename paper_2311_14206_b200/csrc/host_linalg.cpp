@@ -1,5 +1,7 @@
 #include "host_linalg.hpp"
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -138,6 +140,12 @@ double HostQR::solve_cached(double* y) {  // incremental_qr.hpp:107-135
   return hnorm(res.data(), s);
 }
 
+bool HostQR::clean() const {
+  for (int st : state_)
+    if (st != 0) return false;
+  return true;
+}
+
 void HostQR::factors(double* Q, double* R) const {
   if (Q) std::copy(q_.begin(), q_.begin() + rows_ * p_, Q);
   if (R)
@@ -190,13 +198,27 @@ double cond2(const HMat& A) {
   return sv.back() > 0.0 ? sv.front() / sv.back() : std::numeric_limits<double>::infinity();
 }
 
-Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_tol) {
+Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_tol, const HMat* Qf, const HMat* Rf) {
   if (!(rank_tol >= 0.0)) throw invalid("truncated_svd: rank_tol must be >= 0");
   if (k < 0) throw invalid("harmonic_pairs: k must be nonnegative");
   if (SW.rows != SAW.rows || SW.cols != SAW.cols) throw invalid("fill_pencil: SW dimensions do not match the decomposition");
   std::vector<double> sv;
   HMat U, V;
-  thin_svd(SAW, sv, &U, &V);
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  if (Qf && Rf && Qf->rows == SAW.rows && Qf->cols == SAW.cols && Rf->rows == SAW.cols && Rf->cols == SAW.cols) {
+    // SAW = Q R: singular values / right vectors of R, left vectors Q U_R
+    HMat UR;
+    thin_svd(*Rf, sv, &UR, &V);
+    U = HMat(SAW.rows, UR.cols);
+    const int m = static_cast<int>(SAW.rows), n = static_cast<int>(UR.cols), kk = static_cast<int>(Qf->cols);
+    const double one = 1.0, zero = 0.0;
+    if (m > 0 && n > 0 && kk > 0)
+      scipy_dgemm_("N", "N", &m, &n, &kk, &one, Qf->a.data(), &m, UR.a.data(), &kk, &zero, U.a.data(), &m, 1, 1);
+  } else {
+    thin_svd(SAW, sv, &U, &V);
+  }
+  const auto t1 = clk::now();
   i64 l = 0;  // recycle.hpp:102-104
   const double cutoff = sv.empty() ? 0.0 : rank_tol * sv[0];
   while (l < static_cast<i64>(sv.size()) && sv[static_cast<size_t>(l)] > cutoff && sv[static_cast<size_t>(l)] > 0.0) ++l;
@@ -226,8 +248,10 @@ Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_to
   std::vector<double> wr(static_cast<size_t>(l)), wi(static_cast<size_t>(l));
   int sdim = 0, info = 0, lwork = 80 * n + 64;
   std::vector<double> work(static_cast<size_t>(lwork));
+  const auto t2 = clk::now();
   scipy_dgees_("V", "N", nullptr, &n, C.a.data(), &n, &sdim, wr.data(), wi.data(), Q.a.data(), &n, work.data(), &lwork,
                nullptr, &info, 1, 1);
+  const auto t3 = clk::now();
   if (info != 0) throw runtime("real_schur: dgees failed with info = " + std::to_string(info));
   std::vector<i64> order(static_cast<size_t>(l));
   std::iota(order.begin(), order.end(), i64{0});
@@ -264,6 +288,11 @@ Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_to
   out.coeffs = HMat(p, ke);
   for (i64 c = 0; c < ke; ++c) hgemv(false, p, l, 1.0, V.a.data(), p, Q.col(c), 0.0, out.coeffs.col(c));
   for (i64 i = 0; i < ke; ++i) out.mu.emplace_back(wr[static_cast<size_t>(i)], wi[static_cast<size_t>(i)]);
+  const auto t4 = clk::now();
+  auto ms = [](clk::duration d) { return std::chrono::duration<double, std::milli>(d).count(); };
+  out.svd_ms = ms(t1 - t0);
+  out.schur_ms = ms(t3 - t2);
+  out.rest_ms = ms(t2 - t1) + ms(t4 - t3);
   return out;
 }
 

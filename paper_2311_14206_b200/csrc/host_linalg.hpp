@@ -14,6 +14,9 @@
 extern "C" {
 void scipy_dgemv_(const char* trans, const int* m, const int* n, const double* alpha, const double* a, const int* lda,
                   const double* x, const int* incx, const double* beta, double* y, const int* incy, size_t);
+void scipy_dgemm_(const char* ta, const char* tb, const int* m, const int* n, const int* k, const double* alpha,
+                  const double* a, const int* lda, const double* b, const int* ldb, const double* beta, double* c,
+                  const int* ldc, size_t, size_t);
 double scipy_ddot_(const int* n, const double* x, const int* incx, const double* y, const int* incy);
 double scipy_dnrm2_(const int* n, const double* x, const int* incx);
 void scipy_dgees_(const char* jobvs, const char* sort, void* select, const int* n, double* a, const int* lda, int* sdim,
@@ -71,6 +74,8 @@ class HostQR {
   void set_rhs(const double* rhs, i64 len);
   double solve_cached(double* y);
   void factors(double* Q, double* R) const;
+  /// No column rank-deficient or excluded: M = Q R holds for all columns.
+  bool clean() const;
 
  private:
   void grow();
@@ -89,8 +94,12 @@ struct Harmonic {
   bool pair_extended = false, rank_limited = false;
   HMat coeffs;
   std::vector<std::complex<double>> mu;
+  double svd_ms = 0.0, schur_ms = 0.0, rest_ms = 0.0;  // host cost breakdown
 };
-Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_tol);
+/// With Q (s x p, orthonormal) and R (p x p) such that SAW = Q R (the cycle's
+/// least-squares factorization), the SVD is taken of R: SAW = (Q U_R) S V^T.
+Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_tol, const HMat* Q = nullptr,
+                          const HMat* R = nullptr);
 
 /// sigma_max / sigma_min of a small dense block (basis_cond, solver.hpp:230-236).
 double cond2(const HMat& A);

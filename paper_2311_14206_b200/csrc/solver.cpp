@@ -239,6 +239,7 @@ struct CycleOut {
   i64 steps = 0;
   bool converged = false, breakdown = false, have_correction = false;
   double safety = 1.0;
+  std::shared_ptr<HostQR> qr;  // the cycle's factorization of [SAU SAV] (reused by the recycle SVD)
 };
 
 struct StepEvent {  // mirrors sdr_iteration_event in the C-ABI
@@ -558,7 +559,8 @@ void host_job_while_pumping(F&& job, const std::function<void()>* pump) {
 /// computes the harmonic pencil (the GPU otherwise idles at every restart).
 void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recycle& sp, i64 k, double rank_tol,
                     Counters& cnt, std::vector<std::string>* notes, Report& rep,
-                    const std::function<void()>* pump = nullptr, bool side_stream = false) {  // recycle.hpp:226-289
+                    const std::function<void()>* pump = nullptr, bool side_stream = false,
+                    const HostQR* qr = nullptr) {  // recycle.hpp:226-289
   const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
   if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
   HMat SAW(s, kh + j), SW(s, kh + j);
@@ -576,11 +578,22 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     host_job_while_pumping(
         [&] {
           const auto t0 = std::chrono::steady_clock::now();
-          hp = harmonic_extract(SAW, SW, k, rank_tol);
+          // SAW = [SAU SAV] is exactly the cycle's least-squares matrix: when
+          // its incremental QR kept every column, take the SVD of R (p x p)
+          if (qr && qr->clean() && qr->cols() == kh + j) {
+            HMat Q(s, kh + j), R(kh + j, kh + j);
+            qr->factors(Q.a.data(), R.a.data());
+            hp = harmonic_extract(SAW, SW, k, rank_tol, &Q, &R);
+          } else {
+            hp = harmonic_extract(SAW, SW, k, rank_tol);
+          }
           ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         },
         pump);
     rep.phase_ms["recycle_harmonic"] += ms;
+    rep.phase_ms["harmonic_svd"] += hp.svd_ms;
+    rep.phase_ms["harmonic_schur"] += hp.schur_ms;
+    rep.phase_ms["harmonic_rest"] += hp.rest_ms;
   }
   if (notes) {
     if (hp.rank_limited)
@@ -737,7 +750,7 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
   out.sketched_entry = hnorm(sr0.data(), s);
 
   // ---- seed the QR with the deflation block (solver.hpp:144-159)
-  auto qr = std::make_unique<HostQR>(s, space.dim() + m, cfg.rank_tol);
+  auto qr = std::make_shared<HostQR>(s, space.dim() + m, cfg.rank_tol);
   for (;;) {
     std::vector<i64> bad;
     for (i64 q = 0; q < space.dim(); ++q)
@@ -746,7 +759,7 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
     space.drop_columns(bad);
     rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": dropped " + std::to_string(bad.size()) +
                         " deflation columns with rank-deficient sketched images");
-    qr = std::make_unique<HostQR>(s, space.dim() + m, cfg.rank_tol);
+    qr = std::make_shared<HostQR>(s, space.dim() + m, cfg.rank_tol);
     if (space.empty()) break;
   }
   const i64 k_hat = space.dim();
@@ -819,6 +832,7 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
   out.steps = st.j;
   out.sres = sres;
   out.breakdown = st.breakdown;
+  out.qr = qr;
   rep.host_wait_ms += ap.wait_ms;
   rep.phase_ms["step_wait"] += ap.wait_ms;
   return out;
@@ -864,7 +878,7 @@ void finish_cycle(Context& c, Workspace& w, const ArnoldiPipeline& ap, const Cyc
     if (cfg.k > 0 && st.j >= 1) {
       std::vector<std::string> notes;
       PhaseTimer pt(rep, "recycle");
-      update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep, pump, side_stream);
+      update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep, pump, side_stream, out.qr.get());
       cs.deflation_rank = space.dim();
       for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
     } else if (cfg.k == 0) {
