@@ -64,8 +64,20 @@ def c3_small():
     return [summary(x, r) for x, r in zip(xs, reps)]
 
 
+def c3_first():
+    """BASELINE C3 at full size, its first system alone (N = 1024^2, same
+    construction and seeds as tools/bench_sequence.py; ~3 min on one core)."""
+    n = 1024
+    b0 = O.gaussian_vector(n * n, 0x3000)
+    rel = 1e-3 * (2.0 * O.uniform_stream(0x3100, n * n) - 1.0)
+    A = O.gen_convdiff2d(n, 100.0, 100.0, 0.0, rel)
+    cfg = O.SolverConfig(m=50, k=20, t=2, s=140, tol=1e-8, variant="exact")
+    x, rep = O.solve(A, b0, cfg)
+    return summary(x, rep, dict(config=dict(n=n, m=50, k=20, t=2, s=140, tol=1e-8, variant="exact")))
+
+
 def main(which):
-    jobs = {"c1": c1, "c2": c2, "c3_small": c3_small}
+    jobs = {"c1": c1, "c2": c2, "c3_small": c3_small, "c3_first": c3_first}
     for name in which:
         t0 = time.time()
         data = jobs[name]()
@@ -76,4 +88,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c3_small", "c2"])
+    main(sys.argv[1:] or ["c1", "c3_small", "c2", "c3_first"])

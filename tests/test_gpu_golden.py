@@ -91,3 +91,48 @@ def test_c2_golden(sk, O, device_gen):
         assert i1 == i2
         assert r1 == pytest.approx(r2, rel=1e-3)
     assert np.linalg.norm(res.x) == pytest.approx(g["x_norm"], rel=1e-6)
+
+
+def _c3_system(sk, i, n=1024):
+    N = n * n
+    b0 = sk.gaussian_vector(N, 0x3000)
+    rel = 1e-3 * (2.0 * sk.uniform_stream(0x3100 + i, N) - 1.0)
+    off, col, val = sk.gen_convdiff2d(n, 100.0 + 2 * i, 100.0 - 2 * i, 0.01 * i, rel)
+    A = sk.SparseMatrix(N, N, off, col, val)
+    b = b0 + 0.05 * sk.gaussian_vector(N, 0x3000 + i) if i else b0
+    return A, b
+
+
+def test_c3_first_system_golden(sk, O):
+    """BASELINE C3 at full size (N = 1024^2), first system against the oracle
+    run (tests/golden/make_golden.py c3_first)."""
+    g = load("c3_first")
+    A, b = _c3_system(sk, 0)
+    c = g["config"]
+    res = sk.solve(A, b, sk.SolverConfig(m=c["m"], k=c["k"], t=c["t"], s=c["s"], tol=c["tol"], variant=c["variant"]))
+    assert res.report.status == g["status"]
+    assert close_iters(res.report.iterations, g["iterations"])
+    assert res.report.cycles == g["cycles"]
+    assert res.report.final_relative_residual == pytest.approx(g["final_relative_residual"], rel=1e-6)
+    for (i1, r1), (i2, r2) in zip(res.report.true_residuals, g["true_residuals"]):
+        assert i1 == i2 and r1 == pytest.approx(r2, rel=1e-6)
+
+
+def test_c3_sequence_head_with_exact_refresh(sk):
+    """The first four systems of the C3 sequence: every system reports a valid status, the
+    first matches the standalone first solve, and each matrix change costs k
+    matvecs + k sketches of exact refresh (counters, recycle.hpp:297-318)."""
+    probs = [sk.ProblemInstance(*_c3_system(sk, i)) for i in range(4)]
+    cfg = sk.SolverConfig(m=50, k=20, t=2, s=140, tol=1e-8, variant="exact")
+    out = sk.solve_sequence(probs, cfg)
+    first = sk.solve(probs[0].matrix, probs[0].rhs, cfg)
+    assert out.reports[0].iterations == first.report.iterations
+    for r in out.reports:
+        assert r.status in ("converged", "max_restarts", "diverged", "breakdown")
+        assert r.iterations > 0
+    # an exact refresh of the q recycle columns on each change costs q matvecs
+    # and q sketches on top of the per-step / per-check / per-cycle counts
+    for r in out.reports[1:]:
+        extra_mv = r.counters["matvecs"] - r.iterations - len(r.true_residuals)
+        extra_sk = r.counters["sketch_applies"] - r.iterations - r.cycles
+        assert 1 <= extra_mv <= 21 and extra_mv == extra_sk
