@@ -269,6 +269,81 @@ __global__ void __launch_bounds__(kThreads) k_tallskinny(const double* const* __
   }
 }
 
+/// Dense tall-skinny product of the recycle update, one pass over the inputs:
+/// C (n x nout, ldc) = [A1 (n x k1) | A2 (n x k2)] B ((k1+k2) x nout), plus the
+/// CTA partials of the column sums of squares (CTA-major, folded by
+/// k_col_fold). Each thread owns two rows (one 16-byte load per input
+/// column); UD input columns are in flight one group ahead of the FMAs, so
+/// the HBM stream does not wait on the arithmetic. Coefficients are read from
+/// shared memory as 16-byte pairs.
+template <int NOUT, int UD>
+__global__ void __launch_bounds__(kThreads, NOUT > 12 ? 1 : 2) k_tsgemm(const double* __restrict__ A1, int64_t lda1, int k1,
+                                                        const double* __restrict__ A2, int64_t lda2, int k2,
+                                                        const double* __restrict__ B, int nout, double* __restrict__ C,
+                                                        int64_t ldc, int64_t npairs, double* __restrict__ partials) {
+  extern __shared__ double bs[];  // (k1 + k2) x NOUT, row-major by input
+  const int kk = k1 + k2;
+  for (int q = threadIdx.x; q < kk * NOUT; q += blockDim.x) {
+    const int i = q / NOUT, o = q % NOUT;
+    bs[q] = o < nout ? B[static_cast<int64_t>(o) * kk + i] : 0.0;
+  }
+  __syncthreads();
+  double nrm[NOUT];
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) nrm[o] = 0.0;
+  auto col = [&](int i) -> const double2* {
+    return reinterpret_cast<const double2*>(i < k1 ? A1 + static_cast<int64_t>(i) * lda1
+                                                   : A2 + static_cast<int64_t>(i - k1) * lda2);
+  };
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t pr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; pr < npairs; pr += stride) {
+    double2 acc[NOUT];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) acc[o] = make_double2(0.0, 0.0);
+    double2 cur[UD], nxt[UD];
+#pragma unroll
+    for (int u = 0; u < UD; ++u) cur[u] = u < kk ? __ldcs(col(u) + pr) : make_double2(0.0, 0.0);
+    for (int i0 = 0; i0 < kk; i0 += UD) {
+#pragma unroll
+      for (int u = 0; u < UD; ++u) nxt[u] = i0 + UD + u < kk ? __ldcs(col(i0 + UD + u) + pr) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < UD; ++u) {
+        if (i0 + u < kk) {
+          const double2* cf2 = reinterpret_cast<const double2*>(bs + (i0 + u) * NOUT);
+#pragma unroll
+          for (int o2 = 0; o2 < NOUT / 2; ++o2) {
+            const double2 cf = cf2[o2];
+            acc[2 * o2] = make_double2(fma(cf.x, cur[u].x, acc[2 * o2].x), fma(cf.x, cur[u].y, acc[2 * o2].y));
+            acc[2 * o2 + 1] = make_double2(fma(cf.y, cur[u].x, acc[2 * o2 + 1].x), fma(cf.y, cur[u].y, acc[2 * o2 + 1].y));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UD; ++u) cur[u] = nxt[u];
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+      if (o < nout) {
+        reinterpret_cast<double2*>(C + static_cast<int64_t>(o) * ldc)[pr] = acc[o];
+        nrm[o] = fma(acc[o].x, acc[o].x, fma(acc[o].y, acc[o].y, nrm[o]));
+      }
+    }
+  }
+  __shared__ double red[NOUT][kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) {
+    const double v = warp_sum(nrm[o]);
+    if (lane == 0) red[o][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nout) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
+    partials[static_cast<int64_t>(threadIdx.x) * gridDim.x + blockIdx.x] = v;
+  }
+}
+
 int stream_grid(const Context& c, int64_t n, int per_thread = 1) {
   const int64_t want = (n / per_thread + kThreads - 1) / kThreads;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.num_sms) * 8)));
@@ -340,11 +415,55 @@ void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, dou
   SDR_KERNEL_CHECK();
 }
 
-void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2) {
+template <int NOUT>
+void tsgemm_impl(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
+                 const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2, double* scratch) {
+  constexpr int UD = NOUT <= 8 ? 8 : (NOUT <= 12 ? 4 : 2);
+  auto kern = k_tsgemm<NOUT, UD>;
+  const size_t smem = sizeof(double) * static_cast<size_t>(k1 + k2) * NOUT;
+  if (smem > 48 * 1024)
+    SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kThreads, smem);
+  const int64_t npairs = n / 2;
+  const int g = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((npairs + kThreads - 1) / kThreads, static_cast<int64_t>(c.num_sms) * per_sm)));
+  double* part = scratch ? scratch : c.partials(static_cast<int64_t>(nout) * g);
+  {
+    TimedLaunch t(c, "recycle_gemm");
+    kern<<<g, kThreads, smem, c.stream>>>(A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, npairs, part);
+    SDR_KERNEL_CHECK();
+  }
+  TimedLaunch t(c, "col_norms");
+  k_col_fold<<<(nout + 7) / 8, 256, 0, c.stream>>>(part, g, nout, norms2);
+  SDR_KERNEL_CHECK();
+}
+
+bool tsgemm_supported(int nout, int64_t n, int64_t lda1, int64_t lda2, int64_t ldc) {
+  return nout >= 1 && nout <= 24 && n % 2 == 0 && lda1 % 2 == 0 && lda2 % 2 == 0 && ldc % 2 == 0;
+}
+
+int64_t tsgemm_scratch_size(int num_sms) { return static_cast<int64_t>(24) * num_sms * 8; }
+
+void launch_tsgemm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
+                   const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2, double* scratch) {
+  if (!tsgemm_supported(nout, n, lda1, lda2, ldc)) throw invalid("tall-skinny product: unsupported shape");
+  if (nout <= 4)
+    tsgemm_impl<4>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+  else if (nout <= 8)
+    tsgemm_impl<8>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+  else if (nout <= 12)
+    tsgemm_impl<12>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+  else if (nout <= 16)
+    tsgemm_impl<16>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+  else
+    tsgemm_impl<24>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+}
+
+void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2, double* scratch) {
   if (ncol == 0) return;
   const int chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 4 * c.num_sms / std::max(1, ncol) + 1)));
   const int64_t chunk = (n + chunks - 1) / chunks;
-  double* part = c.partials(static_cast<int64_t>(chunks) * ncol);
+  double* part = scratch ? scratch : c.partials(static_cast<int64_t>(chunks) * ncol);
   {
     TimedLaunch t(c, "col_norms");
     k_col_sumsq<<<dim3(chunks, ncol), kThreads, 0, c.stream>>>(C, ldc, n, chunk, part);

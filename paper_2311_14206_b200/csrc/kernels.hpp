@@ -74,8 +74,19 @@ void launch_update(Context& c, const double* y, double* V, int64_t ldv, const Ve
                    int ngram, double* rec, const RecLayout& L, double* cvec, const double* coef_ready);
 void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, double* norm2);
 void launch_axpy(Context& c, double a, const double* x, double* y, int64_t n);
+/// C = [A1 A2] B (column-major; B is (k1+k2) x nout with leading dim k1+k2)
+/// in one pass over the inputs, norms2[o] = ||C(:, o)||^2 (deterministic).
+bool tsgemm_supported(int nout, int64_t n, int64_t lda1, int64_t lda2, int64_t ldc);
+/// scratch: tsgemm_scratch_size doubles for the norm partials (null: the
+/// context's shared scratch — not safe beside other streams' kernels).
+int64_t tsgemm_scratch_size(int num_sms);
+void launch_tsgemm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
+                   const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2,
+                   double* scratch = nullptr);
 /// norms2[q] = ||C(:, q)||^2 for q < ncol (column-major, ldc), deterministic.
-void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2);
+/// scratch: at least (4 num_sms + ncol) doubles, or null for the context's scratch.
+void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2,
+                       double* scratch = nullptr);
 void launch_scale_copy(Context& c, double a, const double* x, double* y, int64_t n);
 void launch_tallskinny(Context& c, const double* const* in_dev, int nin, const double* coef_dev, int nout,
                        double* const* out_dev, int64_t n, double* norms2);

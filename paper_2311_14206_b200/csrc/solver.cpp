@@ -67,6 +67,7 @@ struct Workspace {
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
   DeviceBuffer<double> gcoef;      // recycle-update GEMM coefficients
+  DeviceBuffer<double> pside;      // recycle-update norm partials (runs on the side stream)
   DeviceBuffer<double> ps[2], pu[2];  // split pipeline: SRDCT / update partials by step parity
   cudaStream_t sk_stream = nullptr;   // split pipeline: SRDCT beside K1 / K2'
   cudaEvent_t ev_sk[2] = {nullptr, nullptr}, ev_u = nullptr, ev_skq = nullptr;
@@ -634,7 +635,30 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     SDR_CUDA(cudaStreamWaitEvent(w.side_stream, w.ev_side_in, 0));
     std::swap(c.stream, w.side_stream);
   }
-  if (dense_u) {
+  static const bool own_gemm = [] {
+    const char* e = std::getenv("SDR_TSGEMM");
+    return !e || std::atoi(e) != 0;
+  }();
+  // k_tsgemm (one HBM pass over [V U], norms fused) wins where the product is
+  // memory-bound (few outputs: C5, k = 10: 17.4 vs 37 ms per restart); with
+  // ~20 outputs (C2) cuBLAS's DMMA GEMM is faster (0.8 vs 1.4 ms)
+  if (dense_u && own_gemm && ke <= 12 && tsgemm_supported(static_cast<int>(ke), nloc, w.lay.ld, sp.ld, sp.ld)) {
+    const i64 kk = j + kc;
+    w.gcoef.ensure(std::max<i64>(kk * ke, 1));
+    w.hgcoef.ensure(std::max<i64>(kk * ke, 1));
+    double* hb = w.hgcoef.get();
+    std::fill(hb, hb + kk * ke, 0.0);
+    for (i64 q = 0; q < ke; ++q) {
+      for (i64 i = 0; i < j; ++i) hb[q * kk + i] = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
+      for (i64 p = 0; p < kh; ++p)
+        hb[q * kk + j + sp.slot[static_cast<size_t>(p)]] = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
+    }
+    SDR_CUDA(cudaMemcpyAsync(w.gcoef.get(), hb, sizeof(double) * static_cast<size_t>(kk * ke), cudaMemcpyHostToDevice,
+                             c.stream));
+    w.pside.ensure(tsgemm_scratch_size(c.num_sms));
+    launch_tsgemm(c, w.Vcol(vb, 0), w.lay.ld, static_cast<int>(j), sp.buf[sp.cur].get(), sp.ld, static_cast<int>(kc),
+                  w.gcoef.get(), static_cast<int>(ke), sp.buf[other].get(), sp.ld, nloc, w.scal.get(), w.pside.get());
+  } else if (dense_u) {
     const i64 ncoef = j * ke + kc * ke;
     w.gcoef.ensure(std::max<i64>(ncoef, 1));
     w.hgcoef.ensure(std::max<i64>(ncoef, 1));
@@ -650,7 +674,8 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     double* unew = sp.buf[other].get();
     c.dgemm_tall(nloc, ke, j, w.Vcol(vb, 0), w.lay.ld, w.gcoef.get(), j, 0.0, unew, sp.ld);
     if (kc > 0) c.dgemm_tall(nloc, ke, kc, sp.buf[sp.cur].get(), sp.ld, w.gcoef.get() + j * ke, kc, 1.0, unew, sp.ld);
-    launch_col_norms2(c, unew, sp.ld, nloc, static_cast<int>(ke), w.scal.get());
+    w.pside.ensure(tsgemm_scratch_size(c.num_sms));
+    launch_col_norms2(c, unew, sp.ld, nloc, static_cast<int>(ke), w.scal.get(), w.pside.get());
   } else {
     std::vector<const double*> in;
     HMat coef(kh + j, ke);
