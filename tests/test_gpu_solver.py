@@ -226,3 +226,25 @@ def test_sequence_failure_isolation_and_empty(sk, O):
     assert res.reports[1].error and "aborted" in res.reports[1].notes[-1]
     assert res.reports[2].status == "converged"
     assert sk.solve_sequence([], c).reports == []
+
+
+def test_c4_real_equivalent_small_lattice_matches_oracle(sk, O):
+    """BASELINE C4's operator (complex 4-D lattice) at 4^4 sites in its
+    real-equivalent form (tools/c4_problem.py): GPU solve == oracle solve."""
+    from tools.c4_problem import c4_csr
+    off, col, val = c4_csr((4, 4, 4, 4), m0=-0.8, seed=2, uniform=O.uniform_stream)
+    n2 = len(off) - 1
+    A = sk.SparseMatrix(n2, n2, off, col, val)
+    Ao = O.SparseMatrix.from_csr(n2, n2, off, col, val)
+    b = O.gaussian_vector(n2, 4)
+    c, co = cfgs(sk, O, m=20, k=6, t=3, s=60, tol=1e-8, max_restarts=30)
+    g = sk.solve(A, b, c)
+    o = O.solve(Ao, b, co)
+    assert_same_solve(g, o, iters_tol=0.02)
+    assert g.report.status == "converged"
+    # the interleaved solution is the complex solution of (4 + m0) x + sum couplings = b
+    z = g.x[0::2] + 1j * g.x[1::2]
+    Ac = (O.SparseMatrix.from_csr(n2, n2, off, col, val).dense())
+    Acx = Ac[0::2, 0::2] + 1j * Ac[1::2, 0::2]
+    bc = b[0::2] + 1j * b[1::2]
+    assert np.linalg.norm(Acx @ z - bc) <= 1e-7 * np.linalg.norm(bc)
