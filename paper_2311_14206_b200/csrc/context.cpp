@@ -79,7 +79,7 @@ Context::Context(int dev, int rk, int ws, const void* nccl_id) : device(dev), ra
   SDR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   counters_.resize(kNumCounters);
   SDR_CUDA(cudaMemset(counters_.get(), 0, sizeof(unsigned) * kNumCounters));
-  if (world > 1) {
+  if (world > 1 || nccl_id) {
     if (!nccl_id) throw invalid("sdr_ctx_create_dist: NCCL id required for world > 1");
     nccl_ = load_nccl();
     ncclUniqueId id;
@@ -106,7 +106,7 @@ Context::~Context() {
 }
 
 void Context::allreduce_sum(double* dev, i64 n) {
-  if (world <= 1 || n <= 0) return;
+  if (!comm_ || n <= 0) return;
   ++launches;
   if (timing) time_begin("allreduce");
   SDR_NCCL(nccl_->AllReduce(dev, dev, static_cast<size_t>(n), ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream));
@@ -114,7 +114,7 @@ void Context::allreduce_sum(double* dev, i64 n) {
 }
 
 void Context::allgather_i64(const i64* host_in, i64 count, i64* host_out) {
-  if (world <= 1) {
+  if (!comm_) {
     std::memcpy(host_out, host_in, sizeof(i64) * static_cast<size_t>(count));
     return;
   }
@@ -127,7 +127,7 @@ void Context::allgather_i64(const i64* host_in, i64 count, i64* host_out) {
 }
 
 void Context::halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin) {
-  if (world <= 1 || plan.empty()) return;
+  if (!comm_ || plan.empty()) return;
   ++launches;
   if (timing) time_begin("halo");
   auto comm = static_cast<ncclComm_t>(comm_);

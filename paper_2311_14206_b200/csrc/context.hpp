@@ -40,7 +40,10 @@ class Context {
   cudaStream_t stream = nullptr;
   i64 launches = 0;
 
-  bool distributed() const { return world > 1; }
+  /// Multi-GPU code path: world > 1, or a one-rank NCCL communicator
+  /// (sdr_ctx_create_dist with world = 1 and an id) that runs the distributed
+  /// pipeline — halo plans, allreduces, fold kernels — on a single GPU.
+  bool distributed() const { return world > 1 || comm_ != nullptr; }
 
   // ---- reductions scratch: per-kernel-class partial buffers and
   // last-block-done counters (zeroed once, reset by the last block).

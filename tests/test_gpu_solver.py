@@ -248,3 +248,27 @@ def test_c4_real_equivalent_small_lattice_matches_oracle(sk, O):
     Acx = Ac[0::2, 0::2] + 1j * Ac[1::2, 0::2]
     bc = b[0::2] + 1j * b[1::2]
     assert np.linalg.norm(Acx @ z - bc) <= 1e-7 * np.linalg.norm(bc)
+
+
+def test_distributed_pipeline_on_one_rank(sk, O):
+    """The multi-GPU code path (NCCL halo plans and allreduces, last-CTA folds,
+    coefficients formed after the allreduce, fold kernel + allreduce of the B
+    record) run on a one-rank NCCL communicator: same solve as the one-GPU
+    deferred pipeline and the oracle."""
+    cfg = sk.SolverConfig(m=30, k=8, t=2, s=80, tol=1e-8, max_restarts=20)
+    n = 24
+    dctx = sk.Context(0, 0, 1, sk.Context.nccl_unique_id())
+    Ad = sk.SparseMatrix.convdiff3d_device(n, 100.0, 50.0, 25.0, ctx=dctx)
+    A1 = sk.SparseMatrix.convdiff3d_device(n, 100.0, 50.0, 25.0)
+    b = O.gaussian_vector(n ** 3, 1)
+    gd = sk.solve(Ad, b, cfg, space=sk.RecycleSpace(dctx),
+                  sketch=sk.SketchOperator.subsampled_dct(n ** 3, 80, cfg.sketch_seed, ctx=dctx))
+    g1 = sk.solve(A1, b, cfg)
+    Ao = O.gen_convdiff3d(n, 100.0, 50.0, 25.0)
+    o = O.solve(Ao, b, O.SolverConfig(m=30, k=8, t=2, s=80, tol=1e-8, max_restarts=20))
+    assert gd.report.status == g1.report.status == o[1].status
+    assert gd.report.iterations == g1.report.iterations
+    assert abs(gd.report.iterations - o[1].iterations) <= max(1, 0.02 * o[1].iterations)
+    for (i1, r1), (i2, r2) in zip(gd.report.true_residuals, g1.report.true_residuals):
+        assert i1 == i2 and r1 == pytest.approx(r2, rel=1e-8)
+    assert np.linalg.norm(gd.x - g1.x) <= 1e-9 * np.linalg.norm(g1.x)
