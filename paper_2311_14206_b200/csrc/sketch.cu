@@ -265,7 +265,7 @@ struct TileArgs {
   const uint32_t* sign_bits = nullptr;
   const int64_t* rows = nullptr;
   const double* row_scale = nullptr;
-  const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][jump4 s][jump2 s][twiddle 256]
+  const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][jump z^24, z^8, z^28 (3s)][twiddle 256]
   const int* uq = nullptr;       // k mod 256
   double* partials = nullptr;    // [G][nvp] CTA partials
   unsigned long long* trace = nullptr;  // SDR_TRACE=1: per-CTA phase timestamps [G][16]
@@ -393,27 +393,31 @@ __device__ __forceinline__ void deferred_prologue(const UpdateArgs& ua, int s, c
 // buffer and Horner state and synchronises on its own named barrier, so the
 // groups' load, FFT and accumulation phases interleave on the SM.
 constexpr int kGPairs = 8;                       // column pairs per tile (16 columns)
-constexpr int kGThreads = kGPairs * 16;          // threads per group
 constexpr int kGroupsMax = 4;                    // tile groups per CTA (GRP template: 4, or 2 to co-reside)
 
+template <int NT>
 __device__ __forceinline__ void group_sync(int g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGThreads) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(NT) : "memory");
 }
 
-template <int SRC, int NI, bool PAIRED, int MAXT, int GRP, int CHK = 0>
+/// Table slot of the group jump z^{PR (GRP - 1)} (k_srdct_tables).
+constexpr int jump_slot(int pr, int grp) { return pr * (grp - 1) == 24 ? 4 : (pr * (grp - 1) == 8 ? 5 : 6); }
+
+template <int SRC, int NI, bool PAIRED, int MAXT, int GRP, int CHK = 0, int PR = kGPairs>
 // GRP = 2 sketches run beside K1 / K2' on the same SMs (split pipeline): <= 85 registers.
-__global__ void __launch_bounds__(GRP * kGThreads, (GRP == 2 && SRC == kSrcSketch) ? 3 : 1) k_srdct_tiles(TileArgs ta, const double* __restrict__ x,
+__global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch) ? 3 : 1) k_srdct_tiles(TileArgs ta, const double* __restrict__ x,
                                                                  double xscale, double* __restrict__ out,
                                                                  UpdateArgs ua) {
-  constexpr int kCta = GRP * kGThreads;
+  constexpr int kGT = PR * 16;  // threads per group
+  constexpr int kCta = GRP * kGT;
   extern __shared__ double2 sm[];
   const int s = ta.s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = tid / kGThreads, lt = tid % kGThreads;
-  double2* X = sm + g * (kGPairs * kXS);                  // [8][257] per group
-  double2* S1s = sm + GRP * (kGPairs * kXS) + g * 2 * s;  // [s] per group
+  const int g = tid / kGT, lt = tid % kGT;
+  double2* X = sm + g * (PR * kXS);                  // [8][257] per group
+  double2* S1s = sm + GRP * (PR * kXS) + g * 2 * s;  // [s] per group
   double2* S2s = S1s + s;                                  // [s] per group
-  double2* zq = sm + GRP * (kGPairs * kXS + 2 * s);   // [s]  z = e^{2 i pi k/N}
+  double2* zq = sm + GRP * (PR * kXS + 2 * s);   // [s]  z = e^{2 i pi k/N}
   double2* zj = zq + s;                                    // [s]  z^{8 (GRP - 1)}: jump over the other groups' tiles
   double2* tw = zj + s;                                    // [256]
   int* uq = reinterpret_cast<int*>(tw + 256);              // [s]
@@ -423,10 +427,10 @@ __global__ void __launch_bounds__(GRP * kGThreads, (GRP == 2 && SRC == kSrcSketc
   const uint64_t twoN = 2u * static_cast<uint64_t>(ta.N);
   stamp_begin(ta.stamp);
   trace_mark(ta.trace, 0);
-  for (int k = tid; k < 256; k += kCta) tw[k] = ta.tab[6 * s + k];
+  for (int k = tid; k < 256; k += kCta) tw[k] = ta.tab[7 * s + k];
   for (int q = tid; q < s; q += kCta) {
     zq[q] = ta.tab[2 * s + q];
-    zj[q] = ta.tab[(GRP == 4 ? 4 : 5) * s + q];
+    zj[q] = ta.tab[jump_slot(PR, GRP) * s + q];
     uq[q] = ta.uq[q];
   }
   for (int q = tid; q < GRP * 2 * s; q += kCta) S1s[q - g * 2 * s] = make_double2(0.0, 0.0);
@@ -457,14 +461,14 @@ __global__ void __launch_bounds__(GRP * kGThreads, (GRP == 2 && SRC == kSrcSketc
       W[d] = ua.V + static_cast<int64_t>(ua.j - (d < ua.nwin ? d : 0)) * ua.ldv + ua.own_off;
     wout = ua.V + static_cast<int64_t>(ua.j + 1) * ua.ldv + ua.own_off;
   }
-  const int p = lt & (kGPairs - 1), t = lt / kGPairs;
+  const int p = lt & (PR - 1), t = lt / PR;
   const int nI = NI ? NI : (ta.M >> 4);  // <= 8 nonzero stage-1 inputs
   // CTA b owns tiles [tb, te); group g takes te-1-g, te-1-g-GRP, ... (descending)
   const int64_t tb = static_cast<int64_t>(b) * ta.ntiles / G, te = static_cast<int64_t>(b + 1) * ta.ntiles / G;
   int64_t tlow = -1;
 
   for (int64_t tile = te - 1 - g; tile >= tb; tile -= GRP) {
-    const int64_t aa = tile * (2 * kGPairs) + 2 * p;
+    const int64_t aa = tile * (2 * PR) + 2 * p;
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = make_double2(0.0, 0.0);
@@ -538,21 +542,21 @@ __global__ void __launch_bounds__(GRP * kGThreads, (GRP == 2 && SRC == kSrcSketc
     else dft16(v);
 #pragma unroll
     for (int vv = 1; vv < 16; ++vv) v[vv] = cmul(v[vv], tw[(vv * t) & 255]);
-    group_sync(g);  // the group's previous Horner pass has finished reading X
+    group_sync<kGT>(g);  // the group's previous Horner pass has finished reading X
 #pragma unroll
     for (int vv = 0; vv < 16; ++vv) X[p * kXS + vv * 16 + t] = v[vv];
-    group_sync(g);
+    group_sync<kGT>(g);
 #pragma unroll
     for (int tt = 0; tt < 16; ++tt) v[tt] = X[p * kXS + t * 16 + tt];
     dft16(v);
-    group_sync(g);
+    group_sync<kGT>(g);
 #pragma unroll
     for (int w = 0; w < 16; ++w) X[p * kXS + t + 16 * w] = v[w];
-    group_sync(g);
+    group_sync<kGT>(g);
     // Horner over the tile's 8 pairs, continuing the group's recurrence;
     // the first step also jumps over the GRP - 1 tiles in between
     const bool first = tlow < 0;
-    for (int q = lt; q < s; q += kGThreads) {
+    for (int q = lt; q < s; q += kGT) {
       const int u = uq[q], um = (256 - u) & 255;
       const double2 zz = zq[q];
       double2 S1 = S1s[q], S2 = S2s[q];
@@ -562,7 +566,7 @@ __global__ void __launch_bounds__(GRP * kGThreads, (GRP == 2 && SRC == kSrcSketc
         S2 = cmul(S2, jz);
       }
 #pragma unroll
-      for (int pp = kGPairs - 1; pp >= 0; --pp) {
+      for (int pp = PR - 1; pp >= 0; --pp) {
         const double2 C = X[pp * kXS + u];
         const double2 Cm = X[pp * kXS + um];
         S1 = make_double2(fma(S1.x, zz.x, fma(-S1.y, zz.y, C.x)), fma(S1.x, zz.y, fma(S1.y, zz.x, C.y)));
@@ -597,9 +601,9 @@ __global__ void __launch_bounds__(GRP * kGThreads, (GRP == 2 && SRC == kSrcSketc
     double2 acc = make_double2(0.0, 0.0);
     for (int gg = 0; gg < GRP; ++gg) {
       if (glow[gg] < 0) continue;
-      const double2* S = sm + GRP * (kGPairs * kXS) + gg * 2 * s;
+      const double2* S = sm + GRP * (PR * kXS) + gg * 2 * s;
       double sn, cs;
-      const uint64_t ph = (k * static_cast<uint64_t>(ta.r0 + glow[gg] * 2 * kGPairs)) % twoN;
+      const uint64_t ph = (k * static_cast<uint64_t>(ta.r0 + glow[gg] * 2 * PR)) % twoN;
       sincospi(static_cast<double>(ph) / static_cast<double>(ta.N), &sn, &cs);
       acc = cadd(acc, cmul(make_double2(cs, sn), cadd(cmul(ga, S[q]), cmul(gb, S[s + q]))));
     }
@@ -762,10 +766,10 @@ __global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int 
       tab[2 * s + q] = make_double2(cs, sn);
       sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
       tab[3 * s + q] = make_double2(cs, sn);
-      // group jumps z^{8 (GRP - 1)} = e^{2 i pi k 8 (GRP-1) / N} for GRP = 4, 2, exact reduction
-      for (int gi = 0; gi < 2; ++gi) {
-        const uint64_t grp = gi == 0 ? 4 : 2;
-        const uint64_t e = (2 * k * static_cast<uint64_t>(kGPairs) * (grp - 1)) % twoN;
+      // group jumps z^E = e^{2 i pi k E / N}, E = pairs (groups - 1) in {24, 8, 28}, exact reduction
+      for (int gi = 0; gi < 3; ++gi) {
+        const uint64_t E = gi == 0 ? 24 : (gi == 1 ? 8 : 28);
+        const uint64_t e = (2 * k * E) % twoN;
         sincospi(static_cast<double>(e) / static_cast<double>(N), &sn, &cs);
         tab[(4 + gi) * s + q] = make_double2(cs, sn);
       }
@@ -773,7 +777,7 @@ __global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int 
     } else {
       const int k = q - s;
       sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
-      tab[6 * s + k] = make_double2(cs, sn);
+      tab[7 * s + k] = make_double2(cs, sn);
     }
   }
 }
@@ -933,8 +937,8 @@ __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restri
 namespace {
 
 
-size_t tiles_smem(int64_t s, int grp = kGroupsMax) {
-  return sizeof(double2) * static_cast<size_t>(grp * (kGPairs * kXS + 2 * s) + 2 * s + 256) +
+size_t tiles_smem(int64_t s, int grp = kGroupsMax, int pr = kGPairs) {
+  return sizeof(double2) * static_cast<size_t>(grp * (pr * kXS + 2 * s) + 2 * s + 256) +
          sizeof(int) * static_cast<size_t>(s);
 }
 
@@ -942,10 +946,10 @@ bool tiles_eligible(const SketchDev& S, const SrdctPlan& p) {
   return p.F == 256 && p.M % 16 == 0 && S.tab.size() > 0 && tiles_smem(S.s) <= 227 * 1024;
 }
 
-template <int SRC, int NI, bool PAIRED, int MAXT, int GRP = kGroupsMax, int CHK = 0>
+template <int SRC, int NI, bool PAIRED, int MAXT, int GRP = kGroupsMax, int CHK = 0, int PR = kGPairs>
 void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctPlan& p, int64_t row_begin,
                   const double* x, double xscale, double* out, const UpdateArgs& ua, StepFold* sf = nullptr) {
-  const int64_t ntiles = (p.L + 2 * kGPairs - 1) / (2 * kGPairs);
+  const int64_t ntiles = (p.L + 2 * PR - 1) / (2 * PR);
   const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((ntiles + GRP - 1) / GRP, c.num_sms)));
   const int64_t nv = (2 * S.s + (SRC == kSrcUpdate ? MAXT : 0) + 1) & ~int64_t{1};
   TileArgs ta;
@@ -963,8 +967,8 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   ta.partials = sf ? sf->out_partials : c.partials(nv * G);
   ta.trace = c.trace(16 * static_cast<int64_t>(G));
   ta.stamp = c.launch_stamp(name);
-  const size_t smem = tiles_smem(S.s, GRP);
-  auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT, GRP, CHK>;
+  const size_t smem = tiles_smem(S.s, GRP, PR);
+  auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT, GRP, CHK, PR>;
   static size_t configured = 0;
   if (smem > configured) {
     SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -974,7 +978,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
     TimedLaunch t(c, name);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(GRP * kGThreads);
+    cfg.blockDim = dim3(GRP * PR * 16);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute at[1] = {pdl_attribute()};
@@ -997,7 +1001,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
 }  // namespace
 
 void prepare_srdct_tables(Context& c, SketchDev& S) {
-  S.tab.resize(6 * S.s + 256);
+  S.tab.resize(7 * S.s + 256);
   S.uq.resize(S.s);
   k_srdct_tables<<<static_cast<int>((S.s + 256 + 255) / 256), 256, 0, c.stream>>>(S.n, S.rows.get(), static_cast<int>(S.s),
                                                                                  S.tab.get(), S.uq.get());
@@ -1045,18 +1049,17 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
       ua.sk_row = j;
     }
   }
+  // t <= 2: two tile groups per CTA with eight rows of loads in flight per
+  // thread (242 registers) measured 2.5 % faster per step than four groups
+  // with two rows (128 registers); SDR_K2_VARIANT=1 selects the latter.
   static const int variant = [] {
     const char* e = std::getenv("SDR_K2_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
   if (need <= 2 && variant == 1)
-    launch_tiles<kSrcUpdate, 8, true, 2, 4, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
-  else if (need <= 2 && variant == 2)
-    launch_tiles<kSrcUpdate, 8, true, 2, 2, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
-  else if (need <= 2 && variant == 3)
-    launch_tiles<kSrcUpdate, 8, true, 2, 2, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
-  else if (need <= 2)
     launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  else if (need <= 2)
+    launch_tiles<kSrcUpdate, 8, true, 2, 2, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
   else
     launch_tiles<kSrcUpdate, 8, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
   return true;
