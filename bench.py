@@ -191,7 +191,9 @@ def main():
     torch.cuda.set_device(local)
     import paper_2311_14206_b200 as sk
 
-    if world > 1:
+    # SDR_BENCH_DIST=1 takes the multi-GPU code path even on one rank (one-rank
+    # NCCL communicator): a check of the torchrun / NCCL plumbing on one GPU
+    if world > 1 or os.environ.get("SDR_BENCH_DIST") == "1":
         import torch.distributed as dist
         dist.init_process_group("gloo", init_method="env://")
         idbuf = [sk.Context.nccl_unique_id() if rank == 0 else None]

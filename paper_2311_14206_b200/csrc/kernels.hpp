@@ -62,7 +62,8 @@ void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y);
 /// coefficients of step j into coef[0..nwin] and the record's H part. With
 /// partials_out (deferred step pipeline) the CTAs only leave their window
 /// dots there, value-major [1 + nwin][grid], and nothing is folded; the
-/// return value is the grid size.
+/// return value is the grid size. max_blocks_per_sm < 0: the full resident
+/// grid regardless of the local size (identical layouts on every rank).
 int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
                         double* coef, double* partials_out = nullptr, int max_blocks_per_sm = 0);
@@ -105,6 +106,7 @@ void prepare_srdct_tables(Context& c, SketchDev& S);
 /// forms the MGS coefficients there and leaves its own partials for K2(j+1).
 /// No kernel of a step ends in a serial last-CTA fold.
 struct StepFold {
+  bool fixed_grid = false;  // several ranks: the tile kernel runs one CTA per SM whatever the local size
   const double* k1_partials = nullptr;
   int k1_G = 0;
   const double* prev_partials = nullptr;  // null at j = 0 (row 0 comes from the cycle init)

@@ -950,7 +950,9 @@ template <int SRC, int NI, bool PAIRED, int MAXT, int GRP = kGroupsMax, int CHK 
 void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctPlan& p, int64_t row_begin,
                   const double* x, double xscale, double* out, const UpdateArgs& ua, StepFold* sf = nullptr) {
   const int64_t ntiles = (p.L + 2 * PR - 1) / (2 * PR);
-  const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((ntiles + GRP - 1) / GRP, c.num_sms)));
+  const int G = (sf && sf->fixed_grid)
+                    ? c.num_sms
+                    : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((ntiles + GRP - 1) / GRP, c.num_sms)));
   const int64_t nv = (2 * S.s + (SRC == kSrcUpdate ? MAXT : 0) + 1) & ~int64_t{1};
   TileArgs ta;
   ta.N = S.n;

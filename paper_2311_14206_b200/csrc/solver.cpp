@@ -326,9 +326,13 @@ struct ArnoldiPipeline {
 
   void setup_deferred() {
     const int need = static_cast<int>(std::max<i64>(std::min(t, m), std::min<i64>(w.RL.T - 1, m) + 1));
-    deferred = !c.distributed() && fuse_update_sketch() &&
+    static const bool defer_dist = [] {
+      const char* e = std::getenv("SDR_DEFER_DIST");
+      return !e || std::atoi(e) != 0;
+    }();
+    deferred = (!c.distributed() || defer_dist) && fuse_update_sketch() &&
                update_sketch_eligible(S, w.lay, need, A.row_begin, w.lay.ld);
-    split = deferred && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
+    split = deferred && !c.distributed() && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
     if (!deferred) return;
     w.p1.ensure(34 * static_cast<i64>(c.num_sms) * 8);
     for (auto& b : w.p2) b.ensure(update_sketch_partials_size(S, c.num_sms));
@@ -352,10 +356,17 @@ struct ArnoldiPipeline {
       return;
     }
     if (deferred) {
+      // several ranks: the CTA partials themselves are summed over ranks (an
+      // allreduce after each kernel, grids fixed so the layouts agree), and
+      // every rank folds the same reduced partials in the same order
+      const bool dist = c.distributed();
+      c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
       StepFold sf;
+      sf.fixed_grid = dist;
       sf.k1_partials = w.p1.get();
       sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
-                                    w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get());
+                                    w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), dist ? -1 : 0);
+      if (dist) c.allreduce_sum(w.p1.get(), static_cast<i64>(1 + nwin) * sf.k1_G);
       if (j > 0) {
         sf.prev_partials = last.out_partials;
         sf.prev_G = last.out_G;
@@ -366,6 +377,7 @@ struct ArnoldiPipeline {
       if (!launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
                                 w.cvec.get(), nullptr, A.row_begin, &sf))
         throw logic("deferred step pipeline: fused update became ineligible");
+      if (dist) c.allreduce_sum(sf.out_partials, static_cast<i64>(sf.out_G) * sf.out_nvp);
       last = sf;
       last_ngram = ngram;
       SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
 template <class K>
 int resident_grid(const Context& c, K kernel, int64_t want_blocks, int max_per_sm = 0) {
   int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), kThreads, 0);
+  if (max_per_sm < 0) return c.num_sms * per_sm;  // fixed grid (CTAs past the work write zero partials)
   if (max_per_sm > 0) per_sm = std::min(per_sm, max_per_sm);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_blocks, static_cast<int64_t>(c.num_sms) * per_sm)));
 }
