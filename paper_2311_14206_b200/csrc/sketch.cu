@@ -265,7 +265,7 @@ struct TileArgs {
   const uint32_t* sign_bits = nullptr;
   const int64_t* rows = nullptr;
   const double* row_scale = nullptr;
-  const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][jump z^24, z^8, z^28 (3s)][twiddle 256]
+  const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][jump z^24, z^8, z^28, z^16 (4s)][twiddle 256]
   const int* uq = nullptr;       // k mod 256
   double* partials = nullptr;    // [G][nvp] CTA partials
   unsigned long long* trace = nullptr;  // SDR_TRACE=1: per-CTA phase timestamps [G][16]
@@ -364,7 +364,7 @@ __device__ __forceinline__ void deferred_prologue(const UpdateArgs& ua, int s, c
   const int b_off = 2 * ua.T + 3;
   if (ua.prev_sk) {
     double* dst = ua.rec + static_cast<int64_t>(ua.sk_row) * R + b_off + ua.T;
-    for (int q = b * (NT / 32) + warp; q < s; q += G * (NT / 32))
+    for (int q = warp * G + b; q < s; q += G * (NT / 32))  // at most a row or two per CTA
       sketch_row_fold(ua.prev_sk, ua.prev_sk_G, ua.prev_sk_ld, q, lane, s, tab, row_scale, dst);
   }
   __syncthreads();
@@ -401,7 +401,9 @@ __device__ __forceinline__ void group_sync(int g) {
 }
 
 /// Table slot of the group jump z^{PR (GRP - 1)} (k_srdct_tables).
-constexpr int jump_slot(int pr, int grp) { return pr * (grp - 1) == 24 ? 4 : (pr * (grp - 1) == 8 ? 5 : 6); }
+constexpr int jump_slot(int pr, int grp) {
+  return pr * (grp - 1) == 24 ? 4 : (pr * (grp - 1) == 8 ? 5 : (pr * (grp - 1) == 28 ? 6 : 7));
+}
 
 template <int SRC, int NI, bool PAIRED, int MAXT, int GRP, int CHK = 0, int PR = kGPairs>
 // GRP = 2 sketches run beside K1 / K2' on the same SMs (split pipeline): <= 85 registers.
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch)
   const uint64_t twoN = 2u * static_cast<uint64_t>(ta.N);
   stamp_begin(ta.stamp);
   trace_mark(ta.trace, 0);
-  for (int k = tid; k < 256; k += kCta) tw[k] = ta.tab[7 * s + k];
+  for (int k = tid; k < 256; k += kCta) tw[k] = ta.tab[8 * s + k];
   for (int q = tid; q < s; q += kCta) {
     zq[q] = ta.tab[2 * s + q];
     zj[q] = ta.tab[jump_slot(PR, GRP) * s + q];
@@ -603,7 +605,8 @@ __global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch)
       if (glow[gg] < 0) continue;
       const double2* S = sm + GRP * (PR * kXS) + gg * 2 * s;
       double sn, cs;
-      const uint64_t ph = (k * static_cast<uint64_t>(ta.r0 + glow[gg] * 2 * PR)) % twoN;
+      const uint64_t kx = k * static_cast<uint64_t>(ta.r0 + glow[gg] * 2 * PR);
+      const uint64_t ph = (twoN & (twoN - 1)) == 0 ? (kx & (twoN - 1)) : kx % twoN;
       sincospi(static_cast<double>(ph) / static_cast<double>(ta.N), &sn, &cs);
       acc = cadd(acc, cmul(make_double2(cs, sn), cadd(cmul(ga, S[q]), cmul(gb, S[s + q]))));
     }
@@ -767,8 +770,8 @@ __global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int 
       sincospi(static_cast<double>(k) / (2.0 * static_cast<double>(N)), &sn, &cs);
       tab[3 * s + q] = make_double2(cs, sn);
       // group jumps z^E = e^{2 i pi k E / N}, E = pairs (groups - 1) in {24, 8, 28}, exact reduction
-      for (int gi = 0; gi < 3; ++gi) {
-        const uint64_t E = gi == 0 ? 24 : (gi == 1 ? 8 : 28);
+      for (int gi = 0; gi < 4; ++gi) {
+        const uint64_t E = gi == 0 ? 24 : (gi == 1 ? 8 : (gi == 2 ? 28 : 16));
         const uint64_t e = (2 * k * E) % twoN;
         sincospi(static_cast<double>(e) / static_cast<double>(N), &sn, &cs);
         tab[(4 + gi) * s + q] = make_double2(cs, sn);
@@ -777,7 +780,7 @@ __global__ void k_srdct_tables(int64_t N, const int64_t* __restrict__ rows, int 
     } else {
       const int k = q - s;
       sincospi(static_cast<double>(k) / 128.0, &sn, &cs);
-      tab[7 * s + k] = make_double2(cs, sn);
+      tab[8 * s + k] = make_double2(cs, sn);
     }
   }
 }
@@ -1003,7 +1006,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
 }  // namespace
 
 void prepare_srdct_tables(Context& c, SketchDev& S) {
-  S.tab.resize(7 * S.s + 256);
+  S.tab.resize(8 * S.s + 256);
   S.uq.resize(S.s);
   k_srdct_tables<<<static_cast<int>((S.s + 256 + 255) / 256), 256, 0, c.stream>>>(S.n, S.rows.get(), static_cast<int>(S.s),
                                                                                  S.tab.get(), S.uq.get());
