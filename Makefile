@@ -30,7 +30,7 @@ $(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -L$(LAPACK_DIR) -l:$(LAPACK_LIB) -Xlinker -rpath=$(LAPACK_DIR) -L/usr/local/cuda/lib64 -lcublas -Xlinker -rpath=/usr/local/cuda/lib64 -ldl -lpthread
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -L$(LAPACK_DIR) -l:$(LAPACK_LIB) -Xlinker -rpath=$(LAPACK_DIR) -L/usr/local/cuda/lib64 -lcublas -Xlinker -rpath=/usr/local/cuda/lib64 -ldl -lpthread -Xlinker --no-undefined
 
 oracle:
 	$(MAKE) -s -C oracle PY=$(PY)

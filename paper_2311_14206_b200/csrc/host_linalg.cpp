@@ -60,7 +60,13 @@ HostQR::AppendInfo HostQR::append(const double* col, i64 len) {  // incremental_
   if (p_ == cap_) grow();
   const i64 p = p_, s = rows_;
   std::copy(col, col + s, m_.data() + p * s);
-  std::vector<double> w(col, col + s), c(static_cast<size_t>(p)), coeffs(static_cast<size_t>(p), 0.0);
+  // scratch reused across appends (one column per Arnoldi step on the host)
+  std::vector<double>& w = ws_;
+  std::vector<double>& c = wc_;
+  std::vector<double>& coeffs = wcoef_;
+  w.assign(col, col + s);
+  c.resize(static_cast<size_t>(p));
+  coeffs.assign(static_cast<size_t>(p), 0.0);
   for (int pass = 0; pass < 2; ++pass) {
     if (p > 0) {
       hgemv(true, s, p, 1.0, q_.data(), s, w.data(), 0.0, c.data());
@@ -129,13 +135,19 @@ double HostQR::solve_cached(double* y) {  // incremental_qr.hpp:107-135
       qtb_valid_[static_cast<size_t>(c)] = 1;
     }
   }
+  // back substitution by columns (contiguous reads of R)
+  std::vector<double>& acc = wc_;
+  acc.resize(used.size());
+  for (size_t q = 0; q < used.size(); ++q) acc[q] = qtb_[static_cast<size_t>(used[q])];
   for (size_t q = used.size(); q-- > 0;) {
     const i64 uq = used[q];
-    double acc = qtb_[static_cast<size_t>(uq)];
-    for (size_t q2 = q + 1; q2 < used.size(); ++q2) acc -= r_[static_cast<size_t>(uq + used[q2] * cap_)] * y[used[q2]];
-    y[uq] = acc / r_[static_cast<size_t>(uq + uq * cap_)];
+    const double yq = acc[q] / r_[static_cast<size_t>(uq + uq * cap_)];
+    y[uq] = yq;
+    const double* rcol = r_.data() + uq * cap_;
+    for (size_t q2 = 0; q2 < q; ++q2) acc[q2] -= rcol[used[q2]] * yq;
   }
-  std::vector<double> res(rhs_);
+  std::vector<double>& res = ws_;
+  res.assign(rhs_.begin(), rhs_.end());
   hgemv(false, s, p_, -1.0, m_.data(), s, y, 1.0, res.data());
   return hnorm(res.data(), s);
 }

@@ -86,6 +86,7 @@ class HostQR {
   std::vector<int> state_;         // 0 ok, 1 excluded, 2 unresolved
   std::vector<double> rhs_, qtb_;
   std::vector<char> qtb_valid_;
+  std::vector<double> ws_, wc_, wcoef_;  // append / solve scratch
 };
 
 /// truncated_svd + fill_pencil + harmonic_pairs. coeffs: p x k_eff.

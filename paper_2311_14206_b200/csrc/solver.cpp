@@ -529,7 +529,8 @@ struct ArnoldiPipeline {
       st.H(j + 1, j) = h_next;
       st.cv[static_cast<size_t>(j + 1)] = 1.0 / h_next;
       const double* sk = rj + RL.sketch_off();
-      for (i64 r = 0; r < s; ++r) st.SV(r, j + 1) = sk[r] / h_next;
+      const double inv_h = 1.0 / h_next;
+      for (i64 r = 0; r < s; ++r) st.SV(r, j + 1) = sk[r] * inv_h;
       ++cnt.sketch_applies;
       for (i64 r = 0; r < s; ++r) {  // arnoldi.hpp:115
         double acc = 0.0;
