@@ -235,12 +235,92 @@ struct HostKrylov {
   bool breakdown = false;
 };
 
+/// Harmonic pencil (and basis condition number) of a cycle, started on a host
+/// thread as soon as the cycle's trigger fires — before the correction and
+/// the verification residual — from copies of the cycle's sketched blocks.
+/// Discarded (thread detached, result dropped) if the cycle continues.
+struct EarlyHarmonic {
+  i64 j = -1, kh = -1;
+  Harmonic hp;
+  bool have_hp = false, have_cond = false;
+  double cond = 1.0, ms = 0.0, cond_ms = 0.0;
+  std::exception_ptr err;
+  std::atomic<bool> done{false};
+  std::thread th;
+  ~EarlyHarmonic() {
+    if (th.joinable()) th.join();
+  }
+};
+
+std::shared_ptr<EarlyHarmonic> start_early_harmonic(const HostKrylov& st, const Recycle& sp, const HostQR* qr, i64 k,
+                                                    double rank_tol) {
+  auto e = std::make_shared<EarlyHarmonic>();
+  const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
+  e->j = j;
+  e->kh = kh;
+  auto SAW = std::make_shared<HMat>(s, kh + j), SW = std::make_shared<HMat>(s, kh + j);
+  for (i64 q = 0; q < kh; ++q) {
+    std::copy(sp.SAU.col(q), sp.SAU.col(q) + s, SAW->col(q));
+    std::copy(sp.SU.col(q), sp.SU.col(q) + s, SW->col(q));
+  }
+  for (i64 i = 0; i < j; ++i) {
+    std::copy(st.SAV.col(i), st.SAV.col(i) + s, SAW->col(kh + i));
+    std::copy(st.SV.col(i), st.SV.col(i) + s, SW->col(kh + i));
+  }
+  std::shared_ptr<HMat> Q, R;
+  if (qr && qr->clean() && qr->cols() == kh + j) {
+    Q = std::make_shared<HMat>(s, kh + j);
+    R = std::make_shared<HMat>(kh + j, kh + j);
+    qr->factors(Q->a.data(), R->a.data());
+  }
+  std::shared_ptr<HMat> B;
+  if (!st.breakdown) {
+    B = std::make_shared<HMat>(s, j + 1);
+    std::copy(st.SV.a.begin(), st.SV.a.begin() + s * (j + 1), B->a.begin());
+  }
+  std::weak_ptr<EarlyHarmonic> self = e;
+  EarlyHarmonic* raw = e.get();
+  // two threads: the basis condition number and the pencil are independent
+  raw->th = std::thread([raw, SAW, SW, Q, R, B, k, rank_tol] {
+    std::exception_ptr cond_err;
+    std::thread tc;
+    if (B) {
+      tc = std::thread([raw, B, &cond_err] {
+        try {
+          const auto t0 = std::chrono::steady_clock::now();
+          raw->cond = cond2(*B);
+          raw->cond_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+          raw->have_cond = true;
+        } catch (...) {
+          cond_err = std::current_exception();
+        }
+      });
+    }
+    try {
+      if (k > 0) {
+        const auto t0 = std::chrono::steady_clock::now();
+        raw->hp = (Q && R) ? harmonic_extract(*SAW, *SW, k, rank_tol, Q.get(), R.get())
+                           : harmonic_extract(*SAW, *SW, k, rank_tol);
+        raw->have_hp = true;
+        raw->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      }
+    } catch (...) {
+      raw->err = std::current_exception();
+    }
+    if (tc.joinable()) tc.join();
+    if (!raw->err && cond_err) raw->err = cond_err;
+    raw->done.store(true, std::memory_order_release);
+  });
+  return e;
+}
+
 struct CycleOut {
   double residual_norm = 0, sres = 0, entry_norm = 0, sketched_entry = 0;
   i64 steps = 0;
   bool converged = false, breakdown = false, have_correction = false;
   double safety = 1.0;
   std::shared_ptr<HostQR> qr;  // the cycle's factorization of [SAU SAV] (reused by the recycle SVD)
+  std::shared_ptr<EarlyHarmonic> early;
 };
 
 struct StepEvent {  // mirrors sdr_iteration_event in the C-ABI
@@ -574,7 +654,7 @@ void host_job_while_pumping(F&& job, const std::function<void()>* pump) {
 void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recycle& sp, i64 k, double rank_tol,
                     Counters& cnt, std::vector<std::string>* notes, Report& rep,
                     const std::function<void()>* pump = nullptr, bool side_stream = false,
-                    const HostQR* qr = nullptr) {  // recycle.hpp:226-289
+                    const HostQR* qr = nullptr, const Harmonic* pre = nullptr) {  // recycle.hpp:226-289
   const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
   if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
   HMat SAW(s, kh + j), SW(s, kh + j);
@@ -587,7 +667,9 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     std::copy(st.SV.col(i), st.SV.col(i) + s, SW.col(kh + i));
   }
   Harmonic hp;
-  {
+  if (pre) {
+    hp = *pre;
+  } else {
     double ms = 0.0;
     host_job_while_pumping(
         [&] {
@@ -832,6 +914,8 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
     }
     const bool last = jj == m || st.breakdown;
     if (sres < tol_abs / out.safety || last) {
+      // the cycle very likely ends here: start its restart bookkeeping now
+      out.early = start_early_harmonic(st, space, qr.get(), cfg.k, cfg.rank_tol);
       // correction = V(:,0:j) y_tail + U y_head (solver.hpp:197-198), on the device
       PhaseTimer pt_check(rep, "check");
       std::vector<const double*> in;
@@ -865,6 +949,14 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
         if (sres > 0.0) out.safety = std::max(out.safety, out.residual_norm / sres);
         if (last) done = true;
       }
+      if (!done && out.early) {  // the cycle goes on: let the thread finish on its own
+        out.early->th.detach();
+        auto keep = out.early;
+        std::thread([keep] {
+          while (!keep->done.load(std::memory_order_acquire)) std::this_thread::sleep_for(std::chrono::microseconds(200));
+        }).detach();
+        out.early.reset();
+      }
     }
   }
   out.steps = st.j;
@@ -889,13 +981,43 @@ void finish_cycle(Context& c, Workspace& w, const ArnoldiPipeline& ap, const Cyc
   cs.exit_sres = out.sres;
   cs.exit_residual = out.residual_norm;
   cs.safety_after = out.safety;
-  // the basis condition number (an SVD of SV) runs on its own host thread,
-  // concurrently with the harmonic update below
+  const bool want_bc = st.j >= 1 && !st.breakdown;
+  // early pencil from the trigger point (run_cycle) when it matches this cycle
+  EarlyHarmonic* early = (out.early && out.early->j == st.j && out.early->kh == space.dim()) ? out.early.get() : nullptr;
+  if (early) {
+    while (!early->done.load(std::memory_order_acquire)) {
+      if (pump) (*pump)();
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    if (early->th.joinable()) early->th.join();
+    if (early->err) std::rethrow_exception(early->err);
+    if (want_bc && early->have_cond) {
+      cs.basis_cond = early->cond;
+      rep.phase_ms["basis_cond"] += early->cond_ms;
+    }
+    if (cfg.k > 0 && st.j >= 1) {
+      rep.phase_ms["recycle_harmonic"] += early->ms;
+      rep.phase_ms["harmonic_svd"] += early->hp.svd_ms;
+      rep.phase_ms["harmonic_schur"] += early->hp.schur_ms;
+      rep.phase_ms["harmonic_rest"] += early->hp.rest_ms;
+      std::vector<std::string> notes;
+      PhaseTimer pt(rep, "recycle");
+      update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep, pump, side_stream, out.qr.get(),
+                     early->have_hp ? &early->hp : nullptr);
+      cs.deflation_rank = space.dim();
+      for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
+    } else if (cfg.k == 0) {
+      space.clear();
+    }
+    rep.cycle_stats.push_back(cs);
+    return;
+  }
+  // otherwise: the basis condition number (an SVD of SV) on its own host
+  // thread, concurrently with the harmonic update below
   HMat B;
   double bc_ms = 0.0;
   std::exception_ptr bc_err;
   std::thread bc_thread;
-  const bool want_bc = st.j >= 1 && !st.breakdown;
   if (want_bc) {
     B = HMat(s, st.j + 1);
     std::copy(st.SV.a.begin(), st.SV.a.begin() + s * (st.j + 1), B.a.begin());
