@@ -477,9 +477,12 @@ __global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch)
     if (aa < ta.L) {
       if constexpr (SRC == kSrcUpdate) {
         // loads in chunks of CH rows, all issued before the chunk's math
-        constexpr int CH = CHK > 0 ? CHK : (MAXT <= 2 ? 2 : 1);
+        // NI = M/16 rows of 16 per column pair (M = 128 on one GPU; 64, 32, 16
+        // on 2, 4, 8 ranks, where F = 2N/L stays 256)
+        constexpr int CH0 = CHK > 0 ? CHK : (MAXT <= 2 ? 2 : 1);
+        constexpr int CH = CH0 < NI ? CH0 : NI;
 #pragma unroll
-        for (int i0 = 0; i0 < 8; i0 += CH) {
+        for (int i0 = 0; i0 < NI; i0 += CH) {
           double2 yv[CH], wv[CH][MAXT];
           uint32_t bits[CH];
 #pragma unroll
@@ -1017,7 +1020,8 @@ void prepare_srdct_tables(Context& c, SketchDev& S) {
 bool update_sketch_eligible(const SketchDev& S, const VecLayout& lay, int need, int64_t row_begin, int64_t ldv) {
   if (S.kind != kSrdct || need > 4) return false;
   const SrdctPlan p = plan_srdct(S.n, lay.nloc);
-  return tiles_eligible(S, p) && p.M == 128 && p.L % 2 == 0 && row_begin % 2 == 0 && lay.own_off % 2 == 0 &&
+  return tiles_eligible(S, p) && (p.M == 128 || p.M == 64 || p.M == 32 || p.M == 16) && p.L % 2 == 0 &&
+         row_begin % 2 == 0 && lay.own_off % 2 == 0 &&
          ldv % 2 == 0;
 }
 
@@ -1061,12 +1065,29 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
     const char* e = std::getenv("SDR_K2_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
-  if (need <= 2 && variant == 1)
-    launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
-  else if (need <= 2)
-    launch_tiles<kSrcUpdate, 8, true, 2, 2, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
-  else
-    launch_tiles<kSrcUpdate, 8, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  if (p.M == 128) {
+    if (need <= 2 && variant == 1)
+      launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+    else if (need <= 2)
+      launch_tiles<kSrcUpdate, 8, true, 2, 2, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+    else
+      launch_tiles<kSrcUpdate, 8, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  } else if (p.M == 64) {  // the per-rank row blocks of a 2..8-rank z-slab run
+    if (need <= 2)
+      launch_tiles<kSrcUpdate, 4, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+    else
+      launch_tiles<kSrcUpdate, 4, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  } else if (p.M == 32) {
+    if (need <= 2)
+      launch_tiles<kSrcUpdate, 2, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+    else
+      launch_tiles<kSrcUpdate, 2, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  } else {
+    if (need <= 2)
+      launch_tiles<kSrcUpdate, 1, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+    else
+      launch_tiles<kSrcUpdate, 1, true, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+  }
   return true;
 }
 
