@@ -61,6 +61,31 @@ def test_spmv_matches_oracle(sk, O, case):
         assert rel(A.apply(x), Ao.apply(x)) <= REL
 
 
+@pytest.mark.parametrize("offsets,rows,cols,fmt", [
+    ((-1, 0, 1), 1000, 1000, "dia"),                      # runtime D = 3
+    ((-200, -1, 0, 1, 200), 4000, 4000, "dia"),           # compile-time D = 5
+    (tuple(range(-4, 5)), 2000, 2000, "dia"),             # runtime D = 9
+    (tuple(range(-8, 9)), 2000, 2000, "sell"),            # 17 diagonals: SELL-32
+    ((-3, 0, 2, 7), 300, 500, "dia"),                     # rectangular
+])
+def test_banded_storage_forms_match_oracle(sk, O, offsets, rows, cols, fmt):
+    """SELL-DIA (compile-time and runtime diagonal counts, rectangular, gaps at
+    the matrix edges) and the SELL-32 fallback against the oracle's CSR."""
+    rng = np.random.default_rng(len(offsets) + rows)
+    r, c = [], []
+    for o in offsets:
+        i = np.arange(max(0, -o), min(rows, cols - o))
+        r.append(i)
+        c.append(i + o)
+    r, c = np.concatenate(r), np.concatenate(c)
+    M = O.SparseMatrix.from_triplets(rows, cols, r, c, rng.standard_normal(r.size))
+    off, col, val = M.csr()
+    A = sk.SparseMatrix(rows, cols, off, col, val)
+    assert A.storage["format"] == fmt
+    x = O.gaussian_vector(cols, 9)
+    assert rel(A.apply(x), M.apply(x)) <= REL
+
+
 def test_device_generated_operator_matches_host_csr(sk, O):
     n = 48
     Ad = sk.SparseMatrix.convdiff3d_device(n, 100.0, 50.0, 25.0)
