@@ -251,6 +251,23 @@ SDR_API int sdr_solve_sequence(sdr_ctx* ctx, int32_t nprob, const sdr_csr* const
                                const sdr_config* cfg, const sdr_sketch* sketch, sdr_recycle* space,
                                double* const* x_outs, sdr_report** reports_out);
 
+/* ----------------------------------------------------------- baseline --
+ * Classical restarted GMRES, the reference's comparison point
+ * (baseline.hpp:24-39 BaselineConfig, :51-216 baseline_gmres): full
+ * orthogonalisation against the whole basis every step, Givens rotations,
+ * one verification product per cycle. Same statuses / notes / counters
+ * (one inner product per MGS dot) as the reference; m <= 255 on the device.
+ * b, x0 (may be NULL), x_out: this rank's block, host or device. */
+typedef struct {
+  int64_t m;
+  double tol;
+  int32_t max_restarts;
+  double breakdown_tol;
+} sdr_baseline_config;
+SDR_API int sdr_baseline_config_default(sdr_baseline_config* cfg);
+SDR_API int sdr_baseline_gmres(sdr_ctx* ctx, const sdr_csr* A, const double* b, const double* x0,
+                               const sdr_baseline_config* cfg, double* x_out, sdr_report** report_out);
+
 /* SolveReport accessors (report.hpp:50-63). */
 SDR_API int sdr_report_destroy(sdr_report* r);
 SDR_API int sdr_report_summary(const sdr_report* r, int* status, int64_t* iterations, int32_t* cycles,

@@ -302,6 +302,26 @@ void* orc_solve(void* csr, const double* b, int64_t n, const orc_config* c, void
   return rep;
 }
 
+void* orc_baseline_gmres(void* csr, const double* b, int64_t n, int64_t m, double tol, int32_t max_restarts,
+                         double breakdown_tol, const double* x0, double* x_out) {
+  SolveReport* rep = nullptr;
+  guard([&] {
+    const SparseMatrix& A = *static_cast<Csr*>(csr)->A;
+    OperatorRef op(A);
+    Vec bb(b, b + n), xx0;
+    if (x0) xx0.assign(x0, x0 + n);
+    BaselineConfig cfg;
+    cfg.m = m;
+    cfg.tol = tol;
+    cfg.max_restarts = max_restarts;
+    cfg.breakdown_tol = breakdown_tol;
+    SolveResult r = baseline_gmres(op, bb, cfg, x0 ? &xx0 : nullptr);
+    std::memcpy(x_out, r.x.data(), sizeof(double) * r.x.size());
+    rep = new SolveReport(std::move(r.report));
+  });
+  return rep;
+}
+
 int orc_solve_sequence(int32_t nprob, void** mats, const double** rhs, const double** x0s, const double* tols,
                        int32_t shared, const orc_config* c, void* sketch, void* space, double** x_outs,
                        void** reports_out) {

@@ -90,6 +90,7 @@ def lib():
             "orc_space_get": (None, [vp, P(f64), P(f64), P(f64)]),
             "orc_space_set": (None, [vp, i64, i64, i64, P(f64), P(f64), P(f64), C.c_int]),
             "orc_solve": (vp, [vp, P(f64), i64, P(orc_config), vp, vp, P(f64), P(f64)]),
+            "orc_baseline_gmres": (vp, [vp, P(f64), i64, i64, f64, i32, f64, P(f64), P(f64)]),
             "orc_solve_sequence": (C.c_int, [i32, P(vp), P(P(f64)), P(P(f64)), P(f64), i32, P(orc_config),
                                              vp, vp, P(P(f64)), P(vp)]),
             "orc_report_status": (C.c_int, [vp]), "orc_report_iterations": (i64, [vp]),
@@ -498,6 +499,19 @@ def solve(A: SparseMatrix, b, cfg: SolverConfig, space: RecycleSpace | None = No
     c = cfg.c()
     h = lib().orc_solve(A._h, pb, len(b), C.byref(c), space._h if space else None,
                         sketch._h if sketch else None, px0, _f64(x)[1])
+    if not h:
+        raise ValueError(_err())
+    return x, _report(h)
+
+
+def baseline_gmres(A: SparseMatrix, b, m=100, tol=1e-6, max_restarts=10, breakdown_tol=1e-14, x0=None):
+    """Classical restarted GMRES (baseline.hpp:51-216)."""
+    b, pb = _f64(b)
+    x = np.empty(len(b))
+    px0 = None
+    if x0 is not None:
+        x0, px0 = _f64(x0)
+    h = lib().orc_baseline_gmres(A._h, pb, len(b), m, tol, max_restarts, breakdown_tol, px0, _f64(x)[1])
     if not h:
         raise ValueError(_err())
     return x, _report(h)

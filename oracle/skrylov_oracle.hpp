@@ -439,6 +439,71 @@ inline std::uint64_t mix64(std::uint64_t z) {
   return z ^ (z >> 31);
 }
 
+/// min ||A y - b|| by Householder QR with column pivoting, the basic
+/// solution for a rank-deficient A (the fallback of baseline.hpp:175-177,
+/// Eigen's colPivHouseholderQr: rank threshold eps * min(rows, cols) * |r_max|).
+inline Vec least_squares(Mat A, Vec b) {
+  const Index m = A.rows, n = A.cols;
+  std::vector<Index> perm(static_cast<size_t>(n));
+  for (Index j = 0; j < n; ++j) perm[static_cast<size_t>(j)] = j;
+  std::vector<double> cn(static_cast<size_t>(n));
+  for (Index j = 0; j < n; ++j) cn[static_cast<size_t>(j)] = dot(A.col(j), A.col(j), m);
+  const Index kmax = std::min(m, n);
+  double rmax = 0.0;
+  Index rank = 0;
+  for (Index k = 0; k < kmax; ++k) {
+    Index piv = k;  // the column of largest remaining norm
+    for (Index j = k + 1; j < n; ++j)
+      if (cn[static_cast<size_t>(j)] > cn[static_cast<size_t>(piv)]) piv = j;
+    if (piv != k) {
+      for (Index i = 0; i < m; ++i) std::swap(A(i, k), A(i, piv));
+      std::swap(cn[static_cast<size_t>(k)], cn[static_cast<size_t>(piv)]);
+      std::swap(perm[static_cast<size_t>(k)], perm[static_cast<size_t>(piv)]);
+    }
+    double nrm = 0.0;
+    for (Index i = k; i < m; ++i) nrm += A(i, k) * A(i, k);
+    nrm = std::sqrt(nrm);
+    if (nrm > 0.0) {
+      const double alpha = A(k, k) > 0.0 ? -nrm : nrm;
+      std::vector<double> v(static_cast<size_t>(m - k));
+      for (Index i = k; i < m; ++i) v[static_cast<size_t>(i - k)] = A(i, k);
+      v[0] -= alpha;
+      const double vn2 = dot(v.data(), v.data(), m - k);
+      if (vn2 > 0.0) {
+        for (Index j = k; j < n; ++j) {
+          double d = 0.0;
+          for (Index i = k; i < m; ++i) d += v[static_cast<size_t>(i - k)] * A(i, j);
+          d *= 2.0 / vn2;
+          for (Index i = k; i < m; ++i) A(i, j) -= d * v[static_cast<size_t>(i - k)];
+        }
+        double d = 0.0;
+        for (Index i = k; i < m; ++i) d += v[static_cast<size_t>(i - k)] * b[static_cast<size_t>(i)];
+        d *= 2.0 / vn2;
+        for (Index i = k; i < m; ++i) b[static_cast<size_t>(i)] -= d * v[static_cast<size_t>(i - k)];
+      }
+    }
+    rmax = std::max(rmax, std::abs(A(k, k)));
+    for (Index j = k + 1; j < n; ++j) {  // downdate the remaining column norms
+      double s = 0.0;
+      for (Index i = k + 1; i < m; ++i) s += A(i, j) * A(i, j);
+      cn[static_cast<size_t>(j)] = s;
+    }
+  }
+  const double thr = std::numeric_limits<double>::epsilon() * static_cast<double>(kmax) * rmax;
+  for (Index k = 0; k < kmax; ++k)
+    if (std::abs(A(k, k)) > thr) rank = k + 1;
+    else break;
+  Vec z(static_cast<size_t>(n), 0.0);
+  for (Index i = rank - 1; i >= 0; --i) {
+    double acc = b[static_cast<size_t>(i)];
+    for (Index j = i + 1; j < rank; ++j) acc -= A(i, j) * z[static_cast<size_t>(j)];
+    z[static_cast<size_t>(i)] = acc / A(i, i);
+  }
+  Vec y(static_cast<size_t>(n), 0.0);
+  for (Index j = 0; j < n; ++j) y[static_cast<size_t>(perm[static_cast<size_t>(j)])] = z[static_cast<size_t>(j)];
+  return y;
+}
+
 }  // namespace detail
 
 enum class SketchKind { subsampled_dct = 0, identity = 1, sparse_sign = 2 };
@@ -1405,6 +1470,180 @@ inline SequenceResult solve_sequence(const ProblemSequence& seq, const SolverCon
     prev = prob.matrix.get();
   }
   return result;
+}
+
+// ------------------------------------------------------------- baseline ---
+// Classical restarted GMRES, the reference's comparison point
+// (baseline.hpp:51-216): full modified Gram-Schmidt against the whole basis,
+// Givens rotations on the Hessenberg column, one verification product per
+// cycle. Statuses / counters / notes as the reference.
+
+struct BaselineConfig {
+  Index m = 100;
+  double tol = 1e-6;
+  int max_restarts = 10;
+  double breakdown_tol = 1e-14;
+};
+
+inline SolveResult baseline_gmres(const OperatorRef& A, const Vec& b, const BaselineConfig& cfg,
+                                  const Vec* x0 = nullptr) {
+  if (cfg.m < 1) throw std::invalid_argument("BaselineConfig: m must be at least 1");
+  if (!(cfg.tol > 0.0 && cfg.tol < 1.0)) throw std::invalid_argument("BaselineConfig: tol must lie in (0, 1)");
+  if (cfg.max_restarts < 1) throw std::invalid_argument("BaselineConfig: max_restarts must be at least 1");
+  if (!(cfg.breakdown_tol >= 0.0)) throw std::invalid_argument("BaselineConfig: breakdown_tol must be >= 0");
+  const Index n = static_cast<Index>(b.size());
+  if (A.rows() != A.cols())
+    throw std::invalid_argument("baseline_gmres: operator must be square, got " + std::to_string(A.rows()) + " x " +
+                                std::to_string(A.cols()));
+  if (n != A.rows())
+    throw std::invalid_argument("baseline_gmres: rhs length " + std::to_string(n) + " does not match operator size " +
+                                std::to_string(A.rows()));
+  if (x0 && static_cast<Index>(x0->size()) != n)
+    throw std::invalid_argument("baseline_gmres: x0 length " + std::to_string(x0->size()) +
+                                " does not match rhs length " + std::to_string(n));
+  const auto t0 = std::chrono::steady_clock::now();
+  SolveResult out;
+  SolveReport& rep = out.report;
+  rep.rhs_norm = norm(b.data(), n);
+  ++rep.counters.inner_products;
+  const double tol_abs = cfg.tol * rep.rhs_norm;
+  out.x = x0 ? *x0 : Vec(static_cast<size_t>(n), 0.0);
+  Vec r = b;
+  bool x0_nonzero = false;
+  if (x0)
+    for (double v : *x0) x0_nonzero = x0_nonzero || v != 0.0;
+  if (x0_nonzero) {
+    Vec ax(static_cast<size_t>(n));
+    A.apply_raw(x0->data(), ax.data());
+    ++rep.counters.matvecs;
+    for (Index i = 0; i < n; ++i) r[static_cast<size_t>(i)] -= ax[static_cast<size_t>(i)];
+  }
+  const Index m = cfg.m;
+  std::vector<Vec> V(static_cast<size_t>(m + 1), Vec(static_cast<size_t>(n)));
+  Mat H(m + 1, m), R(m + 1, m);
+  Vec g(static_cast<size_t>(m + 1)), cs(static_cast<size_t>(m)), sn(static_cast<size_t>(m)), w(static_cast<size_t>(n));
+  double res_norm = std::numeric_limits<double>::quiet_NaN();
+  bool have = false;
+  for (int cycle = 1; cycle <= cfg.max_restarts; ++cycle) {
+    const double beta = norm(r.data(), n);
+    ++rep.counters.inner_products;
+    if (beta == 0.0) {
+      rep.status = SolveStatus::converged;
+      res_norm = 0.0;
+      have = true;
+      break;
+    }
+    rep.cycles = cycle;
+    for (Index i = 0; i < n; ++i) V[0][static_cast<size_t>(i)] = r[static_cast<size_t>(i)] / beta;
+    H = Mat(m + 1, m);
+    R = Mat(m + 1, m);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    Index p = 0;
+    bool breakdown = false;
+    double est = beta;
+    while (p < m) {
+      const Index q = p;
+      A.apply_raw(V[static_cast<size_t>(q)].data(), w.data());
+      ++rep.counters.matvecs;
+      for (Index i = 0; i <= q; ++i) {  // modified Gram-Schmidt over the whole basis
+        const double h = dot(V[static_cast<size_t>(i)].data(), w.data(), n);
+        ++rep.counters.inner_products;
+        H(i, q) = h;
+        for (Index e = 0; e < n; ++e) w[static_cast<size_t>(e)] -= h * V[static_cast<size_t>(i)][static_cast<size_t>(e)];
+      }
+      const double h_next = norm(w.data(), n);
+      ++rep.counters.inner_products;
+      H(q + 1, q) = h_next;
+      double cn = 0.0;
+      for (Index i = 0; i <= q + 1; ++i) cn += H(i, q) * H(i, q);
+      cn = std::sqrt(cn);
+      if (h_next <= cfg.breakdown_tol * cn) {
+        H(q + 1, q) = 0.0;
+        breakdown = true;
+      } else {
+        for (Index e = 0; e < n; ++e) V[static_cast<size_t>(q + 1)][static_cast<size_t>(e)] = w[static_cast<size_t>(e)] / h_next;
+      }
+      for (Index i = 0; i <= q + 1; ++i) R(i, q) = H(i, q);
+      for (Index i = 0; i < q; ++i) {  // earlier rotations
+        const double a = R(i, q), bb = R(i + 1, q);
+        R(i, q) = cs[static_cast<size_t>(i)] * a + sn[static_cast<size_t>(i)] * bb;
+        R(i + 1, q) = -sn[static_cast<size_t>(i)] * a + cs[static_cast<size_t>(i)] * bb;
+      }
+      const double a = R(q, q), bb = R(q + 1, q), rr = std::hypot(a, bb);
+      const double c = rr > 0.0 ? a / rr : 1.0, sg = rr > 0.0 ? bb / rr : 0.0;
+      cs[static_cast<size_t>(q)] = c;
+      sn[static_cast<size_t>(q)] = sg;
+      R(q, q) = rr;
+      R(q + 1, q) = 0.0;
+      const double ga = g[static_cast<size_t>(q)];
+      g[static_cast<size_t>(q)] = c * ga;
+      g[static_cast<size_t>(q + 1)] = -sg * ga;
+      est = std::abs(g[static_cast<size_t>(q + 1)]);
+      ++p;
+      rep.sketched_residuals.push_back({rep.iterations + p, est});
+      if (est < tol_abs || breakdown) break;
+    }
+    // cycle iterate: R y = g (dense least squares on H if a pivot vanished)
+    Vec y(static_cast<size_t>(p), 0.0);
+    bool diag_ok = true;
+    for (Index i = 0; i < p; ++i) diag_ok = diag_ok && R(i, i) != 0.0;
+    if (diag_ok) {
+      for (Index i = p - 1; i >= 0; --i) {
+        double acc = g[static_cast<size_t>(i)];
+        for (Index k2 = i + 1; k2 < p; ++k2) acc -= R(i, k2) * y[static_cast<size_t>(k2)];
+        y[static_cast<size_t>(i)] = acc / R(i, i);
+      }
+    } else {
+      Mat Hp(p + 1, p);
+      for (Index jj = 0; jj < p; ++jj)
+        for (Index i = 0; i <= p; ++i) Hp(i, jj) = H(i, jj);
+      Vec rhs(static_cast<size_t>(p + 1), 0.0);
+      rhs[0] = beta;
+      y = detail::least_squares(Hp, rhs);
+    }
+    Vec corr(static_cast<size_t>(n), 0.0);
+    for (Index jj = 0; jj < p; ++jj)
+      for (Index e = 0; e < n; ++e)
+        corr[static_cast<size_t>(e)] += V[static_cast<size_t>(jj)][static_cast<size_t>(e)] * y[static_cast<size_t>(jj)];
+    for (Index e = 0; e < n; ++e) out.x[static_cast<size_t>(e)] += corr[static_cast<size_t>(e)];
+    Vec acorr(static_cast<size_t>(n));
+    A.apply_raw(corr.data(), acorr.data());
+    ++rep.counters.matvecs;
+    for (Index e = 0; e < n; ++e) r[static_cast<size_t>(e)] -= acorr[static_cast<size_t>(e)];
+    res_norm = norm(r.data(), n);
+    ++rep.counters.inner_products;
+    have = true;
+    rep.iterations += p;
+    rep.true_residuals.push_back({rep.iterations, res_norm});
+    CycleStats st;
+    st.steps = p;
+    st.entry_residual = beta;
+    st.sketched_entry = beta;
+    st.exit_sres = est;
+    st.exit_residual = res_norm;
+    st.safety_after = 1.0;
+    rep.cycle_stats.push_back(st);
+    if (res_norm < tol_abs) {
+      rep.status = SolveStatus::converged;
+      break;
+    }
+    if (breakdown) {
+      rep.status = SolveStatus::breakdown;
+      rep.notes.push_back("cycle " + std::to_string(cycle) + ": basis exhausted before reaching the target");
+      break;
+    }
+    if (p == m && est > 0.99 * beta) {
+      rep.status = SolveStatus::diverged;
+      rep.notes.push_back("cycle " + std::to_string(cycle) +
+                          ": residual estimate improved by less than 1% over a full cycle");
+      break;
+    }
+    if (cycle == cfg.max_restarts) rep.status = SolveStatus::max_restarts;
+  }
+  if (have) rep.final_relative_residual = rep.rhs_norm > 0.0 ? res_norm / rep.rhs_norm : res_norm;
+  rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return out;
 }
 
 }  // namespace oracle

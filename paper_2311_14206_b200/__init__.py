@@ -32,11 +32,12 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
-from ._capi import sdr_config, sdr_callbacks, ITER_CB, RES_CB
+from ._capi import sdr_config, sdr_baseline_config, sdr_callbacks, ITER_CB, RES_CB
 
 __all__ = [
     "Context", "default_context", "SparseMatrix", "SketchOperator", "SolverConfig", "RecycleSpace", "SolveReport",
-    "SolveResult", "SequenceResult", "ProblemInstance", "solve", "solve_sequence", "IncrementalQR", "harmonic_pairs",
+    "SolveResult", "SequenceResult", "ProblemInstance", "solve", "solve_sequence",
+    "BaselineConfig", "BaselineResult", "baseline_gmres", "IncrementalQR", "harmonic_pairs",
     "gaussian_vector", "gen_convdiff", "gen_convdiff2d", "gen_convdiff3d", "sparse_sign_entries", "partition_halo",
     "partition_rows", "SdrError", "CudaError",
 ]
@@ -707,6 +708,49 @@ def solve(A: SparseMatrix, b, cfg: SolverConfig, space: RecycleSpace | None = No
     _check(_lib.sdr_solve(ctx._h, A._h, pb, px0, C.byref(c), space._h, sketch._h if sketch else None,
                           C.byref(cb) if cb is not None else None, px, C.byref(rep)))
     return SolveResult(x, _report(rep), space)
+
+
+@dataclass
+class BaselineConfig:
+    """baseline.hpp:24-39 (same defaults)."""
+    m: int = 100
+    tol: float = 1e-6
+    max_restarts: int = 10
+    breakdown_tol: float = 1e-14
+
+    def c(self):
+        return sdr_baseline_config(self.m, self.tol, self.max_restarts, self.breakdown_tol)
+
+
+@dataclass
+class BaselineResult:
+    """baseline.hpp:41-44."""
+    x: object
+    report: SolveReport
+
+
+def baseline_gmres(A: SparseMatrix, b, cfg: BaselineConfig | None = None, x0=None) -> BaselineResult:
+    """Classical restarted GMRES on the device (baseline.hpp:51-216): the
+    reference's comparison point. b / x0: numpy or float64 CUDA tensors."""
+    cfg = cfg or BaselineConfig()
+    ctx = A.ctx
+    kb, pb, nb = _ptr(b)
+    if nb != A.local_rows:
+        raise ValueError(f"baseline_gmres: rhs length {nb} does not match operator size {A.local_rows}")
+    kx0, px0, nx0 = _ptr(x0)
+    if x0 is not None and nx0 != nb:
+        raise ValueError(f"baseline_gmres: x0 length {nx0} does not match rhs length {nb}")
+    if _is_torch_cuda(b):
+        import torch
+        x = torch.empty(nb, dtype=torch.float64, device=b.device)
+        px = C.c_void_p(x.data_ptr())
+    else:
+        x = np.empty(nb)
+        px = x.ctypes.data_as(C.c_void_p)
+    c = cfg.c()
+    rep = C.c_void_p()
+    _check(_lib.sdr_baseline_gmres(ctx._h, A._h, pb, px0, C.byref(c), px, C.byref(rep)))
+    return BaselineResult(x, _report(rep))
 
 
 @dataclass

@@ -25,6 +25,10 @@ class sdr_config(C.Structure):
                 ("breakdown_tol", f64)]
 
 
+class sdr_baseline_config(C.Structure):
+    _fields_ = [("m", i64), ("tol", f64), ("max_restarts", i32), ("breakdown_tol", f64)]
+
+
 class sdr_iteration_event(C.Structure):
     _fields_ = [("cycle", i32), ("step", i64), ("iteration", i64), ("sres", f64), ("new_basis_sketch_norm", f64),
                 ("y", P(f64)), ("y_len", i64), ("space_dim", i64)]
@@ -101,6 +105,8 @@ SIGNATURES = {
     "sdr_recycle_refresh": (cint, [vp, vp, vp, vp, cint, vp]),
     "sdr_krylov_run": (cint, [vp, vp, vp, vp, i64, i64, i64, f64, vp, vp, vp, vp, P(i64), P(cint), P(f64), vp]),
     "sdr_solve": (cint, [vp, vp, vp, vp, P(sdr_config), vp, vp, P(sdr_callbacks), vp, P(vp)]),
+    "sdr_baseline_config_default": (cint, [P(sdr_baseline_config)]),
+    "sdr_baseline_gmres": (cint, [vp, vp, vp, vp, P(sdr_baseline_config), vp, P(vp)]),
     "sdr_solve_sequence": (cint, [vp, i32, vp, vp, vp, vp, i32, P(sdr_config), vp, vp, vp, vp]),
     "sdr_report_destroy": (cint, [vp]),
     "sdr_report_summary": (cint, [vp, P(cint), P(i64), P(i32), P(f64), P(f64), P(f64)]),

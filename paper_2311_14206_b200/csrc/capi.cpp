@@ -2,6 +2,7 @@
 // pointer staging. No exception crosses this boundary.
 #include "../../include/sdr_b200.h"
 
+#include "baseline.hpp"
 #include "context.hpp"
 #include "host_linalg.hpp"
 #include "operator.hpp"
@@ -807,6 +808,44 @@ int sdr_solve(sdr_ctx* ctx, const sdr_csr* A, const double* b, const double* x0,
     DeviceOut xo(x_out, n);
     solve(c, op, bin.ptr, x0in.ptr, nz, to_cfg(cfg), sp, sketch ? sketch->S.get() : nullptr, cb ? &cbs : nullptr, xo.ptr,
           rep->r);
+    xo.finish(c);
+    if (report_out) *report_out = rep.release();
+  });
+}
+
+int sdr_baseline_config_default(sdr_baseline_config* cfg) {
+  return guard([&] {
+    need(cfg, "cfg");
+    BaselineConfig d;
+    cfg->m = d.m;
+    cfg->tol = d.tol;
+    cfg->max_restarts = d.max_restarts;
+    cfg->breakdown_tol = d.breakdown_tol;
+  });
+}
+
+int sdr_baseline_gmres(sdr_ctx* ctx, const sdr_csr* A, const double* b, const double* x0,
+                       const sdr_baseline_config* cfg, double* x_out, sdr_report** report_out) {
+  return guard([&] {  // baseline.hpp:51-216
+    need(ctx, "ctx");
+    need(A, "A");
+    need(b, "b");
+    need(cfg, "cfg");
+    Context& c = *ctx->c;
+    const auto& op = *A->op;
+    const i64 n = op.local_rows;
+    BaselineConfig bc;
+    bc.m = cfg->m;
+    bc.tol = cfg->tol;
+    bc.max_restarts = cfg->max_restarts;
+    bc.breakdown_tol = cfg->breakdown_tol;
+    bc.validate();
+    auto rep = std::make_unique<sdr_report>();
+    DeviceIn bin(c, b, n);
+    DeviceIn x0in(c, x0, n);
+    const bool nz = x0 && host_nonzero(c, x0, n);
+    DeviceOut xo(x_out, n);
+    baseline_solve(c, op, bin.ptr, x0in.ptr, nz, bc, xo.ptr, rep->r);
     xo.finish(c);
     if (report_out) *report_out = rep.release();
   });

@@ -68,6 +68,8 @@ int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t 
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
                         double* coef, double* partials_out = nullptr, int max_blocks_per_sm = 0);
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2);
+/// y = A x, skipped (no stores) when *stop != 0 on the device.
+void launch_spmv_guarded(Context& c, const SellView& A, const double* x_ext, double* y, const int* stop);
 
 // ---- Arnoldi update (arnoldi.cu). coef_ready: coefficients already formed
 // by K1 (single GPU); null: formed in the K2 prologue from allreduced records.

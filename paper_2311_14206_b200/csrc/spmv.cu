@@ -18,6 +18,8 @@
 //   MODE 1  y = A w_j, plus ||y||^2 and y.w_{j-d} for the MGS window (K1);
 //           on one GPU the last CTA also forms the MGS coefficients (mgs.cuh)
 //   MODE 2  r = b - A x, plus ||r||^2                (verification, K6)
+//   MODE 3  y = A x unless the int flag at aux is set (speculatively
+//           enqueued steps of the classical baseline, baseline.cu)
 #include "kernels.hpp"
 #include "mgs.cuh"
 #include "reduce.cuh"
@@ -129,6 +131,8 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
   if (FMT != 0 && gw < A.nslices && lane < D) nx_off = __ldg(A.doff + gw * D + lane);
   pdl_trigger();  // the next kernel may start its constant-data prologue
   pdl_wait();     // x / the window vectors come from the previous kernel
+  if constexpr (MODE == 3)
+    if (*reinterpret_cast<const volatile int*>(aux)) return;
   for (int64_t sl = gw; sl < A.nslices; sl += nwarps) {
     const int cur_off = nx_off;
     if (FMT != 0 && sl + nwarps < A.nslices && lane < D) nx_off = __ldg(A.doff + (sl + nwarps) * D + lane);
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
     }
     const double s = slice_row_sum<FMT>(A, x_ext, sl, row, halo_lo, lane, cur_off);
     if (live) {
-      if constexpr (MODE == 0) {
+      if constexpr (MODE == 0 || MODE == 3) {
         y[row] = s;
       } else if constexpr (MODE == 1) {
         y[row] = s;
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
       }
     }
   }
-  if constexpr (MODE != 0) {
+  if constexpr (MODE == 1 || MODE == 2) {
     const int nv = MODE == 1 ? 1 + nwin : 1;
     block_partials<NV>(acc, nv, partials);
     if (counter == nullptr) {  // deferred: the consumer folds the partials
@@ -197,7 +201,7 @@ int launch_impl(Context& c, const char* name, const SellView& A, const double* x
                 const MgsArgs& mg, double* partials_out, int max_per_sm) {
   auto kern = k_sell_spmv<MODE, NV, FMT>;
   const int g = resident_grid(c, kern, blocks_for(A.nslices), max_per_sm);
-  double* part = partials_out ? partials_out : (MODE ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
+  double* part = partials_out ? partials_out : ((MODE == 1 || MODE == 2) ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
   TimedLaunch t(c, name);
   if (partials_out) {  // deferred step pipeline: programmatic dependent launch
     cudaLaunchConfig_t cfg{};
@@ -256,6 +260,12 @@ int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t 
                              c.counters() + 0, recA, mg, partials_out, max_per_sm);
   else
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
+}
+
+void launch_spmv_guarded(Context& c, const SellView& A, const double* x_ext, double* y, const int* stop) {
+  if (A.nrows == 0) return;
+  launch_fmt<3, 1>(c, "baseline_spmv", A, x_ext, y, reinterpret_cast<const double*>(stop), 0, 0, A.halo_lo, 0, 0,
+                   nullptr, nullptr, MgsArgs{});
 }
 
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2) {

@@ -323,3 +323,93 @@ def test_sequence_recycling_cuts_iterations(O):  # test_sequence.cpp:46-74
     xs, reps = O.solve_sequence([M] * 3, rhs, cfg, tols=[1e-8] * 3, shared_matrix=True)
     assert all(r.status == "converged" for r in reps)
     assert reps[1].iterations < reps[0].iterations and reps[2].iterations <= reps[1].iterations
+
+
+# ---------------------------------------------------------------- baseline
+# baseline.hpp:51-216 (classical restarted GMRES, the comparison point)
+
+def _dense_gmres_residuals(A, b, m):
+    """Minimal residual over K_p(A, b) for p = 1..m (Arnoldi in numpy, then
+    a dense least-squares solve per p) — an independent restatement."""
+    n = len(b)
+    V = np.zeros((n, m + 1))
+    H = np.zeros((m + 1, m))
+    beta = np.linalg.norm(b)
+    V[:, 0] = b / beta
+    out = []
+    for q in range(m):
+        w = A @ V[:, q]
+        for _ in range(2):
+            h = V[:, :q + 1].T @ w
+            w -= V[:, :q + 1] @ h
+            H[:q + 1, q] += h
+        H[q + 1, q] = np.linalg.norm(w)
+        V[:, q + 1] = w / H[q + 1, q]
+        e1 = np.zeros(q + 2)
+        e1[0] = beta
+        y = np.linalg.lstsq(H[:q + 2, :q + 1], e1, rcond=None)[0]
+        out.append(np.linalg.norm(e1 - H[:q + 2, :q + 1] @ y))
+    return np.array(out)
+
+
+def test_baseline_estimates_are_minimal_residuals(O):
+    A = random_matrix(O, 60, 41)
+    b = O.gaussian_vector(60, 42)
+    M = O.SparseMatrix.from_dense(A)
+    x, rep = O.baseline_gmres(M, b, m=12, tol=1e-14, max_restarts=1)
+    est = np.array([v for _, v in rep.sketched_residuals])
+    np.testing.assert_allclose(est, _dense_gmres_residuals(A, b, 12), rtol=1e-7, atol=1e-15 * np.linalg.norm(b))
+    assert rep.status == "max_restarts" and rep.iterations == 12 and rep.cycles == 1
+    # one verification product per cycle; the verified residual is b - A x
+    assert rep.true_residuals[0][0] == 12
+    assert rep.true_residuals[0][1] == pytest.approx(np.linalg.norm(b - A @ x), rel=1e-9)
+    assert rep.true_residuals[0][1] == pytest.approx(est[-1], rel=1e-8)
+
+
+def test_baseline_counters_closed_form(O):
+    # 1 (||b||) + per cycle: 1 (beta) + sum_q (q+1 dots + ||w||) + 1 (verification)
+    M = O.gen_convdiff(20, -20.0)
+    b = O.gaussian_vector(400, 3)
+    x, rep = O.baseline_gmres(M, b, m=10, tol=1e-12, max_restarts=3)
+    assert rep.status == "max_restarts" and rep.iterations == 30
+    assert rep.counters == {"matvecs": 30 + 3, "inner_products": 1 + 3 * (1 + sum(q + 2 for q in range(10)) + 1),
+                            "sketch_applies": 0}
+    assert len(rep.sketched_residuals) == 30 and [i for i, _ in rep.true_residuals] == [10, 20, 30]
+
+
+def test_baseline_converges_and_restarts(O):
+    M = O.gen_convdiff(30, -10.0)
+    b = O.gaussian_vector(900, 5)
+    x, rep = O.baseline_gmres(M, b, m=40, tol=1e-8, max_restarts=30)
+    off, col, val = M.csr()
+    import scipy.sparse as sp
+    A = sp.csr_matrix((val, col, off), shape=(900, 900))
+    assert rep.status == "converged" and rep.cycles > 1
+    assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) < 1e-8
+    assert rep.final_relative_residual == pytest.approx(rep.true_residuals[-1][1] / rep.rhs_norm)
+
+
+def test_baseline_edge_cases(O):
+    n = 30
+    I3 = O.SparseMatrix.from_dense(3.0 * np.eye(n))
+    b = O.gaussian_vector(n, 9)
+    x, rep = O.baseline_gmres(I3, b, m=5, tol=1e-10)  # A = cI: one step
+    assert rep.status == "converged" and rep.iterations == 1
+    np.testing.assert_allclose(x, b / 3.0, rtol=1e-14)
+    x, rep = O.baseline_gmres(I3, np.zeros(n), m=5, tol=1e-10)  # zero rhs: no step
+    assert rep.status == "converged" and rep.iterations == 0 and rep.cycles == 0
+    assert not np.any(x)
+    # cyclic shift, b = e_0: the residual cannot drop before step n -> diverged
+    P = np.roll(np.eye(n), 1, axis=0)
+    e0 = np.zeros(n)
+    e0[0] = 1.0
+    x, rep = O.baseline_gmres(O.SparseMatrix.from_dense(P), e0, m=10, tol=1e-8, max_restarts=5)
+    assert rep.status == "diverged" and rep.iterations == 10
+    assert rep.notes == ["cycle 1: residual estimate improved by less than 1% over a full cycle"]
+    # x0 = exact solution: beta == 0 at the first cycle
+    x, rep = O.baseline_gmres(O.SparseMatrix.from_dense(np.eye(n)), b, m=5, tol=1e-10, x0=b)
+    assert rep.status == "converged" and rep.iterations == 0 and rep.counters["matvecs"] == 1
+    with pytest.raises(ValueError):
+        O.baseline_gmres(I3, b, m=0)
+    with pytest.raises(ValueError):
+        O.baseline_gmres(I3, b, tol=1.0)
