@@ -893,14 +893,76 @@ __global__ void __launch_bounds__(32) k_sparse_sign_lanes(const double* __restri
 /// out[r] = inv_sqrt_zeta * sum_b partials[b][r]: one warp per row, lane-
 /// strided sums then a fixed xor tree.
 __global__ void __launch_bounds__(256) k_sparse_fold(const double* __restrict__ partials, int G, int s,
-                                                     double inv_sqrt_zeta, double* __restrict__ out) {
+                                                     double inv_sqrt_zeta, double* __restrict__ out,
+                                                     const double* __restrict__ row_scale = nullptr) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= s) return;
   double a = 0.0;
   for (int b = lane; b < G; b += 32) a += partials[static_cast<int64_t>(b) * s + r];
   a = warp_sum(a);
-  if (lane == 0) out[r] = a * inv_sqrt_zeta;
+  if (lane == 0) out[r] = a * (row_scale ? row_scale[r] : inv_sqrt_zeta);
+}
+
+// ------------------------------------------------------- direct SRDCT rows
+// For blocks whose length has no four-step factorisation with F = 256 (odd
+// or otherwise awkward n, e.g. the 103^2 acceptance grid): every selected
+// row evaluated term by term, X[k] = sum_j z_j cos(pi k (2j+1) / 2N), the
+// cosine generated by a unit-complex rotation z <- z e^{i pi k / N} that is
+// re-anchored from an exactly reduced integer phase every kAnchor terms
+// (rounding grows ~kAnchor·eps, not with n). CTA = (256 selected rows, one
+// column chunk staged in shared memory with the signs applied); partials
+// [chunk][row] are folded per row in a fixed order by k_sparse_fold.
+// Cost s·n·5 fp64 ops, no O(s·G) serial fold.
+constexpr int kAnchor = 64;
+
+__global__ void __launch_bounds__(kThreads) k_srdct_direct(const double* __restrict__ x, double xscale, int64_t N,
+                                                           int64_t r0, int64_t nloc, int64_t chunk,
+                                                           const uint32_t* __restrict__ sign_bits,
+                                                           const int64_t* __restrict__ rows, int s,
+                                                           double* __restrict__ partials) {
+  extern __shared__ double zs[];  // chunk values sign ⊙ x
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * chunk;
+  const int64_t c1 = min(nloc, c0 + chunk);
+  for (int64_t jl = c0 + threadIdx.x; jl < c1; jl += blockDim.x) {
+    const int64_t jg = r0 + jl;
+    const bool pos = (__ldg(sign_bits + (jg >> 5)) >> (jg & 31)) & 1u;
+    const double v = __ldg(x + jl) * xscale;
+    zs[jl - c0] = pos ? v : -v;
+  }
+  __syncthreads();
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= s) return;
+  const uint64_t k = static_cast<uint64_t>(__ldg(rows + q));
+  const uint64_t fourN = 4u * static_cast<uint64_t>(N);
+  const double inv2N = 0.5 / static_cast<double>(N);
+  double sn, cs;
+  sincospi(static_cast<double>((2u * k) % fourN) * inv2N, &sn, &cs);
+  const double2 step = make_double2(cs, sn);
+  const uint64_t jump = (static_cast<uint64_t>(2 * kAnchor) * k) % fourN;  // phase advance per anchor block
+  uint64_t ph = (k * (2u * static_cast<uint64_t>(r0 + c0) + 1u)) % fourN;
+  double acc = 0.0;
+  for (int64_t a = c0; a < c1; a += kAnchor) {
+    sincospi(static_cast<double>(ph) * inv2N, &sn, &cs);
+    double2 z = make_double2(cs, sn);
+    const int len = c1 - a < kAnchor ? static_cast<int>(c1 - a) : kAnchor;
+    const double* zp = zs + (a - c0);
+    if (len == kAnchor) {
+#pragma unroll 8
+      for (int t = 0; t < kAnchor; ++t) {
+        acc = fma(zp[t], z.x, acc);
+        z = cmul(z, step);
+      }
+    } else {
+      for (int t = 0; t < len; ++t) {
+        acc = fma(zp[t], z.x, acc);
+        z = cmul(z, step);
+      }
+    }
+    ph += jump;
+    if (ph >= fourN) ph -= fourN;
+  }
+  partials[static_cast<int64_t>(blockIdx.y) * s + q] = acc;
 }
 
 __global__ void __launch_bounds__(kThreads) k_sparse_sign(const double* __restrict__ x, double xscale, int64_t nloc,
@@ -1209,6 +1271,25 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
         launch_tiles<kSrcSketch, 8, true, 1>(c, "sketch", S, p, row_begin, x_own, xscale, out, UpdateArgs{});
       else
         launch_tiles<kSrcSketch, 0, false, 1>(c, "sketch", S, p, row_begin, x_own, xscale, out, UpdateArgs{});
+      return;
+    }
+    if (p.F < 32 || static_cast<double>(S.s) * static_cast<double>(nloc) <= 4e9) {
+      // direct rows: (row blocks) x (column chunks) ~ 2 CTAs per SM
+      const int rb = static_cast<int>((S.s + kThreads - 1) / kThreads);
+      const int64_t cb_want = std::max<int64_t>(1, (2 * c.num_sms + rb - 1) / rb);
+      const int64_t chunk = std::min<int64_t>(round_up((nloc + cb_want - 1) / cb_want, kAnchor), 6144);  // <= 48 KB shared
+      const int cb = static_cast<int>(std::max<int64_t>(1, (nloc + chunk - 1) / chunk));
+      double* part = c.partials(static_cast<int64_t>(cb) * S.s);
+      {
+        TimedLaunch t(c, "sketch");
+        k_srdct_direct<<<dim3(rb, cb), kThreads, sizeof(double) * static_cast<size_t>(chunk), c.stream>>>(
+            x_own, xscale, S.n, row_begin, nloc, chunk, S.sign_bits.get(), S.rows.get(), static_cast<int>(S.s), part);
+        SDR_KERNEL_CHECK();
+      }
+      TimedLaunch t(c, "sketch_fold");
+      k_sparse_fold<<<static_cast<int>((S.s + 7) / 8), 256, 0, c.stream>>>(part, cb, static_cast<int>(S.s), 0.0, out,
+                                                                          S.row_scale.get());
+      SDR_KERNEL_CHECK();
       return;
     }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * c.num_sms)));

@@ -120,7 +120,8 @@ def test_srdct_rows_and_signs_bit_exact(sk, O, n, s, seed):
 
 
 @pytest.mark.parametrize("n,s", [(200, 48), (256, 64), (1000, 120), (10000, 120), (65536, 240), (2 ** 20, 140),
-                                 (2 ** 21, 240), (3 * 2 ** 15, 200), (997, 60)])
+                                 (2 ** 21, 240), (3 * 2 ** 15, 200), (997, 60), (10609, 1200), (12345, 777),
+                                 (2 ** 13 + 1, 300)])
 def test_srdct_apply_matches_oracle(sk, O, n, s):
     S = sk.SketchOperator.subsampled_dct(n, s, 0x5EED)
     So = O.SketchOperator.subsampled_dct(n, s, 0x5EED)
