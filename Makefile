@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibi
 CXXFLAGS := -O3 -std=c++17 -fPIC -fvisibility=hidden -Wall -Wextra -Wno-unused-parameter -I/usr/local/cuda/include
 
 CU := spmv arnoldi sketch operator baseline
-CC := context host_linalg space solver baseline_host capi
+CC := context host_linalg space solver baseline_host io capi
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .cu.o,$(CU)) $(addsuffix .o,$(CC)))
 HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh) include/sdr_b200.h
 

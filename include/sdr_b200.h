@@ -251,6 +251,42 @@ SDR_API int sdr_solve_sequence(sdr_ctx* ctx, int32_t nprob, const sdr_csr* const
                                const sdr_config* cfg, const sdr_sketch* sketch, sdr_recycle* space,
                                double* const* x_outs, sdr_report** reports_out);
 
+/* ---------------------------------------------------------------- files --
+ * Matrix Market (matrix_market.hpp:83-181) and the SKRYRCY1 recycle-space dump
+ * (recycle.hpp:337-385). Host only except sdr_csr_read_matrix_market /
+ * sdr_recycle_save_file / sdr_recycle_load_file. Parse and IO failures return
+ * SDR_ERUNTIME with the reference's message text (line numbers included). */
+typedef struct sdr_host_csr sdr_host_csr;
+SDR_API int sdr_mm_read_file(const char* path, sdr_host_csr** out);
+SDR_API int sdr_mm_read_string(const char* text, int64_t len, sdr_host_csr** out);
+SDR_API int sdr_host_csr_info(const sdr_host_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz);
+SDR_API int sdr_host_csr_arrays(const sdr_host_csr* h, const int64_t** offsets, const int64_t** columns,
+                                const double** values);
+SDR_API int sdr_host_csr_destroy(sdr_host_csr* h);
+/* coordinate / real / general, 17 significant digits. _string: buf NULL -> *len = bytes needed (with NUL). */
+SDR_API int sdr_mm_write_file(const char* path, int64_t rows, int64_t cols, const int64_t* offsets,
+                              const int64_t* columns, const double* values);
+SDR_API int sdr_mm_write_string(int64_t rows, int64_t cols, const int64_t* offsets, const int64_t* columns,
+                                const double* values, char* buf, int64_t* len);
+/* read_matrix_market_file + upload (single-rank context). */
+SDR_API int sdr_csr_read_matrix_market(sdr_ctx* ctx, const char* path, sdr_csr** out);
+
+typedef struct sdr_space_file sdr_space_file;
+SDR_API int sdr_space_file_read(const char* path, sdr_space_file** out);
+SDR_API int sdr_space_file_read_bytes(const void* data, int64_t len, sdr_space_file** out);
+SDR_API int sdr_space_file_info(const sdr_space_file* f, int64_t* n, int64_t* s, int64_t* k, int* provenance);
+SDR_API int sdr_space_file_arrays(const sdr_space_file* f, const double** U, const double** SU, const double** SAU);
+SDR_API int sdr_space_file_destroy(sdr_space_file* f);
+SDR_API int sdr_space_file_write(const char* path, int64_t n, int64_t s, int64_t k, int provenance, const double* U,
+                                 const double* SU, const double* SAU);
+/* buf NULL -> *len = bytes needed. */
+SDR_API int sdr_space_file_write_bytes(int64_t n, int64_t s, int64_t k, int provenance, const double* U,
+                                       const double* SU, const double* SAU, void* buf, int64_t* len);
+/* save_recycle_space_file / load_recycle_space_file on a device space (this
+ * rank's rows: one file per rank in a distributed context). */
+SDR_API int sdr_recycle_save_file(sdr_ctx* ctx, const sdr_recycle* sp, const char* path);
+SDR_API int sdr_recycle_load_file(sdr_ctx* ctx, sdr_recycle* sp, const char* path);
+
 /* ----------------------------------------------------------- baseline --
  * Classical restarted GMRES, the reference's comparison point
  * (baseline.hpp:24-39 BaselineConfig, :51-216 baseline_gmres): full

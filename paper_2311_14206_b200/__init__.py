@@ -37,7 +37,8 @@ from ._capi import sdr_config, sdr_baseline_config, sdr_callbacks, ITER_CB, RES_
 __all__ = [
     "Context", "default_context", "SparseMatrix", "SketchOperator", "SolverConfig", "RecycleSpace", "SolveReport",
     "SolveResult", "SequenceResult", "ProblemInstance", "solve", "solve_sequence",
-    "BaselineConfig", "BaselineResult", "baseline_gmres", "IncrementalQR", "harmonic_pairs",
+    "BaselineConfig", "BaselineResult", "baseline_gmres", "read_matrix_market", "write_matrix_market",
+    "matrix_market_string", "save_recycle_space", "load_recycle_space", "read_space_file", "space_file_bytes", "IncrementalQR", "harmonic_pairs",
     "gaussian_vector", "gen_convdiff", "gen_convdiff2d", "gen_convdiff3d", "sparse_sign_entries", "partition_halo",
     "partition_rows", "SdrError", "CudaError",
 ]
@@ -200,6 +201,14 @@ class SparseMatrix:
         # device storage: "sell" or "dia", diagonals per slice, stored entries, bytes per SpMV
         self.storage = dict(format=("sell", "dia")[fmt.value], diagonals=dg.value, stored=st.value,
                             bytes=nb.value)
+
+    @classmethod
+    def from_matrix_market(cls, path, ctx=None):
+        """read_matrix_market_file (matrix_market.hpp:161-165) straight to the device."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(_lib.sdr_csr_read_matrix_market(ctx._h, os.fsencode(path), C.byref(h)))
+        return cls(0, 0, None, None, None, ctx=ctx, _handle=h)
 
     @classmethod
     def from_triplets(cls, rows, cols, r, c, v, ctx=None):
@@ -708,6 +717,110 @@ def solve(A: SparseMatrix, b, cfg: SolverConfig, space: RecycleSpace | None = No
     _check(_lib.sdr_solve(ctx._h, A._h, pb, px0, C.byref(c), space._h, sketch._h if sketch else None,
                           C.byref(cb) if cb is not None else None, px, C.byref(rep)))
     return SolveResult(x, _report(rep), space)
+
+
+# ------------------------------------------------------------------- files
+# matrix_market.hpp:83-181 and the SKRYRCY1 recycle-space dump (recycle.hpp:337-390)
+
+def _host_csr(h):
+    try:
+        r, c, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(_lib.sdr_host_csr_info(h, C.byref(r), C.byref(c), C.byref(nz)))
+        po, pc, pv = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_double)()
+        _check(_lib.sdr_host_csr_arrays(h, C.byref(po), C.byref(pc), C.byref(pv)))
+        off = np.ctypeslib.as_array(po, (r.value + 1,)).copy()
+        col = np.ctypeslib.as_array(pc, (nz.value,)).copy() if nz.value else np.zeros(0, np.int64)
+        val = np.ctypeslib.as_array(pv, (nz.value,)).copy() if nz.value else np.zeros(0)
+        return r.value, c.value, off, col, val
+    finally:
+        _lib.sdr_host_csr_destroy(h)
+
+
+def read_matrix_market(path=None, text=None):
+    """Parses a Matrix Market file (or string) into CSR arrays
+    (rows, cols, offsets, columns, values); errors raise SdrError with the
+    reference's message, including the line number."""
+    h = C.c_void_p()
+    if text is not None:
+        t = text.encode() if isinstance(text, str) else bytes(text)
+        _check(_lib.sdr_mm_read_string(t, len(t), C.byref(h)))
+    else:
+        _check(_lib.sdr_mm_read_file(os.fsencode(path), C.byref(h)))
+    return _host_csr(h)
+
+
+def _csr_args(offsets, columns, values):
+    o = np.ascontiguousarray(offsets, dtype=np.int64)
+    c_ = np.ascontiguousarray(columns, dtype=np.int64)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    return (o, c_, v), (o.ctypes.data_as(C.c_void_p), c_.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p))
+
+
+def write_matrix_market(path, rows, cols, offsets, columns, values):
+    keep, ptrs = _csr_args(offsets, columns, values)
+    _check(_lib.sdr_mm_write_file(os.fsencode(path), rows, cols, *ptrs))
+
+
+def matrix_market_string(rows, cols, offsets, columns, values) -> str:
+    keep, ptrs = _csr_args(offsets, columns, values)
+    n = C.c_int64()
+    _check(_lib.sdr_mm_write_string(rows, cols, *ptrs, None, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(_lib.sdr_mm_write_string(rows, cols, *ptrs, buf, C.byref(n)))
+    return buf.value.decode()
+
+
+def read_space_file(path=None, data=None) -> dict:
+    """SKRYRCY1 dump -> {n, s, k, provenance, U (n x k), SU, SAU (s x k)}."""
+    h = C.c_void_p()
+    if data is not None:
+        _check(_lib.sdr_space_file_read_bytes(bytes(data), len(data), C.byref(h)))
+    else:
+        _check(_lib.sdr_space_file_read(os.fsencode(path), C.byref(h)))
+    try:
+        n, s_, k, prov = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        _check(_lib.sdr_space_file_info(h, C.byref(n), C.byref(s_), C.byref(k), C.byref(prov)))
+        pu, psu, psau = (C.POINTER(C.c_double)() for _ in range(3))
+        _check(_lib.sdr_space_file_arrays(h, C.byref(pu), C.byref(psu), C.byref(psau)))
+
+        def mat(p, r, c):
+            if r * c == 0:
+                return np.zeros((r, c), order="F")
+            return np.ctypeslib.as_array(p, (r * c,)).copy().reshape((r, c), order="F")
+        return dict(n=n.value, s=s_.value, k=k.value, provenance=PROVENANCE[prov.value],
+                    U=mat(pu, n.value, k.value), SU=mat(psu, s_.value, k.value), SAU=mat(psau, s_.value, k.value))
+    finally:
+        _lib.sdr_space_file_destroy(h)
+
+
+def _space_args(U, SU, SAU):
+    U = np.asfortranarray(U, dtype=np.float64)
+    SU = np.asfortranarray(SU, dtype=np.float64)
+    SAU = np.asfortranarray(SAU, dtype=np.float64)
+    return (U, SU, SAU), (U.ctypes.data_as(C.c_void_p), SU.ctypes.data_as(C.c_void_p), SAU.ctypes.data_as(C.c_void_p))
+
+
+def space_file_bytes(U, SU, SAU, provenance="fresh") -> bytes:
+    keep, ptrs = _space_args(U, SU, SAU)
+    n, k = keep[0].shape
+    s_ = keep[1].shape[0]
+    ln = C.c_int64()
+    _check(_lib.sdr_space_file_write_bytes(n, s_, k, PROVENANCE_ID[provenance], *ptrs, None, C.byref(ln)))
+    buf = C.create_string_buffer(ln.value)
+    _check(_lib.sdr_space_file_write_bytes(n, s_, k, PROVENANCE_ID[provenance], *ptrs, buf, C.byref(ln)))
+    return buf.raw[:ln.value]
+
+
+def save_recycle_space(path, space):
+    """save_recycle_space_file (recycle.hpp:380-384) of a device space."""
+    _check(_lib.sdr_recycle_save_file(space.ctx._h, space._h, os.fsencode(path)))
+
+
+def load_recycle_space(path, ctx=None):
+    """load_recycle_space_file (recycle.hpp:386-390) into a new device space."""
+    sp = RecycleSpace(ctx)
+    _check(_lib.sdr_recycle_load_file(sp.ctx._h, sp._h, os.fsencode(path)))
+    return sp
 
 
 @dataclass

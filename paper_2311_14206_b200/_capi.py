@@ -105,6 +105,23 @@ SIGNATURES = {
     "sdr_recycle_refresh": (cint, [vp, vp, vp, vp, cint, vp]),
     "sdr_krylov_run": (cint, [vp, vp, vp, vp, i64, i64, i64, f64, vp, vp, vp, vp, P(i64), P(cint), P(f64), vp]),
     "sdr_solve": (cint, [vp, vp, vp, vp, P(sdr_config), vp, vp, P(sdr_callbacks), vp, P(vp)]),
+    "sdr_mm_read_file": (cint, [C.c_char_p, P(vp)]),
+    "sdr_mm_read_string": (cint, [C.c_char_p, i64, P(vp)]),
+    "sdr_host_csr_info": (cint, [vp, P(i64), P(i64), P(i64)]),
+    "sdr_host_csr_arrays": (cint, [vp, P(P(i64)), P(P(i64)), P(P(f64))]),
+    "sdr_host_csr_destroy": (cint, [vp]),
+    "sdr_mm_write_file": (cint, [C.c_char_p, i64, i64, vp, vp, vp]),
+    "sdr_mm_write_string": (cint, [i64, i64, vp, vp, vp, C.c_char_p, P(i64)]),
+    "sdr_csr_read_matrix_market": (cint, [vp, C.c_char_p, P(vp)]),
+    "sdr_space_file_read": (cint, [C.c_char_p, P(vp)]),
+    "sdr_space_file_read_bytes": (cint, [C.c_char_p, i64, P(vp)]),
+    "sdr_space_file_info": (cint, [vp, P(i64), P(i64), P(i64), P(cint)]),
+    "sdr_space_file_arrays": (cint, [vp, P(P(f64)), P(P(f64)), P(P(f64))]),
+    "sdr_space_file_destroy": (cint, [vp]),
+    "sdr_space_file_write": (cint, [C.c_char_p, i64, i64, i64, cint, vp, vp, vp]),
+    "sdr_space_file_write_bytes": (cint, [i64, i64, i64, cint, vp, vp, vp, C.c_char_p, P(i64)]),
+    "sdr_recycle_save_file": (cint, [vp, vp, C.c_char_p]),
+    "sdr_recycle_load_file": (cint, [vp, vp, C.c_char_p]),
     "sdr_baseline_config_default": (cint, [P(sdr_baseline_config)]),
     "sdr_baseline_gmres": (cint, [vp, vp, vp, vp, P(sdr_baseline_config), vp, P(vp)]),
     "sdr_solve_sequence": (cint, [vp, i32, vp, vp, vp, vp, i32, P(sdr_config), vp, vp, vp, vp]),

@@ -5,6 +5,7 @@
 #include "baseline.hpp"
 #include "context.hpp"
 #include "host_linalg.hpp"
+#include "io.hpp"
 #include "operator.hpp"
 #include "sketch.hpp"
 #include "solver.hpp"
@@ -14,6 +15,7 @@
 #include <cstring>
 #include <memory>
 #include <new>
+#include <sstream>
 
 using namespace sdr;
 
@@ -38,6 +40,12 @@ struct sdr_recycle {
 };
 struct sdr_report {
   Report r;
+};
+struct sdr_host_csr {
+  HostCsr h;
+};
+struct sdr_space_file {
+  SpaceFile f;
 };
 struct sdr_qr {
   std::unique_ptr<HostQR> qr;
@@ -810,6 +818,216 @@ int sdr_solve(sdr_ctx* ctx, const sdr_csr* A, const double* b, const double* x0,
           rep->r);
     xo.finish(c);
     if (report_out) *report_out = rep.release();
+  });
+}
+
+int sdr_mm_read_file(const char* path, sdr_host_csr** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    auto h = std::make_unique<sdr_host_csr>();
+    h->h = mm_read_file(path);
+    *out = h.release();
+  });
+}
+
+int sdr_mm_read_string(const char* text, int64_t len, sdr_host_csr** out) {
+  return guard([&] {
+    need(text, "text");
+    need(out, "out");
+    std::istringstream in(std::string(text, static_cast<size_t>(len)));
+    auto h = std::make_unique<sdr_host_csr>();
+    h->h = mm_read(in);
+    *out = h.release();
+  });
+}
+
+int sdr_host_csr_info(const sdr_host_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  return guard([&] {
+    need(h, "csr");
+    if (rows) *rows = h->h.rows;
+    if (cols) *cols = h->h.cols;
+    if (nnz) *nnz = static_cast<int64_t>(h->h.values.size());
+  });
+}
+
+int sdr_host_csr_arrays(const sdr_host_csr* h, const int64_t** offsets, const int64_t** columns,
+                        const double** values) {
+  return guard([&] {
+    need(h, "csr");
+    if (offsets) *offsets = h->h.offsets.data();
+    if (columns) *columns = h->h.columns.data();
+    if (values) *values = h->h.values.data();
+  });
+}
+
+int sdr_host_csr_destroy(sdr_host_csr* h) {
+  delete h;
+  return SDR_OK;
+}
+
+int sdr_mm_write_file(const char* path, int64_t rows, int64_t cols, const int64_t* offsets, const int64_t* columns,
+                      const double* values) {
+  return guard([&] {
+    need(path, "path");
+    need(offsets, "offsets");
+    mm_write_file(path, rows, cols, offsets, columns, values);
+  });
+}
+
+int sdr_mm_write_string(int64_t rows, int64_t cols, const int64_t* offsets, const int64_t* columns,
+                        const double* values, char* buf, int64_t* len) {
+  return guard([&] {
+    need(offsets, "offsets");
+    need(len, "len");
+    std::ostringstream out;
+    mm_write(out, rows, cols, offsets, columns, values);
+    const std::string t = out.str();
+    if (buf) {
+      if (*len < static_cast<int64_t>(t.size() + 1)) throw invalid("sdr_mm_write_string: buffer too small");
+      std::memcpy(buf, t.c_str(), t.size() + 1);
+    }
+    *len = static_cast<int64_t>(t.size() + 1);
+  });
+}
+
+int sdr_csr_read_matrix_market(sdr_ctx* ctx, const char* path, sdr_csr** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(path, "path");
+    need(out, "out");
+    if (ctx->c->distributed()) throw invalid("sdr_csr_read_matrix_market: use sdr_csr_create_local in a distributed context");
+    const HostCsr m = mm_read_file(path);
+    auto h = std::make_unique<sdr_csr>();
+    h->ctx = ctx->c.get();
+    h->op.reset(create_operator_csr(*ctx->c, m.rows, m.cols, 0, m.rows, m.offsets.data(), m.columns.data(),
+                                    m.values.data()));
+    *out = h.release();
+  });
+}
+
+int sdr_space_file_read(const char* path, sdr_space_file** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    auto f = std::make_unique<sdr_space_file>();
+    f->f = space_read_file(path);
+    *out = f.release();
+  });
+}
+
+int sdr_space_file_read_bytes(const void* data, int64_t len, sdr_space_file** out) {
+  return guard([&] {
+    need(data, "data");
+    need(out, "out");
+    std::istringstream in(std::string(static_cast<const char*>(data), static_cast<size_t>(len)), std::ios::binary);
+    auto f = std::make_unique<sdr_space_file>();
+    f->f = space_read(in);
+    *out = f.release();
+  });
+}
+
+int sdr_space_file_info(const sdr_space_file* f, int64_t* n, int64_t* s, int64_t* k, int* provenance) {
+  return guard([&] {
+    need(f, "file");
+    if (n) *n = f->f.n;
+    if (s) *s = f->f.s;
+    if (k) *k = f->f.k;
+    if (provenance) *provenance = static_cast<int>(f->f.provenance);
+  });
+}
+
+int sdr_space_file_arrays(const sdr_space_file* f, const double** U, const double** SU, const double** SAU) {
+  return guard([&] {
+    need(f, "file");
+    if (U) *U = f->f.U.data();
+    if (SU) *SU = f->f.SU.data();
+    if (SAU) *SAU = f->f.SAU.data();
+  });
+}
+
+int sdr_space_file_destroy(sdr_space_file* f) {
+  delete f;
+  return SDR_OK;
+}
+
+namespace {
+SpaceFile space_from(int64_t n, int64_t s, int64_t k, int provenance, const double* U, const double* SU,
+                     const double* SAU) {
+  if (n < 0 || s < 0 || k < 0 || provenance < 0 || provenance > 4)
+    throw invalid("recycle-space save: invalid dimensions or provenance");
+  if (k > 0) {
+    need(U, "U");
+    need(SU, "SU");
+    need(SAU, "SAU");
+  }
+  SpaceFile f;
+  f.n = n, f.s = s, f.k = k, f.provenance = provenance;
+  f.U.assign(U, U + n * k);
+  f.SU.assign(SU, SU + s * k);
+  f.SAU.assign(SAU, SAU + s * k);
+  return f;
+}
+}  // namespace
+
+int sdr_space_file_write(const char* path, int64_t n, int64_t s, int64_t k, int provenance, const double* U,
+                         const double* SU, const double* SAU) {
+  return guard([&] {
+    need(path, "path");
+    space_write_file(path, space_from(n, s, k, provenance, U, SU, SAU));
+  });
+}
+
+int sdr_space_file_write_bytes(int64_t n, int64_t s, int64_t k, int provenance, const double* U, const double* SU,
+                               const double* SAU, void* buf, int64_t* len) {
+  return guard([&] {
+    need(len, "len");
+    const int64_t bytes = 40 + 8 * (n * k + 2 * s * k);
+    if (buf) {
+      if (*len < bytes) throw invalid("sdr_space_file_write_bytes: buffer too small");
+      std::ostringstream out(std::ios::binary);
+      space_write(out, space_from(n, s, k, provenance, U, SU, SAU));
+      const std::string t = out.str();
+      std::memcpy(buf, t.data(), t.size());
+    }
+    *len = bytes;
+  });
+}
+
+int sdr_recycle_save_file(sdr_ctx* ctx, const sdr_recycle* sp, const char* path) {
+  return guard([&] {  // save_recycle_space_file (recycle.hpp:380-384)
+    need(ctx, "ctx");
+    need(sp, "space");
+    need(path, "path");
+    Context& c = *ctx->c;
+    const Recycle& r = sp->sp;
+    SpaceFile f;
+    f.n = r.dim() > 0 ? r.nloc : 0;
+    f.s = r.SU.rows;
+    f.k = r.dim();
+    f.provenance = r.provenance;
+    f.U.resize(static_cast<size_t>(f.n * f.k));
+    if (f.k > 0) {
+      DeviceBuffer<double> u(f.n * f.k);
+      for (i64 q = 0; q < f.k; ++q) launch_scale_copy(c, r.uscale[static_cast<size_t>(q)], r.col(q), u.get() + q * f.n, f.n);
+      SDR_CUDA(cudaMemcpyAsync(f.U.data(), u.get(), sizeof(double) * f.U.size(), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+    }
+    f.SU.assign(r.SU.a.begin(), r.SU.a.begin() + f.s * f.k);
+    f.SAU.assign(r.SAU.a.begin(), r.SAU.a.begin() + f.s * f.k);
+    space_write_file(path, f);
+  });
+}
+
+int sdr_recycle_load_file(sdr_ctx* ctx, sdr_recycle* sp, const char* path) {
+  return guard([&] {  // load_recycle_space_file (recycle.hpp:386-390)
+    need(ctx, "ctx");
+    need(sp, "space");
+    need(path, "path");
+    const SpaceFile f = space_read_file(path);
+    const int rc = sdr_recycle_set(ctx, sp, f.n, f.s, f.k, f.U.data(), f.SU.data(), f.SAU.data(),
+                                   static_cast<int>(f.provenance));
+    if (rc != SDR_OK) throw Error(rc, g_err);
   });
 }
 
