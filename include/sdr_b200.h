@@ -106,6 +106,11 @@ SDR_API int sdr_csr_storage(const sdr_csr* A, int32_t* format, int32_t* diagonal
 /* y = A x (OperatorRef::apply, operator_ref.hpp:38-44). x: local_rows entries of this
  * rank's block (halos are exchanged internally); y: local_rows entries. Host or device. */
 SDR_API int sdr_spmv(sdr_ctx* ctx, const sdr_csr* A, const double* x, int64_t xlen, double* y);
+/* Y(:, q) = A X(:, q) for q < nb (column-major, host or device): the batched
+ * product of the exact recycle refresh (recycle.hpp:309-316), one pass over A
+ * per 8 columns; each column equals sdr_spmv bit for bit. Single-rank context. */
+SDR_API int sdr_spmm(sdr_ctx* ctx, const sdr_csr* A, int64_t nb, const double* X, int64_t ldx, double* Y,
+                     int64_t ldy);
 
 /* ------------------------------------------------------------- sketch -- */
 typedef enum { SDR_SKETCH_SRDCT = 0, SDR_SKETCH_IDENTITY = 1, SDR_SKETCH_SPARSE_SIGN = 2 } sdr_sketch_kind;

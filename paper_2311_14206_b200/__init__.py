@@ -271,6 +271,17 @@ class SparseMatrix:
 
     __matmul__ = apply
 
+    def apply_batch(self, X):
+        """Y = A X for an n x nb block (numpy, column-major copy taken), one
+        pass over A per 8 columns (the exact-refresh product)."""
+        X = np.asfortranarray(X, dtype=np.float64)
+        if X.ndim != 2 or X.shape[0] != self.cols:
+            raise ValueError(f"apply_batch: expected {self.cols} x nb block, got {X.shape}")
+        Y = np.empty((self.local_rows, X.shape[1]), order="F")
+        _check(_lib.sdr_spmm(self.ctx._h, self._h, X.shape[1], X.ctypes.data_as(C.c_void_p), X.shape[0],
+                             Y.ctypes.data_as(C.c_void_p), Y.shape[0]))
+        return Y
+
     def __del__(self):
         if getattr(self, "_h", None):
             _lib.sdr_csr_destroy(self._h)

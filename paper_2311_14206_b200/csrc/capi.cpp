@@ -321,6 +321,36 @@ int sdr_spmv(sdr_ctx* ctx, const sdr_csr* A, const double* x, int64_t xlen, doub
   });
 }
 
+int sdr_spmm(sdr_ctx* ctx, const sdr_csr* A, int64_t nb, const double* X, int64_t ldx, double* Y, int64_t ldy) {
+  return guard([&] {  // nb products of one operator in ceil(nb / 8) passes over it
+    need(ctx, "ctx");
+    need(A, "A");
+    if (nb < 0) throw invalid("sdr_spmm: negative column count");
+    if (nb == 0) return;
+    need(X, "X");
+    need(Y, "Y");
+    Context& c = *ctx->c;
+    const auto& op = *A->op;
+    if (c.distributed()) throw invalid("sdr_spmm: single-rank contexts only (use sdr_spmv per column)");
+    if (ldx < op.cols || ldy < op.local_rows) throw invalid("sdr_spmm: leading dimension smaller than the operator");
+    const VecLayout L = op.layout();
+    DeviceIn xin(c, X, ldx * (nb - 1) + op.cols);
+    DeviceBuffer<double> xb(L.ld * std::min<i64>(nb, kSpmmMax));
+    DeviceOut yo(Y, ldy * (nb - 1) + op.local_rows);
+    for (i64 q0 = 0; q0 < nb; q0 += kSpmmMax) {
+      const int k = static_cast<int>(std::min<i64>(kSpmmMax, nb - q0));
+      SpmmCols cols;
+      for (int q = 0; q < k; ++q) {  // the operator layout (halo / padding) of each column
+        SDR_CUDA(cudaMemcpyAsync(xb.get() + q * L.ld + L.own_off, xin.ptr + (q0 + q) * ldx,
+                                 sizeof(double) * static_cast<size_t>(op.cols), cudaMemcpyDeviceToDevice, c.stream));
+        cols.x[q] = xb.get() + q * L.ld + L.ext_shift();
+      }
+      launch_spmm(c, op.view(), cols, k, yo.ptr + q0 * ldy, ldy);
+    }
+    yo.finish(c);
+  });
+}
+
 // ------------------------------------------------------------------- sketch
 int sdr_sketch_create_srdct(sdr_ctx* ctx, int64_t n, int64_t s, uint64_t seed, sdr_sketch** out) {
   return guard([&] {

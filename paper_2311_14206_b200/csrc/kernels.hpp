@@ -68,6 +68,13 @@ int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t 
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
                         double* coef, double* partials_out = nullptr, int max_blocks_per_sm = 0);
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2);
+/// Column pointers of a batched product (extended-vector layout, like x_ext).
+constexpr int kSpmmMax = 8;
+struct SpmmCols {
+  const double* x[kSpmmMax] = {};
+};
+/// Y(:, q) = A X(:, q), q < nb <= 8, one pass over A (Y column-major, ldy).
+void launch_spmm(Context& c, const SellView& A, const SpmmCols& X, int nb, double* Y, int64_t ldy);
 /// y = A x, skipped (no stores) when *stop != 0 on the device.
 void launch_spmv_guarded(Context& c, const SellView& A, const double* x_ext, double* y, const int* stop);
 

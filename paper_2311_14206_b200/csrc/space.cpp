@@ -142,11 +142,18 @@ void refresh_recycle(Context& c, Recycle& sp, const DeviceOperator& A, const Ske
   const bool in_place = lay.halo_lo == 0 && lay.halo_hi == 0 && lay.own_off == 0;
   DeviceBuffer<double> ubuf(in_place ? 1 : lay.ld), au(std::max<i64>(lay.nloc, 1) * k), sk(S.s * k);
   if (!in_place) SDR_CUDA(cudaMemsetAsync(ubuf.get(), 0, sizeof(double) * static_cast<size_t>(lay.ld), c.stream));
+  const i64 ldau = std::max<i64>(lay.nloc, 1);
+  if (in_place) {  // one pass over A per 8 columns (batched SpMM)
+    for (i64 q0 = 0; q0 < k; q0 += kSpmmMax) {
+      const int nb = static_cast<int>(std::min<i64>(kSpmmMax, k - q0));
+      SpmmCols X;
+      for (int q = 0; q < nb; ++q) X.x[q] = sp.col(q0 + q);
+      launch_spmm(c, A.view(), X, nb, au.get() + q0 * ldau, ldau);
+    }
+  }
   for (i64 q = 0; q < k; ++q) {
-    double* aq = au.get() + q * std::max<i64>(lay.nloc, 1);
-    if (in_place) {
-      launch_spmv(c, A.view(), sp.col(q), aq);
-    } else {
+    double* aq = au.get() + q * ldau;
+    if (!in_place) {
       launch_scale_copy(c, 1.0, sp.col(q), ubuf.get() + lay.own_off, lay.nloc);
       operator_apply(c, A, ubuf.get(), aq);
     }

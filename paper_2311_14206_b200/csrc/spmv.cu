@@ -185,6 +185,54 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
   }
 }
 
+/// Y(:, q) = A X(:, q) for q < nb (<= NB) in one pass over the operator
+/// (the exact recycle refresh, recycle.hpp:309-316: k products of one
+/// matrix). Per column the row sums run in the same order as
+/// slice_row_sum, so each column equals the single-vector SpMV bit for bit.
+template <int NB, int FMT>
+__global__ void __launch_bounds__(kThreads) k_sell_spmm(SellView A, SpmmCols X, int nb, double* __restrict__ Y,
+                                                        int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int D = FMT > 0 ? FMT : (FMT < 0 ? A.dia_d : 0);
+  for (int64_t sl = gw; sl < A.nslices; sl += nwarps) {
+    const int64_t row = sl * kSlice + lane;
+    double acc[NB];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) acc[q] = 0.0;
+    if constexpr (FMT != 0) {
+      const int cur_off = lane < D ? __ldg(A.doff + sl * D + lane) : 0;
+      const double* vp = A.vals + sl * kSlice * D + lane;
+      const int64_t rx = A.halo_lo + row;
+      for (int k = 0; k < D; ++k) {
+        const int o = __shfl_sync(0xffffffffu, cur_off, k & 31);
+        int64_t cidx = rx + o;
+        cidx = cidx < 0 ? 0 : (cidx >= A.ext_len ? A.ext_len - 1 : cidx);
+        const double v = __ldcs(vp + k * kSlice);
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q < nb) acc[q] = fma(v, __ldg(X.x[q] + cidx), acc[q]);
+      }
+    } else {
+      const int64_t p0 = A.slice_ptr[sl];
+      const int len = static_cast<int>((A.slice_ptr[sl + 1] - p0) >> 5);
+      for (int k = 0; k < len; ++k) {
+        const int32_t c = __ldcs(A.cols + p0 + k * kSlice + lane);
+        const double v = __ldcs(A.vals + p0 + k * kSlice + lane);
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q < nb) acc[q] = fma(v, __ldg(X.x[q] + c), acc[q]);
+      }
+    }
+    if (row < A.nrows) {
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+        if (q < nb) Y[q * ldy + row] = acc[q];
+    }
+  }
+}
+
 template <class K>
 int resident_grid(const Context& c, K kernel, int64_t want_blocks, int max_per_sm = 0) {
   int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), kThreads, 0);
@@ -260,6 +308,25 @@ int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t 
                              c.counters() + 0, recA, mg, partials_out, max_per_sm);
   else
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
+}
+
+void launch_spmm(Context& c, const SellView& A, const SpmmCols& X, int nb, double* Y, int64_t ldy) {
+  if (A.nrows == 0 || nb == 0) return;
+  if (nb > kSpmmMax) throw invalid("launch_spmm: at most 8 columns per launch");
+  auto go = [&](auto kern) {
+    const int g = resident_grid(c, kern, blocks_for(A.nslices));
+    TimedLaunch t(c, "spmm");
+    kern<<<g, kThreads, 0, c.stream>>>(A, X, nb, Y, ldy);
+    SDR_KERNEL_CHECK();
+  };
+  if (!A.doff)
+    go(k_sell_spmm<kSpmmMax, 0>);
+  else if (A.dia_d == 7)
+    go(k_sell_spmm<kSpmmMax, 7>);
+  else if (A.dia_d == 5)
+    go(k_sell_spmm<kSpmmMax, 5>);
+  else
+    go(k_sell_spmm<kSpmmMax, -1>);
 }
 
 void launch_spmv_guarded(Context& c, const SellView& A, const double* x_ext, double* y, const int* stop) {

@@ -241,3 +241,28 @@ def test_zero_start_is_domain_error(sk):
     S = sk.SketchOperator.identity(8)
     with pytest.raises(ArithmeticError):
         krylov(sk, A, S, np.zeros(8), 1, 4)
+
+
+@pytest.mark.parametrize("kind", ["dia7", "dia5", "sell", "csr_wide"])
+@pytest.mark.parametrize("nb", [1, 5, 8, 13, 20])
+def test_spmm_columns_equal_spmv_bitwise(sk, O, kind, nb):
+    """The batched refresh product (recycle.hpp:309-316) per column equals the single SpMV exactly."""
+    if kind == "dia7":
+        off, col, val = sk.gen_convdiff3d(12, 100.0, 50.0, 25.0)
+        n = 12 ** 3
+    elif kind == "dia5":
+        off, col, val = sk.gen_convdiff(30, -20.0)
+        n = 900
+    else:
+        rng = np.random.default_rng(3)
+        n = 700
+        per = 9 if kind == "sell" else 40
+        r = np.repeat(np.arange(n), per)
+        c = rng.integers(0, n, n * per)
+        M = O.SparseMatrix.from_triplets(n, n, r, c, rng.standard_normal(n * per))
+        off, col, val = M.csr()
+    A = sk.SparseMatrix(n, n, off, col, val)
+    X = np.asfortranarray(np.stack([O.gaussian_vector(n, 100 + q) for q in range(nb)], axis=1))
+    Y = A.apply_batch(X)
+    for q in range(nb):
+        assert np.array_equal(Y[:, q], A.apply(X[:, q]))
