@@ -231,3 +231,16 @@ def test_partition_halo_plan_is_symmetric(sk):
         assert plans[p]["recv_cnt"].sum() == (rb[p] - mn[p]) + (mx[p] + 1 - re[p])
     assert plans[0]["recv_cnt"].tolist() == [0, n2, 0, 0]
     assert plans[1]["recv_lo"][0] == rb[1] - n2 and plans[1]["recv_lo"][2] == re[1]
+
+
+def test_campaign_out_dir_resolution_and_solver_names(monkeypatch):
+    """campaign.cpp:185-193 (test_campaign.cpp output-directory case)."""
+    from paper_2311_14206_b200 import campaign as cp
+    monkeypatch.delenv("SKRYLOV_OUT_DIR", raising=False)
+    assert cp.resolve_out_dir("explicit", "fallback") == "explicit"
+    assert cp.resolve_out_dir("", "fallback") == "fallback"
+    monkeypatch.setenv("SKRYLOV_OUT_DIR", "from-env")
+    assert cp.resolve_out_dir("", "fallback") == "from-env"
+    assert cp.resolve_out_dir("explicit", "fallback") == "explicit"
+    assert [cp.known_solver(s) for s in ("gmres-sdr", "sgmres", "gmres", "cg")] == [True, True, True, False]
+    assert cp.num(0.1) == "0.10000000000000001" and cp.num(float("nan")) == "nan"
