@@ -243,6 +243,13 @@ SDR_API int sdr_krylov_run(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, 
                            int64_t steps, double breakdown_tol, double* V, double* H, double* SV, double* SAV,
                            int64_t* j_out, int* breakdown, double* r0_norm, int64_t* counters3);
 
+/* Measurement: init + `steps` pipelined Arnoldi steps from r0, then the mean
+ * CUDA-event duration (microseconds) of `reps` back-to-back relaunches of the
+ * last step's K1 (SpMV + window dots) and K2 (fused update + SRDCT) on the
+ * library stream. The relaunches are idempotent. One-GPU SRDCT contexts. */
+SDR_API int sdr_debug_time_step(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, const double* r0, int64_t t,
+                                int64_t m, int64_t steps, int32_t reps, double* k1_us, double* k2_us);
+
 /* solve (solver.hpp:269-365). b, x0 (may be NULL), x_out: this rank's block,
  * host or device. space (may be NULL) is updated in place. sketch may be NULL
  * (SRDCT from cfg->s, cfg->sketch_seed). report_out may be NULL. */

@@ -820,6 +820,21 @@ int sdr_krylov_run(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, const do
   });
 }
 
+int sdr_debug_time_step(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, const double* r0, int64_t t, int64_t m,
+                        int64_t steps, int32_t reps, double* k1_us, double* k2_us) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(A, "A");
+    need(S, "S");
+    need(r0, "r0");
+    need(k1_us, "k1_us");
+    need(k2_us, "k2_us");
+    Context& c = *ctx->c;
+    DeviceIn rin(c, r0, A->op->local_rows);
+    time_step_kernels(c, *A->op, *S->S, rin.ptr, t, m, steps, reps, k1_us, k2_us);
+  });
+}
+
 int sdr_solve(sdr_ctx* ctx, const sdr_csr* A, const double* b, const double* x0, const sdr_config* cfg,
               sdr_recycle* space, const sdr_sketch* sketch, const sdr_callbacks* cb, double* x_out,
               sdr_report** report_out) {

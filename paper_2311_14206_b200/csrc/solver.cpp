@@ -401,7 +401,41 @@ struct ArnoldiPipeline {
   bool deferred = false;
   bool split = false;  // deferred + SRDCT on the side stream (SplitFold)
   StepFold last;  // partials K2(issued - 1) left
-  i64 last_ngram = 0;
+  i64 last_ngram = 0, last_j = -1;
+
+  /// Measurement: CUDA-event time of `reps` back-to-back relaunches of the
+  /// last enqueued step's K1 and of its K2 on the library stream. Both are
+  /// idempotent for fixed inputs (same y / w_{j+1} / partials / record rows
+  /// are rewritten), so the state stays what the step left.
+  void time_last_step(int reps, double* k1_us, double* k2_us) {
+    if (!deferred || split || last_j < 1) throw logic("time_last_step: needs an enqueued deferred step j >= 1");
+    const i64 j = last_j;
+    const VecLayout& lay = w.lay;
+    const RecLayout& RL = w.RL;
+    const int nwin = static_cast<int>(std::min<i64>(t, j + 1));
+    const int ngram = static_cast<int>(std::min<i64>(RL.T - 1, j + 1));
+    double* Vb = w.V[vb].get();
+    cudaEvent_t e[3];
+    for (auto& x : e) SDR_CUDA(cudaEventCreate(&x));
+    c.sync();
+    SDR_CUDA(cudaEventRecord(e[0], c.stream));
+    for (int r = 0; r < reps; ++r)
+      launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr, w.rec.get(),
+                          RL.stride, RL.T, w.cvec.get(), nullptr, w.p1.get(), 0);
+    SDR_CUDA(cudaEventRecord(e[1], c.stream));
+    StepFold sf = last;
+    for (int r = 0; r < reps; ++r)
+      launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
+                           w.cvec.get(), nullptr, A.row_begin, &sf);
+    SDR_CUDA(cudaEventRecord(e[2], c.stream));
+    SDR_CUDA(cudaEventSynchronize(e[2]));
+    float a = 0.f, b = 0.f;
+    SDR_CUDA(cudaEventElapsedTime(&a, e[0], e[1]));
+    SDR_CUDA(cudaEventElapsedTime(&b, e[1], e[2]));
+    for (auto& x : e) cudaEventDestroy(x);
+    *k1_us = 1e3 * a / reps;
+    *k2_us = 1e3 * b / reps;
+  }
   int pu_G[2] = {0, 0}, ps_G[2] = {0, 0}, ps_ld[2] = {0, 0};
 
   void setup_deferred() {
@@ -460,6 +494,7 @@ struct ArnoldiPipeline {
       if (dist) c.allreduce_sum(sf.out_partials, static_cast<i64>(sf.out_G) * sf.out_nvp);
       last = sf;
       last_ngram = ngram;
+      last_j = j;
       SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
       if (j > 0)  // row j is complete now
         w.copy_back(c, w.hrec.get() + j * R, w.rec.get() + j * R, R, w.evk[static_cast<size_t>(j)],
@@ -1096,6 +1131,21 @@ void krylov_run(Context& c, const DeviceOperator& A, const SketchDev& S, const d
     counters3[1] = cnt.inner_products;
     counters3[2] = cnt.sketch_applies;
   }
+}
+
+void time_step_kernels(Context& c, const DeviceOperator& A, const SketchDev& S, const double* r0, i64 t, i64 m,
+                       i64 steps, int reps, double* k1_us, double* k2_us) {
+  if (steps < 2 || steps > m || reps < 1) throw invalid("time_step_kernels: need 2 <= steps <= m and reps >= 1");
+  init_host_blas();
+  const VecLayout lay = A.layout();
+  Workspace& w = workspace(c, lay, m, S.s, static_cast<int>(std::min(t, m)));
+  Counters cnt;
+  ArnoldiPipeline ap(c, w, A, S, t, m, 1e-14, 0);
+  ap.init_enqueue(r0);
+  ap.init_finish(cnt);
+  for (i64 q = 0; q < steps && !ap.st.breakdown && ap.st.j < m; ++q) ap.step(cnt);
+  c.sync();
+  ap.time_last_step(reps, k1_us, k2_us);
 }
 
 void solve(Context& c, const DeviceOperator& A, const double* b, const double* x0, bool x0_nonzero, const Config& cfg,

@@ -105,6 +105,11 @@ void krylov_run(Context& c, const DeviceOperator& A, const SketchDev& S, const d
                 double breakdown_tol, double* V, double* H, double* SV, double* SAV, i64* j_out, int* breakdown,
                 double* r0_norm, i64* counters3);
 
+/// Measurement hook: init + `steps` pipelined Arnoldi steps, then CUDA-event
+/// timing of `reps` back-to-back relaunches of the last step's K1 and K2.
+void time_step_kernels(Context& c, const DeviceOperator& A, const SketchDev& S, const double* r0, i64 t, i64 m,
+                       i64 steps, int reps, double* k1_us, double* k2_us);
+
 /// Builds the default SRDCT sketch of the reference (solver.hpp:283-287).
 SketchDev* create_sketch(Context& c, int kind, i64 n, i64 s, std::uint64_t seed, i64 zeta);
 
