@@ -160,6 +160,13 @@ SDR_API int sdr_qr_factors(const sdr_qr* qr, double* Q, double* R);
 SDR_API int sdr_harmonic(const double* SAW, const double* SW, int64_t s, int64_t p, int64_t k, double rank_tol,
                          int64_t* rank, int64_t* k_eff, int* pair_extended, int* rank_limited, double* coeffs,
                          double* mu_re, double* mu_im);
+/* Same, with via_qr != 0: SAW is first factored by the incremental QR the
+ * solver keeps per cycle (two-pass Gram-Schmidt, incremental_qr.hpp:46-93), and
+ * the extraction runs on the factors as in the solver (when R is well
+ * conditioned the pencil is formed as R^{-1} Q^T SW without an SVD). */
+SDR_API int sdr_harmonic_qr(const double* SAW, const double* SW, int64_t s, int64_t p, int64_t k, double rank_tol,
+                            int32_t via_qr, int64_t* rank, int64_t* k_eff, int* pair_extended, int* rank_limited,
+                            double* coeffs, double* mu_re, double* mu_im);
 
 /* 1-D row partition of a banded operator: given every rank's
  * [row_begin, row_end) and referenced column range [min_col, max_col],

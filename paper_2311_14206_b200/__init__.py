@@ -489,8 +489,9 @@ class IncrementalQR:
             self._h = None
 
 
-def harmonic_pairs(SAW, SW, k, rank_tol=1e-12):
-    """truncated_svd + fill_pencil + harmonic_pairs (recycle.hpp:98-218)."""
+def harmonic_pairs(SAW, SW, k, rank_tol=1e-12, via_qr=False):
+    """truncated_svd + fill_pencil + harmonic_pairs (recycle.hpp:98-218).
+    via_qr: through the solver's per-cycle QR of SAW (see sdr_harmonic_qr)."""
     SAW = np.asfortranarray(SAW, dtype=np.float64)
     SW = np.asfortranarray(SW, dtype=np.float64)
     s, p = SAW.shape
@@ -499,8 +500,8 @@ def harmonic_pairs(SAW, SW, k, rank_tol=1e-12):
     kk = max(k, 0) + 2
     coeffs = np.zeros(p * kk)
     mre, mim = np.zeros(kk), np.zeros(kk)
-    _check(_lib.sdr_harmonic(SAW.ctypes.data_as(C.c_void_p), SW.ctypes.data_as(C.c_void_p), s, p, k, rank_tol,
-                             C.byref(rank), C.byref(keff), C.byref(pe), C.byref(rl),
+    _check(_lib.sdr_harmonic_qr(SAW.ctypes.data_as(C.c_void_p), SW.ctypes.data_as(C.c_void_p), s, p, k, rank_tol,
+                             int(via_qr), C.byref(rank), C.byref(keff), C.byref(pe), C.byref(rl),
                              coeffs.ctypes.data_as(C.c_void_p), mre.ctypes.data_as(C.c_void_p),
                              mim.ctypes.data_as(C.c_void_p)))
     ke = keff.value

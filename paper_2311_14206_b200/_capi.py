@@ -89,6 +89,7 @@ SIGNATURES = {
     "sdr_qr_solve": (cint, [vp, vp, i64, vp, P(f64)]),
     "sdr_qr_factors": (cint, [vp, vp, vp]),
     "sdr_harmonic": (cint, [vp, vp, i64, i64, i64, f64, P(i64), P(i64), P(cint), P(cint), vp, vp, vp]),
+    "sdr_harmonic_qr": (cint, [vp, vp, i64, i64, i64, f64, i32, P(i64), P(i64), P(cint), P(cint), vp, vp, vp]),
     "sdr_partition_halo": (cint, [cint, cint, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sdr_partition_rows": (cint, [i64, cint, i64, vp, vp]),
     "sdr_gen_convdiff2d": (cint, [i64, f64, f64, f64, vp, P(i64), vp, vp, vp]),

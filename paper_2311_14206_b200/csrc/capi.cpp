@@ -565,6 +565,12 @@ int sdr_qr_factors(const sdr_qr* qr, double* Q, double* R) {
 
 int sdr_harmonic(const double* SAW, const double* SW, int64_t s, int64_t p, int64_t k, double rank_tol, int64_t* rank,
                  int64_t* k_eff, int* pair_extended, int* rank_limited, double* coeffs, double* mu_re, double* mu_im) {
+  return sdr_harmonic_qr(SAW, SW, s, p, k, rank_tol, 0, rank, k_eff, pair_extended, rank_limited, coeffs, mu_re, mu_im);
+}
+
+int sdr_harmonic_qr(const double* SAW, const double* SW, int64_t s, int64_t p, int64_t k, double rank_tol,
+                    int32_t via_qr, int64_t* rank, int64_t* k_eff, int* pair_extended, int* rank_limited,
+                    double* coeffs, double* mu_re, double* mu_im) {
   return guard([&] {
     init_host_blas();
     if (s < 0 || p < 0) throw invalid("sdr_harmonic: negative dimensions");
@@ -575,7 +581,17 @@ int sdr_harmonic(const double* SAW, const double* SW, int64_t s, int64_t p, int6
       std::memcpy(a.a.data(), SAW, sizeof(double) * static_cast<size_t>(s * p));
       std::memcpy(w.a.data(), SW, sizeof(double) * static_cast<size_t>(s * p));
     }
-    Harmonic h = harmonic_extract(a, w, k, rank_tol);
+    Harmonic h;
+    HostQR qr(s, std::max<i64>(p, 1), 1e-12);
+    bool use_qr = via_qr != 0;
+    for (i64 j = 0; use_qr && j < p; ++j) use_qr = !qr.append(a.col(j), s).rank_deficient;
+    if (use_qr && qr.clean()) {  // the solver's route: the cycle's least-squares QR of SAW
+      HMat Q(s, p), R(p, p);
+      qr.factors(Q.a.data(), R.a.data());
+      h = harmonic_extract(a, w, k, rank_tol, &Q, &R);
+    } else {
+      h = harmonic_extract(a, w, k, rank_tol);
+    }
     if (rank) *rank = h.rank;
     if (k_eff) *k_eff = h.k_eff;
     if (pair_extended) *pair_extended = h.pair_extended;

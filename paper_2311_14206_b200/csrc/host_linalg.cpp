@@ -218,7 +218,37 @@ Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_to
   HMat U, V;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
-  if (Qf && Rf && Qf->rows == SAW.rows && Qf->cols == SAW.cols && Rf->rows == SAW.cols && Rf->cols == SAW.cols) {
+  const bool have_qr =
+      Qf && Rf && Qf->rows == SAW.rows && Qf->cols == SAW.cols && Rf->rows == SAW.cols && Rf->cols == SAW.cols;
+  // Fast path. With SAW = Q R and R well conditioned, every singular value
+  // of SAW lies far above rank_tol·sigma_1, so the truncated SVD keeps all p
+  // directions (l = p) and the pencil C = Sigma^{-1} U^T SW V is the
+  // orthogonal similarity V^T M V of M = R^{-1} Q^T SW. The Schur form of M
+  // then carries the same eigenvalues, and its reordered leading Schur
+  // vectors span V times C's (the coefficients below, since V is implicit).
+  // The 1-norm estimate of cond(R) is within a factor ~p of the 2-norm one,
+  // so rcond > 1e-7 keeps the decision exact for rank_tol <= 1e-10.
+  bool fast = false;
+  HMat Mf;
+  if (have_qr && rank_tol <= 1e-10 && SAW.cols > 0) {
+    const int pp = static_cast<int>(SAW.cols);
+    double rcond = 0.0;
+    int info = 0;
+    std::vector<double> wk(static_cast<size_t>(3 * pp));
+    std::vector<int> iwk(static_cast<size_t>(pp));
+    scipy_dtrcon_("1", "U", "N", &pp, Rf->a.data(), &pp, &rcond, wk.data(), iwk.data(), &info, 1, 1, 1);
+    if (info == 0 && rcond > 1e-7) {
+      const int ss = static_cast<int>(SAW.rows);
+      const double one = 1.0, zero = 0.0;
+      Mf = HMat(pp, pp);
+      scipy_dgemm_("T", "N", &pp, &pp, &ss, &one, Qf->a.data(), &ss, SW.a.data(), &ss, &zero, Mf.a.data(), &pp, 1, 1);
+      scipy_dtrsm_("L", "U", "N", "N", &pp, &pp, &one, Rf->a.data(), &pp, Mf.a.data(), &pp, 1, 1, 1, 1);
+      fast = true;
+    }
+  }
+  if (fast) {
+    // l = p; V = I
+  } else if (have_qr) {
     // SAW = Q R: singular values / right vectors of R, left vectors Q U_R
     HMat UR;
     thin_svd(*Rf, sv, &UR, &V);
@@ -233,7 +263,10 @@ Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_to
   const auto t1 = clk::now();
   i64 l = 0;  // recycle.hpp:102-104
   const double cutoff = sv.empty() ? 0.0 : rank_tol * sv[0];
-  while (l < static_cast<i64>(sv.size()) && sv[static_cast<size_t>(l)] > cutoff && sv[static_cast<size_t>(l)] > 0.0) ++l;
+  if (fast)
+    l = SAW.cols;
+  else
+    while (l < static_cast<i64>(sv.size()) && sv[static_cast<size_t>(l)] > cutoff && sv[static_cast<size_t>(l)] > 0.0) ++l;
   const i64 s = SAW.rows, p = SAW.cols;
   Harmonic out;
   out.rank = l;
@@ -247,12 +280,16 @@ Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_to
     return out;
   }
   // m = u^T SW v (recycle.hpp:114-118), C = diag(1/sigma) m
-  HMat swv(s, l);
-  for (i64 c = 0; c < l; ++c) hgemv(false, s, p, 1.0, SW.a.data(), s, V.col(c), 0.0, swv.col(c));
   HMat C(l, l);
-  for (i64 c = 0; c < l; ++c) {
-    hgemv(true, s, l, 1.0, U.a.data(), s, swv.col(c), 0.0, C.col(c));
-    for (i64 r = 0; r < l; ++r) C(r, c) = (1.0 / sv[static_cast<size_t>(r)]) * C(r, c);
+  if (fast) {
+    C = std::move(Mf);
+  } else {
+    HMat swv(s, l);
+    for (i64 c = 0; c < l; ++c) hgemv(false, s, p, 1.0, SW.a.data(), s, V.col(c), 0.0, swv.col(c));
+    for (i64 c = 0; c < l; ++c) {
+      hgemv(true, s, l, 1.0, U.a.data(), s, swv.col(c), 0.0, C.col(c));
+      for (i64 r = 0; r < l; ++r) C(r, c) = (1.0 / sv[static_cast<size_t>(r)]) * C(r, c);
+    }
   }
   // real Schur (dgees), ordering, conjugate-pair closure, dtrsen (recycle.hpp:167-205)
   const int n = static_cast<int>(l);
@@ -298,7 +335,10 @@ Harmonic harmonic_extract(const HMat& SAW, const HMat& SW, i64 k, double rank_to
   if (info != 0) throw runtime("reorder_schur: dtrsen failed with info = " + std::to_string(info));
   out.k_eff = ke;
   out.coeffs = HMat(p, ke);
-  for (i64 c = 0; c < ke; ++c) hgemv(false, p, l, 1.0, V.a.data(), p, Q.col(c), 0.0, out.coeffs.col(c));
+  if (fast)
+    for (i64 c = 0; c < ke; ++c) std::copy(Q.col(c), Q.col(c) + p, out.coeffs.col(c));
+  else
+    for (i64 c = 0; c < ke; ++c) hgemv(false, p, l, 1.0, V.a.data(), p, Q.col(c), 0.0, out.coeffs.col(c));
   for (i64 i = 0; i < ke; ++i) out.mu.emplace_back(wr[static_cast<size_t>(i)], wi[static_cast<size_t>(i)]);
   const auto t4 = clk::now();
   auto ms = [](clk::duration d) { return std::chrono::duration<double, std::milli>(d).count(); };

@@ -31,6 +31,11 @@ void scipy_dgesvd_(const char* jobu, const char* jobvt, const int* m, const int*
 void scipy_dgesdd_(const char* jobz, const int* m, const int* n, double* a, const int* lda, double* s, double* u,
                    const int* ldu, double* vt, const int* ldvt, double* work, const int* lwork, int* iwork, int* info,
                    size_t);
+void scipy_dtrcon_(const char* norm, const char* uplo, const char* diag, const int* n, const double* a, const int* lda,
+                   double* rcond, double* work, int* iwork, int* info, size_t, size_t, size_t);
+void scipy_dtrsm_(const char* side, const char* uplo, const char* transa, const char* diag, const int* m, const int* n,
+                  const double* alpha, const double* a, const int* lda, double* b, const int* ldb, size_t, size_t, size_t,
+                  size_t);
 void scipy_openblas_set_num_threads(int);
 }
 

@@ -185,6 +185,29 @@ def test_harmonic_matches_oracle_subspace(sk, O):  # test_recycle.cpp:87-129
         assert np.allclose(np.sort(np.abs(h["mu"])), np.sort(np.abs(ho["mu"])), rtol=1e-10)
 
 
+def test_harmonic_via_solver_qr_matches_oracle(sk, O):
+    """The solver's route (QR factors of SAW; no SVD when R is well conditioned)
+    extracts the same values and subspace as the reference's SVD route."""
+    rng = np.random.default_rng(9)
+    for p, scale in ((8, 1.0), (30, 1.0), (60, 1e-3)):
+        SAW = rng.standard_normal((120, p)) * np.logspace(0, np.log10(scale), p)
+        SW = rng.standard_normal((120, p))
+        for k in (1, 4, min(20, p)):
+            h = sk.harmonic_pairs(SAW, SW, k, via_qr=True)
+            ho = O.harmonic(SAW, SW, k)
+            assert h["k_effective"] == ho["k_effective"] and h["rank"] == ho["rank"] == p
+            A, B = sl.orth(h["coeffs"]), sl.orth(ho["coeffs"])
+            assert np.linalg.norm(A - B @ (B.T @ A)) <= 1e-9
+            assert np.allclose(np.sort(np.abs(h["mu"])), np.sort(np.abs(ho["mu"])), rtol=1e-9)
+    # numerically rank-deficient SAW: the QR route falls back to the truncated SVD
+    U = rng.standard_normal((40, 5))
+    SAW = np.column_stack([U, U[:, :2] @ rng.standard_normal((2, 3))])
+    SW = rng.standard_normal((40, 8))
+    h = sk.harmonic_pairs(SAW, SW, 3, via_qr=True)
+    ho = O.harmonic(SAW, SW, 3)
+    assert h["rank"] == ho["rank"] == 5 and h["k_effective"] == ho["k_effective"]
+
+
 def test_harmonic_conjugate_pair_and_rank_limit(sk):  # test_recycle.cpp:131-185
     rng = np.random.default_rng(55)
     Q = np.linalg.qr(rng.standard_normal((4, 4)))[0]
