@@ -250,6 +250,14 @@ SDR_API int sdr_krylov_run(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, 
                            int64_t steps, double breakdown_tol, double* V, double* H, double* SV, double* SAV,
                            int64_t* j_out, int* breakdown, double* r0_norm, int64_t* counters3);
 
+/* Test hook: C = [A1 A2] B (n rows, k1 + k2 inputs, nout <= 24 outputs,
+ * column-major) and norms2[q] = ||C(:, q)||^2 through the recycle-product
+ * kernels (kernel 0: k_tsgemm, nout <= 24 and even n / leading dims;
+ * 1: k_rgemm). Host or device arrays. */
+SDR_API int sdr_debug_block_product(sdr_ctx* ctx, int32_t kernel, int64_t n, const double* A1, int64_t lda1,
+                                    int32_t k1, const double* A2, int64_t lda2, int32_t k2, const double* B,
+                                    int32_t nout, double* C, int64_t ldc, double* norms2);
+
 /* Measurement: init + `steps` pipelined Arnoldi steps from r0, then the mean
  * CUDA-event duration (microseconds) of `reps` back-to-back relaunches of the
  * last step's K1 (SpMV + window dots) and K2 (fused update + SRDCT) on the

@@ -344,6 +344,168 @@ __global__ void __launch_bounds__(kThreads, NOUT > 12 ? 1 : 2) k_tsgemm(const do
   }
 }
 
+/// Recycle product for many outputs (U_new = [A1 A2] B, nout <= NO <= 24),
+/// norm partials fused. Shared-memory tiled: persistent CTAs (two per SM)
+/// walk 256-row tiles; each tile's inputs stream through a double-buffered
+/// 16-input x 256-row chunk filled by cp.async (16-byte pieces, zero-filled
+/// past the last row and input), so the HBM stream runs ahead of the
+/// arithmetic. The arithmetic is fp64 tensor-core mma (m8n8k4, DMMA): a warp
+/// owns 32 rows x NO outputs = 4 x NO/8 accumulator tiles, one 8-byte shared
+/// load per m-tile and per n-tile feeds 32·NO/8 FMAs per lane. One pass over
+/// the inputs, one write of the outputs (cuBLAS took two GEMMs, the second
+/// re-reading and re-writing the outputs).
+constexpr int kRgRows = 256, kRgKC = 16, kRgLda = kRgRows + 8;  // padded: k-rows alternate bank halves
+
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, int bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
+
+template <int NO>
+__global__ void __launch_bounds__(kThreads, 2) k_rgemm(const double* __restrict__ A1, int64_t lda1, int k1,
+                                                       const double* __restrict__ A2, int64_t lda2, int k2,
+                                                       const double* __restrict__ B, int nout, double* __restrict__ C,
+                                                       int64_t ldc, int64_t n, double* __restrict__ partials) {
+  constexpr int NT = NO / 8;  // 8-output tiles
+  extern __shared__ __align__(16) double rg_sm[];
+  double* As = rg_sm;                        // [2][kRgKC][kRgLda]
+  double* Bs = rg_sm + 2 * kRgKC * kRgLda;   // [K + 4][NO], zero rows past K
+  const int K = k1 + k2, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Kp = (K + 3) & ~3;
+  for (int q = tid; q < Kp * NO; q += blockDim.x) {
+    const int i = q / NO, o = q % NO;
+    Bs[q] = (o < nout && i < K) ? B[static_cast<int64_t>(o) * K + i] : 0.0;
+  }
+  const int g8 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+  const int64_t ntiles = (n + kRgRows - 1) / kRgRows;
+  const int nch = (K + kRgKC - 1) / kRgKC;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nstage = my_tiles * nch;
+  auto issue = [&](int64_t st, int buf) {
+    const int64_t tile = blockIdx.x + (st / nch) * gridDim.x;
+    const int ch = static_cast<int>(st % nch);
+    const int64_t row0 = tile * kRgRows;
+    double* dstb = As + buf * (kRgKC * kRgLda);
+#pragma unroll 4
+    for (int q = tid; q < kRgKC * (kRgRows / 2); q += kThreads) {
+      const int ii = q / (kRgRows / 2), pc = q % (kRgRows / 2);
+      const int i = ch * kRgKC + ii;
+      const int64_t r = row0 + 2 * pc;
+      const double* src = A1;
+      int bytes = 0;
+      if (i < K && r < n) {
+        src = (i < k1 ? A1 + static_cast<int64_t>(i) * lda1 : A2 + static_cast<int64_t>(i - k1) * lda2) + r;
+        bytes = r + 1 < n ? 16 : 8;
+      }
+      cp_async16z(dstb + ii * kRgLda + 2 * pc, src, bytes);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][NT][2], nrm[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) nrm[nt][0] = nrm[nt][1] = 0.0;
+  if (nstage > 0) issue(0, 0);
+  for (int64_t st = 0; st < nstage; ++st) {
+    const int buf = static_cast<int>(st & 1);
+    const int ch = static_cast<int>(st % nch);
+    if (st + 1 < nstage) {
+      issue(st + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // chunk st (and, at st = 0, the coefficients) visible to every thread
+    if (ch == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    }
+    // warp = 32 rows (4 m-tiles of 8) x NO outputs; fp64 mma m8n8k4 per
+    // (m-tile, n-tile, 4 inputs); rows past K are zero in Bs, so partial
+    // k-steps add nothing
+    const double* ab = As + buf * (kRgKC * kRgLda) + warp * 32 + g8;
+    const double* bb = Bs + (ch * kRgKC) * NO + g8;
+    const int ksteps = (min(kRgKC, K - ch * kRgKC) + 3) >> 2;
+    for (int ks = 0; ks < ksteps; ++ks) {
+      const int kr = ks * 4 + t4;
+      double a[4], b[NT];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) a[mt] = ab[kr * kRgLda + mt * 8];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt] = bb[kr * NO + nt * 8];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+                       : "d"(a[mt]), "d"(b[nt]));
+    }
+    if (ch == nch - 1) {  // tile complete: C(row, col) = acc[mt][nt][e], row = 8 mt + g8, col = 8 nt + 2 t4 + e
+      const int64_t row = (blockIdx.x + (st / nch) * gridDim.x) * kRgRows + warp * 32 + g8;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        if (row + mt * 8 < n) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = nt * 8 + 2 * t4 + e;
+              if (col < nout) {
+                C[static_cast<int64_t>(col) * ldc + row + mt * 8] = acc[mt][nt][e];
+                nrm[nt][e] = fma(acc[mt][nt][e], acc[mt][nt][e], nrm[nt][e]);
+              }
+            }
+        }
+      }
+    }
+    __syncthreads();  // buffer buf is refilled by the issue of stage st + 2
+  }
+  // norms: lanes with the same t4 hold the same columns; fold over g8, then warps
+  __shared__ double red[NO][kThreads / 32];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = nrm[nt][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if (g8 == 0) red[nt * 8 + 2 * t4 + e][warp] = v;
+    }
+  __syncthreads();
+  if (tid < nout) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[tid][w];
+    partials[static_cast<int64_t>(tid) * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+template <int NO>
+void rgemm_impl(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
+                const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2, double* scratch) {
+  auto kern = k_rgemm<NO>;
+  const size_t smem = sizeof(double) * (static_cast<size_t>(2 * kRgKC * kRgLda) + static_cast<size_t>(k1 + k2 + 4) * NO);
+  static size_t configured = 0;
+  if (smem > configured) {
+    SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    configured = smem;
+  }
+  const int64_t ntiles = (n + kRgRows - 1) / kRgRows;
+  const int per_sm = std::max(1, blocks_per_sm(reinterpret_cast<const void*>(kern), kThreads, smem));
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, static_cast<int64_t>(c.num_sms) * per_sm)));
+  double* part = scratch ? scratch : c.partials(static_cast<int64_t>(nout) * g);
+  {
+    TimedLaunch t(c, "recycle_gemm");
+    kern<<<g, kThreads, smem, c.stream>>>(A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, part);
+    SDR_KERNEL_CHECK();
+  }
+  TimedLaunch t(c, "col_norms");
+  k_col_fold<<<(nout + 7) / 8, 256, 0, c.stream>>>(part, g, nout, norms2);
+  SDR_KERNEL_CHECK();
+}
+
 int stream_grid(const Context& c, int64_t n, int per_thread = 1) {
   const int64_t want = (n / per_thread + kThreads - 1) / kThreads;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(c.num_sms) * 8)));
@@ -438,11 +600,27 @@ void tsgemm_impl(Context& c, const double* A1, int64_t lda1, int k1, const doubl
   SDR_KERNEL_CHECK();
 }
 
+bool rgemm_supported(int nout, int k, int64_t lda1, int64_t lda2) {
+  const size_t smem = sizeof(double) * (static_cast<size_t>(2 * kRgKC * kRgLda) + static_cast<size_t>(k + 4) * 24);
+  return nout >= 1 && nout <= 24 && k >= 1 && lda1 % 2 == 0 && lda2 % 2 == 0 && smem <= 227 * 1024;
+}
+
+void launch_rgemm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
+                  const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2, double* scratch) {
+  if (!rgemm_supported(nout, k1 + k2, lda1, lda2)) throw invalid("recycle product: unsupported shape");
+  if (nout <= 8)
+    rgemm_impl<8>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+  else if (nout <= 16)
+    rgemm_impl<16>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+  else
+    rgemm_impl<24>(c, A1, lda1, k1, A2, lda2, k2, B, nout, C, ldc, n, norms2, scratch);
+}
+
 bool tsgemm_supported(int nout, int64_t n, int64_t lda1, int64_t lda2, int64_t ldc) {
   return nout >= 1 && nout <= 24 && n % 2 == 0 && lda1 % 2 == 0 && lda2 % 2 == 0 && ldc % 2 == 0;
 }
 
-int64_t tsgemm_scratch_size(int num_sms) { return static_cast<int64_t>(24) * num_sms * 8; }
+int64_t tsgemm_scratch_size(int num_sms) { return static_cast<int64_t>(24) * num_sms * 8; }  // also k_rgemm (<= 2 CTAs / SM)
 
 void launch_tsgemm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
                    const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2, double* scratch) {

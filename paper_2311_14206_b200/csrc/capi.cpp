@@ -836,6 +836,27 @@ int sdr_krylov_run(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, const do
   });
 }
 
+int sdr_debug_block_product(sdr_ctx* ctx, int32_t kernel, int64_t n, const double* A1, int64_t lda1, int32_t k1,
+                            const double* A2, int64_t lda2, int32_t k2, const double* B, int32_t nout, double* C,
+                            int64_t ldc, double* norms2) {
+  return guard([&] {  // recycle product U_new = [A1 A2] B + norms (test hook; host or device arrays)
+    need(ctx, "ctx");
+    Context& c = *ctx->c;
+    const i64 K = k1 + k2;
+    DeviceIn a1(c, A1, lda1 * std::max(k1 - 1, 0) + n), a2(c, A2, k2 > 0 ? lda2 * (k2 - 1) + n : 0), b(c, B, K * nout);
+    DeviceOut co(C, ldc * (nout - 1) + n);
+    DeviceBuffer<double> nr(std::max(nout, 1)), scratch(tsgemm_scratch_size(c.num_sms));
+    if (kernel == 0)
+      launch_tsgemm(c, a1.ptr, lda1, k1, a2.ptr ? a2.ptr : a1.ptr, lda2, k2, b.ptr, nout, co.ptr, ldc, n, nr.get(),
+                    scratch.get());
+    else
+      launch_rgemm(c, a1.ptr, lda1, k1, a2.ptr ? a2.ptr : a1.ptr, lda2, k2, b.ptr, nout, co.ptr, ldc, n, nr.get(),
+                   scratch.get());
+    co.finish(c);
+    SDR_CUDA(cudaMemcpy(norms2, nr.get(), sizeof(double) * static_cast<size_t>(nout), cudaMemcpyDeviceToHost));
+  });
+}
+
 int sdr_debug_time_step(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, const double* r0, int64_t t, int64_t m,
                         int64_t steps, int32_t reps, double* k1_us, double* k2_us) {
   return guard([&] {

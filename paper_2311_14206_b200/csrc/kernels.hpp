@@ -93,6 +93,12 @@ int64_t tsgemm_scratch_size(int num_sms);
 void launch_tsgemm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
                    const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2,
                    double* scratch = nullptr);
+/// Same product for up to 24 outputs and any row count: shared-memory tiled,
+/// cp.async double-buffered, one pass over the inputs (k1 + k2 inputs).
+bool rgemm_supported(int nout, int k, int64_t lda1, int64_t lda2);
+void launch_rgemm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
+                  const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2,
+                  double* scratch = nullptr);
 /// norms2[q] = ||C(:, q)||^2 for q < ncol (column-major, ldc), deterministic.
 /// scratch: at least (4 num_sms + ncol) doubles, or null for the context's scratch.
 void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2,

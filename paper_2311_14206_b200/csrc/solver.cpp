@@ -769,10 +769,16 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     const char* e = std::getenv("SDR_TSGEMM");
     return !e || std::atoi(e) != 0;
   }();
-  // k_tsgemm (one HBM pass over [V U], norms fused) wins where the product is
-  // memory-bound (few outputs: C5, k = 10: 17.4 vs 37 ms per restart); with
-  // ~20 outputs (C2) cuBLAS's DMMA GEMM is faster (0.8 vs 1.4 ms)
-  if (dense_u && own_gemm && ke <= 12 && tsgemm_supported(static_cast<int>(ke), nloc, w.lay.ld, sp.ld, sp.ld)) {
+  // one HBM pass over [V U] with the norms fused: k_tsgemm for few outputs
+  // (C5, k = 10: 17.4 vs 37 ms per restart through cuBLAS), the shared-memory
+  // tiled k_rgemm for up to 24 (C2, k = 20); SDR_RGEMM=0 selects cuBLAS there
+  static const bool own_rgemm = [] {
+    const char* e = std::getenv("SDR_RGEMM");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool use_ts = ke <= 12 && tsgemm_supported(static_cast<int>(ke), nloc, w.lay.ld, sp.ld, sp.ld);
+  const bool use_rg = !use_ts && own_rgemm && rgemm_supported(static_cast<int>(ke), static_cast<int>(j + kc), w.lay.ld, sp.ld);
+  if (dense_u && own_gemm && (use_ts || use_rg)) {
     const i64 kk = j + kc;
     w.gcoef.ensure(std::max<i64>(kk * ke, 1));
     w.hgcoef.ensure(std::max<i64>(kk * ke, 1));
@@ -786,8 +792,12 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     SDR_CUDA(cudaMemcpyAsync(w.gcoef.get(), hb, sizeof(double) * static_cast<size_t>(kk * ke), cudaMemcpyHostToDevice,
                              c.stream));
     w.pside.ensure(tsgemm_scratch_size(c.num_sms));
-    launch_tsgemm(c, w.Vcol(vb, 0), w.lay.ld, static_cast<int>(j), sp.buf[sp.cur].get(), sp.ld, static_cast<int>(kc),
-                  w.gcoef.get(), static_cast<int>(ke), sp.buf[other].get(), sp.ld, nloc, w.scal.get(), w.pside.get());
+    if (use_ts)
+      launch_tsgemm(c, w.Vcol(vb, 0), w.lay.ld, static_cast<int>(j), sp.buf[sp.cur].get(), sp.ld, static_cast<int>(kc),
+                    w.gcoef.get(), static_cast<int>(ke), sp.buf[other].get(), sp.ld, nloc, w.scal.get(), w.pside.get());
+    else
+      launch_rgemm(c, w.Vcol(vb, 0), w.lay.ld, static_cast<int>(j), sp.buf[sp.cur].get(), sp.ld, static_cast<int>(kc),
+                   w.gcoef.get(), static_cast<int>(ke), sp.buf[other].get(), sp.ld, nloc, w.scal.get(), w.pside.get());
   } else if (dense_u) {
     const i64 ncoef = j * ke + kc * ke;
     w.gcoef.ensure(std::max<i64>(ncoef, 1));

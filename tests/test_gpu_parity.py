@@ -266,3 +266,26 @@ def test_spmm_columns_equal_spmv_bitwise(sk, O, kind, nb):
     Y = A.apply_batch(X)
     for q in range(nb):
         assert np.array_equal(Y[:, q], A.apply(X[:, q]))
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("n,k1,k2,nout", [(1000, 7, 3, 5), (4096, 100, 20, 20), (8191, 50, 0, 21), (300, 33, 31, 24),
+                                          (257, 1, 0, 1), (65536, 121, 20, 12)])
+def test_recycle_product_kernels(sk, kernel, n, k1, k2, nout):
+    """U_new = [V U] C with fused column norms (recycle.hpp:257-280 product)."""
+    import ctypes as C
+    if kernel == 0 and (n % 2 or nout > 24):
+        pytest.skip("k_tsgemm needs an even row count")
+    rng = np.random.default_rng(n + k1)
+    lda1, lda2 = n + (n % 2) + 32, n + (n % 2) + 64
+    A1 = rng.standard_normal((k1, lda1)).T.copy(order="F")
+    A2 = rng.standard_normal((max(k2, 1), lda2)).T.copy(order="F")
+    B = np.asfortranarray(rng.standard_normal((k1 + k2, nout)))
+    Cm = np.zeros((n, nout), order="F")
+    nr = np.zeros(nout)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    sk._check(sk._lib.sdr_debug_block_product(sk.default_context()._h, kernel, n, p(A1), lda1, k1, p(A2), lda2, k2,
+                                              p(B), nout, p(Cm), n, p(nr)))
+    ref = A1[:n, :k1] @ B[:k1] + (A2[:n, :k2] @ B[k1:] if k2 else 0.0)
+    assert np.linalg.norm(Cm - ref) <= 1e-13 * np.linalg.norm(ref)
+    np.testing.assert_allclose(nr, (ref ** 2).sum(axis=0), rtol=1e-12)
