@@ -959,8 +959,6 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
     }
     const bool last = jj == m || st.breakdown;
     if (sres < tol_abs / out.safety || last) {
-      // the cycle very likely ends here: start its restart bookkeeping now
-      out.early = start_early_harmonic(st, space, qr.get(), cfg.k, cfg.rank_tol);
       // correction = V(:,0:j) y_tail + U y_head (solver.hpp:197-198), on the device
       PhaseTimer pt_check(rep, "check");
       std::vector<const double*> in;
@@ -978,6 +976,9 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
       c.halo_exchange(A.plan, w.corr.get() + lay.ext_shift(), A.ext_begin, corr_own, A.row_begin);
       launch_residual(c, A.view(), w.corr.get() + lay.ext_shift(), r0, w.rnew.get(), w.scal.get());
       c.allreduce_sum(w.scal.get(), 1);
+      // the cycle very likely ends here: start its restart bookkeeping (host
+      // threads) while the verification runs on the device
+      out.early = start_early_harmonic(st, space, qr.get(), cfg.k, cfg.rank_tol);
       out.residual_norm = std::sqrt(d2h_scalar(c, w, w.scal.get()));
       out.have_correction = true;
       ++cnt.matvecs;
