@@ -386,16 +386,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_rgemm(const double* __restrict_
     const int ch = static_cast<int>(st % nch);
     const int64_t row0 = tile * kRgRows;
     double* dstb = As + buf * (kRgKC * kRgLda);
-#pragma unroll 4
-    for (int q = tid; q < kRgKC * (kRgRows / 2); q += kThreads) {
-      const int ii = q / (kRgRows / 2), pc = q % (kRgRows / 2);
+    // a warp copies 32 consecutive 16-byte pieces (512 B) of one input column
+    // per instruction; each thread keeps its row pair and walks the inputs
+    const int pc = tid & (kRgRows / 2 - 1), iw = tid / (kRgRows / 2);
+    const int64_t r = row0 + 2 * pc;
+    const int rbytes = r + 1 < n ? 16 : (r < n ? 8 : 0);
+#pragma unroll
+    for (int u = 0; u < kRgKC * (kRgRows / 2) / kThreads; ++u) {
+      const int ii = iw + u * (kThreads / (kRgRows / 2));
       const int i = ch * kRgKC + ii;
-      const int64_t r = row0 + 2 * pc;
       const double* src = A1;
       int bytes = 0;
-      if (i < K && r < n) {
+      if (i < K && rbytes) {
         src = (i < k1 ? A1 + static_cast<int64_t>(i) * lda1 : A2 + static_cast<int64_t>(i - k1) * lda2) + r;
-        bytes = r + 1 < n ? 16 : 8;
+        bytes = rbytes;
       }
       cp_async16z(dstb + ii * kRgLda + 2 * pc, src, bytes);
     }
