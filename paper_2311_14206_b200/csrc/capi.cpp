@@ -112,8 +112,11 @@ struct DeviceOut {
   double* ptr;
   i64 n;
   DeviceBuffer<double> own;
-  DeviceOut(double* p, i64 nn) : user(p), ptr(p), n(nn) {
-    if (p && !is_device_pointer(p)) {
+  /// pinned_ok: the callee only copies into the destination (cudaMemcpyAsync),
+  /// so page-locked host memory is used in place and the copy-out can overlap
+  /// the callee's remaining host work.
+  DeviceOut(double* p, i64 nn, bool pinned_ok = false) : user(p), ptr(p), n(nn) {
+    if (p && !is_device_pointer(p) && !(pinned_ok && is_pinned_host_pointer(p))) {
       own.resize(std::max<i64>(n, 1));
       ptr = own.get();
     }
@@ -895,7 +898,7 @@ int sdr_solve(sdr_ctx* ctx, const sdr_csr* A, const double* b, const double* x0,
     DeviceIn bin(c, b, n);
     DeviceIn x0in(c, x0, n);
     const bool nz = x0 && host_nonzero(c, x0, n);
-    DeviceOut xo(x_out, n);
+    DeviceOut xo(x_out, n, true);  // solve() writes x_out by cudaMemcpyAsync only
     solve(c, op, bin.ptr, x0in.ptr, nz, to_cfg(cfg), sp, sketch ? sketch->S.get() : nullptr, cb ? &cbs : nullptr, xo.ptr,
           rep->r);
     xo.finish(c);

@@ -155,6 +155,16 @@ inline bool is_device_pointer(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+inline bool is_pinned_host_pointer(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 inline i64 round_up(i64 v, i64 m) { return (v + m - 1) / m * m; }
 
 #ifdef __CUDACC__

@@ -1215,7 +1215,7 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
   }
 
   double safety = cfg.safety_init, res_norm = std::numeric_limits<double>::quiet_NaN();
-  bool have = false;
+  bool have = false, x_copied = false;
   pt_setup.reset();
   auto cur = std::make_unique<ArnoldiPipeline>(c, w, A, *sketch, cfg.t, cfg.m, cfg.breakdown_tol, 0);
   cur->init_enqueue(w.r0.get());
@@ -1254,6 +1254,13 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
     } else if (cycle == cfg.max_restarts) {
       status = 1;
     }
+    // the solve ends with this cycle: x is final, so its copy-out runs while
+    // the host computes the last recycle update
+    if (status >= 0 && x_out) {
+      x_copied = true;
+      SDR_CUDA(cudaMemcpyAsync(x_out, w.x.get(), sizeof(double) * static_cast<size_t>(lay.nloc), cudaMemcpyDefault,
+                               c.stream));
+    }
     // the finished cycle's device work is all enqueued: the recycle product
     // may start as soon as it completes (side stream, see update_recycle)
     SDR_CUDA(cudaEventRecord(w.ev_side_in, c.stream));
@@ -1281,7 +1288,7 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
     cur = std::move(next);
   }
   if (have) rep.final_relative_residual = rep.rhs_norm > 0.0 ? res_norm / rep.rhs_norm : res_norm;
-  if (x_out)
+  if (x_out && !x_copied)
     SDR_CUDA(cudaMemcpyAsync(x_out, w.x.get(), sizeof(double) * static_cast<size_t>(lay.nloc), cudaMemcpyDefault, c.stream));
   c.sync();
   rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
