@@ -169,6 +169,17 @@ def run_reference(args, wl, rank, world):
     return line
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line on the real stdout (library / NCCL banners that write to
+    fd 1 during the run are sent to stderr, see __main__)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,7 +195,7 @@ def main():
     if args.impl == "reference":
         line = run_reference(args, wl, rank, world)
         if line is not None:
-            print(json.dumps(line), flush=True)
+            emit(line)
         return
 
     import torch
@@ -379,10 +390,15 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": launches,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist is not None:
         dist.destroy_process_group()
 
 
 if __name__ == "__main__":
+    # keep stdout for the JSON line alone: fd 1 points at stderr while the
+    # workload runs (NCCL prints its version banner to stdout on rank 0)
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     main()

@@ -604,6 +604,25 @@ void tsgemm_impl(Context& c, const double* A1, int64_t lda1, int k1, const doubl
   SDR_KERNEL_CHECK();
 }
 
+namespace {
+__global__ void k_fold_partials(const double* __restrict__ partials, int G, int nv, int value_major,
+                                double* __restrict__ out) {
+  const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (v >= nv) return;
+  double a = 0.0;
+  for (int b = lane; b < G; b += 32)
+    a += value_major ? partials[static_cast<int64_t>(v) * G + b] : partials[static_cast<int64_t>(b) * nv + v];
+  a = warp_sum(a);
+  if (lane == 0) out[v] = a;
+}
+}  // namespace
+
+void launch_fold_partials(Context& c, const double* partials, int G, int nv, bool value_major, double* out) {
+  TimedLaunch t(c, "fold_partials");
+  k_fold_partials<<<(nv + 7) / 8, 256, 0, c.stream>>>(partials, G, nv, value_major ? 1 : 0, out);
+  SDR_KERNEL_CHECK();
+}
+
 bool rgemm_supported(int nout, int k, int64_t lda1, int64_t lda2) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(2 * kRgKC * kRgLda) + static_cast<size_t>(k + 4) * 24);
   return nout >= 1 && nout <= 24 && k >= 1 && lda1 % 2 == 0 && lda2 % 2 == 0 && smem <= 227 * 1024;

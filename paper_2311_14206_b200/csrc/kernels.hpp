@@ -129,6 +129,10 @@ struct StepFold {
   double* out_partials = nullptr;  // this update's partials (update_sketch_partials_size doubles)
   int out_G = 0, out_nvp = 0;      // set by the launch
 };
+/// out[v] = sum_b partials over G CTAs, fixed order: value-major [nv][G]
+/// (K1) or CTA-major [G][nv] (K2). The several-rank pipeline folds locally
+/// before its allreduces.
+void launch_fold_partials(Context& c, const double* partials, int G, int nv, bool value_major, double* out);
 bool update_sketch_eligible(const SketchDev& S, const VecLayout& lay, int need, int64_t row_begin, int64_t ldv);
 int64_t update_sketch_partials_size(const SketchDev& S, int num_sms);
 /// Fused K2 + K3a (update pass and SRDCT of w_{j+1} in one sweep), writing

@@ -66,6 +66,7 @@ struct Workspace {
   int nV = 0;
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
+  DeviceBuffer<double> p1f, p2f[2];  // several ranks: the same, folded over this rank's CTAs before the allreduce
   DeviceBuffer<double> gcoef;      // recycle-update GEMM coefficients
   DeviceBuffer<double> pside;      // recycle-update norm partials (runs on the side stream)
   DeviceBuffer<double> ps[2], pu[2];  // split pipeline: SRDCT / update partials by step parity
@@ -450,6 +451,10 @@ struct ArnoldiPipeline {
     if (!deferred) return;
     w.p1.ensure(34 * static_cast<i64>(c.num_sms) * 8);
     for (auto& b : w.p2) b.ensure(update_sketch_partials_size(S, c.num_sms));
+    if (c.distributed()) {
+      w.p1f.ensure(34);
+      for (auto& b : w.p2f) b.ensure(update_sketch_partials_size(S, 1));
+    }
     if (split) {
       for (auto& b : w.ps) b.ensure(sketch_partials_size(S, c.num_sms));
       for (auto& b : w.pu) b.ensure(update_split_partials_size(c.num_sms));
@@ -475,12 +480,20 @@ struct ArnoldiPipeline {
       // every rank folds the same reduced partials in the same order
       const bool dist = c.distributed();
       c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
+      // several ranks: each rank folds its own CTA partials (fixed order) and
+      // only the folded values cross the NVLink fabric (1 + nwin values after
+      // K1, 2s + t after K2, instead of every CTA's row); NCCL's allreduce
+      // hands every rank the same sums, so all ranks fold identically
       StepFold sf;
-      sf.fixed_grid = dist;
       sf.k1_partials = w.p1.get();
       sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
-                                    w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), dist ? -1 : 0);
-      if (dist) c.allreduce_sum(w.p1.get(), static_cast<i64>(1 + nwin) * sf.k1_G);
+                                    w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), 0);
+      if (dist) {
+        launch_fold_partials(c, w.p1.get(), sf.k1_G, 1 + nwin, true, w.p1f.get());
+        c.allreduce_sum(w.p1f.get(), 1 + nwin);
+        sf.k1_partials = w.p1f.get();
+        sf.k1_G = 1;
+      }
       if (j > 0) {
         sf.prev_partials = last.out_partials;
         sf.prev_G = last.out_G;
@@ -491,7 +504,13 @@ struct ArnoldiPipeline {
       if (!launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
                                 w.cvec.get(), nullptr, A.row_begin, &sf))
         throw logic("deferred step pipeline: fused update became ineligible");
-      if (dist) c.allreduce_sum(sf.out_partials, static_cast<i64>(sf.out_G) * sf.out_nvp);
+      if (dist) {
+        double* folded = w.p2f[j & 1].get();
+        launch_fold_partials(c, sf.out_partials, sf.out_G, sf.out_nvp, false, folded);
+        c.allreduce_sum(folded, sf.out_nvp);
+        sf.out_partials = folded;
+        sf.out_G = 1;
+      }
       last = sf;
       last_ngram = ngram;
       last_j = j;
