@@ -66,7 +66,10 @@ struct Workspace {
   int nV = 0;
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
-  DeviceBuffer<double> p1f, p2f[2];  // several ranks: the same, folded over this rank's CTAs before the allreduce
+  // several ranks: the same partials folded over this rank's CTAs before the
+  // allreduce; comb[j & 1] = [K2(j) folded (nvp) | K1(j + 1) folded], one
+  // allreduce per step
+  DeviceBuffer<double> p1f, comb[2];
   DeviceBuffer<double> gcoef;      // recycle-update GEMM coefficients
   DeviceBuffer<double> pside;      // recycle-update norm partials (runs on the side stream)
   DeviceBuffer<double> ps[2], pu[2];  // split pipeline: SRDCT / update partials by step parity
@@ -403,6 +406,8 @@ struct ArnoldiPipeline {
   bool split = false;  // deferred + SRDCT on the side stream (SplitFold)
   StepFold last;  // partials K2(issued - 1) left
   i64 last_ngram = 0, last_j = -1;
+  double* pend_buf = nullptr;  // several ranks: K2's folded partials not yet allreduced
+  int pend_n = 0;
 
   /// Measurement: CUDA-event time of `reps` back-to-back relaunches of the
   /// last enqueued step's K1 and of its K2 on the library stream. Both are
@@ -453,7 +458,7 @@ struct ArnoldiPipeline {
     for (auto& b : w.p2) b.ensure(update_sketch_partials_size(S, c.num_sms));
     if (c.distributed()) {
       w.p1f.ensure(34);
-      for (auto& b : w.p2f) b.ensure(update_sketch_partials_size(S, 1));
+      for (auto& b : w.comb) b.ensure(update_sketch_partials_size(S, 1) + 34);
     }
     if (split) {
       for (auto& b : w.ps) b.ensure(sketch_partials_size(S, c.num_sms));
@@ -475,24 +480,25 @@ struct ArnoldiPipeline {
       return;
     }
     if (deferred) {
-      // several ranks: the CTA partials themselves are summed over ranks (an
-      // allreduce after each kernel, grids fixed so the layouts agree), and
-      // every rank folds the same reduced partials in the same order
       const bool dist = c.distributed();
       c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
       // several ranks: each rank folds its own CTA partials (fixed order) and
-      // only the folded values cross the NVLink fabric (1 + nwin values after
-      // K1, 2s + t after K2, instead of every CTA's row); NCCL's allreduce
-      // hands every rank the same sums, so all ranks fold identically
+      // only the folded values cross the NVLink fabric, once per step
+      // ([2s + t after K2(j-1) | 1 + nwin after K1(j)] instead of every
+      // CTA's row after each kernel); NCCL's allreduce hands every rank the
+      // same sums, so all ranks fold identically
       StepFold sf;
       sf.k1_partials = w.p1.get();
       sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
                                     w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), 0);
-      if (dist) {
-        launch_fold_partials(c, w.p1.get(), sf.k1_G, 1 + nwin, true, w.p1f.get());
-        c.allreduce_sum(w.p1f.get(), 1 + nwin);
-        sf.k1_partials = w.p1f.get();
+      if (dist) {  // K1(j)'s folded dots ride on the allreduce of K2(j-1)'s folded partials
+        double* cb = pend_n > 0 ? pend_buf : w.p1f.get();
+        const int off = pend_n;
+        launch_fold_partials(c, w.p1.get(), sf.k1_G, 1 + nwin, true, cb + off);
+        c.allreduce_sum(cb, off + 1 + nwin);
+        sf.k1_partials = cb + off;
         sf.k1_G = 1;
+        pend_n = 0;
       }
       if (j > 0) {
         sf.prev_partials = last.out_partials;
@@ -504,12 +510,13 @@ struct ArnoldiPipeline {
       if (!launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
                                 w.cvec.get(), nullptr, A.row_begin, &sf))
         throw logic("deferred step pipeline: fused update became ineligible");
-      if (dist) {
-        double* folded = w.p2f[j & 1].get();
+      if (dist) {  // reduced together with K1(j+1)'s dots (or by flush at the cycle's end)
+        double* folded = w.comb[j & 1].get();
         launch_fold_partials(c, sf.out_partials, sf.out_G, sf.out_nvp, false, folded);
-        c.allreduce_sum(folded, sf.out_nvp);
         sf.out_partials = folded;
         sf.out_G = 1;
+        pend_buf = folded;
+        pend_n = sf.out_nvp;
       }
       last = sf;
       last_ngram = ngram;
@@ -602,6 +609,10 @@ struct ArnoldiPipeline {
   /// Deferred pipeline: completes row j + 1 when no K2(j + 1) will follow.
   void flush(i64 j) {
     const i64 R = w.RL.stride;
+    if (pend_n > 0) {
+      c.allreduce_sum(pend_buf, pend_n);
+      pend_n = 0;
+    }
     launch_update_sketch_flush(c, S, last, w.rec.get(), w.RL, static_cast<int>(j), static_cast<int>(last_ngram));
     w.copy_back(c, w.hrec.get() + (j + 1) * R, w.rec.get() + (j + 1) * R, R, w.evk[static_cast<size_t>(j + 1)],
                 w.ev[static_cast<size_t>(j + 1)]);
