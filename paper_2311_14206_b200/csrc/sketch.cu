@@ -890,6 +890,75 @@ __global__ void __launch_bounds__(32) k_sparse_sign_lanes(const double* __restri
   }
 }
 
+/// Sparse sign with one warp per 4-entry hash chunk (ZETA = 4·NCH): warp c
+/// evaluates h_c for its lanes' columns and scatters entries 4c..4c+3, whose
+/// rows lie in blocks 4c..4c+3 — a contiguous row range no other warp
+/// touches. The CTA's lane-private bins are the same [s][32] doubles as in
+/// k_sparse_sign_lanes, shared by NCH warps instead of one, so twice (ζ = 8)
+/// the warps fit on an SM and each thread does half the hashing and
+/// scattering per column. Same map, same deterministic fold.
+template <int ZETA>
+__global__ void __launch_bounds__(32 * (ZETA / 4)) k_sparse_sign_chunks(const double* __restrict__ x, double xscale,
+                                                                        int64_t nloc, int64_t r0, uint64_t key, int s,
+                                                                        double* __restrict__ partials) {
+  constexpr int NCH = ZETA / 4;
+  extern __shared__ double bins[];  // [s][32]
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < s * 32; i += blockDim.x) bins[i] = 0.0;
+  int b0r[4], bsr[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int l = 4 * c + e;
+    b0r[e] = static_cast<int>((static_cast<int64_t>(l) * s) / ZETA);
+    bsr[e] = static_cast<int>((static_cast<int64_t>(l + 1) * s) / ZETA) - b0r[e];
+  }
+  const int rlo = b0r[0], rhi = b0r[3] + bsr[3];  // this warp's rows
+  __syncthreads();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * 32;
+  constexpr int UE = 4;
+  const int64_t step = UE * stride;
+  int64_t j0 = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  double vn[UE];
+#pragma unroll
+  for (int u = 0; u < UE; ++u) vn[u] = j0 + u * stride < nloc ? __ldcs(x + j0 + u * stride) : 0.0;
+  for (; j0 < nloc; j0 += step) {
+    double v[UE];
+#pragma unroll
+    for (int u = 0; u < UE; ++u) {
+      v[u] = vn[u] * xscale;
+      const int64_t jn = j0 + step + u * stride;
+      vn[u] = jn < nloc ? __ldcs(x + jn) : 0.0;
+    }
+    int row[UE][4];
+    double sv[UE][4];
+#pragma unroll
+    for (int u = 0; u < UE; ++u) {
+      const uint64_t jg = static_cast<uint64_t>(r0 + j0 + u * stride);
+      const uint64_t h = mix64(key + (jg * NCH + static_cast<uint64_t>(c) + 1u) * kPhi64);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t f = static_cast<uint32_t>(h >> (16 * e)) & 0xFFFFu;
+        row[u][e] = (b0r[e] + static_cast<int>(((f >> 1) & 0x7FFFu) * static_cast<uint32_t>(bsr[e]) >> 15)) * 32 + lane;
+        sv[u][e] = (f & 1u) ? v[u] : -v[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UE; ++u) {
+      double t[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) t[e] = bins[row[u][e]];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) bins[row[u][e]] = t[e] + sv[u][e];
+    }
+  }
+  __syncwarp();
+  for (int r = rlo + lane; r < rhi; r += 32) {
+    double acc = 0.0;
+    for (int e = 0; e < 32; ++e) acc += bins[r * 32 + e];
+    partials[static_cast<int64_t>(blockIdx.x) * s + r] = acc;
+  }
+}
+
 /// out[r] = inv_sqrt_zeta * sum_b partials[b][r]: one warp per row, lane-
 /// strided sums then a fixed xor tree.
 __global__ void __launch_bounds__(256) k_sparse_fold(const double* __restrict__ partials, int G, int s,
@@ -1316,7 +1385,14 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
     double* part = c.partials(static_cast<int64_t>(grid) * S.s);
     {
       TimedLaunch t(c, "sketch");
-      if (S.zeta == 8)
+      static const bool chunk_warps = [] {
+        const char* e = std::getenv("SDR_SPARSE_CHUNKS");
+        return !e || std::atoi(e) != 0;
+      }();
+      if (S.zeta == 8 && chunk_warps)
+        k_sparse_sign_chunks<8><<<grid, 64, lane_smem, c.stream>>>(x_own, xscale, nloc, row_begin, S.key,
+                                                                   static_cast<int>(S.s), part);
+      else if (S.zeta == 8)
         k_sparse_sign_lanes<8><<<grid, 32, lane_smem, c.stream>>>(x_own, xscale, nloc, row_begin, S.key,
                                                                   static_cast<int>(S.s), 8, part);
       else
