@@ -802,11 +802,12 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
   // one HBM pass over [V U] with the norms fused: k_tsgemm for few outputs
   // (C5, k = 10: 17.4 vs 37 ms per restart through cuBLAS), the shared-memory
   // tiled k_rgemm for up to 24 (C2, k = 20); SDR_RGEMM=0 selects cuBLAS there
-  static const bool own_rgemm = [] {
+  static const int rgemm_mode = [] {  // 0: cuBLAS above 12 outputs, 1: default, 2: k_rgemm for every count
     const char* e = std::getenv("SDR_RGEMM");
-    return !e || std::atoi(e) != 0;
+    return e ? std::atoi(e) : 1;
   }();
-  const bool use_ts = ke <= 12 && tsgemm_supported(static_cast<int>(ke), nloc, w.lay.ld, sp.ld, sp.ld);
+  const bool own_rgemm = rgemm_mode != 0;
+  const bool use_ts = rgemm_mode != 2 && ke <= 12 && tsgemm_supported(static_cast<int>(ke), nloc, w.lay.ld, sp.ld, sp.ld);
   const bool use_rg = !use_ts && own_rgemm && rgemm_supported(static_cast<int>(ke), static_cast<int>(j + kc), w.lay.ld, sp.ld);
   if (dense_u && own_gemm && (use_ts || use_rg)) {
     const i64 kk = j + kc;
