@@ -617,6 +617,25 @@ __global__ void k_fold_partials(const double* __restrict__ partials, int G, int 
 }
 }  // namespace
 
+namespace {
+__global__ void k_fold_partials2(const double* __restrict__ p1, int G1, const double* __restrict__ p2, int G2, int nv,
+                                 double* __restrict__ out) {
+  const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (v >= nv) return;
+  double a = 0.0;
+  for (int b = lane; b < G1; b += 32) a += p1[static_cast<int64_t>(v) * G1 + b];
+  for (int b = lane; b < G2; b += 32) a += p2[static_cast<int64_t>(v) * G2 + b];
+  a = warp_sum(a);
+  if (lane == 0) out[v] = a;
+}
+}  // namespace
+
+void launch_fold_partials2(Context& c, const double* p1, int G1, const double* p2, int G2, int nv, double* out) {
+  TimedLaunch t(c, "fold_partials");
+  k_fold_partials2<<<(nv + 7) / 8, 256, 0, c.stream>>>(p1, G1, p2, G2, nv, out);
+  SDR_KERNEL_CHECK();
+}
+
 void launch_fold_partials(Context& c, const double* partials, int G, int nv, bool value_major, double* out) {
   TimedLaunch t(c, "fold_partials");
   k_fold_partials<<<(nv + 7) / 8, 256, 0, c.stream>>>(partials, G, nv, value_major ? 1 : 0, out);

@@ -126,10 +126,13 @@ void Context::allgather_i64(const i64* host_in, i64 count, i64* host_out) {
   sync();
 }
 
-void Context::halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin) {
+void Context::halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin,
+                            cudaStream_t on) {
   if (!comm_ || plan.empty()) return;
+  cudaStream_t stream = on ? on : this->stream;
+  const bool timed = timing && stream == this->stream;
   ++launches;
-  if (timing) time_begin("halo");
+  if (timed) time_begin("halo");
   auto comm = static_cast<ncclComm_t>(comm_);
   SDR_NCCL(nccl_->GroupStart());
   for (int q = 0; q < world; ++q) {
@@ -142,7 +145,7 @@ void Context::halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, 
                            comm, stream));
   }
   SDR_NCCL(nccl_->GroupEnd());
-  if (timing) time_end();
+  if (timed) time_end();
 }
 
 cudaEvent_t Context::take_event() {

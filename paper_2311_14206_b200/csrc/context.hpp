@@ -68,7 +68,9 @@ class Context {
   // ---- collectives (no-ops on one rank)
   void allreduce_sum(double* dev, i64 n);
   void allgather_i64(const i64* host_in, i64 count, i64* host_out);  // host in/out, small
-  void halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin);
+  /// on: the stream the transfers are issued on (default: the context stream).
+  void halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin,
+                     cudaStream_t on = nullptr);
 
   // ---- timing
   bool timing = false;

@@ -64,9 +64,12 @@ void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y);
 /// dots there, value-major [1 + nwin][grid], and nothing is folded; the
 /// return value is the grid size. max_blocks_per_sm < 0: the full resident
 /// grid regardless of the local size (identical layouts on every rank).
+/// [sl_begin, sl_end): the 32-row slices this launch covers (default all),
+/// so the halo-free interior can run while the halo is in flight.
 int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
-                        double* coef, double* partials_out = nullptr, int max_blocks_per_sm = 0);
+                        double* coef, double* partials_out = nullptr, int max_blocks_per_sm = 0,
+                        int64_t sl_begin = 0, int64_t sl_end = -1);
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2);
 /// Column pointers of a batched product (extended-vector layout, like x_ext).
 constexpr int kSpmmMax = 8;
@@ -133,6 +136,8 @@ struct StepFold {
 /// (K1) or CTA-major [G][nv] (K2). The several-rank pipeline folds locally
 /// before its allreduces.
 void launch_fold_partials(Context& c, const double* partials, int G, int nv, bool value_major, double* out);
+/// The same over two value-major partial arrays (a split K1: [nv][G1] then [nv][G2]), in that order.
+void launch_fold_partials2(Context& c, const double* p1, int G1, const double* p2, int G2, int nv, double* out);
 bool update_sketch_eligible(const SketchDev& S, const VecLayout& lay, int need, int64_t row_begin, int64_t ldv);
 int64_t update_sketch_partials_size(const SketchDev& S, int num_sms);
 /// Fused K2 + K3a (update pass and SRDCT of w_{j+1} in one sweep), writing

@@ -70,6 +70,9 @@ struct Workspace {
   // allreduce; comb[j & 1] = [K2(j) folded (nvp) | K1(j + 1) folded], one
   // allreduce per step
   DeviceBuffer<double> p1f, comb[2];
+  DeviceBuffer<double> p1b;                 // several ranks: boundary-slice partials of a split K1
+  cudaStream_t halo_stream = nullptr;       // several ranks: halo transfers beside K1's interior
+  cudaEvent_t ev_w = nullptr, ev_halo = nullptr;
   DeviceBuffer<double> gcoef;      // recycle-update GEMM coefficients
   DeviceBuffer<double> pside;      // recycle-update norm partials (runs on the side stream)
   DeviceBuffer<double> ps[2], pu[2];  // split pipeline: SRDCT / update partials by step parity
@@ -409,6 +412,29 @@ struct ArnoldiPipeline {
   double* pend_buf = nullptr;  // several ranks: K2's folded partials not yet allreduced
   int pend_n = 0;
 
+  /// Slices [b_lo, b_hi) whose stencils stay inside the own rows (rows
+  /// [halo_lo, nloc - halo_hi)); false when there is no halo or no interior.
+  /// SDR_K1_SPLIT=force splits a halo-free operator too (four slices each
+  /// side), which exercises the split launches on one rank.
+  bool k1_split_range(i64& b_lo, i64& b_hi) const {
+    static const int mode = [] {
+      const char* e = std::getenv("SDR_K1_SPLIT");
+      if (!e) return 1;
+      return std::string(e) == "force" ? 2 : std::atoi(e);
+    }();
+    if (mode == 0) return false;
+    const i64 ns = A.view().nslices;
+    if (A.plan.empty()) {
+      if (mode != 2 || ns < 16) return false;
+      b_lo = 4;
+      b_hi = ns - 4;
+      return true;
+    }
+    b_lo = (A.halo_lo + kSlice - 1) / kSlice;
+    b_hi = std::max<i64>(0, A.local_rows - A.halo_hi) / kSlice;
+    return b_lo < b_hi;
+  }
+
   /// Measurement: CUDA-event time of `reps` back-to-back relaunches of the
   /// last enqueued step's K1 and of its K2 on the library stream. Both are
   /// idempotent for fixed inputs (same y / w_{j+1} / partials / record rows
@@ -458,7 +484,13 @@ struct ArnoldiPipeline {
     for (auto& b : w.p2) b.ensure(update_sketch_partials_size(S, c.num_sms));
     if (c.distributed()) {
       w.p1f.ensure(34);
+      w.p1b.ensure(34 * static_cast<i64>(c.num_sms) * 8);
       for (auto& b : w.comb) b.ensure(update_sketch_partials_size(S, 1) + 34);
+      if (!w.halo_stream) {
+        SDR_CUDA(cudaStreamCreateWithFlags(&w.halo_stream, cudaStreamNonBlocking));
+        SDR_CUDA(cudaEventCreateWithFlags(&w.ev_w, cudaEventDisableTiming));
+        SDR_CUDA(cudaEventCreateWithFlags(&w.ev_halo, cudaEventDisableTiming));
+      }
     }
     if (split) {
       for (auto& b : w.ps) b.ensure(sketch_partials_size(S, c.num_sms));
@@ -481,7 +513,20 @@ struct ArnoldiPipeline {
     }
     if (deferred) {
       const bool dist = c.distributed();
-      c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
+      // several ranks: K1 over the interior slices (no halo rows in their
+      // stencils) runs while the halo of w_j moves on its own stream; the
+      // boundary slices follow once it has landed
+      i64 b_lo = 0, b_hi = 0;
+      const bool split_k1 = dist && k1_split_range(b_lo, b_hi);
+      if (split_k1) {
+        SDR_CUDA(cudaEventRecord(w.ev_w, c.stream));
+        SDR_CUDA(cudaStreamWaitEvent(w.halo_stream, w.ev_w, 0));
+        c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin,
+                        w.halo_stream);
+        SDR_CUDA(cudaEventRecord(w.ev_halo, w.halo_stream));
+      } else {
+        c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
+      }
       // several ranks: each rank folds its own CTA partials (fixed order) and
       // only the folded values cross the NVLink fabric, once per step
       // ([2s + t after K2(j-1) | 1 + nwin after K1(j)] instead of every
@@ -489,12 +534,25 @@ struct ArnoldiPipeline {
       // same sums, so all ranks fold identically
       StepFold sf;
       sf.k1_partials = w.p1.get();
-      sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
-                                    w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), 0);
+      int gb = 0;
+      if (split_k1) {
+        const i64 ns = A.view().nslices;
+        sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
+                                      w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), 0, b_lo, b_hi);
+        SDR_CUDA(cudaStreamWaitEvent(c.stream, w.ev_halo, 0));
+        gb = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
+                                 w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1b.get(), 0, b_hi, ns + b_lo);
+      } else {
+        sf.k1_G = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
+                                      w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), 0);
+      }
       if (dist) {  // K1(j)'s folded dots ride on the allreduce of K2(j-1)'s folded partials
         double* cb = pend_n > 0 ? pend_buf : w.p1f.get();
         const int off = pend_n;
-        launch_fold_partials(c, w.p1.get(), sf.k1_G, 1 + nwin, true, cb + off);
+        if (split_k1)
+          launch_fold_partials2(c, w.p1.get(), sf.k1_G, w.p1b.get(), gb, 1 + nwin, cb + off);
+        else
+          launch_fold_partials(c, w.p1.get(), sf.k1_G, 1 + nwin, true, cb + off);
         c.allreduce_sum(cb, off + 1 + nwin);
         sf.k1_partials = cb + off;
         sf.k1_G = 1;

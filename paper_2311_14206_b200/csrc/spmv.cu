@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
                                                                          int nwin, double* __restrict__ partials,
                                                                          unsigned* __restrict__ counter,
                                                                          double* __restrict__ out, MgsArgs mg,
-                                                                         unsigned long long* stamp) {
+                                                                         unsigned long long* stamp, int64_t sl_begin,
+                                                                         int64_t sl_end) {
   stamp_begin(stamp);
   const int lane = threadIdx.x & 31;
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -128,14 +129,18 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView
   // iteration ahead, so no load of the current slice waits on an index load
   const int D = FMT > 0 ? FMT : (FMT < 0 ? A.dia_d : 0);
   int nx_off = 0;
-  if (FMT != 0 && gw < A.nslices && lane < D) nx_off = __ldg(A.doff + gw * D + lane);
   pdl_trigger();  // the next kernel may start its constant-data prologue
   pdl_wait();     // x / the window vectors come from the previous kernel
   if constexpr (MODE == 3)
     if (*reinterpret_cast<const volatile int*>(aux)) return;
-  for (int64_t sl = gw; sl < A.nslices; sl += nwarps) {
+  // [sl_begin, sl_end) may run past nslices: slice indices wrap (a boundary
+  // launch covers the last slices and then the first ones)
+  auto wrap = [&](int64_t q) { return q >= A.nslices ? q - A.nslices : q; };
+  if (FMT != 0 && sl_begin + gw < sl_end && lane < D) nx_off = __ldg(A.doff + wrap(sl_begin + gw) * D + lane);
+  for (int64_t slv = sl_begin + gw; slv < sl_end; slv += nwarps) {
+    const int64_t sl = wrap(slv);
     const int cur_off = nx_off;
-    if (FMT != 0 && sl + nwarps < A.nslices && lane < D) nx_off = __ldg(A.doff + (sl + nwarps) * D + lane);
+    if (FMT != 0 && slv + nwarps < sl_end && lane < D) nx_off = __ldg(A.doff + wrap(slv + nwarps) * D + lane);
     const int64_t row = sl * kSlice + lane;
     const bool live = row < A.nrows;
     // epilogue operands are independent of the product: fetch them first
@@ -246,9 +251,9 @@ int64_t blocks_for(int64_t nslices) { return (nslices + (kThreads / 32) - 1) / (
 template <int MODE, int NV, int FMT>
 int launch_impl(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
                 int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
-                const MgsArgs& mg, double* partials_out, int max_per_sm) {
+                const MgsArgs& mg, double* partials_out, int max_per_sm, int64_t sl_begin, int64_t sl_end) {
   auto kern = k_sell_spmv<MODE, NV, FMT>;
-  const int g = resident_grid(c, kern, blocks_for(A.nslices), max_per_sm);
+  const int g = resident_grid(c, kern, blocks_for(std::max<int64_t>(sl_end - sl_begin, 1)), max_per_sm);
   double* part = partials_out ? partials_out : ((MODE == 1 || MODE == 2) ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
   TimedLaunch t(c, name);
   if (partials_out) {  // deferred step pipeline: programmatic dependent launch
@@ -260,10 +265,10 @@ int launch_impl(Context& c, const char* name, const SellView& A, const double* x
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     SDR_CUDA(cudaLaunchKernelEx(&cfg, kern, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part,
-                                static_cast<unsigned*>(nullptr), out, mg, c.launch_stamp(name)));
+                                static_cast<unsigned*>(nullptr), out, mg, c.launch_stamp(name), sl_begin, sl_end));
   } else {
     kern<<<g, kThreads, 0, c.stream>>>(A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, part, counter, out, mg,
-                                       static_cast<unsigned long long*>(nullptr));
+                                       static_cast<unsigned long long*>(nullptr), sl_begin, sl_end);
     SDR_KERNEL_CHECK();
   }
   return g;
@@ -272,8 +277,10 @@ int launch_impl(Context& c, const char* name, const SellView& A, const double* x
 template <int MODE, int NV>
 int launch_fmt(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
                int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
-               const MgsArgs& mg, double* partials_out = nullptr, int max_per_sm = 0) {
-#define SDR_SPMV_FMT(F) return launch_impl<MODE, NV, F>(c, name, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, counter, out, mg, partials_out, max_per_sm)
+               const MgsArgs& mg, double* partials_out = nullptr, int max_per_sm = 0, int64_t sl_begin = 0,
+               int64_t sl_end = -1) {
+  if (sl_end < 0) sl_end = A.nslices;
+#define SDR_SPMV_FMT(F) return launch_impl<MODE, NV, F>(c, name, A, x_ext, y, aux, ldv, own_off, halo_lo, j, nwin, counter, out, mg, partials_out, max_per_sm, sl_begin, sl_end)
   if (!A.doff)
     SDR_SPMV_FMT(0);
   else if (A.dia_d == 7)  // 3-D 7-point stencils
@@ -294,18 +301,18 @@ void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) 
 
 int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
-                        double* coef, double* partials_out, int max_per_sm) {
+                        double* coef, double* partials_out, int max_per_sm, int64_t sl_begin, int64_t sl_end) {
   const MgsArgs mg{rec, rstride, T, cvec, coef};
   const double* x_ext = V + j * ldv + lay.ext_shift();
   if (nwin <= 3)
     return launch_fmt<1, 4>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0,
-                            recA, mg, partials_out, max_per_sm);
+                            recA, mg, partials_out, max_per_sm, sl_begin, sl_end);
   else if (nwin <= 7)
     return launch_fmt<1, 8>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0,
-                            recA, mg, partials_out, max_per_sm);
+                            recA, mg, partials_out, max_per_sm, sl_begin, sl_end);
   else if (nwin <= 33)
     return launch_fmt<1, 34>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin,
-                             c.counters() + 0, recA, mg, partials_out, max_per_sm);
+                             c.counters() + 0, recA, mg, partials_out, max_per_sm, sl_begin, sl_end);
   else
     throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
 }

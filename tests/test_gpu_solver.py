@@ -272,3 +272,38 @@ def test_distributed_pipeline_on_one_rank(sk, O):
     for (i1, r1), (i2, r2) in zip(gd.report.true_residuals, g1.report.true_residuals):
         assert i1 == i2 and r1 == pytest.approx(r2, rel=1e-8)
     assert np.linalg.norm(gd.x - g1.x) <= 1e-9 * np.linalg.norm(g1.x)
+
+
+def test_distributed_split_k1_matches(sk, O):
+    """The several-rank K1 split (interior slices beside the halo transfer,
+    boundary slices after it, partials folded over both launches) forced on a
+    one-rank communicator (SDR_K1_SPLIT=force, a fresh process): same solve."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2311_14206_b200 as sk
+from oracle import pyoracle as O
+n = 24
+cfg = sk.SolverConfig(m=30, k=8, t=2, s=80, tol=1e-8, max_restarts=20)
+ctx = sk.Context(0, 0, 1, sk.Context.nccl_unique_id())
+A = sk.SparseMatrix.convdiff3d_device(n, 100.0, 50.0, 25.0, ctx=ctx)
+b = O.gaussian_vector(n ** 3, 1)
+r = sk.solve(A, b, cfg, space=sk.RecycleSpace(ctx), sketch=sk.SketchOperator.subsampled_dct(n ** 3, 80, cfg.sketch_seed, ctx=ctx))
+print(json.dumps(dict(it=r.report.iterations, st=r.report.status, res=[v for _, v in r.report.true_residuals],
+                      x=np.asarray(r.x).tolist())))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("0", "force"):
+        env = dict(os.environ, SDR_K1_SPLIT=mode)
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs[mode] = json.loads(p.stdout.strip().splitlines()[-1])
+    a, f = outs["0"], outs["force"]
+    assert a["st"] == f["st"] and a["it"] == f["it"]
+    np.testing.assert_allclose(f["res"], a["res"], rtol=1e-8)
+    np.testing.assert_allclose(f["x"], a["x"], rtol=1e-8, atol=1e-10 * np.linalg.norm(a["x"]))
