@@ -182,6 +182,11 @@ SDR_API int sdr_partition_rows(int64_t rows, int world, int64_t granule, int64_t
 /* CSR arrays are written by the caller-allocated buffers; call with NULL
  * buffers first to get nnz. convdiff2d(n, bx, by, shift, diag_rel):
  * −Δu + β·∇u on n×n, equals −gen_convdiff(n, −β) when bx == by (problems.hpp:70-88). */
+/* gen_neumann (problems.hpp:38-61): shifted five-point grid operator with mirrored
+ * boundary neighbours, CSR as SparseMatrix::from_triplets builds it. Two-call:
+ * NULL arrays -> *nnz. */
+SDR_API int sdr_gen_neumann(int64_t grid_side, double shift, int64_t* nnz, int64_t* offsets, int64_t* columns,
+                            double* values);
 SDR_API int sdr_gen_convdiff2d(int64_t n, double bx, double by, double shift, const double* diag_rel,
                                int64_t* nnz, int64_t* offsets, int64_t* columns, double* values);
 SDR_API int sdr_gen_convdiff3d(int64_t n, double bx, double by, double bz, int64_t z_begin, int64_t z_end,

@@ -39,7 +39,8 @@ __all__ = [
     "SolveResult", "SequenceResult", "ProblemInstance", "solve", "solve_sequence",
     "BaselineConfig", "BaselineResult", "baseline_gmres", "read_matrix_market", "write_matrix_market",
     "matrix_market_string", "save_recycle_space", "load_recycle_space", "read_space_file", "space_file_bytes", "IncrementalQR", "harmonic_pairs",
-    "gaussian_vector", "gen_convdiff", "gen_convdiff2d", "gen_convdiff3d", "sparse_sign_entries", "partition_halo",
+    "gaussian_vector", "gen_convdiff", "gen_convdiff2d", "gen_convdiff3d", "gen_neumann", "neumann_sequence",
+    "convdiff_sequence", "sparse_sign_entries", "partition_halo",
     "partition_rows", "SdrError", "CudaError",
 ]
 
@@ -415,6 +416,36 @@ def gen_convdiff(n, alpha):
     """Reference gen_convdiff(n, alpha) (problems.hpp:70-88) = −convdiff2d(n, −alpha, −alpha)."""
     off, col, val = gen_convdiff2d(n, -alpha, -alpha)
     return off, col, -val
+
+
+def gen_neumann(grid_side, shift):
+    """(offsets, columns, values) of gen_neumann (problems.hpp:38-61)."""
+    nnz = _gen_csr(_lib.sdr_gen_neumann, grid_side, shift)
+    n = grid_side * grid_side
+    off = np.empty(n + 1, dtype=np.int64)
+    col = np.empty(nnz, dtype=np.int64)
+    val = np.empty(nnz)
+    _check(_lib.sdr_gen_neumann(grid_side, shift, None, off.ctypes.data_as(C.c_void_p), col.ctypes.data_as(C.c_void_p),
+                                val.ctypes.data_as(C.c_void_p)))
+    return off, col, val
+
+
+def neumann_sequence(grid_side, shift, count, seed, tol, ctx=None):
+    """problems.hpp:92-107: one operator, rhs i = gaussian_vector(n, seed + i),
+    target_tol = tol; solve with solve_sequence(..., shared_matrix=True)."""
+    off, col, val = gen_neumann(grid_side, shift)
+    n = grid_side * grid_side
+    A = SparseMatrix(n, n, off, col, val, ctx=ctx)
+    return [ProblemInstance(A, gaussian_vector(n, seed + i), target_tol=tol) for i in range(count)]
+
+
+def convdiff_sequence(n, alphas, tol, ctx=None):
+    """problems.hpp:109-123: one gen_convdiff(n, alpha) system per alpha, all-ones rhs."""
+    out = []
+    for a in alphas:
+        off, col, val = gen_convdiff(n, a)
+        out.append(ProblemInstance(SparseMatrix(n * n, n * n, off, col, val, ctx=ctx), np.ones(n * n), target_tol=tol))
+    return out
 
 
 def gen_convdiff3d(n, bx, by, bz, z_begin=0, z_end=None):

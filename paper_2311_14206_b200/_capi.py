@@ -92,6 +92,7 @@ SIGNATURES = {
     "sdr_harmonic_qr": (cint, [vp, vp, i64, i64, i64, f64, i32, P(i64), P(i64), P(cint), P(cint), vp, vp, vp]),
     "sdr_partition_halo": (cint, [cint, cint, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sdr_partition_rows": (cint, [i64, cint, i64, vp, vp]),
+    "sdr_gen_neumann": (cint, [i64, f64, P(i64), vp, vp, vp]),
     "sdr_gen_convdiff2d": (cint, [i64, f64, f64, f64, vp, P(i64), vp, vp, vp]),
     "sdr_gen_convdiff3d": (cint, [i64, f64, f64, f64, i64, i64, P(i64), vp, vp, vp]),
     "sdr_csr_create_convdiff3d": (cint, [vp, i64, i64, i64, f64, f64, f64, i64, i64, P(vp)]),

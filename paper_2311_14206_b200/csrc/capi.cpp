@@ -10,6 +10,7 @@
 #include "sketch.hpp"
 #include "solver.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -649,6 +650,36 @@ int sdr_gen_convdiff2d(int64_t n, double bx, double by, double shift, const doub
           if (!has[e] || vv[e] == 0.0) continue;  // from_triplets drops exact zeros
           if (col) col[k] = cc[e];
           if (val) val[k] = vv[e];
+          ++k;
+        }
+        if (off) off[p + 1] = k;
+      }
+    if (nnz) *nnz = k;
+  });
+}
+
+int sdr_gen_neumann(int64_t g, double shift, int64_t* nnz, int64_t* off, int64_t* col, double* val) {
+  return guard([&] {  // gen_neumann (problems.hpp:38-61): mirrored neighbours, duplicates summed, zeros dropped
+    if (g < 2) throw invalid("gen_neumann: grid_side must be at least 2");
+    auto reflect = [g](int64_t i) { return i < 0 ? -i : (i >= g ? 2 * g - 2 - i : i); };
+    int64_t k = 0;
+    if (off) off[0] = 0;
+    for (int64_t r = 0; r < g; ++r)
+      for (int64_t c = 0; c < g; ++c) {
+        const int64_t p = r * g + c;
+        std::pair<int64_t, double> e[5] = {{p, 4.0 + shift},
+                                           {reflect(r - 1) * g + c, -1.0},
+                                           {reflect(r + 1) * g + c, -1.0},
+                                           {r * g + reflect(c - 1), -1.0},
+                                           {r * g + reflect(c + 1), -1.0}};
+        std::stable_sort(e, e + 5, [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (int i = 0; i < 5;) {
+          const int64_t cc = e[i].first;
+          double v = 0.0;
+          for (; i < 5 && e[i].first == cc; ++i) v += e[i].second;
+          if (v == 0.0) continue;
+          if (col) col[k] = cc;
+          if (val) val[k] = v;
           ++k;
         }
         if (off) off[p + 1] = k;

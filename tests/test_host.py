@@ -267,3 +267,17 @@ def test_campaign_out_dir_resolution_and_solver_names(monkeypatch):
     assert cp.resolve_out_dir("explicit", "fallback") == "explicit"
     assert [cp.known_solver(s) for s in ("gmres-sdr", "sgmres", "gmres", "cg")] == [True, True, True, False]
     assert cp.num(0.1) == "0.10000000000000001" and cp.num(float("nan")) == "nan"
+
+
+@pytest.mark.parametrize("g,shift", [(2, 0.0), (5, 0.1), (103, 1e-4), (12, 0.5)])
+def test_gen_neumann_matches_oracle(sk, O, g, shift):
+    """problems.hpp:38-61 (mirrored neighbours, duplicates summed): CSR identical to the oracle's."""
+    off, col, val = sk.gen_neumann(g, shift)
+    oo, oc, ov = O.gen_neumann(g, shift).csr()
+    assert np.array_equal(off, oo) and np.array_equal(col, oc) and np.array_equal(val, ov)
+    # the unshifted operator's rows sum to zero (all-ones null space)
+    off0, col0, val0 = sk.gen_neumann(g, 0.0)
+    sums = np.add.reduceat(val0, off0[:-1])
+    assert np.all(sums == 0.0)
+    with pytest.raises(ValueError):
+        sk.gen_neumann(1, 0.0)
