@@ -100,8 +100,11 @@ SDR_API int sdr_csr_info(const sdr_csr* A, int64_t* rows, int64_t* cols, int64_t
                          int64_t* local_rows, int64_t* halo_lo, int64_t* halo_hi);
 /* NEW: device storage chosen for the block. format 0 = SELL-32 (12 B per stored
  * entry), 1 = SELL-DIA (8 B per stored entry + one int32 offset per slice
- * diagonal); diagonals = DIA diagonals per slice (0 for SELL); stored =
- * entries incl. padding; bytes = storage bytes one SpMV streams. */
+ * diagonal), 2 = ZSELL (a one-rank operator whose 2x2 blocks are all
+ * [[a, -b], [b, a]]: a complex matrix on interleaved (re, im) vectors, stored
+ * as complex entries, 20 B each — the complex-fp64 SpMV of BASELINE C4);
+ * diagonals = DIA diagonals per slice (0 otherwise); stored = entries incl.
+ * padding (complex entries for ZSELL); bytes = storage bytes one SpMV streams. */
 SDR_API int sdr_csr_storage(const sdr_csr* A, int32_t* format, int32_t* diagonals, int64_t* stored, int64_t* bytes);
 /* y = A x (OperatorRef::apply, operator_ref.hpp:38-44). x: local_rows entries of this
  * rank's block (halos are exchanged internally); y: local_rows entries. Host or device. */

@@ -200,7 +200,7 @@ class SparseMatrix:
         fmt, dg, st, nb = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
         _check(_lib.sdr_csr_storage(self._h, C.byref(fmt), C.byref(dg), C.byref(st), C.byref(nb)))
         # device storage: "sell" or "dia", diagonals per slice, stored entries, bytes per SpMV
-        self.storage = dict(format=("sell", "dia")[fmt.value], diagonals=dg.value, stored=st.value,
+        self.storage = dict(format=("sell", "dia", "zsell")[fmt.value], diagonals=dg.value, stored=st.value,
                             bytes=nb.value)
 
     @classmethod

@@ -278,12 +278,13 @@ int sdr_csr_storage(const sdr_csr* A, int32_t* format, int32_t* diagonals, int64
   return guard([&] {
     need(A, "A");
     const auto& o = *A->op;
-    const int64_t nslices = (o.local_rows + sdr::kSlice - 1) / sdr::kSlice;
-    if (format) *format = o.dia ? 1 : 0;
+    const int64_t nslices = o.view().nslices;
+    if (format) *format = o.dia ? 1 : (o.cplx ? 2 : 0);
     if (diagonals) *diagonals = o.dia ? o.dia_d : 0;
     if (stored) *stored = o.stored;
     if (bytes)
-      *bytes = o.dia ? 8 * o.stored + 4 * nslices * o.dia_d : 12 * o.stored + 8 * (nslices + 1);
+      *bytes = o.dia ? 8 * o.stored + 4 * nslices * o.dia_d
+                     : (o.cplx ? 20 * o.stored : 12 * o.stored) + 8 * (nslices + 1);
   });
 }
 

@@ -15,6 +15,8 @@ struct SellView {
   const double* vals = nullptr;
   const int32_t* doff = nullptr;  // SELL-DIA: [nslices][dia_d] diagonal offsets; null for plain SELL
   int dia_d = 0;                   // SELL-DIA diagonals per slice (slice_ptr unused)
+  int cplx = 0;  // ZSELL: 2x2 [[a, -b], [b, a]] blocks stored as complex a + ib; slices of 32 complex rows,
+                 // cols = complex column of the extended vector, vals = (re, im) pairs; vectors interleaved
   int64_t nrows = 0, nslices = 0;
   int64_t halo_lo = 0, ext_len = 0;  // own row r is extended index halo_lo + r
 };

@@ -20,6 +20,45 @@ bool pdl_enabled() {
 }
 
 /// SDR_DIA=0 forces plain SELL storage (A/B and parity checks).
+bool zsell_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SDR_ZSELL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+/// Complex structure of a one-rank real operator: every 2x2 block (rows
+/// 2p, 2p+1; columns 2q, 2q+1) is [[a, -b], [b, a]] (missing entries = 0),
+/// i.e. the operator is a complex matrix acting on interleaved (re, im)
+/// vectors. On success ccol / cval / coff hold its complex CSR (value pairs).
+bool complex_structure(int64_t rows, const int64_t* off, const int64_t* col, const double* val,
+                       std::vector<int64_t>& coff, std::vector<int64_t>& ccol, std::vector<double>& cval) {
+  if (rows % 2) return false;
+  const int64_t nc = rows / 2;
+  coff.assign(static_cast<size_t>(nc) + 1, 0);
+  ccol.clear();
+  cval.clear();
+  for (int64_t pr = 0; pr < nc; ++pr) {
+    int64_t i0 = off[2 * pr], i1 = off[2 * pr + 1];          // row 2p (real part)
+    int64_t k0 = off[2 * pr + 1], k1 = off[2 * pr + 2];      // row 2p + 1 (imaginary part)
+    while (i0 < i1 || k0 < k1) {
+      const int64_t q = std::min(i0 < i1 ? col[i0] / 2 : std::numeric_limits<int64_t>::max(), k0 < k1 ? col[k0] / 2 : std::numeric_limits<int64_t>::max());
+      double a = 0, mb = 0, b = 0, a2 = 0;
+      if (i0 < i1 && col[i0] == 2 * q) a = val[i0++];
+      if (i0 < i1 && col[i0] == 2 * q + 1) mb = val[i0++];
+      if (k0 < k1 && col[k0] == 2 * q) b = val[k0++];
+      if (k0 < k1 && col[k0] == 2 * q + 1) a2 = val[k0++];
+      if (a != a2 || mb != -b) return false;
+      ccol.push_back(q);
+      cval.push_back(a);
+      cval.push_back(b);
+    }
+    coff[static_cast<size_t>(pr) + 1] = static_cast<int64_t>(ccol.size());
+  }
+  return true;
+}
+
 bool dia_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("SDR_DIA");
@@ -136,6 +175,60 @@ DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int6
   const int64_t ext_len = op->halo_lo + local_rows + op->halo_hi;
   if (ext_len > std::numeric_limits<int32_t>::max())
     throw invalid("SparseMatrix: local extended block of " + std::to_string(ext_len) + " rows exceeds int32 indexing");
+  // ZSELL: a complex matrix in real-equivalent form (interleaved vectors)
+  // is stored as complex entries — 20 bytes per complex entry instead of four
+  // 12-byte real entries (BASELINE C4)
+  {
+    std::vector<int64_t> coff, ccol;
+    std::vector<double> cval;
+    if (!c.distributed() && zsell_enabled() && rows == cols && local_rows > 0 &&
+        complex_structure(local_rows, off, col, val, coff, ccol, cval)) {
+      const int64_t nc = local_rows / 2, ns = (nc + kSlice - 1) / kSlice;
+      std::vector<int64_t> zsp(static_cast<size_t>(ns) + 1, 0);
+      for (int64_t sl = 0; sl < ns; ++sl) {
+        int64_t mx = 0;
+        for (int64_t r = sl * kSlice; r < std::min(nc, (sl + 1) * kSlice); ++r)
+          mx = std::max(mx, coff[static_cast<size_t>(r) + 1] - coff[static_cast<size_t>(r)]);
+        zsp[static_cast<size_t>(sl) + 1] = zsp[static_cast<size_t>(sl)] + mx * kSlice;
+      }
+      const int64_t total = zsp[static_cast<size_t>(ns)];
+      std::vector<int32_t> hc(static_cast<size_t>(total));
+      std::vector<double> hv(static_cast<size_t>(2 * total), 0.0);
+      for (int64_t sl = 0; sl < ns; ++sl) {
+        const int64_t len = (zsp[static_cast<size_t>(sl) + 1] - zsp[static_cast<size_t>(sl)]) / kSlice;
+        for (int lane = 0; lane < kSlice; ++lane) {
+          const int64_t r = sl * kSlice + lane;
+          const int64_t self = std::min(r, nc - 1);
+          for (int64_t k = 0; k < len; ++k) {
+            const size_t dst = static_cast<size_t>(zsp[static_cast<size_t>(sl)] + k * kSlice + lane);
+            const int64_t n_r = r < nc ? coff[static_cast<size_t>(r) + 1] - coff[static_cast<size_t>(r)] : 0;
+            if (k < n_r) {
+              const size_t src = static_cast<size_t>(coff[static_cast<size_t>(r)] + k);
+              hc[dst] = static_cast<int32_t>(ccol[src]);
+              hv[2 * dst] = cval[2 * src];
+              hv[2 * dst + 1] = cval[2 * src + 1];
+            } else {
+              hc[dst] = static_cast<int32_t>(self);  // padding: zero value, own column
+            }
+          }
+        }
+      }
+      op->cplx = true;
+      op->stored = total;
+      op->slice_ptr.resize(ns + 1);
+      op->cols_idx.resize(std::max<int64_t>(total, 1));
+      op->vals.resize(std::max<int64_t>(2 * total, 2));
+      SDR_CUDA(cudaMemcpyAsync(op->slice_ptr.get(), zsp.data(), sizeof(int64_t) * zsp.size(), cudaMemcpyHostToDevice,
+                               c.stream));
+      if (total) {
+        SDR_CUDA(cudaMemcpyAsync(op->cols_idx.get(), hc.data(), sizeof(int32_t) * hc.size(), cudaMemcpyHostToDevice,
+                                 c.stream));
+        SDR_CUDA(cudaMemcpyAsync(op->vals.get(), hv.data(), sizeof(double) * hv.size(), cudaMemcpyHostToDevice, c.stream));
+      }
+      c.sync();
+      return op.release();
+    }
+  }
   const int64_t nslices = (local_rows + kSlice - 1) / kSlice;
   std::vector<int64_t> sp(static_cast<size_t>(nslices) + 1, 0);
   // SELL-DIA when every slice's entries lie on at most kMaxDiag diagonals

@@ -22,8 +22,9 @@ struct DeviceOperator {
   DeviceBuffer<double> vals;
   HaloPlan plan;
   bool dia = false;
+  bool cplx = false;  // ZSELL (complex-structured real operator, see SellView::cplx)
   int dia_d = 0;  // SELL-DIA diagonals per slice
-  int64_t stored = 0;  // stored entries (incl. padding) — bytes = stored * (dia ? 8 : 12)
+  int64_t stored = 0;  // stored entries (incl. padding) — bytes = stored * (dia ? 8 : cplx ? 20 : 12)
 
   SellView view() const {
     SellView v;
@@ -31,9 +32,10 @@ struct DeviceOperator {
     v.cols = dia ? nullptr : cols_idx.get();
     v.doff = dia ? doff.get() : nullptr;
     v.dia_d = dia ? dia_d : 0;
+    v.cplx = cplx ? 1 : 0;
     v.vals = vals.get();
     v.nrows = local_rows;
-    v.nslices = (local_rows + kSlice - 1) / kSlice;
+    v.nslices = cplx ? (local_rows / 2 + kSlice - 1) / kSlice : (local_rows + kSlice - 1) / kSlice;
     v.halo_lo = halo_lo;
     v.ext_len = halo_lo + local_rows + halo_hi;
     return v;

@@ -238,6 +238,110 @@ __global__ void __launch_bounds__(kThreads) k_sell_spmm(SellView A, SpmmCols X, 
   }
 }
 
+/// ZSELL (complex-structured operator, interleaved vectors): lane = complex
+/// row p (real rows 2p, 2p+1), one 16-byte value and one 16-byte x gather per
+/// complex entry. The real / imaginary sums run over the entries in the order
+/// of the real CSR rows (a·xr then −b·xi; b·xr then a·xi per column), so the
+/// result equals the real SELL path's bit for bit. Same MODEs / epilogues as
+/// k_sell_spmv, on double2 rows.
+template <int MODE, int NV>
+__global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_zsell_spmv(SellView A, const double* __restrict__ x_ext,
+                                                                          double* __restrict__ y,
+                                                                          const double* __restrict__ aux, int64_t ldv,
+                                                                          int64_t own_off, int64_t halo_lo, int j,
+                                                                          int nwin, double* __restrict__ partials,
+                                                                          unsigned* __restrict__ counter,
+                                                                          double* __restrict__ out, MgsArgs mg,
+                                                                          unsigned long long* stamp, int64_t,
+                                                                          int64_t) {  // slice range: one-rank only
+  stamp_begin(stamp);
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t nrc = A.nrows / 2, hlc = halo_lo / 2;
+  const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x_ext);
+  const double2* __restrict__ v2 = reinterpret_cast<const double2*>(A.vals);
+  double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  pdl_trigger();
+  pdl_wait();
+  if constexpr (MODE == 3)
+    if (*reinterpret_cast<const volatile int*>(aux)) return;
+  for (int64_t sl = gw; sl < A.nslices; sl += nwarps) {
+    const int64_t p = sl * kSlice + lane;
+    const bool live = p < nrc;
+    double2 e0 = make_double2(0.0, 0.0), ew[NV > 2 ? NV - 2 : 1];
+    if constexpr (MODE == 1) {
+      if (live) e0 = x2[hlc + p];
+#pragma unroll
+      for (int d = 1; d < NV - 1; ++d)
+        ew[d - 1] = (live && d < nwin) ? __ldcs(reinterpret_cast<const double2*>(aux + (j - d) * ldv + own_off) + p)
+                                       : make_double2(0.0, 0.0);
+    } else if constexpr (MODE == 2) {
+      if (live) e0 = __ldcs(reinterpret_cast<const double2*>(aux) + p);
+    }
+    const int64_t p0 = A.slice_ptr[sl];
+    const int len = static_cast<int>((A.slice_ptr[sl + 1] - p0) >> 5);
+    double sr = 0.0, si = 0.0;
+    for (int k0 = 0; k0 < len; k0 += kBatch) {
+      int32_t c[kBatch];
+      double2 v[kBatch], xv[kBatch];
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        const bool ok = k0 + k < len;
+        c[k] = ok ? __ldcs(A.cols + p0 + (k0 + k) * kSlice + lane) : 0;
+        v[k] = ok ? __ldcs(v2 + p0 + (k0 + k) * kSlice + lane) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) xv[k] = k0 + k < len ? __ldg(x2 + c[k]) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k)
+        if (k0 + k < len) {
+          sr = fma(v[k].x, xv[k].x, sr);
+          sr = fma(-v[k].y, xv[k].y, sr);
+          si = fma(v[k].y, xv[k].x, si);
+          si = fma(v[k].x, xv[k].y, si);
+        }
+    }
+    if (live) {
+      if constexpr (MODE == 0 || MODE == 3) {
+        y2[p] = make_double2(sr, si);
+      } else if constexpr (MODE == 1) {
+        y2[p] = make_double2(sr, si);
+        acc[0] = fma(sr, sr, fma(si, si, acc[0]));
+        acc[1] = fma(sr, e0.x, fma(si, e0.y, acc[1]));
+#pragma unroll
+        for (int d = 1; d < NV - 1; ++d)
+          if (d < nwin) acc[1 + d] = fma(sr, ew[d - 1].x, fma(si, ew[d - 1].y, acc[1 + d]));
+      } else {
+        const double rr = e0.x - sr, ri = e0.y - si;
+        y2[p] = make_double2(rr, ri);
+        acc[0] = fma(rr, rr, fma(ri, ri, acc[0]));
+      }
+    }
+  }
+  if constexpr (MODE == 1 || MODE == 2) {
+    const int nv = MODE == 1 ? 1 + nwin : 1;
+    block_partials<NV>(acc, nv, partials);
+    if (counter == nullptr) {
+      stamp_end(stamp);
+      return;
+    }
+    if (last_block_done(counter)) {
+      fold_partials(partials, gridDim.x, nv, out);
+      if constexpr (MODE == 1) {
+        if (mg.coef) {
+          __syncthreads();
+          if (threadIdx.x == 0) mgs_coefficients<NV - 1>(mg.rec, mg.rstride, mg.T, j, nwin, mg.cvec, mg.coef, true);
+        }
+      }
+      if (threadIdx.x == 0) *counter = 0u;
+    }
+  }
+}
+
 template <class K>
 int resident_grid(const Context& c, K kernel, int64_t want_blocks, int max_per_sm = 0) {
   int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), kThreads, 0);
@@ -252,7 +356,7 @@ template <int MODE, int NV, int FMT>
 int launch_impl(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
                 int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
                 const MgsArgs& mg, double* partials_out, int max_per_sm, int64_t sl_begin, int64_t sl_end) {
-  auto kern = k_sell_spmv<MODE, NV, FMT>;
+  auto kern = A.cplx ? k_zsell_spmv<MODE, NV> : k_sell_spmv<MODE, NV, FMT>;
   const int g = resident_grid(c, kern, blocks_for(std::max<int64_t>(sl_end - sl_begin, 1)), max_per_sm);
   double* part = partials_out ? partials_out : ((MODE == 1 || MODE == 2) ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
   TimedLaunch t(c, name);
@@ -319,6 +423,10 @@ int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t 
 
 void launch_spmm(Context& c, const SellView& A, const SpmmCols& X, int nb, double* Y, int64_t ldy) {
   if (A.nrows == 0 || nb == 0) return;
+  if (A.cplx) {  // ZSELL: one product per column
+    for (int q = 0; q < nb; ++q) launch_spmv(c, A, X.x[q], Y + q * ldy);
+    return;
+  }
   if (nb > kSpmmMax) throw invalid("launch_spmm: at most 8 columns per launch");
   auto go = [&](auto kern) {
     const int g = resident_grid(c, kern, blocks_for(A.nslices));

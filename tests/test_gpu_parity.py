@@ -5,6 +5,7 @@ outputs within 1e-12 relative (fp64), sketch rows/signs bit-identical,
 solver status equal with iteration counts within ±2%.
 """
 import numpy as np
+import scipy.sparse as sp
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -289,3 +290,89 @@ def test_recycle_product_kernels(sk, kernel, n, k1, k2, nout):
     ref = A1[:n, :k1] @ B[:k1] + (A2[:n, :k2] @ B[k1:] if k2 else 0.0)
     assert np.linalg.norm(Cm - ref) <= 1e-13 * np.linalg.norm(ref)
     np.testing.assert_allclose(nr, (ref ** 2).sum(axis=0), rtol=1e-12)
+
+
+def _complex_realified(rng, nc, per_row, zero_imag_diag=True):
+    """Random complex CSR -> its real-equivalent (interleaved (re, im)) CSR."""
+    rows, cols, vals = [], [], []
+    for p in range(nc):
+        qs = np.unique(np.concatenate([[p], rng.integers(0, nc, per_row)]))
+        for q in qs:
+            a = rng.standard_normal() + (4.0 if q == p else 0.0)
+            b = 0.0 if (q == p and zero_imag_diag) else rng.standard_normal()
+            for rr, cc, vv in ((2 * p, 2 * q, a), (2 * p, 2 * q + 1, -b), (2 * p + 1, 2 * q, b), (2 * p + 1, 2 * q + 1, a)):
+                if vv != 0.0:
+                    rows.append(rr)
+                    cols.append(cc)
+                    vals.append(vv)
+    M = sp.csr_matrix((vals, (rows, cols)), shape=(2 * nc, 2 * nc))
+    M.sort_indices()
+    return M
+
+
+def test_complex_spmv_zsell_matches_real_path(sk, O):
+    """ZSELL (complex-fp64 SpMV on interleaved vectors) equals the real SELL
+    path on the realified operator bit for bit, and the complex product."""
+    import os
+    import subprocess
+    import sys
+    rng = np.random.default_rng(5)
+    nc = 3000
+    M = _complex_realified(rng, nc, 8)
+    A = sk.SparseMatrix(2 * nc, 2 * nc, M.indptr.astype(np.int64), M.indices.astype(np.int64), M.data)
+    assert A.storage["format"] == "zsell"
+    x = O.gaussian_vector(2 * nc, 3)
+    y = A.apply(x)
+    ref = M @ x
+    assert np.linalg.norm(y - ref) <= 1e-14 * np.linalg.norm(ref)
+    # the same operator with ZSELL off (real SELL-32) in a fresh process: identical bits
+    code = ("import sys, numpy as np; sys.path.insert(0, '.'); import paper_2311_14206_b200 as sk; "
+            "d = np.load(sys.argv[1]); A = sk.SparseMatrix(d['n'], d['n'], d['o'], d['c'], d['v']); "
+            "assert A.storage['format'] == 'sell'; np.save(sys.argv[2], A.apply(d['x']))")
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        np.savez(os.path.join(td, "in.npz"), n=2 * nc, o=M.indptr.astype(np.int64), c=M.indices.astype(np.int64),
+                 v=M.data, x=x)
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        p = subprocess.run([sys.executable, "-c", code, os.path.join(td, "in.npz"), os.path.join(td, "out.npy")],
+                           cwd=root, env=dict(os.environ, SDR_ZSELL="0"), capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        y_real = np.load(os.path.join(td, "out.npy"))
+    assert np.array_equal(y, y_real)
+    # as a complex product
+    z = x[0::2] + 1j * x[1::2]
+    Z = (M[0::2, 0::2] + 1j * M[1::2, 0::2])
+    yz = Z @ z
+    np.testing.assert_allclose(y[0::2] + 1j * y[1::2], yz, rtol=1e-12, atol=1e-12 * np.abs(yz).max())
+
+
+def test_complex_structure_detection_rejects_real_operators(sk):
+    off, col, val = sk.gen_convdiff(30, -20.0)
+    A = sk.SparseMatrix(900, 900, off, col, val)
+    assert A.storage["format"] != "zsell"
+    rng = np.random.default_rng(6)
+    M = _complex_realified(rng, 200, 4)
+    M = M.tolil()
+    M[0, 1] += 1e-3  # breaks one 2x2 block
+    M = M.tocsr()
+    B = sk.SparseMatrix(400, 400, M.indptr.astype(np.int64), M.indices.astype(np.int64), M.data)
+    assert B.storage["format"] == "sell"
+
+
+def test_complex_system_solves_through_zsell(sk, O):
+    """A complex system in real-equivalent form: the solve on ZSELL storage
+    equals the oracle's real GMRES-SDR on the realified CSR."""
+    rng = np.random.default_rng(8)
+    nc = 2000
+    M = _complex_realified(rng, nc, 6)
+    off, col, val = M.indptr.astype(np.int64), M.indices.astype(np.int64), M.data
+    A = sk.SparseMatrix(2 * nc, 2 * nc, off, col, val)
+    assert A.storage["format"] == "zsell"
+    b = O.gaussian_vector(2 * nc, 9)
+    cfg = sk.SolverConfig(m=40, k=8, t=3, s=100, tol=1e-10, max_restarts=20)
+    r = sk.solve(A, b, cfg)
+    xo, ro = O.solve(O.SparseMatrix.from_csr(2 * nc, 2 * nc, off, col, val), b,
+                     O.SolverConfig(m=40, k=8, t=3, s=100, tol=1e-10, max_restarts=20))
+    assert r.report.status == ro.status == "converged"
+    assert abs(r.report.iterations - ro.iterations) <= max(1, 0.02 * ro.iterations)
+    assert np.linalg.norm(b - M @ r.x) <= 1e-10 * np.linalg.norm(b) * (1 + 1e-9)
