@@ -351,6 +351,30 @@ def main():
                 "arnoldi_step": {"bytes": step_bytes, "us": step_us, "GBps": step_bytes / (step_us * 1e-6) / 1e9,
                                  "frac": step_bytes / (step_us * 1e-6) / 1e9 / peak,
                                  "timer": "sum of per-launch CUDA events in one instrumented solve"}}
+    # the step as it runs inside a solve: device-clock stamps (no host events
+    # in the stream), median interval between consecutive K1 starts
+    try:
+        import tempfile
+        sk._check(sk._lib.sdr_ctx_set_stamps(ctx._h, 1))
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "stamps.csv").encode()
+            sk._check(sk._lib.sdr_debug_stamps(ctx._h, path))  # reset
+            one(b_dev)
+            ctx.synchronize()
+            sk._check(sk._lib.sdr_debug_stamps(ctx._h, path))
+            starts = sorted(int(ln.split(",")[1]) for ln in open(path.decode()).read().splitlines()[1:]
+                            if ln.startswith("spmv_arnoldi,") and int(ln.split(",")[2]) > 0)
+        sk._check(sk._lib.sdr_ctx_set_stamps(ctx._h, 0))
+        d = np.diff(np.array(starts, dtype=np.float64)) / 1e3
+        med = float(np.median(d))
+        per = float(np.median(d[d < 2.0 * med]))  # restart boundaries excluded
+        roofline["arnoldi_step_pipelined"] = {"bytes": step_bytes, "period_us": per,
+                                              "GBps": step_bytes / (per * 1e-6) / 1e9,
+                                              "frac": step_bytes / (per * 1e-6) / 1e9 / peak,
+                                              "timer": "device %globaltimer launch stamps in one solve: median "
+                                                       "interval between consecutive K1 starts (restarts excluded)"}
+    except Exception as e:  # measurement only
+        print(f"step period measurement skipped: {e}", file=sys.stderr)
     if iso:
         iso_us = iso["spmv_arnoldi"] + iso["update_sketch"]
         roofline["arnoldi_step_isolated"] = {"bytes": step_bytes, "us": iso_us,

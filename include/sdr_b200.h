@@ -272,6 +272,14 @@ SDR_API int sdr_debug_block_product(sdr_ctx* ctx, int32_t kernel, int64_t n, con
  * library stream. The relaunches are idempotent. One-GPU SRDCT contexts. */
 SDR_API int sdr_debug_time_step(sdr_ctx* ctx, const sdr_csr* A, const sdr_sketch* S, const double* r0, int64_t t,
                                 int64_t m, int64_t steps, int32_t reps, double* k1_us, double* k2_us);
+/* Debugging / measurement: kernel phase trace (SDR_TRACE=1), per-launch CUDA-event
+ * timeline and device-clock launch stamps (first CTA start, last CTA end,
+ * %globaltimer), written as CSV; stamps are recorded with SDR_TRACE=2 or after
+ * sdr_ctx_set_stamps(ctx, 1), and reading them resets the buffer. */
+SDR_API int sdr_debug_trace(sdr_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n);
+SDR_API int sdr_debug_timeline(sdr_ctx* ctx, const char* path);
+SDR_API int sdr_debug_stamps(sdr_ctx* ctx, const char* path);
+SDR_API int sdr_ctx_set_stamps(sdr_ctx* ctx, int on);
 
 /* solve (solver.hpp:269-365). b, x0 (may be NULL), x_out: this rank's block,
  * host or device. space (may be NULL) is updated in place. sketch may be NULL

@@ -1366,6 +1366,13 @@ SDR_API int sdr_debug_timeline(sdr_ctx* ctx, const char* path) {
 }
 
 /* internal: device-clock launch timeline (SDR_TRACE=2) as CSV name,start_ns,end_ns */
+SDR_API int sdr_ctx_set_stamps(sdr_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->stamps_on = on != 0;
+  });
+}
+
 SDR_API int sdr_debug_stamps(sdr_ctx* ctx, const char* path) {
   return guard([&] {
     const auto v = ctx->c->launch_stamps_read();

@@ -247,7 +247,7 @@ unsigned long long* Context::trace(i64 n) {
 
 unsigned long long* Context::launch_stamp(const char* name) {
   constexpr i64 kCap = 1 << 16;
-  if (trace_mode() != 2) return nullptr;
+  if (trace_mode() != 2 && !stamps_on) return nullptr;
   if (stamps_.size() == 0) {
     stamps_.resize(2 * kCap);
     SDR_CUDA(cudaMemsetAsync(stamps_.get(), 0xFF, sizeof(unsigned long long) * kCap, stream));

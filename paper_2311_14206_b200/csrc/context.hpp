@@ -61,6 +61,7 @@ class Context {
   /// Device-clock launch timeline (SDR_TRACE=2, debugging only): a (first CTA
   /// start, last CTA end) %globaltimer pair for this launch, or null.
   unsigned long long* launch_stamp(const char* name);
+  bool stamps_on = false;  // launch stamps without SDR_TRACE=2 (sdr_ctx_set_stamps, bench measurements)
   std::vector<std::pair<std::string, std::pair<unsigned long long, unsigned long long>>> launch_stamps_read();
   std::vector<unsigned long long> trace_read();
   static constexpr int kNumCounters = 64;
