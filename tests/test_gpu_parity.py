@@ -376,3 +376,23 @@ def test_complex_system_solves_through_zsell(sk, O):
     assert r.report.status == ro.status == "converged"
     assert abs(r.report.iterations - ro.iterations) <= max(1, 0.02 * ro.iterations)
     assert np.linalg.norm(b - M @ r.x) <= 1e-10 * np.linalg.norm(b) * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("rows,cols,density", [(1, 1, 1.0), (5, 5, 0.3), (31, 31, 0.2), (33, 7, 0.5), (7, 33, 0.5),
+                                               (64, 64, 0.0), (97, 97, 0.05)])
+def test_spmv_small_and_degenerate_shapes(sk, O, rows, cols, density):
+    """Partial slices (rows not a multiple of 32), a single row, rectangular
+    blocks and an operator with no stored entry at all."""
+    rng = np.random.default_rng(rows * 131 + cols)
+    mask = rng.random((rows, cols)) < density
+    D = np.where(mask, rng.standard_normal((rows, cols)), 0.0)
+    S = sp.csr_matrix(D)
+    A = sk.SparseMatrix(rows, cols, S.indptr.astype(np.int64), S.indices.astype(np.int64), S.data)
+    x = O.gaussian_vector(cols, 3)
+    y = A.apply(x)
+    ref = D @ x
+    assert y.shape == (rows,)
+    if np.linalg.norm(ref) == 0:
+        assert not np.any(y)
+    else:
+        assert rel(y, ref) <= REL
