@@ -307,3 +307,31 @@ print(json.dumps(dict(it=r.report.iterations, st=r.report.status, res=[v for _, 
     assert a["st"] == f["st"] and a["it"] == f["it"]
     np.testing.assert_allclose(f["res"], a["res"], rtol=1e-8)
     np.testing.assert_allclose(f["x"], a["x"], rtol=1e-8, atol=1e-10 * np.linalg.norm(a["x"]))
+
+
+@pytest.mark.parametrize("t", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("k", [0, 6])
+@pytest.mark.parametrize("sketch", ["srdct", "sparse"])
+def test_config_sweep_matches_oracle(sk, O, t, k, sketch):
+    """Window t (fused update+SRDCT up to t = 4, the unfused path beyond),
+    deflation on / off, both sketches, on a 32^3 convection-diffusion system
+    (deferred step pipeline eligible): same status, iterations within 2 %,
+    identical books when the iteration counts agree."""
+    n = 32
+    off, col, val = sk.gen_convdiff3d(n, 60.0, 30.0, 15.0)
+    N = n ** 3
+    A = sk.SparseMatrix(N, N, off, col, val)
+    Ao = O.SparseMatrix.from_csr(N, N, off, col, val)
+    b = O.gaussian_vector(N, 7)
+    kw = dict(m=30, t=t, k=k, s=80, tol=1e-8, max_restarts=30)
+    if sketch == "srdct":
+        S, So = sk.SketchOperator.subsampled_dct(N, 80, 0x5EED), O.SketchOperator.subsampled_dct(N, 80, 0x5EED)
+    else:
+        S, So = sk.SketchOperator.sparse_sign(N, 80, 0x5EED, 8), O.SketchOperator.sparse_sign(N, 80, 0x5EED, 8)
+    g = sk.solve(A, b, sk.SolverConfig(**kw), sketch=S)
+    o = O.solve(Ao, b, O.SolverConfig(**kw), sketch=So)
+    assert_same_solve(g, o, iters_tol=0.02)
+    if g.report.iterations == o[1].iterations:
+        assert g.report.counters == o[1].counters
+    if o[1].status == "converged":
+        assert np.linalg.norm(b - Ao.apply(g.x)) <= 1e-8 * np.linalg.norm(b) * (1 + 1e-9)
