@@ -266,6 +266,13 @@ SDR_API int sdr_debug_block_product(sdr_ctx* ctx, int32_t kernel, int64_t n, con
                                     int32_t k1, const double* A2, int64_t lda2, int32_t k2, const double* B,
                                     int32_t nout, double* C, int64_t ldc, double* norms2);
 
+/* Test hook for the NVLink peer-memory one-shot allreduce (SDR_PEER=1 on
+ * several ranks): `world` virtual ranks as CTAs of one cooperative launch on
+ * this GPU run `epochs` allreduces of n values back to back through the same
+ * device code. vals / out: host [epochs][world][n]; out[e][r] must equal the
+ * rank-ordered sum over vals[e][*] for every r. */
+SDR_API int sdr_debug_peer_emulate(int32_t world, int32_t n, int32_t epochs, const double* vals, double* out);
+
 /* Measurement: init + `steps` pipelined Arnoldi steps from r0, then the mean
  * CUDA-event duration (microseconds) of `reps` back-to-back relaunches of the
  * last step's K1 (SpMV + window dots) and K2 (fused update + SRDCT) on the

@@ -125,6 +125,7 @@ SIGNATURES = {
     "sdr_recycle_save_file": (cint, [vp, vp, C.c_char_p]),
     "sdr_recycle_load_file": (cint, [vp, vp, C.c_char_p]),
     "sdr_debug_block_product": (cint, [vp, i32, i64, vp, i64, i32, vp, i64, i32, vp, i32, vp, i64, vp]),
+    "sdr_debug_peer_emulate": (cint, [i32, i32, i32, vp, vp]),
     "sdr_ctx_set_stamps": (cint, [vp, cint]),
     "sdr_debug_time_step": (cint, [vp, vp, vp, vp, i64, i64, i64, i32, P(f64), P(f64)]),
     "sdr_spmm": (cint, [vp, vp, i64, vp, i64, vp, i64]),

@@ -6,6 +6,7 @@
 #include "context.hpp"
 #include "host_linalg.hpp"
 #include "io.hpp"
+#include "peer.hpp"
 #include "operator.hpp"
 #include "sketch.hpp"
 #include "solver.hpp"
@@ -889,6 +890,14 @@ int sdr_debug_block_product(sdr_ctx* ctx, int32_t kernel, int64_t n, const doubl
                    scratch.get());
     co.finish(c);
     SDR_CUDA(cudaMemcpy(norms2, nr.get(), sizeof(double) * static_cast<size_t>(nout), cudaMemcpyDeviceToHost));
+  });
+}
+
+int sdr_debug_peer_emulate(int32_t world, int32_t n, int32_t epochs, const double* vals, double* out) {
+  return guard([&] {
+    need(vals, "vals");
+    need(out, "out");
+    peer_emulate(world, n, epochs, vals, out);
   });
 }
 

@@ -2,6 +2,7 @@
 // shares whatever libnccl.so.2 the host process — e.g. torch — already
 // loaded instead of linking a second copy), and event timing.
 #include "context.hpp"
+#include "peer.hpp"
 
 #include <cublas_v2.h>
 
@@ -96,6 +97,9 @@ Context::~Context() {
   if (stream) cudaStreamSynchronize(stream);
   if (blas_) cublasDestroy(static_cast<cublasHandle_t>(blas_));
   if (comm_ && nccl_) nccl_->CommDestroy(static_cast<ncclComm_t>(comm_));
+  for (void* m : peer_mapped_)
+    if (m) cudaIpcCloseMemHandle(m);
+  if (peer_own_) cudaFree(peer_own_);
   for (auto& p : pending_) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -105,8 +109,51 @@ Context::~Context() {
   if (stream) cudaStreamDestroy(stream);
 }
 
+bool Context::peer_setup() {
+  if (peer_tried_) return peer_ok_;
+  peer_tried_ = true;
+  const char* e = std::getenv("SDR_PEER");
+  if (!e || std::atoi(e) == 0 || world < 2) return false;
+  const size_t slot_bytes = sizeof(double) * 2 * static_cast<size_t>(world) * kPeerMaxN;
+  const size_t bytes = slot_bytes + sizeof(uint64_t) * static_cast<size_t>(world);
+  SDR_CUDA(cudaMalloc(&peer_own_, bytes));
+  SDR_CUDA(cudaMemset(peer_own_, 0, bytes));
+  cudaIpcMemHandle_t h{};
+  SDR_CUDA(cudaIpcGetMemHandle(&h, peer_own_));
+  static_assert(sizeof(cudaIpcMemHandle_t) % sizeof(i64) == 0, "IPC handle size");
+  constexpr i64 kWords = sizeof(cudaIpcMemHandle_t) / sizeof(i64);
+  std::vector<i64> mine(kWords), all(static_cast<size_t>(kWords * world));
+  std::memcpy(mine.data(), &h, sizeof(h));
+  allgather_i64(mine.data(), kWords, all.data());
+  peer_mapped_.assign(static_cast<size_t>(world), nullptr);
+  std::vector<double*> sl(static_cast<size_t>(world));
+  std::vector<uint64_t*> fl(static_cast<size_t>(world));
+  for (int q = 0; q < world; ++q) {
+    void* base = peer_own_;
+    if (q != rank) {
+      cudaIpcMemHandle_t hq{};
+      std::memcpy(&hq, all.data() + q * kWords, sizeof(hq));
+      SDR_CUDA(cudaIpcOpenMemHandle(&base, hq, cudaIpcMemLazyEnablePeerAccess));
+      peer_mapped_[static_cast<size_t>(q)] = base;
+    }
+    sl[static_cast<size_t>(q)] = static_cast<double*>(base);
+    fl[static_cast<size_t>(q)] = reinterpret_cast<uint64_t*>(static_cast<char*>(base) + slot_bytes);
+  }
+  peer_slots_.resize(world);
+  peer_flags_.resize(world);
+  SDR_CUDA(cudaMemcpy(peer_slots_.get(), sl.data(), sizeof(double*) * sl.size(), cudaMemcpyHostToDevice));
+  SDR_CUDA(cudaMemcpy(peer_flags_.get(), fl.data(), sizeof(uint64_t*) * fl.size(), cudaMemcpyHostToDevice));
+  peer_ok_ = true;
+  return true;
+}
+
 void Context::allreduce_sum(double* dev, i64 n) {
   if (!comm_ || n <= 0) return;
+  if (n <= kPeerMaxN && peer_setup()) {
+    launch_peer_allreduce(*this, PeerView{peer_slots_.get(), peer_flags_.get(), world, rank}, dev, static_cast<int>(n),
+                          ++peer_epoch_);
+    return;
+  }
   ++launches;
   if (timing) time_begin("allreduce");
   SDR_NCCL(nccl_->AllReduce(dev, dev, static_cast<size_t>(n), ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream));

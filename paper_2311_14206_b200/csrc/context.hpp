@@ -67,6 +67,8 @@ class Context {
   static constexpr int kNumCounters = 64;
 
   // ---- collectives (no-ops on one rank)
+  /// Sum over ranks in place: NCCL, or with SDR_PEER=1 (several ranks, n <=
+  /// kPeerMaxN) the one-shot NVLink peer-memory kernel (peer.cu).
   void allreduce_sum(double* dev, i64 n);
   void allgather_i64(const i64* host_in, i64 count, i64* host_out);  // host in/out, small
   /// on: the stream the transfers are issued on (default: the context stream).
@@ -116,6 +118,14 @@ class Context {
   NcclApi* nccl_ = nullptr;
   void* blas_ = nullptr;  // cublasHandle_t, created on first use
   void* comm_ = nullptr;
+  // peer-memory allreduce (SDR_PEER=1): own symmetric buffer, mapped peers, epoch
+  bool peer_tried_ = false, peer_ok_ = false;
+  void* peer_own_ = nullptr;                 // cudaMalloc'ed: slots then flags
+  std::vector<void*> peer_mapped_;           // IPC-opened peer buffers (null for self)
+  DeviceBuffer<double*> peer_slots_;
+  DeviceBuffer<uint64_t*> peer_flags_;
+  uint64_t peer_epoch_ = 0;
+  bool peer_setup();
   struct Pending {
     std::string name;
     cudaEvent_t a, b;
