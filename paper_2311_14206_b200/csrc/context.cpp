@@ -151,7 +151,7 @@ void Context::allreduce_sum(double* dev, i64 n) {
   if (!comm_ || n <= 0) return;
   if (n <= kPeerMaxN && peer_setup()) {
     launch_peer_allreduce(*this, PeerView{peer_slots_.get(), peer_flags_.get(), world, rank}, dev, static_cast<int>(n),
-                          ++peer_epoch_);
+                          next_peer_epoch());
     return;
   }
   ++launches;

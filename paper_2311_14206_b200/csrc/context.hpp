@@ -125,7 +125,16 @@ class Context {
   DeviceBuffer<double*> peer_slots_;
   DeviceBuffer<uint64_t*> peer_flags_;
   uint64_t peer_epoch_ = 0;
+
+ public:
+  /// SDR_PEER=1 on several ranks: the mapped peer buffers are set up (first
+  /// call) and allreduces of <= kPeerMaxN values go through peer memory.
   bool peer_setup();
+  const double* const* peer_slots() const { return peer_slots_.get(); }
+  uint64_t* const* peer_flags() const { return peer_flags_.get(); }
+  uint64_t next_peer_epoch() { return ++peer_epoch_; }
+
+ private:
   struct Pending {
     std::string name;
     cudaEvent_t a, b;

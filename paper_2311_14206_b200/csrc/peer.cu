@@ -16,6 +16,7 @@
 // measured on several GPUs). The same device function runs in
 // sdr_debug_peer_emulate: all ranks as CTAs of one cooperative launch on one
 // GPU (co-resident, so the spins are safe), which is how it is tested here.
+#include "kernels.hpp"
 #include "peer.hpp"
 
 #include <cooperative_groups.h>
@@ -61,6 +62,25 @@ __global__ void __launch_bounds__(256) k_peer_allreduce(PeerView a, double* vals
   peer_allreduce_cta(a, vals, n, epoch, vals);
 }
 
+/// Fold (fixed order: p1's CTAs then p2's) into buf[off ..], then the peer
+/// allreduce of buf[0 .. off + nv) — one launch per step on several ranks.
+__global__ void __launch_bounds__(256) k_fold_peer_allreduce(PeerView a, const double* __restrict__ p1, int G1,
+                                                             const double* __restrict__ p2, int G2, int nv,
+                                                             double* buf, int off, uint64_t epoch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int v = warp; v < nv; v += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int b = lane; b < G1; b += 32) s += p1[static_cast<int64_t>(v) * G1 + b];
+    if (p2)
+      for (int b = lane; b < G2; b += 32) s += p2[static_cast<int64_t>(v) * G2 + b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) buf[off + v] = s;
+  }
+  __syncthreads();
+  peer_allreduce_cta(a, buf, off + nv, epoch, buf);
+}
+
 /// Emulation: CTA r acts as rank r with its own view; vals[r * n ..] in/out.
 __global__ void __launch_bounds__(256) k_peer_emulate(const PeerView* views, double* vals, int n, uint64_t epoch) {
   const PeerView a = views[blockIdx.x];
@@ -75,6 +95,21 @@ void launch_peer_allreduce(Context& c, const PeerView& v, double* dev, int n, ui
   TimedLaunch t(c, "peer_allreduce");
   k_peer_allreduce<<<1, 256, 0, c.stream>>>(v, dev, n, epoch);
   SDR_KERNEL_CHECK();
+}
+
+void fold_allreduce(Context& c, const double* p1, int G1, const double* p2, int G2, int nv, double* buf, int off) {
+  if (off + nv <= kPeerMaxN && c.peer_setup()) {
+    const PeerView v{const_cast<double* const*>(c.peer_slots()), c.peer_flags(), c.world, c.rank};
+    TimedLaunch t(c, "fold_peer_allreduce");
+    k_fold_peer_allreduce<<<1, 256, 0, c.stream>>>(v, p1, G1, p2, G2, nv, buf, off, c.next_peer_epoch());
+    SDR_KERNEL_CHECK();
+    return;
+  }
+  if (p2)
+    launch_fold_partials2(c, p1, G1, p2, G2, nv, buf + off);
+  else
+    launch_fold_partials(c, p1, G1, nv, true, buf + off);
+  c.allreduce_sum(buf, off + nv);
 }
 
 void peer_emulate(int world, int n, int epochs, const double* vals_host, double* out_host) {

@@ -17,6 +17,7 @@
 // under device work (the recycle product U_new = [V U] P reads the finished
 // buffer, which the new cycle does not touch).
 #include "solver.hpp"
+#include "peer.hpp"
 
 #include <atomic>
 #include <exception>
@@ -549,11 +550,7 @@ struct ArnoldiPipeline {
       if (dist) {  // K1(j)'s folded dots ride on the allreduce of K2(j-1)'s folded partials
         double* cb = pend_n > 0 ? pend_buf : w.p1f.get();
         const int off = pend_n;
-        if (split_k1)
-          launch_fold_partials2(c, w.p1.get(), sf.k1_G, w.p1b.get(), gb, 1 + nwin, cb + off);
-        else
-          launch_fold_partials(c, w.p1.get(), sf.k1_G, 1 + nwin, true, cb + off);
-        c.allreduce_sum(cb, off + 1 + nwin);
+        fold_allreduce(c, w.p1.get(), sf.k1_G, split_k1 ? w.p1b.get() : nullptr, gb, 1 + nwin, cb, off);
         sf.k1_partials = cb + off;
         sf.k1_G = 1;
         pend_n = 0;
