@@ -927,21 +927,20 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
   // host: SU_new, SAU_new (recycle.hpp:257-265) while the product runs
   HMat SU(s, ke), SAU(s, ke);
   host_job_while_pumping(
-      [&] {
-        for (i64 q = 0; q < ke; ++q) {
-          for (i64 i = 0; i < j; ++i) {
-            const double cf = hp.coeffs(kh + i, q);
-            for (i64 r = 0; r < s; ++r) {
-              SU(r, q) += st.SV(r, i) * cf;
-              SAU(r, q) += st.SAV(r, i) * cf;
-            }
-          }
-          for (i64 p = 0; p < kh; ++p) {
-            const double cf = hp.coeffs(p, q);
-            for (i64 r = 0; r < s; ++r) {
-              SU(r, q) += sp.SU(r, p) * cf;
-              SAU(r, q) += sp.SAU(r, p) * cf;
-            }
+      [&] {  // [SU SV] C and [SAU SAV] C as BLAS-3 products (V block, then U block added)
+        const int ms = static_cast<int>(s), nk = static_cast<int>(ke), kj = static_cast<int>(j),
+                  kk = static_cast<int>(kh), ldc = static_cast<int>(hp.coeffs.rows);
+        const double one = 1.0, zero = 0.0;
+        if (ms > 0 && nk > 0) {
+          scipy_dgemm_("N", "N", &ms, &nk, &kj, &one, st.SV.a.data(), &ms, hp.coeffs.a.data() + kh, &ldc, &zero,
+                       SU.a.data(), &ms, 1, 1);
+          scipy_dgemm_("N", "N", &ms, &nk, &kj, &one, st.SAV.a.data(), &ms, hp.coeffs.a.data() + kh, &ldc, &zero,
+                       SAU.a.data(), &ms, 1, 1);
+          if (kk > 0) {
+            scipy_dgemm_("N", "N", &ms, &nk, &kk, &one, sp.SU.a.data(), &ms, hp.coeffs.a.data(), &ldc, &one,
+                         SU.a.data(), &ms, 1, 1);
+            scipy_dgemm_("N", "N", &ms, &nk, &kk, &one, sp.SAU.a.data(), &ms, hp.coeffs.a.data(), &ldc, &one,
+                         SAU.a.data(), &ms, 1, 1);
           }
         }
       },
