@@ -91,6 +91,12 @@ SDR_API int sdr_ctx_launch_count(const sdr_ctx* ctx, int64_t* launches);
  * [row_begin, row_begin + local_rows) with GLOBAL column indices. */
 SDR_API int sdr_csr_create(sdr_ctx* ctx, int64_t rows, int64_t cols, const int64_t* offsets,
                            const int64_t* columns, const double* values, sdr_csr** out);
+/* Complex fp64 CSR (values: nnz (re, im) pairs; BASELINE C4 operators): the
+ * operator acts on interleaved vectors [re_0, im_0, re_1, im_1, ...] of length
+ * 2·rows and is stored as ZSELL (see sdr_csr_storage). Single-rank contexts;
+ * validated like sdr_csr_create in complex row / column terms. */
+SDR_API int sdr_csr_create_complex(sdr_ctx* ctx, int64_t rows, int64_t cols, const int64_t* offsets,
+                                   const int64_t* columns, const double* values, sdr_csr** out);
 SDR_API int sdr_csr_create_local(sdr_ctx* ctx, int64_t global_rows, int64_t global_cols, int64_t row_begin,
                                  int64_t local_rows, const int64_t* offsets, const int64_t* columns,
                                  const double* values, sdr_csr** out);

@@ -204,6 +204,26 @@ class SparseMatrix:
                             bytes=nb.value)
 
     @classmethod
+    def from_complex(cls, rows, cols, offsets, columns, values, ctx=None):
+        """Complex fp64 CSR (values complex128): the operator on interleaved
+        (re, im) vectors of length 2·rows, stored as ZSELL (BASELINE C4)."""
+        ctx = ctx or default_context()
+        o = np.ascontiguousarray(offsets, dtype=np.int64)
+        c_ = np.ascontiguousarray(columns, dtype=np.int64)
+        v = np.ascontiguousarray(values, dtype=np.complex128).view(np.float64)
+        h = C.c_void_p()
+        _check(_lib.sdr_csr_create_complex(ctx._h, rows, cols, o.ctypes.data_as(C.c_void_p),
+                                           c_.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p), C.byref(h)))
+        A = cls(0, 0, None, None, None, ctx=ctx, _handle=h)
+        A.complex_rows = rows
+        return A
+
+    def apply_complex(self, z):
+        """y = A z for a complex operator (from_complex) on a complex128 vector."""
+        x = np.ascontiguousarray(z, dtype=np.complex128).view(np.float64)
+        return self.apply(x).view(np.complex128)
+
+    @classmethod
     def from_matrix_market(cls, path, ctx=None):
         """read_matrix_market_file (matrix_market.hpp:161-165) straight to the device."""
         ctx = ctx or default_context()

@@ -128,6 +128,7 @@ SIGNATURES = {
     "sdr_debug_peer_emulate": (cint, [i32, i32, i32, vp, vp]),
     "sdr_ctx_set_stamps": (cint, [vp, cint]),
     "sdr_debug_time_step": (cint, [vp, vp, vp, vp, i64, i64, i64, i32, P(f64), P(f64)]),
+    "sdr_csr_create_complex": (cint, [vp, i64, i64, vp, vp, vp, P(vp)]),
     "sdr_spmm": (cint, [vp, vp, i64, vp, i64, vp, i64]),
     "sdr_baseline_config_default": (cint, [P(sdr_baseline_config)]),
     "sdr_baseline_gmres": (cint, [vp, vp, vp, vp, P(sdr_baseline_config), vp, P(vp)]),

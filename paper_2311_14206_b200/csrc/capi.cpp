@@ -247,6 +247,55 @@ int sdr_csr_create(sdr_ctx* ctx, int64_t rows, int64_t cols, const int64_t* offs
   });
 }
 
+int sdr_csr_create_complex(sdr_ctx* ctx, int64_t rows, int64_t cols, const int64_t* offsets, const int64_t* columns,
+                           const double* values, sdr_csr** out) {
+  return guard([&] {  // complex CSR (values as (re, im) pairs) -> the real-equivalent operator, stored as ZSELL
+    need(ctx, "ctx");
+    need(out, "out");
+    if (ctx->c->distributed()) throw invalid("sdr_csr_create_complex: single-rank contexts only");
+    if (rows < 0 || cols < 0) throw invalid("SparseMatrix: negative dimensions");
+    need(offsets, "offsets");
+    if (offsets[0] != 0) throw invalid("SparseMatrix: offsets must start at 0");
+    const int64_t nnz = offsets[rows];
+    if (nnz > 0 && (!columns || !values)) throw invalid("SparseMatrix: offsets/columns/values sizes inconsistent");
+    std::vector<int64_t> ro(static_cast<size_t>(2 * rows) + 1, 0), rc;
+    std::vector<double> rv;
+    rc.reserve(static_cast<size_t>(4 * nnz));
+    rv.reserve(static_cast<size_t>(4 * nnz));
+    for (int64_t r = 0; r < rows; ++r) {
+      if (offsets[r + 1] < offsets[r]) throw invalid("SparseMatrix: offsets decrease at row " + std::to_string(r));
+      for (int64_t p = offsets[r]; p < offsets[r + 1]; ++p) {
+        if (columns[p] < 0 || columns[p] >= cols)
+          throw invalid("SparseMatrix: column index " + std::to_string(columns[p]) + " out of range in row " +
+                        std::to_string(r));
+        if (p > offsets[r] && columns[p - 1] >= columns[p])
+          throw invalid("SparseMatrix: column indices not strictly increasing in row " + std::to_string(r));
+        if (!std::isfinite(values[2 * p]) || !std::isfinite(values[2 * p + 1]))
+          throw invalid("SparseMatrix: non-finite value in row " + std::to_string(r));
+      }
+      for (int half = 0; half < 2; ++half) {  // real row 2r (re), 2r + 1 (im): [[a, -b], [b, a]]
+        for (int64_t p = offsets[r]; p < offsets[r + 1]; ++p) {
+          const double a = values[2 * p], b = values[2 * p + 1];
+          const double v0 = half == 0 ? a : b, v1 = half == 0 ? -b : a;
+          if (v0 != 0.0) {
+            rc.push_back(2 * columns[p]);
+            rv.push_back(v0);
+          }
+          if (v1 != 0.0) {
+            rc.push_back(2 * columns[p] + 1);
+            rv.push_back(v1);
+          }
+        }
+        ro[static_cast<size_t>(2 * r + half) + 1] = static_cast<int64_t>(rc.size());
+      }
+    }
+    auto h = std::make_unique<sdr_csr>();
+    h->ctx = ctx->c.get();
+    h->op.reset(create_operator_csr(*ctx->c, 2 * rows, 2 * cols, 0, 2 * rows, ro.data(), rc.data(), rv.data()));
+    *out = h.release();
+  });
+}
+
 int sdr_csr_create_local(sdr_ctx* ctx, int64_t grows, int64_t gcols, int64_t row_begin, int64_t local_rows,
                          const int64_t* offsets, const int64_t* columns, const double* values, sdr_csr** out) {
   return guard([&] {

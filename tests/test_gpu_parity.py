@@ -396,3 +396,21 @@ def test_spmv_small_and_degenerate_shapes(sk, O, rows, cols, density):
         assert not np.any(y)
     else:
         assert rel(y, ref) <= REL
+
+
+def test_complex_csr_api(sk, O):
+    """sdr_csr_create_complex: complex CSR in, ZSELL operator on interleaved vectors."""
+    rng = np.random.default_rng(12)
+    nc = 1500
+    Z = sp.random(nc, nc, density=0.004, random_state=3, format="csr", dtype=np.float64)
+    Z = (Z + 1j * sp.random(nc, nc, density=0.004, random_state=4, format="csr")).tocsr()
+    Z = (Z + sp.identity(nc) * (5.0 + 0.5j)).tocsr()
+    Z.sort_indices()
+    A = sk.SparseMatrix.from_complex(nc, nc, Z.indptr, Z.indices, Z.data)
+    assert A.storage["format"] == "zsell" and A.rows == 2 * nc
+    z = rng.standard_normal(nc) + 1j * rng.standard_normal(nc)
+    y = A.apply_complex(z)
+    ref = Z @ z
+    assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+    with pytest.raises(ValueError, match="not strictly increasing"):
+        sk.SparseMatrix.from_complex(2, 2, [0, 2, 2], [1, 1], np.array([1 + 1j, 2.0]))
