@@ -1,3 +1,5 @@
+"""Host LAPACK probe on the GPU box: 120 x 120 SVD / Schur / Hessenberg times at
+1..8 OpenBLAS threads (the restart pencil's host cost). Usage: python tools/lapack_probe.py"""
 import sys, os; sys.path.insert(0, os.getcwd())
 import time, numpy as np, scipy.linalg as sl
 print('cpus', os.cpu_count(), open('/proc/cpuinfo').read().split('model name')[1].split('\n')[0])
