@@ -335,3 +335,41 @@ def test_config_sweep_matches_oracle(sk, O, t, k, sketch):
         assert g.report.counters == o[1].counters
     if o[1].status == "converged":
         assert np.linalg.norm(b - Ao.apply(g.x)) <= 1e-8 * np.linalg.norm(b) * (1 + 1e-9)
+
+
+def test_nonzero_x0_matches_oracle(sk, O):
+    """solver.hpp:307-316: r0 = b - A x0 with one extra product booked."""
+    n = 32
+    off, col, val = sk.gen_convdiff3d(n, 60.0, 30.0, 15.0)
+    N = n ** 3
+    A = sk.SparseMatrix(N, N, off, col, val)
+    Ao = O.SparseMatrix.from_csr(N, N, off, col, val)
+    b = O.gaussian_vector(N, 3)
+    x0 = 0.01 * O.gaussian_vector(N, 4)
+    kw = dict(m=25, t=2, k=5, s=60, tol=1e-9, max_restarts=30)
+    g = sk.solve(A, b, sk.SolverConfig(**kw), x0=x0)
+    o = O.solve(Ao, b, O.SolverConfig(**kw), x0=x0)
+    assert_same_solve(g, o, iters_tol=0.02)
+    if g.report.iterations == o[1].iterations:
+        assert g.report.counters == o[1].counters
+    assert np.linalg.norm(b - Ao.apply(g.x)) <= 1e-9 * np.linalg.norm(b) * (1 + 1e-9)
+
+
+def test_breakdown_status_and_note(sk, O):
+    """A lucky breakdown that does not solve the system (b has a component in
+    the null space of a singular A) ends the solve as `breakdown` with the
+    reference's note (solver.hpp:344-350)."""
+    n = 60
+    d = np.linspace(1.0, 3.0, n)
+    d[-1] = 0.0  # singular
+    M = np.diag(d)
+    A, Ao = sk.SparseMatrix.from_dense(M), O.SparseMatrix.from_dense(M)
+    b = np.zeros(n)
+    b[:3] = 1.0
+    b[-1] = 1.0  # null-space component: the residual cannot drop below 1
+    kw = dict(m=10, t=10, k=0, s=40, tol=1e-8, max_restarts=5)
+    g = sk.solve(A, b, sk.SolverConfig(**kw))
+    o = O.solve(Ao, b, O.SolverConfig(**kw))
+    assert g.report.status == o[1].status == "breakdown"
+    assert g.report.iterations == o[1].iterations
+    assert g.report.notes == o[1].notes
