@@ -39,3 +39,11 @@ clean:
 	rm -rf build $(LIB) oracle/_build
 
 .PHONY: all oracle clean
+
+# a plain C++ caller of the C-ABI (no Python): make examples && ./examples/solve_c2
+examples: examples/solve_c2
+
+examples/solve_c2: examples/solve_c2.cpp include/sdr_b200.h $(LIB)
+	$(CXX) -O2 -std=c++17 -Iinclude -o $@ $< -L$(dir $(LIB)) -lsdr_b200 -Wl,-rpath,'$$ORIGIN/../paper_2311_14206_b200/_lib'
+
+.PHONY: examples
