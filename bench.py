@@ -348,6 +348,7 @@ def main():
                            "step j = 20)" if iso else "CUDA events around each launch of one instrumented solve"),
                 "in_solve_event_us": kern[dom]["avg_us"],
                 "isolated_us": iso,
+                "isolated_frac": ({k: kb[k] / (v * 1e-6) / 1e9 / peak for k, v in iso.items()} if iso else None),
                 "arnoldi_step": {"bytes": step_bytes, "us": step_us, "GBps": step_bytes / (step_us * 1e-6) / 1e9,
                                  "frac": step_bytes / (step_us * 1e-6) / 1e9 / peak,
                                  "timer": "sum of per-launch CUDA events in one instrumented solve"}}
