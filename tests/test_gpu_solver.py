@@ -373,3 +373,26 @@ def test_breakdown_status_and_note(sk, O):
     assert g.report.status == o[1].status == "breakdown"
     assert g.report.iterations == o[1].iterations
     assert g.report.notes == o[1].notes
+
+
+def test_workspace_reuse_across_operators(sk, O):
+    """One context, operators of different sizes / storage forms / windows in
+    turn (the cached workspace is re-laid out): every solve equals the first
+    solve of the same problem."""
+    probs = []
+    for n, t, k in ((24, 2, 6), (16, 3, 4), (24, 2, 6), (20, 1, 0), (16, 3, 4)):
+        off, col, val = sk.gen_convdiff3d(n, 60.0, 30.0, 15.0)
+        N = n ** 3
+        probs.append((sk.SparseMatrix(N, N, off, col, val), O.gaussian_vector(N, n), dict(m=20, t=t, k=k, s=60, tol=1e-9,
+                                                                                            max_restarts=40)))
+    first = {}
+    for i, (A, b, kw) in enumerate(probs):
+        r = sk.solve(A, b, sk.SolverConfig(**kw))
+        key = (A.rows, kw["t"], kw["k"])
+        if key in first:
+            r0 = first[key]
+            assert r.report.iterations == r0.report.iterations
+            assert np.array_equal(r.x, r0.x)
+        else:
+            first[key] = r
+        assert r.report.status == "converged"
