@@ -14,6 +14,10 @@
 // device scales c_i = 1/||w_i||, so normalisation costs no extra pass.
 // Algorithmic bytes per row: y + window vectors read, w_{j+1} written.
 #include "kernels.hpp"
+
+#include <map>
+#include <mutex>
+#include <tuple>
 #include "mgs.cuh"
 #include "reduce.cuh"
 
@@ -491,11 +495,7 @@ void rgemm_impl(Context& c, const double* A1, int64_t lda1, int k1, const double
                 const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2, double* scratch) {
   auto kern = k_rgemm<NO>;
   const size_t smem = sizeof(double) * (static_cast<size_t>(2 * kRgKC * kRgLda) + static_cast<size_t>(k1 + k2 + 4) * NO);
-  static size_t configured = 0;
-  if (smem > configured) {
-    SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    configured = smem;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   const int64_t ntiles = (n + kRgRows - 1) / kRgRows;
   const int per_sm = std::max(1, blocks_per_sm(reinterpret_cast<const void*>(kern), kThreads, smem));
   const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, static_cast<int64_t>(c.num_sms) * per_sm)));
@@ -548,8 +548,13 @@ void tallskinny_impl(Context& c, const double* const* in, int nin, const double*
 }  // namespace
 
 int blocks_per_sm(const void* kernel, int threads, size_t smem) {
-  static std::map<std::pair<const void*, size_t>, int> cache;
-  auto key = std::make_pair(kernel, smem * 4096 + static_cast<size_t>(threads));
+  // shared by every context / thread of the process: guarded, keyed by device
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, kernel, smem * 4096 + static_cast<size_t>(threads));
+  std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int n = 0;
@@ -559,6 +564,20 @@ int blocks_per_sm(const void* kernel, int threads, size_t smem) {
   }
   cache[key] = n;
   return n;
+}
+
+void ensure_dyn_smem(const void* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  SDR_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = done[std::make_pair(dev, kernel)];
+  if (bytes > have) {
+    SDR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    have = bytes;
+  }
 }
 
 void launch_update(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,

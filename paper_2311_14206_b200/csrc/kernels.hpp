@@ -55,8 +55,12 @@ struct SketchDev;  // sketch.cu
 /// SDR_PDL=0 disables programmatic dependent launch in the step pipeline.
 bool pdl_enabled();
 
-/// Occupancy-derived resident CTAs per SM for a kernel (cached per kernel).
+/// Occupancy-derived resident CTAs per SM for a kernel (cached per device and
+/// kernel; thread-safe).
 int blocks_per_sm(const void* kernel, int threads, size_t smem);
+/// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
+/// current device (once per device and kernel; thread-safe).
+void ensure_dyn_smem(const void* kernel, size_t bytes);
 
 // ---- SpMV family (spmv.cu)
 void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y);

@@ -1108,11 +1108,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   ta.stamp = c.launch_stamp(name);
   const size_t smem = tiles_smem(S.s, GRP, PR);
   auto kern = k_srdct_tiles<SRC, NI, PAIRED, MAXT, GRP, CHK, PR>;
-  static size_t configured = 0;
-  if (smem > configured) {
-    SDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    configured = smem;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   {
     TimedLaunch t(c, name);
     cudaLaunchConfig_t cfg{};
@@ -1363,11 +1359,7 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
     }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * c.num_sms)));
     const size_t smem = sizeof(double2) * static_cast<size_t>((kTileA / 2) * p.F + p.F / 2 + S.s);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      SDR_CUDA(cudaFuncSetAttribute(k_srdct, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      configured = smem;
-    }
+    ensure_dyn_smem(reinterpret_cast<const void*>(k_srdct), smem);
     TimedLaunch t(c, "sketch");
     k_srdct<<<grid, kThreads, smem, c.stream>>>(x_own, xscale, S.n, row_begin, p.M, p.L, static_cast<int>(p.F), p.logF,
                                                 S.sign_bits.get(), S.rows.get(), S.row_scale.get(),
@@ -1410,11 +1402,7 @@ void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, d
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4 * c.num_sms)));
   const int64_t chunk = round_up((nloc + grid - 1) / grid, 32);
   const size_t smem = sizeof(double) * 32 * static_cast<size_t>(S.s);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    SDR_CUDA(cudaFuncSetAttribute(k_sparse_sign, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    configured = smem;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(k_sparse_sign), smem);
   TimedLaunch t(c, "sketch");
   k_sparse_sign<<<grid, kThreads, smem, c.stream>>>(x_own, xscale, nloc, row_begin, S.key, static_cast<int>(S.s),
                                                     static_cast<int>(S.zeta), 1.0 / std::sqrt(static_cast<double>(S.zeta)),

@@ -396,3 +396,33 @@ def test_workspace_reuse_across_operators(sk, O):
         else:
             first[key] = r
         assert r.report.status == "converged"
+
+
+def test_concurrent_solves_on_separate_contexts(sk, O):
+    """Distinct problems on separate contexts may run concurrently (SPEC
+    threading contract): two host threads, two contexts, results identical to
+    the sequential solves."""
+    import threading
+    jobs = []
+    for n in (24, 20):
+        ctx = sk.Context(0)
+        off, col, val = sk.gen_convdiff3d(n, 60.0, 30.0, 15.0)
+        N = n ** 3
+        A = sk.SparseMatrix(N, N, off, col, val, ctx=ctx)
+        jobs.append((ctx, A, O.gaussian_vector(N, n), sk.SolverConfig(m=20, t=2, k=5, s=60, tol=1e-9, max_restarts=40)))
+    seq = [sk.solve(A, b, cfg, space=sk.RecycleSpace(ctx)) for ctx, A, b, cfg in jobs]
+    out = [None, None]
+
+    def run(i):
+        ctx, A, b, cfg = jobs[i]
+        out[i] = [sk.solve(A, b, cfg, space=sk.RecycleSpace(ctx)) for _ in range(3)]
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(2):
+        for r in out[i]:
+            assert r.report.iterations == seq[i].report.iterations
+            assert np.array_equal(r.x, seq[i].x)
