@@ -426,3 +426,21 @@ def test_concurrent_solves_on_separate_contexts(sk, O):
         for r in out[i]:
             assert r.report.iterations == seq[i].report.iterations
             assert np.array_equal(r.x, seq[i].x)
+
+
+@pytest.mark.parametrize("m,k,t", [(250, 20, 2), (60, 30, 2), (40, 0, 4)])
+def test_long_cycles_and_wide_recycle_spaces(sk, O, m, k, t):
+    """m = 250 (record / event arrays, 251-column bases), k = 30 (recycle
+    product beyond the 24-output kernels: the cuBLAS route), k = 0."""
+    n = 20
+    off, col, val = sk.gen_convdiff3d(n, 80.0, 40.0, 20.0)
+    N = n ** 3
+    A = sk.SparseMatrix(N, N, off, col, val)
+    Ao = O.SparseMatrix.from_csr(N, N, off, col, val)
+    b = O.gaussian_vector(N, 17)
+    kw = dict(m=m, t=t, k=k, s=2 * (m + k), tol=1e-10, max_restarts=20)
+    g = sk.solve(A, b, sk.SolverConfig(**kw))
+    o = O.solve(Ao, b, O.SolverConfig(**kw))
+    assert_same_solve(g, o, iters_tol=0.02)
+    if o[1].status == "converged":
+        assert np.linalg.norm(b - Ao.apply(g.x)) <= 1e-10 * np.linalg.norm(b) * (1 + 1e-9)
