@@ -56,6 +56,10 @@ for _ in range(args.steps):
     walls.append(time.perf_counter() - t1)
     iters += sum(r.iterations for r in out.reports)
 total = sum(walls)
+phases = {}
+for r in out.reports:
+    for k, v in r.phases.items():
+        phases[k] = phases.get(k, 0.0) + v
 line = {
     "metric": "gmres_sdr_arnoldi_steps_per_s", "value": iters / total, "unit": "steps/s", "n_gpus": 1,
     "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
@@ -65,6 +69,7 @@ line = {
     "sequence": {"iterations": [r.iterations for r in out.reports], "status": [r.status for r in out.reports],
                  "cycles": [r.cycles for r in out.reports],
                  "final_relative_residual": [r.final_relative_residual for r in out.reports],
-                 "wall_s": [round(w, 4) for w in walls], "setup_s": round(setup_s, 2)},
+                 "wall_s": [round(w, 4) for w in walls], "setup_s": round(setup_s, 2),
+                 "phases_ms": {k: round(v, 2) for k, v in sorted(phases.items(), key=lambda kv: -kv[1])}},
 }
 print(json.dumps(line), flush=True)
