@@ -921,7 +921,12 @@ __global__ void __launch_bounds__(32 * (ZETA / 4)) k_sparse_sign_chunks(const do
   double vn[UE];
 #pragma unroll
   for (int u = 0; u < UE; ++u) vn[u] = j0 + u * stride < nloc ? __ldcs(x + j0 + u * stride) : 0.0;
-  for (; j0 < nloc; j0 += step) {
+  // hash arguments key + (jg*NCH + c + 1)*phi advance by step*NCH*phi per
+  // iteration and stride*NCH*phi per element of the batch (mod 2^64, exact)
+  const uint64_t d_u = static_cast<uint64_t>(stride) * NCH * kPhi64;
+  const uint64_t d_it = static_cast<uint64_t>(step) * NCH * kPhi64;
+  uint64_t arg0 = key + (static_cast<uint64_t>(r0 + j0) * NCH + static_cast<uint64_t>(c) + 1u) * kPhi64;
+  for (; j0 < nloc; j0 += step, arg0 += d_it) {
     double v[UE];
 #pragma unroll
     for (int u = 0; u < UE; ++u) {
@@ -933,8 +938,7 @@ __global__ void __launch_bounds__(32 * (ZETA / 4)) k_sparse_sign_chunks(const do
     double sv[UE][4];
 #pragma unroll
     for (int u = 0; u < UE; ++u) {
-      const uint64_t jg = static_cast<uint64_t>(r0 + j0 + u * stride);
-      const uint64_t h = mix64(key + (jg * NCH + static_cast<uint64_t>(c) + 1u) * kPhi64);
+      const uint64_t h = mix64(arg0 + static_cast<uint64_t>(u) * d_u);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t f = static_cast<uint32_t>(h >> (16 * e)) & 0xFFFFu;
