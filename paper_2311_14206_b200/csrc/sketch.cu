@@ -913,6 +913,9 @@ __global__ void __launch_bounds__(32 * (ZETA / 4)) k_sparse_sign_chunks(const do
     bsr[e] = static_cast<int>((static_cast<int64_t>(l + 1) * s) / ZETA) - b0r[e];
   }
   const int rlo = b0r[0], rhi = b0r[3] + bsr[3];  // this warp's rows
+  int rb[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) rb[e] = b0r[e] * 32 + lane;
   __syncthreads();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * 32;
   constexpr int UE = 4;
@@ -942,8 +945,9 @@ __global__ void __launch_bounds__(32 * (ZETA / 4)) k_sparse_sign_chunks(const do
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t f = static_cast<uint32_t>(h >> (16 * e)) & 0xFFFFu;
-        row[u][e] = (b0r[e] + static_cast<int>(((f >> 1) & 0x7FFFu) * static_cast<uint32_t>(bsr[e]) >> 15)) * 32 + lane;
-        sv[u][e] = (f & 1u) ? v[u] : -v[u];
+        row[u][e] = rb[e] + static_cast<int>(((f >> 1) & 0x7FFFu) * static_cast<uint32_t>(bsr[e]) >> 15) * 32;
+        // sign bit flipped when the entry's sign bit is clear
+        sv[u][e] = __longlong_as_double(__double_as_longlong(v[u]) ^ (static_cast<long long>(~f & 1u) << 63));
       }
     }
 #pragma unroll
