@@ -124,3 +124,33 @@ def test_space_file_rejects_bad_input(sk):
         sk.read_space_file(data=bytes(bad))
     with pytest.raises(RuntimeError, match="cannot open recycle-space file"):
         sk.read_space_file("/nonexistent/path/space.bin")
+
+
+def test_matrix_market_random_round_trips(sk):
+    """Randomised round trips (shapes incl. empty rows / columns, 1 x n,
+    values over many magnitudes): write -> read reproduces the CSR exactly,
+    and the symmetric form mirrors the lower triangle."""
+    rng = np.random.default_rng(123)
+    for trial in range(25):
+        rows, cols = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+        nnz = int(rng.integers(0, rows * cols + 1))
+        r = rng.integers(0, rows, nnz)
+        c = rng.integers(0, cols, nnz)
+        v = rng.standard_normal(nnz) * 10.0 ** rng.integers(-12, 12, nnz)
+        A = sp.coo_matrix((v, (r, c)), shape=(rows, cols)).tocsr()
+        A.sum_duplicates()
+        A.eliminate_zeros()
+        text = sk.matrix_market_string(rows, cols, A.indptr, A.indices, A.data)
+        B = sk.read_matrix_market(text=text)
+        assert B[0] == rows and B[1] == cols
+        assert np.array_equal(B[2], A.indptr) and np.array_equal(B[3], A.indices)
+        assert np.array_equal(B[4], A.data)
+    # symmetric coordinate: the mirror of a random lower triangle
+    n = 25
+    L = sp.tril(sp.random(n, n, density=0.2, random_state=5)).tocoo()
+    body = "".join(f"{i + 1} {j + 1} {x!r}\n" for i, j, x in zip(L.row, L.col, L.data))
+    S = sk.read_matrix_market(text=f"%%MatrixMarket matrix coordinate real symmetric\n{n} {n} {L.nnz}\n{body}")
+    D = L.toarray()
+    ref = D + D.T - np.diag(np.diag(D))
+    got = sp.csr_matrix((S[4], S[3], S[2]), shape=(n, n)).toarray()
+    assert np.array_equal(got, ref)
