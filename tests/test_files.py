@@ -148,7 +148,7 @@ def test_matrix_market_random_round_trips(sk):
     # symmetric coordinate: the mirror of a random lower triangle
     n = 25
     L = sp.tril(sp.random(n, n, density=0.2, random_state=5)).tocoo()
-    body = "".join(f"{i + 1} {j + 1} {x!r}\n" for i, j, x in zip(L.row, L.col, L.data))
+    body = "".join(f"{i + 1} {j + 1} {float(x)!r}\n" for i, j, x in zip(L.row, L.col, L.data))
     S = sk.read_matrix_market(text=f"%%MatrixMarket matrix coordinate real symmetric\n{n} {n} {L.nnz}\n{body}")
     D = L.toarray()
     ref = D + D.T - np.diag(np.diag(D))
