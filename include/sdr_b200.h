@@ -22,7 +22,13 @@
  *   sdr_krylov_run       init_krylov + arnoldi_step                  arnoldi.hpp:47-119
  *   sdr_solve            solve(A, b, cfg, space, sketch, x0, cb)    solver.hpp:269-365
  *   sdr_solve_sequence   solve_sequence(seq, cfg, sketch, space)     solver.hpp:385-459
- *   sdr_gen_*            gen_convdiff (+ BASELINE generators)        problems.hpp:70-88
+ *   sdr_gen_*            gen_convdiff, gen_neumann (+ BASELINE generators)  problems.hpp:38-88
+ *   sdr_spmm             the exact refresh's k products              recycle.hpp:309-316
+ *   sdr_baseline_*       BaselineConfig, baseline_gmres              baseline.hpp:24-216
+ *   sdr_mm_*, sdr_csr_read_matrix_market  read/write_matrix_market   matrix_market.hpp:83-181
+ *   sdr_space_file_*, sdr_recycle_save/load_file  SKRYRCY1 dump      recycle.hpp:337-390
+ *   sdr_csr_create_complex   complex-fp64 operators (BASELINE C4; no reference counterpart)
+ *   sdr_debug_*, sdr_ctx_set_stamps   measurement / test hooks (no reference counterpart)
  */
 #ifndef SDR_B200_H
 #define SDR_B200_H
