@@ -1,24 +1,33 @@
 """GMRES-SDR benchmark (BASELINE.json metric: Arnoldi steps/s & time-to-solution,
-achieved HBM GB/s vs peak).
+achieved HBM GB/s vs peak, 1/2/4/8 GPU).
 
-One bench "step" = one complete GMRES-SDR solve of the workload (fresh recycle
-space each time) — every Arnoldi step, host least-squares, verification and
-harmonic recycle update inside the timed region. value = total Arnoldi steps
-of all ranks / max-over-ranks device time.
+One bench "step" = one complete GMRES-SDR solve of the workload to its
+tolerance (fresh recycle space each time): every Arnoldi step, host least
+squares, verification and harmonic recycle update inside the timed region.
+value = Arnoldi steps of the (global) solve / max-over-ranks device time;
+time_to_solution_ms = device time per solve.
 
-Workloads (BASELINE.json configs, synthetic data per their generators):
-  c2 (default, N=1): 3D 7-point −Δu+β·∇u on 128³, β=(100,50,25), b=gaussian_vector(N,1),
-                     m=100 k=20 t=2 s=240 tol=1e-8, SRDCT seed 0x5eed.
-  With --gpus N>1 each rank owns a 128³ z-slab of a 128×128×(128·N) grid (weak scaling).
-  c5:               512³, β=(200,100,50), b seed 3, m=50 k=10 t=2 s=120 tol=1e-7, sparse sign ζ=8.
+Workloads (BASELINE.json configs, synthetic data from their generators):
+  c5 (default): 3D 7-point -Δu+β·∇u on 512³ (N = 134,217,728), β=(200,100,50),
+                b = gaussian_vector(N, 3), m=50 k=10 t=2 s=120 tol=1e-7, sparse
+                sign ζ=8 (seed 0x5eed). max_restarts raised from the reference
+                default 10 to 100 so the solve reaches 1e-7 (33 cycles).
+  c2:           128³ (N = 2,097,152), β=(100,50,25), b seed 1, m=100 k=20 t=2 s=240
+                tol=1e-8, SRDCT seed 0x5eed (reference default sketch).
+--gpus N (N > 1): the same global problem, z-slab row partition over N ranks
+(strong scaling); without torchrun's env, bench.py relaunches itself under
+torch.distributed.run with N processes (NCCL_DEBUG=INFO).
 
---impl reference times the CPU oracle (the reference cannot be compiled here:
-Eigen/FFTW/LAPACKE absent — DESIGN.md §oracle) on the same workload: a bounded
-sample of init_krylov + Arnoldi steps per bench step, single-threaded like the reference.
+--impl reference: the CPU oracle (the reference cannot be compiled here:
+Eigen/FFTW/LAPACKE absent — DESIGN.md §6) on the same workload, rank 0 only:
+init_krylov once, then one solve_cycle step (arnoldi_step + QR append + LS
+solve, solver.hpp:165-179) per bench step, single-threaded like the reference.
 """
 import argparse
 import json
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,24 +40,47 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 WORKLOADS = {
-    "c2": dict(n=128, beta=(100.0, 50.0, 25.0), seed=1, m=100, k=20, t=2, s=240, tol=1e-8, sketch="srdct"),
-    "c5": dict(n=512, beta=(200.0, 100.0, 50.0), seed=3, m=50, k=10, t=2, s=120, tol=1e-7, sketch="sparse_sign"),
+    "c5": dict(n=512, beta=(200.0, 100.0, 50.0), seed=3, m=50, k=10, t=2, s=120, tol=1e-7, sketch="sparse_sign",
+               max_restarts=100),
+    "c2": dict(n=128, beta=(100.0, 50.0, 25.0), seed=1, m=100, k=20, t=2, s=240, tol=1e-8, sketch="srdct",
+               max_restarts=10),
 }
 METRIC = "gmres_sdr_arnoldi_steps_per_s"
+STEP_KERNELS = ("spmv_arnoldi", "update", "sketch", "update_sketch", "sketch_fold", "fold_partials")
 
 
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_info():
+    """CPU model, logical cores and RAM of the box the CPU baseline runs on."""
+    model = platform.processor() or ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                ram = round(int(ln.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "ram_gib": ram}
 
 
 class ClockSampler:
     """SM clocks + clock-event (throttle) reasons sampled during the timed
-    region through NVML (the library nvidia-smi queries; polling in-process
-    avoids a competing nvidia-smi client contending for the driver)."""
+    region through NVML (the library nvidia-smi queries)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
@@ -114,26 +146,25 @@ def dist_env():
 
 
 def bytes_per_step(N, a_bytes, t):
-    """B_step = bytes(A) + 8 N (4 + 2t), with bytes(A) the
-    operator storage one SpMV streams (CSR in the reference: 12 nnz + 4 (N+1);
-    here SELL-DIA 8 B per stored entry, or SELL-32 12 B; A.storage["bytes"])."""
+    """B_step = bytes(A) + 8 N (4 + 2t); bytes(A) = the
+    operator storage one SpMV streams (`A.storage["bytes"]`: SELL-DIA 8 B per
+    stored entry here; the reference's CSR 12 nnz + 4 (N + 1) for §8(d)'s figure)."""
     return a_bytes + 8 * N * (4 + 2 * t)
 
 
 def kernel_bytes(N, a_bytes, t, sketch):
-    """Algorithmic bytes per launch of each hot kernel."""
+    """Algorithmic bytes per launch of each step kernel."""
     return {
-        "spmv_arnoldi": a_bytes + 8 * N * (2 + (t - 1)),          # A, x, y write, t-1 window reads
-        "update": 8 * N * (1 + t) + 8 * N,                        # y + t window reads, w write
-        "update_sketch": 8 * N * (1 + t) + 8 * N + N // 8,        # fused update + SRDCT: the update's bytes (+ sign bits)
+        "spmv_arnoldi": a_bytes + 8 * N * (2 + (t - 1)),          # A, x read, y written, t-1 window reads
+        "update": 8 * N * (1 + t) + 8 * N,                        # y + t window reads, w written
+        "update_sketch": 8 * N * (1 + t) + 8 * N + (N // 8 if sketch == "srdct" else 0),  # fused: + sign bits
         "sketch": 8 * N + (N // 8 if sketch == "srdct" else 0),  # one read of w (+ sign bits)
     }
 
 
-def run_reference(args, wl, rank, world):
-    """CPU oracle on a bounded sample of the same workload (rank 0 only)."""
-    if rank != 0:
-        return None
+def oracle_sample(wl, steps):
+    """The CPU oracle on the workload: builds A (direct CSR), b and the sketch,
+    runs init_krylov once and `steps` solve_cycle steps; per-step seconds."""
     from oracle import pyoracle as O
     n = wl["n"]
     N = n ** 3
@@ -143,30 +174,37 @@ def run_reference(args, wl, rank, world):
     S = (O.SketchOperator.subsampled_dct(N, wl["s"], 0x5EED) if wl["sketch"] == "srdct"
          else O.SketchOperator.sparse_sign(N, wl["s"], 0x5EED, 8))
     setup = time.time() - t0
-    steps_per_sample = int(os.environ.get("SDR_REF_STEPS", "8"))
-    for _ in range(args.warmup and 1):
-        O.run_arnoldi(A, b, S, wl["t"], 1, steps=1)
-    times = []
-    for _ in range(args.steps):
-        t1 = time.perf_counter()
-        st = O.run_arnoldi(A, b, S, wl["t"], steps_per_sample, steps=steps_per_sample)
-        times.append(time.perf_counter() - t1)
-        assert st.j == steps_per_sample
-    total = sum(times)
-    value = steps_per_sample * args.steps / total
-    sample = (f"init_krylov + {steps_per_sample} arnoldi_step of workload {args.config} (N={N}) per bench step "
-              f"(oracle C++ restatement, 1 thread; reference unbuildable here)")
-    line = {
+    done, init_s, step_s = O.step_sample(A, b, S, wl["t"], steps)
+    assert done == steps, (done, steps)
+    return dict(N=N, nnz=A.nnz, setup_s=setup, init_s=init_s, step_s=step_s, steps=steps)
+
+
+def run_reference(args, wl, rank, world):
+    """--impl reference: the CPU oracle on the same workload (rank 0 only)."""
+    if rank != 0:
+        return None
+    warm = min(args.warmup, 1)
+    # steps are timed as a whole after one warm step (the per-step work is identical)
+    from oracle import pyoracle as O  # noqa: F401
+    r = oracle_sample(wl, warm + args.steps)
+    per_step = r["step_s"] / r["steps"]
+    value = 1.0 / per_step
+    sample = (f"{args.config} at full size (N={r['N']}): init_krylov once ({r['init_s']:.1f} s, untimed), then "
+              f"{warm}+{args.steps} solve_cycle steps (arnoldi_step + IncrementalQR append + LS solve, "
+              f"solver.hpp:165-179), 1 step per bench step; oracle C++ restatement, 1 thread (the reference is "
+              f"single-threaded and unbuildable here)")
+    return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "N": N, "nnz": A.nnz, "m": wl["m"], "k": wl["k"], "t": wl["t"],
-                   "s": wl["s"], "sketch": wl["sketch"]},
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "port", "sample": sample},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE generators, seeded)",
+        "config": {"workload": args.config, "N": r["N"], "nnz": r["nnz"], "m": wl["m"], "k": wl["k"], "t": wl["t"],
+                   "s": wl["s"], "tol": wl["tol"], "sketch": wl["sketch"]},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "port", "sample": sample,
+                         **host_info()},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "setup_s": setup,
+        "setup_s": r["setup_s"],
     }
-    return line
 
 
 _JSON_OUT = None
@@ -180,17 +218,32 @@ def emit(line):
     out.flush()
 
 
+def relaunch(ngpus):
+    """bench.py --gpus N outside torchrun: N ranks through torch.distributed.run
+    on this node (127.0.0.1), NCCL_DEBUG=INFO so the communicator set-up is logged."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ngpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.config]
     rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}; using {world} ranks", file=sys.stderr)
 
     if args.impl == "reference":
         line = run_reference(args, wl, rank, world)
@@ -198,6 +251,7 @@ def main():
             emit(line)
         return
 
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
     import torch
     torch.cuda.set_device(local)
     import paper_2311_14206_b200 as sk
@@ -215,28 +269,36 @@ def main():
         ctx = sk.Context(local)
 
     n = wl["n"]
-    nz = n * world if args.config == "c2" else n
-    z0, z1 = (rank * n, (rank + 1) * n) if args.config == "c2" else (nz * rank // world, nz * (rank + 1) // world)
-    A = sk.SparseMatrix.convdiff3d_device(n, *wl["beta"], z_begin=z0, z_end=z1, ctx=ctx, ny=n, nz=nz)
+    z0, z1 = n * rank // world, n * (rank + 1) // world  # z-slab of the global grid (strong scaling)
+    t_setup = time.time()
+    A = sk.SparseMatrix.convdiff3d_device(n, *wl["beta"], z_begin=z0, z_end=z1, ctx=ctx)
     N = A.rows
     nloc = A.local_rows
     # b = gaussian_vector(N, seed): every rank draws the same stream and keeps its block
-    b_full = sk.gaussian_vector(N, wl["seed"]) if world == 1 else sk.gaussian_vector(N, wl["seed"])[A.row_begin:A.row_begin + nloc]
-    b_host = torch.from_numpy(np.ascontiguousarray(b_full)).pin_memory()
+    b_full = sk.gaussian_vector(N, wl["seed"])
+    b_host = torch.from_numpy(np.ascontiguousarray(b_full[A.row_begin:A.row_begin + nloc])).pin_memory()
+    del b_full
     b_dev = b_host.to(f"cuda:{local}")
     S = (sk.SketchOperator.subsampled_dct(N, wl["s"], 0x5EED, ctx=ctx) if wl["sketch"] == "srdct"
          else sk.SketchOperator.sparse_sign(N, wl["s"], 0x5EED, 8, ctx=ctx))
-    cfg = sk.SolverConfig(m=wl["m"], k=wl["k"], t=wl["t"], s=wl["s"], tol=wl["tol"])
+    cfg = sk.SolverConfig(m=wl["m"], k=wl["k"], t=wl["t"], s=wl["s"], tol=wl["tol"], max_restarts=wl["max_restarts"])
     stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+    setup_s = time.time() - t_setup
 
     def barrier():
         if dist is not None:
             dist.barrier()
 
-    def one(b, host=False):
-        space = sk.RecycleSpace(ctx)
-        r = sk.solve(A, b, cfg, space=space, sketch=S)
-        return r
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        return max(float(g[0]) for g in gathered)
+
+    def one(b, out=None):
+        return sk.solve(A, b, cfg, space=sk.RecycleSpace(ctx), sketch=S, out=out)
 
     for _ in range(args.warmup):
         r = one(b_dev)
@@ -263,48 +325,38 @@ def main():
     torch.cuda.synchronize()
     barrier()
     launches = ctx.launches - launches0
-    ms = ev0.elapsed_time(ev1)
-    if dist is not None:
-        t = torch.tensor([ms, float(iters)], dtype=torch.float64)
-        gathered = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
-        dist.all_gather(gathered, t)
-        ms = max(float(g[0]) for g in gathered)
-    # Every rank takes the same (global) Arnoldi steps, each over its own 128³
-    # slab: whole-job throughput counts slab-steps, iterations x world / time.
-    value = (iters * world) / (ms / 1e3)
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    # strong scaling: every rank takes the same (global) Arnoldi steps on its
+    # slab; whole-job throughput = global steps / max-over-ranks time
+    value = iters / (ms / 1e3)
 
-    # ---- e2e through the public API with host buffers (H2D of b, D2H of x inside)
-    e2e_iters = 0
-    e2e_walls = []
-    x_host = torch.empty(nloc, dtype=torch.float64).pin_memory()  # the user's pinned result buffer
-    for _ in range(max(1, args.warmup // 2)):  # warm the host-buffer path (first-touch staging)
-        sk.solve(A, b_host.numpy(), cfg, space=sk.RecycleSpace(ctx), sketch=S, out=x_host.numpy())
+    # ---- e2e through the public API with host buffers: H2D of b (pinned), D2H of x (pinned)
+    x_host = torch.empty(nloc, dtype=torch.float64).pin_memory()
+    one(b_host.numpy(), out=x_host.numpy())  # first-touch staging of the host-buffer path
     ctx.synchronize()
     barrier()
+    e2e_iters = 0
+    e2e_walls = []
     t_e2e0 = time.perf_counter()
     for _ in range(args.steps):
         tw = time.perf_counter()
-        space = sk.RecycleSpace(ctx)
-        r = sk.solve(A, b_host.numpy(), cfg, space=space, sketch=S, out=x_host.numpy())
+        r = one(b_host.numpy(), out=x_host.numpy())
         e2e_iters += r.report.iterations
         e2e_walls.append(1e3 * (time.perf_counter() - tw))
     ctx.synchronize()
-    e2e_s = time.perf_counter() - t_e2e0
-    if dist is not None:
-        t = torch.tensor([e2e_s], dtype=torch.float64)
-        gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
-        dist.all_gather(gathered, t)
-        e2e_s = max(float(g[0]) for g in gathered)
-    e2e_value = e2e_iters * world / e2e_s
+    e2e_s = max_over_ranks(time.perf_counter() - t_e2e0)
+    e2e_value = e2e_iters / e2e_s
 
-    # ---- per-kernel roofline from CUDA events on the library stream (one instrumented solve)
+    # ---- per-kernel in-solve durations: CUDA events around every launch of one
+    # instrumented solve (on the library stream)
     ctx.set_timing(True)
     ctx.timing_reset()
     rt = one(b_dev)
     ctx.synchronize()
-    ktimes = {k: ctx.timing(k) for k in ("spmv_arnoldi", "update", "sketch", "update_sketch", "sketch_fold", "sketch_side",
-                                         "tallskinny", "recycle_gemm", "col_norms", "correction", "residual",
-                                         "copy_norm", "allreduce", "halo", "axpy")}
+    names = ("spmv_arnoldi", "update", "sketch", "update_sketch", "sketch_fold", "sketch_side", "tallskinny",
+             "recycle_gemm", "col_norms", "correction", "residual", "copy_norm", "allreduce", "halo", "axpy",
+             "fold_partials")
+    ktimes = {k: ctx.timing(k) for k in names}
     ctx.set_timing(False)
     kb = kernel_bytes(nloc, A.storage["bytes"], wl["t"], wl["sketch"])
     peak, peak_kind = measured_peak()
@@ -313,6 +365,7 @@ def main():
         if cnt:
             d = {"launches": cnt, "avg_us": 1e3 * tot / cnt, "share": 0.0}
             if name in kb:
+                d["bytes"] = kb[name]
                 d["GBps"] = kb[name] / (tot / cnt * 1e-3) / 1e9
                 d["frac"] = d["GBps"] / peak
             kern[name] = d
@@ -320,100 +373,77 @@ def main():
     for v in kern.values():
         v["share"] = v["avg_us"] * v["launches"] / tot_all if tot_all else 0.0
     dom = max((k for k in kern if k in kb), key=lambda k: kern[k]["avg_us"] * kern[k]["launches"])
-    step_us = sum(kern[k]["avg_us"] for k in kb if k in kern)
+    # the per-step kernels' time per Arnoldi step (a cycle's init sketch and
+    # other once-per-cycle launches of the same names are left out)
+    its = rt.report.iterations
+    per_step = [k for k in STEP_KERNELS if k in kern and kern[k]["launches"] >= its]
+    step_us = sum(kern[k]["avg_us"] * kern[k]["launches"] for k in per_step) / max(1, its)
     step_bytes = bytes_per_step(nloc, A.storage["bytes"], wl["t"])
+    csr_bytes = bytes_per_step(nloc, 12 * A.nnz + 4 * (nloc + 1), wl["t"])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as fh:
-            traffic = json.load(fh).get(dom)
+            traffic = json.load(fh).get(args.config, {}).get(dom)
     except Exception:
         pass
-    # the dominant kernel's launch duration without the per-launch event
-    # instrumentation of the solve above: CUDA events around back-to-back
-    # relaunches of a mid-cycle step's K1 / K2 on this workload (idempotent)
-    iso = None
-    if world == 1 and wl["sketch"] == "srdct" and dom in ("spmv_arnoldi", "update_sketch"):
-        import ctypes as C
-        k1, k2 = C.c_double(), C.c_double()
-        b_np = np.ascontiguousarray(b_full)
-        sk._check(sk._lib.sdr_debug_time_step(ctx._h, A._h, S._h, b_np.ctypes.data_as(C.c_void_p), wl["t"], wl["m"],
-                                              20, 50, C.byref(k1), C.byref(k2)))
-        iso = {"spmv_arnoldi": k1.value, "update_sketch": k2.value}
-    dom_us = iso[dom] if iso else kern[dom]["avg_us"]
+    dom_us = kern[dom]["avg_us"]
     dom_gbps = kb[dom] / (dom_us * 1e-6) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbps, "peak": peak, "unit": "GB/s",
-                "frac": dom_gbps / peak, "traffic": traffic, "peak_source": peak_kind,
-                "bytes_per_launch": kb[dom], "launch_us": dom_us,
-                "method": ("CUDA events around 50 back-to-back launches of the step kernel (C2 operator, mid-cycle "
-                           "step j = 20)" if iso else "CUDA events around each launch of one instrumented solve"),
-                "in_solve_event_us": kern[dom]["avg_us"],
-                "isolated_us": iso,
-                "isolated_frac": ({k: kb[k] / (v * 1e-6) / 1e9 / peak for k, v in iso.items()} if iso else None),
-                "arnoldi_step": {"bytes": step_bytes, "us": step_us, "GBps": step_bytes / (step_us * 1e-6) / 1e9,
-                                 "frac": step_bytes / (step_us * 1e-6) / 1e9 / peak,
-                                 "timer": "sum of per-launch CUDA events in one instrumented solve"}}
-    # the step as it runs inside a solve: device-clock stamps (no host events
-    # in the stream), median interval between consecutive K1 starts
-    try:
-        import tempfile
-        sk._check(sk._lib.sdr_ctx_set_stamps(ctx._h, 1))
-        with tempfile.TemporaryDirectory() as td:
-            path = os.path.join(td, "stamps.csv").encode()
-            sk._check(sk._lib.sdr_debug_stamps(ctx._h, path))  # reset
-            one(b_dev)
-            ctx.synchronize()
-            sk._check(sk._lib.sdr_debug_stamps(ctx._h, path))
-            starts = sorted(int(ln.split(",")[1]) for ln in open(path.decode()).read().splitlines()[1:]
-                            if ln.startswith("spmv_arnoldi,") and int(ln.split(",")[2]) > 0)
-        sk._check(sk._lib.sdr_ctx_set_stamps(ctx._h, 0))
-        d = np.diff(np.array(starts, dtype=np.float64)) / 1e3
-        med = float(np.median(d))
-        per = float(np.median(d[d < 2.0 * med]))  # restart boundaries excluded
-        roofline["arnoldi_step_pipelined"] = {"bytes": step_bytes, "period_us": per,
-                                              "GBps": step_bytes / (per * 1e-6) / 1e9,
-                                              "frac": step_bytes / (per * 1e-6) / 1e9 / peak,
-                                              "timer": "device %globaltimer launch stamps in one solve: median "
-                                                       "interval between consecutive K1 starts (restarts excluded)"}
-    except Exception as e:  # measurement only
-        print(f"step period measurement skipped: {e}", file=sys.stderr)
-    if iso:
-        iso_us = iso["spmv_arnoldi"] + iso["update_sketch"]
-        roofline["arnoldi_step_isolated"] = {"bytes": step_bytes, "us": iso_us,
-                                             "GBps": step_bytes / (iso_us * 1e-6) / 1e9,
-                                             "frac": step_bytes / (iso_us * 1e-6) / 1e9 / peak}
+    solve_ms = ms / args.steps
+    per_step_all_us = 1e3 * solve_ms / max(1, iters // args.steps)
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": dom_gbps, "peak": peak, "unit": "GB/s", "frac": dom_gbps / peak,
+        "traffic": traffic, "peak_source": peak_kind, "bytes_per_launch": kb[dom], "launch_us": dom_us,
+        "method": "CUDA events around every launch of one instrumented solve (library stream); algorithmic bytes "
+                  "per launch from the operator's storage (DESIGN.md §4)",
+        "arnoldi_step": {"bytes": step_bytes, "us": step_us, "GBps": step_bytes / (step_us * 1e-6) / 1e9,
+                         "frac": step_bytes / (step_us * 1e-6) / 1e9 / peak,
+                         "kernels": per_step,
+                         "timer": "in-solve launch durations of the per-step kernels, summed per Arnoldi step"},
+        "whole_solve_per_step": {"bytes_storage": step_bytes, "bytes_csr_8d": csr_bytes, "us": per_step_all_us,
+                                 "frac_storage": step_bytes / (per_step_all_us * 1e-6) / 1e9 / peak,
+                                 "frac_csr_8d": csr_bytes / (per_step_all_us * 1e-6) / 1e9 / peak,
+                                 "timer": "timed solve / Arnoldi steps (restarts, verifications and recycle "
+                                          "updates included)"},
+    }
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        class A2:
-            steps = 2
-            warmup = 0
-            config = args.config
-        os.environ.setdefault("SDR_REF_STEPS", "8")
-        ref = run_reference(A2, wl, 0, 1)
-        cpu_baseline = dict(ref["cpu_baseline"])
-        cpu_baseline["value"] = ref["value"]
+        r = oracle_sample(wl, 2)
+        v = r["steps"] / r["step_s"]
+        cpu_baseline = {"value": v, "unit": "steps/s", "cores": 1, "kind": "port",
+                        "sample": (f"{args.config} at full size (N={r['N']}): init_krylov ({r['init_s']:.1f} s, "
+                                   f"untimed) then {r['steps']} solve_cycle steps (arnoldi_step + QR append + LS "
+                                   f"solve), oracle C++ restatement on 1 host thread (the reference is "
+                                   f"single-threaded); {r['step_s']:.1f} s of CPU work"),
+                        "time_to_solution_s_extrapolated": rt.report.iterations / v,
+                        **host_info()}
 
     if rank == 0:
         rep = reports[-1]
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE generators, seeded)",
-            "config": {"workload": args.config, "N": N, "N_per_gpu": nloc, "nnz": A.nnz, "storage": A.storage, "m": wl["m"], "k": wl["k"],
-                       "t": wl["t"], "s": wl["s"], "tol": wl["tol"], "sketch": wl["sketch"],
-                       "parallelism": f"zslab{world}", "l2": "inputs > L2 per solve (V basis 1.7 GB)"},
-            "time_to_solution_ms": ms / args.steps,
+            "warmup": args.warmup, "ms_per_step": solve_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE generators, seeded)",
+            "config": {"workload": args.config, "N": N, "N_per_gpu": nloc, "nnz": A.nnz, "storage": A.storage,
+                       "m": wl["m"], "k": wl["k"], "t": wl["t"], "s": wl["s"], "tol": wl["tol"],
+                       "max_restarts": wl["max_restarts"], "sketch": wl["sketch"],
+                       "parallelism": f"zslab{world}",
+                       "l2": "inputs larger than L2 (Krylov basis (m+1) x 8N bytes per cycle, no L2 flush)"},
+            "time_to_solution_ms": solve_ms,
             "solve": {"status": rep.status, "iterations": rep.iterations, "cycles": rep.cycles,
                       "final_relative_residual": rep.final_relative_residual,
-                      "wall_ms": [round(v, 2) for v in walls], "e2e_wall_ms": [round(v, 2) for v in e2e_walls],
-                      "internal_ms": [round(1e3 * rr.seconds, 2) for rr in reports],
-                      "phases_ms": {k: round(v, 3) for k, v in rep.phases.items()}},
-            "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * nloc, "d2h_bytes_per_step": 8 * nloc},
+                      "wall_ms": [round(v, 1) for v in walls], "e2e_wall_ms": [round(v, 1) for v in e2e_walls],
+                      "phases_ms": {k: round(v, 1) for k, v in rep.phases.items()}},
+            "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * nloc,
+                    "d2h_bytes_per_step": 8 * nloc,
+                    "path": "sdr_solve with host (pinned) b and host x, copies inside the timed region"},
             "roofline": roofline,
             "kernels": kern,
             "cpu_baseline": cpu_baseline,
             "clocks": clk.summary(),
             "gpu_launches": launches,
+            "setup_s": round(setup_s, 2),
         }
         emit(line)
     if dist is not None:
@@ -421,6 +451,14 @@ def main():
 
 
 if __name__ == "__main__":
+    _ngpus = 1
+    for _i, _a in enumerate(sys.argv):
+        if _a == "--gpus" and _i + 1 < len(sys.argv):
+            _ngpus = int(sys.argv[_i + 1])
+        elif _a.startswith("--gpus="):
+            _ngpus = int(_a.split("=", 1)[1])
+    if _ngpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(_ngpus))
     # keep stdout for the JSON line alone: fd 1 points at stderr while the
     # workload runs (NCCL prints its version banner to stdout on rank 0)
     _JSON_OUT = os.fdopen(os.dup(1), "w")

@@ -3,6 +3,7 @@
 // restatement through ctypes (oracle/pyoracle.py). Never linked by the product.
 #include "skrylov_oracle.hpp"
 
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -219,6 +220,41 @@ void orc_krylov_get(void* h, int which, double* out) {
   std::memcpy(out, M[which]->a.data(), sizeof(double) * M[which]->a.size());
 }
 void orc_krylov_free(void* h) { delete static_cast<Krylov*>(h); }
+
+/// CPU baseline sample (bench.py): the per-step work of solve_cycle
+/// (solver.hpp:165-179) with an empty recycle space — init_krylov, then per
+/// step arnoldi_step + IncrementalQR::append + solve — timed on the steps
+/// alone (steady clock). Returns the steps taken; seconds in *step_s and
+/// *init_s.
+int64_t orc_step_sample(void* csr, const double* r0, int64_t n, void* sketch, int64_t t, int64_t steps,
+                        double* init_s, double* step_s) {
+  int64_t done = -1;
+  guard([&] {
+    const auto& S = *static_cast<SketchOperator*>(sketch);
+    OperatorRef op(*static_cast<Csr*>(csr)->A);
+    Counters c;
+    const auto t0 = std::chrono::steady_clock::now();
+    KrylovState st = init_krylov(Vec(r0, r0 + n), S, t, steps, &c);
+    const Index s = S.sketch_dim();
+    Vec sr0(static_cast<size_t>(s));
+    for (Index r = 0; r < s; ++r) sr0[static_cast<size_t>(r)] = st.SV(r, 0) * st.r0_norm;
+    IncrementalQR qr(s, steps, 1e-12);
+    const auto t1 = std::chrono::steady_clock::now();
+    double sres = 0.0;
+    while (st.j < steps && !st.breakdown) {
+      arnoldi_step(st, op, S, &c, 1e-14);
+      const auto info = qr.append(st.SAV.col(st.j - 1), s);
+      if (info.rank_deficient) qr.exclude(info.column);
+      sres += qr.solve(sr0).residual_norm;
+    }
+    const auto t2 = std::chrono::steady_clock::now();
+    *init_s = std::chrono::duration<double>(t1 - t0).count();
+    *step_s = std::chrono::duration<double>(t2 - t1).count();
+    (void)sres;
+    done = st.j;
+  });
+  return done;
+}
 
 // ---- harmonic extraction (test_recycle restatement driver)
 int orc_harmonic(const double* SAW, const double* SW, int64_t s, int64_t p, int64_t k, double rank_tol,

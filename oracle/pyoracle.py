@@ -82,6 +82,7 @@ def lib():
             "orc_krylov_info": (None, [vp, P(i64), P(i32), P(f64), P(i64)]),
             "orc_krylov_get": (None, [vp, C.c_int, P(f64)]),
             "orc_krylov_free": (None, [vp]),
+            "orc_step_sample": (i64, [vp, P(f64), i64, vp, i64, i64, P(f64), P(f64)]),
             "orc_harmonic": (C.c_int, [P(f64), P(f64), i64, i64, i64, f64, P(i64), P(i64), P(i32),
                                        P(f64), P(f64), P(f64), P(f64)]),
             "orc_space_create": (vp, []), "orc_space_free": (None, [vp]),
@@ -372,6 +373,18 @@ def run_arnoldi(A: SparseMatrix, r0, S: SketchOperator, t, m, steps=None, breakd
                            counters=tuple(cnt))
     finally:
         lib().orc_krylov_free(h)
+
+
+def step_sample(A: SparseMatrix, r0, S: SketchOperator, t, steps):
+    """init_krylov + `steps` solve_cycle steps (arnoldi_step, QR append, LS
+    solve); returns (steps, init seconds, step seconds) — bench.py's CPU
+    baseline sample."""
+    r0, pr = _f64(r0)
+    a, b = C.c_double(), C.c_double()
+    done = lib().orc_step_sample(A._h, pr, len(r0), S._h, t, steps, C.byref(a), C.byref(b))
+    if done < 0:
+        raise ValueError(_err())
+    return done, a.value, b.value
 
 
 def harmonic(SAW, SW, k, rank_tol=1e-12):

@@ -342,26 +342,40 @@ inline SparseMatrix gen_convdiff2d(Index n, double bx, double by, double shift =
 
 /// NEW (BASELINE C2/C5): 7-point −Δu + β·∇u on an n³ interior grid,
 /// h = 1/(n+1), Dirichlet, p = iz·n² + iy·n + ix (x fastest).
+/// 3D analogue of gen_convdiff (BASELINE C2/C5: 7-point -Δu + β·∇u, h = 1/(n+1),
+/// lexicographic order x fastest). No reference code (unpinned);
+/// entries as from_triplets would produce them (:40-73: rows in order,
+/// increasing columns, exact zeros dropped), written row by row so C5
+/// (N = 2^27, 0.94 G entries) needs no 22 GB triplet sort.
 inline SparseMatrix gen_convdiff3d(Index n, double bx, double by, double bz) {
   const double h2 = static_cast<double>((n + 1) * (n + 1));
   const double c[3] = {bx * static_cast<double>(n + 1) / 2.0, by * static_cast<double>(n + 1) / 2.0,
                        bz * static_cast<double>(n + 1) / 2.0};
   const Index N = n * n * n;
   const Index stride[3] = {1, n, n * n};
-  std::vector<Triplet> t;
-  t.reserve(static_cast<size_t>(7 * N));
+  std::vector<Index> offsets(static_cast<size_t>(N) + 1, 0), columns;
+  Vec values;
+  columns.reserve(static_cast<size_t>(7 * N));
+  values.reserve(static_cast<size_t>(7 * N));
+  auto put = [&](Index col, double v) {
+    if (v != 0.0) {
+      columns.push_back(col);
+      values.push_back(v);
+    }
+  };
   for (Index z = 0; z < n; ++z)
     for (Index y = 0; y < n; ++y)
       for (Index x = 0; x < n; ++x) {
         const Index p = z * n * n + y * n + x;
         const Index coord[3] = {x, y, z};
-        t.push_back({p, p, 6.0 * h2});
-        for (int d = 0; d < 3; ++d) {
-          if (coord[d] > 0) t.push_back({p, p - stride[d], -h2 - c[d]});
-          if (coord[d] + 1 < n) t.push_back({p, p + stride[d], -h2 + c[d]});
-        }
+        for (int d = 2; d >= 0; --d)  // columns below p, increasing
+          if (coord[d] > 0) put(p - stride[d], -h2 - c[d]);
+        put(p, 6.0 * h2);
+        for (int d = 0; d < 3; ++d)  // columns above p, increasing
+          if (coord[d] + 1 < n) put(p + stride[d], -h2 + c[d]);
+        offsets[static_cast<size_t>(p) + 1] = static_cast<Index>(columns.size());
       }
-  return SparseMatrix::from_triplets(N, N, std::move(t));
+  return SparseMatrix(N, N, std::move(offsets), std::move(columns), std::move(values));
 }
 
 // --------------------------------------------------------------- sketch ---
@@ -596,13 +610,29 @@ class SketchOperator {
     if (kind_ == SketchKind::sparse_sign) {
       std::fill(out, out + s_, 0.0);
       const double inv = 1.0 / std::sqrt(static_cast<double>(zeta_));
-      for (Index j = 0; j < n_; ++j)
-        for (Index l = 0; l < zeta_; ++l) {
-          Index r;
-          double sg;
-          sparse_entry(j, l, &r, &sg);
-          out[r] += sg * x[j] * inv;
+      // sparse_entry's map with each chunk hash evaluated once (four entries
+      // per hash), the same additions in the same order
+      const std::uint64_t nc = static_cast<std::uint64_t>((zeta_ + 3) / 4);
+      std::vector<Index> b0(static_cast<size_t>(zeta_)), bs(static_cast<size_t>(zeta_));
+      for (Index l = 0; l < zeta_; ++l) {
+        b0[static_cast<size_t>(l)] = (l * s_) / zeta_;
+        bs[static_cast<size_t>(l)] = ((l + 1) * s_) / zeta_ - b0[static_cast<size_t>(l)];
+      }
+      for (Index j = 0; j < n_; ++j) {
+        const double xv = x[j] * inv;
+        for (std::uint64_t c = 0; c < nc; ++c) {
+          const std::uint64_t h = detail::mix64(key_ + (static_cast<std::uint64_t>(j) * nc + c + 1u) * 0x9E3779B97F4A7C15ull);
+          for (Index e = 0; e < 4; ++e) {
+            const Index l = static_cast<Index>(4 * c) + e;
+            if (l >= zeta_) break;
+            const std::uint32_t f = static_cast<std::uint32_t>(h >> (16 * e)) & 0xFFFFu;
+            const Index r = b0[static_cast<size_t>(l)] +
+                            static_cast<Index>((static_cast<std::uint64_t>((f >> 1) & 0x7FFFu) *
+                                                static_cast<std::uint64_t>(bs[static_cast<size_t>(l)])) >> 15);
+            out[r] += (f & 1u) ? xv : -xv;
+          }
         }
+      }
       return;
     }
     Vec flipped(static_cast<size_t>(n_));

@@ -567,7 +567,9 @@ int blocks_per_sm(const void* kernel, int threads, size_t smem) {
 }
 
 void ensure_dyn_smem(const void* kernel, size_t bytes) {
-  if (bytes <= 48 * 1024) return;
+  // the 48 KB default covers static + dynamic shared memory together: opt in
+  // early enough for kernels with a few KB of static buffers
+  if (bytes <= 32 * 1024) return;
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, size_t> done;
   int dev = 0;

@@ -94,17 +94,25 @@ Config to_cfg(const sdr_config* c) {
 }
 
 bool host_nonzero(Context& c, const double* x, i64 n) {
-  if (!x) return false;
   std::vector<double> h;
   const double* p = x;
-  if (is_device_pointer(x)) {
+  if (!x) n = 0;
+  if (x && is_device_pointer(x)) {
     h.resize(static_cast<size_t>(n));
     SDR_CUDA(cudaMemcpy(h.data(), x, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
     p = h.data();
   }
-  for (i64 i = 0; i < n; ++i)
-    if (p[i] != 0.0) return true;
-  return false;
+  i64 nz = 0;
+  for (i64 i = 0; i < n && !nz; ++i)
+    if (p[i] != 0.0) nz = 1;
+  if (c.distributed()) {
+    // every rank must take the same branch (the x0 != 0 residual exchanges the
+    // halo): x0 counts as nonzero when any rank's slice is
+    std::vector<i64> all(static_cast<size_t>(c.world));
+    c.allgather_i64(&nz, 1, all.data());
+    for (i64 v : all) nz |= v;
+  }
+  return nz != 0;
 }
 
 /// Output staging: device pointers are written directly, host pointers via a

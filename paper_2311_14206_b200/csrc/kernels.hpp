@@ -122,6 +122,14 @@ void launch_sketch(Context& c, const SketchDev& S, const double* x_own, int64_t 
                    double* out);
 void launch_sketch_scaled(Context& c, const SketchDev& S, const double* x_own, double xscale, int64_t nloc,
                           int64_t row_begin, double* out);
+/// out[r] = scale * sum_b partials[b][r] (CTA-major [G][s]), fixed order.
+void launch_sparse_fold(Context& c, const double* partials, int G, int s, double scale, double* out);
+/// Fused update + ζ = 8 sparse sign (sparse_update.cu): w_{j+1}, the record's
+/// norm / Gram entries and S w_{j+1} (record row j+1) in one pass.
+bool update_sparse_eligible(const SketchDev& S, const VecLayout& lay, const RecLayout& RL, int need, int64_t ldv);
+void launch_update_sparse(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv,
+                          const VecLayout& lay, int j, int nwin, int ngram, double* rec, const RecLayout& RL,
+                          double* cvec, const double* coef_ready, int64_t row_begin);
 /// Builds SketchDev::tab / uq (per-row SRDCT constants) once per sketch.
 void prepare_srdct_tables(Context& c, SketchDev& S);
 /// Deferred folds of the one-GPU step pipeline: K1(j) leaves its window dots

@@ -138,7 +138,11 @@ DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int6
   const int64_t nnz = off[local_rows];
   if (nnz > 0 && (!col || !val)) throw invalid("SparseMatrix: offsets/columns/values sizes inconsistent");
   int64_t mnc = std::numeric_limits<int64_t>::max(), mxc = std::numeric_limits<int64_t>::min();
+  int64_t reach_lo_end = 0, reach_hi_begin = local_rows;  // see DeviceOperator::reach_lo_end
+  const int64_t row_end = row_begin + local_rows;
   for (int64_t r = 0; r < local_rows; ++r) {
+    if (off[r + 1] > off[r] && col && col[off[r]] < row_begin) reach_lo_end = r + 1;
+    if (off[r + 1] > off[r] && col && col[off[r + 1] - 1] >= row_end && reach_hi_begin == local_rows) reach_hi_begin = r;
     if (off[r + 1] < off[r]) throw invalid("SparseMatrix: offsets decrease at row " + std::to_string(row_begin + r));
     for (int64_t p = off[r]; p < off[r + 1]; ++p) {
       const int64_t cc = col[p];
@@ -158,6 +162,8 @@ DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int6
   op->row_begin = row_begin;
   op->local_rows = local_rows;
   op->nnz = nnz;
+  op->reach_lo_end = reach_lo_end;
+  op->reach_hi_begin = reach_hi_begin;
   if (!c.distributed() && rows != cols) {
     // rectangular operators are accepted (apply checks dims); ext covers all columns
   }
@@ -428,6 +434,9 @@ DeviceOperator* create_operator_convdiff3d(Context& c, int64_t nx, int64_t ny, i
   op->nnz = op->local_rows;
   for (int d = 0; d < 6; ++d)
     if (coef[d] != 0.0) op->nnz += std::max<int64_t>(cnt[d], 0);
+  // only the first / last plane of the slab reaches into a neighbour's rows
+  op->reach_lo_end = z0 > 0 ? std::min(n2, op->local_rows) : 0;
+  op->reach_hi_begin = z1 < nz ? std::max<int64_t>(0, op->local_rows - n2) : op->local_rows;
   const int64_t mnc = z0 > 0 ? op->row_begin - n2 : op->row_begin;
   const int64_t mxc = z1 < nz ? op->row_begin + op->local_rows - 1 + n2 : op->row_begin + op->local_rows - 1;
   if (c.distributed()) {

@@ -16,6 +16,11 @@ struct DeviceOperator {
   int64_t nnz = 0;                        // stored entries of the block (before padding)
   int64_t ext_begin = 0;                  // global row of extended-vector index 0
   int64_t halo_lo = 0, halo_hi = 0;
+  /// Stencil reach of the local rows: rows [0, reach_lo_end) are the only ones
+  /// that read a column below row_begin, rows [reach_hi_begin, local_rows) the
+  /// only ones that read a column at/after row_begin + local_rows. Rows in
+  /// between never touch the halo, so their SpMV may overlap the halo transfer.
+  int64_t reach_lo_end = 0, reach_hi_begin = 0;
   DeviceBuffer<int64_t> slice_ptr;
   DeviceBuffer<int32_t> cols_idx;  // SELL
   DeviceBuffer<int32_t> doff;      // SELL-DIA

@@ -1143,6 +1143,12 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
 
 }  // namespace
 
+void launch_sparse_fold(Context& c, const double* partials, int G, int s, double scale, double* out) {
+  TimedLaunch t(c, "sketch_fold");
+  k_sparse_fold<<<(s + 7) / 8, 256, 0, c.stream>>>(partials, G, s, scale, out);
+  SDR_KERNEL_CHECK();
+}
+
 void prepare_srdct_tables(Context& c, SketchDev& S) {
   S.tab.resize(8 * S.s + 256);
   S.uq.resize(S.s);

@@ -413,8 +413,10 @@ struct ArnoldiPipeline {
   double* pend_buf = nullptr;  // several ranks: K2's folded partials not yet allreduced
   int pend_n = 0;
 
-  /// Slices [b_lo, b_hi) whose stencils stay inside the own rows (rows
-  /// [halo_lo, nloc - halo_hi)); false when there is no halo or no interior.
+  /// Slices [b_lo, b_hi) whose rows never read a halo entry (rows
+  /// [reach_lo_end, reach_hi_begin), recorded per row when the operator was
+  /// created — not the halo widths, which bound only the columns, not which
+  /// rows reach them); false when there is no halo or no interior.
   /// SDR_K1_SPLIT=force splits a halo-free operator too (four slices each
   /// side), which exercises the split launches on one rank.
   bool k1_split_range(i64& b_lo, i64& b_hi) const {
@@ -431,8 +433,8 @@ struct ArnoldiPipeline {
       b_hi = ns - 4;
       return true;
     }
-    b_lo = (A.halo_lo + kSlice - 1) / kSlice;
-    b_hi = std::max<i64>(0, A.local_rows - A.halo_hi) / kSlice;
+    b_lo = (A.reach_lo_end + kSlice - 1) / kSlice;
+    b_hi = std::max<i64>(0, A.reach_hi_begin) / kSlice;
     return b_lo < b_hi;
   }
 
@@ -590,8 +592,13 @@ struct ArnoldiPipeline {
     launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
                         w.rec.get(), R, T, w.cvec.get(), coef);
     c.allreduce_sum(recj + RL.a_off(), T + 1);
-    if (!fuse_update_sketch() || !launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin,
-                                                       ngram, w.rec.get(), RL, w.cvec.get(), coef, A.row_begin)) {
+    if (update_sparse_eligible(S, lay, RL, std::max(nwin, ngram + 1), lay.ld)) {
+      // sparse sign: update and sketch of w_{j+1} in one pass (sparse_update.cu)
+      launch_update_sparse(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
+                           w.cvec.get(), coef, A.row_begin);
+    } else if (!fuse_update_sketch() ||
+               !launch_update_sketch(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(),
+                                     RL, w.cvec.get(), coef, A.row_begin)) {
       launch_update(c, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(),
                     coef);
       launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());

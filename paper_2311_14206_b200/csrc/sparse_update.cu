@@ -1,0 +1,314 @@
+// K2s: truncated-Arnoldi update fused with the ζ = 8 sparse-sign sketch of
+// the new basis vector (BASELINE C1/C5), sm_100a.
+//
+// Replaces arnoldi.hpp:91-114 (MGS window update, normalisation) plus the
+// sketch application S v_{j+1} (arnoldi.hpp:110-114 / sketch.hpp:139-162)
+// for the sparse-sign map of DESIGN.md §4 — one HBM pass instead of two
+// (the separate sketch re-read w_{j+1} and was issue-bound at 0.15 of HBM).
+//
+// Data movement: a producer warp streams y = A w_j and the window columns
+// w_{j-d} tile by tile (256 rows) into a 3-stage shared-memory ring with
+// bulk-async copies (cp.async.bulk, mbarrier transaction counts), so the
+// bytes in flight do not depend on how many warps are resident — the
+// sketch's lane-private bins (s x 32 doubles per CTA) cap residency at five
+// CTAs per SM. (Measured alternative, slower: no producer warp, the second
+// consumer to release a stage issuing its refill — 1.17 vs 1.11 ms at C5.)
+// Consumer warp c (0, 1) evaluates chunk hash h_c of its lanes' rows
+// (entries 4c..4c+3, blocks 4c..4c+3: a row range no other warp touches)
+// and scatters them; both recompute the (bitwise identical) update, warp 0
+// stores w_{j+1} and accumulates ||w||^2 and the Gram entries. Per tile a
+// warp first forms all its rows' hashes and updates (independent chains,
+// issued back to back), releases the stage, then runs the scatter.
+// Determinism: bins are lane-private, CTA rows are reduced in a fixed xor
+// tree, CTA partials folded in a fixed order (k_sparse_fold / fold_partials).
+#include "kernels.hpp"
+#include "mgs.cuh"
+#include "reduce.cuh"
+#include "sketch.hpp"
+#include "tma.cuh"
+
+#include <cstdlib>
+
+namespace sdr {
+
+namespace {
+
+constexpr int kTileRows = 256;  // rows per ring stage (2 KB per vector)
+constexpr int kStages = 3;
+constexpr int kConsumers = 2;  // one warp per 4-entry hash chunk (ζ = 8)
+constexpr int kThreadsUS = 32 * (1 + kConsumers);  // producer + consumers
+
+struct UpdSparseArgs {
+  const double* y;
+  double* V;
+  int64_t ldv, own_off, n;
+  int j, nwin, ngram;
+  double* rec;
+  int64_t rstride;
+  int T;
+  double* cvec;
+  const double* coef_ready;
+  double* ng_partials;
+  double* sk_partials;  // [grid][s]
+  int64_t row_begin;
+  uint64_t key;
+  int s;
+  int64_t ntiles;
+  unsigned long long* stamp;
+};
+
+/// NW = nwin window columns, NG = ngram Gram entries (compile time: the
+/// per-row code has no window predicates).
+template <int NW, int NG>
+__global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ double coef[NW + 1];
+  stamp_begin(a.stamp);
+  const int s = a.s;
+  double* bins = smem;                                 // [s][32]
+  double* ring = smem + static_cast<int64_t>(s) * 32;  // [stage][1 + NW][kTileRows]
+  constexpr int kNvec = 1 + NW;
+  constexpr int kStageElems = kNvec * kTileRows;
+  constexpr int kRowsPerLane = kTileRows / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < s * 32; i += blockDim.x) bins[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kStages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kConsumers);
+    }
+    mbar_fence_init();
+  }
+  if (a.coef_ready) {
+    if (threadIdx.x <= NW) coef[threadIdx.x] = a.coef_ready[threadIdx.x];
+  } else if (threadIdx.x == 0) {
+    // several ranks: records were allreduced after K1; every CTA forms the
+    // same coefficients, CTA 0 publishes them in the record
+    double cfull[NW + 1];
+    mgs_coefficients<NW>(a.rec, a.rstride, a.T, a.j, NW, a.cvec, cfull, blockIdx.x == 0);
+    for (int k = 0; k <= NW; ++k) coef[k] = cfull[k];
+  }
+  __syncthreads();
+
+  // this CTA's contiguous tile range
+  const int64_t t0 = a.ntiles * blockIdx.x / gridDim.x, t1 = a.ntiles * (blockIdx.x + 1) / gridDim.x;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // ||w||^2 and Gram entries (consumer 0; zero elsewhere)
+  // Bulk copy of tile t into ring stage st (one thread): y and the window
+  // columns, a 16-byte multiple (an odd last row of the vector is read directly).
+  auto feed = [&](int64_t t, int st) {
+    const int64_t r0 = t * kTileRows;
+    const int64_t rows = min(static_cast<int64_t>(kTileRows), a.n - r0);
+    const uint32_t bytes = static_cast<uint32_t>((rows & ~int64_t{1}) * 8);
+    double* dst = ring + st * kStageElems;
+    mbar_arrive_expect_tx(&full[st], bytes * kNvec);
+    if (bytes) {
+      bulk_g2s(dst, a.y + r0, bytes, &full[st]);
+#pragma unroll
+      for (int d = 0; d < NW; ++d)
+        bulk_g2s(dst + (1 + d) * kTileRows, a.V + static_cast<int64_t>(a.j - d) * a.ldv + a.own_off + r0, bytes,
+                 &full[st]);
+    }
+  };
+  if (warp == 0) {
+    // ---- producer: the warp walks the tiles, one elected lane feeds the ring
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      if (t - t0 >= kStages) mbar_wait_sleep(&empty[st], ph ^ 1u);
+      if (lane == 0) feed(t, st);
+      __syncwarp();
+      if (++st == kStages) st = 0, ph ^= 1u;
+    }
+  } else {
+    // ---- consumers
+    const int c = warp - 1;
+    double cf[NW + 1];
+#pragma unroll
+    for (int k = 0; k <= NW; ++k) cf[k] = coef[k];
+    int rb[4], bsz[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int l = 4 * c + e;
+      rb[e] = (l * s) / 8;
+      bsz[e] = ((l + 1) * s) / 8 - rb[e];
+      rb[e] = rb[e] * 32 + lane;
+    }
+    // hash argument key + (jg*2 + c + 1)*phi; 32 rows further = 64 phi
+    const uint64_t d_row = 64ull * kPhi64;
+    double* wout = a.V + static_cast<int64_t>(a.j + 1) * a.ldv + a.own_off;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      const double* ys = ring + st * kStageElems + lane;
+      const int64_t r0 = t * kTileRows;
+      const int rows = static_cast<int>(min(static_cast<int64_t>(kTileRows), a.n - r0));
+      const uint64_t arg0 =
+          a.key + (static_cast<uint64_t>(a.row_begin + r0 + lane) * 2u + static_cast<uint64_t>(c) + 1u) * kPhi64;
+      uint64_t h[kRowsPerLane];
+#pragma unroll
+      for (int u = 0; u < kRowsPerLane; ++u) h[u] = mix64(arg0 + u * d_row);
+      mbar_wait(&full[st], ph);
+      double w[kRowsPerLane];
+      if (rows == kTileRows) {  // full tile: no bounds checks
+#pragma unroll
+        for (int u = 0; u < kRowsPerLane; ++u) {
+          double wv[NW];
+#pragma unroll
+          for (int d = 0; d < NW; ++d) wv[d] = ys[(1 + d) * kTileRows + 32 * u];
+          double x = cf[0] * ys[32 * u];
+#pragma unroll
+          for (int d = NW - 1; d >= 0; --d) x = fma(cf[1 + d], wv[d], x);
+          w[u] = x;
+          if (c == 0) {
+            __stcs(wout + r0 + 32 * u + lane, x);
+            acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+            for (int g = 1; g <= NG; ++g) acc[g] = fma(x, wv[g - 1], acc[g]);
+          }
+        }
+      } else {  // the vector's last, partial tile
+        const int even = rows & ~1;
+        for (int u = 0; u < kRowsPerLane; ++u) {
+          const int r = 32 * u + lane;
+          double yv = 0.0, wv[NW];
+#pragma unroll
+          for (int d = 0; d < NW; ++d) wv[d] = 0.0;
+          if (r < even) {
+            yv = ys[32 * u];
+#pragma unroll
+            for (int d = 0; d < NW; ++d) wv[d] = ys[(1 + d) * kTileRows + 32 * u];
+          } else if (r < rows) {  // odd last row of the vector: not in the bulk copy
+            yv = a.y[r0 + r];
+#pragma unroll
+            for (int d = 0; d < NW; ++d) wv[d] = a.V[static_cast<int64_t>(a.j - d) * a.ldv + a.own_off + r0 + r];
+          }
+          // rows past the end carry w = 0 and store nothing
+          double x = cf[0] * yv;
+#pragma unroll
+          for (int d = NW - 1; d >= 0; --d) x = fma(cf[1 + d], wv[d], x);
+          w[u] = x;
+          if (c == 0 && r < rows) {
+            __stcs(wout + r0 + r, x);
+            acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+            for (int g = 1; g <= NG; ++g) acc[g] = fma(x, wv[g - 1], acc[g]);
+          }
+        }
+      }
+      // the stage's inputs are in registers now: release it to the producer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == kStages) st = 0, ph ^= 1u;
+#pragma unroll
+      for (int u = 0; u < kRowsPerLane; ++u) {
+        const int whi = __double2hiint(w[u]), wlo = __double2loint(w[u]);
+        int row[4];
+        double sv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t f = static_cast<uint32_t>(h[u] >> (16 * e));  // sign bit 0, row bits 1..15
+          row[e] = rb[e] + static_cast<int>((((f >> 1) & 0x7FFFu) * static_cast<uint32_t>(bsz[e])) >> 15) * 32;
+          // sign bit of w flipped when the entry's sign bit is clear
+          sv[e] = __hiloint2double(whi ^ static_cast<int>((~f & 1u) << 31), wlo);
+        }
+        // a row's four entries lie in four distinct blocks: distinct bins
+        double tv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) tv[e] = bins[row[e]];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bins[row[e]] = tv[e] + sv[e];
+      }
+    }
+    // CTA sketch rows of this warp's blocks: lane-ordered xor tree per row
+    const int rlo = (4 * c * s) / 8, rhi = ((4 * c + 4) * s) / 8;
+    for (int r = rlo; r < rhi; ++r) {
+      const double v = warp_sum(bins[r * 32 + lane]);
+      if (lane == 0) a.sk_partials[static_cast<int64_t>(blockIdx.x) * s + r] = v;
+    }
+  }
+  // T values (entries past ngram are zero): value-major CTA partials, folded
+  // into the record by a separate fixed-order kernel (no last-CTA fold: its
+  // 8 KB of shared memory would cost a resident CTA per SM)
+  block_partials<4>(acc, a.T, a.ng_partials);
+  stamp_end(a.stamp);
+}
+
+size_t upd_sparse_smem(int s, int nwin) {
+  return sizeof(double) * (static_cast<size_t>(s) * 32 + static_cast<size_t>(kStages) * (1 + nwin) * kTileRows);
+}
+
+template <int NW, int NG>
+void upd_sparse_impl(Context& c, const SketchDev& S, UpdSparseArgs a, const RecLayout& RL, double* out) {
+  auto kern = k_update_sparse8<NW, NG>;
+  const size_t smem = upd_sparse_smem(static_cast<int>(S.s), NW);
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+  const int per_sm = std::max(1, blocks_per_sm(reinterpret_cast<const void*>(kern), kThreadsUS, smem));
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(a.ntiles, static_cast<int64_t>(c.num_sms) * per_sm)));
+  a.ng_partials = c.partials(4 * static_cast<int64_t>(g));
+  a.sk_partials = c.partials2(static_cast<int64_t>(g) * S.s);
+  a.stamp = c.launch_stamp("update_sketch");
+  {
+    TimedLaunch t(c, "update_sketch");
+    kern<<<g, kThreadsUS, smem, c.stream>>>(a);
+    SDR_KERNEL_CHECK();
+  }
+  launch_fold_partials(c, a.ng_partials, g, RL.T, true, a.rec + static_cast<int64_t>(a.j + 1) * RL.stride + RL.b_off());
+  launch_sparse_fold(c, a.sk_partials, g, static_cast<int>(S.s), 1.0 / std::sqrt(8.0), out);
+}
+
+template <int NW>
+void upd_sparse_ng(Context& c, const SketchDev& S, const UpdSparseArgs& a, const RecLayout& RL, double* out) {
+  switch (a.ngram) {
+    case 0: return upd_sparse_impl<NW, 0>(c, S, a, RL, out);
+    case 1: return upd_sparse_impl<NW, (NW >= 1 ? 1 : 0)>(c, S, a, RL, out);
+    case 2: return upd_sparse_impl<NW, (NW >= 2 ? 2 : 0)>(c, S, a, RL, out);
+    default: return upd_sparse_impl<NW, (NW >= 3 ? 3 : 0)>(c, S, a, RL, out);
+  }
+}
+
+}  // namespace
+
+bool update_sparse_eligible(const SketchDev& S, const VecLayout& lay, const RecLayout& RL, int need, int64_t ldv) {
+  static const bool on = [] {
+    const char* e = std::getenv("SDR_FUSE_SPARSE");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on && S.kind == kSparseSign && S.zeta == 8 && need <= 4 && RL.T <= 4 && S.s >= 8 && S.s <= 128 &&
+         lay.own_off % 2 == 0 && ldv % 2 == 0 && upd_sparse_smem(static_cast<int>(S.s), 4) <= 200 * 1024;
+}
+
+void launch_update_sparse(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv,
+                          const VecLayout& lay, int j, int nwin, int ngram, double* rec, const RecLayout& RL,
+                          double* cvec, const double* coef_ready, int64_t row_begin) {
+  if (nwin < 1 || nwin > 4 || ngram < 0 || ngram > 3 || ngram > nwin)
+    throw logic("launch_update_sparse: window outside the compiled range");
+  UpdSparseArgs a{};
+  a.y = y;
+  a.V = V;
+  a.ldv = ldv;
+  a.own_off = lay.own_off;
+  a.n = lay.nloc;
+  a.j = j;
+  a.nwin = nwin;
+  a.ngram = ngram;
+  a.rec = rec;
+  a.rstride = RL.stride;
+  a.T = RL.T;
+  a.cvec = cvec;
+  a.coef_ready = coef_ready;
+  a.ntiles = (lay.nloc + kTileRows - 1) / kTileRows;
+  a.row_begin = row_begin;
+  a.key = S.key;
+  a.s = static_cast<int>(S.s);
+  double* out = rec + static_cast<int64_t>(j + 1) * RL.stride + RL.sketch_off();
+  switch (nwin) {
+    case 1: return upd_sparse_ng<1>(c, S, a, RL, out);
+    case 2: return upd_sparse_ng<2>(c, S, a, RL, out);
+    case 3: return upd_sparse_ng<3>(c, S, a, RL, out);
+    default: return upd_sparse_ng<4>(c, S, a, RL, out);
+  }
+}
+
+}  // namespace sdr

@@ -1,0 +1,142 @@
+"""GPU parity on the kernels the BASELINE workloads actually run.
+
+* The fused update + SRDCT tile kernel (k_srdct_tiles<update>, taken when the
+  block length has an F = 256 four-step plan) and the fused update +
+  sparse-sign kernel (k_update_sparse8): H, SV, SAV of sdr_krylov_run within
+  1e-12 of the oracle's literal truncated Arnoldi (arnoldi.hpp:82-119).
+* The sparse-sign apply at C5's N = 2^27 against the oracle's apply.
+* Solves with C5's parameters (sparse sign, m=50 k=10 t=2 s=120, tol 1e-7),
+  C4's lattice operator at 8^3 x 16 and the full 20-system C3 sequence at a
+  reduced grid: status, cycles and counters equal, iterations within ±2 %.
+"""
+import numpy as np
+import pytest
+
+from tests.test_gpu_parity import krylov, rel, to_both
+
+pytestmark = pytest.mark.gpu
+
+
+def conv3d(sk, O, n, beta=(100.0, 50.0, 25.0)):
+    off, col, val = sk.gen_convdiff3d(n, *beta)
+    N = n ** 3
+    return to_both(sk, O, off, col, val, N, N)
+
+
+@pytest.mark.parametrize("n,steps", [(32, 20), (128, 10)])
+@pytest.mark.parametrize("t", [2, 3])
+def test_fused_update_srdct_steps_match_oracle(sk, O, n, steps, t):
+    """Tile-eligible sizes (N = 32^3, 128^3: F = 256, M % 16 == 0) take the
+    fused update + SRDCT kernel on every step."""
+    A, Ao = conv3d(sk, O, n)
+    N = n ** 3
+    s = 240
+    S, So = sk.SketchOperator.subsampled_dct(N, s, 0x5EED), O.SketchOperator.subsampled_dct(N, s, 0x5EED)
+    r0 = O.gaussian_vector(N, 1)
+    g = krylov(sk, A, S, r0, t, steps)
+    o = O.run_arnoldi(Ao, r0, So, t, steps)
+    assert g["j"] == o.j == steps
+    assert g["counters"] == tuple(o.counters)
+    assert rel(g["H"], o.H) <= 1e-12
+    assert rel(g["SV"], o.SV) <= 1e-12
+    assert rel(g["SAV"], o.SAV) <= 1e-12
+    assert rel(g["V"], o.V) <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["conv32", "conv48", "odd_2d"])
+@pytest.mark.parametrize("t", [1, 2, 3])
+def test_fused_update_sparse_sign_steps_match_oracle(sk, O, case, t):
+    """Sparse sign (ζ = 8) steps run the fused update + sketch kernel; an odd
+    row count exercises the direct-load tail row of the bulk-copy ring."""
+    if case == "odd_2d":  # 99^2 = 9801 rows: odd length
+        off, col, val = sk.gen_convdiff2d(99, 100.0, 60.0)
+        N = 99 * 99
+        A, Ao = to_both(sk, O, off, col, val, N, N)
+    else:
+        nn = 32 if case == "conv32" else 48
+        A, Ao = conv3d(sk, O, nn, (200.0, 100.0, 50.0))
+        N = nn ** 3
+    S, So = sk.SketchOperator.sparse_sign(N, 120, 0x5EED, 8), O.SketchOperator.sparse_sign(N, 120, 0x5EED, 8)
+    r0 = O.gaussian_vector(N, 3)
+    steps = 12
+    g = krylov(sk, A, S, r0, t, steps)
+    o = O.run_arnoldi(Ao, r0, So, t, steps)
+    assert g["j"] == o.j == steps
+    assert g["counters"] == tuple(o.counters)
+    assert rel(g["H"], o.H) <= 1e-12
+    assert rel(g["SV"], o.SV) <= 1e-12
+    assert rel(g["SAV"], o.SAV) <= 1e-12
+    assert rel(g["V"], o.V) <= 1e-12
+
+
+def test_sparse_sign_apply_at_c5_size_matches_oracle(sk, O):
+    """C5's N = 2^27: the device sparse-sign apply within 1e-12 of the oracle's."""
+    N = 2 ** 27
+    S, So = sk.SketchOperator.sparse_sign(N, 120, 0x5EED, 8), O.SketchOperator.sparse_sign(N, 120, 0x5EED, 8)
+    x = O.gaussian_vector(N, 3)
+    assert rel(S.apply(x), So.apply(x)) <= 1e-12
+
+
+def test_c5_parameters_solve_matches_oracle(sk, O):
+    """C5's solver parameters (sparse sign, m=50 k=10 t=2 s=120, tol 1e-7) on
+    the same operator family at 48^3."""
+    n = 48
+    A, Ao = conv3d(sk, O, n, (200.0, 100.0, 50.0))
+    N = n ** 3
+    S, So = sk.SketchOperator.sparse_sign(N, 120, 0x5EED, 8), O.SketchOperator.sparse_sign(N, 120, 0x5EED, 8)
+    b = O.gaussian_vector(N, 3)
+    kw = dict(m=50, k=10, t=2, s=120, tol=1e-7, max_restarts=100)
+    g = sk.solve(A, b, sk.SolverConfig(**kw), sketch=S)
+    xo, ro = O.solve(Ao, b, O.SolverConfig(**kw), sketch=So)
+    assert g.report.status == ro.status == "converged"
+    assert abs(g.report.iterations - ro.iterations) <= max(1, 0.02 * ro.iterations)
+    if g.report.iterations == ro.iterations:
+        assert g.report.cycles == ro.cycles
+        assert g.report.counters == ro.counters
+    assert g.report.final_relative_residual < 1e-7
+    assert rel(g.x, xo) <= 1e-5
+
+
+def test_c4_lattice_8x8x8x16_matches_oracle(sk, O):
+    """BASELINE C4's operator (complex 4-D lattice, m0 = -0.8, θ from seed 2)
+    at 8^3 x 16 sites with C4's m=80 k=20 t=3 s=200, tol 1e-8."""
+    from tools.c4_problem import c4_csr
+    off, col, val = c4_csr((8, 8, 8, 16), m0=-0.8, seed=2, uniform=O.uniform_stream)
+    n2 = len(off) - 1
+    A = sk.SparseMatrix(n2, n2, off, col, val)
+    Ao = O.SparseMatrix.from_csr(n2, n2, off, col, val)
+    b = O.gaussian_vector(n2, 4)
+    kw = dict(m=80, k=20, t=3, s=200, tol=1e-8, max_restarts=40)
+    g = sk.solve(A, b, sk.SolverConfig(**kw))
+    xo, ro = O.solve(Ao, b, O.SolverConfig(**kw))
+    assert g.report.status == ro.status
+    assert abs(g.report.iterations - ro.iterations) <= max(1, 0.02 * ro.iterations)
+    if ro.status == "converged":
+        assert g.report.final_relative_residual < 1e-8
+
+
+def test_c3_full_sequence_reduced_grid_matches_oracle(sk, O):
+    """All 20 systems of the C3 sequence (β = (100+2i, 100-2i), σ = 0.01 i,
+    relative diagonal perturbation 1e-3, b_i = b_0 + 0.05 ξ_i; exact refresh,
+    recycle space carried) on a 128^2 grid against the oracle's solve_sequence."""
+    n, count = 128, 20
+    N = n * n
+    b0 = sk.gaussian_vector(N, 0x3000)
+    mats, omats, rhs = [], [], []
+    for i in range(count):
+        d_rel = 1e-3 * (2.0 * sk.uniform_stream(0x3100 + i, N) - 1.0)
+        off, col, val = sk.gen_convdiff2d(n, 100.0 + 2 * i, 100.0 - 2 * i, 0.01 * i, d_rel)
+        mats.append(sk.SparseMatrix(N, N, off, col, val))
+        omats.append(O.SparseMatrix.from_csr(N, N, off, col, val))
+        rhs.append(b0 + 0.05 * sk.gaussian_vector(N, 0x3000 + i) if i else b0)
+    kw = dict(m=50, k=20, t=2, s=140, tol=1e-8, variant="exact")
+    res = sk.solve_sequence([sk.ProblemInstance(A, b, target_tol=1e-8) for A, b in zip(mats, rhs)],
+                          sk.SolverConfig(**kw))
+    xs, reps = O.solve_sequence(omats, rhs, O.SolverConfig(**kw), tols=[1e-8] * count)
+    assert len(res.reports) == len(reps) == count
+    for i, (g, o) in enumerate(zip(res.reports, reps)):
+        assert g.status == o.status, i
+        assert abs(g.iterations - o.iterations) <= max(1, 0.02 * o.iterations), (i, g.iterations, o.iterations)
+        if g.iterations == o.iterations:
+            assert g.cycles == o.cycles, i
+            assert g.counters == o.counters, i
