@@ -108,6 +108,13 @@ bool rgemm_supported(int nout, int k, int64_t lda1, int64_t lda2);
 void launch_rgemm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
                   const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2,
                   double* scratch = nullptr);
+/// Same product on a bulk-copy ring with fp64 tensor-core accumulation
+/// (tsmm.cu), outputs through a pointer list (out[o], n rows each; up to 24),
+/// so one pass can write the correction and the new recycle columns.
+bool tsmm_supported(int nout, int k, int64_t n, int64_t lda1, int64_t lda2);
+int64_t tsmm_scratch_size(int num_sms);
+void launch_tsmm(Context& c, const double* A1, int64_t lda1, int k1, const double* A2, int64_t lda2, int k2,
+                 const double* B, int nout, double* const* out, int64_t n, double* norms2, double* scratch = nullptr);
 /// norms2[q] = ||C(:, q)||^2 for q < ncol (column-major, ldc), deterministic.
 /// scratch: at least (4 num_sms + ncol) doubles, or null for the context's scratch.
 void launch_col_norms2(Context& c, const double* C, int64_t ldc, int64_t n, int ncol, double* norms2,

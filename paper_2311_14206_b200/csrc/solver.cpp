@@ -66,6 +66,8 @@ struct Workspace {
   DeviceBuffer<double> V[2];
   int nV = 0;
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
+  DeviceBuffer<double> unorm;  // ||.||^2 of the fused restart pass's outputs (correction, U_new)
+  double last_harmonic_ms = -1.0;  // host time of the previous cycle's harmonic pencil
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
   // several ranks: the same partials folded over this rank's CTAs before the
   // allreduce; comb[j & 1] = [K2(j) folded (nvp) | K1(j + 1) folded], one
@@ -194,6 +196,7 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
   w->x.ensure(nl);
   w->tmp.ensure(lay.ld);
   w->scal.ensure(64);
+  w->unorm.ensure(32);
   w->coef_dev.ensure(64);
   w->hscal.ensure(64);
   return *w;
@@ -251,6 +254,7 @@ struct EarlyHarmonic {
   i64 j = -1, kh = -1;
   Harmonic hp;
   bool have_hp = false, have_cond = false;
+  bool product_done = false;  // U_new (and its norms, Workspace::unorm + 1) came out of the fused restart pass
   double cond = 1.0, ms = 0.0, cond_ms = 0.0;
   std::exception_ptr err;
   std::atomic<bool> done{false};
@@ -781,7 +785,8 @@ void host_job_while_pumping(F&& job, const std::function<void()>* pump) {
 void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recycle& sp, i64 k, double rank_tol,
                     Counters& cnt, std::vector<std::string>* notes, Report& rep,
                     const std::function<void()>* pump = nullptr, bool side_stream = false,
-                    const HostQR* qr = nullptr, const Harmonic* pre = nullptr) {  // recycle.hpp:226-289
+                    const HostQR* qr = nullptr, const Harmonic* pre = nullptr,
+                    bool product_done = false) {  // recycle.hpp:226-289
   const i64 j = st.j, kh = sp.dim(), s = st.SV.rows;
   if (j < 1) throw invalid("update_recycle: no Arnoldi steps taken");
   HMat SAW(s, kh + j), SW(s, kh + j);
@@ -852,7 +857,7 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
   // with a side stream the product does not queue behind the speculative
   // steps pumped onto the compute stream (it reads the finished cycle's basis
   // and the old U only; the next cycle's correction waits for it below)
-  const bool side = side_stream && dense_u && !c.distributed();
+  const bool side = side_stream && dense_u && !c.distributed() && !product_done;
   if (side) {  // ev_side_in: recorded by solve() when the finished cycle's device work was enqueued
     SDR_CUDA(cudaStreamWaitEvent(w.side_stream, w.ev_side_in, 0));
     std::swap(c.stream, w.side_stream);
@@ -871,7 +876,17 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
   const bool own_rgemm = rgemm_mode != 0;
   const bool use_ts = rgemm_mode != 2 && ke <= 12 && tsgemm_supported(static_cast<int>(ke), nloc, w.lay.ld, sp.ld, sp.ld);
   const bool use_rg = !use_ts && own_rgemm && rgemm_supported(static_cast<int>(ke), static_cast<int>(j + kc), w.lay.ld, sp.ld);
-  if (dense_u && own_gemm && (use_ts || use_rg)) {
+  static const bool tsmm_on = [] {
+    const char* e = std::getenv("SDR_TSMM");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool use_tm = tsmm_on && tsmm_supported(static_cast<int>(ke), static_cast<int>(j + kc), nloc, w.lay.ld, sp.ld);
+  if (product_done) {
+    // the fused restart pass already wrote U_new into sp.buf[other] and its
+    // squared norms after the correction's (run_cycle)
+    SDR_CUDA(cudaMemcpyAsync(w.scal.get(), w.unorm.get() + 1, sizeof(double) * static_cast<size_t>(ke),
+                             cudaMemcpyDeviceToDevice, c.stream));
+  } else if (dense_u && own_gemm && (use_tm || use_ts || use_rg)) {
     const i64 kk = j + kc;
     w.gcoef.ensure(std::max<i64>(kk * ke, 1));
     w.hgcoef.ensure(std::max<i64>(kk * ke, 1));
@@ -884,8 +899,13 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     }
     SDR_CUDA(cudaMemcpyAsync(w.gcoef.get(), hb, sizeof(double) * static_cast<size_t>(kk * ke), cudaMemcpyHostToDevice,
                              c.stream));
-    w.pside.ensure(tsgemm_scratch_size(c.num_sms));
-    if (use_ts)
+    w.pside.ensure(std::max(tsgemm_scratch_size(c.num_sms), tsmm_scratch_size(c.num_sms)));
+    if (use_tm) {
+      std::vector<double*> outs(static_cast<size_t>(ke));
+      for (i64 q = 0; q < ke; ++q) outs[static_cast<size_t>(q)] = sp.buf[other].get() + q * sp.ld;
+      launch_tsmm(c, w.Vcol(vb, 0), w.lay.ld, static_cast<int>(j), sp.buf[sp.cur].get(), sp.ld, static_cast<int>(kc),
+                  w.gcoef.get(), static_cast<int>(ke), outs.data(), nloc, w.scal.get(), w.pside.get());
+    } else if (use_ts)
       launch_tsgemm(c, w.Vcol(vb, 0), w.lay.ld, static_cast<int>(j), sp.buf[sp.cur].get(), sp.ld, static_cast<int>(kc),
                     w.gcoef.get(), static_cast<int>(ke), sp.buf[other].get(), sp.ld, nloc, w.scal.get(), w.pside.get());
     else
@@ -924,7 +944,7 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     for (i64 q = 0; q < ke; ++q) out.push_back(sp.buf[other].get() + q * sp.ld);
     tallskinny(c, w, in, coef, out, nloc, w.scal.get());
   }
-  c.allreduce_sum(w.scal.get(), ke);
+  if (!product_done) c.allreduce_sum(w.scal.get(), ke);
   SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), w.scal.get(), sizeof(double) * ke, cudaMemcpyDeviceToHost, c.stream));
   SDR_CUDA(cudaEventRecord(w.ev_side_out, c.stream));
   if (side) {
@@ -984,6 +1004,67 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     if (notes) notes->push_back("dropped " + std::to_string(bad.size()) + " degenerate deflation columns after the harmonic update");
   }
   if (sp.empty()) sp.provenance = 0;
+}
+
+/// Restart boundary in one pass over [V U]: when the cycle's harmonic pencil
+/// is cheap next to a pass over the basis (C5: ~0.8 ms vs ~13 ms), the host
+/// forms it first and one tall-skinny kernel writes both the correction
+/// (solver.hpp:197-198) and U_new = [U V] P (recycle.hpp:257-265), reading
+/// the basis once instead of twice. SDR_FUSE_RESTART=0/1 forces it off/on.
+bool fuse_restart_wanted(const Context& c, const Workspace& w, i64 kh, i64 j) {
+  static const int mode = [] {
+    const char* e = std::getenv("SDR_FUSE_RESTART");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (mode == 0 || c.distributed()) return false;
+  if (mode == 1) return true;
+  const double pass_ms = static_cast<double>(kh + j) * static_cast<double>(w.lay.nloc) * 8.0 / 5.0e9;
+  const double p = static_cast<double>(kh + j);
+  const double harm_ms = w.last_harmonic_ms >= 0.0 ? w.last_harmonic_ms : 2.5 * (p / 120.0) * (p / 120.0) * (p / 120.0);
+  return pass_ms > 4.0 * harm_ms;
+}
+
+/// Launches the fused pass (outputs: correction, then the k_eff new recycle
+/// columns into sp.buf[1 - sp.cur], squared norms into Workspace::unorm);
+/// false when the shape is not eligible (the caller runs the two passes).
+bool launch_fused_restart(Context& c, Workspace& w, const HostKrylov& st, int vb, Recycle& sp, const Harmonic& hp,
+                          const std::vector<double>& y, double* corr_own) {
+  const i64 j = st.j, kh = sp.dim(), ke = hp.k_eff, nloc = w.lay.nloc;
+  if (ke + 1 > 24 || j < 1) return false;
+  sp.ensure(nloc, std::max<i64>(ke, kh));
+  i64 kc = 0;
+  std::vector<char> used(static_cast<size_t>(std::max<i64>(sp.cap, 1)), 0);
+  for (i64 p = 0; p < kh; ++p) {
+    used[static_cast<size_t>(sp.slot[static_cast<size_t>(p)])] = 1;
+    kc = std::max<i64>(kc, sp.slot[static_cast<size_t>(p)] + 1);
+  }
+  for (i64 q = 0; q < kc; ++q)
+    if (!used[static_cast<size_t>(q)]) return false;  // dead U slots could hold non-finite data
+  const int nout = static_cast<int>(1 + ke);
+  if (!tsmm_supported(nout, static_cast<int>(j + kc), nloc, w.lay.ld, sp.ld)) return false;
+  const i64 kk = j + kc;
+  w.gcoef.ensure(kk * nout);
+  w.hgcoef.ensure(kk * nout);
+  double* hb = w.hgcoef.get();
+  std::fill(hb, hb + kk * nout, 0.0);
+  for (i64 i = 0; i < j; ++i) hb[i] = y[static_cast<size_t>(kh + i)] * st.cv[static_cast<size_t>(i)];
+  for (i64 p = 0; p < kh; ++p)
+    hb[j + sp.slot[static_cast<size_t>(p)]] = y[static_cast<size_t>(p)] * sp.uscale[static_cast<size_t>(p)];
+  for (i64 q = 0; q < ke; ++q) {
+    double* col = hb + (q + 1) * kk;
+    for (i64 i = 0; i < j; ++i) col[i] = hp.coeffs(kh + i, q) * st.cv[static_cast<size_t>(i)];
+    for (i64 p = 0; p < kh; ++p)
+      col[j + sp.slot[static_cast<size_t>(p)]] = hp.coeffs(p, q) * sp.uscale[static_cast<size_t>(p)];
+  }
+  SDR_CUDA(cudaMemcpyAsync(w.gcoef.get(), hb, sizeof(double) * static_cast<size_t>(kk * nout), cudaMemcpyHostToDevice,
+                           c.stream));
+  std::vector<double*> outs(static_cast<size_t>(nout));
+  outs[0] = corr_own;
+  for (i64 q = 0; q < ke; ++q) outs[static_cast<size_t>(q + 1)] = sp.buf[1 - sp.cur].get() + q * sp.ld;
+  w.pside.ensure(std::max(tsgemm_scratch_size(c.num_sms), tsmm_scratch_size(c.num_sms)));
+  launch_tsmm(c, w.Vcol(vb, 0), w.lay.ld, static_cast<int>(j), sp.buf[sp.cur].get(), sp.ld, static_cast<int>(kc),
+              w.gcoef.get(), nout, outs.data(), nloc, w.unorm.get(), w.pside.get());
+  return true;
 }
 
 /// Steps, least squares and verification of one restart cycle
@@ -1053,24 +1134,38 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
     if (sres < tol_abs / out.safety || last) {
       // correction = V(:,0:j) y_tail + U y_head (solver.hpp:197-198), on the device
       PhaseTimer pt_check(rep, "check");
-      std::vector<const double*> in;
-      HMat coef(jj + k_hat, 1);
-      for (i64 i = 0; i < jj; ++i) {
-        in.push_back(w.Vcol(ap.vb, i));
-        coef(i, 0) = y[static_cast<size_t>(k_hat + i)] * st.cv[static_cast<size_t>(i)];
-      }
-      for (i64 q = 0; q < k_hat; ++q) {
-        in.push_back(space.col(q));
-        coef(jj + q, 0) = y[static_cast<size_t>(q)] * space.uscale[static_cast<size_t>(q)];
-      }
       double* corr_own = w.corr.get() + lay.own_off;
-      tallskinny(c, w, in, coef, {corr_own}, lay.nloc, nullptr);
+      bool fused = false;
+      if (cfg.k > 0 && fuse_restart_wanted(c, w, k_hat, jj)) {
+        // the cycle very likely ends here: form its harmonic pencil now and
+        // write the correction and U_new in one pass over the basis
+        auto e = start_early_harmonic(st, space, qr.get(), cfg.k, cfg.rank_tol);
+        if (e->th.joinable()) e->th.join();
+        if (e->err) std::rethrow_exception(e->err);
+        w.last_harmonic_ms = e->ms;
+        if (e->have_hp) fused = launch_fused_restart(c, w, st, ap.vb, space, e->hp, y, corr_own);
+        e->product_done = fused;
+        out.early = e;
+      }
+      if (!fused) {
+        std::vector<const double*> in;
+        HMat coef(jj + k_hat, 1);
+        for (i64 i = 0; i < jj; ++i) {
+          in.push_back(w.Vcol(ap.vb, i));
+          coef(i, 0) = y[static_cast<size_t>(k_hat + i)] * st.cv[static_cast<size_t>(i)];
+        }
+        for (i64 q = 0; q < k_hat; ++q) {
+          in.push_back(space.col(q));
+          coef(jj + q, 0) = y[static_cast<size_t>(q)] * space.uscale[static_cast<size_t>(q)];
+        }
+        tallskinny(c, w, in, coef, {corr_own}, lay.nloc, nullptr);
+      }
       c.halo_exchange(A.plan, w.corr.get() + lay.ext_shift(), A.ext_begin, corr_own, A.row_begin);
       launch_residual(c, A.view(), w.corr.get() + lay.ext_shift(), r0, w.rnew.get(), w.scal.get());
       c.allreduce_sum(w.scal.get(), 1);
       // the cycle very likely ends here: start its restart bookkeeping (host
       // threads) while the verification runs on the device
-      out.early = start_early_harmonic(st, space, qr.get(), cfg.k, cfg.rank_tol);
+      if (!out.early) out.early = start_early_harmonic(st, space, qr.get(), cfg.k, cfg.rank_tol);
       out.residual_norm = std::sqrt(d2h_scalar(c, w, w.scal.get()));
       out.have_correction = true;
       ++cnt.matvecs;
@@ -1087,7 +1182,9 @@ CycleOut run_cycle(Context& c, Workspace& w, ArnoldiPipeline& ap, const DeviceOp
         if (sres > 0.0) out.safety = std::max(out.safety, out.residual_norm / sres);
         if (last) done = true;
       }
-      if (!done && out.early) {  // the cycle goes on: let the thread finish on its own
+      if (!done && out.early && !out.early->th.joinable()) {  // fused: nothing running, result discarded
+        out.early.reset();
+      } else if (!done && out.early) {  // the cycle goes on: let the thread finish on its own
         out.early->th.detach();
         auto keep = out.early;
         std::thread([keep] {
@@ -1141,7 +1238,8 @@ void finish_cycle(Context& c, Workspace& w, const ArnoldiPipeline& ap, const Cyc
       std::vector<std::string> notes;
       PhaseTimer pt(rep, "recycle");
       update_recycle(c, w, st, ap.vb, space, cfg.k, cfg.rank_tol, cnt, &notes, rep, pump, side_stream, out.qr.get(),
-                     early->have_hp ? &early->hp : nullptr);
+                     early->have_hp ? &early->hp : nullptr, early->product_done);
+      if (!early->product_done) w.last_harmonic_ms = early->ms;
       cs.deflation_rank = space.dim();
       for (auto& n : notes) rep.notes.push_back("cycle " + std::to_string(cycle_index) + ": " + n);
     } else if (cfg.k == 0) {
