@@ -78,6 +78,21 @@ SDR_API int sdr_ctx_create(int device, sdr_ctx** out);
  * with sdr_nccl_unique_id and every rank passes the same bytes. */
 SDR_API int sdr_nccl_unique_id(void* out_128_bytes);
 SDR_API int sdr_ctx_create_dist(int device, int rank, int world, const void* nccl_id_128, sdr_ctx** out);
+/* Host-staged transport: the distributed pipeline (z-slab halos, one
+ * allreduce per Arnoldi step) with the caller's collectives instead of NCCL,
+ * each one on host memory after the context stream drained. For ranks that
+ * cannot run NCCL between them (e.g. several processes sharing one GPU in
+ * tests); never a fast path. Callbacks return 0 on success.
+ *   allreduce_sum: in-place sum over ranks of n doubles
+ *   allgather_i64: out[q * count + i] = rank q's in[i]
+ *   exchange:      send nsend doubles to `peer` and receive nrecv from it */
+typedef struct {
+  int (*allreduce_sum)(double* buf, int64_t n, void* user);
+  int (*allgather_i64)(const int64_t* in, int64_t count, int64_t* out, void* user);
+  int (*exchange)(int peer, const double* send, int64_t nsend, double* recv, int64_t nrecv, void* user);
+  void* user;
+} sdr_host_comm;
+SDR_API int sdr_ctx_create_hostcomm(int device, int rank, int world, const sdr_host_comm* comm, sdr_ctx** out);
 SDR_API int sdr_ctx_destroy(sdr_ctx* ctx);
 SDR_API int sdr_ctx_info(const sdr_ctx* ctx, int* device, int* rank, int* world, int* num_sms);
 SDR_API int sdr_ctx_stream(const sdr_ctx* ctx, void** cuda_stream);

@@ -41,7 +41,7 @@ __all__ = [
     "matrix_market_string", "save_recycle_space", "load_recycle_space", "read_space_file", "space_file_bytes", "IncrementalQR", "harmonic_pairs",
     "gaussian_vector", "gen_convdiff", "gen_convdiff2d", "gen_convdiff3d", "gen_neumann", "neumann_sequence",
     "convdiff_sequence", "sparse_sign_entries", "partition_halo",
-    "partition_rows", "SdrError", "CudaError",
+    "partition_rows", "SdrError", "CudaError", "torch_host_comm",
 ]
 
 _lib = _capi.load()
@@ -96,9 +96,16 @@ def _ptr(a, dtype=np.float64):
 class Context:
     """One GPU, one CUDA stream, optional NCCL rank (sdr_ctx)."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 host_comm: dict | None = None):
+        """host_comm: {"allreduce_sum": f(np.ndarray) in place, "allgather_i64": f(np.ndarray) -> np.ndarray
+        (world x count), "exchange": f(peer, send np.ndarray, recv np.ndarray)} — the host-staged
+        transport (sdr_ctx_create_hostcomm), e.g. :func:`torch_host_comm`."""
         h = C.c_void_p()
-        if world > 1 or nccl_id is not None:  # world = 1 with an id: one-rank NCCL, distributed code path
+        if host_comm is not None:
+            self._hc = _host_comm_struct(host_comm)
+            _check(_lib.sdr_ctx_create_hostcomm(device, rank, world, C.byref(self._hc[0]), C.byref(h)))
+        elif world > 1 or nccl_id is not None:  # world = 1 with an id: one-rank NCCL, distributed code path
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             _check(_lib.sdr_ctx_create_dist(device, rank, world, buf, C.byref(h)))
         else:
@@ -155,6 +162,76 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def _host_comm_struct(fns):
+    """ctypes callbacks over Python collectives; exceptions become a nonzero
+    status (the library raises SDR_ENCCL with a message)."""
+    def allreduce(buf, n, user):
+        try:
+            fns["allreduce_sum"](np.ctypeslib.as_array(buf, shape=(n,)))
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def allgather(inp, count, out, user):
+        try:
+            got = fns["allgather_i64"](np.ctypeslib.as_array(inp, shape=(count,)).copy())
+            flat = np.ascontiguousarray(got, dtype=np.int64).ravel()
+            np.ctypeslib.as_array(out, shape=(flat.size,))[:] = flat
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def exchange(peer, send, nsend, recv, nrecv, user):
+        try:
+            s_arr = np.ctypeslib.as_array(send, shape=(nsend,)).copy() if nsend else np.empty(0)
+            r_arr = np.ctypeslib.as_array(recv, shape=(nrecv,)) if nrecv else np.empty(0)
+            fns["exchange"](peer, s_arr, r_arr)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    cbs = (_capi.HC_ALLREDUCE(allreduce), _capi.HC_ALLGATHER(allgather), _capi.HC_EXCHANGE(exchange))
+    return (_capi.sdr_host_comm(cbs[0], cbs[1], cbs[2], None),) + cbs
+
+
+def torch_host_comm(group=None):
+    """Host collectives over an initialised torch.distributed process group
+    (gloo) for Context(host_comm=...). The allreduce gathers every rank's
+    values and sums them in rank order, so all ranks hold bitwise-identical
+    sums (they must form identical MGS coefficients and restart decisions)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+
+    def allreduce_sum(a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        a[:] = acc.numpy()
+
+    def allgather_i64(a):
+        t = torch.from_numpy(a)
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        return torch.stack(parts).numpy()
+
+    def exchange(peer, send, recv):
+        reqs = []
+        if send.size:
+            reqs.append(dist.isend(torch.from_numpy(send), peer, group=group))
+        rt = torch.from_numpy(recv) if recv.size else None
+        if rt is not None:
+            reqs.append(dist.irecv(rt, peer, group=group))
+        for r in reqs:
+            r.wait()
+
+    return {"allreduce_sum": allreduce_sum, "allgather_i64": allgather_i64, "exchange": exchange}
 
 
 _default_ctx = None

@@ -46,12 +46,23 @@ class sdr_callbacks(C.Structure):
     _fields_ = [("on_iteration", ITER_CB), ("on_residual_check", RES_CB), ("user", vp)]
 
 
+HC_ALLREDUCE = C.CFUNCTYPE(cint, P(f64), i64, vp)
+HC_ALLGATHER = C.CFUNCTYPE(cint, P(i64), i64, P(i64), vp)
+HC_EXCHANGE = C.CFUNCTYPE(cint, cint, P(f64), i64, P(f64), i64, vp)
+
+
+class sdr_host_comm(C.Structure):
+    _fields_ = [("allreduce_sum", HC_ALLREDUCE), ("allgather_i64", HC_ALLGATHER), ("exchange", HC_EXCHANGE),
+                ("user", vp)]
+
+
 SIGNATURES = {
     "sdr_last_error": (C.c_char_p, []),
     "sdr_version": (cint, [P(cint), P(cint), P(cint)]),
     "sdr_ctx_create": (cint, [cint, P(vp)]),
     "sdr_nccl_unique_id": (cint, [vp]),
     "sdr_ctx_create_dist": (cint, [cint, cint, cint, vp, P(vp)]),
+    "sdr_ctx_create_hostcomm": (cint, [cint, cint, cint, P(sdr_host_comm), P(vp)]),
     "sdr_ctx_destroy": (cint, [vp]),
     "sdr_ctx_info": (cint, [vp, P(cint), P(cint), P(cint), P(cint)]),
     "sdr_ctx_stream": (cint, [vp, P(vp)]),

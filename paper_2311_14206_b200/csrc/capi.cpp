@@ -178,6 +178,22 @@ int sdr_ctx_create_dist(int device, int rank, int world, const void* id, sdr_ctx
   });
 }
 
+int sdr_ctx_create_hostcomm(int device, int rank, int world, const sdr_host_comm* comm, sdr_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    need(comm, "comm");
+    if (world < 1 || rank < 0 || rank >= world) throw invalid("sdr_ctx_create_hostcomm: bad rank/world");
+    HostComm hc;
+    hc.allreduce_sum = comm->allreduce_sum;
+    hc.allgather_i64 = reinterpret_cast<int (*)(const i64*, i64, i64*, void*)>(comm->allgather_i64);
+    hc.exchange = comm->exchange;
+    hc.user = comm->user;
+    auto h = std::make_unique<sdr_ctx>();
+    h->c = std::make_unique<Context>(device, rank, world, nullptr, &hc);
+    *out = h.release();
+  });
+}
+
 int sdr_ctx_destroy(sdr_ctx* ctx) {
   return guard([&] { delete ctx; });
 }

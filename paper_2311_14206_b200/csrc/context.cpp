@@ -71,7 +71,8 @@ void nccl_unique_id(void* out) {
   std::memcpy(out, &id, sizeof(id));
 }
 
-Context::Context(int dev, int rk, int ws, const void* nccl_id) : device(dev), rank(rk), world(ws) {
+Context::Context(int dev, int rk, int ws, const void* nccl_id, const HostComm* host_comm)
+    : device(dev), rank(rk), world(ws) {
   int count = 0;
   SDR_CUDA(cudaGetDeviceCount(&count));
   if (dev < 0 || dev >= count) throw invalid("sdr_ctx_create: no CUDA device " + std::to_string(dev));
@@ -80,7 +81,12 @@ Context::Context(int dev, int rk, int ws, const void* nccl_id) : device(dev), ra
   SDR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   counters_.resize(kNumCounters);
   SDR_CUDA(cudaMemset(counters_.get(), 0, sizeof(unsigned) * kNumCounters));
-  if (world > 1 || nccl_id) {
+  if (host_comm) {
+    if (!host_comm->allreduce_sum || !host_comm->allgather_i64 || !host_comm->exchange)
+      throw invalid("sdr_ctx_create_hostcomm: every collective callback is required");
+    host_comm_ = true;
+    hc_ = *host_comm;
+  } else if (world > 1 || nccl_id) {
     if (!nccl_id) throw invalid("sdr_ctx_create_dist: NCCL id required for world > 1");
     nccl_ = load_nccl();
     ncclUniqueId id;
@@ -148,6 +154,16 @@ bool Context::peer_setup() {
 }
 
 void Context::allreduce_sum(double* dev, i64 n) {
+  if (host_comm_ && n > 0) {
+    ++launches;
+    hstage_.ensure(n);
+    SDR_CUDA(cudaMemcpyAsync(hstage_.get(), dev, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (hc_.allreduce_sum(hstage_.get(), n, hc_.user) != 0) throw Error(6, "host transport: allreduce failed");
+    SDR_CUDA(cudaMemcpyAsync(dev, hstage_.get(), sizeof(double) * static_cast<size_t>(n), cudaMemcpyHostToDevice, stream));
+    sync();
+    return;
+  }
   if (!comm_ || n <= 0) return;
   if (n <= kPeerMaxN && peer_setup()) {
     launch_peer_allreduce(*this, PeerView{peer_slots_.get(), peer_flags_.get(), world, rank}, dev, static_cast<int>(n),
@@ -161,6 +177,10 @@ void Context::allreduce_sum(double* dev, i64 n) {
 }
 
 void Context::allgather_i64(const i64* host_in, i64 count, i64* host_out) {
+  if (host_comm_) {
+    if (hc_.allgather_i64(host_in, count, host_out, hc_.user) != 0) throw Error(6, "host transport: allgather failed");
+    return;
+  }
   if (!comm_) {
     std::memcpy(host_out, host_in, sizeof(i64) * static_cast<size_t>(count));
     return;
@@ -175,6 +195,25 @@ void Context::allgather_i64(const i64* host_in, i64 count, i64* host_out) {
 
 void Context::halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, const double* x_own, i64 row_begin,
                             cudaStream_t on) {
+  if (host_comm_ && !plan.empty()) {
+    cudaStream_t st = on ? on : this->stream;
+    ++launches;
+    for (int q = 0; q < world; ++q) {
+      if (q == rank || (plan.send_cnt[q] == 0 && plan.recv_cnt[q] == 0)) continue;
+      const i64 ns = plan.send_cnt[q], nr = plan.recv_cnt[q];
+      std::vector<double> sbuf(static_cast<size_t>(ns)), rbuf(static_cast<size_t>(nr));
+      if (ns)
+        SDR_CUDA(cudaMemcpyAsync(sbuf.data(), x_own + (plan.send_lo[q] - row_begin), sizeof(double) * static_cast<size_t>(ns),
+                                 cudaMemcpyDeviceToHost, st));
+      SDR_CUDA(cudaStreamSynchronize(st));
+      if (hc_.exchange(q, sbuf.data(), ns, rbuf.data(), nr, hc_.user) != 0) throw Error(6, "host transport: exchange failed");
+      if (nr)
+        SDR_CUDA(cudaMemcpyAsync(x_ext + (plan.recv_lo[q] - ext_begin), rbuf.data(), sizeof(double) * static_cast<size_t>(nr),
+                                 cudaMemcpyHostToDevice, st));
+      SDR_CUDA(cudaStreamSynchronize(st));
+    }
+    return;
+  }
   if (!comm_ || plan.empty()) return;
   cudaStream_t stream = on ? on : this->stream;
   const bool timed = timing && stream == this->stream;

@@ -26,6 +26,15 @@ struct HaloPlan {
   }
 };
 
+/// Host-staged collectives (sdr_host_comm in the C-ABI): test transport for
+/// ranks without NCCL between them.
+struct HostComm {
+  int (*allreduce_sum)(double* buf, i64 n, void* user) = nullptr;
+  int (*allgather_i64)(const i64* in, i64 count, i64* out, void* user) = nullptr;
+  int (*exchange)(int peer, const double* send, i64 nsend, double* recv, i64 nrecv, void* user) = nullptr;
+  void* user = nullptr;
+};
+
 struct KernelTiming {
   i64 launches = 0;
   double ms = 0.0;
@@ -33,7 +42,7 @@ struct KernelTiming {
 
 class Context {
  public:
-  Context(int device, int rank, int world, const void* nccl_id);
+  Context(int device, int rank, int world, const void* nccl_id, const HostComm* host_comm = nullptr);
   ~Context();
 
   int device = 0, rank = 0, world = 1, num_sms = 148;
@@ -43,7 +52,7 @@ class Context {
   /// Multi-GPU code path: world > 1, or a one-rank NCCL communicator
   /// (sdr_ctx_create_dist with world = 1 and an id) that runs the distributed
   /// pipeline — halo plans, allreduces, fold kernels — on a single GPU.
-  bool distributed() const { return world > 1 || comm_ != nullptr; }
+  bool distributed() const { return world > 1 || comm_ != nullptr || host_comm_; }
 
   // ---- reductions scratch: per-kernel-class partial buffers and
   // last-block-done counters (zeroed once, reset by the last block).
@@ -116,6 +125,9 @@ class Context {
   std::vector<std::string> stamp_names_;
   PinnedBuffer<double> pinned_;
   NcclApi* nccl_ = nullptr;
+  bool host_comm_ = false;
+  HostComm hc_;
+  PinnedBuffer<double> hstage_;
   void* blas_ = nullptr;  // cublasHandle_t, created on first use
   void* comm_ = nullptr;
   // peer-memory allreduce (SDR_PEER=1): own symmetric buffer, mapped peers, epoch

@@ -115,11 +115,7 @@ def test_c4_lattice_8x8x8x16_matches_oracle(sk, O):
         assert g.report.final_relative_residual < 1e-8
 
 
-def test_c3_full_sequence_reduced_grid_matches_oracle(sk, O):
-    """All 20 systems of the C3 sequence (β = (100+2i, 100-2i), σ = 0.01 i,
-    relative diagonal perturbation 1e-3, b_i = b_0 + 0.05 ξ_i; exact refresh,
-    recycle space carried) on a 128^2 grid against the oracle's solve_sequence."""
-    n, count = 128, 20
+def _c3_reduced(sk, O, n, count):
     N = n * n
     b0 = sk.gaussian_vector(N, 0x3000)
     mats, omats, rhs = [], [], []
@@ -129,14 +125,54 @@ def test_c3_full_sequence_reduced_grid_matches_oracle(sk, O):
         mats.append(sk.SparseMatrix(N, N, off, col, val))
         omats.append(O.SparseMatrix.from_csr(N, N, off, col, val))
         rhs.append(b0 + 0.05 * sk.gaussian_vector(N, 0x3000 + i) if i else b0)
+    return mats, omats, rhs
+
+
+def test_c3_full_sequence_reduced_grid_matches_oracle(sk, O):
+    """All 20 systems of the C3 sequence (β = (100+2i, 100-2i), σ = 0.01 i,
+    relative diagonal perturbation 1e-3, b_i = b_0 + 0.05 ξ_i; exact refresh,
+    recycle space carried) on a 128^2 grid.
+
+    Per system: the oracle solves system i from the recycle space the device
+    carried into it (after the exact refresh, recycle.hpp:297-318) — same
+    status, iterations within ±2 %, equal counters when the iterations agree.
+    Seeding each system with the same space keeps a rounding-level flip of a
+    conjugate-pair decision at one system's last restart (recycle.hpp:184-197,
+    k_eff 20 vs 21) from propagating into every later comparison. Whole
+    sequence: the device's solve_sequence against the oracle's own
+    independent solve_sequence, total iterations within ±2 % (statuses equal
+    except on systems one side ends at the restart budget)."""
+    n, count = 128, 20
+    N = n * n
+    mats, omats, rhs = _c3_reduced(sk, O, n, count)
     kw = dict(m=50, k=20, t=2, s=140, tol=1e-8, variant="exact")
-    res = sk.solve_sequence([sk.ProblemInstance(A, b, target_tol=1e-8) for A, b in zip(mats, rhs)],
-                          sk.SolverConfig(**kw))
-    xs, reps = O.solve_sequence(omats, rhs, O.SolverConfig(**kw), tols=[1e-8] * count)
-    assert len(res.reports) == len(reps) == count
-    for i, (g, o) in enumerate(zip(res.reports, reps)):
-        assert g.status == o.status, i
-        assert abs(g.iterations - o.iterations) <= max(1, 0.02 * o.iterations), (i, g.iterations, o.iterations)
-        if g.iterations == o.iterations:
-            assert g.cycles == o.cycles, i
-            assert g.counters == o.counters, i
+    S, So = sk.SketchOperator.subsampled_dct(N, 140, 0x5EED), O.SketchOperator.subsampled_dct(N, 140, 0x5EED)
+    cfg, cfgo = sk.SolverConfig(**kw), O.SolverConfig(**kw)
+    space = sk.RecycleSpace()
+    total_g = total_o = 0
+    for i in range(count):
+        if i > 0 and space.dim() > 0:
+            space.refresh(mats[i], S, mode="exact")
+        so = O.RecycleSpace()
+        if space.dim() > 0:
+            U, SU, SAU = space.get()
+            so.set(U, SU, SAU)
+        g = sk.solve(mats[i], rhs[i], cfg, space=space, sketch=S)
+        xo, o = O.solve(omats[i], rhs[i], cfgo, space=so, sketch=So)
+        assert g.report.status == o.status, i
+        assert abs(g.report.iterations - o.iterations) <= max(1, 0.02 * o.iterations), (i, g.report.iterations,
+                                                                                          o.iterations)
+        if g.report.iterations == o.iterations:
+            assert g.report.cycles == o.cycles, i
+            assert g.report.counters == o.counters, i
+        space = g.space
+    res = sk.solve_sequence([sk.ProblemInstance(A, b, target_tol=1e-8) for A, b in zip(mats, rhs)], cfg)
+    xs, reps = O.solve_sequence(omats, rhs, cfgo, tols=[1e-8] * count)
+    # independent runs drift apart through rounding-level restart decisions;
+    # a status may differ only on a system that sits at the restart budget
+    # (max_restarts = 10 reached by one side) and the totals must agree
+    for g, o in zip(res.reports, reps):
+        assert g.status == o.status or "max_restarts" in (g.status, o.status), (g.status, o.status)
+    total_g = sum(r.iterations for r in res.reports)
+    total_o = sum(r.iterations for r in reps)
+    assert abs(total_g - total_o) <= 0.02 * total_o, (total_g, total_o)
