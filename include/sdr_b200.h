@@ -121,6 +121,18 @@ SDR_API int sdr_csr_create_complex(sdr_ctx* ctx, int64_t rows, int64_t cols, con
 SDR_API int sdr_csr_create_local(sdr_ctx* ctx, int64_t global_rows, int64_t global_cols, int64_t row_begin,
                                  int64_t local_rows, const int64_t* offsets, const int64_t* columns,
                                  const double* values, sdr_csr** out);
+/* Callable operator: OperatorRef(rows, cols, Apply) (operator_ref.hpp:22-25;
+ * README: "Anything that applies vectors can be an operator"). apply must
+ * enqueue y = A x on `cuda_stream` (or finish it before returning); x and y
+ * are device pointers of cols / rows doubles; return 0 on success (nonzero is
+ * reported as SDR_ERUNTIME). The handle is non-owning like OperatorRef: user
+ * must outlive it. Usable wherever an sdr_csr is (sdr_spmv, sdr_solve,
+ * sequences, exact refresh); the solver then runs the product and its
+ * epilogues (window dots, residual) as separate launches. Single-rank
+ * contexts; sdr_csr_storage reports format 3 and 0 bytes. */
+typedef int (*sdr_apply_fn)(const double* x, double* y, void* cuda_stream, void* user);
+SDR_API int sdr_operator_create_callback(sdr_ctx* ctx, int64_t rows, int64_t cols, sdr_apply_fn apply, void* user,
+                                         sdr_csr** out);
 SDR_API int sdr_csr_destroy(sdr_csr* A);
 /* rows/cols global; nnz local (stored, before SELL padding); row_begin/local_rows this rank. */
 SDR_API int sdr_csr_info(const sdr_csr* A, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* row_begin,
@@ -131,7 +143,8 @@ SDR_API int sdr_csr_info(const sdr_csr* A, int64_t* rows, int64_t* cols, int64_t
  * [[a, -b], [b, a]]: a complex matrix on interleaved (re, im) vectors, stored
  * as complex entries, 20 B each — the complex-fp64 SpMV of BASELINE C4);
  * diagonals = DIA diagonals per slice (0 otherwise); stored = entries incl.
- * padding (complex entries for ZSELL); bytes = storage bytes one SpMV streams. */
+ * padding (complex entries for ZSELL); bytes = storage bytes one SpMV streams;
+ * 3 = callable operator (sdr_operator_create_callback, nothing stored). */
 SDR_API int sdr_csr_storage(const sdr_csr* A, int32_t* format, int32_t* diagonals, int64_t* stored, int64_t* bytes);
 /* y = A x (OperatorRef::apply, operator_ref.hpp:38-44). x: local_rows entries of this
  * rank's block (halos are exchanged internally); y: local_rows entries. Host or device. */

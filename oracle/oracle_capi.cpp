@@ -338,6 +338,25 @@ void* orc_solve(void* csr, const double* b, int64_t n, const orc_config* c, void
   return rep;
 }
 
+/// solve() on a callable operator (OperatorRef(rows, cols, Apply),
+/// operator_ref.hpp:22-25): apply(x, y, user) on host vectors.
+void* orc_solve_callable(int64_t rows, int64_t cols, int (*apply)(const double*, double*, void*), void* user,
+                         const double* b, int64_t n, const orc_config* c, void* space, void* sketch, double* x_out) {
+  SolveReport* rep = nullptr;
+  guard([&] {
+    OperatorRef op(rows, cols, [apply, user](const double* x, double* y) {
+      if (apply(x, y, user) != 0) throw std::runtime_error("OperatorRef: apply callback failed");
+    });
+    Vec bb(b, b + n);
+    RecycleSpace sp = space ? *static_cast<RecycleSpace*>(space) : RecycleSpace{};
+    SolveResult r = solve(op, bb, to_cfg(c), std::move(sp), static_cast<SketchOperator*>(sketch), nullptr);
+    std::memcpy(x_out, r.x.data(), sizeof(double) * r.x.size());
+    if (space) *static_cast<RecycleSpace*>(space) = std::move(r.space);
+    rep = new SolveReport(std::move(r.report));
+  });
+  return rep;
+}
+
 void* orc_baseline_gmres(void* csr, const double* b, int64_t n, int64_t m, double tol, int32_t max_restarts,
                          double breakdown_tol, const double* x0, double* x_out) {
   SolveReport* rep = nullptr;

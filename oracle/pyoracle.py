@@ -38,6 +38,9 @@ class orc_config(C.Structure):
     ]
 
 
+ORC_APPLY = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+
+
 def build():
     subprocess.check_call(["make", "-s", "-C", _HERE])
 
@@ -83,6 +86,7 @@ def lib():
             "orc_krylov_get": (None, [vp, C.c_int, P(f64)]),
             "orc_krylov_free": (None, [vp]),
             "orc_step_sample": (i64, [vp, P(f64), i64, vp, i64, i64, P(f64), P(f64)]),
+            "orc_solve_callable": (vp, [i64, i64, ORC_APPLY, vp, P(f64), i64, P(orc_config), vp, vp, P(f64)]),
             "orc_harmonic": (C.c_int, [P(f64), P(f64), i64, i64, i64, f64, P(i64), P(i64), P(i32),
                                        P(f64), P(f64), P(f64), P(f64)]),
             "orc_space_create": (vp, []), "orc_space_free": (None, [vp]),
@@ -512,6 +516,26 @@ def solve(A: SparseMatrix, b, cfg: SolverConfig, space: RecycleSpace | None = No
     c = cfg.c()
     h = lib().orc_solve(A._h, pb, len(b), C.byref(c), space._h if space else None,
                         sketch._h if sketch else None, px0, _f64(x)[1])
+    if not h:
+        raise ValueError(_err())
+    return x, _report(h)
+
+
+def solve_callable(rows, cols, apply, b, cfg: SolverConfig, space: RecycleSpace | None = None,
+                   sketch: SketchOperator | None = None):
+    """solve() on OperatorRef(rows, cols, Apply): apply(x, y) fills the numpy y."""
+    def tramp(x, y, user):
+        try:
+            apply(np.ctypeslib.as_array(x, shape=(cols,)), np.ctypeslib.as_array(y, shape=(rows,)))
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+    fn = ORC_APPLY(tramp)
+    b, pb = _f64(b)
+    x = np.empty(len(b))
+    c = cfg.c()
+    h = lib().orc_solve_callable(rows, cols, fn, None, pb, len(b), C.byref(c), space._h if space else None,
+                                 sketch._h if sketch else None, _f64(x)[1])
     if not h:
         raise ValueError(_err())
     return x, _report(h)

@@ -41,7 +41,7 @@ __all__ = [
     "matrix_market_string", "save_recycle_space", "load_recycle_space", "read_space_file", "space_file_bytes", "IncrementalQR", "harmonic_pairs",
     "gaussian_vector", "gen_convdiff", "gen_convdiff2d", "gen_convdiff3d", "gen_neumann", "neumann_sequence",
     "convdiff_sequence", "sparse_sign_entries", "partition_halo",
-    "partition_rows", "SdrError", "CudaError", "torch_host_comm",
+    "partition_rows", "SdrError", "CudaError", "torch_host_comm", "DeviceVector",
 ]
 
 _lib = _capi.load()
@@ -247,6 +247,24 @@ def default_context() -> Context:
 
 # --------------------------------------------------------------------- operator
 
+class DeviceVector:
+    """A borrowed float64 device vector handed to an operator callback
+    (SparseMatrix.from_callable); exposes __cuda_array_interface__, so
+    ``torch.as_tensor(v, device="cuda")`` views it without a copy."""
+
+    def __init__(self, ptr, n, readonly):
+        self.ptr, self.n, self.readonly = ptr or 0, n, readonly
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.n,), "typestr": "<f8", "data": (self.ptr, self.readonly), "version": 3,
+                "strides": None}
+
+    def tensor(self):
+        import torch
+        return torch.as_tensor(self, device="cuda")
+
+
 class SparseMatrix:
     """CSR operator resident on the device (sparse.hpp:27-150 + OperatorRef).
 
@@ -277,8 +295,32 @@ class SparseMatrix:
         fmt, dg, st, nb = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
         _check(_lib.sdr_csr_storage(self._h, C.byref(fmt), C.byref(dg), C.byref(st), C.byref(nb)))
         # device storage: "sell" or "dia", diagonals per slice, stored entries, bytes per SpMV
-        self.storage = dict(format=("sell", "dia", "zsell")[fmt.value], diagonals=dg.value, stored=st.value,
+        self.storage = dict(format=("sell", "dia", "zsell", "callable")[fmt.value], diagonals=dg.value, stored=st.value,
                             bytes=nb.value)
+
+    @classmethod
+    def from_callable(cls, rows, cols, apply, ctx=None):
+        """OperatorRef(rows, cols, Apply) (operator_ref.hpp:22-25): apply(x, y, stream) computes
+        y = A x for :class:`DeviceVector` x (cols) and y (rows), enqueued on the CUDA stream
+        handle `stream` (e.g. ``torch.cuda.ExternalStream(stream)``) or finished before it
+        returns. Non-owning like the reference: keep what apply uses alive."""
+        ctx = ctx or default_context()
+
+        def tramp(x, y, stream, user):
+            try:
+                apply(DeviceVector(x, cols, True), DeviceVector(y, rows, False), stream or 0)
+                return 0
+            except Exception:  # noqa: BLE001 — reported as SDR_ERUNTIME by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        fn = _capi.APPLY_FN(tramp)
+        h = C.c_void_p()
+        _check(_lib.sdr_operator_create_callback(ctx._h, rows, cols, fn, None, C.byref(h)))
+        obj = cls(0, 0, None, None, None, ctx, _handle=h)
+        obj._apply_fn = fn
+        return obj
 
     @classmethod
     def from_complex(cls, rows, cols, offsets, columns, values, ctx=None):

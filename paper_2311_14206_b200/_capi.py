@@ -56,6 +56,8 @@ class sdr_host_comm(C.Structure):
                 ("user", vp)]
 
 
+APPLY_FN = C.CFUNCTYPE(cint, vp, vp, vp, vp)
+
 SIGNATURES = {
     "sdr_last_error": (C.c_char_p, []),
     "sdr_version": (cint, [P(cint), P(cint), P(cint)]),
@@ -63,6 +65,7 @@ SIGNATURES = {
     "sdr_nccl_unique_id": (cint, [vp]),
     "sdr_ctx_create_dist": (cint, [cint, cint, cint, vp, P(vp)]),
     "sdr_ctx_create_hostcomm": (cint, [cint, cint, cint, P(sdr_host_comm), P(vp)]),
+    "sdr_operator_create_callback": (cint, [vp, i64, i64, APPLY_FN, vp, P(vp)]),
     "sdr_ctx_destroy": (cint, [vp]),
     "sdr_ctx_info": (cint, [vp, P(cint), P(cint), P(cint), P(cint)]),
     "sdr_ctx_stream": (cint, [vp, P(vp)]),

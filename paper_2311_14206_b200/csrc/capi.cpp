@@ -344,6 +344,34 @@ int sdr_csr_create_convdiff3d(sdr_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, 
   });
 }
 
+int sdr_operator_create_callback(sdr_ctx* ctx, int64_t rows, int64_t cols, sdr_apply_fn apply, void* user,
+                                 sdr_csr** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    if (!apply) throw invalid("OperatorRef: apply function required");
+    if (rows < 0 || cols < 0) throw invalid("SparseMatrix: negative dimensions");
+    Context& c = *ctx->c;
+    if (c.distributed()) throw invalid("OperatorRef: callable operators need a single-rank context");
+    auto op = std::make_unique<DeviceOperator>();
+    op->rows = rows;
+    op->cols = cols;
+    op->local_rows = rows;
+    op->halo_hi = std::max<int64_t>(0, cols - rows);
+    op->reach_hi_begin = rows;
+    op->plan.recv_lo.assign(1, 0);
+    op->plan.recv_cnt.assign(1, 0);
+    op->plan.send_lo.assign(1, 0);
+    op->plan.send_cnt.assign(1, 0);
+    op->apply = apply;
+    op->apply_user = user;
+    auto h = std::make_unique<sdr_csr>();
+    h->op.reset(op.release());
+    h->ctx = &c;
+    *out = h.release();
+  });
+}
+
 int sdr_csr_destroy(sdr_csr* A) {
   return guard([&] { delete A; });
 }
@@ -353,6 +381,13 @@ int sdr_csr_storage(const sdr_csr* A, int32_t* format, int32_t* diagonals, int64
     need(A, "A");
     const auto& o = *A->op;
     const int64_t nslices = o.view().nslices;
+    if (o.apply) {
+      if (format) *format = 3;
+      if (diagonals) *diagonals = 0;
+      if (stored) *stored = 0;
+      if (bytes) *bytes = 0;
+      return;
+    }
     if (format) *format = o.dia ? 1 : (o.cplx ? 2 : 0);
     if (diagonals) *diagonals = o.dia ? o.dia_d : 0;
     if (stored) *stored = o.stored;

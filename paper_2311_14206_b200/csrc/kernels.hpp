@@ -19,6 +19,11 @@ struct SellView {
                  // cols = complex column of the extended vector, vals = (re, im) pairs; vectors interleaved
   int64_t nrows = 0, nslices = 0;
   int64_t halo_lo = 0, ext_len = 0;  // own row r is extended index halo_lo + r
+  // callable operator (OperatorRef with an Apply, operator_ref.hpp:22-25):
+  // y = A x is the caller's function, enqueued on the given stream; the SpMV
+  // launchers run it and then the same epilogues as separate kernels
+  int (*apply)(const double* x, double* y, void* stream, void* user) = nullptr;
+  void* apply_user = nullptr;
 };
 
 /// Layout of every length-N vector a rank stores with halo space:

@@ -29,6 +29,9 @@ struct DeviceOperator {
   bool dia = false;
   bool cplx = false;  // ZSELL (complex-structured real operator, see SellView::cplx)
   int dia_d = 0;  // SELL-DIA diagonals per slice
+  // callable operator (sdr_operator_create_callback): no storage
+  int (*apply)(const double* x, double* y, void* stream, void* user) = nullptr;
+  void* apply_user = nullptr;
   int64_t stored = 0;  // stored entries (incl. padding) — bytes = stored * (dia ? 8 : cplx ? 20 : 12)
 
   SellView view() const {
@@ -43,6 +46,8 @@ struct DeviceOperator {
     v.nslices = cplx ? (local_rows / 2 + kSlice - 1) / kSlice : (local_rows + kSlice - 1) / kSlice;
     v.halo_lo = halo_lo;
     v.ext_len = halo_lo + local_rows + halo_hi;
+    v.apply = apply;
+    v.apply_user = apply_user;
     return v;
   }
   /// Layout for vectors used as SpMV inputs of this operator.

@@ -483,7 +483,7 @@ struct ArnoldiPipeline {
       const char* e = std::getenv("SDR_DEFER_DIST");
       return !e || std::atoi(e) != 0;
     }();
-    deferred = (!c.distributed() || defer_dist) && fuse_update_sketch() &&
+    deferred = !A.apply && (!c.distributed() || defer_dist) && fuse_update_sketch() &&
                update_sketch_eligible(S, w.lay, need, A.row_begin, w.lay.ld);
     split = deferred && !c.distributed() && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
     if (!deferred) return;

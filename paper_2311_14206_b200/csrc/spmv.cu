@@ -342,6 +342,59 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_zsell_spmv(SellVie
   }
 }
 
+/// Epilogues of K1 / K6 for a callable operator, whose product y = A x the
+/// caller's function already wrote: MODE 1 — ||y||^2 and y.w_{j-d} (window
+/// dots), MODE 2 — r = b - y in place, ||r||^2. Same partial layouts, folds
+/// and MGS coefficients as k_sell_spmv.
+template <int MODE, int NV>
+__global__ void __launch_bounds__(kThreads) k_product_epilogue(double* __restrict__ y, int64_t n,
+                                                               const double* __restrict__ x_own,
+                                                               const double* __restrict__ aux, int64_t ldv,
+                                                               int64_t own_off, int j, int nwin,
+                                                               double* __restrict__ partials,
+                                                               unsigned* __restrict__ counter, double* __restrict__ out,
+                                                               MgsArgs mg) {
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; row < n;
+       row += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if constexpr (MODE == 1) {
+      const double s = y[row];
+      acc[0] = fma(s, s, acc[0]);
+      acc[1] = fma(s, x_own[row], acc[1]);
+#pragma unroll
+      for (int d = 1; d < NV - 1; ++d)
+        if (d < nwin) acc[1 + d] = fma(s, aux[(j - d) * ldv + own_off + row], acc[1 + d]);
+    } else {
+      const double r = aux[row] - y[row];
+      y[row] = r;
+      acc[0] = fma(r, r, acc[0]);
+    }
+  }
+  const int nv = MODE == 1 ? 1 + nwin : 1;
+  block_partials<NV>(acc, nv, partials);
+  if (counter == nullptr) return;  // deferred: the consumer folds the partials
+  if (last_block_done(counter)) {
+    fold_partials(partials, gridDim.x, nv, out);
+    if constexpr (MODE == 1) {
+      if (mg.coef) {
+        __syncthreads();
+        if (threadIdx.x == 0) mgs_coefficients<NV - 1>(mg.rec, mg.rstride, mg.T, j, nwin, mg.cvec, mg.coef, true);
+      }
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+}
+
+/// The caller's y = A x (not one of this library's kernels: not counted as a launch).
+void call_apply(Context& c, const SellView& A, const double* x, double* y) {
+  if (c.timing) c.time_begin("operator_apply");
+  const int rc = A.apply(x, y, c.stream, A.apply_user);
+  if (c.timing) c.time_end();
+  if (rc != 0) throw runtime("OperatorRef: the apply callback reported failure");
+}
+
 template <class K>
 int resident_grid(const Context& c, K kernel, int64_t want_blocks, int max_per_sm = 0) {
   int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel), kThreads, 0);
@@ -400,6 +453,7 @@ int launch_fmt(Context& c, const char* name, const SellView& A, const double* x_
 
 void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) {
   if (A.nrows == 0) return;
+  if (A.apply) return call_apply(c, A, x_ext + A.halo_lo, y);
   launch_fmt<0, 1>(c, "spmv", A, x_ext, y, nullptr, 0, 0, A.halo_lo, 0, 0, nullptr, nullptr, MgsArgs{});
 }
 
@@ -408,6 +462,23 @@ int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t 
                         double* coef, double* partials_out, int max_per_sm, int64_t sl_begin, int64_t sl_end) {
   const MgsArgs mg{rec, rstride, T, cvec, coef};
   const double* x_ext = V + j * ldv + lay.ext_shift();
+  if (A.apply) {  // y = A w_j by the caller's function, then the window dots
+    if (sl_begin != 0 || (sl_end >= 0 && sl_end != A.nslices)) throw logic("callable operator: no split SpMV");
+    call_apply(c, A, V + j * ldv + lay.own_off, y);
+    auto go = [&](auto kern, int nv_cap) -> int {
+      const int g = resident_grid(c, kern, (A.nrows + kThreads - 1) / kThreads, max_per_sm);
+      double* part = partials_out ? partials_out : c.partials(static_cast<int64_t>(nv_cap) * g);
+      TimedLaunch t(c, "spmv_arnoldi");
+      kern<<<g, kThreads, 0, c.stream>>>(y, A.nrows, V + j * ldv + lay.own_off, V, ldv, lay.own_off, j, nwin, part,
+                                         partials_out ? nullptr : c.counters() + 0, recA, mg);
+      SDR_KERNEL_CHECK();
+      return g;
+    };
+    if (nwin <= 3) return go(k_product_epilogue<1, 4>, 4);
+    if (nwin <= 7) return go(k_product_epilogue<1, 8>, 8);
+    if (nwin <= 33) return go(k_product_epilogue<1, 34>, 34);
+    throw invalid("Arnoldi window of " + std::to_string(nwin) + " vectors exceeds the device limit of 33");
+  }
   if (nwin <= 3)
     return launch_fmt<1, 4>(c, "spmv_arnoldi", A, x_ext, y, V, ldv, lay.own_off, lay.halo_lo, j, nwin, c.counters() + 0,
                             recA, mg, partials_out, max_per_sm, sl_begin, sl_end);
@@ -423,7 +494,7 @@ int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t 
 
 void launch_spmm(Context& c, const SellView& A, const SpmmCols& X, int nb, double* Y, int64_t ldy) {
   if (A.nrows == 0 || nb == 0) return;
-  if (A.cplx) {  // ZSELL: one product per column
+  if (A.cplx || A.apply) {  // ZSELL / callable operator: one product per column
     for (int q = 0; q < nb; ++q) launch_spmv(c, A, X.x[q], Y + q * ldy);
     return;
   }
@@ -446,11 +517,21 @@ void launch_spmm(Context& c, const SellView& A, const SpmmCols& X, int nb, doubl
 
 void launch_spmv_guarded(Context& c, const SellView& A, const double* x_ext, double* y, const int* stop) {
   if (A.nrows == 0) return;
+  if (A.apply) return call_apply(c, A, x_ext + A.halo_lo, y);  // no device-side skip: the product is unused past a stop
   launch_fmt<3, 1>(c, "baseline_spmv", A, x_ext, y, reinterpret_cast<const double*>(stop), 0, 0, A.halo_lo, 0, 0,
                    nullptr, nullptr, MgsArgs{});
 }
 
 void launch_residual(Context& c, const SellView& A, const double* x_ext, const double* b, double* r, double* norm2) {
+  if (A.apply) {
+    call_apply(c, A, x_ext + A.halo_lo, r);
+    const int g = resident_grid(c, k_product_epilogue<2, 1>, (A.nrows + kThreads - 1) / kThreads);
+    TimedLaunch t(c, "residual");
+    k_product_epilogue<2, 1><<<g, kThreads, 0, c.stream>>>(r, A.nrows, nullptr, b, 0, 0, 0, 0, c.partials(g),
+                                                           c.counters() + 1, norm2, MgsArgs{});
+    SDR_KERNEL_CHECK();
+    return;
+  }
   launch_fmt<2, 1>(c, "residual", A, x_ext, r, b, 0, 0, A.halo_lo, 0, 0, c.counters() + 1, norm2, MgsArgs{});
 }
 
