@@ -35,6 +35,9 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstring>
+#include <map>
+#include <mutex>
 #include <cstdint>
 #include <functional>
 #include <limits>
@@ -383,48 +386,95 @@ inline SparseMatrix gen_convdiff3d(Index n, double bx, double by, double bz) {
 
 namespace detail {
 
-/// In-place iterative radix-2 complex FFT, forward sign e^{-2πi jk/n}.
-inline void fft_pow2(std::vector<std::complex<double>>& a) {
-  const size_t n = a.size();
-  for (size_t i = 1, j = 0; i < n; ++i) {
-    size_t bit = n >> 1;
-    for (; j & bit; bit >>= 1) j ^= bit;
-    j ^= bit;
-    if (i < j) std::swap(a[i], a[j]);
+/// Per-length DCT-II plan, cached like the reference's FFTW plan cache
+/// (DctPlanCache, sketch.hpp:27-50: one plan per n behind a mutex): the
+/// bit reversal and per-stage twiddles of an h = n/2 point complex FFT, the
+/// real-FFT untangling twiddles e^{-2πik/n} and the DCT phase e^{-iπk/2n}.
+struct DctPlan {
+  Index n = 0, h = 0;
+  std::vector<std::uint32_t> rev;
+  std::vector<std::complex<double>> tw;     // stage len: tw[len/2 - 1 + k] = e^{-2πik/len}
+  std::vector<std::complex<double>> post;   // e^{-2πik/n}, k < h
+  std::vector<std::complex<double>> shift;  // e^{-iπk/2n}, k < n
+};
+
+inline const DctPlan& dct_plan(Index n) {
+  static std::mutex mu;
+  static std::map<Index, std::unique_ptr<DctPlan>> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto& slot = cache[n];
+  if (slot) return *slot;
+  auto p = std::make_unique<DctPlan>();
+  const double pi = 3.14159265358979323846;
+  p->n = n;
+  p->h = n / 2;
+  const Index h = p->h;
+  int bits = 0;
+  while ((Index{1} << bits) < h) ++bits;
+  p->rev.resize(static_cast<size_t>(h));
+  for (Index i = 0; i < h; ++i) {
+    std::uint32_t r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((static_cast<std::uint32_t>(i) >> b) & 1u) << (bits - 1 - b);
+    p->rev[static_cast<size_t>(i)] = r;
   }
-  std::vector<std::complex<double>> w(n / 2);
-  for (size_t k = 0; k < n / 2; ++k) {
-    const double ang = -2.0 * 3.14159265358979323846 * static_cast<double>(k) / static_cast<double>(n);
-    w[k] = {std::cos(ang), std::sin(ang)};
+  p->tw.resize(static_cast<size_t>(std::max<Index>(h, 1)));
+  for (Index len = 2; len <= h; len <<= 1)
+    for (Index k = 0; k < len / 2; ++k) {
+      const double ang = -2.0 * pi * static_cast<double>(k) / static_cast<double>(len);
+      p->tw[static_cast<size_t>(len / 2 - 1 + k)] = {std::cos(ang), std::sin(ang)};
+    }
+  p->post.resize(static_cast<size_t>(h));
+  for (Index k = 0; k < h; ++k) {
+    const double ang = -2.0 * pi * static_cast<double>(k) / static_cast<double>(n);
+    p->post[static_cast<size_t>(k)] = {std::cos(ang), std::sin(ang)};
   }
-  for (size_t len = 2; len <= n; len <<= 1) {
-    const size_t step = n / len;
-    for (size_t i = 0; i < n; i += len)
-      for (size_t k = 0; k < len / 2; ++k) {
-        const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w[k * step];
-        a[i + k] = u + v;
-        a[i + k + len / 2] = u - v;
-      }
+  p->shift.resize(static_cast<size_t>(n));
+  for (Index k = 0; k < n; ++k) {
+    const double ang = -pi * static_cast<double>(k) / (2.0 * static_cast<double>(n));
+    p->shift[static_cast<size_t>(k)] = {std::cos(ang), std::sin(ang)};
   }
+  slot = std::move(p);
+  return *slot;
 }
 
-/// Orthonormal DCT-II of length n (power of two) via one length-n complex
-/// FFT (Makhoul reordering). Same map as sketch.hpp:55-61 (FFTW REDFT10 +
-/// orthonormal scaling).
+/// Orthonormal DCT-II of length n (power of two, n >= 2): Makhoul's
+/// reordering v = (x_0, x_2, ..., x_3, x_1), V = FFT_n(v) computed as a
+/// real FFT (one n/2-point complex FFT plus untangling), X_k = Re(e^{-iπk/2n}
+/// V_k) with the orthonormal scaling. Same map as sketch.hpp:55-61 (FFTW
+/// REDFT10 + orthonormal scaling).
 inline void dct2_orthonormal_pow2(const double* in, double* out, Index n) {
-  std::vector<std::complex<double>> v(static_cast<size_t>(n));
-  for (Index j = 0; j < n / 2; ++j) {
-    v[static_cast<size_t>(j)] = in[2 * j];
-    v[static_cast<size_t>(n - 1 - j)] = in[2 * j + 1];
+  if (n == 1) {
+    out[0] = in[0];
+    return;
   }
-  if (n == 1) v[0] = in[0];
-  fft_pow2(v);
+  const DctPlan& p = dct_plan(n);
+  const Index h = p.h;
+  // z_m = v_{2m} + i v_{2m+1}; v_j = x_{2j} (j < n/2), v_{n-1-j} = x_{2j+1}
+  auto v = [&](Index j) { return j < h ? in[2 * j] : in[2 * (n - 1 - j) + 1]; };
+  std::vector<std::complex<double>> z(static_cast<size_t>(h));
+  for (Index m = 0; m < h; ++m) z[p.rev[static_cast<size_t>(m)]] = {v(2 * m), v(2 * m + 1)};
+  for (Index len = 2; len <= h; len <<= 1) {
+    const std::complex<double>* w = p.tw.data() + (len / 2 - 1);
+    for (Index i = 0; i < h; i += len)
+      for (Index k = 0; k < len / 2; ++k) {
+        const std::complex<double> a = z[static_cast<size_t>(i + k)], b = z[static_cast<size_t>(i + k + len / 2)] * w[k];
+        z[static_cast<size_t>(i + k)] = a + b;
+        z[static_cast<size_t>(i + k + len / 2)] = a - b;
+      }
+  }
   const double s0 = 1.0 / std::sqrt(static_cast<double>(n));
   const double s = std::sqrt(2.0 / static_cast<double>(n));
-  for (Index k = 0; k < n; ++k) {
-    const double ang = -3.14159265358979323846 * static_cast<double>(k) / (2.0 * static_cast<double>(n));
-    const double re = (std::complex<double>(std::cos(ang), std::sin(ang)) * v[static_cast<size_t>(k)]).real();
-    out[k] = re * (k == 0 ? s0 : s);
+  auto V = [&](Index k) -> std::complex<double> {  // FFT_n(v)_k for 0 <= k <= h
+    if (k == h) return {z[0].real() - z[0].imag(), 0.0};
+    const std::complex<double> a = z[static_cast<size_t>(k)], b = std::conj(z[static_cast<size_t>((h - k) % h)]);
+    const std::complex<double> even = 0.5 * (a + b), odd = std::complex<double>(0.0, -0.5) * (a - b);
+    return even + p.post[static_cast<size_t>(k)] * odd;
+  };
+  for (Index k = 0; k <= h; ++k) {
+    const std::complex<double> vk = V(k);
+    out[k] = (p.shift[static_cast<size_t>(k)] * vk).real() * (k == 0 ? s0 : s);
+    if (k > 0 && k < h)  // V_{n-k} = conj(V_k) (real input)
+      out[n - k] = (p.shift[static_cast<size_t>(n - k)] * std::conj(vk)).real() * s;
   }
 }
 
@@ -611,25 +661,41 @@ class SketchOperator {
       std::fill(out, out + s_, 0.0);
       const double inv = 1.0 / std::sqrt(static_cast<double>(zeta_));
       // sparse_entry's map with each chunk hash evaluated once (four entries
-      // per hash), the same additions in the same order
+      // per hash) and the sign applied by flipping the sign bit (no
+      // data-dependent branch). Columns go in chunks, within a chunk block
+      // by block: a row belongs to one block, so every out[r] receives its
+      // terms in increasing j — the same additions in the same order as the
+      // plain entry loop (bitwise the same result).
       const std::uint64_t nc = static_cast<std::uint64_t>((zeta_ + 3) / 4);
       std::vector<Index> b0(static_cast<size_t>(zeta_)), bs(static_cast<size_t>(zeta_));
       for (Index l = 0; l < zeta_; ++l) {
         b0[static_cast<size_t>(l)] = (l * s_) / zeta_;
         bs[static_cast<size_t>(l)] = ((l + 1) * s_) / zeta_ - b0[static_cast<size_t>(l)];
       }
-      for (Index j = 0; j < n_; ++j) {
-        const double xv = x[j] * inv;
-        for (std::uint64_t c = 0; c < nc; ++c) {
-          const std::uint64_t h = detail::mix64(key_ + (static_cast<std::uint64_t>(j) * nc + c + 1u) * 0x9E3779B97F4A7C15ull);
-          for (Index e = 0; e < 4; ++e) {
-            const Index l = static_cast<Index>(4 * c) + e;
-            if (l >= zeta_) break;
-            const std::uint32_t f = static_cast<std::uint32_t>(h >> (16 * e)) & 0xFFFFu;
-            const Index r = b0[static_cast<size_t>(l)] +
-                            static_cast<Index>((static_cast<std::uint64_t>((f >> 1) & 0x7FFFu) *
-                                                static_cast<std::uint64_t>(bs[static_cast<size_t>(l)])) >> 15);
-            out[r] += (f & 1u) ? xv : -xv;
+      constexpr Index kChunk = 2048;
+      std::vector<std::uint64_t> hc(static_cast<size_t>(kChunk * nc));
+      std::vector<std::uint64_t> xb(static_cast<size_t>(kChunk));
+      for (Index j0 = 0; j0 < n_; j0 += kChunk) {
+        const Index len = std::min(kChunk, n_ - j0);
+        for (Index q = 0; q < len; ++q) {
+          const std::uint64_t j = static_cast<std::uint64_t>(j0 + q);
+          const double v = x[j0 + q] * inv;
+          std::memcpy(&xb[static_cast<size_t>(q)], &v, sizeof(v));
+          for (std::uint64_t c = 0; c < nc; ++c)
+            hc[static_cast<size_t>(c * kChunk + q)] = detail::mix64(key_ + (j * nc + c + 1u) * 0x9E3779B97F4A7C15ull);
+        }
+        for (Index l = 0; l < zeta_; ++l) {
+          const std::uint64_t* hl = hc.data() + (l / 4) * kChunk;
+          const int sh = static_cast<int>(16 * (l % 4));
+          const Index base = b0[static_cast<size_t>(l)];
+          const std::uint64_t bsz = static_cast<std::uint64_t>(bs[static_cast<size_t>(l)]);
+          for (Index q = 0; q < len; ++q) {
+            const std::uint32_t f = static_cast<std::uint32_t>(hl[q] >> sh) & 0xFFFFu;
+            const Index r = base + static_cast<Index>((static_cast<std::uint64_t>((f >> 1) & 0x7FFFu) * bsz) >> 15);
+            const std::uint64_t bits = xb[static_cast<size_t>(q)] ^ (static_cast<std::uint64_t>(~f & 1u) << 63);
+            double term;
+            std::memcpy(&term, &bits, sizeof(term));
+            out[r] += term;
           }
         }
       }
