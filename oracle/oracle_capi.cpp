@@ -2,6 +2,7 @@
 // the pytest suite (tests/) and bench.py's CPU-baseline leg can drive the CPU
 // restatement through ctypes (oracle/pyoracle.py). Never linked by the product.
 #include "skrylov_oracle.hpp"
+#include "skrylov_oracle_complex.hpp"
 
 #include <chrono>
 #include <cstring>
@@ -446,4 +447,62 @@ int64_t orc_report_n_notes(void* r) { return static_cast<int64_t>(static_cast<So
 const char* orc_report_note(void* r, int64_t i) { return static_cast<SolveReport*>(r)->notes[static_cast<size_t>(i)].c_str(); }
 const char* orc_report_error(void* r) { return static_cast<SolveReport*>(r)->error.c_str(); }
 void orc_report_free(void* r) { delete static_cast<SolveReport*>(r); }
+
+// ---- complex GMRES-SDR (skrylov_oracle_complex.hpp; interleaved (re, im) arrays)
+void* orc_zcsr_create(int64_t n, const int64_t* off, const int64_t* col, const double* val) {
+  auto* A = new cplx::ZCsr();
+  A->n = n;
+  A->off.assign(off, off + n + 1);
+  A->col.assign(col, col + off[n]);
+  A->val.resize(static_cast<size_t>(off[n]));
+  for (int64_t p = 0; p < off[n]; ++p) A->val[static_cast<size_t>(p)] = {val[2 * p], val[2 * p + 1]};
+  return A;
+}
+void orc_zcsr_free(void* h) { delete static_cast<cplx::ZCsr*>(h); }
+void orc_zcsr_apply(void* h, const double* x, double* y) {
+  const auto* A = static_cast<cplx::ZCsr*>(h);
+  A->apply(reinterpret_cast<const cplx::Z*>(x), reinterpret_cast<cplx::Z*>(y));
+}
+void* orc_zspace_create() { return new cplx::RecycleSpace(); }
+void orc_zspace_free(void* h) { delete static_cast<cplx::RecycleSpace*>(h); }
+int64_t orc_zspace_dim(void* h) { return static_cast<cplx::RecycleSpace*>(h)->dim(); }
+/// U (n x k), SU / SAU (s x k), column-major interleaved complex.
+void orc_zspace_get(void* h, double* U, double* SU, double* SAU) {
+  const auto* sp = static_cast<cplx::RecycleSpace*>(h);
+  std::memcpy(U, sp->U.a.data(), sizeof(cplx::Z) * sp->U.a.size());
+  std::memcpy(SU, sp->SU.a.data(), sizeof(cplx::Z) * sp->SU.a.size());
+  std::memcpy(SAU, sp->SAU.a.data(), sizeof(cplx::Z) * sp->SAU.a.size());
+}
+void orc_zspace_set(void* h, int64_t n, int64_t s, int64_t k, const double* U, const double* SU, const double* SAU) {
+  auto* sp = static_cast<cplx::RecycleSpace*>(h);
+  sp->U = cplx::ZMat(n, k);
+  sp->SU = cplx::ZMat(s, k);
+  sp->SAU = cplx::ZMat(s, k);
+  std::memcpy(sp->U.a.data(), U, sizeof(cplx::Z) * n * k);
+  std::memcpy(sp->SU.a.data(), SU, sizeof(cplx::Z) * s * k);
+  std::memcpy(sp->SAU.a.data(), SAU, sizeof(cplx::Z) * s * k);
+}
+void* orc_zsolve(void* A, const double* b, const orc_config* c, void* space, void* sketch, double* x_out) {
+  SolveReport* rep = nullptr;
+  guard([&] {
+    const auto& M = *static_cast<cplx::ZCsr*>(A);
+    cplx::ZVec bb(reinterpret_cast<const cplx::Z*>(b), reinterpret_cast<const cplx::Z*>(b) + M.n);
+    cplx::RecycleSpace tmp;
+    cplx::RecycleSpace& sp = space ? *static_cast<cplx::RecycleSpace*>(space) : tmp;
+    auto r = cplx::solve(M, bb, to_cfg(c), sp, *static_cast<SketchOperator*>(sketch));
+    std::memcpy(x_out, r.x.data(), sizeof(cplx::Z) * r.x.size());
+    rep = new SolveReport(std::move(r.report));
+  });
+  return rep;
+}
+int orc_zrefresh(void* space, void* A, void* sketch, int64_t* counters3) {
+  return guard([&] {
+    Counters cn;
+    cplx::refresh_exact(*static_cast<cplx::RecycleSpace*>(space), *static_cast<cplx::ZCsr*>(A),
+                        *static_cast<SketchOperator*>(sketch), cn);
+    counters3[0] = cn.matvecs;
+    counters3[1] = cn.inner_products;
+    counters3[2] = cn.sketch_applies;
+  });
+}
 }

@@ -86,6 +86,13 @@ def lib():
             "orc_krylov_get": (None, [vp, C.c_int, P(f64)]),
             "orc_krylov_free": (None, [vp]),
             "orc_step_sample": (i64, [vp, P(f64), i64, vp, i64, i64, P(f64), P(f64)]),
+            "orc_zcsr_create": (vp, [i64, P(i64), P(i64), P(f64)]), "orc_zcsr_free": (None, [vp]),
+            "orc_zcsr_apply": (None, [vp, P(f64), P(f64)]),
+            "orc_zspace_create": (vp, []), "orc_zspace_free": (None, [vp]), "orc_zspace_dim": (i64, [vp]),
+            "orc_zspace_get": (None, [vp, P(f64), P(f64), P(f64)]),
+            "orc_zspace_set": (None, [vp, i64, i64, i64, P(f64), P(f64), P(f64)]),
+            "orc_zsolve": (vp, [vp, P(f64), P(orc_config), vp, vp, P(f64)]),
+            "orc_zrefresh": (C.c_int, [vp, vp, vp, P(i64)]),
             "orc_solve_callable": (vp, [i64, i64, ORC_APPLY, vp, P(f64), i64, P(orc_config), vp, vp, P(f64)]),
             "orc_harmonic": (C.c_int, [P(f64), P(f64), i64, i64, i64, f64, P(i64), P(i64), P(i32),
                                        P(f64), P(f64), P(f64), P(f64)]),
@@ -536,6 +543,76 @@ def solve_callable(rows, cols, apply, b, cfg: SolverConfig, space: RecycleSpace 
     c = cfg.c()
     h = lib().orc_solve_callable(rows, cols, fn, None, pb, len(b), C.byref(c), space._h if space else None,
                                  sketch._h if sketch else None, _f64(x)[1])
+    if not h:
+        raise ValueError(_err())
+    return x, _report(h)
+
+
+class ZSparseMatrix:
+    """Complex CSR for the complex GMRES-SDR oracle (skrylov_oracle_complex.hpp)."""
+
+    def __init__(self, n, offsets, columns, values):
+        self.n = n
+        off, po = _i64(np.asarray(offsets))
+        col, pc = _i64(np.asarray(columns))
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.complex128)).view(np.float64)
+        self._keep = (off, col, v)
+        self._h = lib().orc_zcsr_create(n, po, pc, v.ctypes.data_as(C.POINTER(C.c_double)))
+
+    def apply(self, x):
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        y = np.empty(self.n, dtype=np.complex128)
+        lib().orc_zcsr_apply(self._h, x.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
+                             y.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)))
+        return y
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_zcsr_free(self._h)
+            self._h = None
+
+
+class ZRecycleSpace:
+    def __init__(self):
+        self._h = lib().orc_zspace_create()
+
+    @property
+    def dim(self):
+        return lib().orc_zspace_dim(self._h)
+
+    def get(self, n, s):
+        k = self.dim
+        U = np.empty((k, n), dtype=np.complex128)
+        SU = np.empty((k, s), dtype=np.complex128)
+        SAU = np.empty((k, s), dtype=np.complex128)
+        dp = lambda a: a.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        lib().orc_zspace_set  # noqa: B018
+        lib().orc_zspace_get(self._h, dp(U), dp(SU), dp(SAU))
+        return U.T, SU.T, SAU.T
+
+    def set(self, U, SU, SAU):
+        U, SU, SAU = (np.ascontiguousarray(np.asarray(a, dtype=np.complex128).T) for a in (U, SU, SAU))
+        dp = lambda a: a.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        lib().orc_zspace_set(self._h, U.shape[1], SU.shape[1], U.shape[0], dp(U), dp(SU), dp(SAU))
+
+    def refresh(self, A: ZSparseMatrix, S: SketchOperator):
+        cnt = np.zeros(3, dtype=np.int64)
+        _raise(lib().orc_zrefresh(self._h, A._h, S._h, _i64(cnt)[1]))
+        return dict(matvecs=int(cnt[0]), inner_products=int(cnt[1]), sketch_applies=int(cnt[2]))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_zspace_free(self._h)
+            self._h = None
+
+
+def zsolve(A: ZSparseMatrix, b, cfg: SolverConfig, sketch: SketchOperator, space: ZRecycleSpace | None = None):
+    """Complex GMRES-SDR (skrylov_oracle_complex.hpp); b complex. Returns (x, report)."""
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    x = np.empty_like(b)
+    c = cfg.c()
+    dp = lambda a: a.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    h = lib().orc_zsolve(A._h, dp(b), C.byref(c), space._h if space else None, sketch._h, dp(x))
     if not h:
         raise ValueError(_err())
     return x, _report(h)

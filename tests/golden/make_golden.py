@@ -76,8 +76,55 @@ def c3_first():
     return summary(x, rep, dict(config=dict(n=n, m=50, k=20, t=2, s=140, tol=1e-8, variant="exact")))
 
 
+def c4_complex():
+    """BASELINE C4 with complex GMRES-SDR (oracle/skrylov_oracle_complex.hpp;
+    parity unpinned against the reference, which has no complex solver): the
+    full 32^3 x 64 lattice, m0 = -0.8, theta seed 2, b = gaussian_vector(2N, 4)
+    as (re, im) pairs, m=80 k=20 t=3 s=200 tol=1e-8, SRDCT(N, 200, 0x5eed) on
+    Re / Im; then the 10-system sequence m0 += 0.01 with the recycle space
+    carried and refreshed exactly (SAU = S A_i U). Also the realified solve's
+    counts on a reduced lattice for comparison (tools/c4_problem.py)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from tools.c4_problem import c4_complex_csr, c4_csr
+    dims = (32, 32, 32, 64)
+    N = int(np.prod(dims))
+    g = O.gaussian_vector(2 * N, 4)
+    b = g[0::2] + 1j * g[1::2]
+    S = O.SketchOperator.subsampled_dct(N, 200, 0x5EED)
+    kw = dict(m=80, k=20, t=3, s=200, tol=1e-8, max_restarts=40)
+    out = {"config": dict(dims=list(dims), m0=-0.8, **kw), "sequence": []}
+    space = O.ZRecycleSpace()
+    for i in range(10):
+        off, col, val = c4_complex_csr(dims, m0=-0.8 + 0.01 * i, seed=2, uniform=O.uniform_stream)
+        A = O.ZSparseMatrix(N, off, col, val)
+        del off, col, val
+        ref = space.refresh(A, S) if i > 0 and space.dim > 0 else dict(matvecs=0, inner_products=0, sketch_applies=0)
+        x, rep = O.zsolve(A, b, O.SolverConfig(**kw), S, space=space)
+        d = dict(status=rep.status, iterations=rep.iterations, cycles=rep.cycles,
+                 final_relative_residual=rep.final_relative_residual, counters=rep.counters, refresh=ref,
+                 true_residuals=rep.true_residuals, x_norm=float(np.linalg.norm(x)))
+        if i == 0:
+            out["single"] = d
+        out["sequence"].append(d)
+        print(f"  c4 system {i}: {rep.status} {rep.iterations} it", flush=True)
+    small = {}
+    for sd in [(4, 4, 4, 8), (8, 8, 8, 16), (16, 16, 16, 32)]:
+        n = int(np.prod(sd))
+        oc, cc, vc = c4_complex_csr(sd, -0.8, 2, O.uniform_stream)
+        gz = O.gaussian_vector(2 * n, 4)
+        xz, rz = O.zsolve(O.ZSparseMatrix(n, oc, cc, vc), gz[0::2] + 1j * gz[1::2], O.SolverConfig(**kw),
+                          O.SketchOperator.subsampled_dct(n, 200, 0x5EED))
+        orr, cr, vr = c4_csr(sd, -0.8, 2, O.uniform_stream)
+        xr, rr = O.solve(O.SparseMatrix.from_csr(2 * n, 2 * n, orr, cr, vr), gz, O.SolverConfig(**kw),
+                         sketch=O.SketchOperator.subsampled_dct(2 * n, 200, 0x5EED))
+        small["x".join(map(str, sd))] = dict(complex=dict(status=rz.status, iterations=rz.iterations),
+                                             realified=dict(status=rr.status, iterations=rr.iterations))
+    out["complex_vs_realified"] = small
+    return out
+
+
 def main(which):
-    jobs = {"c1": c1, "c2": c2, "c3_small": c3_small, "c3_first": c3_first}
+    jobs = {"c1": c1, "c2": c2, "c3_small": c3_small, "c3_first": c3_first, "c4_complex": c4_complex}
     for name in which:
         t0 = time.time()
         data = jobs[name]()

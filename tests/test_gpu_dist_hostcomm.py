@@ -11,7 +11,6 @@ every collective here completes on the host between kernels.
 The result must equal the one-rank solve: same status, iterations within
 ±2 %, x within 1e-9 relative."""
 import os
-import socket
 import subprocess
 import sys
 
@@ -24,20 +23,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_two_ranks_match_one_rank(sk, tmp_path, case):
-    port = _free_port()
     out = str(tmp_path / case)
     procs = []
     for r in range(2):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
-                   LOCAL_RANK="0")
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK="0")
         procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "workers", "dist_hostcomm_worker.py"),
                                        case, out], env=env, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
     logs = []

@@ -7,7 +7,7 @@ with the host-staged transport (sdr_ctx_create_hostcomm over gloo): the two
 ranks share one GPU, so no kernel ever waits on the other rank's kernels —
 every collective completes on the host. Writes x (this rank's rows) and the
 report to <out>.rank<r>.npz.
-usage: RANK=r WORLD_SIZE=2 MASTER_ADDR=127.0.0.1 MASTER_PORT=p python dist_hostcomm_worker.py <case> <out>"""
+usage: RANK=r WORLD_SIZE=2 python dist_hostcomm_worker.py <case> <out>"""
 import os
 import sys
 
@@ -22,7 +22,8 @@ from tests.workers.dist_cases import CASES, build  # noqa: E402
 def main():
     case, out = sys.argv[1], sys.argv[2]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rendezvous through a file next to the outputs (no TCP port to collide on)
+    dist.init_process_group("gloo", init_method=f"file://{out}.store", rank=rank, world_size=world)
     ctx = sk.Context(0, rank, world, host_comm=sk.torch_host_comm())
     A, b, S, cfg = build(sk, CASES[case], ctx, rank, world)
     r = sk.solve(A, b, cfg, sketch=S)

@@ -53,3 +53,31 @@ def c4_csr(dims=(32, 32, 32, 64), m0=-0.8, seed=2, uniform=None):
     counts = keep.sum(axis=1)
     offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     return offsets, cols[keep].astype(np.int64), vals[keep]
+
+
+def c4_complex_csr(dims=(32, 32, 32, 64), m0=-0.8, seed=2, uniform=None):
+    """(offsets, columns, values) of the complex operator itself (complex128
+    values, columns sorted per row): the input of complex GMRES-SDR
+    (sdr_csr_create_complex / SparseMatrix.from_complex)."""
+    X, Y, Z, T = dims
+    N = X * Y * Z * T
+    p = np.arange(N, dtype=np.int64)
+    x, y, z, t = p % X, (p // X) % Y, (p // (X * Y)) % Z, p // (X * Y * Z)
+    strides = (1, X, X * Y, X * Y * Z)
+    coords = (x, y, z, t)
+    sizes = (X, Y, Z, T)
+    nbr = []
+    for d in range(4):
+        for sgn in (1, -1):
+            c = (coords[d] + sgn) % sizes[d]
+            nbr.append(p + (c - coords[d]) * strides[d])
+    nbr = np.stack(nbr, axis=1)
+    theta = 2.0 * np.pi * uniform(seed, 8 * N).reshape(N, 8)
+    cv = -0.5 * np.exp(1j * theta)
+    ccols = np.concatenate([p[:, None], nbr], axis=1)
+    cvals = np.concatenate([np.full((N, 1), 4.0 + m0, dtype=np.complex128), cv], axis=1)
+    order = np.argsort(ccols, axis=1, kind="stable")
+    ccols = np.take_along_axis(ccols, order, axis=1)
+    cvals = np.take_along_axis(cvals, order, axis=1)
+    offsets = np.arange(0, 9 * N + 1, 9, dtype=np.int64)
+    return offsets, ccols.reshape(-1), cvals.reshape(-1)
