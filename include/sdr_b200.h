@@ -247,7 +247,10 @@ typedef enum {
   SDR_PROV_INEXACT_CARRYOVER = 4
 } sdr_provenance;
 
-/* SolverConfig (solver.hpp:48-79); sdr_config_default fills the reference defaults. */
+/* SolverConfig (solver.hpp:48-79); sdr_config_default fills the reference defaults.
+ * Validation is the reference's plus one device limit: the Arnoldi window
+ * min(t, m) must not exceed 33 (the fused MGS kernels hold it in registers;
+ * the reference accepts any t >= 1) — rejected with SDR_EINVAL. */
 typedef struct {
   int64_t m, t, k, s;
   double tol, safety_init;

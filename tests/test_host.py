@@ -281,3 +281,11 @@ def test_gen_neumann_matches_oracle(sk, O, g, shift):
     assert np.all(sums == 0.0)
     with pytest.raises(ValueError):
         sk.gen_neumann(1, 0.0)
+
+
+def test_config_window_device_limit(sk):
+    """The reference accepts any t >= 1; the device rejects windows above 33
+    with a clear SDR_EINVAL (documented in include/sdr_b200.h)."""
+    sk.SolverConfig(m=100, t=33, k=20, s=240, tol=1e-8).validate()
+    with pytest.raises(ValueError, match="device limit of 33"):
+        sk.SolverConfig(m=100, t=100, k=20, s=240, tol=1e-8).validate()
