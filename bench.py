@@ -260,6 +260,11 @@ def main():
     # NCCL communicator): a check of the torchrun / NCCL plumbing on one GPU
     if world > 1 or os.environ.get("SDR_BENCH_DIST") == "1":
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # SDR_BENCH_DIST=1 without a launcher: a one-rank group
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1")
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(so.getsockname()[1])
         dist.init_process_group("gloo", init_method="env://")
         idbuf = [sk.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(idbuf, src=0)

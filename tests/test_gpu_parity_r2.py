@@ -176,3 +176,29 @@ def test_c3_full_sequence_reduced_grid_matches_oracle(sk, O):
     total_g = sum(r.iterations for r in res.reports)
     total_o = sum(r.iterations for r in reps)
     assert abs(total_g - total_o) <= 0.02 * total_o, (total_g, total_o)
+
+
+@pytest.mark.parametrize("N,s", [(1, 16), (7, 16), (255, 100), (257, 100), (1000, 117), (4099, 120)])
+def test_fused_sparse_sign_small_and_ragged(sk, O, N, s):
+    """The fused update + sparse-sign kernel on tiny and ragged lengths (single
+    partial tile, odd tails, s not a multiple of ζ: blocks of unequal size)."""
+    # a random 5-band operator (diagonally dominant), any length
+    rows, cols = [], []
+    for d in (-7, -1, 0, 1, 3):
+        r = np.arange(max(0, -d), min(N, N - d))
+        rows.append(r)
+        cols.append(r + d)
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    v = O.gaussian_vector(len(r), 9) + np.where(r == c, 6.0, 0.0)
+    A = sk.SparseMatrix.from_triplets(N, N, r, c, v)
+    Ao = O.SparseMatrix.from_triplets(N, N, r, c, v)
+    S, So = sk.SketchOperator.sparse_sign(N, s, 0x5EED, 8), O.SketchOperator.sparse_sign(N, s, 0x5EED, 8)
+    r0 = O.gaussian_vector(N, 4)
+    steps = min(6, N)
+    g = krylov(sk, A, S, r0, 2, steps)
+    o = O.run_arnoldi(Ao, r0, So, 2, steps)
+    assert g["j"] == o.j and g["breakdown"] == o.breakdown
+    assert g["counters"] == tuple(o.counters)
+    assert rel(g["SV"], o.SV) <= 1e-12
+    assert rel(g["SAV"], o.SAV) <= 1e-11
