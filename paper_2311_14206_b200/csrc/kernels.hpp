@@ -114,7 +114,7 @@ void launch_rgemm(Context& c, const double* A1, int64_t lda1, int k1, const doub
                   const double* B, int nout, double* C, int64_t ldc, int64_t n, double* norms2,
                   double* scratch = nullptr);
 /// Same product on a bulk-copy ring with fp64 tensor-core accumulation
-/// (tsmm.cu), outputs through a pointer list (out[o], n rows each; up to 24),
+/// (tsmm.cu), outputs through a pointer list (out[o], n rows each; up to 40),
 /// so one pass can write the correction and the new recycle columns.
 bool tsmm_supported(int nout, int k, int64_t n, int64_t lda1, int64_t lda2);
 int64_t tsmm_scratch_size(int num_sms);

@@ -1030,7 +1030,7 @@ bool fuse_restart_wanted(const Context& c, const Workspace& w, i64 kh, i64 j) {
 bool launch_fused_restart(Context& c, Workspace& w, const HostKrylov& st, int vb, Recycle& sp, const Harmonic& hp,
                           const std::vector<double>& y, double* corr_own) {
   const i64 j = st.j, kh = sp.dim(), ke = hp.k_eff, nloc = w.lay.nloc;
-  if (ke + 1 > 24 || j < 1) return false;
+  if (ke + 1 > 40 || j < 1) return false;
   sp.ensure(nloc, std::max<i64>(ke, kh));
   i64 kc = 0;
   std::vector<char> used(static_cast<size_t>(std::max<i64>(sp.cap, 1)), 0);

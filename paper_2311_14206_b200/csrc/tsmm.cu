@@ -30,7 +30,7 @@ constexpr int kTmLd = kTmRows + 8;       // padded column stride in shared memor
 constexpr int kTmStages = 4;
 constexpr int kTmConsumers = 8;
 constexpr int kTmThreads = 32 * (1 + kTmConsumers);
-constexpr int kTmMaxOut = 24;
+constexpr int kTmMaxOut = 40;
 
 struct TsmmArgs {
   const double* A1;
@@ -202,7 +202,7 @@ void tsmm_impl(Context& c, TsmmArgs a, double* norms2, double* scratch) {
 int64_t tsmm_scratch_size(int num_sms) { return static_cast<int64_t>(kTmMaxOut) * num_sms * 4; }
 
 bool tsmm_supported(int nout, int k, int64_t n, int64_t lda1, int64_t lda2) {
-  const int NO = nout <= 8 ? 8 : (nout <= 16 ? 16 : 24);
+  const int NO = nout <= 8 ? 8 : (nout <= 16 ? 16 : (nout <= 24 ? 24 : 40));
   return nout >= 1 && nout <= kTmMaxOut && k >= 1 && n % 2 == 0 && lda1 % 2 == 0 && lda2 % 2 == 0 &&
          tsmm_smem(k, NO) <= 200 * 1024;
 }
@@ -225,8 +225,10 @@ void launch_tsmm(Context& c, const double* A1, int64_t lda1, int k1, const doubl
     tsmm_impl<8>(c, a, norms2, scratch);
   else if (nout <= 16)
     tsmm_impl<16>(c, a, norms2, scratch);
-  else
+  else if (nout <= 24)
     tsmm_impl<24>(c, a, norms2, scratch);
+  else
+    tsmm_impl<40>(c, a, norms2, scratch);
 }
 
 }  // namespace sdr
