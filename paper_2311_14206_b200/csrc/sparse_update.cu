@@ -7,10 +7,10 @@
 // (the separate sketch re-read w_{j+1} and was issue-bound at 0.15 of HBM).
 //
 // Data movement: a producer warp streams y = A w_j and the window columns
-// w_{j-d} tile by tile (256 rows) into a 3-stage shared-memory ring with
+// w_{j-d} tile by tile (512 rows) into a 2-stage shared-memory ring with
 // bulk-async copies (cp.async.bulk, mbarrier transaction counts), so the
 // bytes in flight do not depend on how many warps are resident — the
-// sketch's lane-private bins (s x 32 doubles per CTA) cap residency at five
+// sketch's lane-private bins (s x 32 doubles per CTA) cap residency at four
 // CTAs per SM. (Measured alternative, slower: no producer warp, the second
 // consumer to release a stage issuing its refill — 1.17 vs 1.11 ms at C5.)
 // Consumer warp c (0, 1) evaluates chunk hash h_c of its lanes' rows
@@ -33,8 +33,12 @@ namespace sdr {
 
 namespace {
 
-constexpr int kTileRows = 256;  // rows per ring stage (2 KB per vector)
-constexpr int kStages = 3;
+// rows per ring stage (4 KB per vector) and stages: C5 sweep (t = 2, isolated,
+// us per launch): 256/3 1108, 256/2 1209, 256/4 1110, 128/4 1356, 128/6 1272,
+// 512/2 1006, 512/3 1252, 768/2 1203, 1024/2 2165 — larger tiles halve the
+// per-tile bookkeeping, more stages cost a resident CTA per SM
+constexpr int kTileRows = 512;
+constexpr int kStages = 2;
 constexpr int kConsumers = 2;  // one warp per 4-entry hash chunk (ζ = 8)
 constexpr int kThreadsUS = 32 * (1 + kConsumers);  // producer + consumers
 
@@ -59,23 +63,23 @@ struct UpdSparseArgs {
 
 /// NW = nwin window columns, NG = ngram Gram entries (compile time: the
 /// per-row code has no window predicates).
-template <int NW, int NG>
+template <int NW, int NG, int TR = kTileRows, int NS = kStages>
 __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
   __shared__ double coef[NW + 1];
   stamp_begin(a.stamp);
   const int s = a.s;
   double* bins = smem;                                 // [s][32]
-  double* ring = smem + static_cast<int64_t>(s) * 32;  // [stage][1 + NW][kTileRows]
+  double* ring = smem + static_cast<int64_t>(s) * 32;  // [stage][1 + NW][TR]
   constexpr int kNvec = 1 + NW;
-  constexpr int kStageElems = kNvec * kTileRows;
-  constexpr int kRowsPerLane = kTileRows / 32;
+  constexpr int kStageElems = kNvec * TR;
+  constexpr int kRowsPerLane = TR / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   for (int i = threadIdx.x; i < s * 32; i += blockDim.x) bins[i] = 0.0;
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kStages; ++q) {
+    for (int q = 0; q < NS; ++q) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], kConsumers);
     }
@@ -98,8 +102,8 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
   // Bulk copy of tile t into ring stage st (one thread): y and the window
   // columns, a 16-byte multiple (an odd last row of the vector is read directly).
   auto feed = [&](int64_t t, int st) {
-    const int64_t r0 = t * kTileRows;
-    const int64_t rows = min(static_cast<int64_t>(kTileRows), a.n - r0);
+    const int64_t r0 = t * TR;
+    const int64_t rows = min(static_cast<int64_t>(TR), a.n - r0);
     const uint32_t bytes = static_cast<uint32_t>((rows & ~int64_t{1}) * 8);
     double* dst = ring + st * kStageElems;
     mbar_arrive_expect_tx(&full[st], bytes * kNvec);
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
       bulk_g2s(dst, a.y + r0, bytes, &full[st]);
 #pragma unroll
       for (int d = 0; d < NW; ++d)
-        bulk_g2s(dst + (1 + d) * kTileRows, a.V + static_cast<int64_t>(a.j - d) * a.ldv + a.own_off + r0, bytes,
+        bulk_g2s(dst + (1 + d) * TR, a.V + static_cast<int64_t>(a.j - d) * a.ldv + a.own_off + r0, bytes,
                  &full[st]);
     }
   };
@@ -116,10 +120,10 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
     int st = 0;
     uint32_t ph = 0;
     for (int64_t t = t0; t < t1; ++t) {
-      if (t - t0 >= kStages) mbar_wait_sleep(&empty[st], ph ^ 1u);
+      if (t - t0 >= NS) mbar_wait_sleep(&empty[st], ph ^ 1u);
       if (lane == 0) feed(t, st);
       __syncwarp();
-      if (++st == kStages) st = 0, ph ^= 1u;
+      if (++st == NS) st = 0, ph ^= 1u;
     }
   } else {
     // ---- consumers
@@ -142,8 +146,8 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
     uint32_t ph = 0;
     for (int64_t t = t0; t < t1; ++t) {
       const double* ys = ring + st * kStageElems + lane;
-      const int64_t r0 = t * kTileRows;
-      const int rows = static_cast<int>(min(static_cast<int64_t>(kTileRows), a.n - r0));
+      const int64_t r0 = t * TR;
+      const int rows = static_cast<int>(min(static_cast<int64_t>(TR), a.n - r0));
       const uint64_t arg0 =
           a.key + (static_cast<uint64_t>(a.row_begin + r0 + lane) * 2u + static_cast<uint64_t>(c) + 1u) * kPhi64;
       uint64_t h[kRowsPerLane];
@@ -151,12 +155,12 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
       for (int u = 0; u < kRowsPerLane; ++u) h[u] = mix64(arg0 + u * d_row);
       mbar_wait(&full[st], ph);
       double w[kRowsPerLane];
-      if (rows == kTileRows) {  // full tile: no bounds checks
+      if (rows == TR) {  // full tile: no bounds checks
 #pragma unroll
         for (int u = 0; u < kRowsPerLane; ++u) {
           double wv[NW];
 #pragma unroll
-          for (int d = 0; d < NW; ++d) wv[d] = ys[(1 + d) * kTileRows + 32 * u];
+          for (int d = 0; d < NW; ++d) wv[d] = ys[(1 + d) * TR + 32 * u];
           double x = cf[0] * ys[32 * u];
 #pragma unroll
           for (int d = NW - 1; d >= 0; --d) x = fma(cf[1 + d], wv[d], x);
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
           if (r < even) {
             yv = ys[32 * u];
 #pragma unroll
-            for (int d = 0; d < NW; ++d) wv[d] = ys[(1 + d) * kTileRows + 32 * u];
+            for (int d = 0; d < NW; ++d) wv[d] = ys[(1 + d) * TR + 32 * u];
           } else if (r < rows) {  // odd last row of the vector: not in the bulk copy
             yv = a.y[r0 + r];
 #pragma unroll
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
       // the stage's inputs are in registers now: release it to the producer
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
-      if (++st == kStages) st = 0, ph ^= 1u;
+      if (++st == NS) st = 0, ph ^= 1u;
 #pragma unroll
       for (int u = 0; u < kRowsPerLane; ++u) {
         const int whi = __double2hiint(w[u]), wlo = __double2loint(w[u]);
@@ -235,16 +239,17 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
   stamp_end(a.stamp);
 }
 
-size_t upd_sparse_smem(int s, int nwin) {
-  return sizeof(double) * (static_cast<size_t>(s) * 32 + static_cast<size_t>(kStages) * (1 + nwin) * kTileRows);
+size_t upd_sparse_smem(int s, int nwin, int tr = kTileRows, int ns = kStages) {
+  return sizeof(double) * (static_cast<size_t>(s) * 32 + static_cast<size_t>(ns) * (1 + nwin) * tr);
 }
 
-template <int NW, int NG>
+template <int NW, int NG, int TR = kTileRows, int NS = kStages>
 void upd_sparse_impl(Context& c, const SketchDev& S, UpdSparseArgs a, const RecLayout& RL, double* out) {
-  auto kern = k_update_sparse8<NW, NG>;
-  const size_t smem = upd_sparse_smem(static_cast<int>(S.s), NW);
+  auto kern = k_update_sparse8<NW, NG, TR, NS>;
+  const size_t smem = upd_sparse_smem(static_cast<int>(S.s), NW, TR, NS);
   ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   const int per_sm = std::max(1, blocks_per_sm(reinterpret_cast<const void*>(kern), kThreadsUS, smem));
+  a.ntiles = (a.n + TR - 1) / TR;
   const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(a.ntiles, static_cast<int64_t>(c.num_sms) * per_sm)));
   a.ng_partials = c.partials(4 * static_cast<int64_t>(g));
   a.sk_partials = c.partials2(static_cast<int64_t>(g) * S.s);
@@ -262,7 +267,8 @@ template <int NW>
 void upd_sparse_ng(Context& c, const SketchDev& S, const UpdSparseArgs& a, const RecLayout& RL, double* out) {
   switch (a.ngram) {
     case 0: return upd_sparse_impl<NW, 0>(c, S, a, RL, out);
-    case 1: return upd_sparse_impl<NW, (NW >= 1 ? 1 : 0)>(c, S, a, RL, out);
+    case 1:
+      return upd_sparse_impl<NW, (NW >= 1 ? 1 : 0)>(c, S, a, RL, out);
     case 2: return upd_sparse_impl<NW, (NW >= 2 ? 2 : 0)>(c, S, a, RL, out);
     default: return upd_sparse_impl<NW, (NW >= 3 ? 3 : 0)>(c, S, a, RL, out);
   }
