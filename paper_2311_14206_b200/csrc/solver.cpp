@@ -944,7 +944,7 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
     for (i64 q = 0; q < ke; ++q) out.push_back(sp.buf[other].get() + q * sp.ld);
     tallskinny(c, w, in, coef, out, nloc, w.scal.get());
   }
-  if (!product_done) c.allreduce_sum(w.scal.get(), ke);
+  c.allreduce_sum(w.scal.get(), ke);  // (the fused pass's norms are this rank's partial sums too)
   SDR_CUDA(cudaMemcpyAsync(w.hscal.get(), w.scal.get(), sizeof(double) * ke, cudaMemcpyDeviceToHost, c.stream));
   SDR_CUDA(cudaEventRecord(w.ev_side_out, c.stream));
   if (side) {
@@ -1016,7 +1016,7 @@ bool fuse_restart_wanted(const Context& c, const Workspace& w, i64 kh, i64 j) {
     const char* e = std::getenv("SDR_FUSE_RESTART");
     return e ? std::atoi(e) : -1;
   }();
-  if (mode == 0 || c.distributed()) return false;
+  if (mode == 0) return false;
   if (mode == 1) return true;
   const double pass_ms = static_cast<double>(kh + j) * static_cast<double>(w.lay.nloc) * 8.0 / 5.0e9;
   const double p = static_cast<double>(kh + j);
