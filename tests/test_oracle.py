@@ -413,3 +413,57 @@ def test_baseline_edge_cases(O):
         O.baseline_gmres(I3, b, m=0)
     with pytest.raises(ValueError):
         O.baseline_gmres(I3, b, tol=1.0)
+
+
+def test_complex_oracle_identity_sketch_is_dense_complex_gmres(O):
+    """Pins the complex GMRES-SDR oracle (skrylov_oracle_complex.hpp; no
+    reference code exists for complex scalars): with the identity
+    sketch, full window and k = 0, every per-step sketched residual equals the
+    residual of dense complex GMRES on the same Krylov space (the complex
+    analogue of test_solver.cpp:38-81)."""
+    rng = np.random.default_rng(0)
+    n, m = 40, 12
+    M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + n * (1 + 0.5j) * np.eye(n)
+    A = O.ZSparseMatrix(n, np.arange(0, n * n + 1, n), np.tile(np.arange(n), n), M.reshape(-1))
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert np.abs(A.apply(x) - M @ x).max() <= 1e-12 * np.abs(M @ x).max()
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    cfg = O.SolverConfig(m=m, t=m, k=0, s=n, tol=1e-10, max_restarts=1)
+    xs, rep = O.zsolve(A, b, cfg, O.SketchOperator.identity(n))
+    K = np.column_stack([np.linalg.matrix_power(M, i) @ b for i in range(m)])
+    for it, sres in rep.sketched_residuals:
+        Q, _ = np.linalg.qr(K[:, :it])
+        y = np.linalg.lstsq(M @ Q, b, rcond=None)[0]
+        assert sres == pytest.approx(np.linalg.norm(b - M @ Q @ y), rel=1e-8)
+    assert rep.counters["matvecs"] == m + 1 and rep.counters["sketch_applies"] == m + 1
+
+
+def test_complex_oracle_recycling_and_counters(O):
+    """Complex GMRES-SDR with a real SRDCT sketch on Re / Im and a recycle
+    space carried to a second right-hand side: converges, the carried space
+    cuts iterations, an exact refresh costs k matvecs + k sketches."""
+    rng = np.random.default_rng(1)
+    n = 600
+    off, col, val = [0], [], []
+    for r in range(n):
+        for c, v in ((r - 1, -1.0 + 0.3j), (r, 4.0 + 0.5j), (r + 1, -1.2 - 0.2j), (r + 7, 0.4j)):
+            if 0 <= c < n:
+                col.append(c)
+                val.append(v)
+        off.append(len(col))
+    A = O.ZSparseMatrix(n, off, col, val)
+    S = O.SketchOperator.subsampled_dct(n, 60, 0x5EED)
+    cfg = O.SolverConfig(m=20, t=2, k=5, s=60, tol=1e-10, max_restarts=30)
+    sp = O.ZRecycleSpace()
+    b1 = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    x1, r1 = O.zsolve(A, b1, cfg, S, space=sp)
+    assert r1.status == "converged" and sp.dim == 5
+    dense = np.zeros((n, n), dtype=complex)
+    for r in range(n):
+        for p in range(off[r], off[r + 1]):
+            dense[r, col[p]] = val[p]
+    assert np.linalg.norm(dense @ x1 - b1) <= 1e-10 * np.linalg.norm(b1) * 1.01
+    cnt = sp.refresh(A, S)
+    assert cnt == dict(matvecs=5, inner_products=0, sketch_applies=5)
+    x2, r2 = O.zsolve(A, b1 + 0.01 * (rng.standard_normal(n) + 1j * rng.standard_normal(n)), cfg, S, space=sp)
+    assert r2.status == "converged" and r2.iterations < r1.iterations
