@@ -141,8 +141,6 @@ DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int6
   int64_t reach_lo_end = 0, reach_hi_begin = local_rows;  // see DeviceOperator::reach_lo_end
   const int64_t row_end = row_begin + local_rows;
   for (int64_t r = 0; r < local_rows; ++r) {
-    if (off[r + 1] > off[r] && col && col[off[r]] < row_begin) reach_lo_end = r + 1;
-    if (off[r + 1] > off[r] && col && col[off[r + 1] - 1] >= row_end && reach_hi_begin == local_rows) reach_hi_begin = r;
     if (off[r + 1] < off[r]) throw invalid("SparseMatrix: offsets decrease at row " + std::to_string(row_begin + r));
     for (int64_t p = off[r]; p < off[r + 1]; ++p) {
       const int64_t cc = col[p];
@@ -154,6 +152,8 @@ DeviceOperator* create_operator_csr(Context& c, int64_t rows, int64_t cols, int6
       if (!std::isfinite(val[p])) throw invalid("SparseMatrix: non-finite value in row " + std::to_string(row_begin + r));
       mnc = std::min(mnc, cc);
       mxc = std::max(mxc, cc);
+      if (cc < row_begin) reach_lo_end = r + 1;
+      if (cc >= row_end && reach_hi_begin == local_rows) reach_hi_begin = r;
     }
   }
   auto op = std::make_unique<DeviceOperator>();
