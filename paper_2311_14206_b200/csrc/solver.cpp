@@ -486,6 +486,17 @@ struct ArnoldiPipeline {
     deferred = !A.apply && (!c.distributed() || defer_dist) && fuse_update_sketch() &&
                update_sketch_eligible(S, w.lay, need, A.row_begin, w.lay.ld);
     split = deferred && !c.distributed() && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
+    if (!deferred && c.distributed() && !A.apply) {
+      // several ranks, non-deferred steps (sparse sign): K1's interior slices
+      // still run beside the halo transfer (enqueue)
+      w.p1.ensure(34 * static_cast<i64>(c.num_sms) * 8);
+      w.p1b.ensure(34 * static_cast<i64>(c.num_sms) * 8);
+      if (!w.halo_stream) {
+        SDR_CUDA(cudaStreamCreateWithFlags(&w.halo_stream, cudaStreamNonBlocking));
+        SDR_CUDA(cudaEventCreateWithFlags(&w.ev_w, cudaEventDisableTiming));
+        SDR_CUDA(cudaEventCreateWithFlags(&w.ev_halo, cudaEventDisableTiming));
+      }
+    }
     if (!deferred) return;
     w.p1.ensure(34 * static_cast<i64>(c.num_sms) * 8);
     for (auto& b : w.p2) b.ensure(update_sketch_partials_size(S, c.num_sms));
@@ -589,12 +600,31 @@ struct ArnoldiPipeline {
       if (j + 1 == m) flush(j);
       return;
     }
-    c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
     // one GPU: K1's last CTA forms the MGS coefficients; several: K2 forms
     // them after the allreduce of the window dots
     double* coef = c.distributed() ? nullptr : w.coef_dev.get();
-    launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
-                        w.rec.get(), R, T, w.cvec.get(), coef);
+    i64 b_lo = 0, b_hi = 0;
+    if (c.distributed() && !A.apply && w.halo_stream && k1_split_range(b_lo, b_hi)) {
+      // several ranks: the interior slices (no halo row in their stencils)
+      // run while the halo of w_j moves on its own stream, the boundary
+      // slices once it has landed; both leave CTA partials, folded into the
+      // record in a fixed order before the allreduce
+      SDR_CUDA(cudaEventRecord(w.ev_w, c.stream));
+      SDR_CUDA(cudaStreamWaitEvent(w.halo_stream, w.ev_w, 0));
+      c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin, w.halo_stream);
+      SDR_CUDA(cudaEventRecord(w.ev_halo, w.halo_stream));
+      const i64 ns = A.view().nslices;
+      const int g1 = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
+                                         w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1.get(), 0, b_lo, b_hi);
+      SDR_CUDA(cudaStreamWaitEvent(c.stream, w.ev_halo, 0));
+      const int g2 = launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), nullptr,
+                                         w.rec.get(), R, T, w.cvec.get(), nullptr, w.p1b.get(), 0, b_hi, ns + b_lo);
+      launch_fold_partials2(c, w.p1.get(), g1, w.p1b.get(), g2, 1 + nwin, recj + RL.a_off());
+    } else {
+      c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
+      launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
+                          w.rec.get(), R, T, w.cvec.get(), coef);
+    }
     c.allreduce_sum(recj + RL.a_off(), T + 1);
     if (update_sparse_eligible(S, lay, RL, std::max(nwin, ngram + 1), lay.ld)) {
       // sparse sign: update and sketch of w_{j+1} in one pass (sparse_update.cu)

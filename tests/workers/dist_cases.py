@@ -12,6 +12,8 @@ CASES = {
     # (non-uniform stencil reach: the K1 interior / boundary split must use
     # the per-row reach, not the halo width)
     "csr_reach": dict(kind="csr_reach", n=24, sketch="srdct", m=30, k=6, t=3, s=120, tol=1e-8),
+    # the same with sparse sign: the non-deferred step's interior / boundary K1 split
+    "csr_reach_sparse": dict(kind="csr_reach", n=24, sketch="sparse_sign", m=30, k=6, t=2, s=120, tol=1e-8),
 }
 
 
