@@ -1037,7 +1037,8 @@ void update_recycle(Context& c, Workspace& w, const HostKrylov& st, int vb, Recy
 }
 
 /// Restart boundary in one pass over [V U]: when the cycle's harmonic pencil
-/// is cheap next to a pass over the basis (C5: ~0.8 ms vs ~13 ms), the host
+/// is cheap next to a pass over the basis (C5: ~0.8 ms vs ~13 ms; chosen when
+/// the pass is estimated at 1.5x the pencil or more), the host
 /// forms it first and one tall-skinny kernel writes both the correction
 /// (solver.hpp:197-198) and U_new = [U V] P (recycle.hpp:257-265), reading
 /// the basis once instead of twice. SDR_FUSE_RESTART=0/1 forces it off/on.
@@ -1051,7 +1052,9 @@ bool fuse_restart_wanted(const Context& c, const Workspace& w, i64 kh, i64 j) {
   const double pass_ms = static_cast<double>(kh + j) * static_cast<double>(w.lay.nloc) * 8.0 / 5.0e9;
   const double p = static_cast<double>(kh + j);
   const double harm_ms = w.last_harmonic_ms >= 0.0 ? w.last_harmonic_ms : 2.5 * (p / 120.0) * (p / 120.0) * (p / 120.0);
-  return pass_ms > 4.0 * harm_ms;
+  // fused: the GPU waits for the pencil (harm_ms) and saves one read of the
+  // basis (~pass_ms); 1.5x margin for the estimates
+  return pass_ms > 1.5 * harm_ms;
 }
 
 /// Launches the fused pass (outputs: correction, then the k_eff new recycle
