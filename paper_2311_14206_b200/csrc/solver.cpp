@@ -412,6 +412,10 @@ struct ArnoldiPipeline {
   // completed by K2(j)'s prologue, so its copy follows K2(j); see StepFold
   bool deferred = false;
   bool split = false;  // deferred + SRDCT on the side stream (SplitFold)
+  // several ranks, non-deferred steps: K2(j)'s record part B (norm, Gram,
+  // sketch rows of w_{j+1}) is reduced together with K1(j+1)'s dots — one
+  // allreduce per step over the contiguous record span [B_{j+1} | A_{j+2}]
+  bool merge_b = false;
   StepFold last;  // partials K2(issued - 1) left
   i64 last_ngram = 0, last_j = -1;
   double* pend_buf = nullptr;  // several ranks: K2's folded partials not yet allreduced
@@ -486,6 +490,7 @@ struct ArnoldiPipeline {
     deferred = !A.apply && (!c.distributed() || defer_dist) && fuse_update_sketch() &&
                update_sketch_eligible(S, w.lay, need, A.row_begin, w.lay.ld);
     split = deferred && !c.distributed() && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
+    merge_b = !deferred && c.distributed();
     if (!deferred && c.distributed() && !A.apply) {
       // several ranks, non-deferred steps (sparse sign): K1's interior slices
       // still run beside the halo transfer (enqueue)
@@ -625,7 +630,15 @@ struct ArnoldiPipeline {
       launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.y.get(), recj + RL.a_off(),
                           w.rec.get(), R, T, w.cvec.get(), coef);
     }
-    c.allreduce_sum(recj + RL.a_off(), T + 1);
+    if (merge_b && j > 0) {
+      // row j's B part (left by K2(j-1)), its padding and row j+1's A part
+      // are contiguous: one allreduce, after which row j is complete
+      c.allreduce_sum(w.rec.get() + j * R + RL.b_off(), (R - RL.b_off()) + (T + 1));
+      w.copy_back(c, w.hrec.get() + j * R, w.rec.get() + j * R, R, w.evk[static_cast<size_t>(j)],
+                  w.ev[static_cast<size_t>(j)]);
+    } else {
+      c.allreduce_sum(recj + RL.a_off(), T + 1);
+    }
     if (update_sparse_eligible(S, lay, RL, std::max(nwin, ngram + 1), lay.ld)) {
       // sparse sign: update and sketch of w_{j+1} in one pass (sparse_update.cu)
       launch_update_sparse(c, S, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL,
@@ -636,6 +649,10 @@ struct ArnoldiPipeline {
       launch_update(c, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(),
                     coef);
       launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
+    }
+    if (merge_b && j + 1 < m) {  // reduced with K1(j+1)'s dots
+      SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
+      return;
     }
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
     SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
