@@ -32,6 +32,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <complex>
@@ -86,7 +88,42 @@ struct Mat {
   }
 };
 
+/// Host threads for the long loops (bench.py's all-cores CPU baseline):
+/// ORC_THREADS, default 1 — the reference is single-threaded, and with one
+/// thread every result is the plain sequential loop's (the parity tests).
+inline int threads() {
+  const char* e = std::getenv("ORC_THREADS");  // read per call: the bench switches it between samples
+  const int v = e ? std::atoi(e) : 1;
+  return v > 1 ? v : 1;
+}
+
+/// f(begin, end, thread) over [0, n) split into threads() contiguous ranges
+/// (plain std::thread: no OpenMP runtime next to the host process's own).
+template <class F>
+inline void parallel_ranges(Index n, F&& f) {
+  const int nt = threads();
+  if (nt == 1 || n < 100000) {
+    f(Index{0}, n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt, t); });
+  f(Index{0}, n / nt, 0);
+  for (auto& x : th) x.join();
+}
+
 inline double dot(const double* x, const double* y, Index n) {
+  if (threads() > 1 && n >= 100000) {  // per-range sums added in range order
+    std::vector<double> part(static_cast<size_t>(threads()), 0.0);
+    parallel_ranges(n, [&](Index b, Index e, int t) {
+      double s = 0.0;
+      for (Index i = b; i < e; ++i) s += x[i] * y[i];
+      part[static_cast<size_t>(t)] = s;
+    });
+    double s = 0.0;
+    for (double v : part) s += v;
+    return s;
+  }
   double s = 0.0;
   for (Index i = 0; i < n; ++i) s += x[i] * y[i];
   return s;
@@ -211,12 +248,14 @@ class SparseMatrix {
     if (xlen != cols_)
       throw std::invalid_argument("SparseMatrix::apply: matrix has " + std::to_string(cols_) +
                                   " columns but vector has " + std::to_string(xlen) + " entries");
-    for (Index r = 0; r < rows_; ++r) {
-      double acc = 0.0;
-      for (Index p = offsets_[static_cast<size_t>(r)]; p < offsets_[static_cast<size_t>(r) + 1]; ++p)
-        acc += values_[static_cast<size_t>(p)] * x[columns_[static_cast<size_t>(p)]];
-      y[r] = acc;
-    }
+    parallel_ranges(rows_, [&](Index rb, Index re, int) {  // rows are independent: same sums, any thread count
+      for (Index r = rb; r < re; ++r) {
+        double acc = 0.0;
+        for (Index p = offsets_[static_cast<size_t>(r)]; p < offsets_[static_cast<size_t>(r) + 1]; ++p)
+          acc += values_[static_cast<size_t>(p)] * x[columns_[static_cast<size_t>(p)]];
+        y[r] = acc;
+      }
+    });
   }
 
  private:
@@ -673,6 +712,39 @@ class SketchOperator {
         bs[static_cast<size_t>(l)] = ((l + 1) * s_) / zeta_ - b0[static_cast<size_t>(l)];
       }
       constexpr Index kChunk = 2048;
+      if (threads() > 1 && n_ > 100000) {
+        // several host threads (bench baseline only): contiguous column
+        // ranges into per-thread rows, added in thread order
+        const int nt = threads();
+        std::vector<Vec> part(static_cast<size_t>(nt), Vec(static_cast<size_t>(s_), 0.0));
+        parallel_ranges(n_, [&](Index jb, Index je, int tid) {
+          Vec& o = part[static_cast<size_t>(tid)];
+          for (Index j = jb; j < je; ++j) {
+            const double xv = x[j] * inv;
+            for (std::uint64_t c = 0; c < nc; ++c) {
+              const std::uint64_t h =
+                  detail::mix64(key_ + (static_cast<std::uint64_t>(j) * nc + c + 1u) * 0x9E3779B97F4A7C15ull);
+              for (Index e = 0; e < 4; ++e) {
+                const Index l = static_cast<Index>(4 * c) + e;
+                if (l >= zeta_) break;
+                const std::uint32_t f = static_cast<std::uint32_t>(h >> (16 * e)) & 0xFFFFu;
+                const Index r = b0[static_cast<size_t>(l)] +
+                                static_cast<Index>((static_cast<std::uint64_t>((f >> 1) & 0x7FFFu) *
+                                                    static_cast<std::uint64_t>(bs[static_cast<size_t>(l)])) >> 15);
+                std::uint64_t bits;
+                std::memcpy(&bits, &xv, sizeof(bits));
+                bits ^= static_cast<std::uint64_t>(~f & 1u) << 63;
+                double term;
+                std::memcpy(&term, &bits, sizeof(term));
+                o[static_cast<size_t>(r)] += term;
+              }
+            }
+          }
+        });
+        for (int t = 0; t < nt; ++t)
+          for (Index r = 0; r < s_; ++r) out[r] += part[static_cast<size_t>(t)][static_cast<size_t>(r)];
+        return;
+      }
       std::vector<std::uint64_t> hc(static_cast<size_t>(kChunk * nc));
       std::vector<std::uint64_t> xb(static_cast<size_t>(kChunk));
       for (Index j0 = 0; j0 < n_; j0 += kChunk) {
@@ -798,7 +870,9 @@ inline StepResult arnoldi_step(KrylovState& st, const OperatorRef& A, const Sket
     if (counters) ++counters->inner_products;
     st.H(i, j) = h;
     const double* vi = st.V.col(i);
-    for (Index r = 0; r < n; ++r) w[static_cast<size_t>(r)] -= h * vi[r];
+    parallel_ranges(n, [&](Index rb, Index re, int) {
+      for (Index r = rb; r < re; ++r) w[static_cast<size_t>(r)] -= h * vi[r];
+    });
   }
   const double h_next = norm(w);
   if (counters) ++counters->inner_products;
@@ -819,7 +893,9 @@ inline StepResult arnoldi_step(KrylovState& st, const OperatorRef& A, const Sket
     return res;
   }
   st.H(j + 1, j) = h_next;
-  for (Index r = 0; r < n; ++r) st.V(r, j + 1) = w[static_cast<size_t>(r)] / h_next;
+  parallel_ranges(n, [&](Index rb, Index re, int) {
+    for (Index r = rb; r < re; ++r) st.V(r, j + 1) = w[static_cast<size_t>(r)] / h_next;
+  });
   Vec sv(static_cast<size_t>(s));
   S.apply(st.V.col(j + 1), n, sv.data());
   if (counters) ++counters->sketch_applies;
