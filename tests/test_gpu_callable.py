@@ -92,3 +92,33 @@ def test_callable_errors(sk, O):
     R = sk.SparseMatrix.from_callable(N, N + 1, ok)
     with pytest.raises(ValueError, match="square"):
         sk.solve(R, np.ones(N), sk.SolverConfig(m=10, k=2, t=2, s=24, tol=1e-6))
+
+
+def test_callable_sequence_equals_csr_sequence(sk, O):
+    """solve_sequence over callable operators (recycle.hpp:297-318 exact
+    refresh applies A to the carried U through the callback, column by
+    column) reproduces the stored-CSR sequence: same status, iterations,
+    counters and solutions per system."""
+    n, count = 12, 4
+    N = n ** 3
+    mats, calls = [], []
+    for i in range(count):
+        off, col, val = sk.gen_convdiff3d(n, 100.0 + 10.0 * i, 50.0, 25.0)
+        A = sk.SparseMatrix(N, N, off, col, val)
+        mats.append(A)
+
+        def apply(x, y, stream, A=A):
+            sk._check(sk._lib.sdr_spmv(A.ctx._h, A._h, C.c_void_p(x.ptr), N, C.c_void_p(y.ptr)))
+
+        calls.append(sk.SparseMatrix.from_callable(N, N, apply))
+    rhs = [O.gaussian_vector(N, 20 + i) for i in range(count)]
+    cfg = sk.SolverConfig(m=30, k=8, t=2, s=80, tol=1e-8, max_restarts=30, variant="exact")
+    S = sk.SketchOperator.subsampled_dct(N, 80, 0x5EED)
+    g = sk.solve_sequence([sk.ProblemInstance(A, b, target_tol=1e-8) for A, b in zip(mats, rhs)], cfg, sketch=S)
+    h = sk.solve_sequence([sk.ProblemInstance(L, b, target_tol=1e-8) for L, b in zip(calls, rhs)], cfg, sketch=S)
+    assert h.space.dim() == g.space.dim() > 0
+    for i, (rg, rh) in enumerate(zip(g.reports, h.reports)):
+        assert rh.status == rg.status == "converged", i
+        assert rh.iterations == rg.iterations, i
+        assert rh.counters == rg.counters, i
+        assert np.linalg.norm(h.solutions[i] - g.solutions[i]) <= 1e-12 * np.linalg.norm(g.solutions[i]), i
