@@ -631,9 +631,8 @@ __global__ void k_fold_partials(const double* __restrict__ partials, int G, int 
   const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (v >= nv) return;
   double a = 0.0;
-  for (int b = lane; b < G; b += 32)
-    a += value_major ? partials[static_cast<int64_t>(v) * G + b] : partials[static_cast<int64_t>(b) * nv + v];
-  a = warp_sum(a);
+  a = warp_sum(value_major ? strided_sum(partials + static_cast<int64_t>(v) * G, 1, lane, G, 32)
+                           : strided_sum(partials + v, nv, lane, G, 32));
   if (lane == 0) out[v] = a;
 }
 }  // namespace
@@ -644,8 +643,8 @@ __global__ void k_fold_partials2(const double* __restrict__ p1, int G1, const do
   const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (v >= nv) return;
   double a = 0.0;
-  for (int b = lane; b < G1; b += 32) a += p1[static_cast<int64_t>(v) * G1 + b];
-  for (int b = lane; b < G2; b += 32) a += p2[static_cast<int64_t>(v) * G2 + b];
+  a = strided_sum(p1 + static_cast<int64_t>(v) * G1, 1, lane, G1, 32);
+  a = strided_sum(p2 + static_cast<int64_t>(v) * G2, 1, lane, G2, 32, a);
   a = warp_sum(a);
   if (lane == 0) out[v] = a;
 }

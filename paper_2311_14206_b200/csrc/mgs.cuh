@@ -20,21 +20,27 @@ namespace sdr {
 /// curB_in: column j's B values (||w_j||^2, w_j.w_{j-g}); null = record row j.
 /// Both are given when the caller folded them itself (the deferred path, in
 /// which the rows are written by CTA 0 of the same launch).
+/// preB / preC: the earlier window columns' B entries
+/// (preB[(d-1) MAXT + g] = B entry g of column j-d) and scales
+/// (preC[d-1] = cvec[j-d]), when the caller loaded them already.
 template <int MAXT>
 __device__ __forceinline__ void mgs_coefficients(double* __restrict__ rec, int64_t rstride, int T, int j, int nwin,
                                                  double* __restrict__ cvec, double* __restrict__ coef, bool write_rec,
-                                                 const double* recA_in = nullptr, const double* curB_in = nullptr) {
+                                                 const double* recA_in = nullptr, const double* curB_in = nullptr,
+                                                 const double* preB = nullptr, const double* preC = nullptr) {
   const int b_off = 2 * T + 3;
   const double* recA = recA_in ? recA_in : rec + static_cast<int64_t>(j + 1) * rstride;
   auto colB = [&](int i, int g) {  // B entry g of column i (g = 0: norm, g >= 1: Gram with column i - g)
-    return (i == j && curB_in) ? curB_in[g] : rec[static_cast<int64_t>(i) * rstride + b_off + g];
+    if (i == j && curB_in) return curB_in[g];
+    if (i != j && preB) return preB[(j - i - 1) * MAXT + g];
+    return rec[static_cast<int64_t>(i) * rstride + b_off + g];
   };
   const double wn2 = colB(j, 0);
   const double cj = 1.0 / sqrt(wn2);
   double ci[MAXT], h[MAXT];
 #pragma unroll
   for (int d = 0; d < MAXT; ++d) {
-    ci[d] = d == 0 ? cj : (d < nwin ? cvec[j - d] : 0.0);
+    ci[d] = d == 0 ? cj : (d < nwin ? (preC ? preC[d - 1] : cvec[j - d]) : 0.0);
     h[d] = 0.0;
   }
   // MGS order i = j-nwin+1 .. j  <=>  d = nwin-1 .. 0

@@ -19,6 +19,40 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+/// sum of p[b * ld] over b = b0, b0 + step, ... < G, added in that order,
+/// with eight loads in flight per round (a fold over a few hundred CTA
+/// partials is one or two L2 round trips instead of one per partial);
+/// `a` is the running sum to continue.
+__device__ __forceinline__ double strided_sum(const double* __restrict__ p, int64_t ld, int b0, int G, int step,
+                                              double a = 0.0) {
+  for (int b = b0; b < G; b += 8 * step) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = b + u * step < G ? __ldcg(p + static_cast<int64_t>(b + u * step) * ld) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a += v[u];
+  }
+  return a;
+}
+
+/// strided_sum over (re, im) pairs p[b * ld], p[b * ld + 1].
+__device__ __forceinline__ double2 strided_sum2(const double* __restrict__ p, int64_t ld, int b0, int G, int step) {
+  double re = 0.0, im = 0.0;
+  for (int b = b0; b < G; b += 8 * step) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = b + u * step < G ? __ldcg(reinterpret_cast<const double2*>(p + static_cast<int64_t>(b + u * step) * ld))
+                              : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      re += v[u].x;
+      im += v[u].y;
+    }
+  }
+  return make_double2(re, im);
+}
+
 /// Block-reduce nv (<= NV) per-thread values; thread 0's warp writes
 /// partials[k * gridDim.x + blockIdx.x]. Requires blockDim.x % 32 == 0.
 template <int NV>

@@ -23,8 +23,10 @@
 #include "reduce.cuh"
 #include "sketch.hpp"
 
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <vector>
 
 namespace sdr {
 
@@ -267,6 +269,7 @@ struct TileArgs {
   const double* row_scale = nullptr;
   const double2* tab = nullptr;  // [g_alpha s][g_beta s][z s][half-phase s][jump z^24, z^8, z^28, z^16 (4s)][twiddle 256]
   const int* uq = nullptr;       // k mod 256
+  const int* uperm = nullptr;    // rows in increasing k mod 256
   double* partials = nullptr;    // [G][nvp] CTA partials
   unsigned long long* trace = nullptr;  // SDR_TRACE=1: per-CTA phase timestamps [G][16]
   unsigned long long* stamp = nullptr;  // SDR_TRACE=2: launch timeline
@@ -307,14 +310,8 @@ struct UpdateArgs {
 __device__ __forceinline__ void sketch_row_fold(const double* __restrict__ partials, int G, int nvp, int q, int lane,
                                                 int s, const double2* __restrict__ tab,
                                                 const double* __restrict__ row_scale, double* __restrict__ dst) {
-  double re = 0.0, im = 0.0;
-  for (int b = lane; b < G; b += 32) {
-    const double2 v = *reinterpret_cast<const double2*>(partials + static_cast<int64_t>(b) * nvp + 2 * q);
-    re += v.x;
-    im += v.y;
-  }
-  re = warp_sum(re);
-  im = warp_sum(im);
+  const double2 v = strided_sum2(partials + 2 * q, nvp, lane, G, 32);
+  const double re = warp_sum(v.x), im = warp_sum(v.y);
   if (lane == 0) {
     const double2 hp = tab[3 * s + q];
     dst[q] = (hp.x * re - hp.y * im) * row_scale[q];
@@ -327,56 +324,69 @@ __device__ __forceinline__ void sketch_row_fold(const double* __restrict__ parti
 /// order in every CTA, folds a pending set of sketch rows (spread over all
 /// warps of the grid), forms the MGS coefficients into coef[0..MAXT]; CTA 0
 /// writes record rows j+1 (A, H), j (norm / Gram) and cvec[j].
+/// The first half of the warps folds the dots, the second half the sketch
+/// rows and loads the earlier window columns' MGS inputs, so every global
+/// load of the prologue is in flight at once (one L2 round trip between
+/// the previous kernel's completion and the coefficients, not three).
 template <int MAXT, int NT>
 __device__ __forceinline__ void deferred_prologue(const UpdateArgs& ua, int s, const double2* __restrict__ tab,
                                                   const double* __restrict__ row_scale, double* coef) {
-  __shared__ double red[2 * MAXT + 1][NT / 32];
-  __shared__ double sA[MAXT + 1], sB[MAXT];
+  constexpr int NW = NT / 32, NWH = NW / 2;
+  __shared__ double red[2 * MAXT + 1][NWH];
+  __shared__ double sA[MAXT + 1], sB[MAXT], preB[MAXT * MAXT], preC[MAXT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x, G = gridDim.x;
   const int nA = 1 + ua.nwin;
   const bool prev = ua.prev_ng != nullptr;
-  double a[MAXT + 1], bs[MAXT];
-#pragma unroll
-  for (int v = 0; v <= MAXT; ++v) a[v] = 0.0;
-#pragma unroll
-  for (int v = 0; v < MAXT; ++v) bs[v] = 0.0;
-  for (int bb = tid; bb < ua.k1_G; bb += NT)
-#pragma unroll
-    for (int v = 0; v <= MAXT; ++v)
-      if (v < nA) a[v] += __ldcg(ua.k1_partials + static_cast<int64_t>(v) * ua.k1_G + bb);
-  if (prev)
-    for (int bb = tid; bb < ua.prev_ng_G; bb += NT)
-#pragma unroll
-      for (int v = 0; v < MAXT; ++v)
-        bs[v] += __ldcg(ua.prev_ng + static_cast<int64_t>(bb) * ua.prev_ng_ld + ua.prev_ng_off + v);
-#pragma unroll
-  for (int v = 0; v <= MAXT; ++v) {
-    const double r = warp_sum(a[v]);
-    if (lane == 0) red[v][warp] = r;
-  }
-#pragma unroll
-  for (int v = 0; v < MAXT; ++v) {
-    const double r = warp_sum(bs[v]);
-    if (lane == 0) red[MAXT + 1 + v][warp] = r;
-  }
   const int64_t R = ua.rstride;
   const int b_off = 2 * ua.T + 3;
-  if (ua.prev_sk) {
-    double* dst = ua.rec + static_cast<int64_t>(ua.sk_row) * R + b_off + ua.T;
-    for (int q = warp * G + b; q < s; q += G * (NT / 32))  // at most a row or two per CTA
-      sketch_row_fold(ua.prev_sk, ua.prev_sk_G, ua.prev_sk_ld, q, lane, s, tab, row_scale, dst);
+  if (warp < NWH) {
+    double a[MAXT + 1], bs[MAXT];
+#pragma unroll
+    for (int v = 0; v <= MAXT; ++v)
+      a[v] = v < nA ? strided_sum(ua.k1_partials + static_cast<int64_t>(v) * ua.k1_G, 1, tid, ua.k1_G, NT / 2) : 0.0;
+#pragma unroll
+    for (int v = 0; v < MAXT; ++v)
+      bs[v] = prev ? strided_sum(ua.prev_ng + ua.prev_ng_off + v, ua.prev_ng_ld, tid, ua.prev_ng_G, NT / 2) : 0.0;
+#pragma unroll
+    for (int v = 0; v <= MAXT; ++v) {
+      const double r = warp_sum(a[v]);
+      if (lane == 0) red[v][warp] = r;
+    }
+#pragma unroll
+    for (int v = 0; v < MAXT; ++v) {
+      const double r = warp_sum(bs[v]);
+      if (lane == 0) red[MAXT + 1 + v][warp] = r;
+    }
+  } else {
+    const int w2 = warp - NWH;
+    if (w2 == NWH - 1 && MAXT > 1) {
+      // B entries and scales of columns j-1 .. j-MAXT+1 (written by earlier steps)
+      if (lane < (MAXT - 1) * MAXT) {
+        const int d = 1 + lane / MAXT, g = lane % MAXT;
+        preB[lane] = d < ua.nwin ? __ldcg(ua.rec + static_cast<int64_t>(ua.j - d) * R + b_off + g) : 0.0;
+      } else if (lane >= 16 && lane < 16 + MAXT - 1) {
+        const int d = lane - 15;
+        preC[d - 1] = d < ua.nwin ? __ldcg(ua.cvec + ua.j - d) : 0.0;
+      }
+    }
+    if (ua.prev_sk) {
+      double* dst = ua.rec + static_cast<int64_t>(ua.sk_row) * R + b_off + ua.T;
+      for (int q = w2 * G + b; q < s; q += G * NWH)  // at most a row or two per CTA
+        sketch_row_fold(ua.prev_sk, ua.prev_sk_G, ua.prev_sk_ld, q, lane, s, tab, row_scale, dst);
+    }
   }
   __syncthreads();
   if (tid < 2 * MAXT + 1) {
     double r = 0.0;
-    for (int w = 0; w < NT / 32; ++w) r += red[tid][w];
+    for (int w = 0; w < NWH; ++w) r += red[tid][w];
     if (tid <= MAXT) sA[tid] = r;
     else sB[tid - MAXT - 1] = (tid - MAXT - 1 <= ua.prev_ngram) ? r : 0.0;
   }
   __syncthreads();
   if (tid == 0) {
-    mgs_coefficients<MAXT>(ua.rec, R, ua.T, ua.j, ua.nwin, ua.cvec, coef, b == 0, sA, prev ? sB : nullptr);
+    mgs_coefficients<MAXT>(ua.rec, R, ua.T, ua.j, ua.nwin, ua.cvec, coef, b == 0, sA, prev ? sB : nullptr,
+                           MAXT > 1 ? preB : nullptr, MAXT > 1 ? preC : nullptr);
     if (b == 0) {
       double* recA = ua.rec + static_cast<int64_t>(ua.j + 1) * R;
       for (int v = 0; v < nA; ++v) recA[v] = sA[v];
@@ -422,7 +432,10 @@ __global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch)
   double2* zq = sm + GRP * (PR * kXS + 2 * s);   // [s]  z = e^{2 i pi k/N}
   double2* zj = zq + s;                                    // [s]  z^{8 (GRP - 1)}: jump over the other groups' tiles
   double2* tw = zj + s;                                    // [256]
+  // per-row tables in Horner order i (rows sorted by u = k mod 256, so a
+  // warp's gathers X[pp][u], X[pp][-u] hit consecutive u: no bank conflicts)
   int* uq = reinterpret_cast<int*>(tw + 256);              // [s]
+  int* pm = uq + s;                                        // [s] row of Horner slot i
   __shared__ double coef[MAXT + 1];
   __shared__ double nred[MAXT][kCta / 32];
   const int G = gridDim.x, b = blockIdx.x;
@@ -430,14 +443,17 @@ __global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch)
   stamp_begin(ta.stamp);
   trace_mark(ta.trace, 0);
   for (int k = tid; k < 256; k += kCta) tw[k] = ta.tab[8 * s + k];
-  for (int q = tid; q < s; q += kCta) {
-    zq[q] = ta.tab[2 * s + q];
-    zj[q] = ta.tab[jump_slot(PR, GRP) * s + q];
-    uq[q] = ta.uq[q];
+  for (int i = tid; i < s; i += kCta) {
+    const int q = ta.uperm[i];
+    zq[i] = ta.tab[2 * s + q];
+    zj[i] = ta.tab[jump_slot(PR, GRP) * s + q];
+    uq[i] = ta.uq[q];
+    pm[i] = q;
   }
   for (int q = tid; q < GRP * 2 * s; q += kCta) S1s[q - g * 2 * s] = make_double2(0.0, 0.0);
   pdl_trigger();
   pdl_wait();  // everything below reads the previous kernels' output
+  trace_mark(ta.trace, 4);
   if constexpr (SRC == kSrcUpdate) {
     if (ua.k1_partials) {
       deferred_prologue<MAXT, kCta>(ua, s, ta.tab, ta.row_scale, coef);
@@ -600,7 +616,8 @@ __global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch)
   // L2 request: a multi-µs tail)
   const int nv = 2 * s + (SRC == kSrcUpdate ? MAXT : 0);
   const int nvp = (nv + 1) & ~1;
-  for (int q = tid; q < s; q += kCta) {
+  for (int i = tid; i < s; i += kCta) {
+    const int q = pm[i];
     const uint64_t k = static_cast<uint64_t>(ta.rows[q]);
     const double2 ga = ta.tab[q], gb = ta.tab[s + q];
     double2 acc = make_double2(0.0, 0.0);
@@ -611,7 +628,7 @@ __global__ void __launch_bounds__(GRP * PR * 16, (GRP == 2 && SRC == kSrcSketch)
       const uint64_t kx = k * static_cast<uint64_t>(ta.r0 + glow[gg] * 2 * PR);
       const uint64_t ph = (twoN & (twoN - 1)) == 0 ? (kx & (twoN - 1)) : kx % twoN;
       sincospi(static_cast<double>(ph) / static_cast<double>(ta.N), &sn, &cs);
-      acc = cadd(acc, cmul(make_double2(cs, sn), cadd(cmul(ga, S[q]), cmul(gb, S[s + q]))));
+      acc = cadd(acc, cmul(make_double2(cs, sn), cadd(cmul(ga, S[i]), cmul(gb, S[s + i]))));
     }
     *reinterpret_cast<double2*>(ta.partials + static_cast<int64_t>(b) * nvp + 2 * q) = acc;
   }
@@ -646,7 +663,7 @@ __global__ void __launch_bounds__(256) k_srdct_fold(const double* __restrict__ p
     const int g = q - s;
     double a = 0.0;
     if (g <= ua.ngram && g < maxt)
-      for (int b = lane; b < G; b += 32) a += partials[static_cast<int64_t>(b) * nvp + 2 * s + g];
+      a = strided_sum(partials + 2 * s + g, nvp, lane, G, 32);
     a = warp_sum(a);
     if (lane == 0) ua.rec[static_cast<int64_t>(ua.j + 1) * ua.rstride + (2 * ua.T + 3) + g] = a;
   }
@@ -976,8 +993,7 @@ __global__ void __launch_bounds__(256) k_sparse_fold(const double* __restrict__ 
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= s) return;
   double a = 0.0;
-  for (int b = lane; b < G; b += 32) a += partials[static_cast<int64_t>(b) * s + r];
-  a = warp_sum(a);
+  a = warp_sum(strided_sum(partials + r, s, lane, G, 32));
   if (lane == 0) out[r] = a * (row_scale ? row_scale[r] : inv_sqrt_zeta);
 }
 
@@ -1084,7 +1100,7 @@ namespace {
 
 size_t tiles_smem(int64_t s, int grp = kGroupsMax, int pr = kGPairs) {
   return sizeof(double2) * static_cast<size_t>(grp * (pr * kXS + 2 * s) + 2 * s + 256) +
-         sizeof(int) * static_cast<size_t>(s);
+         sizeof(int) * static_cast<size_t>(2 * s);
 }
 
 bool tiles_eligible(const SketchDev& S, const SrdctPlan& p) {
@@ -1111,6 +1127,7 @@ void launch_tiles(Context& c, const char* name, const SketchDev& S, const SrdctP
   ta.row_scale = S.row_scale.get();
   ta.tab = S.tab.get();
   ta.uq = S.uq.get();
+  ta.uperm = S.uperm.get();
   ta.partials = sf ? sf->out_partials : c.partials(nv * G);
   ta.trace = c.trace(16 * static_cast<int64_t>(G));
   ta.stamp = c.launch_stamp(name);
@@ -1155,6 +1172,13 @@ void prepare_srdct_tables(Context& c, SketchDev& S) {
   k_srdct_tables<<<static_cast<int>((S.s + 256 + 255) / 256), 256, 0, c.stream>>>(S.n, S.rows.get(), static_cast<int>(S.s),
                                                                                  S.tab.get(), S.uq.get());
   SDR_KERNEL_CHECK();
+  std::vector<int> perm(static_cast<size_t>(S.s));
+  for (int q = 0; q < static_cast<int>(S.s); ++q) perm[static_cast<size_t>(q)] = q;
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) {
+    return (S.rows_host[static_cast<size_t>(a)] & 255) < (S.rows_host[static_cast<size_t>(b)] & 255);
+  });
+  S.uperm.resize(S.s);
+  SDR_CUDA(cudaMemcpyAsync(S.uperm.get(), perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, c.stream));
   c.sync();
 }
 
@@ -1209,6 +1233,10 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
   if (p.M == 128) {
     if (need <= 2 && variant == 1)
       launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+    else if (need <= 2 && variant == 2)
+      launch_tiles<kSrcUpdate, 8, true, 2, 3, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
+    else if (need <= 2 && variant == 3)
+      launch_tiles<kSrcUpdate, 8, true, 2, 3, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
     else if (need <= 2)
       launch_tiles<kSrcUpdate, 8, true, 2, 2, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
     else

@@ -94,6 +94,7 @@ struct SketchDev {
   DeviceBuffer<double> row_scale;          // SRDCT: alpha_k * sqrt(n/s)
   DeviceBuffer<double2> tab;               // SRDCT per-row constants (sketch.cu k_srdct_tables)
   DeviceBuffer<int> uq;                    // SRDCT k mod 256
+  DeviceBuffer<int> uperm;                 // SRDCT rows ordered by k mod 256 (tile kernels' Horner order)
   std::vector<std::int64_t> rows_host;
   std::vector<std::uint32_t> sign_bits_host;
 };

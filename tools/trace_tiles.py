@@ -31,7 +31,7 @@ tr = tr[tr[:, 0] > 0]
 t0 = tr[:, 0].min()
 rel = (tr - t0) / 1e3  # us
 rel[tr == 0] = np.nan
-names = ["start", "prologue", "main", "combine"]
+names = ["start", "prologue", "main", "combine", "pdl_wait"]
 print(f"CTAs {len(tr)}; times in us from the first CTA start")
 for k, nm in enumerate(names):
     col = rel[:, k]
