@@ -1226,6 +1226,11 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
   // t <= 2: two tile groups per CTA with eight rows of loads in flight per
   // thread (242 registers) measured 2.5 % faster per step than four groups
   // with two rows (128 registers); SDR_K2_VARIANT=1 selects the latter.
+  // Also measured slower (C2, isolated / step period): three groups of 168
+  // registers (22.9 us / 52.0 us vs 19.1 / 48.4), an L2 prefetch of each
+  // group's next tile (20.0 us), and a cp.async staging of the next tile in
+  // per-thread shared-memory slots (21.4 us; its 201 KB of shared memory
+  // also keeps K1 from starting early: 60.8 us step).
   static const int variant = [] {
     const char* e = std::getenv("SDR_K2_VARIANT");
     return e ? std::atoi(e) : 0;
@@ -1233,10 +1238,6 @@ bool launch_update_sketch(Context& c, const SketchDev& S, const double* y, doubl
   if (p.M == 128) {
     if (need <= 2 && variant == 1)
       launch_tiles<kSrcUpdate, 8, true, 2>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
-    else if (need <= 2 && variant == 2)
-      launch_tiles<kSrcUpdate, 8, true, 2, 3, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
-    else if (need <= 2 && variant == 3)
-      launch_tiles<kSrcUpdate, 8, true, 2, 3, 4>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
     else if (need <= 2)
       launch_tiles<kSrcUpdate, 8, true, 2, 2, 8>(c, "update_sketch", S, p, row_begin, nullptr, 1.0, nullptr, ua, sf);
     else
