@@ -12,8 +12,12 @@
 // register-staged k_tsgemm / k_rgemm kept 32-64 KB per SM in flight and ran
 // at 0.55-0.62 of HBM). Eight consumer warps own 32 rows each and
 // accumulate all outputs on the fp64 tensor cores (mma.sync m8n8k4, DMMA):
-// 4 m-tiles x NO/8 n-tiles per warp; columns are staged with a 64-byte pad
-// so the fragment loads are bank-conflict free.
+// 4 m-tiles x NO/8 n-tiles per warp. A 64-bit shared load is served per
+// half-warp (lanes 4 g + t, g < 4): fragment rows t of stride 4 mod 16
+// doubles put its 16 addresses in 16 distinct bank pairs, so the ring's
+// columns are padded by 32 bytes and the coefficient rows to NO + 4
+// (measured at C5: strides 264 / NO = 16 made the A loads 2-way and the B
+// loads 4-way conflicted, 63 % of all shared wavefronts).
 #include "kernels.hpp"
 #include "reduce.cuh"
 #include "tma.cuh"
@@ -26,7 +30,7 @@ namespace {
 
 constexpr int kTmRows = 256;             // rows per tile (8 consumer warps x 32)
 constexpr int kTmKC = 8;                 // input columns per ring stage
-constexpr int kTmLd = kTmRows + 8;       // padded column stride in shared memory
+constexpr int kTmLd = kTmRows + 4;       // padded column stride in shared memory (== 4 mod 16 doubles)
 constexpr int kTmStages = 4;
 constexpr int kTmConsumers = 8;
 constexpr int kTmThreads = 32 * (1 + kTmConsumers);
@@ -54,11 +58,12 @@ __global__ void __launch_bounds__(kTmThreads) k_tsmm(TsmmArgs a) {
   const int K = a.k1 + a.k2;
   const int nch = (K + kTmKC - 1) / kTmKC;
   const int Kp = nch * kTmKC;
+  constexpr int LDB = NO + 4;
   double* ring = tm_sm;                                   // [stage][kTmKC][kTmLd]
-  double* Bs = tm_sm + kTmStages * kTmKC * kTmLd;         // [Kp][NO], zero past K / nout
+  double* Bs = tm_sm + kTmStages * kTmKC * kTmLd;         // [Kp][LDB], zero past K / nout
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int q = tid; q < Kp * NO; q += blockDim.x) {
-    const int i = q / NO, o = q % NO;
+  for (int q = tid; q < Kp * LDB; q += blockDim.x) {
+    const int i = q / LDB, o = q % LDB;
     Bs[q] = (o < a.nout && i < K) ? a.B[static_cast<int64_t>(o) * K + i] : 0.0;
   }
   if (tid == 0) {
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(kTmThreads) k_tsmm(TsmmArgs a) {
       for (int ch = 0; ch < nch; ++ch) {
         mbar_wait(&full[st], ph);
         const double* ab = ring + st * (kTmKC * kTmLd) + cw * 32 + g8;
-        const double* bb = Bs + (ch * kTmKC) * NO + g8;
+        const double* bb = Bs + (ch * kTmKC) * LDB + g8;
 #pragma unroll
         for (int ks = 0; ks < kTmKC / 4; ++ks) {
           const int kr = ks * 4 + t4;
@@ -122,7 +127,7 @@ __global__ void __launch_bounds__(kTmThreads) k_tsmm(TsmmArgs a) {
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) af[mt] = ab[kr * kTmLd + mt * 8];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) bf[nt] = bb[kr * NO + nt * 8];
+          for (int nt = 0; nt < NT; ++nt) bf[nt] = bb[kr * LDB + nt * 8];
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -177,7 +182,7 @@ __global__ void __launch_bounds__(kTmThreads) k_tsmm(TsmmArgs a) {
 
 size_t tsmm_smem(int K, int NO) {
   const int Kp = (K + kTmKC - 1) / kTmKC * kTmKC;
-  return sizeof(double) * (static_cast<size_t>(kTmStages) * kTmKC * kTmLd + static_cast<size_t>(Kp) * NO);
+  return sizeof(double) * (static_cast<size_t>(kTmStages) * kTmKC * kTmLd + static_cast<size_t>(Kp) * (NO + 4));
 }
 
 template <int NO>
