@@ -267,6 +267,12 @@ def main():
         return
 
     os.environ.setdefault("NCCL_DEBUG", "INFO")
+    # SDR_BENCH_HOSTCOMM=1: the ranks share GPU 0 and exchange through the
+    # host-staged transport (gloo) instead of NCCL — a one-GPU check of the
+    # multi-rank bench logic (slabs, max over ranks, e2e), not a measurement
+    hostcomm = os.environ.get("SDR_BENCH_HOSTCOMM") == "1" and world > 1
+    if hostcomm:
+        local = 0
     import torch
     torch.cuda.set_device(local)
     import paper_2311_14206_b200 as sk
@@ -281,9 +287,12 @@ def main():
                 so.bind(("127.0.0.1", 0))
                 os.environ["MASTER_PORT"] = str(so.getsockname()[1])
         dist.init_process_group("gloo", init_method="env://")
-        idbuf = [sk.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idbuf, src=0)
-        ctx = sk.Context(local, rank, world, idbuf[0])
+        if hostcomm:
+            ctx = sk.Context(local, rank, world, host_comm=sk.torch_host_comm())
+        else:
+            idbuf = [sk.Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idbuf, src=0)
+            ctx = sk.Context(local, rank, world, idbuf[0])
     else:
         dist = None
         ctx = sk.Context(local)
@@ -453,6 +462,8 @@ def main():
                        "m": wl["m"], "k": wl["k"], "t": wl["t"], "s": wl["s"], "tol": wl["tol"],
                        "max_restarts": wl["max_restarts"], "sketch": wl["sketch"],
                        "parallelism": f"zslab{world}",
+                       **({"transport": "host-staged test transport (SDR_BENCH_HOSTCOMM, ranks share GPU 0)"}
+                          if hostcomm else {}),
                        "l2": "inputs larger than L2 (Krylov basis (m+1) x 8N bytes per cycle, no L2 flush)"},
             "time_to_solution_ms": solve_ms,
             "solve": {"status": rep.status, "iterations": rep.iterations, "cycles": rep.cycles,

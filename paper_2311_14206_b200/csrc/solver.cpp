@@ -740,13 +740,25 @@ struct ArnoldiPipeline {
   /// at least two in flight while the host catches up with finished steps.
   void issue_ahead(i64 j) {
     while (issued < m && issued <= j + kLookahead + (split ? 1 : 0)) enqueue(issued++);
+    if (lockstep()) return;
     poll_done();
     while (issued < m && issued - done_upto < 2) enqueue(issued++);
   }
 
+  /// Several ranks: every step enqueues collectives (halo send/recv,
+  /// allreduce), which NCCL matches by issue order per communicator. Steps
+  /// are then issued only at points of the host program that are the same on
+  /// every rank (a fixed look-ahead from the consumed step), never by how far
+  /// this rank's GPU has progressed: otherwise one rank could enqueue a
+  /// step's allreduce where another enqueues the restart's, and the
+  /// collectives would pair up across different operations.
+  bool lockstep() const { return c.distributed(); }
+
   /// Speculation while the host is busy elsewhere (restart bookkeeping):
-  /// keeps kPumpDepth steps in flight without queueing the whole cycle.
+  /// keeps kPumpDepth steps in flight without queueing the whole cycle
+  /// (one rank only, see lockstep()).
   void pump() {
+    if (lockstep()) return;
     poll_done();
     while (issued < m && issued - done_upto < kPumpDepth) enqueue(issued++);
   }
