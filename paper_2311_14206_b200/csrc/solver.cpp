@@ -68,6 +68,10 @@ struct Workspace {
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<double> unorm;  // ||.||^2 of the fused restart pass's outputs (correction, U_new)
   double last_harmonic_ms = -1.0;  // host time of the previous cycle's harmonic pencil
+  // several ranks: the step pipeline every rank agreed on (ArnoldiPipeline::setup_deferred)
+  const void* defer_key = nullptr;
+  i64 defer_key_need = -1, defer_key_row = -1;
+  bool defer_agreed = false;
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
   // several ranks: the same partials folded over this rank's CTAs before the
   // allreduce; comb[j & 1] = [K2(j) folded (nvp) | K1(j + 1) folded], one
@@ -489,6 +493,21 @@ struct ArnoldiPipeline {
     }();
     deferred = !A.apply && (!c.distributed() || defer_dist) && fuse_update_sketch() &&
                update_sketch_eligible(S, w.lay, need, A.row_begin, w.lay.ld);
+    if (c.distributed() && !A.apply && defer_dist) {
+      // the two step pipelines enqueue different collectives: every rank must
+      // take the same one (eligibility depends on the rank's slab), agreed
+      // once per workspace and sketch
+      if (w.defer_key != &S || w.defer_key_need != need || w.defer_key_row != A.row_begin) {
+        const i64 mine = deferred ? 1 : 0;
+        std::vector<i64> all(static_cast<size_t>(c.world));
+        c.allgather_i64(&mine, 1, all.data());
+        w.defer_agreed = *std::min_element(all.begin(), all.end()) == 1;
+        w.defer_key = &S;
+        w.defer_key_need = need;
+        w.defer_key_row = A.row_begin;
+      }
+      deferred = w.defer_agreed;
+    }
     split = deferred && !c.distributed() && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
     merge_b = !deferred && c.distributed();
     if (!deferred && c.distributed() && !A.apply) {
