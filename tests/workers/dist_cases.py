@@ -8,6 +8,9 @@ CASES = {
     "conv_sparse": dict(kind="conv3d", n=32, sketch="sparse_sign", m=30, k=8, t=2, s=120, tol=1e-8),
     # 32^3 with SRDCT (C2's sketch): the deferred pipeline, fused update + SRDCT, split K1
     "conv_srdct": dict(kind="conv3d", n=32, sketch="srdct", m=40, k=10, t=2, s=120, tol=1e-8),
+    # 33^3 on two slabs of 16 and 17 planes (an odd row count on one rank):
+    # the ranks must agree on one step pipeline although their slabs differ
+    "conv_srdct_uneven": dict(kind="conv3d", n=33, sketch="srdct", m=40, k=10, t=2, s=120, tol=1e-8),
     # a CSR operator whose interior rows reach into the neighbour's rows
     # (non-uniform stencil reach: the K1 interior / boundary split must use
     # the per-row reach, not the halo width)
