@@ -93,6 +93,31 @@ def _ptr(a, dtype=np.float64):
     return arr, arr.ctypes.data_as(C.c_void_p), arr.size
 
 
+_nccl_preloaded = False
+
+
+def _preload_nccl():
+    """Load the NCCL that PyTorch links (the nvidia-nccl wheel) before the
+    library dlopens "libnccl.so.2" by soname, so both share one NCCL. Without
+    it a process that creates a distributed context before importing torch
+    would bind the system libnccl, and torch's later import fails against it
+    (undefined symbol ncclDevCommCreate: the system NCCL is older)."""
+    global _nccl_preloaded
+    if _nccl_preloaded:
+        return
+    _nccl_preloaded = True
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations if spec else []):
+            path = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(path):
+                C.CDLL(path, mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+                return
+    except (ImportError, OSError, ValueError):
+        pass
+
+
 class Context:
     """One GPU, one CUDA stream, optional NCCL rank (sdr_ctx)."""
 
@@ -106,6 +131,7 @@ class Context:
             self._hc = _host_comm_struct(host_comm)
             _check(_lib.sdr_ctx_create_hostcomm(device, rank, world, C.byref(self._hc[0]), C.byref(h)))
         elif world > 1 or nccl_id is not None:  # world = 1 with an id: one-rank NCCL, distributed code path
+            _preload_nccl()
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             _check(_lib.sdr_ctx_create_dist(device, rank, world, buf, C.byref(h)))
         else:
@@ -115,6 +141,7 @@ class Context:
 
     @staticmethod
     def nccl_unique_id() -> bytes:
+        _preload_nccl()
         buf = C.create_string_buffer(128)
         _check(_lib.sdr_nccl_unique_id(buf))
         return buf.raw

@@ -67,6 +67,7 @@ struct Workspace {
   int nV = 0;
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
   DeviceBuffer<double> unorm;  // ||.||^2 of the fused restart pass's outputs (correction, U_new)
+  DeviceBuffer<double> one;    // {1.0}: coefficient of a cycle's first column (w_0 = r0)
   double last_harmonic_ms = -1.0;  // host time of the previous cycle's harmonic pencil
   // several ranks: the step pipeline every rank agreed on (ArnoldiPipeline::setup_deferred)
   const void* defer_key = nullptr;
@@ -385,8 +386,19 @@ struct ArnoldiPipeline {
     w.fence_copies(c);
     SDR_CUDA(cudaEventRecord(w.ev_skq, w.sk_stream));  // earlier side-stream sketches are done before reuse
     SDR_CUDA(cudaStreamWaitEvent(c.stream, w.ev_skq, 0));
-    launch_copy_norm(c, r0, w.Vcol(vb, 0), w.lay.nloc, w.rec.get() + RL.b_off());
-    launch_sketch(c, S, w.Vcol(vb, 0), w.lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
+    if (!A.apply && update_sparse_eligible(S, w.lay, RL, 1, w.lay.ld) && reinterpret_cast<uintptr_t>(r0) % 16 == 0) {
+      // sparse sign: w_0 = r0, ||r0||^2 and S r0 in one bulk-copy pass (K2s with an empty window)
+      if (w.one.size() == 0) {
+        w.one.resize(1);
+        const double v = 1.0;
+        SDR_CUDA(cudaMemcpy(w.one.get(), &v, sizeof(double), cudaMemcpyHostToDevice));
+      }
+      launch_update_sparse(c, S, r0, w.V[vb].get(), w.lay.ld, w.lay, -1, 0, 0, w.rec.get(), RL, w.cvec.get(),
+                           w.one.get(), A.row_begin);
+    } else {
+      launch_copy_norm(c, r0, w.Vcol(vb, 0), w.lay.nloc, w.rec.get() + RL.b_off());
+      launch_sketch(c, S, w.Vcol(vb, 0), w.lay.nloc, A.row_begin, w.rec.get() + RL.sketch_off());
+    }
     c.allreduce_sum(w.rec.get() + RL.b_off(), RL.b_len());
     w.copy_back(c, w.hrec.get(), w.rec.get(), RL.stride, w.ev_init_k, w.ev_init);
     issued = 0;

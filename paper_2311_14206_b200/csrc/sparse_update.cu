@@ -90,9 +90,11 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
   } else if (threadIdx.x == 0) {
     // several ranks: records were allreduced after K1; every CTA forms the
     // same coefficients, CTA 0 publishes them in the record
-    double cfull[NW + 1];
-    mgs_coefficients<NW>(a.rec, a.rstride, a.T, a.j, NW, a.cvec, cfull, blockIdx.x == 0);
-    for (int k = 0; k <= NW; ++k) coef[k] = cfull[k];
+    if constexpr (NW > 0) {
+      double cfull[NW + 1];
+      mgs_coefficients<NW>(a.rec, a.rstride, a.T, a.j, NW, a.cvec, cfull, blockIdx.x == 0);
+      for (int k = 0; k <= NW; ++k) coef[k] = cfull[k];
+    }
   }
   __syncthreads();
 
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
       if (rows == TR) {  // full tile: no bounds checks
 #pragma unroll
         for (int u = 0; u < kRowsPerLane; ++u) {
-          double wv[NW];
+          double wv[NW > 0 ? NW : 1];
 #pragma unroll
           for (int d = 0; d < NW; ++d) wv[d] = ys[(1 + d) * TR + 32 * u];
           double x = cf[0] * ys[32 * u];
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
         const int even = rows & ~1;
         for (int u = 0; u < kRowsPerLane; ++u) {
           const int r = 32 * u + lane;
-          double yv = 0.0, wv[NW];
+          double yv = 0.0, wv[NW > 0 ? NW : 1];
 #pragma unroll
           for (int d = 0; d < NW; ++d) wv[d] = 0.0;
           if (r < even) {
@@ -265,6 +267,7 @@ void upd_sparse_impl(Context& c, const SketchDev& S, UpdSparseArgs a, const RecL
 
 template <int NW>
 void upd_sparse_ng(Context& c, const SketchDev& S, const UpdSparseArgs& a, const RecLayout& RL, double* out) {
+  if constexpr (NW == 0) return upd_sparse_impl<0, 0>(c, S, a, RL, out);
   switch (a.ngram) {
     case 0: return upd_sparse_impl<NW, 0>(c, S, a, RL, out);
     case 1:
@@ -288,7 +291,7 @@ bool update_sparse_eligible(const SketchDev& S, const VecLayout& lay, const RecL
 void launch_update_sparse(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv,
                           const VecLayout& lay, int j, int nwin, int ngram, double* rec, const RecLayout& RL,
                           double* cvec, const double* coef_ready, int64_t row_begin) {
-  if (nwin < 1 || nwin > 4 || ngram < 0 || ngram > 3 || ngram > nwin)
+  if (nwin < 0 || nwin > 4 || ngram < 0 || ngram > 3 || ngram > nwin || (nwin == 0 && !coef_ready))
     throw logic("launch_update_sparse: window outside the compiled range");
   UpdSparseArgs a{};
   a.y = y;
@@ -310,6 +313,7 @@ void launch_update_sparse(Context& c, const SketchDev& S, const double* y, doubl
   a.s = static_cast<int>(S.s);
   double* out = rec + static_cast<int64_t>(j + 1) * RL.stride + RL.sketch_off();
   switch (nwin) {
+    case 0: return upd_sparse_ng<0>(c, S, a, RL, out);  // w = coef_ready[0] y: a cycle's first column
     case 1: return upd_sparse_ng<1>(c, S, a, RL, out);
     case 2: return upd_sparse_ng<2>(c, S, a, RL, out);
     case 3: return upd_sparse_ng<3>(c, S, a, RL, out);
