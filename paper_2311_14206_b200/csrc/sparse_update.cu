@@ -36,7 +36,11 @@ namespace {
 // rows per ring stage (4 KB per vector) and stages: C5 sweep (t = 2, isolated,
 // us per launch): 256/3 1108, 256/2 1209, 256/4 1110, 128/4 1356, 128/6 1272,
 // 512/2 1006, 512/3 1252, 768/2 1203, 1024/2 2165 — larger tiles halve the
-// per-tile bookkeeping, more stages cost a resident CTA per SM
+// per-tile bookkeeping, more stages cost a resident CTA per SM. One consumer
+// warp per CTA doing all eight entries (no duplicated ring reads / update,
+// four consumer warps per SM) measured 1766 us in-solve vs 1120 us: too few
+// warps to cover the bin read-modify-writes (it did keep the GPU off its
+// power cap, 1965 vs 1717 MHz, which is where K1's 1794 vs 1850 us came from)
 constexpr int kTileRows = 512;
 constexpr int kStages = 2;
 constexpr int kConsumers = 2;  // one warp per 4-entry hash chunk (ζ = 8)
