@@ -70,8 +70,9 @@ struct Workspace {
   DeviceBuffer<double> one;    // {1.0}: coefficient of a cycle's first column (w_0 = r0)
   double last_harmonic_ms = -1.0;  // host time of the previous cycle's harmonic pencil
   // several ranks: the step pipeline every rank agreed on (ArnoldiPipeline::setup_deferred)
-  const void* defer_key = nullptr;
-  i64 defer_key_need = -1, defer_key_row = -1, defer_key_sketch[3] = {-1, -1, -1};
+  // (cache key: values every rank derives from the same call sequence — no
+  // addresses, which could match on one rank and not on another)
+  std::vector<i64> defer_key;
   bool defer_agreed = false;
   DeviceBuffer<double> p1, p2[2];  // deferred step pipeline: K1 / K2 CTA partials (K2's by step parity)
   // several ranks: the same partials folded over this rank's CTAs before the
@@ -509,17 +510,13 @@ struct ArnoldiPipeline {
       // the two step pipelines enqueue different collectives: every rank must
       // take the same one (eligibility depends on the rank's slab), agreed
       // once per workspace and sketch
-      const i64 sk_id[3] = {S.kind, S.n, S.s};
-      if (w.defer_key != &S || w.defer_key_need != need || w.defer_key_row != A.row_begin ||
-          !std::equal(sk_id, sk_id + 3, w.defer_key_sketch)) {
+      const std::vector<i64> key = {S.kind, S.n, S.s, S.zeta, need, A.row_begin, w.lay.nloc, w.lay.own_off, w.lay.ld};
+      if (w.defer_key != key) {
         const i64 mine = deferred ? 1 : 0;
         std::vector<i64> all(static_cast<size_t>(c.world));
         c.allgather_i64(&mine, 1, all.data());
         w.defer_agreed = *std::min_element(all.begin(), all.end()) == 1;
-        w.defer_key = &S;
-        w.defer_key_need = need;
-        w.defer_key_row = A.row_begin;
-        std::copy(sk_id, sk_id + 3, w.defer_key_sketch);
+        w.defer_key = key;
       }
       deferred = w.defer_agreed;
     }
