@@ -266,7 +266,6 @@ def main():
             emit(line)
         return
 
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
     # SDR_BENCH_HOSTCOMM=1: the ranks share GPU 0 and exchange through the
     # host-staged transport (gloo) instead of NCCL — a one-GPU check of the
     # multi-rank bench logic (slabs, max over ranks, e2e), not a measurement
@@ -494,6 +493,16 @@ if __name__ == "__main__":
             _ngpus = int(_a.split("=", 1)[1])
     if _ngpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch(_ngpus))
+    if (os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION" and "SDR_BENCH_REEXEC" not in os.environ
+            and "reference" not in sys.argv and "--impl=reference" not in sys.argv):
+        # the communicator set-up lines (NCCL_DEBUG=INFO) for the log; NCCL
+        # takes its debug level from the environment the process starts
+        # with, so re-exec once with it (an interpreter start-up hook on the
+        # GPU boxes presets VERSION, which prints the version banner only)
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["SDR_BENCH_REEXEC"] = "1"
+        sys.stdout.flush()
+        os.execv(sys.executable, [sys.executable] + sys.argv)
     # keep stdout for the JSON line alone: fd 1 points at stderr while the
     # workload runs (NCCL prints its version banner to stdout on rank 0)
     _JSON_OUT = os.fdopen(os.dup(1), "w")
