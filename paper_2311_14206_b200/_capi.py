@@ -11,7 +11,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsdr_b200.so")
+LIB_PATH = os.environ.get("SDR_LIB_PATH") or os.path.join(_HERE, "_lib", "libsdr_b200.so")  # override: A/B builds
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "sdr_b200.h")
 
 vp, i32, i64, u64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double

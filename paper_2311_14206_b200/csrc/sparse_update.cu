@@ -67,7 +67,7 @@ struct UpdSparseArgs {
 
 /// NW = nwin window columns, NG = ngram Gram entries (compile time: the
 /// per-row code has no window predicates).
-template <int NW, int NG, int TR = kTileRows, int NS = kStages>
+template <int NW, int NG, int TR = kTileRows, int NS = kStages, int BS = 0>
 __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
       bsz[e] = ((l + 1) * s) / 8 - rb[e];
       rb[e] = rb[e] * 32 + lane;
     }
+    // shared-memory byte address of bin row 0 of each entry's block (this lane)
+    uint32_t rbB[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) rbB[e] = smem_addr(bins + rb[e]);
     // hash argument key + (jg*2 + c + 1)*phi; 32 rows further = 64 phi
     const uint64_t d_row = 64ull * kPhi64;
     double* wout = a.V + static_cast<int64_t>(a.j + 1) * a.ldv + a.own_off;
@@ -213,22 +217,28 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
       if (++st == NS) st = 0, ph ^= 1u;
 #pragma unroll
       for (int u = 0; u < kRowsPerLane; ++u) {
-        const int whi = __double2hiint(w[u]), wlo = __double2loint(w[u]);
-        int row[4];
+        // w with its sign bit flipped: an entry whose sign bit f & 1 is clear
+        // takes -w, i.e. nwhi ^ (f << 31)
+        const uint32_t nwhi = static_cast<uint32_t>(__double2hiint(w[u])) ^ 0x80000000u;
+        const int wlo = __double2loint(w[u]);
+        const uint32_t hw[2] = {static_cast<uint32_t>(h[u]), static_cast<uint32_t>(h[u] >> 32)};
+        uint32_t addr[4];
         double sv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint32_t f = static_cast<uint32_t>(h[u] >> (16 * e));  // sign bit 0, row bits 1..15
-          row[e] = rb[e] + static_cast<int>((((f >> 1) & 0x7FFFu) * static_cast<uint32_t>(bsz[e])) >> 15) * 32;
-          // sign bit of w flipped when the entry's sign bit is clear
-          sv[e] = __hiloint2double(whi ^ static_cast<int>((~f & 1u) << 31), wlo);
+          const uint32_t f = hw[e >> 1] >> (16 * (e & 1));  // sign bit 0, row bits 1..15
+          // bin ((f >> 1) & 0x7FFF) * bsz >> 15 == ((f & 0xFFFE) * bsz) >> 16 of
+          // the block; 256 bytes (32 lane columns) per bin row
+          const uint32_t xb = (f & 0xFFFEu) * static_cast<uint32_t>(BS > 0 ? BS : bsz[e]);
+          addr[e] = rbB[e] + ((xb >> 16) << 8);
+          sv[e] = __hiloint2double(static_cast<int>(nwhi ^ (f << 31)), wlo);
         }
         // a row's four entries lie in four distinct blocks: distinct bins
         double tv[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) tv[e] = bins[row[e]];
+        for (int e = 0; e < 4; ++e) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(tv[e]) : "r"(addr[e]));
 #pragma unroll
-        for (int e = 0; e < 4; ++e) bins[row[e]] = tv[e] + sv[e];
+        for (int e = 0; e < 4; ++e) asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr[e]), "d"(tv[e] + sv[e]) : "memory");
       }
     }
     // CTA sketch rows of this warp's blocks: lane-ordered xor tree per row
@@ -251,7 +261,12 @@ size_t upd_sparse_smem(int s, int nwin, int tr = kTileRows, int ns = kStages) {
 
 template <int NW, int NG, int TR = kTileRows, int NS = kStages>
 void upd_sparse_impl(Context& c, const SketchDev& S, UpdSparseArgs a, const RecLayout& RL, double* out) {
-  auto kern = k_update_sparse8<NW, NG, TR, NS>;
+  // s = 120 (BASELINE C1 / C5): eight blocks of 15 rows, a compile-time block size
+  static const bool bs_on = [] {
+    const char* e = std::getenv("SDR_K2S_BS");
+    return !e || std::atoi(e) != 0;
+  }();
+  auto kern = (bs_on && S.s == 120) ? k_update_sparse8<NW, NG, TR, NS, 15> : k_update_sparse8<NW, NG, TR, NS, 0>;
   const size_t smem = upd_sparse_smem(static_cast<int>(S.s), NW, TR, NS);
   ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   const int per_sm = std::max(1, blocks_per_sm(reinterpret_cast<const void*>(kern), kThreadsUS, smem));
