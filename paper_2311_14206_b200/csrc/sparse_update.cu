@@ -255,6 +255,26 @@ __global__ void __launch_bounds__(kThreadsUS) k_update_sparse8(UpdSparseArgs a) 
   stamp_end(a.stamp);
 }
 
+/// One fold of a K2s launch's CTA partials into the record's B part, which
+/// is contiguous: out[0, T) = the norm / Gram values (value-major partials),
+/// out[T, T + s) = the sketch rows (CTA-major partials) times 1/sqrt(zeta).
+/// Fixed-order sums (strided_sum, then the xor tree): the values
+/// k_fold_partials / k_sparse_fold give, in one launch instead of two.
+__global__ void __launch_bounds__(256) k_fold_update_sparse(const double* __restrict__ ng, int T,
+                                                             const double* __restrict__ sk, int s, int G,
+                                                             double scale, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q < T) {
+    const double a = warp_sum(strided_sum(ng + static_cast<int64_t>(q) * G, 1, lane, G, 32));
+    if (lane == 0) out[q] = a;
+  } else if (q < T + s) {
+    const int r = q - T;
+    const double a = warp_sum(strided_sum(sk + r, s, lane, G, 32));
+    if (lane == 0) out[T + r] = a * scale;
+  }
+}
+
 size_t upd_sparse_smem(int s, int nwin, int tr = kTileRows, int ns = kStages) {
   return sizeof(double) * (static_cast<size_t>(s) * 32 + static_cast<size_t>(ns) * (1 + nwin) * tr);
 }
@@ -280,8 +300,17 @@ void upd_sparse_impl(Context& c, const SketchDev& S, UpdSparseArgs a, const RecL
     kern<<<g, kThreadsUS, smem, c.stream>>>(a);
     SDR_KERNEL_CHECK();
   }
-  launch_fold_partials(c, a.ng_partials, g, RL.T, true, a.rec + static_cast<int64_t>(a.j + 1) * RL.stride + RL.b_off());
-  launch_sparse_fold(c, a.sk_partials, g, static_cast<int>(S.s), 1.0 / std::sqrt(8.0), out);
+  double* recB = a.rec + static_cast<int64_t>(a.j + 1) * RL.stride + RL.b_off();
+  if (out == recB + RL.T) {  // the record's B part: norm / Gram, then the sketch rows
+    TimedLaunch t(c, "sketch_fold");
+    const int nw = RL.T + static_cast<int>(S.s);
+    k_fold_update_sparse<<<(nw + 7) / 8, 256, 0, c.stream>>>(a.ng_partials, RL.T, a.sk_partials, static_cast<int>(S.s),
+                                                             g, 1.0 / std::sqrt(8.0), recB);
+    SDR_KERNEL_CHECK();
+  } else {
+    launch_fold_partials(c, a.ng_partials, g, RL.T, true, recB);
+    launch_sparse_fold(c, a.sk_partials, g, static_cast<int>(S.s), 1.0 / std::sqrt(8.0), out);
+  }
 }
 
 template <int NW>
