@@ -46,6 +46,19 @@ WORKLOADS = {
                max_restarts=10),
 }
 METRIC = "gmres_sdr_arnoldi_steps_per_s"
+
+
+def workload_config(name, wl, world):
+    """The `config` both arms print (identical dicts): the workload — the
+    global problem (7-point convection-diffusion on n^3, Dirichlet: 7 n^3 -
+    6 n^2 stored entries), the solver parameters, the row partition. How a
+    rank stores its block is an implementation detail (`storage`, top level)."""
+    n = wl["n"]
+    N = n ** 3
+    return {"workload": name, "N": N, "N_per_gpu": N // world, "nnz": 7 * n ** 3 - 6 * n ** 2, "m": wl["m"],
+            "k": wl["k"], "t": wl["t"], "s": wl["s"], "tol": wl["tol"], "max_restarts": wl["max_restarts"],
+            "sketch": wl["sketch"], "parallelism": f"zslab{world}",
+            "l2": "inputs larger than L2 (Krylov basis (m+1) x 8N bytes per cycle, no L2 flush)"}
 STEP_KERNELS = ("spmv_arnoldi", "update", "sketch", "update_sketch", "sketch_fold", "fold_partials")
 
 
@@ -213,8 +226,7 @@ def run_reference(args, wl, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE generators, seeded)",
-        "config": {"workload": args.config, "N": r["N"], "nnz": r["nnz"], "m": wl["m"], "k": wl["k"], "t": wl["t"],
-                   "s": wl["s"], "tol": wl["tol"], "sketch": wl["sketch"]},
+        "config": workload_config(args.config, wl, world),
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "port", "sample": sample,
                          **host_info()},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -457,13 +469,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": solve_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE generators, seeded)",
-            "config": {"workload": args.config, "N": N, "N_per_gpu": nloc, "nnz": A.nnz, "storage": A.storage,
-                       "m": wl["m"], "k": wl["k"], "t": wl["t"], "s": wl["s"], "tol": wl["tol"],
-                       "max_restarts": wl["max_restarts"], "sketch": wl["sketch"],
-                       "parallelism": f"zslab{world}",
-                       **({"transport": "host-staged test transport (SDR_BENCH_HOSTCOMM, ranks share GPU 0)"}
-                          if hostcomm else {}),
-                       "l2": "inputs larger than L2 (Krylov basis (m+1) x 8N bytes per cycle, no L2 flush)"},
+            "config": workload_config(args.config, wl, world),
+            "storage": dict(A.storage, rank0_rows=nloc, rank0_nnz=A.nnz),
+            **({"transport": "host-staged test transport (SDR_BENCH_HOSTCOMM, ranks share GPU 0)"} if hostcomm else {}),
             "time_to_solution_ms": solve_ms,
             "solve": {"status": rep.status, "iterations": rep.iterations, "cycles": rep.cycles,
                       "final_relative_residual": rep.final_relative_residual,
