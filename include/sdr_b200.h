@@ -248,9 +248,9 @@ typedef enum {
 } sdr_provenance;
 
 /* SolverConfig (solver.hpp:48-79); sdr_config_default fills the reference defaults.
- * Validation is the reference's plus one device limit: the Arnoldi window
- * min(t, m) must not exceed 33 (the fused MGS kernels hold it in registers;
- * the reference accepts any t >= 1) — rejected with SDR_EINVAL. */
+ * Validation is the reference's. Any window t >= 1 is accepted as there:
+ * min(t, m) <= 33 runs the fused step kernels (the window lives in
+ * registers), longer windows the unfused passes of wide.cu. */
 typedef struct {
   int64_t m, t, k, s;
   double tol, safety_init;

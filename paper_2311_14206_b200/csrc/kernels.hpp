@@ -97,6 +97,17 @@ void launch_spmv_guarded(Context& c, const SellView& A, const double* x_ext, dou
 void launch_update(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
                    int ngram, double* rec, const RecLayout& L, double* cvec, const double* coef_ready);
 void launch_copy_norm(Context& c, const double* src, double* dst, int64_t n, double* norm2);
+// ---- Long truncation windows (wide.cu): min(t, m) > kFusedWindowMax, the
+// largest window the fused step kernels keep in registers.
+constexpr int kFusedWindowMax = 33;
+/// out = [x.x (self)] then x.V(:, c0 - q) for q < nq (own parts), folded.
+void launch_window_dots_wide(Context& c, const double* x, const double* V, int64_t ldv, int64_t own_off, int c0,
+                             int nq, bool self, int64_t n, double* out);
+/// Step j's modified Gram-Schmidt loop (arnoldi.hpp:91-97) as streaming
+/// passes: w_{j+1} = A v_j - sum h v over the window, record H part, cvec[j].
+/// dots: device scratch of nwin + 1 values (reduced over ranks).
+void launch_mgs_wide(Context& c, const double* y, double* V, int64_t ldv, const VecLayout& lay, int j, int nwin,
+                     double* rec, int64_t rstride, int T, double* cvec, double* dots);
 void launch_axpy(Context& c, double a, const double* x, double* y, int64_t n);
 /// C = [A1 A2] B (column-major; B is (k1+k2) x nout with leading dim k1+k2)
 /// in one pass over the inputs, norms2[o] = ||C(:, o)||^2 (deterministic).

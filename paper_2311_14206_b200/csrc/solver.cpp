@@ -203,7 +203,7 @@ Workspace& workspace(Context& c, const VecLayout& lay, i64 m, i64 s, int T) {
   w->tmp.ensure(lay.ld);
   w->scal.ensure(64);
   w->unorm.ensure(32);
-  w->coef_dev.ensure(64);
+  w->coef_dev.ensure(std::max<i64>(64, T + 2));
   w->hscal.ensure(64);
   return *w;
 }
@@ -433,6 +433,7 @@ struct ArnoldiPipeline {
   // sketch rows of w_{j+1}) is reduced together with K1(j+1)'s dots — one
   // allreduce per step over the contiguous record span [B_{j+1} | A_{j+2}]
   bool merge_b = false;
+  bool wide = false;  // min(t, m) > kFusedWindowMax: enqueue_wide
   StepFold last;  // partials K2(issued - 1) left
   i64 last_ngram = 0, last_j = -1;
   double* pend_buf = nullptr;  // several ranks: K2's folded partials not yet allreduced
@@ -499,6 +500,12 @@ struct ArnoldiPipeline {
   int pu_G[2] = {0, 0}, ps_G[2] = {0, 0}, ps_ld[2] = {0, 0};
 
   void setup_deferred() {
+    // windows past the fused kernels' register capacity: unfused step (wide.cu)
+    wide = std::min(t, m) > kFusedWindowMax;
+    if (wide) {
+      deferred = split = merge_b = false;
+      return;
+    }
     const int need = static_cast<int>(std::max<i64>(std::min(t, m), std::min<i64>(w.RL.T - 1, m) + 1));
     static const bool defer_dist = [] {
       const char* e = std::getenv("SDR_DEFER_DIST");
@@ -563,6 +570,10 @@ struct ArnoldiPipeline {
     double* recj = w.rec.get() + (j + 1) * R;
     if (split) {
       enqueue_split(j, nwin, ngram);
+      return;
+    }
+    if (wide) {
+      enqueue_wide(j, nwin, ngram);
       return;
     }
     if (deferred) {
@@ -685,6 +696,28 @@ struct ArnoldiPipeline {
       SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
       return;
     }
+    c.allreduce_sum(recj + RL.b_off(), RL.b_len());
+    SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
+    w.copy_back(c, w.hrec.get() + (j + 1) * R, recj, R, w.evk[static_cast<size_t>(j + 1)],
+                w.ev[static_cast<size_t>(j + 1)]);
+  }
+
+  /// Long window (min(t, m) > kFusedWindowMax): the step as separate passes
+  /// (wide.cu) — product, the literal MGS loop (one pass and one reduced dot
+  /// per window column), norm / Gram, sketch — into the same record layout.
+  void enqueue_wide(i64 j, int nwin, int ngram) {
+    const VecLayout& lay = w.lay;
+    const RecLayout& RL = w.RL;
+    const i64 R = RL.stride;
+    double* Vb = w.V[vb].get();
+    double* recj = w.rec.get() + (j + 1) * R;
+    c.halo_exchange(A.plan, w.Vbuf(vb, j) + lay.ext_shift(), A.ext_begin, w.Vcol(vb, j), A.row_begin);
+    launch_spmv(c, A.view(), w.Vbuf(vb, j) + lay.ext_shift(), w.y.get());
+    launch_mgs_wide(c, w.y.get(), Vb, lay.ld, lay, static_cast<int>(j), nwin, w.rec.get(), R, RL.T, w.cvec.get(),
+                    w.coef_dev.get());
+    launch_window_dots_wide(c, w.Vcol(vb, j + 1), Vb, lay.ld, lay.own_off, static_cast<int>(j), ngram, true, lay.nloc,
+                            recj + RL.b_off());
+    launch_sketch(c, S, w.Vcol(vb, j + 1), lay.nloc, A.row_begin, recj + RL.sketch_off());
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
     SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
     w.copy_back(c, w.hrec.get() + (j + 1) * R, recj, R, w.evk[static_cast<size_t>(j + 1)],
@@ -1393,7 +1426,6 @@ void krylov_run(Context& c, const DeviceOperator& A, const SketchDev& S, const d
   if (S.n != A.rows)
     throw invalid("init_krylov: residual length " + std::to_string(A.rows) + " does not match sketch input " +
                   std::to_string(S.n));
-  if (std::min(t, m) > 33) throw invalid("init_krylov: window min(t, m) exceeds the device limit of 33");
   init_host_blas();
   const VecLayout lay = A.layout();
   Workspace& w = workspace(c, lay, m, S.s, static_cast<int>(std::min(t, m)));
@@ -1469,7 +1501,6 @@ void solve(Context& c, const DeviceOperator& A, const double* b, const double* x
   auto pt_setup = std::make_unique<PhaseTimer>(rep, "setup");
   const VecLayout lay = A.layout();
   const int T = static_cast<int>(std::min<i64>(cfg.t, cfg.m));
-  if (std::min<i64>(cfg.t, cfg.m) > 33) throw invalid("solve: Arnoldi window min(t, m) exceeds the device limit of 33");
   Workspace& w = workspace(c, lay, cfg.m, sketch->s, T);
   space.n = A.rows;
   space.s = sketch->s;

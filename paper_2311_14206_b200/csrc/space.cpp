@@ -21,11 +21,6 @@ void Config::validate() const {  // solver.hpp:61-78
   if (max_restarts < 1) throw invalid("SolverConfig: max_restarts must be at least 1");
   if (!(rank_tol >= 0.0)) throw invalid("SolverConfig: rank_tol must be >= 0");
   if (!(breakdown_tol >= 0.0)) throw invalid("SolverConfig: breakdown_tol must be >= 0");
-  // device limit, not the reference's (which accepts any t >= 1): the fused
-  // MGS kernels keep the window's dots and coefficients in registers
-  if (std::min(t, m) > 33)
-    throw invalid("SolverConfig: Arnoldi window min(t, m) = " + std::to_string(std::min(t, m)) +
-                  " exceeds the device limit of 33");
 }
 
 void Recycle::drop_columns(const std::vector<i64>& cols) {  // recycle.hpp:48-71
