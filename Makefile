@@ -13,7 +13,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -I/usr/local/cuda/include
 CXXFLAGS := -O3 -std=c++17 -fPIC -fvisibility=hidden -Wall -Wextra -Wno-unused-parameter -I/usr/local/cuda/include
 
-CU := spmv arnoldi sketch sparse_update tsmm wide operator baseline peer
+CU := spmv arnoldi sketch sparse_update fused_step tsmm wide operator baseline peer
 CC := context host_linalg space solver baseline_host io capi
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .cu.o,$(CU)) $(addsuffix .o,$(CC)))
 HDRS := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh) include/sdr_b200.h

@@ -153,6 +153,17 @@ bool update_sparse_eligible(const SketchDev& S, const VecLayout& lay, const RecL
 void launch_update_sparse(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv,
                           const VecLayout& lay, int j, int nwin, int ngram, double* rec, const RecLayout& RL,
                           double* cvec, const double* coef_ready, int64_t row_begin);
+/// KF (fused_step.cu, one GPU, SELL-DIA, sparse sign, t <= 3): the update +
+/// sketch of step j and the SpMV + window dots of step j+1 in one launch
+/// (y_in = y_j, y_out = y_{j+1}, distinct buffers), then a one-CTA fold into
+/// record rows j+1 (B) and j+2 (A) that forms step j+1's coefficients in coef.
+/// chunk_done: fused_step_chunks() counters (zeroed per launch).
+bool fused_step_eligible(const SellView& A, const SketchDev& S, const VecLayout& lay, const RecLayout& RL, int t,
+                         bool distributed);
+int64_t fused_step_chunks(const Context& c, int64_t nloc);
+void launch_fused_step(Context& c, const SellView& A, const SketchDev& S, const double* y_in, double* y_out, double* V,
+                       int64_t ldv, const VecLayout& lay, int j, int nwin, int ngram, int nwin1, double* rec,
+                       const RecLayout& RL, double* cvec, double* coef, int64_t row_begin, unsigned* chunk_done);
 /// Builds SketchDev::tab / uq (per-row SRDCT constants) once per sketch.
 void prepare_srdct_tables(Context& c, SketchDev& S);
 /// Deferred folds of the one-GPU step pipeline: K1(j) leaves its window dots

@@ -66,6 +66,8 @@ struct Workspace {
   DeviceBuffer<double> V[2];
   int nV = 0;
   DeviceBuffer<double> y, rec, cvec, corr, r0, rnew, x, tmp, scal, coef, coef_dev;
+  DeviceBuffer<double> y2;            // KF step pipeline: y_{j+1} beside y_j (by step parity)
+  DeviceBuffer<unsigned> chunk_done;  // KF: per-chunk completion counters of the update front
   DeviceBuffer<double> unorm;  // ||.||^2 of the fused restart pass's outputs (correction, U_new)
   DeviceBuffer<double> one;    // {1.0}: coefficient of a cycle's first column (w_0 = r0)
   double last_harmonic_ms = -1.0;  // host time of the previous cycle's harmonic pencil
@@ -434,6 +436,8 @@ struct ArnoldiPipeline {
   // allreduce per step over the contiguous record span [B_{j+1} | A_{j+2}]
   bool merge_b = false;
   bool wide = false;  // min(t, m) > kFusedWindowMax: enqueue_wide
+  // one GPU, sparse sign, SELL-DIA: update(j) and SpMV(j+1) in one launch (KF, enqueue_fused)
+  bool fused = false;
   StepFold last;  // partials K2(issued - 1) left
   i64 last_ngram = 0, last_j = -1;
   double* pend_buf = nullptr;  // several ranks: K2's folded partials not yet allreduced
@@ -502,6 +506,7 @@ struct ArnoldiPipeline {
   void setup_deferred() {
     // windows past the fused kernels' register capacity: unfused step (wide.cu)
     wide = std::min(t, m) > kFusedWindowMax;
+    fused = false;
     if (wide) {
       deferred = split = merge_b = false;
       return;
@@ -529,6 +534,11 @@ struct ArnoldiPipeline {
     }
     split = deferred && !c.distributed() && split_pipeline() && sketch_partials_eligible(S, w.lay.nloc, A.row_begin);
     merge_b = !deferred && c.distributed();
+    fused = !deferred && m >= 2 && fused_step_eligible(A.view(), S, w.lay, w.RL, static_cast<int>(t), c.distributed());
+    if (fused) {
+      w.y2.ensure(std::max<i64>(w.lay.nloc, 1));
+      w.chunk_done.ensure(fused_step_chunks(c, w.lay.nloc));
+    }
     if (!deferred && c.distributed() && !A.apply) {
       // several ranks, non-deferred steps (sparse sign): K1's interior slices
       // still run beside the halo transfer (enqueue)
@@ -574,6 +584,10 @@ struct ArnoldiPipeline {
     }
     if (wide) {
       enqueue_wide(j, nwin, ngram);
+      return;
+    }
+    if (fused) {
+      enqueue_fused(j, nwin, ngram);
       return;
     }
     if (deferred) {
@@ -697,6 +711,35 @@ struct ArnoldiPipeline {
       return;
     }
     c.allreduce_sum(recj + RL.b_off(), RL.b_len());
+    SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
+    w.copy_back(c, w.hrec.get() + (j + 1) * R, recj, R, w.evk[static_cast<size_t>(j + 1)],
+                w.ev[static_cast<size_t>(j + 1)]);
+  }
+
+  /// KF step (one GPU, sparse sign, SELL-DIA): K1(0) alone at j = 0, then
+  /// per step one launch doing the update + sketch of step j and the SpMV +
+  /// window dots of step j+1 (fused_step.cu) and a one-CTA fold that writes
+  /// record rows j+1 (B) and j+2 (A) and forms step j+1's coefficients; the
+  /// cycle's last step is K2s alone. y_j alternates between two buffers.
+  void enqueue_fused(i64 j, int nwin, int ngram) {
+    const VecLayout& lay = w.lay;
+    const RecLayout& RL = w.RL;
+    const i64 R = RL.stride;
+    double* Vb = w.V[vb].get();
+    double* yj = (j & 1) ? w.y2.get() : w.y.get();
+    double* yn = (j & 1) ? w.y.get() : w.y2.get();
+    double* recj = w.rec.get() + (j + 1) * R;
+    if (j == 0)  // K1(0); its last CTA forms step 0's coefficients
+      launch_spmv_arnoldi(c, A.view(), Vb, lay.ld, lay, 0, nwin, yj, recj + RL.a_off(), w.rec.get(), R, RL.T,
+                          w.cvec.get(), w.coef_dev.get());
+    if (j + 1 < m) {
+      const int nwin1 = static_cast<int>(std::min<i64>(t, j + 2));
+      launch_fused_step(c, A.view(), S, yj, yn, Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, nwin1, w.rec.get(),
+                        RL, w.cvec.get(), w.coef_dev.get(), A.row_begin, w.chunk_done.get());
+    } else {
+      launch_update_sparse(c, S, yj, Vb, lay.ld, lay, static_cast<int>(j), nwin, ngram, w.rec.get(), RL, w.cvec.get(),
+                           w.coef_dev.get(), A.row_begin);
+    }
     SDR_CUDA(cudaEventRecord(w.evd[static_cast<size_t>(j)], c.stream));
     w.copy_back(c, w.hrec.get() + (j + 1) * R, recj, R, w.evk[static_cast<size_t>(j + 1)],
                 w.ev[static_cast<size_t>(j + 1)]);
