@@ -107,8 +107,8 @@ __device__ __forceinline__ double slice_row_sum(const SellView& A, const double*
   return s;
 }
 
-template <int MODE, int NV, int FMT>
-__global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : 3) k_sell_spmv(SellView A, const double* __restrict__ x_ext,
+template <int MODE, int NV, int FMT, int MB = 3>
+__global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : MB) k_sell_spmv(SellView A, const double* __restrict__ x_ext,
                                                                          double* __restrict__ y,
                                                                          const double* __restrict__ aux, int64_t ldv,
                                                                          int64_t own_off, int64_t halo_lo, int j,
@@ -409,8 +409,21 @@ template <int MODE, int NV, int FMT>
 int launch_impl(Context& c, const char* name, const SellView& A, const double* x_ext, double* y, const double* aux,
                 int64_t ldv, int64_t own_off, int64_t halo_lo, int j, int nwin, unsigned* counter, double* out,
                 const MgsArgs& mg, double* partials_out, int max_per_sm, int64_t sl_begin, int64_t sl_end) {
-  auto kern = A.cplx ? k_zsell_spmv<MODE, NV> : k_sell_spmv<MODE, NV, FMT>;
-  const int g = resident_grid(c, kern, blocks_for(std::max<int64_t>(sl_end - sl_begin, 1)), max_per_sm);
+  // CTAs per SM: 4 (64 registers) when each warp has few slices to walk —
+  // latency-bound (C3 1 M rows: K1 16.1 -> 14.2 us; C2: 33.2 -> 31.2 us in-solve),
+  // 3 (77 registers, deeper per-warp pipelining) on long sweeps (C5: 1848 vs
+  // 1908 us). SDR_K1_MINB=3/4 forces one.
+  static const int minb_env = [] {
+    const char* e = std::getenv("SDR_K1_MINB");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int64_t nsl = std::max<int64_t>(sl_end - sl_begin, 1);
+  // (several ranks: always 3 — slab sizes differ per rank and grids / partial
+  // layouts must not depend on them)
+  const int minb = minb_env ? minb_env
+                            : (!c.distributed() && nsl <= static_cast<int64_t>(c.num_sms) * 32 * 64 ? 4 : 3);
+  auto kern = A.cplx ? k_zsell_spmv<MODE, NV> : (minb == 4 ? k_sell_spmv<MODE, NV, FMT, 4> : k_sell_spmv<MODE, NV, FMT>);
+  const int g = resident_grid(c, kern, blocks_for(nsl), max_per_sm);
   double* part = partials_out ? partials_out : ((MODE == 1 || MODE == 2) ? c.partials(static_cast<int64_t>(NV) * g) : nullptr);
   TimedLaunch t(c, name);
   if (partials_out) {  // deferred step pipeline: programmatic dependent launch
