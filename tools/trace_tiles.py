@@ -13,12 +13,18 @@ import paper_2311_14206_b200 as sk  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--n", type=int, default=128)
+ap.add_argument("--c3", action="store_true", help="C3's 1024^2 2-D operator, s = 140")
 args = ap.parse_args()
 assert os.environ.get("SDR_TRACE") == "1"
 ctx = sk.default_context()
-A = sk.SparseMatrix.convdiff3d_device(args.n, 100.0, 50.0, 25.0)
+if args.c3:
+    off, col, val = sk.gen_convdiff2d(1024, 100.0, 100.0)
+    A = sk.SparseMatrix(1 << 20, 1 << 20, off, col, val, ctx=ctx)
+    S = sk.SketchOperator.subsampled_dct(A.rows, 140, 0x5EED)
+else:
+    A = sk.SparseMatrix.convdiff3d_device(args.n, 100.0, 50.0, 25.0)
+    S = sk.SketchOperator.subsampled_dct(A.rows, 240, 0x5EED)
 b = sk.gaussian_vector(A.rows, 1)
-S = sk.SketchOperator.subsampled_dct(A.rows, 240, 0x5EED)
 j, br, rn = C.c_int64(), C.c_int(), C.c_double()
 for rep in range(1):
     sk._check(sk._lib.sdr_krylov_run(ctx._h, A._h, S._h, b.ctypes.data_as(C.c_void_p), 2, 100, args.steps, 1e-14,
