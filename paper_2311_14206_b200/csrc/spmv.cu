@@ -39,6 +39,10 @@ struct MgsArgs {
   int T = 0;
   double* cvec = nullptr;
   double* coef = nullptr;  // null: coefficients are formed later (after an allreduce)
+  // window columns loaded without the evict-first hint: on one GPU when a
+  // step's vectors fit in L2, so the update kernel that follows re-reads
+  // w_{j-1} from L2 (C2: K2 26.5 -> 25.1 us in-solve; C3 14.7 -> 14.5 us)
+  int wkeep = 0;
 };
 
 /// Row sums of one 32-row slice (lane = row), CSR order.
@@ -129,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : MB) k_sell_spmv(SellVie
   // iteration ahead, so no load of the current slice waits on an index load
   const int D = FMT > 0 ? FMT : (FMT < 0 ? A.dia_d : 0);
   int nx_off = 0;
+  const bool wkeep = mg.wkeep != 0;
   pdl_trigger();  // the next kernel may start its constant-data prologue
   pdl_wait();     // x / the window vectors come from the previous kernel
   if constexpr (MODE == 3)
@@ -148,7 +153,10 @@ __global__ void __launch_bounds__(kThreads, NV > 8 ? 1 : MB) k_sell_spmv(SellVie
     if constexpr (MODE == 1) {
       e0 = live ? x_ext[halo_lo + row] : 0.0;
 #pragma unroll
-      for (int d = 1; d < NV - 1; ++d) ew[d - 1] = (live && d < nwin) ? __ldcs(aux + (j - d) * ldv + own_off + row) : 0.0;
+      for (int d = 1; d < NV - 1; ++d) {
+        const double* wp = aux + (j - d) * ldv + own_off + row;
+        ew[d - 1] = (live && d < nwin) ? (wkeep ? __ldg(wp) : __ldcs(wp)) : 0.0;
+      }
     } else if constexpr (MODE == 2) {
       e0 = live ? __ldcs(aux + row) : 0.0;
     }
@@ -473,7 +481,20 @@ void launch_spmv(Context& c, const SellView& A, const double* x_ext, double* y) 
 int launch_spmv_arnoldi(Context& c, const SellView& A, const double* V, int64_t ldv, const VecLayout& lay, int j,
                         int nwin, double* y, double* recA, double* rec, int64_t rstride, int T, double* cvec,
                         double* coef, double* partials_out, int max_per_sm, int64_t sl_begin, int64_t sl_end) {
-  const MgsArgs mg{rec, rstride, T, cvec, coef};
+  static const int wkeep_env = [] {
+    const char* e = std::getenv("SDR_K1_WKEEP");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const int64_t l2_bytes = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return int64_t{0};
+    }
+    return static_cast<int64_t>(v);
+  }();
+  MgsArgs mg{rec, rstride, T, cvec, coef};
+  mg.wkeep = wkeep_env >= 0 ? wkeep_env : (!c.distributed() && 4 * 8 * lay.nloc <= l2_bytes ? 1 : 0);
   const double* x_ext = V + j * ldv + lay.ext_shift();
   if (A.apply) {  // y = A w_j by the caller's function, then the window dots
     if (sl_begin != 0 || (sl_end >= 0 && sl_end != A.nslices)) throw logic("callable operator: no split SpMV");
