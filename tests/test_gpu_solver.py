@@ -444,3 +444,30 @@ def test_long_cycles_and_wide_recycle_spaces(sk, O, m, k, t):
     assert_same_solve(g, o, iters_tol=0.02)
     if o[1].status == "converged":
         assert np.linalg.norm(b - Ao.apply(g.x)) <= 1e-10 * np.linalg.norm(b) * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("seed,n,m,k,t,kind", [(81, 300, 30, 0, 1, "ss"), (82, 300, 30, 0, 1, "dct"),
+                                               (86, 150, 15, 4, 3, "ss")])
+def test_failed_verification_continues_the_cycle(sk, O, seed, n, m, k, t, kind):
+    """A trigger whose true residual misses the tolerance (safety_init = 1):
+    the safety factor ratchets and the same cycle goes on (solver.hpp:199-216)
+    — two true-residual checks in one cycle, the first correction discarded.
+    Status, iterations, cycles, every true residual and x equal the oracle's."""
+    M = random_matrix(O, n, seed)
+    A, Ao = both(sk, O, M)
+    b = O.gaussian_vector(n, seed + 1000)
+    s = 2 * (m + k)
+    c, co = cfgs(sk, O, m=m, t=t, k=k, s=s, tol=1e-10, safety_init=1.0, max_restarts=10)
+    if kind == "ss":
+        S, So = sk.SketchOperator.sparse_sign(n, s, 7, 8), O.SketchOperator.sparse_sign(n, s, 7, 8)
+    else:
+        S, So = sk.SketchOperator.subsampled_dct(n, s, 7), O.SketchOperator.subsampled_dct(n, s, 7)
+    g = sk.solve(A, b, c, sketch=S)
+    xo, ro = O.solve(Ao, b, co, sketch=So)
+    assert len(ro.true_residuals) > ro.cycles  # the oracle took the failed-check path
+    assert g.report.status == ro.status and g.report.iterations == ro.iterations and g.report.cycles == ro.cycles
+    assert len(g.report.true_residuals) == len(ro.true_residuals)
+    for (i1, v1), (i2, v2) in zip(g.report.true_residuals, ro.true_residuals):
+        assert i1 == i2 and v1 == pytest.approx(v2, rel=1e-6, abs=1e-13 * np.linalg.norm(b))
+    assert rel(g.x, xo) <= 1e-9
+    assert np.linalg.norm(b - M @ g.x) <= 1e-10 * np.linalg.norm(b) * (1 + 1e-6)
