@@ -1092,8 +1092,11 @@ class SequenceResult:
 
 
 def solve_sequence(problems, cfg: SolverConfig, sketch: SketchOperator | None = None,
-                   initial_space: RecycleSpace | None = None, shared_matrix: bool = False) -> SequenceResult:
-    """solver.hpp:385-459 (matrix change detected by object identity)."""
+                   initial_space: RecycleSpace | None = None, shared_matrix: bool = False,
+                   outs=None) -> SequenceResult:
+    """solver.hpp:385-459 (matrix change detected by object identity).
+    outs: optional per-system solution buffers (numpy arrays or CUDA float64
+    tensors of the system's length, written in place); default new numpy arrays."""
     n = len(problems)
     if n == 0:
         cfg.validate()
@@ -1114,9 +1117,18 @@ def solve_sequence(problems, cfg: SolverConfig, sketch: SketchOperator | None = 
             k0, p0, _ = _ptr(p.x0)
             keep.append(k0)
             x0s[i] = p0
-        x = np.zeros(nb)
-        xs.append(x)
-        xo[i] = x.ctypes.data_as(C.c_void_p)
+        if outs is not None:
+            if len(outs) != n:
+                raise ValueError("solve_sequence: outs needs one buffer per problem")
+            ko, po, no = _ptr(outs[i])
+            if no != nb or ko is not outs[i]:  # a copy would be written instead of the caller's buffer
+                raise ValueError("solve_sequence: outs[%d] must be a contiguous float64 buffer of length %d" % (i, nb))
+            xs.append(outs[i])
+            xo[i] = po
+        else:
+            x = np.zeros(nb)
+            xs.append(x)
+            xo[i] = x.ctypes.data_as(C.c_void_p)
     tols = np.array([p.target_tol for p in problems], dtype=np.float64)
     reps = (C.c_void_p * n)()
     c = cfg.c()

@@ -4,8 +4,9 @@ N = 1024^2 2-D convection-diffusion, system i: beta = (100+2i, 100-2i), shift
 0x3100+i), b_i = b_0 + 0.05 xi_i (gaussian seeds 0x3000 / 0x3000+i),
 m=50 k=20 t=2 s=140 tol=1e-8, variant exact (refresh on every matrix change).
 Same seeds and construction as tests/golden/make_golden.py c3_small.
-Prints one JSON line: total Arnoldi steps / sequence wall time.
-Usage: python tools/bench_sequence.py [--n 1024] [--count 20] [--steps 2]"""
+Prints one JSON line: total Arnoldi steps / sequence wall time, with b and
+x in HBM (`value`) and through host numpy arrays (`e2e`; --host: only that).
+Usage: python tools/bench_sequence.py [--n 1024] [--count 20] [--steps 2] [--host]"""
 import argparse
 import json
 import os
@@ -22,6 +23,7 @@ ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--count", type=int, default=20)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--warmup", type=int, default=1)
+ap.add_argument("--host", action="store_true", help="right-hand sides and solutions in host memory (e2e only)")
 args = ap.parse_args()
 n, count = args.n, args.count
 N = n * n
@@ -45,17 +47,36 @@ for i in range(count):
 setup_s = time.time() - t0
 cfg = sk.SolverConfig(m=50, k=20, t=2, s=140, tol=1e-8, variant="exact")
 S = sk.SketchOperator.subsampled_dct(N, 140, cfg.sketch_seed, ctx=ctx)
-for _ in range(args.warmup):
-    sk.solve_sequence(probs, cfg, sketch=S)
-ctx.synchronize()
-walls, iters, out = [], 0, None
-for _ in range(args.steps):
-    t1 = time.perf_counter()
-    out = sk.solve_sequence(probs, cfg, sketch=S)
+probs_host = probs
+outs = None
+if not args.host:
+    # value: b and x resident in HBM (as bench.py's `value`); e2e below with host arrays
+    import torch
+    probs = [sk.ProblemInstance(p.matrix, torch.from_numpy(p.rhs).cuda()) for p in probs_host]
+    outs = [torch.zeros(N, dtype=torch.float64, device="cuda") for _ in probs]
+
+
+def run(ps, o):
+    walls, iters, out = [], 0, None
+    for _ in range(args.warmup):
+        sk.solve_sequence(ps, cfg, sketch=S, outs=o)
     ctx.synchronize()
-    walls.append(time.perf_counter() - t1)
-    iters += sum(r.iterations for r in out.reports)
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        out = sk.solve_sequence(ps, cfg, sketch=S, outs=o)
+        ctx.synchronize()
+        walls.append(time.perf_counter() - t1)
+        iters += sum(r.iterations for r in out.reports)
+    return walls, iters, out
+
+
+walls, iters, out = run(probs, outs)
 total = sum(walls)
+e2e = None
+if not args.host:
+    w2, i2, _ = run(probs_host, None)
+    e2e = {"value": i2 / sum(w2), "unit": "steps/s", "h2d_bytes_per_step": 8 * N * count,
+           "d2h_bytes_per_step": 8 * N * count, "path": "solve_sequence with host (pageable numpy) b and x"}
 phases = {}
 for r in out.reports:
     for k, v in r.phases.items():
@@ -66,6 +87,8 @@ line = {
     "dtype": "f64", "data": "synthetic (BASELINE C3 construction, seeded)",
     "config": {"workload": "c3", "N": N, "systems": count, "m": 50, "k": 20, "t": 2, "s": 140, "tol": 1e-8,
                "variant": "exact", "storage": probs[0].matrix.storage},
+    "residency": "host b / x" if args.host else "b / x in HBM",
+    "e2e": e2e,
     "sequence": {"iterations": [r.iterations for r in out.reports], "status": [r.status for r in out.reports],
                  "cycles": [r.cycles for r in out.reports],
                  "final_relative_residual": [r.final_relative_residual for r in out.reports],
