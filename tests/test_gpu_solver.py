@@ -471,3 +471,25 @@ def test_failed_verification_continues_the_cycle(sk, O, seed, n, m, k, t, kind):
         assert i1 == i2 and v1 == pytest.approx(v2, rel=1e-6, abs=1e-13 * np.linalg.norm(b))
     assert rel(g.x, xo) <= 1e-9
     assert np.linalg.norm(b - M @ g.x) <= 1e-10 * np.linalg.norm(b) * (1 + 1e-6)
+
+
+def test_sequence_device_resident_rhs_and_solutions(sk, O):
+    """solve_sequence with CUDA right-hand sides and caller-owned CUDA solution
+    buffers (written in place) gives the host-array run's solutions bit for bit."""
+    import torch
+    n = 400
+    M1, M2 = O.gen_neumann(20, 0.5).dense(), O.gen_neumann(20, 0.7).dense()
+    A1, A2 = sk.SparseMatrix.from_dense(M1), sk.SparseMatrix.from_dense(M2)
+    rhs = [O.gaussian_vector(n, 700 + i) for i in range(3)]
+    c, _ = cfgs(sk, O, m=30, k=8, t=2, s=80, tol=1e-8, variant="exact")
+    host = sk.solve_sequence([sk.ProblemInstance(A1, rhs[0]), sk.ProblemInstance(A2, rhs[1]),
+                              sk.ProblemInstance(A2, rhs[2])], c)
+    outs = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(3)]
+    dev = sk.solve_sequence([sk.ProblemInstance(A, torch.from_numpy(b).cuda())
+                             for A, b in zip((A1, A2, A2), rhs)], c, outs=outs)
+    for i in range(3):
+        assert dev.solutions[i] is outs[i]
+        assert dev.reports[i].iterations == host.reports[i].iterations
+        assert np.array_equal(outs[i].cpu().numpy(), host.solutions[i])
+    with pytest.raises(ValueError):
+        sk.solve_sequence([sk.ProblemInstance(A1, rhs[0])], c, outs=[np.zeros(n - 1)])
