@@ -111,6 +111,11 @@ Context::~Context() {
     cudaEventDestroy(p.b);
   }
   for (auto e : free_events_) cudaEventDestroy(e);
+  for (int i = 0; i < kAuxStreams; ++i) {
+    if (aux_ev_[i]) cudaEventDestroy(aux_ev_[i]);
+    if (aux_[i]) cudaStreamDestroy(aux_[i]);
+  }
+  if (fork_ev_) cudaEventDestroy(fork_ev_);
   if (open_start_) cudaEventDestroy(open_start_);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -232,6 +237,27 @@ void Context::halo_exchange(const HaloPlan& plan, double* x_ext, i64 ext_begin, 
   }
   SDR_NCCL(nccl_->GroupEnd());
   if (timed) time_end();
+}
+
+cudaStream_t Context::aux_stream(int i) {
+  if (!aux_[i]) {
+    SDR_CUDA(cudaStreamCreateWithFlags(&aux_[i], cudaStreamNonBlocking));
+    SDR_CUDA(cudaEventCreateWithFlags(&aux_ev_[i], cudaEventDisableTiming));
+  }
+  return aux_[i];
+}
+
+void Context::aux_fork(int n) {
+  if (!fork_ev_) SDR_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+  SDR_CUDA(cudaEventRecord(fork_ev_, stream));
+  for (int i = 0; i < n; ++i) SDR_CUDA(cudaStreamWaitEvent(aux_stream(i), fork_ev_, 0));
+}
+
+void Context::aux_join(int n) {
+  for (int i = 0; i < n; ++i) {
+    SDR_CUDA(cudaEventRecord(aux_ev_[i], aux_stream(i)));
+    SDR_CUDA(cudaStreamWaitEvent(stream, aux_ev_[i], 0));
+  }
 }
 
 cudaEvent_t Context::take_event() {

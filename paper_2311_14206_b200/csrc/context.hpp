@@ -109,6 +109,16 @@ class Context {
 
   void sync() { SDR_CUDA(cudaStreamSynchronize(stream)); }
 
+  /// Auxiliary streams for independent small launches (created once per
+  /// context): aux_stream(i) for i < kAuxStreams, each with an event that
+  /// aux_join() records and makes the main stream wait on.
+  static constexpr int kAuxStreams = 4;
+  cudaStream_t aux_stream(int i);
+  /// aux streams [0, n) wait for the main stream's work so far
+  void aux_fork(int n);
+  /// the main stream waits for aux streams [0, n)
+  void aux_join(int n);
+
   /// C (n x nout, ldc) = beta C + A (n x k, lda) B (k x nout, ldb), column-major
   /// fp64 on the context stream through cuBLAS (plain tall-skinny GEMM of the
   /// recycle update; deterministic for a fixed GPU).
@@ -120,6 +130,8 @@ class Context {
 
  private:
   DeviceBuffer<double> partials_, partials2_, stage_;
+  cudaStream_t aux_[kAuxStreams] = {};
+  cudaEvent_t aux_ev_[kAuxStreams] = {}, fork_ev_ = nullptr;
   DeviceBuffer<unsigned> counters_;
   DeviceBuffer<unsigned long long> trace_, stamps_;
   std::vector<std::string> stamp_names_;

@@ -213,6 +213,8 @@ int64_t update_split_partials_size(int num_sms);
 /// SRDCT CTA partials of x (two tile groups per CTA, no fold); G / ld out.
 void launch_sketch_partials(Context& c, const SketchDev& S, const double* x_own, int64_t nloc, int64_t row_begin,
                             double* partials, int* G, int* ld);
+/// out[0, s) = the sketch rows folded from launch_sketch_partials' CTA partials.
+void launch_sketch_fold_partials(Context& c, const SketchDev& S, const double* partials, int G, int ld, double* out);
 /// K2' (update alone) with the deferred prologue; returns its grid size.
 int launch_update_split(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,
                         int j, int nwin, int ngram, double* rec, const RecLayout& RL, double* cvec, const SplitFold& sf);

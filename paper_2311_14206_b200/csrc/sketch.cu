@@ -1296,6 +1296,13 @@ void launch_sketch_partials(Context& c, const SketchDev& S, const double* x_own,
   *ld = sf.out_nvp;
 }
 
+void launch_sketch_fold_partials(Context& c, const SketchDev& S, const double* partials, int G, int ld, double* out) {
+  TimedLaunch t(c, "sketch_fold");
+  k_srdct_fold<kSrcSketch><<<static_cast<int>((S.s + 7) / 8), 256, 0, c.stream>>>(
+      partials, G, ld, static_cast<int>(S.s), S.tab.get(), S.row_scale.get(), out, UpdateArgs{}, 1);
+  SDR_KERNEL_CHECK();
+}
+
 int64_t update_split_partials_size(int num_sms) { return static_cast<int64_t>(kNgLd) * num_sms * 8; }
 
 int launch_update_split(Context& c, const SketchDev& S, const double* y, double* V, int64_t ldv, const VecLayout& lay,

@@ -1,5 +1,6 @@
 // Recycle-space bookkeeping (recycle.hpp:31-72, 297-318), solver config
 // validation (solver.hpp:61-78) and sketch construction (sketch.hpp:105-132).
+#include <cstdlib>
 #include "solver.hpp"
 
 #include <algorithm>
@@ -140,7 +141,12 @@ void refresh_recycle(Context& c, Recycle& sp, const DeviceOperator& A, const Ske
   const VecLayout lay = A.layout();
   const i64 k = sp.dim();
   const bool in_place = lay.halo_lo == 0 && lay.halo_hi == 0 && lay.own_off == 0;
-  DeviceBuffer<double> ubuf(in_place ? 1 : lay.ld), au(std::max<i64>(lay.nloc, 1) * k), sk(S.s * k);
+  // (small scratch from the context: a cudaFree per refresh would synchronise the device)
+  DeviceBuffer<double> ubuf(in_place ? 0 : lay.ld), au(std::max<i64>(lay.nloc, 1) * k);
+  struct {
+    double* p;
+    double* get() const { return p; }
+  } sk{c.stage(S.s * k)};  // (not partials(): the one-vector sketch path below folds through it)
   if (!in_place) SDR_CUDA(cudaMemsetAsync(ubuf.get(), 0, sizeof(double) * static_cast<size_t>(lay.ld), c.stream));
   const i64 ldau = std::max<i64>(lay.nloc, 1);
   if (in_place) {  // one pass over A per 8 columns (batched SpMM)
@@ -150,6 +156,49 @@ void refresh_recycle(Context& c, Recycle& sp, const DeviceOperator& A, const Ske
       for (int q = 0; q < nb; ++q) X.x[q] = sp.col(q0 + q);
       launch_spmm(c, A.view(), X, nb, au.get() + q0 * ldau, ldau);
     }
+  }
+  // the k sketches are small, latency-bound launches (C3: 15 us + a 6 us
+  // fold each, back to back 0.86 ms per refresh): with the SRDCT tile kernel
+  // they run on kSides streams at once, each into its own CTA partials, and
+  // u_q's scale is applied to the folded image on the host
+  static const bool side_on = [] {
+    const char* e = std::getenv("SDR_REFRESH_STREAMS");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool side = side_on && in_place && k > 1 && sketch_partials_eligible(S, lay.nloc, A.row_begin);
+  if (side) {
+    constexpr int kSides = Context::kAuxStreams;
+    const i64 psz = sketch_partials_size(S, c.num_sms);
+    struct {
+      double* p;
+      double* get() const { return p; }
+    } parts{c.partials2(psz * k)};
+    c.aux_fork(kSides);
+    cudaStream_t own = c.stream;
+    try {
+      for (i64 q = 0; q < k; ++q) {
+        c.stream = c.aux_stream(static_cast<int>(q % kSides));
+        int G = 0, ld = 0;
+        launch_sketch_partials(c, S, au.get() + q * ldau, lay.nloc, A.row_begin, parts.get() + q * psz, &G, &ld);
+        launch_sketch_fold_partials(c, S, parts.get() + q * psz, G, ld, sk.get() + q * S.s);
+        if (cnt) ++cnt->matvecs, ++cnt->sketch_applies;
+      }
+    } catch (...) {
+      c.stream = own;
+      throw;
+    }
+    c.stream = own;
+    c.aux_join(kSides);
+    c.allreduce_sum(sk.get(), S.s * k);
+    std::vector<double> h(static_cast<size_t>(S.s * k));
+    SDR_CUDA(cudaMemcpyAsync(h.data(), sk.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    for (i64 q = 0; q < k; ++q) {
+      const double us = sp.uscale[static_cast<size_t>(q)];
+      for (i64 r = 0; r < S.s; ++r) sp.SAU(r, q) = us * h[static_cast<size_t>(q * S.s + r)];
+    }
+    sp.provenance = 3;
+    return;
   }
   for (i64 q = 0; q < k; ++q) {
     double* aq = au.get() + q * ldau;

@@ -493,3 +493,28 @@ def test_sequence_device_resident_rhs_and_solutions(sk, O):
         assert np.array_equal(outs[i].cpu().numpy(), host.solutions[i])
     with pytest.raises(ValueError):
         sk.solve_sequence([sk.ProblemInstance(A1, rhs[0])], c, outs=[np.zeros(n - 1)])
+
+
+def test_exact_refresh_at_c3_size_matches_per_column_sketches(sk, O):
+    """refresh_for_new_matrix (recycle.hpp:297-318) at C3's size (1024^2,
+    SRDCT s = 140, k = 20): the k sketches run on concurrent streams into
+    their own partials; every SAU column equals S (A u_q) from the one-vector
+    apply to 1e-12."""
+    n = 1024
+    N = n * n
+    off, col, val = sk.gen_convdiff2d(n, 100.0, 100.0)
+    A = sk.SparseMatrix(N, N, off, col, val)
+    off2, col2, val2 = sk.gen_convdiff2d(n, 102.0, 98.0, 0.01)
+    A2 = sk.SparseMatrix(N, N, off2, col2, val2)
+    S = sk.SketchOperator.subsampled_dct(N, 140, 0x5EED)
+    k = 20
+    U = np.stack([O.gaussian_vector(N, 900 + q) for q in range(k)], axis=1)
+    U /= np.linalg.norm(U, axis=0)
+    space = sk.RecycleSpace(A.ctx)
+    space.set(U, np.zeros((140, k)), np.zeros((140, k)))
+    cnt = space.refresh(A2, S)
+    assert cnt["matvecs"] == k and cnt["sketch_applies"] == k
+    _, _, SAU = space.get()
+    for q in range(k):
+        ref = S.apply(A2.apply(U[:, q]))
+        assert np.linalg.norm(SAU[:, q] - ref) <= 1e-12 * np.linalg.norm(ref), q
